@@ -1,0 +1,221 @@
+"""Pins for the oracle's DiT arithmetic against closed forms, brute force and
+invariants.  None of these re-types the oracle's formula:
+each checks a consequence that a dropped term, wrong sign/index or transposed
+operand would break."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from oracle import dit
+from oracle import params as OP
+from synth.configs import TINY, MID, IMAGE, VIDEO, with_layers
+
+
+# ---------------------------------------------------------------- P4 schedule
+@pytest.mark.parametrize("shift,want", [
+    (1.0, [1, .75, .5, .25, 0]),
+    (3.0, [1, .9, .75, .5, 0]),
+    (5.0, [1, .9375, 5 / 6, .625, 0]),
+])
+def test_sigma_worked_values(shift, want):
+    np.testing.assert_allclose(dit.sigmas(4, shift), want, rtol=0, atol=1e-15)
+
+
+# ---------------------------------------------------------------- P1-P3 Euler
+def _euler_run(field, x0, sig):
+    x = x0.copy()
+    for i in range(len(sig) - 1):
+        x = dit.euler_update(x, field(x, sig[i]), sig[i], sig[i + 1])
+    return x
+
+
+@pytest.mark.parametrize("S,shift", [(4, 1.0), (28, 3.0), (50, 5.0)])
+def test_euler_constant_field(S, shift):
+    # v == c  =>  x_S = x0 + c * (sigma_S - sigma_0) = x0 - c
+    x0 = np.linspace(-1, 1, 7)
+    c = np.linspace(0.3, -2, 7)
+    xs = _euler_run(lambda x, s: c, x0, dit.sigmas(S, shift))
+    np.testing.assert_allclose(xs, x0 - c, atol=1e-14)
+
+
+@pytest.mark.parametrize("S,shift", [(4, 1.0), (28, 3.0), (50, 5.0)])
+def test_euler_linear_field(S, shift):
+    a = 0.7
+    sig = dit.sigmas(S, shift)
+    x0 = np.array([1.0, -2.0, 0.5])
+    xs = _euler_run(lambda x, s: a * x, x0, sig)
+    np.testing.assert_allclose(xs, np.prod(1 + a * np.diff(sig)) * x0, rtol=1e-14)
+    # first-order convergence to exp(-a) x0
+    fine = _euler_run(lambda x, s: a * x, x0, dit.sigmas(4000, 1.0))
+    np.testing.assert_allclose(fine, math.exp(-a) * x0, rtol=1e-3)
+
+
+@pytest.mark.parametrize("S,shift", [(4, 1.0), (28, 3.0), (50, 5.0)])
+def test_euler_rectified_flow_field_hits_target(S, shift):
+    # v(x, s) = (x - xhat)/s  =>  x_S = xhat exactly (sigma_S = 0)
+    xhat = np.array([0.25, -1.5, 3.0])
+    x0 = np.array([2.0, 0.0, -1.0])
+    xs = _euler_run(lambda x, s: (x - xhat) / s, x0, dit.sigmas(S, shift))
+    np.testing.assert_allclose(xs, xhat, atol=1e-14)
+
+
+# ---------------------------------------------------------------- P5 attention
+def _loop_attention(q, k, v):
+    H, Nq, dh = q.shape
+    Nk = k.shape[1]
+    o = np.zeros((H, Nq, dh))
+    for h in range(H):
+        for i in range(Nq):
+            logits = [sum(q[h, i, t] * k[h, j, t] for t in range(dh)) / math.sqrt(dh) for j in range(Nk)]
+            m = max(logits)
+            ws = [math.exp(x - m) for x in logits]
+            z = sum(ws)
+            for t in range(dh):
+                o[h, i, t] = sum(ws[j] * v[h, j, t] for j in range(Nk)) / z
+    return o
+
+
+def test_attention_bruteforce():
+    r = np.random.default_rng(0)
+    q, k, v = r.normal(size=(2, 5, 4)), r.normal(size=(2, 7, 4)), r.normal(size=(2, 7, 4))
+    np.testing.assert_allclose(dit.softmax_attention(q, k, v), _loop_attention(q, k, v), atol=1e-13)
+
+
+def test_attention_special_cases():
+    r = np.random.default_rng(1)
+    v = r.normal(size=(3, 6, 8))
+    # q = 0 -> equal logits -> mean of V
+    o = dit.softmax_attention(np.zeros((3, 4, 8)), r.normal(size=(3, 6, 8)), v)
+    np.testing.assert_allclose(o, np.broadcast_to(v.mean(axis=1, keepdims=True), o.shape), atol=1e-14)
+    # one key -> V
+    v1 = r.normal(size=(3, 1, 8))
+    o = dit.softmax_attention(r.normal(size=(3, 4, 8)), r.normal(size=(3, 1, 8)), v1)
+    np.testing.assert_allclose(o, np.broadcast_to(v1, o.shape), atol=1e-14)
+    # one dominant logit -> that row of V
+    k = np.zeros((1, 5, 2))
+    k[0, 3] = [100.0, 0]
+    o = dit.softmax_attention(np.array([[[10.0, 0]]]), k, r.normal(size=(1, 5, 2)) * 0 + np.arange(10).reshape(1, 5, 2))
+    np.testing.assert_allclose(o[0, 0], [6.0, 7.0], atol=1e-12)
+
+
+# ---------------------------------------------------------------- P6 RoPE
+def test_rope_invariants():
+    cfg = with_layers(MID, 1)
+    r = np.random.default_rng(2)
+    N, H, dh = 50, 2, cfg.dh
+    pos = np.stack([r.integers(0, 5, N), r.integers(0, 32, N), r.integers(0, 32, N)], axis=1)
+    u = r.normal(size=(N, H, dh))
+    ru = dit.rope3(u, pos, cfg.rope_axes, cfg.rope_theta)
+    # each pair keeps its norm
+    np.testing.assert_allclose(ru[..., 0::2] ** 2 + ru[..., 1::2] ** 2, u[..., 0::2] ** 2 + u[..., 1::2] ** 2, rtol=1e-12)
+    # origin is the identity
+    z = dit.rope3(u[:1], np.zeros((1, 3), int), cfg.rope_axes, cfg.rope_theta)
+    np.testing.assert_allclose(z, u[:1], atol=0)
+    # <R(p) q, R(p') k> = <q, R(p' - p) k>
+    q, k = r.normal(size=(1, 1, dh)), r.normal(size=(1, 1, dh))
+    p, p2 = np.array([[3, 7, 11]]), np.array([[1, 20, 4]])
+    lhs = np.sum(dit.rope3(q, p, cfg.rope_axes, cfg.rope_theta) * dit.rope3(k, p2, cfg.rope_axes, cfg.rope_theta))
+    rhs = np.sum(q * dit.rope3(k, p2 - p, cfg.rope_axes, cfg.rope_theta))
+    assert abs(lhs - rhs) < 1e-11
+    # f = 0 leaves the first D_f dims unchanged, h/w rotate the rest
+    Df = cfg.rope_axes[0]
+    z = dit.rope3(u[:1], np.array([[0, 3, 5]]), cfg.rope_axes, cfg.rope_theta)
+    np.testing.assert_allclose(z[..., :Df], u[:1, :, :Df], atol=0)
+    assert not np.allclose(z[..., Df:], u[:1, :, Df:])
+    # axis assignment: only the w-axis block moves when only w changes
+    z = dit.rope3(u[:1], np.array([[0, 0, 5]]), cfg.rope_axes, cfg.rope_theta)
+    np.testing.assert_allclose(z[..., :Df + cfg.rope_axes[1]], u[:1, :, :Df + cfg.rope_axes[1]], atol=0)
+    # pair (2m, 2m+1) at angle phi: first w pair rotates by exactly pos_w (j = 0)
+    m = (Df + cfg.rope_axes[1]) // 2
+    c, s = math.cos(5.0), math.sin(5.0)
+    a, b = u[0, 0, 2 * m], u[0, 0, 2 * m + 1]
+    np.testing.assert_allclose(z[0, 0, 2 * m:2 * m + 2], [a * c - b * s, a * s + b * c], rtol=1e-13)
+
+
+def test_rope_axes_split():
+    assert IMAGE.rope_axes == (44, 42, 42) and VIDEO.rope_axes == (44, 42, 42)
+    assert TINY.rope_axes == (8, 4, 4)
+
+
+# ---------------------------------------------------------------- P7 RMSNorm
+def test_rmsnorm_invariants():
+    r = np.random.default_rng(3)
+    x = r.normal(size=(6, 64))
+    y = dit.rms_norm(x, 0.0)
+    np.testing.assert_allclose(np.sqrt(np.mean(y * y, axis=-1)), 1.0, rtol=1e-14)
+    np.testing.assert_allclose(dit.rms_norm(7.5 * x, 0.0), y, rtol=1e-13)
+    hn = dit.head_rms_norm(x, 4, 0.0).reshape(6, 4, 16)
+    np.testing.assert_allclose(np.sqrt(np.mean(hn * hn, axis=-1)), 1.0, rtol=1e-14)
+
+
+# ---------------------------------------------------------------- P9 patchify
+@pytest.mark.parametrize("cfg", [TINY, MID])
+def test_patchify_roundtrip_and_index(cfg):
+    x = np.random.default_rng(4).normal(size=cfg.latent_shape)
+    X = dit.patchify(x, cfg)
+    assert X.shape == (cfg.N, cfg.P)
+    np.testing.assert_array_equal(dit.unpatchify(X, cfg), x)
+    # hand-indexed element: token (f=0, hh=1, ww=2), channel c=1, (i,j,k) = (0,1,0)
+    n = (0 * cfg.Hp + 1) * cfg.Wp + 2
+    p = ((1 * cfg.pt + 0) * cfg.ph + 1) * cfg.pw + 0
+    assert X[n, p] == x[1, 0, 1 * cfg.ph + 1, 2 * cfg.pw + 0]
+
+
+def test_token_counts():
+    assert TINY.N == 16 and IMAGE.N == 4096 and VIDEO.N == 32760 and MID.N == 1024
+    assert IMAGE.P == 64 and VIDEO.ffn == 13824 and IMAGE.ffn == 8192
+
+
+# ---------------------------------------------------------------- P10 + scalar fns
+def test_sinusoid_t0_and_scalars():
+    s = dit.sinusoid(0.0, 256)
+    np.testing.assert_array_equal(s, np.concatenate([np.ones(128), np.zeros(128)]))
+    # last frequency is 10000^(-127/128)
+    s = dit.sinusoid(1.0, 256)
+    assert abs(s[127] - math.cos(10000 ** (-127 / 128))) < 1e-15
+    assert abs(dit.silu(1.0) - 0.7310585786300049) < 1e-15
+    assert abs(dit.gelu_tanh(1.0) - 0.8411919906082768) < 1e-12
+    assert dit.gelu_tanh(0.0) == 0.0
+
+
+# ---------------------------------------------------------------- P8 adaLN-zero
+def test_adaln_zero_block_is_identity():
+    cfg = with_layers(TINY, 1)
+    P = OP.Params(cfg, 0)
+    r0 = np.random.default_rng(5).normal(size=(cfg.N, cfg.d))
+    e6 = np.random.default_rng(6).normal(size=(6, cfg.d)) * 0.1
+    mod = P.layer(0, "mod").copy()
+    mod[2] = -e6[2]      # g1 = 0
+    mod[5] = -e6[5]      # g2 = 0
+    P.set("L0.mod", mod)
+    P.set("L0.co_w", np.zeros((cfg.d, cfg.d)))
+    P.set("L0.co_b", np.zeros(cfg.d))
+    kv = (np.ones((cfg.L_txt, cfg.d)), np.ones((cfg.L_txt, cfg.d)))
+    r1 = dit.block(P, cfg, 0, r0, e6, kv, dit.token_positions(cfg))
+    np.testing.assert_array_equal(r1, r0)
+    # and a non-zero gate changes it (the wiring is live)
+    P.set("L0.mod", P.layer(0, "mod") + np.eye(6, cfg.d) * 0)
+    mod2 = mod.copy(); mod2[2] += 0.1
+    P.set("L0.mod", mod2)
+    assert not np.array_equal(dit.block(P, cfg, 0, r0, e6, kv, dit.token_positions(cfg)), r0)
+
+
+def test_cross_attention_uses_text():
+    # permuting text tokens leaves cross-attn invariant (set semantics, no mask/positions),
+    # while changing one token's K/V changes the output
+    cfg = with_layers(TINY, 1)
+    P = OP.Params(cfg, 0)
+    r0 = np.random.default_rng(7).normal(size=(cfg.N, cfg.d))
+    e6 = np.zeros((6, cfg.d))
+    rr = np.random.default_rng(8)
+    kc, vc = rr.normal(size=(cfg.L_txt, cfg.d)), rr.normal(size=(cfg.L_txt, cfg.d))
+    pos = dit.token_positions(cfg)
+    a = dit.block(P, cfg, 0, r0, e6, (kc, vc), pos)
+    perm = rr.permutation(cfg.L_txt)
+    b = dit.block(P, cfg, 0, r0, e6, (kc[perm], vc[perm]), pos)
+    np.testing.assert_allclose(a, b, atol=1e-12)
+    vc2 = vc.copy(); vc2[0] += 1.0
+    c = dit.block(P, cfg, 0, r0, e6, (kc, vc2), pos)
+    assert np.abs(c - a).max() > 1e-6
