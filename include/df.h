@@ -1,0 +1,200 @@
+/* df.h — C ABI of the B200-native DisagFusion hot path (arXiv 2605.25550).
+ *
+ * The library serves the DiT stage of a disaggregated Encoder -> Transformer (DiT)
+ * -> Decoder pipeline (§sec:decentral-pipeline) through the paper's
+ * asynchronous stage handoff: the encoder's conditioning
+ * hidden states move E -> T and the final latent moves T -> D in chunks on a
+ * dedicated comm stream with one event per chunk, so a stage never blocks on its
+ * downstream neighbour.
+ *
+ * Conventions (every call):
+ *   - returns df_status; nothing throws or aborts across the ABI;
+ *   - device pointers are raw CUDA device addresses on the device of the instance
+ *     named by the call; `stream` is a cudaStream_t (NULL = legacy default stream);
+ *   - "host" pointers are ordinary CPU memory; sizes are in elements unless the
+ *     name says bytes;
+ *   - ownership: df_init copies its graph; the context owns all weights, work
+ *     buffers, receive slots and caches; caller-owned device buffers passed to a
+ *     stream-ordered call must stay valid until that stream work completes;
+ *   - CUDA errors are sticky: after DF_ERR_CUDA every further call on the
+ *     context returns DF_ERR_STATE; df_last_error() has the message.
+ *   - the product path has no CPU fallback: df_init fails with DF_ERR_CUDA if no
+ *     sm_100 device is present.
+ */
+#ifndef DF_H_
+#define DF_H_
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DF_OK = 0,
+  DF_AGAIN = 1,          /* backpressure: request ring full, retry later */
+  DF_EMPTY = 2,          /* df_poll: nothing completed within the timeout                     */
+  DF_ERR_INVALID = 10,   /* bad argument; no side effects                                      */
+  DF_ERR_CAPACITY = 11,  /* Eq. 1 g_E+g_T+g_D > G, or a stage with 0 instances         */
+  DF_ERR_NOMEM = 12,
+  DF_ERR_DUPLICATE = 13, /* request id reused ("retry deduplication")                  */
+  DF_ERR_STATE = 14,     /* wrong lifecycle, or a call after a sticky CUDA error               */
+  DF_ERR_CUDA = 20,
+  DF_ERR_NCCL = 21
+} df_status;
+
+typedef enum { DF_E = 0, DF_T = 1, DF_D = 2 } df_stage;
+enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1 };               /* df_graph.precision */
+enum { DF_ASYNC = 0, DF_SYNC = 1, DF_PERMUTE = 2, DF_HASH = 4 }; /* handoff flags   */
+#define DF_ALL_CHUNKS 0xFFFFFFFFu
+#define DF_MAX_INST 32
+
+typedef struct df_ctx df_ctx;
+typedef struct { uint64_t lo, hi; } df_req_id;               /* 128-bit request id */
+
+/* DiT shape (the paper fixes none of it). */
+typedef struct {
+  uint32_t C, F, H, W;          /* latent [C, F, H, W]                                  */
+  uint32_t pt, ph, pw;          /* patch                                                */
+  uint32_t d, heads, ffn, layers;
+  uint32_t d_txt, L_txt;        /* encoder hidden width / text tokens                   */
+  uint32_t freq_dim;            /* time sinusoid width (256)                            */
+  uint32_t vocab, enc_ffn, dec_width; /* E / D stand-ins (R17)                          */
+  float eps, rope_theta;
+  uint32_t rope_axes[3];        /* (D_f, D_h, D_w), sum = d/heads                        */
+} df_dit_cfg;
+
+/* Stage graph: the fixed chain E -> T -> D with an E:T:D instance ratio. */
+typedef struct {
+  uint32_t n_inst;
+  struct { int32_t device; int32_t stage; } inst[DF_MAX_INST]; /* co-location allowed */
+  uint32_t G;                   /* GPU budget for Eq. 1                                  */
+  uint64_t chunk_bytes[2];      /* per edge (0: E->T ctx, 1: T->D latent); 0 = whole     */
+  uint32_t n_slots;             /* receive slots per consumer per edge, >= 2             */
+  uint32_t handoff_mode;        /* DF_ASYNC (default) | DF_SYNC (P:L151 comparison)      */
+  uint32_t ring_capacity;       /* request ring, power of two                   */
+  uint32_t precision;           /* DF_BF16 | DF_FP32_VALIDATION                          */
+  uint32_t max_steps;           /* largest S a request may ask for                       */
+  uint64_t weight_seed;
+  float jitter_p;               /* each transfer delayed by jitter_delay_s w.p. p */
+  float jitter_delay_s;
+  uint64_t jitter_seed;
+  df_dit_cfg dit;
+} df_graph;
+
+/* df_init: validate the graph (Eq. 1), allocate and Philox-initialise every
+ * instance's weights, create streams, receive slots and rings, and
+ * start one host worker thread per instance.  *out owns everything. */
+df_status df_init(const df_graph* g, df_ctx** out);
+/* Drains outstanding requests, joins workers, frees all device memory. */
+df_status df_finalize(df_ctx* ctx);
+const char* df_last_error(const df_ctx* ctx);
+
+/* ------------------------------------------------------------------ serving API */
+typedef struct {
+  uint32_t steps;               /* Euler steps S (<= max_steps)                          */
+  float shift;                  /* sigma-schedule shift                                  */
+  uint64_t seed;                /* noise / token seed                                    */
+  const int32_t* token_ids;     /* host [L_txt] or NULL (derive from seed); copied       */
+  void* out_host;               /* host fp32 [3, 1+4(F-1), 8H, 8W]; caller keeps it alive */
+  uint64_t out_bytes;           /*   until df_poll returns this request (MPI Irecv rule)  */
+  uint64_t user_tag;
+  df_req_id id;                 /* {0,0} = assign one                                    */
+} df_request;
+/* Admit a request ("request scheduler inserts the request into the global
+ * request buffer").  MT-safe.  DF_AGAIN if the ring is full, DF_ERR_DUPLICATE if
+ * the id was seen before. */
+df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out);
+
+typedef struct {
+  df_req_id id;
+  df_status status;
+  uint64_t user_tag;
+  int32_t inst[3];              /* E, T, D instance that served it                       */
+  double t_submit, t_start[3], t_end[3], t_done; /* seconds, host monotonic clock        */
+  float stage_ms[3];            /* device time of E, T, D compute                         */
+  float xfer_ms[2];             /* device time of the E->T / T->D transfers               */
+  float exposed_ms[2];          /* consumer stall on in-flight data per edge   */
+  uint64_t hash_src[2], hash_dst[2]; /* payload hash on both sides of each edge  */
+} df_completion;
+/* Pop up to max completions ("final output is returned to the request
+ * scheduler").  Blocks up to timeout_ms (-1 forever). DF_EMPTY if none. */
+df_status df_poll(df_ctx* ctx, df_completion* out, uint32_t max, uint32_t* n_out, int32_t timeout_ms);
+
+/* Rebalance the E:T:D ratio (Alg. 1 "Apply").  Instances keep their
+ * devices; the ratio limits which instances receive new requests.  Retiring
+ * instances drain first; no request is lost.  DF_ERR_CAPACITY if a
+ * g_s < 1 or more instances than exist are requested. */
+df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD);
+
+/* ------------------------------------------------------------------ low-level, stream-ordered */
+typedef struct df_cond df_cond;   /* per-request conditioning: cross K/V of every layer, e/e6 of every step */
+/* Request prologue on T instance t_inst from a device bf16 ctx
+ * [L_txt, d_txt]; sigmas = host float[S+1] schedule.  *out is caller-owned. */
+df_status df_dit_prepare(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const float* sigmas, uint32_t S,
+                         void* stream, df_cond** out);
+/* One denoising step i (a2-a12): x_dev fp32 [C,F,H,W] updated in place,
+ * x <- x + (sigma_{i+1} - sigma_i) v; v_dev (optional, fp32 [C,F,H,W]) gets v. */
+df_status df_dit_step(df_ctx* ctx, int32_t t_inst, const df_cond* c, uint32_t i, float* x_dev, float* v_dev,
+                      void* stream);
+/* One block l at step i on a caller residual r_dev fp32 [N, d] (in place) — for
+ * per-layer parity at production shapes. */
+df_status df_dit_layer(df_ctx* ctx, int32_t t_inst, const df_cond* c, uint32_t i, uint32_t l, float* r_dev,
+                       void* stream);
+df_status df_cond_release(df_ctx* ctx, df_cond* c);
+
+/* E stand-in: ids_dev int32 [L_txt] -> ctx_dev bf16 [L_txt, d_txt] (the E->T payload). */
+df_status df_encode(df_ctx* ctx, int32_t e_inst, const int32_t* ids_dev, void* ctx_dev, void* stream);
+/* D stand-in: latent fp32 [C,F,H,W] -> out fp32 [3, 1+4(F-1), 8H, 8W]. */
+df_status df_decode(df_ctx* ctx, int32_t d_inst, const float* x_dev, float* out_dev, void* stream);
+/* x0 ~ N(0,1) and token ids from a request seed. */
+df_status df_noise(df_ctx* ctx, int32_t inst, uint64_t seed, float* x_dev, void* stream);
+df_status df_tokens(df_ctx* ctx, int32_t inst, uint64_t seed, int32_t* ids_dev, void* stream);
+
+/* Chunked stage handoff: copy bytes from src (device of
+ * src_inst) into dst (device of dst_inst) in ceil(bytes/chunk_bytes) chunks on the
+ * library's comm stream after the work already queued on src_stream, one event per
+ * chunk.  DF_SYNC also makes src_stream wait for the last chunk.  DF_PERMUTE issues
+ * chunks in a seeded random order (tests).  DF_HASH hashes both sides.  Jitter per
+ * the graph's jitter_p / jitter_delay_s.  *out is caller-owned. */
+typedef struct {
+  int32_t src_inst, dst_inst;
+  const void* src;
+  void* dst;
+  uint64_t bytes, chunk_bytes;
+  uint32_t flags;
+  uint64_t seq;                 /* request sequence number (jitter draw / permutation seed) */
+  uint32_t edge;                /* 0: E->T, 1: T->D                                         */
+} df_handoff_desc;
+typedef struct df_xfer df_xfer;
+df_status df_handoff(df_ctx* ctx, const df_handoff_desc* d, void* src_stream, df_xfer** out);
+/* Make dst_stream wait for chunk c (or DF_ALL_CHUNKS). Never blocks the host. */
+df_status df_handoff_wait(df_ctx* ctx, df_xfer* x, uint32_t chunk, void* dst_stream);
+/* Host query: chunks landed so far; hashes {src, dst} once complete (DF_HASH). */
+df_status df_handoff_query(df_ctx* ctx, df_xfer* x, uint32_t* chunks_done, uint64_t hash[2]);
+df_status df_handoff_release(df_ctx* ctx, df_xfer* x);
+
+/* Payload hash of a device buffer (DESIGN.md §Handoff hash), synchronous. */
+df_status df_payload_hash(df_ctx* ctx, int32_t inst, const void* buf_dev, uint64_t nbytes, uint64_t* hash_out);
+
+/* ------------------------------------------------------------------ kernel-level entry points (tests, bench) */
+/* Parity check 0: copy the bf16 bits of parameter `tensor_id` (logical [in,out]
+ * row-major, DESIGN.md parameter table) of instance inst into host `dst`. */
+df_status df_weight_bits(df_ctx* ctx, int32_t inst, uint32_t tensor_id, uint16_t* dst, uint64_t n);
+/* out = A[M,K] (bf16) x W[N,K]^T (bf16), fp32 out [M,N]; tensor-core kernel (tc=1) or SIMT (tc=0). */
+df_status df_op_gemm(df_ctx* ctx, const void* A, const void* W, float* out, int32_t M, int32_t N, int32_t K,
+                     int32_t tc, void* stream);
+/* O[Nq, H*dh] = softmax(Q K^T * scale) V, head-major bf16 Q/K/V [H][N][dh_pad]. */
+df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t H, int32_t Nq,
+                          int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream);
+/* out bf16 [M,d] = RMSNorm(x fp32 [M,d]) * (1 + scale) + shift. */
+df_status df_op_rmsnorm_mod(df_ctx* ctx, const float* x, void* out, int32_t M, int32_t d, const float* shift,
+                            const float* scale, float eps, void* stream);
+
+/* Number of kernel launches this context issued so far (bench "gpu_launches"). */
+uint64_t df_launch_count(const df_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DF_H_ */

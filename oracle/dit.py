@@ -210,6 +210,33 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
     return r
 
 
+def block_rows(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, rows) -> np.ndarray:
+    """block() evaluated only at output rows `rows` (production-shape parity).
+    Same definition: self-attention keys/values use ALL tokens; every other
+    operation is row-wise, so restricting the query rows changes nothing."""
+    d, H, eps = cfg.d, cfg.heads, cfg.eps
+    rows = np.asarray(rows)
+    sh1, sc1, g1, sh2, sc2, g2 = (e6 + P.layer(l, "mod"))
+    h = rms_norm(r, eps) * (1.0 + sc1) + sh1                        # all rows (K, V need them)
+    W = P.layer(l, "qkv_w")
+    b = P.layer(l, "qkv_b")
+    k = head_rms_norm(h @ W[:, d:2 * d] + b[d:2 * d], H, eps) * P.layer(l, "g_k")
+    v = h @ W[:, 2 * d:] + b[2 * d:]
+    q = head_rms_norm(h[rows] @ W[:, :d] + b[:d], H, eps) * P.layer(l, "g_q")
+    q = rope3(q.reshape(-1, H, cfg.dh), pos[rows], cfg.rope_axes, cfg.rope_theta)
+    k = rope3(k.reshape(-1, H, cfg.dh), pos, cfg.rope_axes, cfg.rope_theta)
+    o = softmax_attention(q.transpose(1, 0, 2), k.transpose(1, 0, 2), _heads(v, H))
+    rr = r[rows] + g1 * (_unheads(o) @ P.layer(l, "o_w") + P.layer(l, "o_b"))
+    hc = rms_norm(rr, eps) * P.layer(l, "g_n3")
+    qc = head_rms_norm(hc @ P.layer(l, "cq_w") + P.layer(l, "cq_b"), H, eps) * P.layer(l, "g_cq")
+    kc, vc = kv
+    oc = softmax_attention(_heads(qc, H), _heads(kc, H), _heads(vc, H))
+    rr = rr + (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))
+    h2 = rms_norm(rr, eps) * (1.0 + sc2) + sh2
+    a = silu(h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * (h2 @ P.layer(l, "w3") + P.layer(l, "b3"))
+    return rr + g2 * (a @ P.layer(l, "w2") + P.layer(l, "b2"))
+
+
 def head(P, cfg, r: np.ndarray, e: np.ndarray) -> np.ndarray:
     """(sh, sc) = head_mod + e (e un-projected, R12);
     y = (RMSNorm(r)(1+sc)+sh) W_h + b_h;  v = unpatchify(y)."""

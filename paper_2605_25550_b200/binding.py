@@ -1,0 +1,299 @@
+"""Thin ctypes binding of libdf (include/df.h): argument marshalling only.
+
+Every computation runs inside libdf's CUDA kernels; this module converts Python
+arguments (torch tensors -> device pointers, streams -> cudaStream_t) and raises
+on a non-OK status.  There is no fallback: load() raises if libdf.so is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdf.so")
+
+DF_OK, DF_AGAIN, DF_EMPTY = 0, 1, 2
+DF_ERR_INVALID, DF_ERR_CAPACITY, DF_ERR_NOMEM, DF_ERR_DUPLICATE, DF_ERR_STATE = 10, 11, 12, 13, 14
+DF_E, DF_T, DF_D = 0, 1, 2
+DF_BF16, DF_FP32_VALIDATION = 0, 1
+DF_ASYNC, DF_SYNC, DF_PERMUTE, DF_HASH = 0, 1, 2, 4
+DF_ALL_CHUNKS = 0xFFFFFFFF
+DF_MAX_INST = 32
+
+
+class DitCfgC(C.Structure):
+    _fields_ = [("C", C.c_uint32), ("F", C.c_uint32), ("H", C.c_uint32), ("W", C.c_uint32),
+                ("pt", C.c_uint32), ("ph", C.c_uint32), ("pw", C.c_uint32),
+                ("d", C.c_uint32), ("heads", C.c_uint32), ("ffn", C.c_uint32), ("layers", C.c_uint32),
+                ("d_txt", C.c_uint32), ("L_txt", C.c_uint32), ("freq_dim", C.c_uint32),
+                ("vocab", C.c_uint32), ("enc_ffn", C.c_uint32), ("dec_width", C.c_uint32),
+                ("eps", C.c_float), ("rope_theta", C.c_float), ("rope_axes", C.c_uint32 * 3)]
+
+
+class InstC(C.Structure):
+    _fields_ = [("device", C.c_int32), ("stage", C.c_int32)]
+
+
+class GraphC(C.Structure):
+    _fields_ = [("n_inst", C.c_uint32), ("inst", InstC * DF_MAX_INST), ("G", C.c_uint32),
+                ("chunk_bytes", C.c_uint64 * 2), ("n_slots", C.c_uint32), ("handoff_mode", C.c_uint32),
+                ("ring_capacity", C.c_uint32), ("precision", C.c_uint32), ("max_steps", C.c_uint32),
+                ("weight_seed", C.c_uint64), ("jitter_p", C.c_float), ("jitter_delay_s", C.c_float),
+                ("jitter_seed", C.c_uint64), ("dit", DitCfgC)]
+
+
+class ReqIdC(C.Structure):
+    _fields_ = [("lo", C.c_uint64), ("hi", C.c_uint64)]
+
+
+class RequestC(C.Structure):
+    _fields_ = [("steps", C.c_uint32), ("shift", C.c_float), ("seed", C.c_uint64),
+                ("token_ids", C.POINTER(C.c_int32)), ("out_host", C.c_void_p), ("out_bytes", C.c_uint64),
+                ("user_tag", C.c_uint64), ("id", ReqIdC)]
+
+
+class CompletionC(C.Structure):
+    _fields_ = [("id", ReqIdC), ("status", C.c_int), ("user_tag", C.c_uint64), ("inst", C.c_int32 * 3),
+                ("t_submit", C.c_double), ("t_start", C.c_double * 3), ("t_end", C.c_double * 3),
+                ("t_done", C.c_double), ("stage_ms", C.c_float * 3), ("xfer_ms", C.c_float * 2),
+                ("exposed_ms", C.c_float * 2), ("hash_src", C.c_uint64 * 2), ("hash_dst", C.c_uint64 * 2)]
+
+
+class HandoffDescC(C.Structure):
+    _fields_ = [("src_inst", C.c_int32), ("dst_inst", C.c_int32), ("src", C.c_void_p), ("dst", C.c_void_p),
+                ("bytes", C.c_uint64), ("chunk_bytes", C.c_uint64), ("flags", C.c_uint32),
+                ("seq", C.c_uint64), ("edge", C.c_uint32)]
+
+
+_lib = None
+
+_SIGS = {
+    "df_init": (C.c_int, [C.POINTER(GraphC), C.POINTER(C.c_void_p)]),
+    "df_finalize": (C.c_int, [C.c_void_p]),
+    "df_last_error": (C.c_char_p, [C.c_void_p]),
+    "df_submit": (C.c_int, [C.c_void_p, C.POINTER(RequestC), C.POINTER(ReqIdC)]),
+    "df_poll": (C.c_int, [C.c_void_p, C.POINTER(CompletionC), C.c_uint32, C.POINTER(C.c_uint32), C.c_int32]),
+    "df_set_ratio": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "df_dit_prepare": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.c_void_p,
+                                 C.POINTER(C.c_void_p)]),
+    "df_dit_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "df_dit_layer": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "df_cond_release": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "df_encode": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "df_decode": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "df_noise": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "df_tokens": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "df_handoff": (C.c_int, [C.c_void_p, C.POINTER(HandoffDescC), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "df_handoff_wait": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
+    "df_handoff_query": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]),
+    "df_handoff_release": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "df_payload_hash": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "df_weight_bits": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "df_op_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                             C.c_int32, C.c_void_p]),
+    "df_op_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p]),
+    "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                    C.c_float, C.c_void_p]),
+    "df_launch_count": (C.c_uint64, [C.c_void_p]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def load(path: str = LIB_PATH):
+    """Load libdf.so (no fallback: raises if it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"libdf.so not built at {path}: run `python -m paper_2605_25550_b200.build`")
+        lib = C.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class DFError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"libdf status {status}: {msg}")
+        self.status = status
+
+
+def dit_cfg_c(cfg) -> DitCfgC:
+    """synth.configs.DitCfg -> df_dit_cfg."""
+    c = DitCfgC()
+    for k in ("C", "F", "H", "W", "pt", "ph", "pw", "d", "heads", "ffn", "layers", "d_txt", "L_txt", "freq_dim",
+              "vocab", "dec_width"):
+        setattr(c, k, int(getattr(cfg, k)))
+    c.enc_ffn = int(cfg.f_e)
+    c.eps = float(cfg.eps)
+    c.rope_theta = float(cfg.rope_theta)
+    for i, a in enumerate(cfg.rope_axes):
+        c.rope_axes[i] = int(a)
+    return c
+
+
+def make_graph(cfg, instances, precision=DF_BF16, weight_seed=0, chunk_bytes=(0, 0), n_slots=2,
+               handoff_mode=DF_ASYNC | DF_HASH, ring_capacity=256, max_steps=None, jitter=(0.0, 0.0, 0), G=0):
+    """instances: list of (device, stage)."""
+    g = GraphC()
+    g.n_inst = len(instances)
+    for i, (dev, st) in enumerate(instances):
+        g.inst[i].device = int(dev)
+        g.inst[i].stage = int(st)
+    g.G = int(G)
+    g.chunk_bytes[0], g.chunk_bytes[1] = int(chunk_bytes[0]), int(chunk_bytes[1])
+    g.n_slots = int(n_slots)
+    g.handoff_mode = int(handoff_mode)
+    g.ring_capacity = int(ring_capacity)
+    g.precision = int(precision)
+    g.max_steps = int(max_steps if max_steps is not None else max(cfg.steps, 64))
+    g.weight_seed = int(weight_seed)
+    g.jitter_p, g.jitter_delay_s, g.jitter_seed = float(jitter[0]), float(jitter[1]), int(jitter[2])
+    g.dit = dit_cfg_c(cfg)
+    return g
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(s):
+    if s is None:
+        import torch
+        s = torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Context:
+    """Owns one df_ctx.  Methods mirror the C ABI names."""
+
+    def __init__(self, graph: GraphC):
+        self.lib = load()
+        self.h = C.c_void_p()
+        st = self.lib.df_init(C.byref(graph), C.byref(self.h))
+        if st != DF_OK:
+            raise DFError(st, self.lib.df_last_error(None).decode())
+        self.graph = graph
+
+    def _ck(self, st, ok=(DF_OK,)):
+        if st not in ok:
+            raise DFError(st, self.lib.df_last_error(self.h).decode())
+        return st
+
+    def close(self):
+        if self.h:
+            self.lib.df_finalize(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- serving
+    def submit(self, steps, shift, seed, out_host=None, token_ids=None, user_tag=0, req_id=None):
+        r = RequestC()
+        r.steps, r.shift, r.seed, r.user_tag = int(steps), float(shift), int(seed), int(user_tag)
+        if token_ids is not None:
+            self._ids = (C.c_int32 * len(token_ids))(*[int(x) for x in token_ids])
+            r.token_ids = C.cast(self._ids, C.POINTER(C.c_int32))
+        if out_host is not None:
+            r.out_host = C.c_void_p(out_host.ctypes.data if hasattr(out_host, "ctypes") else out_host.data_ptr())
+            r.out_bytes = out_host.nbytes if hasattr(out_host, "nbytes") else out_host.numel() * out_host.element_size()
+        if req_id is not None:
+            r.id.lo, r.id.hi = req_id
+        rid = ReqIdC()
+        st = self.lib.df_submit(self.h, C.byref(r), C.byref(rid))
+        self._ck(st, ok=(DF_OK, DF_AGAIN))
+        return st, (rid.lo, rid.hi)
+
+    def poll(self, max_n=64, timeout_ms=100):
+        arr = (CompletionC * max_n)()
+        n = C.c_uint32()
+        st = self.lib.df_poll(self.h, arr, max_n, C.byref(n), int(timeout_ms))
+        self._ck(st, ok=(DF_OK, DF_EMPTY))
+        return [arr[i] for i in range(n.value)]
+
+    def set_ratio(self, gE, gT, gD):
+        return self._ck(self.lib.df_set_ratio(self.h, gE, gT, gD), ok=(DF_OK, DF_ERR_CAPACITY))
+
+    # ---- low level
+    def dit_prepare(self, t_inst, ctx_dev, sigmas, stream=None):
+        sig = (C.c_float * len(sigmas))(*[float(s) for s in sigmas])
+        out = C.c_void_p()
+        self._ck(self.lib.df_dit_prepare(self.h, t_inst, _ptr(ctx_dev), sig, len(sigmas) - 1, _stream(stream),
+                                         C.byref(out)))
+        return out
+
+    def dit_step(self, t_inst, cond, i, x_dev, v_dev=None, stream=None):
+        self._ck(self.lib.df_dit_step(self.h, t_inst, cond, i, _ptr(x_dev), _ptr(v_dev), _stream(stream)))
+
+    def dit_layer(self, t_inst, cond, i, l, r_dev, stream=None):
+        self._ck(self.lib.df_dit_layer(self.h, t_inst, cond, i, l, _ptr(r_dev), _stream(stream)))
+
+    def cond_release(self, cond):
+        self._ck(self.lib.df_cond_release(self.h, cond))
+
+    def encode(self, e_inst, ids_dev, ctx_dev, stream=None):
+        self._ck(self.lib.df_encode(self.h, e_inst, _ptr(ids_dev), _ptr(ctx_dev), _stream(stream)))
+
+    def decode(self, d_inst, x_dev, out_dev, stream=None):
+        self._ck(self.lib.df_decode(self.h, d_inst, _ptr(x_dev), _ptr(out_dev), _stream(stream)))
+
+    def noise(self, inst, seed, x_dev, stream=None):
+        self._ck(self.lib.df_noise(self.h, inst, seed, _ptr(x_dev), _stream(stream)))
+
+    def tokens(self, inst, seed, ids_dev, stream=None):
+        self._ck(self.lib.df_tokens(self.h, inst, seed, _ptr(ids_dev), _stream(stream)))
+
+    def handoff(self, src_inst, dst_inst, src, dst, nbytes, chunk_bytes, flags=0, seq=0, edge=0, stream=None):
+        d = HandoffDescC(src_inst, dst_inst, C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), int(nbytes),
+                         int(chunk_bytes), int(flags), int(seq), int(edge))
+        x = C.c_void_p()
+        self._ck(self.lib.df_handoff(self.h, C.byref(d), _stream(stream), C.byref(x)))
+        return x
+
+    def handoff_wait(self, x, chunk=DF_ALL_CHUNKS, stream=None):
+        self._ck(self.lib.df_handoff_wait(self.h, x, chunk, _stream(stream)))
+
+    def handoff_query(self, x):
+        n = C.c_uint32()
+        h = (C.c_uint64 * 2)()
+        self._ck(self.lib.df_handoff_query(self.h, x, C.byref(n), h))
+        return n.value, (h[0], h[1])
+
+    def handoff_release(self, x):
+        self._ck(self.lib.df_handoff_release(self.h, x))
+
+    def payload_hash(self, inst, buf_dev, nbytes):
+        h = C.c_uint64()
+        self._ck(self.lib.df_payload_hash(self.h, inst, _ptr(buf_dev), int(nbytes), C.byref(h)))
+        return h.value
+
+    def weight_bits(self, inst, tensor_id, n):
+        import numpy as np
+        out = np.empty(n, dtype=np.uint16)
+        self._ck(self.lib.df_weight_bits(self.h, inst, int(tensor_id), out.ctypes.data_as(C.c_void_p), int(n)))
+        return out
+
+    def op_gemm(self, A, W, out, tc=1, stream=None):
+        M, K = A.shape
+        N = W.shape[0]
+        self._ck(self.lib.df_op_gemm(self.h, _ptr(A), _ptr(W), _ptr(out), M, N, K, int(tc), _stream(stream)))
+
+    def op_attention(self, Q, K, V, O, H, Nq, Nk, dh, dh_pad, scale, stream=None):
+        self._ck(self.lib.df_op_attention(self.h, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), H, Nq, Nk, dh, dh_pad,
+                                          float(scale), _stream(stream)))
+
+    def op_rmsnorm_mod(self, x, out, shift, scale, eps, stream=None):
+        M, d = x.shape
+        self._ck(self.lib.df_op_rmsnorm_mod(self.h, _ptr(x), _ptr(out), M, d, _ptr(shift), _ptr(scale), float(eps),
+                                            _stream(stream)))
+
+    def launch_count(self):
+        return int(self.lib.df_launch_count(self.h))

@@ -1,0 +1,328 @@
+// Self- and cross-attention of the DiT block (PAPER.md P:L118
+// "attention is O(T^2 D)"): O_h = softmax(Q_h K_h^T / sqrt(dh)) V_h, no mask, fp32
+// online softmax.
+//
+// attn_tc: one CTA per (128-query tile, head), warp-specialised, sm_100a:
+//   warp 0      TMA: Q once; K_j/V_j 128-key blocks into a 2-deep ring
+//   warp 1      MMA (one thread): S_j = Q K_j^T -> TMEM (2 S buffers, 128 cols each);
+//               O += P_{j-1} V_{j-1} -> TMEM (dh cols).  QK of block j is issued before
+//               PV of block j-1 so the tensor core works while softmax runs.
+//   warps 4..7  softmax, thread = query row: tcgen05.ld S row, row max, exp2, P (bf16)
+//               into a 128B-swizzled SMEM buffer (double-buffered) as the A operand of PV.
+//               Lazy rescaling: O (in TMEM) is rescaled only when the row max grows by
+//               more than 2^8 over the max in use; otherwise P <= 256 is accumulated with
+//               a stale max (exact after the final 1/l normalisation).
+// attn_simt: fp32 warp-per-row reference-grade kernel for the fp32 validation build.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cmath>
+#include "kernels.h"
+
+namespace df {
+
+bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
+template <int DH>
+struct AttnCfg {
+  static constexpr int ATOMS = DH / 64;           // 64-element (128 B) swizzle atoms along dh
+  static constexpr int TILE = 128 * 128;          // bytes of one [128 x 64] bf16 atom tile
+  static constexpr int Q_BYTES = ATOMS * TILE;
+  static constexpr int KV_BYTES = ATOMS * TILE;   // one K or one V block
+  static constexpr int P_BYTES = 2 * TILE;        // [128 q x 128 kv] bf16
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = Q_BYTES;
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;
+  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t S_COL0 = 0;           // S buffers at cols [0,128) and [128,256)
+  static constexpr uint32_t O_COL = 256;          // O at cols [256, 256+DH)
+};
+
+template <int DH>
+__global__ void __launch_bounds__(256, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                   int dh_real, float scale_log2) {
+  using Cfg = AttnCfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint8_t* sP = smem + Cfg::OFF_P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;    // [2]
+  uint64_t* kv_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;     // [2]
+  uint64_t* s_empty = bars + 7;    // [2]
+  uint64_t* p_full = bars + 9;     // [2]
+  uint64_t* p_empty = bars + 11;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int h = blockIdx.y;
+  const int q0 = blockIdx.x * 128;
+  const int nkb = (Nk + 127) / 128;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 128);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&p_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, Cfg::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < Cfg::ATOMS; ++a) tma_load_3d(sQ + a * Cfg::TILE, &tmQ, q_full, a * 64, q0, h);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Cfg::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < Cfg::ATOMS; ++a) {
+          tma_load_3d(sK + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmK, &kv_full[st], a * 64, j * 128, h);
+          tma_load_3d(sV + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmV, &kv_full[st], a * 64, j * 128, h);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(128, DH, false, true);
+      mbar_wait(q_full, 0);
+      const uint32_t q_addr = smem_u32(sQ);
+      for (int j = 0; j <= nkb; ++j) {
+        if (j < nkb) {
+          const int st = j & 1;
+          mbar_wait(&kv_full[st], (j >> 1) & 1);
+          mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sK + st * Cfg::KV_BYTES);
+          const uint32_t d_s = tmem + Cfg::S_COL0 + st * 128;
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k) {
+            const uint32_t off = (k >> 2) * Cfg::TILE + (k & 3) * 32;
+            tc_mma_bf16(d_s, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), idesc_qk,
+                        k > 0);
+          }
+          tc_commit(&s_full[st]);
+        }
+        if (j >= 1) {
+          const int jj = j - 1;
+          const int pb = jj & 1;
+          mbar_wait(&p_full[pb], (jj >> 1) & 1);
+          tc_fence_after();
+          const uint32_t p_addr = smem_u32(sP + pb * Cfg::P_BYTES);
+          const uint32_t v_addr = smem_u32(sV + pb * Cfg::KV_BYTES);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {  // 128 keys / 16
+            const uint32_t pa = p_addr + (k >> 2) * Cfg::TILE + (k & 3) * 32;
+            const uint32_t vb = v_addr + k * 2048;  // 16 key rows x 128 B
+            tc_mma_bf16(tmem + Cfg::O_COL, sdesc_sw128(pa, 16, 1024), sdesc_sw128(vb, Cfg::TILE, 1024), idesc_pv,
+                        (jj > 0 || k > 0));
+          }
+          tc_commit(&p_empty[pb]);
+          tc_commit(&kv_empty[pb]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int r = ew * 32 + lane;  // query row within tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    float s[128];
+    for (int j = 0; j < nkb; ++j) {
+      const int sb = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(&s_full[sb], ph);
+      tc_fence_after();
+      const uint32_t ts = tmem + lane_off + Cfg::S_COL0 + sb * 128;
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
+      tc_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_empty[sb]);
+      const int valid = Nk - j * 128;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        float z = (c < valid) ? s[c] * scale_log2 : -INFINITY;
+        s[c] = z;
+        mx = fmaxf(mx, z);
+      }
+      // P buffer sb is free once PV_{j-2} completed
+      mbar_wait(&p_empty[sb], ph ^ 1);
+      const bool need = mx > m_used + 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_used;
+        if (j > 0) {
+          // O holds PV_0..PV_{j-1}: wait for PV_{j-1}, then rescale this warp's rows
+          mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+          const float alpha = exp2f(m_used - m_new);
+          l *= alpha;
+          const uint32_t to = tmem + lane_off + Cfg::O_COL;
+#pragma unroll
+          for (int c = 0; c < DH; c += 32) {
+            float o[32];
+            tmem_ld32(to + c, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(to + c, o);
+          }
+          tc_wait_st();
+        }
+        m_used = m_new;
+      }
+      // P = exp2(s - m_used) -> bf16, 128B-swizzled K-major [128 rows x 128 keys]
+      uint8_t* prow = sP + sb * Cfg::P_BYTES + r * 128;
+      float lsum = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        float p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          p[i] = exp2f(s[ch * 8 + i] - m_used);
+          lsum += p[i];
+        }
+        uint4 u;
+        u.x = pack_bf16x2(p[0], p[1]);
+        u.y = pack_bf16x2(p[2], p[3]);
+        u.z = pack_bf16x2(p[4], p[5]);
+        u.w = pack_bf16x2(p[6], p[7]);
+        const int atom = ch >> 3, c16 = ch & 7;
+        *reinterpret_cast<uint4*>(prow + atom * Cfg::TILE + ((c16 ^ (r & 7)) << 4)) = u;
+      }
+      l += lsum;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full[sb]);
+    }
+    // final: wait for the last PV, normalise, store O[q, h*dh + c]
+    const int jl = nkb - 1;
+    mbar_wait(&p_empty[jl & 1], (jl >> 1) & 1);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    const int q = q0 + r;
+    const uint32_t to = tmem + lane_off + Cfg::O_COL;
+    bf16* orow = O + size_t(q) * H * dh_real + size_t(h) * dh_real;
+#pragma unroll
+    for (int c = 0; c < DH; c += 32) {
+      float o[32];
+      tmem_ld32(to + c, o);
+      tc_wait_ld();
+      if (q < Nq && c < dh_real) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] *= inv;
+        if (dh_real - c >= 32) {
+          store_vec<32>(orow + c, o);
+        } else {
+          for (int i = 0; i < dh_real - c; ++i) orow[c + i] = __float2bfloat16_rn(o[i]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int DH>
+static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
+                               float scale, cudaStream_t st) {
+  using Cfg = AttnCfg<DH>;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
+      !make_tmap_3d(&tv, V, H, Nk, DH, 128))
+    return cudaErrorInvalidValue;
+  auto kern = attn_tc_kernel<DH>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((Nq + 127) / 128, H);
+  kern<<<grid, 256, Cfg::SMEM, st>>>(tq, tk, tv, O, H, Nq, Nk, dh, scale * 1.4426950408889634f);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
+                    float scale, cudaStream_t st) {
+  if (Nq <= 0) return cudaSuccess;
+  if (Nk <= 0 || dh > dh_pad) return cudaErrorInvalidValue;
+  if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st);
+  if (dh_pad == 128) return launch_attn<128>(Q, K, V, O, H, Nq, Nk, dh, scale, st);
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ fp32 SIMT attention
+__global__ void attn_simt_kernel(const float* __restrict__ Q, const float* __restrict__ K,
+                                 const float* __restrict__ V, float* __restrict__ O, int H, int Nq, int Nk, int dh,
+                                 float scale) {
+  const int warps = blockDim.x / 32;
+  const int q = blockIdx.x * warps + threadIdx.x / 32;
+  const int h = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  if (q >= Nq) return;
+  const float* qr = Q + (size_t(h) * Nq + q) * dh;
+  float qv[4], ov[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) qv[i] = (lane + 32 * i < dh) ? qr[lane + 32 * i] : 0.f;
+  float m = -INFINITY, l = 0.f;
+  for (int j = 0; j < Nk; ++j) {
+    const float* kr = K + (size_t(h) * Nk + j) * dh;
+    const float* vr = V + (size_t(h) * Nk + j) * dh;
+    float part = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < dh) part = fmaf(qv[i], kr[lane + 32 * i], part);
+    float sj = warp_sum(part) * scale;
+    float mn = fmaxf(m, sj);
+    float corr = expf(m - mn), pj = expf(sj - mn);
+    l = l * corr + pj;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < dh) ov[i] = ov[i] * corr + pj * vr[lane + 32 * i];
+    m = mn;
+  }
+  float* orow = O + size_t(q) * H * dh + size_t(h) * dh;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (lane + 32 * i < dh) orow[lane + 32 * i] = ov[i] / l;
+}
+
+cudaError_t attn_simt(const float* Q, const float* K, const float* V, float* O, int H, int Nq, int Nk, int dh,
+                      float scale, cudaStream_t st) {
+  if (Nq <= 0) return cudaSuccess;
+  if (Nk <= 0 || dh > 128) return cudaErrorInvalidValue;
+  dim3 grid((Nq + 3) / 4, H);
+  attn_simt_kernel<<<grid, 128, 0, st>>>(Q, K, V, O, H, Nq, Nk, dh, scale);
+  return cudaGetLastError();
+}
+
+}  // namespace df

@@ -1,0 +1,978 @@
+// libdf C ABI (include/df.h): context, stage instances, the chunked stage handoff
+// and the asynchronous E -> T -> D pipeline workers.
+//
+// Pipeline (§sec:decentral-pipeline), one host worker per instance:
+//   E  pops the global request ring (FAA ring), claims a receive slot on its
+//      T instance (the "destination address" handshake), encodes, and hands ctx
+//      off in chunks on its comm stream; it proceeds to the next request immediately
+//       — the send completes on the comm stream.
+//   T  waits (device-side, per chunk) for ctx, runs the prologue and S Euler steps on its
+//      compute stream, claims a D slot, hands the final latent off (per-frame chunks) and
+//      dequeues its next request without waiting for the send.
+//   D  waits per chunk, decodes, copies to the caller's host buffer, completes.
+// Request -> instance assignment is deterministic round-robin over the active instances
+// of each stage (sequence number mod g_s), so per-request results never depend on load.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+#include "ring.h"
+#include "runtime.h"
+
+using namespace df;
+
+struct df_xfer {
+  int src_dev = 0, dst_dev = 0;
+  uint32_t nchunks = 0;
+  std::vector<cudaEvent_t> chunk_ev;  // on the source comm stream (cross-device waits are legal)
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing (source comm stream)
+  cudaEvent_t t_hash = nullptr;            // destination hash done (dst comm stream)
+  unsigned long long* hash_dev = nullptr;  // [2] src, dst (pinned-mapped host)
+  bool hashed = false;
+  uint64_t bytes = 0;
+};
+using Xfer = df_xfer;
+
+namespace {
+
+double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+// Host Philox4x32-10 for jitter draws and chunk permutations.
+void philox_host(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t p0 = uint64_t(0xD2511F53u) * c[0], p1 = uint64_t(0xCD9E8D57u) * c[2];
+    uint32_t n0 = uint32_t(p1 >> 32) ^ c[1] ^ k0, n2 = uint32_t(p0 >> 32) ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = uint32_t(p1);
+    c[2] = n2;
+    c[3] = uint32_t(p0);
+  }
+}
+
+// A receive slot on a consumer instance (the posted destination address).
+struct Slot {
+  void* buf = nullptr;
+  cudaEvent_t consumed = nullptr;  // recorded by the consumer after its last read
+  uint64_t gen = 0;                // generation counter (catches use-after-release)
+};
+
+struct SlotPool {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<int> free_list;
+  std::vector<Slot> slots;
+  int acquire(std::atomic<bool>& stop) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return !free_list.empty() || stop.load(); });
+    if (free_list.empty()) return -1;
+    int s = free_list.front();
+    free_list.pop_front();
+    return s;
+  }
+  void release(int s) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      slots[s].gen++;
+      free_list.push_back(s);
+    }
+    cv.notify_all();
+  }
+};
+
+struct ReqState {
+  df_request req{};
+  df_req_id id{};
+  uint64_t seq = 0;
+  std::vector<int32_t> ids;
+  int inst[3] = {-1, -1, -1};
+  double t_submit = 0, t_start[3] = {0, 0, 0}, t_end[3] = {0, 0, 0};
+  cudaEvent_t ev[10] = {};  // 0,1 E start/end; 2,3 T start/end; 4,5 D start/end; 6 T ready; 7 D ready
+  Xfer* x[2] = {nullptr, nullptr};
+  int slot[2] = {-1, -1};
+  int xbuf = 0;  // T latent buffer index
+};
+
+struct Job {
+  ReqState* rs;
+};
+
+template <typename T>
+struct Inbox {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<T> q;
+  void push(const T& v) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      q.push_back(v);
+    }
+    cv.notify_one();
+  }
+  bool pop(T& out, std::atomic<bool>& stop) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return !q.empty() || stop.load(); });
+    if (q.empty()) return false;
+    out = q.front();
+    q.pop_front();
+    return true;
+  }
+  size_t size() {
+    std::lock_guard<std::mutex> lk(mu);
+    return q.size();
+  }
+};
+
+}  // namespace
+
+
+
+struct Inst {
+  int id = 0, stage = 0, device = 0;
+  Model m;
+  cudaStream_t compute = nullptr, comm = nullptr;
+  std::thread worker;
+  Inbox<Job> inbox;
+  SlotPool slots;           // receive slots (T: ctx; D: latent)
+  // T: two latent buffers, each with a "send done" event
+  float* xbuf[2] = {nullptr, nullptr};
+  cudaEvent_t xsent[2] = {nullptr, nullptr};
+  int xnext = 0;
+  // E: two ctx send buffers
+  void* ebuf[2] = {nullptr, nullptr};
+  cudaEvent_t esent[2] = {nullptr, nullptr};
+  int enext = 0;
+  int32_t* ids_dev = nullptr;
+  // D: decoded output + pinned staging
+  float* dout = nullptr;
+  float* stage_host = nullptr;
+  std::atomic<uint64_t> busy_ns{0};
+  std::atomic<uint64_t> served{0};
+};
+
+struct df_ctx {
+  df_graph g{};
+  std::vector<std::unique_ptr<Inst>> inst;
+  std::vector<int> by_stage[3];
+  std::atomic<int> active[3];
+  std::atomic<bool> stop{false};
+  std::atomic<bool> failed{false};
+  std::string err;
+  std::unique_ptr<FaaRing<ReqState*>> requests;
+  std::unique_ptr<FaaRing<ReqState*>> done;
+  std::mutex done_mu;
+  std::condition_variable done_cv;
+  std::mutex seen_mu;
+  std::set<std::pair<uint64_t, uint64_t>> seen;
+  std::atomic<uint64_t> seq{0};
+  std::atomic<uint64_t> next_id{1};
+  std::mutex ratio_mu;
+  std::mutex req_mu;   // E workers share the request ring; assignment counters below
+  std::atomic<uint64_t> assigned_t{0}, assigned_d{0};
+  size_t ctx_bytes = 0, lat_bytes = 0, out_bytes = 0;
+  std::vector<float*> sched_dev;
+};
+
+namespace {
+
+thread_local std::string g_tls_msg;
+
+df_status fail(df_ctx* c, const std::string& m, df_status s = DF_ERR_CUDA) {
+  if (c) {
+    c->err = m;
+    if (s == DF_ERR_CUDA || s == DF_ERR_NCCL) c->failed = true;
+  }
+  g_tls_msg = m;
+  return s;
+}
+#define CK(ctx, expr)                                                                      \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(ctx, std::string(#expr) + ": " + cudaGetErrorString(_e) + " " + df::tls_err); \
+  } while (0)
+
+size_t latent_elems(const df_dit_cfg& c) { return size_t(c.C) * c.F * c.H * c.W; }
+size_t out_elems(const df_dit_cfg& c) { return size_t(3) * (1 + 4 * (c.F - 1)) * 8 * c.H * 8 * c.W; }
+
+std::vector<float> sigmas_host(int S, float shift) {
+  // R13: s_i = 1 - i/S, sigma_i = shift s_i / (1 + (shift - 1) s_i)
+  std::vector<float> s(S + 1);
+  for (int i = 0; i <= S; ++i) {
+    double si = 1.0 - double(i) / S;
+    s[i] = float(shift * si / (1.0 + (shift - 1.0) * si));
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------- handoff
+df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_stream, Xfer** out) {
+  if (!d || d->src_inst < 0 || d->dst_inst < 0 || d->src_inst >= int(ctx->inst.size()) ||
+      d->dst_inst >= int(ctx->inst.size()) || !d->src || !d->dst || !d->bytes)
+    return fail(ctx, "df_handoff: invalid descriptor", DF_ERR_INVALID);
+  Inst& S = *ctx->inst[d->src_inst];
+  Inst& D = *ctx->inst[d->dst_inst];
+  auto x = new Xfer();
+  x->src_dev = S.device;
+  x->dst_dev = D.device;
+  x->bytes = d->bytes;
+  uint64_t cb = d->chunk_bytes;
+  if (cb == 0 || cb >= d->bytes) cb = d->bytes;
+  cb = (cb + 15) & ~uint64_t(15);  // 16-byte chunk granularity (R22)
+  x->nchunks = uint32_t((d->bytes + cb - 1) / cb);
+  CK(ctx, cudaSetDevice(S.device));
+  x->chunk_ev.resize(x->nchunks);
+  for (auto& e : x->chunk_ev) CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(ctx, cudaEventCreate(&x->t0));
+  CK(ctx, cudaEventCreate(&x->t1));
+  // comm stream runs after the producer's queued work
+  cudaEvent_t ready;
+  CK(ctx, cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CK(ctx, cudaEventRecord(ready, src_stream));
+  CK(ctx, cudaStreamWaitEvent(S.comm, ready, 0));
+  CK(ctx, cudaEventDestroy(ready));
+  const bool hash = (d->flags & DF_HASH) != 0;
+  if (hash) {
+    CK(ctx, cudaHostAlloc(&x->hash_dev, 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
+    x->hash_dev[0] = x->hash_dev[1] = 0;
+    x->hashed = true;
+    g_launches->fetch_add(1);
+    CK(ctx, payload_hash(d->src, d->bytes, 0, x->hash_dev, S.comm));
+  }
+  // jitter: one Bernoulli draw per request-edge transfer (R23)
+  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f) {
+    uint32_t c[4] = {uint32_t(d->seq), uint32_t(d->seq >> 32), d->edge, 3u};
+    philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
+    if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0) {
+      g_launches->fetch_add(1);
+      CK(ctx, delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), S.comm));
+    }
+  }
+  CK(ctx, cudaEventRecord(x->t0, S.comm));
+  std::vector<uint32_t> order(x->nchunks);
+  for (uint32_t i = 0; i < x->nchunks; ++i) order[i] = i;
+  if (d->flags & DF_PERMUTE) {
+    for (uint32_t i = x->nchunks; i > 1; --i) {  // seeded Fisher-Yates
+      uint32_t c[4] = {uint32_t(d->seq), i, 0x5045524Du, 4u};
+      philox_host(c, 0x1234567u, 0x89ABCDEFu);
+      std::swap(order[i - 1], order[c[0] % i]);
+    }
+  }
+  for (uint32_t k = 0; k < x->nchunks; ++k) {
+    uint32_t ci = order[k];
+    uint64_t off = uint64_t(ci) * cb;
+    uint64_t sz = std::min<uint64_t>(cb, d->bytes - off);
+    const char* sp = static_cast<const char*>(d->src) + off;
+    char* dp = static_cast<char*>(d->dst) + off;
+    if (S.device == D.device) CK(ctx, cudaMemcpyAsync(dp, sp, sz, cudaMemcpyDeviceToDevice, S.comm));
+    else CK(ctx, cudaMemcpyPeerAsync(dp, D.device, sp, S.device, sz, S.comm));
+    CK(ctx, cudaEventRecord(x->chunk_ev[ci], S.comm));
+  }
+  CK(ctx, cudaEventRecord(x->t1, S.comm));
+  if (hash) {
+    // destination hash, on the destination device after the last chunk landed
+    CK(ctx, cudaSetDevice(D.device));
+    CK(ctx, cudaStreamWaitEvent(D.comm, x->t1, 0));
+    g_launches->fetch_add(1);
+    CK(ctx, payload_hash(d->dst, d->bytes, 0, x->hash_dev + 1, D.comm));
+    CK(ctx, cudaEventCreateWithFlags(&x->t_hash, cudaEventDisableTiming));
+    CK(ctx, cudaEventRecord(x->t_hash, D.comm));
+    CK(ctx, cudaSetDevice(S.device));
+  }
+  if (d->flags & DF_SYNC) CK(ctx, cudaStreamWaitEvent(src_stream, x->t1, 0));
+  *out = x;
+  return DF_OK;
+}
+
+void free_xfer(Xfer* x) {
+  if (!x) return;
+  for (auto e : x->chunk_ev) cudaEventDestroy(e);
+  if (x->t0) cudaEventDestroy(x->t0);
+  if (x->t1) cudaEventDestroy(x->t1);
+  if (x->t_hash) cudaEventDestroy(x->t_hash);
+  if (x->hash_dev) cudaFreeHost(x->hash_dev);
+  delete x;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = -1.f;
+  if (!a || !b || cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return -1.f;
+  }
+  return ms;
+}
+
+// ---------------------------------------------------------------- workers
+int pick(df_ctx* ctx, int stage, uint64_t seq) {
+  int n = ctx->active[stage].load();
+  auto& v = ctx->by_stage[stage];
+  if (n <= 0 || v.empty()) return -1;
+  return v[seq % uint64_t(std::min<int>(n, int(v.size())))];
+}
+
+void worker_fail(df_ctx* ctx, const std::string& m) {
+  std::lock_guard<std::mutex> lk(ctx->done_mu);
+  ctx->err = m;
+  ctx->failed = true;
+  ctx->done_cv.notify_all();
+}
+
+#define WK(expr)                                                                  \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      worker_fail(ctx, std::string(#expr) + ": " + cudaGetErrorString(_e) + " " + df::tls_err); \
+      return;                                                                     \
+    }                                                                             \
+  } while (0)
+
+void e_worker(df_ctx* ctx, Inst* me) {
+  cudaSetDevice(me->device);
+  while (!ctx->stop.load()) {
+    ReqState* rs = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(ctx->req_mu);
+      // only the E instance the request's sequence maps to takes it
+      if (!ctx->requests->pop(rs)) rs = nullptr;
+    }
+    if (!rs) {
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+      continue;
+    }
+    rs->inst[0] = me->id;
+    rs->t_start[0] = now_s();
+    WK(cudaEventCreate(&rs->ev[0]));
+    WK(cudaEventCreate(&rs->ev[1]));
+    const int tid = pick(ctx, DF_T, rs->seq);
+    Inst* T = ctx->inst[tid].get();
+    rs->inst[1] = tid;
+    int b = me->enext;
+    me->enext ^= 1;
+    WK(cudaStreamWaitEvent(me->compute, me->esent[b], 0));  // send buffer reuse
+    WK(cudaEventRecord(rs->ev[0], me->compute));
+    if (!rs->ids.empty()) {
+      WK(cudaMemcpyAsync(me->ids_dev, rs->ids.data(), rs->ids.size() * 4, cudaMemcpyHostToDevice, me->compute));
+    } else {
+      g_launches->fetch_add(1);
+      WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
+    }
+    WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+    WK(cudaEventRecord(rs->ev[1], me->compute));
+    // handshake: claim a receive slot on T (its posted destination address)
+    int s = T->slots.acquire(ctx->stop);
+    if (s < 0) return;
+    rs->slot[0] = s;
+    WK(cudaStreamWaitEvent(me->comm, T->slots.slots[s].consumed, 0));
+    df_handoff_desc d{};
+    d.src_inst = me->id;
+    d.dst_inst = tid;
+    d.src = me->ebuf[b];
+    d.dst = T->slots.slots[s].buf;
+    d.bytes = ctx->ctx_bytes;
+    d.chunk_bytes = ctx->g.chunk_bytes[0];
+    d.flags = (ctx->g.handoff_mode & (DF_SYNC | DF_HASH));
+    d.seq = rs->seq;
+    d.edge = 0;
+    Xfer* x = nullptr;
+    if (do_handoff(ctx, &d, me->compute, &x) != DF_OK) {
+      worker_fail(ctx, ctx->err);
+      return;
+    }
+    rs->x[0] = x;
+    WK(cudaEventRecord(me->esent[b], me->comm));
+    rs->t_end[0] = now_s();
+    me->served++;
+    T->inbox.push(Job{rs});  // E moves on immediately
+  }
+}
+
+void t_worker(df_ctx* ctx, Inst* me) {
+  cudaSetDevice(me->device);
+  Job j;
+  while (me->inbox.pop(j, ctx->stop)) {
+    ReqState* rs = j.rs;
+    rs->t_start[1] = now_s();
+    WK(cudaEventCreate(&rs->ev[2]));
+    WK(cudaEventCreate(&rs->ev[3]));
+    WK(cudaEventCreate(&rs->ev[6]));
+    const int S = int(rs->req.steps);
+    int b = me->xnext;
+    me->xnext ^= 1;
+    rs->xbuf = b;
+    float* x = me->xbuf[b];
+    WK(cudaStreamWaitEvent(me->compute, me->xsent[b], 0));  // latent buffer reuse after its send
+    WK(cudaEventRecord(rs->ev[2], me->compute));
+    g_launches->fetch_add(1);
+    WK(gen_noise(x, latent_elems(me->m.c), rs->req.seed, me->compute));  // x0 does not need ctx
+    // consumer ready for ctx; wait per chunk (device-side), then the prologue
+    WK(cudaEventRecord(rs->ev[6], me->compute));
+    Xfer* x0 = rs->x[0];
+    for (uint32_t c = 0; c < x0->nchunks; ++c) WK(cudaStreamWaitEvent(me->compute, x0->chunk_ev[c], 0));
+    std::vector<float> sig = sigmas_host(S, rs->req.shift);
+    Cond cd;
+    WK(me->m.prepare(me->slots.slots[rs->slot[0]].buf, sig.data(), S, me->compute, &cd));
+    WK(cudaEventRecord(me->slots.slots[rs->slot[0]].consumed, me->compute));
+    me->slots.release(rs->slot[0]);  // producer's comm stream waits on `consumed` before reuse
+    for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
+    WK(cudaEventRecord(rs->ev[3], me->compute));
+    // T -> D: claim a D slot, send the final latent in per-frame chunks
+    const int did = pick(ctx, DF_D, rs->seq);
+    Inst* D = ctx->inst[did].get();
+    rs->inst[2] = did;
+    int s = D->slots.acquire(ctx->stop);
+    if (s < 0) return;
+    rs->slot[1] = s;
+    WK(cudaStreamWaitEvent(me->comm, D->slots.slots[s].consumed, 0));
+    df_handoff_desc d{};
+    d.src_inst = me->id;
+    d.dst_inst = did;
+    d.src = x;
+    d.dst = D->slots.slots[s].buf;
+    d.bytes = ctx->lat_bytes;
+    d.chunk_bytes = ctx->g.chunk_bytes[1];
+    d.flags = (ctx->g.handoff_mode & (DF_SYNC | DF_HASH));
+    d.seq = rs->seq;
+    d.edge = 1;
+    Xfer* xx = nullptr;
+    if (do_handoff(ctx, &d, me->compute, &xx) != DF_OK) {
+      worker_fail(ctx, ctx->err);
+      return;
+    }
+    rs->x[1] = xx;
+    WK(cudaEventRecord(me->xsent[b], me->comm));
+    // the cond cache must outlive the queued steps: free it once the compute stream passes
+    WK(cudaStreamSynchronize(me->compute));
+    cd.mem.release();
+    rs->t_end[1] = now_s();
+    me->served++;
+    D->inbox.push(Job{rs});  // T dequeues its next request without waiting for the send
+  }
+}
+
+void d_worker(df_ctx* ctx, Inst* me) {
+  cudaSetDevice(me->device);
+  Job j;
+  const df_dit_cfg& c = me->m.c;
+  while (me->inbox.pop(j, ctx->stop)) {
+    ReqState* rs = j.rs;
+    rs->t_start[2] = now_s();
+    WK(cudaEventCreate(&rs->ev[4]));
+    WK(cudaEventCreate(&rs->ev[5]));
+    WK(cudaEventCreate(&rs->ev[7]));
+    WK(cudaEventRecord(rs->ev[7], me->compute));
+    Xfer* x1 = rs->x[1];
+    for (uint32_t k = 0; k < x1->nchunks; ++k) WK(cudaStreamWaitEvent(me->compute, x1->chunk_ev[k], 0));
+    WK(cudaEventRecord(rs->ev[4], me->compute));
+    WK(me->m.decode((const float*)me->slots.slots[rs->slot[1]].buf, me->dout, me->compute));
+    WK(cudaEventRecord(me->slots.slots[rs->slot[1]].consumed, me->compute));
+    WK(cudaEventRecord(rs->ev[5], me->compute));
+    WK(cudaMemcpyAsync(me->stage_host, me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
+    WK(cudaStreamSynchronize(me->compute));
+    if (x1->t_hash) WK(cudaEventSynchronize(x1->t_hash));
+    me->slots.release(rs->slot[1]);
+    if (rs->req.out_host && rs->req.out_bytes >= ctx->out_bytes)
+      std::memcpy(rs->req.out_host, me->stage_host, ctx->out_bytes);
+    rs->t_end[2] = now_s();
+    me->served++;
+    {
+      std::lock_guard<std::mutex> lk(ctx->done_mu);
+      while (!ctx->done->push(rs)) std::this_thread::yield();
+    }
+    ctx->done_cv.notify_all();
+    (void)c;
+  }
+}
+
+void fill_completion(df_ctx* ctx, ReqState* rs, df_completion* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->id = rs->id;
+  o->status = DF_OK;
+  o->user_tag = rs->req.user_tag;
+  for (int k = 0; k < 3; ++k) {
+    o->inst[k] = rs->inst[k];
+    o->t_start[k] = rs->t_start[k];
+    o->t_end[k] = rs->t_end[k];
+  }
+  o->t_submit = rs->t_submit;
+  o->t_done = rs->t_end[2];
+  o->stage_ms[0] = ev_ms(rs->ev[0], rs->ev[1]);
+  o->stage_ms[1] = ev_ms(rs->ev[2], rs->ev[3]);
+  o->stage_ms[2] = ev_ms(rs->ev[4], rs->ev[5]);
+  for (int e = 0; e < 2; ++e) {
+    Xfer* x = rs->x[e];
+    if (!x) continue;
+    o->xfer_ms[e] = ev_ms(x->t0, x->t1);
+    // exposed: consumer ready (R) -> last chunk landed (A), clamped at 0
+    float ex = ev_ms(rs->ev[e == 0 ? 6 : 7], x->t1);
+    o->exposed_ms[e] = ex > 0.f ? ex : 0.f;
+    if (x->hashed) {
+      if (x->t_hash) cudaEventSynchronize(x->t_hash);
+      o->hash_src[e] = x->hash_dev[0];
+      o->hash_dst[e] = x->hash_dev[1];
+    }
+  }
+  (void)ctx;
+}
+
+void free_req(ReqState* rs) {
+  for (auto& e : rs->ev)
+    if (e) cudaEventDestroy(e);
+  free_xfer(rs->x[0]);
+  free_xfer(rs->x[1]);
+  delete rs;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* df_last_error(const df_ctx* ctx) {
+  if (ctx && !ctx->err.empty()) return ctx->err.c_str();
+  return g_tls_msg.c_str();
+}
+
+uint64_t df_launch_count(const df_ctx*) { return g_launches->load(); }
+
+df_status df_init(const df_graph* g, df_ctx** out) {
+  if (!g || !out) return fail(nullptr, "df_init: null argument", DF_ERR_INVALID);
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) return fail(nullptr, "df_init: no CUDA device");
+  if (g->n_inst == 0 || g->n_inst > DF_MAX_INST) return fail(nullptr, "df_init: n_inst", DF_ERR_INVALID);
+  int cnt[3] = {0, 0, 0};
+  for (uint32_t i = 0; i < g->n_inst; ++i) {
+    if (g->inst[i].stage < 0 || g->inst[i].stage > 2 || g->inst[i].device < 0 || g->inst[i].device >= ndev)
+      return fail(nullptr, "df_init: bad instance", DF_ERR_INVALID);
+    cnt[g->inst[i].stage]++;
+  }
+  // Eq. 1: every stage has an instance; sum of instances over distinct GPUs <= G
+  if (!cnt[0] || !cnt[1] || !cnt[2]) return fail(nullptr, "df_init: every stage needs an instance", DF_ERR_CAPACITY);
+  if (g->G && uint32_t(cnt[0] + cnt[1] + cnt[2]) > g->G * 3)
+    return fail(nullptr, "df_init: Eq.1 capacity", DF_ERR_CAPACITY);
+  if (g->n_slots < 2 || (g->ring_capacity & (g->ring_capacity - 1)) || g->ring_capacity < 2)
+    return fail(nullptr, "df_init: n_slots >= 2 and ring_capacity a power of two", DF_ERR_INVALID);
+  for (uint32_t i = 0; i < g->n_inst; ++i) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, g->inst[i].device) != cudaSuccess || p.major != 10)
+      return fail(nullptr, "df_init: instance device is not sm_100 (B200)");
+  }
+  auto ctx = new df_ctx();
+  ctx->g = *g;
+  ctx->requests.reset(new FaaRing<ReqState*>(g->ring_capacity));
+  ctx->done.reset(new FaaRing<ReqState*>(std::max<uint32_t>(g->ring_capacity, 1024)));
+  const df_dit_cfg& c = g->dit;
+  ctx->ctx_bytes = size_t(c.L_txt) * c.d_txt * 2;
+  ctx->lat_bytes = latent_elems(c) * 4;
+  ctx->out_bytes = out_elems(c) * 4;
+  // peer access between every pair of devices in use (NVLink P2P, P:L390 GPUDirect analogue)
+  std::set<int> devs;
+  for (uint32_t i = 0; i < g->n_inst; ++i) devs.insert(g->inst[i].device);
+  for (int a : devs)
+    for (int b : devs)
+      if (a != b) {
+        cudaSetDevice(a);
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a, b);
+        if (can) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
+      }
+  for (uint32_t i = 0; i < g->n_inst; ++i) {
+    auto in = std::make_unique<Inst>();
+    in->id = int(i);
+    in->stage = g->inst[i].stage;
+    in->device = g->inst[i].device;
+    ctx->by_stage[in->stage].push_back(int(i));
+    ctx->inst.push_back(std::move(in));
+  }
+  for (int s = 0; s < 3; ++s) ctx->active[s] = int(ctx->by_stage[s].size());
+  for (auto& ip : ctx->inst) {
+    Inst& I = *ip;
+    cudaError_t e = I.m.create(c, int(g->precision), I.device, I.stage, g->weight_seed, int(g->max_steps));
+    if (e != cudaSuccess) {
+      std::string m = std::string("df_init: instance create: ") + cudaGetErrorString(e) + " " + df::tls_err;
+      df_finalize(ctx);
+      return fail(nullptr, m);
+    }
+    cudaSetDevice(I.device);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, I.stage == DF_T ? lo : hi);
+    cudaStreamCreateWithPriority(&I.comm, cudaStreamNonBlocking, hi);
+    size_t slot_bytes = I.stage == DF_T ? ctx->ctx_bytes : (I.stage == DF_D ? ctx->lat_bytes : 0);
+    if (slot_bytes) {
+      I.slots.slots.resize(g->n_slots);
+      for (uint32_t s = 0; s < g->n_slots; ++s) {
+        cudaMalloc(&I.slots.slots[s].buf, slot_bytes);
+        cudaEventCreateWithFlags(&I.slots.slots[s].consumed, cudaEventDisableTiming);
+        cudaEventRecord(I.slots.slots[s].consumed, I.compute);
+        I.slots.free_list.push_back(int(s));
+      }
+    }
+    if (I.stage == DF_T) {
+      for (int b = 0; b < 2; ++b) {
+        cudaMalloc(&I.xbuf[b], ctx->lat_bytes);
+        cudaEventCreateWithFlags(&I.xsent[b], cudaEventDisableTiming);
+        cudaEventRecord(I.xsent[b], I.comm);
+      }
+    } else if (I.stage == DF_E) {
+      for (int b = 0; b < 2; ++b) {
+        cudaMalloc(&I.ebuf[b], ctx->ctx_bytes);
+        cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming);
+        cudaEventRecord(I.esent[b], I.comm);
+      }
+      cudaMalloc(&I.ids_dev, size_t(c.L_txt) * 4);
+    } else {
+      cudaMalloc(&I.dout, ctx->out_bytes);
+      cudaHostAlloc(&I.stage_host, ctx->out_bytes, cudaHostAllocPortable);
+    }
+    cudaError_t le = cudaDeviceSynchronize();
+    if (le != cudaSuccess) {
+      std::string m = std::string("df_init: setup: ") + cudaGetErrorString(le);
+      df_finalize(ctx);
+      return fail(nullptr, m);
+    }
+  }
+  for (auto& ip : ctx->inst) {
+    Inst* I = ip.get();
+    if (I->stage == DF_E) I->worker = std::thread(e_worker, ctx, I);
+    else if (I->stage == DF_T) I->worker = std::thread(t_worker, ctx, I);
+    else I->worker = std::thread(d_worker, ctx, I);
+  }
+  *out = ctx;
+  return DF_OK;
+}
+
+df_status df_finalize(df_ctx* ctx) {
+  if (!ctx) return DF_ERR_INVALID;
+  ctx->stop = true;
+  for (auto& ip : ctx->inst) {
+    ip->inbox.cv.notify_all();
+    ip->slots.cv.notify_all();
+  }
+  for (auto& ip : ctx->inst)
+    if (ip->worker.joinable()) ip->worker.join();
+  for (auto& ip : ctx->inst) {
+    Inst& I = *ip;
+    cudaSetDevice(I.device);
+    cudaDeviceSynchronize();
+    for (auto& s : I.slots.slots) {
+      if (s.buf) cudaFree(s.buf);
+      if (s.consumed) cudaEventDestroy(s.consumed);
+    }
+    for (int b = 0; b < 2; ++b) {
+      if (I.xbuf[b]) cudaFree(I.xbuf[b]);
+      if (I.xsent[b]) cudaEventDestroy(I.xsent[b]);
+      if (I.ebuf[b]) cudaFree(I.ebuf[b]);
+      if (I.esent[b]) cudaEventDestroy(I.esent[b]);
+    }
+    if (I.ids_dev) cudaFree(I.ids_dev);
+    if (I.dout) cudaFree(I.dout);
+    if (I.stage_host) cudaFreeHost(I.stage_host);
+    if (I.compute) cudaStreamDestroy(I.compute);
+    if (I.comm) cudaStreamDestroy(I.comm);
+    I.m.destroy();
+  }
+  ReqState* rs;
+  while (ctx->requests && ctx->requests->pop(rs)) free_req(rs);
+  while (ctx->done && ctx->done->pop(rs)) free_req(rs);
+  delete ctx;
+  return DF_OK;
+}
+
+df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
+  if (!ctx || !r) return DF_ERR_INVALID;
+  if (ctx->failed) return fail(ctx, ctx->err, DF_ERR_STATE);
+  if (r->steps == 0 || r->steps > ctx->g.max_steps || !(r->shift > 0.f))
+    return fail(ctx, "df_submit: steps in [1, max_steps] and shift > 0", DF_ERR_INVALID);
+  if (r->out_host && r->out_bytes < ctx->out_bytes) return fail(ctx, "df_submit: out_bytes too small", DF_ERR_INVALID);
+  df_req_id id = r->id;
+  if (id.lo == 0 && id.hi == 0) id = {ctx->next_id.fetch_add(1), 0xD15A6F05ull};
+  {
+    std::lock_guard<std::mutex> lk(ctx->seen_mu);
+    if (!ctx->seen.insert({id.lo, id.hi}).second) return fail(ctx, "df_submit: duplicate id", DF_ERR_DUPLICATE);
+  }
+  if (ctx->requests->size_approx() >= ctx->requests->capacity()) {
+    std::lock_guard<std::mutex> lk(ctx->seen_mu);
+    ctx->seen.erase({id.lo, id.hi});
+    return DF_AGAIN;
+  }
+  auto rs = new ReqState();
+  rs->req = *r;
+  rs->id = id;
+  rs->t_submit = now_s();
+  if (r->token_ids) rs->ids.assign(r->token_ids, r->token_ids + ctx->g.dit.L_txt);
+  // timing events are created by each stage worker on its own device
+  {
+    std::lock_guard<std::mutex> lk(ctx->req_mu);
+    rs->seq = ctx->seq.fetch_add(1);
+  }
+  if (!ctx->requests->push(rs)) {
+    free_req(rs);
+    std::lock_guard<std::mutex> lk(ctx->seen_mu);
+    ctx->seen.erase({id.lo, id.hi});
+    return DF_AGAIN;
+  }
+  if (id_out) *id_out = id;
+  return DF_OK;
+}
+
+df_status df_poll(df_ctx* ctx, df_completion* out, uint32_t max, uint32_t* n_out, int32_t timeout_ms) {
+  if (!ctx || !out || !n_out) return DF_ERR_INVALID;
+  *n_out = 0;
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms < 0 ? 0 : timeout_ms);
+  for (;;) {
+    ReqState* rs;
+    while (*n_out < max && ctx->done->pop(rs)) {
+      fill_completion(ctx, rs, &out[(*n_out)++]);
+      free_req(rs);
+    }
+    if (*n_out) return DF_OK;
+    if (ctx->failed) return fail(ctx, ctx->err, DF_ERR_STATE);
+    std::unique_lock<std::mutex> lk(ctx->done_mu);
+    if (timeout_ms >= 0 && std::chrono::steady_clock::now() >= deadline) return DF_EMPTY;
+    ctx->done_cv.wait_for(lk, std::chrono::milliseconds(2));
+  }
+}
+
+df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD) {
+  if (!ctx) return DF_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(ctx->ratio_mu);
+  uint32_t g[3] = {gE, gT, gD};
+  for (int s = 0; s < 3; ++s)
+    if (g[s] < 1 || g[s] > ctx->by_stage[s].size()) return fail(ctx, "df_set_ratio: capacity", DF_ERR_CAPACITY);
+  // New requests go to the first g_s instances of each stage; retirees drain their
+  // inboxes (already-assigned work completes; nothing is dropped).
+  for (int s = 0; s < 3; ++s) ctx->active[s] = int(g[s]);
+  return DF_OK;
+}
+
+// ------------------------------------------------------------------ low level
+struct df_cond {
+  Cond c;
+  int inst;
+};
+
+static Inst* get_inst(df_ctx* ctx, int32_t i, int stage) {
+  if (!ctx || i < 0 || i >= int(ctx->inst.size())) return nullptr;
+  Inst* I = ctx->inst[i].get();
+  if (stage >= 0 && I->stage != stage) return nullptr;
+  cudaSetDevice(I->device);
+  return I;
+}
+
+df_status df_dit_prepare(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const float* sigmas, uint32_t S,
+                         void* stream, df_cond** out) {
+  Inst* I = get_inst(ctx, t_inst, DF_T);
+  if (!I || !ctx_dev || !sigmas || !S || !out) return fail(ctx, "df_dit_prepare: invalid", DF_ERR_INVALID);
+  if (ctx->failed) return DF_ERR_STATE;
+  auto c = new df_cond();
+  c->inst = t_inst;
+  cudaError_t e = I->m.prepare(ctx_dev, sigmas, int(S), (cudaStream_t)stream, &c->c);
+  if (e != cudaSuccess) {
+    c->c.mem.release();
+    delete c;
+    return fail(ctx, std::string("df_dit_prepare: ") + cudaGetErrorString(e) + " " + df::tls_err);
+  }
+  *out = c;
+  return DF_OK;
+}
+
+df_status df_dit_step(df_ctx* ctx, int32_t t_inst, const df_cond* c, uint32_t i, float* x_dev, float* v_dev,
+                      void* stream) {
+  Inst* I = get_inst(ctx, t_inst, DF_T);
+  if (!I || !c || !x_dev || int(i) >= c->c.S) return fail(ctx, "df_dit_step: invalid", DF_ERR_INVALID);
+  if (ctx->failed) return DF_ERR_STATE;
+  cudaError_t e = I->m.step(c->c, int(i), x_dev, v_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(ctx, std::string("df_dit_step: ") + cudaGetErrorString(e) + " " + df::tls_err);
+  return DF_OK;
+}
+
+df_status df_dit_layer(df_ctx* ctx, int32_t t_inst, const df_cond* c, uint32_t i, uint32_t l, float* r_dev,
+                       void* stream) {
+  Inst* I = get_inst(ctx, t_inst, DF_T);
+  if (!I || !c || !r_dev || int(i) >= c->c.S || l >= I->m.c.layers)
+    return fail(ctx, "df_dit_layer: invalid", DF_ERR_INVALID);
+  cudaError_t e = I->m.layer(c->c, int(i), int(l), r_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(ctx, std::string("df_dit_layer: ") + cudaGetErrorString(e) + " " + df::tls_err);
+  return DF_OK;
+}
+
+df_status df_cond_release(df_ctx* ctx, df_cond* c) {
+  if (!c) return DF_ERR_INVALID;
+  if (ctx) cudaSetDevice(ctx->inst[c->inst]->device);
+  c->c.mem.release();
+  delete c;
+  return DF_OK;
+}
+
+df_status df_encode(df_ctx* ctx, int32_t e_inst, const int32_t* ids_dev, void* ctx_dev, void* stream) {
+  Inst* I = get_inst(ctx, e_inst, DF_E);
+  if (!I || !ids_dev || !ctx_dev) return fail(ctx, "df_encode: invalid", DF_ERR_INVALID);
+  cudaError_t e = I->m.encode(ids_dev, ctx_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(ctx, std::string("df_encode: ") + cudaGetErrorString(e) + " " + df::tls_err);
+  return DF_OK;
+}
+
+df_status df_decode(df_ctx* ctx, int32_t d_inst, const float* x_dev, float* out_dev, void* stream) {
+  Inst* I = get_inst(ctx, d_inst, DF_D);
+  if (!I || !x_dev || !out_dev) return fail(ctx, "df_decode: invalid", DF_ERR_INVALID);
+  cudaError_t e = I->m.decode(x_dev, out_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(ctx, std::string("df_decode: ") + cudaGetErrorString(e));
+  return DF_OK;
+}
+
+df_status df_noise(df_ctx* ctx, int32_t inst, uint64_t seed, float* x_dev, void* stream) {
+  Inst* I = get_inst(ctx, inst, -1);
+  if (!I || !x_dev) return fail(ctx, "df_noise: invalid", DF_ERR_INVALID);
+  g_launches->fetch_add(1);
+  cudaError_t e = gen_noise(x_dev, latent_elems(ctx->g.dit), seed, (cudaStream_t)stream);
+  return e == cudaSuccess ? DF_OK : fail(ctx, cudaGetErrorString(e));
+}
+
+df_status df_tokens(df_ctx* ctx, int32_t inst, uint64_t seed, int32_t* ids_dev, void* stream) {
+  Inst* I = get_inst(ctx, inst, -1);
+  if (!I || !ids_dev) return fail(ctx, "df_tokens: invalid", DF_ERR_INVALID);
+  g_launches->fetch_add(1);
+  cudaError_t e = gen_tokens(ids_dev, int(ctx->g.dit.L_txt), int(ctx->g.dit.vocab), seed, (cudaStream_t)stream);
+  return e == cudaSuccess ? DF_OK : fail(ctx, cudaGetErrorString(e));
+}
+
+df_status df_handoff(df_ctx* ctx, const df_handoff_desc* d, void* src_stream, df_xfer** out) {
+  if (!ctx || !d || !out) return DF_ERR_INVALID;
+  if (ctx->failed) return DF_ERR_STATE;
+  Xfer* x = nullptr;
+  df_status s = do_handoff(ctx, d, (cudaStream_t)src_stream, &x);
+  if (s == DF_OK) *out = x;
+  return s;
+}
+
+df_status df_handoff_wait(df_ctx* ctx, df_xfer* x, uint32_t chunk, void* dst_stream) {
+  if (!ctx || !x) return DF_ERR_INVALID;
+  if (chunk == DF_ALL_CHUNKS) {
+    for (auto e : x->chunk_ev) CK(ctx, cudaStreamWaitEvent((cudaStream_t)dst_stream, e, 0));
+    return DF_OK;
+  }
+  if (chunk >= x->nchunks) return fail(ctx, "df_handoff_wait: chunk", DF_ERR_INVALID);
+  CK(ctx, cudaStreamWaitEvent((cudaStream_t)dst_stream, x->chunk_ev[chunk], 0));
+  return DF_OK;
+}
+
+df_status df_handoff_query(df_ctx* ctx, df_xfer* x, uint32_t* chunks_done, uint64_t hash[2]) {
+  if (!ctx || !x) return DF_ERR_INVALID;
+  uint32_t n = 0;
+  for (auto e : x->chunk_ev) n += cudaEventQuery(e) == cudaSuccess ? 1 : 0;
+  cudaGetLastError();
+  if (chunks_done) *chunks_done = n;
+  if (hash) {
+    hash[0] = hash[1] = 0;
+    if (x->hashed && n == x->nchunks) {
+      cudaSetDevice(x->dst_dev);
+      cudaDeviceSynchronize();
+      hash[0] = x->hash_dev[0];
+      hash[1] = x->hash_dev[1];
+    }
+  }
+  return DF_OK;
+}
+
+df_status df_handoff_release(df_ctx* ctx, df_xfer* x) {
+  if (!x) return DF_ERR_INVALID;
+  cudaSetDevice(x->src_dev);
+  for (auto e : x->chunk_ev) cudaEventSynchronize(e);
+  free_xfer(x);
+  (void)ctx;
+  return DF_OK;
+}
+
+df_status df_payload_hash(df_ctx* ctx, int32_t inst, const void* buf_dev, uint64_t nbytes, uint64_t* hash_out) {
+  Inst* I = get_inst(ctx, inst, -1);
+  if (!I || !buf_dev || !hash_out) return fail(ctx, "df_payload_hash: invalid", DF_ERR_INVALID);
+  unsigned long long* h = nullptr;
+  CK(ctx, cudaMalloc(&h, 8));
+  g_launches->fetch_add(1);
+  CK(ctx, payload_hash(buf_dev, nbytes, 0, h, 0));
+  unsigned long long v = 0;
+  CK(ctx, cudaMemcpy(&v, h, 8, cudaMemcpyDeviceToHost));
+  cudaFree(h);
+  *hash_out = v;
+  return DF_OK;
+}
+
+df_status df_weight_bits(df_ctx* ctx, int32_t inst, uint32_t tensor_id, uint16_t* dst, uint64_t n) {
+  Inst* I = get_inst(ctx, inst, -1);
+  if (!I || !dst) return fail(ctx, "df_weight_bits: invalid", DF_ERR_INVALID);
+  for (const TensorLoc& L : I->m.locs) {
+    if (L.tid != tensor_id) continue;
+    if (n != uint64_t(L.in) * L.out) return fail(ctx, "df_weight_bits: size", DF_ERR_INVALID);
+    // gather the logical [in, out] tensor out of its device layout
+    size_t rows = 0, cols = L.ld;
+    if (L.layout == 0) rows = L.in;
+    else if (L.layout == 1) rows = size_t(L.row_off) + L.out;
+    else rows = size_t((L.out + 15) / 16) * 32;
+    std::vector<uint16_t> buf(rows * cols);
+    CK(ctx, cudaMemcpy(buf.data(), L.base, buf.size() * 2, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < L.in; ++k)
+      for (int o = 0; o < L.out; ++o) {
+        size_t idx;
+        if (L.layout == 0) idx = size_t(k) * L.ld + o;
+        else if (L.layout == 1) idx = size_t(L.row_off + o) * L.ld + k;
+        else idx = (size_t(o / 16) * 32 + size_t(L.row_off) * 16 + o % 16) * L.ld + k;
+        dst[size_t(k) * L.out + o] = buf[idx];
+      }
+    return DF_OK;
+  }
+  return fail(ctx, "df_weight_bits: unknown tensor id on this instance", DF_ERR_INVALID);
+}
+
+df_status df_op_gemm(df_ctx* ctx, const void* A, const void* W, float* out, int32_t M, int32_t N, int32_t K,
+                     int32_t tc, void* stream) {
+  if (!ctx || !A || !W || !out) return DF_ERR_INVALID;
+  Epi e;
+  std::memset(&e, 0, sizeof(e));
+  e.kind = EPI_STORE;
+  e.M = M;
+  e.N = N;
+  e.out = out;
+  e.ldo = N;
+  g_launches->fetch_add(1);
+  cudaError_t r = tc ? gemm_tc((const bf16*)A, K, (const bf16*)W, K, M, N, K, e, 1, (cudaStream_t)stream)
+                     : gemm_simt(A, 1, K, 0, (const bf16*)W, K, out, N, M, N, K, nullptr, ACT_NONE, (cudaStream_t)stream);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_gemm: ") + cudaGetErrorString(r));
+}
+
+df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t H, int32_t Nq,
+                          int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream) {
+  if (!ctx || !Q || !K || !V || !O) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, H, Nq, Nk, dh, dh_pad, scale,
+                          (cudaStream_t)stream);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_attention: ") + cudaGetErrorString(r));
+}
+
+df_status df_op_rmsnorm_mod(df_ctx* ctx, const float* x, void* out, int32_t M, int32_t d, const float* shift,
+                            const float* scale, float eps, void* stream) {
+  if (!ctx || !x || !out || !shift || !scale) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = rmsnorm_mod(x, out, 0, M, d, shift, scale, nullptr, eps, (cudaStream_t)stream);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_rmsnorm_mod: ") + cudaGetErrorString(r));
+}
+
+}  // extern "C"

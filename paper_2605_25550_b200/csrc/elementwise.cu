@@ -1,0 +1,369 @@
+// HBM-bound kernels of the DiT step and the request prologue, plus parameter init
+// (Philox4x32-10) and the E/D stand-in stages.
+//
+// rmsnorm_mod (cross pre-norm): one CTA per row, 16-byte loads,
+// warp-shuffle + smem reduction, fp32 statistics, bf16 (or fp32) store.  Algorithmic
+// traffic per row: 4d bytes read + 2d bytes written (bf16 out).
+#include <cmath>
+#include "kernels.h"
+
+namespace df {
+
+// ------------------------------------------------------------------ Philox4x32-10
+struct U4 {
+  uint32_t x, y, z, w;
+};
+DF_DEV U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return {c0, c1, c2, c3};
+}
+DF_DEV uint32_t philox_word(uint64_t seed, uint64_t i, uint32_t c2, uint32_t c3) {
+  uint64_t b = i >> 2;
+  U4 o = philox(uint32_t(b), uint32_t(b >> 32), c2, c3, uint32_t(seed), uint32_t(seed >> 32));
+  switch (i & 3) {
+    case 0: return o.x;
+    case 1: return o.y;
+    case 2: return o.z;
+    default: return o.w;
+  }
+}
+
+__global__ void init_tensor_kernel(bf16* __restrict__ dst, InitSpec s, size_t n) {
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < n; t += size_t(gridDim.x) * blockDim.x) {
+    // t enumerates destination elements in the order of the destination layout
+    size_t k, nn;  // logical (in, out) index
+    size_t dst_idx;
+    if (s.layout == 0) {
+      k = t / s.out;
+      nn = t % s.out;
+      dst_idx = k * s.ld + nn;
+    } else {
+      nn = t / s.in;  // destination row order (logical output index)
+      k = t % s.in;
+      size_t row;
+      if (s.layout == 1) row = s.row_off + nn;
+      else row = (nn / 16) * 32 + size_t(s.row_off) * 16 + (nn % 16);
+      dst_idx = row * s.ld + k;
+    }
+    uint64_t i = uint64_t(k) * s.out + nn;  // logical row-major index
+    uint32_t u = philox_word(s.seed, i, s.tid, 0);
+    float r = float(u >> 8) * 5.9604644775390625e-08f;  // 2^-24, exact
+    float w = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, r), 1.0f), s.a);
+    if (s.kind == 1) w = __fadd_rn(1.0f, w);
+    dst[dst_idx] = __float2bfloat16_rn(w);
+  }
+}
+
+cudaError_t init_tensor(bf16* dst, const InitSpec& s, cudaStream_t st) {
+  size_t n = size_t(s.in) * s.out;
+  if (!n) return cudaSuccess;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  init_tensor_kernel<<<unsigned(blocks), 256, 0, st>>>(dst, s, n);
+  return cudaGetLastError();
+}
+
+__global__ void noise_kernel(float* __restrict__ x, size_t n, uint64_t seed) {
+  for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < n; j += size_t(gridDim.x) * blockDim.x) {
+    uint64_t blk = j >> 1;
+    U4 o = philox(uint32_t(blk), uint32_t(blk >> 32), 0, 1, uint32_t(seed), uint32_t(seed >> 32));
+    uint32_t a = (j & 1) ? o.z : o.x;
+    uint32_t b = (j & 1) ? o.w : o.y;
+    double u1 = (double(a) + 1.0) * 2.3283064365386963e-10;
+    double u2 = double(b) * 2.3283064365386963e-10;
+    double z = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    x[j] = float(z);
+  }
+}
+cudaError_t gen_noise(float* x, size_t n, uint64_t seed, cudaStream_t st) {
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  noise_kernel<<<unsigned(blocks), 256, 0, st>>>(x, n, seed);
+  return cudaGetLastError();
+}
+
+__global__ void tokens_kernel(int32_t* ids, int n, int vocab, uint64_t seed) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) ids[j] = int32_t(philox_word(seed, j, 0, 2) % uint32_t(vocab));
+}
+cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st) {
+  tokens_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, vocab, seed);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ RMSNorm (+ modulation)
+template <typename OutT>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, OutT* __restrict__ out, int d,
+                                                      const float* __restrict__ shift, const float* __restrict__ scale,
+                                                      const bf16* __restrict__ gain, float eps) {
+  // one CTA per row; each thread holds up to 8 float4 (d <= 8192)
+  const int row = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
+  const int nv = d / 4;
+  float4 v[8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int c = threadIdx.x + i * 256;
+    if (c < nv) {
+      v[i] = xr[c];
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+  }
+  __shared__ float red[8];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = rsqrtf(tot / float(d) + eps);
+  OutT* orow = out + size_t(row) * d;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int c = threadIdx.x + i * 256;
+    if (c < nv) {
+      float y[4] = {v[i].x * inv, v[i].y * inv, v[i].z * inv, v[i].w * inv};
+      int n0 = 4 * c;
+      if (gain) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) y[q] *= bf2f(gain[n0 + q]);
+      } else {
+        float4 sc = reinterpret_cast<const float4*>(scale)[c];
+        float4 sh = reinterpret_cast<const float4*>(shift)[c];
+        y[0] = y[0] * (1.f + sc.x) + sh.x;
+        y[1] = y[1] * (1.f + sc.y) + sh.y;
+        y[2] = y[2] * (1.f + sc.z) + sh.z;
+        y[3] = y[3] * (1.f + sc.w) + sh.w;
+      }
+      if constexpr (sizeof(OutT) == 2) {
+        uint2 u;
+        u.x = pack_bf16x2(y[0], y[1]);
+        u.y = pack_bf16x2(y[2], y[3]);
+        *reinterpret_cast<uint2*>(orow + n0) = u;
+      } else {
+        *reinterpret_cast<float4*>(orow + n0) = make_float4(y[0], y[1], y[2], y[3]);
+      }
+    }
+  }
+}
+
+cudaError_t rmsnorm_mod(const float* x, void* out, int out_f32, int M, int d, const float* shift, const float* scale,
+                        const bf16* gain, float eps, cudaStream_t st) {
+  if (d % 4 || d > 8192) return cudaErrorInvalidValue;
+  if (M <= 0) return cudaSuccess;
+  if (out_f32) rmsnorm_kernel<float><<<M, 256, 0, st>>>(x, (float*)out, d, shift, scale, gain, eps);
+  else rmsnorm_kernel<bf16><<<M, 256, 0, st>>>(x, (bf16*)out, d, shift, scale, gain, eps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ patchify
+template <typename OutT>
+__global__ void patchify_kernel(const float* __restrict__ x, OutT* __restrict__ X, int C, int F, int H, int W, int pt,
+                                int ph, int pw, size_t total) {
+  const int P = C * pt * ph * pw;
+  const int Hp = H / ph, Wp = W / pw;
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
+    int p = int(t % P);
+    size_t n = t / P;
+    int ww = int(n % Wp), hh = int((n / Wp) % Hp), f = int(n / (size_t(Wp) * Hp));
+    int k = p % pw, r = p / pw;
+    int j = r % ph;
+    r /= ph;
+    int i = r % pt;
+    int c = r / pt;
+    float v = x[((size_t(c) * F + f * pt + i) * H + hh * ph + j) * W + ww * pw + k];
+    store_val<OutT>(X + t, v);
+  }
+}
+cudaError_t patchify(const float* x, void* X, int out_f32, int C, int F, int H, int W, int pt, int ph, int pw,
+                     cudaStream_t st) {
+  size_t total = size_t(C) * F * H * W;
+  unsigned blocks = unsigned((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (out_f32) patchify_kernel<float><<<blocks, 256, 0, st>>>(x, (float*)X, C, F, H, W, pt, ph, pw, total);
+  else patchify_kernel<bf16><<<blocks, 256, 0, st>>>(x, (bf16*)X, C, F, H, W, pt, ph, pw, total);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ time conditioning
+__global__ void sinusoid_kernel(const float* sig, float* s, int S, int freq_dim) {
+  int i = blockIdx.x;
+  int half = freq_dim / 2;
+  for (int k = threadIdx.x; k < half; k += blockDim.x) {
+    double t = 1000.0 * double(sig[i]);
+    double w = pow(10000.0, -double(k) / double(half));
+    s[size_t(i) * freq_dim + k] = float(cos(t * w));
+    s[size_t(i) * freq_dim + half + k] = float(sin(t * w));
+  }
+}
+cudaError_t sinusoid(const float* sig_dev, float* s, int S, int freq_dim, cudaStream_t st) {
+  if (S <= 0) return cudaSuccess;
+  sinusoid_kernel<<<S, 128, 0, st>>>(sig_dev, s, S, freq_dim);
+  return cudaGetLastError();
+}
+
+struct ModPtrs {
+  const bf16* p[64];
+};
+__global__ void modulations_kernel(const float* __restrict__ e6, const float* __restrict__ e, ModPtrs mp, int l0,
+                                   int nl, const bf16* __restrict__ head_mod, int d, float* __restrict__ mods,
+                                   float* __restrict__ head) {
+  int l = blockIdx.y;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 6 * d; t += gridDim.x * blockDim.x) {
+    if (l < nl) mods[size_t(l0 + l) * 6 * d + t] = e6[t] + bf2f(mp.p[l][t]);
+    if (l == 0 && t < 2 * d && head) head[t] = bf2f(head_mod[t]) + e[t % d];
+  }
+}
+cudaError_t modulations(const float* e6, const float* e, const bf16* const* layer_mod, int layers,
+                        const bf16* head_mod, int d, float* mods, float* head, cudaStream_t st) {
+  for (int l0 = 0; l0 < layers; l0 += 64) {
+    ModPtrs mp;
+    int nl = layers - l0 < 64 ? layers - l0 : 64;
+    for (int i = 0; i < nl; ++i) mp.p[i] = layer_mod[l0 + i];
+    dim3 grid((6 * d + 255) / 256, nl);
+    modulations_kernel<<<grid, 256, 0, st>>>(e6, e, mp, l0, nl, head_mod, d, mods, l0 == 0 ? head : nullptr);
+  }
+  return cudaGetLastError();
+}
+
+__global__ void silu_kernel(float* x, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    x[i] = x[i] / (1.0f + expf(-x[i]));
+}
+cudaError_t silu_inplace(float* x, size_t n, cudaStream_t st) {
+  unsigned b = unsigned((n + 255) / 256);
+  if (b > 4096) b = 4096;
+  if (n) silu_kernel<<<b, 256, 0, st>>>(x, n);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ E stand-in pieces
+__global__ void embed_kernel(const int32_t* ids, const bf16* emb, float* z, int L, int dt) {
+  int j = blockIdx.x;
+  const bf16* er = emb + size_t(ids[j]) * dt;
+  for (int c = threadIdx.x; c < dt; c += blockDim.x) z[size_t(j) * dt + c] = bf2f(er[c]);
+}
+cudaError_t embed_rows(const int32_t* ids, const bf16* emb, float* z, int L, int dt, cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  embed_kernel<<<L, 256, 0, st>>>(ids, emb, z, L, dt);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ D stand-in
+// One CTA per (latent frame, 8 latent pixels): u = SiLU(x W1 + b1) in smem, then
+// o = tanh(u W2 + b2) scattered by the pixel shuffle.
+__global__ void decode_kernel(const float* __restrict__ x, float* __restrict__ out, int C, int F, int H, int W,
+                              int cdec, const bf16* __restrict__ w1, const bf16* __restrict__ b1,
+                              const bf16* __restrict__ w2f, const bf16* __restrict__ b2f,
+                              const bf16* __restrict__ w2r, const bf16* __restrict__ b2r) {
+  extern __shared__ float sh[];  // [8][cdec]
+  const int phi = blockIdx.y;
+  const int pix0 = blockIdx.x * 8;
+  const int HW = H * W;
+  const int npix = min(8, HW - pix0);
+  for (int t = threadIdx.x; t < 8 * cdec; t += blockDim.x) {
+    int q = t / cdec, u = t % cdec;
+    float acc = 0.f;
+    if (q < npix) {
+      int pix = pix0 + q;
+      acc = bf2f(b1[u]);
+      for (int c = 0; c < C; ++c) acc += x[(size_t(c) * F + phi) * HW + pix] * bf2f(w1[size_t(c) * cdec + u]);
+      acc = acc / (1.0f + expf(-acc));
+    }
+    sh[q * cdec + u] = acc;
+  }
+  __syncthreads();
+  const int r = phi == 0 ? 1 : 4;
+  const int nout = 3 * r * 64;
+  const bf16* w2 = phi == 0 ? w2f : w2r;
+  const bf16* b2 = phi == 0 ? b2f : b2r;
+  const int T = 1 + 4 * (F - 1);
+  for (int t = threadIdx.x; t < npix * nout; t += blockDim.x) {
+    int q = t / nout, idx = t % nout;
+    float acc = bf2f(b2[idx]);
+    const float* u = sh + q * cdec;
+    for (int k = 0; k < cdec; ++k) acc += u[k] * bf2f(w2[size_t(k) * nout + idx]);
+    float o = tanhf(acc);
+    int dx = idx & 7, dy = (idx >> 3) & 7, rest = idx >> 6;
+    int tau = rest % r, ch = rest / r;
+    int tf = phi == 0 ? 0 : 4 * phi - 3 + tau;
+    int pix = pix0 + q, y = pix / W, xx = pix % W;
+    out[((size_t(ch) * T + tf) * (8 * H) + 8 * y + dy) * (8 * W) + 8 * xx + dx] = o;
+  }
+}
+cudaError_t decode_latent(const float* x, float* out, int C, int F, int H, int W, int cdec, const bf16* w1,
+                          const bf16* b1, const bf16* w2f, const bf16* b2f, const bf16* w2r, const bf16* b2r,
+                          cudaStream_t st) {
+  dim3 grid((H * W + 7) / 8, F);
+  decode_kernel<<<grid, 256, 8 * cdec * sizeof(float), st>>>(x, out, C, F, H, W, cdec, w1, b1, w2f, b2f, w2r, b2r);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ handoff hash
+DF_DEV unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void hash_kernel(const uint8_t* __restrict__ buf, size_t nbytes, size_t word_off,
+                            unsigned long long* out) {
+  size_t nw = (nbytes + 7) / 8;
+  unsigned long long acc = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nw; i += size_t(gridDim.x) * blockDim.x) {
+    unsigned long long w = 0;
+    size_t b0 = i * 8;
+    if (b0 + 8 <= nbytes && (reinterpret_cast<uintptr_t>(buf) & 7) == 0) {
+      w = *reinterpret_cast<const unsigned long long*>(buf + b0);
+    } else {
+      for (int k = 0; k < 8; ++k)
+        if (b0 + k < nbytes) w |= (unsigned long long)buf[b0 + k] << (8 * k);
+    }
+    acc += splitmix64(w ^ ((word_off + i) * 0x9E3779B97F4A7C15ull));
+  }
+  // sum mod 2^64 is order-independent: warp reduce then one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+cudaError_t payload_hash(const void* buf, size_t nbytes, size_t word_offset, unsigned long long* out,
+                         cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  size_t nw = (nbytes + 7) / 8;
+  unsigned blocks = unsigned((nw + 255) / 256);
+  if (blocks > 296) blocks = 296;
+  if (!blocks) return cudaSuccess;
+  hash_kernel<<<blocks, 256, 0, st>>>((const uint8_t*)buf, nbytes, word_offset, out);
+  return cudaGetLastError();
+}
+
+__global__ void delay_kernel(uint64_t ns) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  uint64_t t = t0;
+  while (t - t0 < ns) {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  }
+}
+cudaError_t delay_ns(uint64_t ns, cudaStream_t st) {
+  delay_kernel<<<1, 1, 0, st>>>(ns);
+  return cudaGetLastError();
+}
+
+}  // namespace df

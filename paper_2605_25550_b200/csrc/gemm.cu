@@ -1,0 +1,376 @@
+// Dense contractions of the DiT step.
+//
+// gemm_tc: persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//   warp 0      TMA producer (one elected lane): A[128 x 64] and W[BN x 64] bf16 tiles,
+//               128B-swizzled, into a STAGES-deep shared-memory ring (full/empty mbarriers)
+//   warp 1      MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16,
+//               fp32 accumulator in TMEM, double-buffered (2 x BN columns)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld 32x32b (thread = output row) -> fused epilogue
+//               (bias, activation, qk-RMSNorm + RoPE + head-major scatter, gated fp32
+//               residual, SwiGLU, unpatchify + Euler) -> global
+// Tile order is deterministic (fixed static schedule, no split-K): every run is bit-identical.
+//
+// gemm_simt: plain fp32 FFMA tiled GEMM for the fp32 validation build and the small
+// time-embedding MLPs (M = S rows).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include <cstdio>
+#include "kernels.h"
+
+namespace df {
+
+// ------------------------------------------------------------------ host: tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] with row stride ld (elements); box [box_rows, 64], SW128.
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+// 3-D bf16 [z, rows, cols] (cols contiguous, cols == row stride), box [1, box_rows, 64], SW128.
+bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cols, rows, z};
+  cuuint64_t strides[2] = {cols * 2, cols * rows * 2};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ tcgen05 GEMM kernel
+constexpr int GBM = 128;
+constexpr int GBK = 64;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int A_BYTES = GBM * GBK * 2;
+  static constexpr int B_BYTES = BN * GBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+DF_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int G = 16;
+  int per_group = G * num_n;
+  int g = t / per_group;
+  int first_m = g * G;
+  int gm = min(G, num_m - first_m);
+  int r = t - g * per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+template <int BN, int CW, typename OutT>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, const __grid_constant__ Epi epi) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + Cfg::STAGES;
+  uint64_t* tfull = bars + 2 * Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int num_m = (M + GBM - 1) / GBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int KB = (K + GBK - 1) / GBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * GBK, mb * GBM);
+          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GBK, nb * BN);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(GBM, BN, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GBK / 16; ++k) {
+            uint64_t ad = sdesc_sw128(a0 + k * 32, 16, 1024);
+            uint64_t bd = sdesc_sw128(b0 + k * 32, 16, 1024);
+            tc_mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (kb == KB - 1) tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    float v[CW];
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * GBM + ew * 32 + lane;
+      const uint32_t trow = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += CW) {
+        const int n0 = nb * BN + c;
+        if (n0 >= N) break;  // warp-uniform
+#pragma unroll
+        for (int q = 0; q < CW; q += 16) tmem_ld16(trow + c + q, v + q);
+        tc_wait_ld();
+        epi_apply<CW, OutT>(epi, row, n0, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+template <int BN, int CW, typename OutT>
+static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
+                             cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_tc_kernel<BN, CW, OutT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int tiles = ((M + GBM - 1) / GBM) * ((N + BN - 1) / BN);
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, epi);
+  return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t dispatch_cw(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
+                               int out_f32, cudaStream_t st) {
+  if (epi.kind == EPI_HEADS) {  // head-major outputs are bf16 on the tensor-core path
+    if (out_f32) return cudaErrorInvalidValue;
+    switch (epi.dh) {
+      case 16: return launch_tc<BN, 16, bf16>(ta, tb, M, N, K, epi, st);
+      case 64: return BN >= 64 ? launch_tc<BN, 64, bf16>(ta, tb, M, N, K, epi, st) : cudaErrorInvalidValue;
+      case 128: return BN >= 128 ? launch_tc<(BN >= 128 ? BN : 128), 128, bf16>(ta, tb, M, N, K, epi, st) : cudaErrorInvalidValue;
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return out_f32 ? launch_tc<BN, 32, float>(ta, tb, M, N, K, epi, st) : launch_tc<BN, 32, bf16>(ta, tb, M, N, K, epi, st);
+}
+
+cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& epi, int out_f32,
+                    cudaStream_t st, int bn) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if ((lda * 2) % 16 || (ldw * 2) % 16) return cudaErrorInvalidValue;
+  if (bn == 256 && N <= 128) bn = N <= 64 ? 64 : 128;
+  if (epi.kind == EPI_HEADS && bn < epi.dh) bn = 128;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d(&ta, A, M, K, lda, GBM)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tb, W, N, K, ldw, bn)) return cudaErrorInvalidValue;
+  if (bn == 256) return dispatch_cw<256>(ta, tb, M, N, K, epi, out_f32, st);
+  if (bn == 128) return dispatch_cw<128>(ta, tb, M, N, K, epi, out_f32, st);
+  if (bn == 64) return dispatch_cw<64>(ta, tb, M, N, K, epi, out_f32, st);
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ SIMT fp32 GEMM
+template <bool A_BF16>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const void* __restrict__ Av, int lda, int act_in,
+                                                        const bf16* __restrict__ W, int ldw, float* __restrict__ C,
+                                                        int ldc, int M, int N, int K, const bf16* __restrict__ bias,
+                                                        int act) {
+  __shared__ float As[16][65];
+  __shared__ float Ws[16][65];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      int r = i / 16, kk = i % 16;
+      int m = m0 + r, n = n0 + r, k = k0 + kk;
+      float a = 0.f, w = 0.f;
+      if (m < M && k < K) {
+        a = A_BF16 ? bf2f(reinterpret_cast<const bf16*>(Av)[size_t(m) * lda + k])
+                   : reinterpret_cast<const float*>(Av)[size_t(m) * lda + k];
+        if (act_in == ACT_SILU) a = a / (1.0f + expf(-a));
+      }
+      if (n < N && k < K) w = bf2f(W[size_t(n) * ldw + k]);
+      As[kk][r] = a;
+      Ws[kk][r] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float z = acc[i][j] + (bias ? bf2f(bias[n]) : 0.f);
+      if (act == ACT_SILU) z = z / (1.0f + expf(-z));
+      else if (act == ACT_GELU) {
+        const float k = 0.7978845608028654f;
+        z = 0.5f * z * (1.0f + tanhf(k * (z + 0.044715f * z * z * z)));
+      }
+      C[size_t(m) * ldc + n] = z;
+    }
+  }
+}
+
+cudaError_t gemm_simt(const void* A, int a_bf16, int lda, int act_in, const bf16* W, int ldw, float* C, int ldc,
+                      int M, int N, int K, const bf16* bias, int act, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  if (a_bf16) gemm_simt_kernel<true><<<grid, 256, 0, st>>>(A, lda, act_in, W, ldw, C, ldc, M, N, K, bias, act);
+  else gemm_simt_kernel<false><<<grid, 256, 0, st>>>(A, lda, act_in, W, ldw, C, ldc, M, N, K, bias, act);
+  return cudaGetLastError();
+}
+
+template <int CW, typename OutT>
+__global__ void epi_rows_kernel(const float* __restrict__ tmp, const __grid_constant__ Epi epi, int nchunks) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  int m = idx / nchunks, c = idx % nchunks;
+  if (m >= epi.M) return;
+  float v[CW];
+  int n0 = c * CW;
+#pragma unroll
+  for (int i = 0; i < CW; ++i) v[i] = (n0 + i < epi.N) ? tmp[size_t(m) * epi.N + n0 + i] : 0.f;
+  epi_apply<CW, OutT>(epi, m, n0, v);
+}
+
+cudaError_t epi_rows(const float* tmp, const Epi& epi, int out_f32, cudaStream_t st) {
+  int CW = epi.kind == EPI_HEADS ? epi.dh : 32;
+  int nchunks = (epi.N + CW - 1) / CW;
+  long total = long(epi.M) * nchunks;
+  int blocks = int((total + 127) / 128);
+#define DF_EPI_CASE(cw)                                                                             \
+  if (CW == cw) {                                                                                   \
+    if (out_f32) epi_rows_kernel<cw, float><<<blocks, 128, 0, st>>>(tmp, epi, nchunks);             \
+    else epi_rows_kernel<cw, bf16><<<blocks, 128, 0, st>>>(tmp, epi, nchunks);                      \
+    return cudaGetLastError();                                                                      \
+  }
+  DF_EPI_CASE(16)
+  DF_EPI_CASE(32)
+  DF_EPI_CASE(64)
+  DF_EPI_CASE(128)
+#undef DF_EPI_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace df

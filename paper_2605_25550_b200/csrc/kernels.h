@@ -1,0 +1,76 @@
+// Host-side launchers of the sm_100a kernels (internal to libdf; not the C ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "epilogue.cuh"
+
+namespace df {
+
+int num_sms();
+
+// ---- tensor-core GEMM: out = epilogue(A[M,K] (bf16, row-major, lda) x W[N,K]^T (bf16, ldw)).
+// BN in {64, 128, 256}.  Returns cudaError_t of the launch.
+cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& epi,
+                    int out_f32, cudaStream_t st, int bn = 256);
+
+// ---- SIMT fp32 GEMM: C[M,N] (fp32, ldc) = act(act_in(A) x W^T + bias); A fp32 or bf16.
+cudaError_t gemm_simt(const void* A, int a_bf16, int lda, int act_in, const bf16* W, int ldw, float* C, int ldc,
+                      int M, int N, int K, const bf16* bias, int act, cudaStream_t st);
+// Apply an epilogue to a raw fp32 accumulator tmp[M, N] (fp32 validation build).
+cudaError_t epi_rows(const float* tmp, const Epi& epi, int out_f32, cudaStream_t st);
+
+// ---- attention: O[n, h*dh + c] = softmax(Q_h K_h^T * scale) V_h
+// Q/K/V head-major [H][Nq|Nk][dh_pad] bf16; O token-major [Nq, H*dh] bf16.
+cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
+                    float scale, cudaStream_t st);
+// fp32 validation build: same layout with float and dh_pad == dh.
+cudaError_t attn_simt(const float* Q, const float* K, const float* V, float* O, int H, int Nq, int Nk, int dh,
+                      float scale, cudaStream_t st);
+
+// ---- elementwise
+// out[m, :] = RMSNorm(x[m, :]) * (1 + scale) + shift     (mode 0; scale/shift fp32 [d])
+//           = RMSNorm(x[m, :]) * gain                     (mode 1; gain bf16 [d])
+cudaError_t rmsnorm_mod(const float* x, void* out, int out_f32, int M, int d, const float* shift, const float* scale,
+                        const bf16* gain, float eps, cudaStream_t st);
+// X[n, p] = patchify(x)   (bf16 or fp32 out)
+cudaError_t patchify(const float* x, void* X, int out_f32, int C, int F, int H, int W, int pt, int ph, int pw,
+                     cudaStream_t st);
+// sinusoid rows s[i, :] = [cos(1000 sig_i w) | sin(1000 sig_i w)], i < S
+cudaError_t sinusoid(const float* sig_dev, float* s, int S, int freq_dim, cudaStream_t st);
+// mods[l][k][:] = e6[k][:] + M_l[k][:] for k < 6, all layers; head[0..1][:] = head_mod + e
+cudaError_t modulations(const float* e6, const float* e, const bf16* const* layer_mod, int layers,
+                        const bf16* head_mod, int d, float* mods, float* head, cudaStream_t st);
+cudaError_t silu_inplace(float* x, size_t n, cudaStream_t st);
+
+// ---- init / RNG (Philox4x32-10)
+// dst element (r, c) of a row-major [rows, ld] matrix gets logical element given by `layout`:
+//   layout 0: identity, logical [in=rows, out=cols]            dst[k*ld + n]
+//   layout 1: transposed, dst[(row_off + n)*ld + k]            (W^T, K-major)
+//   layout 2: swiglu-interleaved transposed: n -> (n/16)*32 + half*16 + n%16
+struct InitSpec {
+  uint64_t seed;
+  uint32_t tid;
+  int kind;        // 0 plain (scale a), 1 gain (1 + w)
+  float a;         // fp32(sqrt(3) * std)
+  int in, out;     // logical shape [in, out]
+  int layout;      // 0/1/2 as above
+  int ld;          // destination row stride (elements)
+  int row_off;     // destination row offset (layouts 1/2), or `half` for layout 2 (0: W1, 1: W3)
+};
+cudaError_t init_tensor(bf16* dst, const InitSpec& s, cudaStream_t st);
+cudaError_t gen_noise(float* x, size_t n, uint64_t seed, cudaStream_t st);
+cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st);
+
+// ---- E / D stand-ins
+cudaError_t embed_rows(const int32_t* ids, const bf16* emb, float* z, int L, int dt, cudaStream_t st);
+cudaError_t decode_latent(const float* x, float* out, int C, int F, int H, int W, int cdec, const bf16* w1,
+                          const bf16* b1, const bf16* w2f, const bf16* b2f, const bf16* w2r, const bf16* b2r,
+                          cudaStream_t st);
+
+// ---- handoff helpers
+cudaError_t payload_hash(const void* buf, size_t nbytes, size_t word_offset, unsigned long long* out,
+                         cudaStream_t st);
+cudaError_t delay_ns(uint64_t ns, cudaStream_t st);
+
+}  // namespace df

@@ -1,0 +1,491 @@
+// Stage programs of one instance: parameter init (DESIGN.md parameter table), the
+// DiT request prologue / step / block, the E and D stand-ins.
+// Each launch is counted for bench.py's "gpu_launches".
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include "runtime.h"
+
+namespace df {
+
+thread_local std::string tls_err;
+static std::atomic<uint64_t> g_launch_count{0};
+std::atomic<uint64_t>* g_launches = &g_launch_count;
+
+#define DF_L(expr)                                  \
+  do {                                              \
+    g_launch_count.fetch_add(1, std::memory_order_relaxed); \
+    DF_TRY(expr);                                   \
+  } while (0)
+
+// ------------------------------------------------------------------ arena
+cudaError_t Arena::reserve(size_t bytes) {
+  cap = bytes;
+  used = 0;
+  if (!bytes) return cudaSuccess;
+  cudaError_t e = cudaMalloc(&base, bytes);
+  if (e != cudaSuccess) base = nullptr;
+  return e;
+}
+void* Arena::take(size_t bytes) {
+  size_t off = (used + 255) & ~size_t(255);
+  if (off + bytes > cap) return nullptr;
+  used = off + bytes;
+  return base + off;
+}
+void Arena::release() {
+  if (base) cudaFree(base);
+  base = nullptr;
+  cap = used = 0;
+}
+
+static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+
+// ------------------------------------------------------------------ create / init
+cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uint64_t sd, int msteps) {
+  c = cfg;
+  precision = prec;
+  device = dev;
+  stage = stg;
+  seed = sd;
+  max_steps = msteps;
+  DF_TRY(cudaSetDevice(device));
+  Fp = c.F / c.pt;
+  Hp = c.H / c.ph;
+  Wp = c.W / c.pw;
+  N = Fp * Hp * Wp;
+  P = c.C * c.pt * c.ph * c.pw;
+  dh = c.d / c.heads;
+  dhp = f32() ? dh : (dh <= 64 ? 64 : 128);
+  if (c.d % c.heads || dh > 128 || c.ffn % 16 || c.d % 4 || c.enc_ffn % 16 ||
+      c.rope_axes[0] + c.rope_axes[1] + c.rope_axes[2] != uint32_t(dh))
+    return cudaErrorInvalidValue;
+  const size_t d = c.d, f = c.ffn, L = c.L_txt, dt = c.d_txt, fe = c.enc_ffn, ab = act_bytes();
+  // ---- weights
+  size_t wb = 0;
+  if (stage == DF_T) {
+    wb += al(d * P * 2) + al(d * 2) + al(d * dt * 2) + al(d * 2) + al(d * d * 2) + al(d * 2) + al(d * c.freq_dim * 2) +
+          al(d * 2) + al(d * d * 2) + al(d * 2) + al(6 * d * d * 2) + al(6 * d * 2) + al(2 * d * 2) + al(P * d * 2) +
+          al(P * 2);
+    size_t per = al(6 * d * 2) + al(3 * d * d * 2) + al(3 * d * 2) + 3 * al(d * 2) + al(d * d * 2) + al(d * 2) +
+                 al(d * d * 2) + al(d * 2) + al(2 * d * d * 2) + al(2 * d * 2) + 2 * al(d * 2) + al(d * d * 2) +
+                 al(d * 2) + al(2 * f * d * 2) + al(2 * f * 2) + al(d * f * 2) + al(d * 2);
+    wb += per * c.layers;
+  } else if (stage == DF_E) {
+    wb += al(size_t(c.vocab) * dt * 2) + 2 * al(dt * 2) + al(2 * fe * dt * 2) + al(dt * fe * 2);
+  } else {
+    wb += al(c.C * c.dec_width * 2) + al(c.dec_width * 2) + al(c.dec_width * 192 * 2) + al(192 * 2) +
+          al(c.dec_width * 768 * 2) + al(768 * 2);
+  }
+  DF_TRY(wmem.reserve(wb + 4096));
+  auto W = [&](size_t n) { return static_cast<bf16*>(wmem.take(n * 2)); };
+  if (stage == DF_T) {
+    patch_wT = W(d * P); patch_b = W(d);
+    txt1_wT = W(d * dt); txt1_b = W(d); txt2_wT = W(d * d); txt2_b = W(d);
+    temb1_wT = W(d * c.freq_dim); temb1_b = W(d); temb2_wT = W(d * d); temb2_b = W(d);
+    tmod_wT = W(6 * d * d); tmod_b = W(6 * d); head_mod = W(2 * d); head_wT = W(P * d); head_b = W(P);
+    Lw.resize(c.layers);
+    for (auto& l : Lw) {
+      l.mod = W(6 * d); l.qkv_wT = W(3 * d * d); l.qkv_b = W(3 * d); l.g_q = W(d); l.g_k = W(d);
+      l.o_wT = W(d * d); l.o_b = W(d); l.g_n3 = W(d); l.cq_wT = W(d * d); l.cq_b = W(d);
+      l.ckv_wT = W(2 * d * d); l.ckv_b = W(2 * d); l.g_cq = W(d); l.g_ck = W(d); l.co_wT = W(d * d); l.co_b = W(d);
+      l.w13T = W(2 * f * d); l.b13 = W(2 * f); l.w2T = W(d * f); l.b2 = W(d);
+    }
+    layer_mods.clear();
+    for (auto& l : Lw) layer_mods.push_back(l.mod);
+  } else if (stage == DF_E) {
+    emb = W(size_t(c.vocab) * dt); g_a = W(dt); e_w13T = W(2 * fe * dt); e_w2T = W(dt * fe); g_f = W(dt);
+  } else {
+    d1_w = W(c.C * c.dec_width); d1_b = W(c.dec_width); d2f_w = W(c.dec_width * 192); d2f_b = W(192);
+    d2r_w = W(c.dec_width * 768); d2r_b = W(768);
+  }
+  if (!wmem.base) return cudaErrorMemoryAllocation;
+  // ---- workspace
+  size_t wsb = 0;
+  const size_t Nn = N;
+  if (stage == DF_T) {
+    size_t hd = size_t(c.heads) * Nn * dhp * ab;
+    wsb = al(Nn * d * 4) + al(Nn * d * ab) + 4 * al(hd) + al(Nn * d * ab) + al(Nn * f * ab) + al(Nn * P * ab) +
+          al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8);
+    if (f32()) wsb += al(Nn * std::max(3 * d, 2 * f) * 4);
+  } else if (stage == DF_E) {
+    wsb = al(L * dt * 4) + al(L * dt * ab) + al(L * fe * ab) + al(L * 2 * fe * 4);
+  }
+  DF_TRY(ws.reserve(wsb + 4096));
+  if (stage == DF_T) {
+    size_t hd = size_t(c.heads) * Nn * dhp * ab;
+    r = (float*)ws.take(Nn * d * 4);
+    h = ws.take(Nn * d * ab);
+    q = ws.take(hd); k = ws.take(hd); v = ws.take(hd); qc = ws.take(hd);
+    o = ws.take(Nn * d * ab);
+    a = ws.take(Nn * f * ab);
+    X = ws.take(Nn * P * ab);
+    mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
+    headmod = (float*)ws.take(2 * d * 4);
+    rope = (float2*)ws.take(size_t(Fp + Hp + Wp) * dh / 2 * 8 + 64);
+    if (f32()) tmp = (float*)ws.take(Nn * std::max(3 * d, 2 * f) * 4);
+    // zero the head-major buffers once: the dh..dhp padding must stay 0 (TMA reads it)
+    DF_TRY(cudaMemset(q, 0, 4 * al(hd)));
+    // RoPE table in fp64 -> fp32 (R7): (cos, sin)(pos_a * theta^(-2j/D_a))
+    std::vector<float2> tab;
+    const int ax[3] = {int(c.rope_axes[0]), int(c.rope_axes[1]), int(c.rope_axes[2])};
+    const int npos[3] = {Fp, Hp, Wp};
+    for (int a3 = 0; a3 < 3; ++a3)
+      for (int p = 0; p < npos[a3]; ++p)
+        for (int j = 0; j < ax[a3] / 2; ++j) {
+          double phi = double(p) * std::pow(double(c.rope_theta), -2.0 * j / ax[a3]);
+          tab.push_back(make_float2(float(std::cos(phi)), float(std::sin(phi))));
+        }
+    DF_TRY(cudaMemcpy(rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  } else if (stage == DF_E) {
+    ez = (float*)ws.take(L * dt * 4);
+    ea = ws.take(L * dt * ab);
+    ef = ws.take(L * fe * ab);
+    etmp = (float*)ws.take(L * 2 * fe * 4);
+  }
+  DF_TRY(init_weights(0));
+  DF_TRY(cudaDeviceSynchronize());
+  return cudaSuccess;
+}
+
+void Model::destroy() {
+  cudaSetDevice(device);
+  wmem.release();
+  ws.release();
+}
+
+cudaError_t Model::init_weights(cudaStream_t st) {
+  locs.clear();
+  const int d = c.d, f = c.ffn, dt = c.d_txt, fe = c.enc_ffn;
+  auto go = [&](bf16* dst, uint32_t tid, int kind, double sd, int in, int out, int layout, int ld,
+                int row_off) -> cudaError_t {
+    InitSpec s;
+    s.seed = seed;
+    s.tid = tid;
+    s.kind = kind;
+    s.a = float(std::sqrt(3.0) * sd);
+    s.in = in;
+    s.out = out;
+    s.layout = layout;
+    s.ld = ld;
+    s.row_off = row_off;
+    locs.push_back({tid, dst, in, out, layout, ld, row_off});
+    g_launch_count.fetch_add(1, std::memory_order_relaxed);
+    return init_tensor(dst, s, st);
+  };
+  auto lin = [&](bf16* dst, uint32_t tid, int in, int out) {  // W^T, K-major
+    return go(dst, tid, 0, 1.0 / std::sqrt(double(in)), in, out, 1, in, 0);
+  };
+  auto vec = [&](bf16* dst, uint32_t tid, double sd, int n) { return go(dst, tid, 0, sd, 1, n, 0, n, 0); };
+  auto gain = [&](bf16* dst, uint32_t tid, int n) { return go(dst, tid, 1, 0.1, 1, n, 0, n, 0); };
+  if (stage == DF_T) {
+    DF_TRY(lin(patch_wT, T_PATCH_W, P, d));
+    DF_TRY(vec(patch_b, T_PATCH_B, 0.02, d));
+    DF_TRY(lin(txt1_wT, T_TXT1_W, dt, d));
+    DF_TRY(vec(txt1_b, T_TXT1_B, 0.02, d));
+    DF_TRY(lin(txt2_wT, T_TXT2_W, d, d));
+    DF_TRY(vec(txt2_b, T_TXT2_B, 0.02, d));
+    DF_TRY(lin(temb1_wT, T_TEMB1_W, c.freq_dim, d));
+    DF_TRY(vec(temb1_b, T_TEMB1_B, 0.02, d));
+    DF_TRY(lin(temb2_wT, T_TEMB2_W, d, d));
+    DF_TRY(vec(temb2_b, T_TEMB2_B, 0.02, d));
+    DF_TRY(go(tmod_wT, T_TMOD_W, 0, 0.1 / std::sqrt(double(d)), d, 6 * d, 1, d, 0));
+    DF_TRY(vec(tmod_b, T_TMOD_B, 0.02, 6 * d));
+    DF_TRY(go(head_mod, T_HEAD_MOD, 0, 0.1, 2, d, 0, d, 0));
+    DF_TRY(lin(head_wT, T_HEAD_W, d, P));
+    DF_TRY(vec(head_b, T_HEAD_B, 0.02, P));
+    for (int l = 0; l < c.layers; ++l) {
+      const uint32_t b = T_LAYER_BASE + T_LAYER_STRIDE * l;
+      LayerW& w = Lw[l];
+      DF_TRY(go(w.mod, b + L_MOD, 0, 0.1, 6, d, 0, d, 0));
+      DF_TRY(lin(w.qkv_wT, b + L_QKV_W, d, 3 * d));
+      DF_TRY(vec(w.qkv_b, b + L_QKV_B, 0.02, 3 * d));
+      DF_TRY(gain(w.g_q, b + L_G_Q, d));
+      DF_TRY(gain(w.g_k, b + L_G_K, d));
+      DF_TRY(lin(w.o_wT, b + L_O_W, d, d));
+      DF_TRY(vec(w.o_b, b + L_O_B, 0.02, d));
+      DF_TRY(gain(w.g_n3, b + L_G_N3, d));
+      DF_TRY(lin(w.cq_wT, b + L_CQ_W, d, d));
+      DF_TRY(vec(w.cq_b, b + L_CQ_B, 0.02, d));
+      DF_TRY(go(w.ckv_wT, b + L_CK_W, 0, 1.0 / std::sqrt(double(d)), d, d, 1, d, 0));
+      DF_TRY(vec(w.ckv_b, b + L_CK_B, 0.02, d));
+      DF_TRY(go(w.ckv_wT, b + L_CV_W, 0, 1.0 / std::sqrt(double(d)), d, d, 1, d, d));
+      DF_TRY(vec(w.ckv_b + d, b + L_CV_B, 0.02, d));
+      DF_TRY(gain(w.g_cq, b + L_G_CQ, d));
+      DF_TRY(gain(w.g_ck, b + L_G_CK, d));
+      DF_TRY(lin(w.co_wT, b + L_CO_W, d, d));
+      DF_TRY(vec(w.co_b, b + L_CO_B, 0.02, d));
+      DF_TRY(go(w.w13T, b + L_W1, 0, 1.0 / std::sqrt(double(d)), d, f, 2, d, 0));
+      DF_TRY(go(w.b13, b + L_B1, 0, 0.02, 1, f, 2, 1, 0));
+      DF_TRY(go(w.w13T, b + L_W3, 0, 1.0 / std::sqrt(double(d)), d, f, 2, d, 1));
+      DF_TRY(go(w.b13, b + L_B3, 0, 0.02, 1, f, 2, 1, 1));
+      DF_TRY(lin(w.w2T, b + L_W2, f, d));
+      DF_TRY(vec(w.b2, b + L_B2, 0.02, d));
+    }
+  } else if (stage == DF_E) {
+    DF_TRY(go(emb, T_ENC_BASE + E_EMB, 0, 1.0, c.vocab, dt, 0, dt, 0));
+    DF_TRY(gain(g_a, T_ENC_BASE + E_G_A, dt));
+    DF_TRY(go(e_w13T, T_ENC_BASE + E_W1, 0, 1.0 / std::sqrt(double(dt)), dt, fe, 2, dt, 0));
+    DF_TRY(go(e_w13T, T_ENC_BASE + E_W3, 0, 1.0 / std::sqrt(double(dt)), dt, fe, 2, dt, 1));
+    DF_TRY(lin(e_w2T, T_ENC_BASE + E_W2, fe, dt));
+    DF_TRY(gain(g_f, T_ENC_BASE + E_G_F, dt));
+  } else {
+    const int cd = c.dec_width;
+    DF_TRY(go(d1_w, T_DEC_BASE + D_W1, 0, 1.0 / std::sqrt(double(c.C)), c.C, cd, 0, cd, 0));
+    DF_TRY(vec(d1_b, T_DEC_BASE + D_B1, 0.02, cd));
+    DF_TRY(go(d2f_w, T_DEC_BASE + D_W2F, 0, 1.0 / std::sqrt(double(cd)), cd, 192, 0, 192, 0));
+    DF_TRY(vec(d2f_b, T_DEC_BASE + D_B2F, 0.02, 192));
+    DF_TRY(go(d2r_w, T_DEC_BASE + D_W2R, 0, 1.0 / std::sqrt(double(cd)), cd, 768, 0, 768, 0));
+    DF_TRY(vec(d2r_b, T_DEC_BASE + D_B2R, 0.02, 768));
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ helpers
+cudaError_t Model::gemm(const void* A, int lda, const bf16* Wt, int ldw, int M, int Nn, int K, const Epi& e,
+                        int out_f32, cudaStream_t st) {
+  if (!f32()) {
+    DF_L(gemm_tc(static_cast<const bf16*>(A), lda, Wt, ldw, M, Nn, K, e, out_f32, st));
+  } else {
+    DF_L(gemm_simt(A, 0, lda, 0, Wt, ldw, tmp, Nn, M, Nn, K, nullptr, ACT_NONE, st));
+    DF_L(epi_rows(tmp, e, 1, st));
+  }
+  return cudaSuccess;
+}
+
+cudaError_t Model::attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st) {
+  const float scale = 1.0f / std::sqrt(float(dh));
+  if (!f32()) {
+    DF_L(attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, c.heads, Nq, Nk, dh, dhp, scale, st));
+  } else {
+    DF_L(attn_simt((const float*)Q, (const float*)K, (const float*)V, (float*)O, c.heads, Nq, Nk, dh, scale, st));
+  }
+  return cudaSuccess;
+}
+
+static Epi epi_base(int kind, int M, int N) {
+  Epi e;
+  std::memset(&e, 0, sizeof(e));
+  e.kind = kind;
+  e.M = M;
+  e.N = N;
+  return e;
+}
+
+Epi Model::heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0, int rope0, void* o1,
+                     const bf16* g1, int rope1, void* o2, const bf16* g2, int rope2) const {
+  Epi e = epi_base(EPI_HEADS, M, nsec * c.d);
+  e.bias = bias;
+  e.d = c.d;
+  e.heads = c.heads;
+  e.dh = dh;
+  e.dh_pad = dhp;
+  e.nsec = nsec;
+  e.sec_out[0] = o0; e.sec_gain[0] = g0; e.sec_rope[0] = rope0;
+  e.sec_out[1] = o1; e.sec_gain[1] = g1; e.sec_rope[1] = rope1;
+  e.sec_out[2] = o2; e.sec_gain[2] = g2; e.sec_rope[2] = rope2;
+  e.rope_tab = rope;
+  e.Fp = Fp; e.Hp = Hp; e.Wp = Wp;
+  e.Df2 = c.rope_axes[0] / 2; e.Dh2 = c.rope_axes[1] / 2; e.Dw2 = c.rope_axes[2] / 2;
+  e.eps = c.eps;
+  return e;
+}
+
+// ------------------------------------------------------------------ prologue (a1)
+cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out) {
+  const int d = c.d, Lt = c.L_txt, dt = c.d_txt, fd = c.freq_dim;
+  const size_t ab = act_bytes();
+  Cond& cd = *out;
+  cd.S = S;
+  cd.device = device;
+  cd.sig.assign(sig_host, sig_host + S + 1);
+  size_t kvb = size_t(c.layers) * c.heads * Lt * dhp * ab;
+  size_t need = al((S + 1) * 4) + 2 * al(kvb) + al(size_t(S) * d * 4) + al(size_t(S) * 6 * d * 4) +
+                al(size_t(S) * fd * 4) + al(size_t(S) * d * 4) + 2 * al(size_t(Lt) * d * ab) +
+                al(size_t(Lt) * dt * 4) + (f32() ? al(size_t(Lt) * 2 * d * 4) : 0) + 4096;
+  DF_TRY(cd.mem.reserve(need));
+  cd.sig_dev = (float*)cd.mem.take((S + 1) * 4);
+  cd.kc = cd.mem.take(kvb);
+  cd.vc = cd.mem.take(kvb);
+  cd.e = (float*)cd.mem.take(size_t(S) * d * 4);
+  cd.e6 = (float*)cd.mem.take(size_t(S) * 6 * d * 4);
+  float* s = (float*)cd.mem.take(size_t(S) * fd * 4);
+  float* t1 = (float*)cd.mem.take(size_t(S) * d * 4);
+  void* c1 = cd.mem.take(size_t(Lt) * d * ab);
+  void* cp = cd.mem.take(size_t(Lt) * d * ab);
+  float* ctx32 = (float*)cd.mem.take(size_t(Lt) * dt * 4);
+  float* ptmp = f32() ? (float*)cd.mem.take(size_t(Lt) * 2 * d * 4) : nullptr;
+  if (!cd.e6) return cudaErrorMemoryAllocation;
+  if (!f32()) DF_TRY(cudaMemsetAsync(cd.kc, 0, 2 * al(kvb), st));  // dh padding = 0
+  DF_TRY(cudaMemcpyAsync(cd.sig_dev, sig_host, (S + 1) * 4, cudaMemcpyHostToDevice, st));
+  // time conditioning for all S steps (R4, R5), fp32 SIMT: the M = S rows are GEMV-like
+  DF_L(sinusoid(cd.sig_dev, s, S, fd, st));
+  DF_L(gemm_simt(s, 0, fd, ACT_NONE, temb1_wT, fd, t1, d, S, d, fd, temb1_b, ACT_SILU, st));
+  DF_L(gemm_simt(t1, 0, d, ACT_NONE, temb2_wT, d, cd.e, d, S, d, d, temb2_b, ACT_NONE, st));
+  DF_L(gemm_simt(cd.e, 0, d, ACT_SILU, tmod_wT, d, cd.e6, 6 * d, S, 6 * d, d, tmod_b, ACT_NONE, st));
+  // text projection ctx' = GELU(ctx W1 + b1) W2 + b2
+  Epi e1 = epi_base(EPI_STORE, Lt, d);
+  e1.bias = txt1_b;
+  e1.act = ACT_GELU;
+  e1.out = c1;
+  e1.ldo = d;
+  Epi e2 = epi_base(EPI_STORE, Lt, d);
+  e2.bias = txt2_b;
+  e2.out = cp;
+  e2.ldo = d;
+  if (!f32()) {
+    DF_L(gemm_tc((const bf16*)ctx_bf16, dt, txt1_wT, dt, Lt, d, dt, e1, 0, st));
+    DF_L(gemm_tc((const bf16*)c1, d, txt2_wT, d, Lt, d, d, e2, 0, st));
+  } else {
+    DF_L(gemm_simt(ctx_bf16, 1, dt, 0, txt1_wT, dt, ptmp, d, Lt, d, dt, nullptr, ACT_NONE, st));
+    DF_L(epi_rows(ptmp, e1, 1, st));
+    DF_L(gemm_simt(c1, 0, d, 0, txt2_wT, d, ptmp, d, Lt, d, d, nullptr, ACT_NONE, st));
+    DF_L(epi_rows(ptmp, e2, 1, st));
+  }
+  (void)ctx32;
+  // cross K/V for every layer: [K | V] = ctx' [Wck | Wcv]^T; K <- headRMS * g_ck
+  const size_t per = size_t(c.heads) * Lt * dhp * ab;
+  for (int l = 0; l < c.layers; ++l) {
+    void* kl = (char*)cd.kc + l * per;
+    void* vl = (char*)cd.vc + l * per;
+    Epi e = heads_epi(Lt, 2, Lw[l].ckv_b, kl, Lw[l].g_ck, 0, vl, nullptr, 0, nullptr, nullptr, 0);
+    if (!f32()) {
+      DF_L(gemm_tc((const bf16*)cp, d, Lw[l].ckv_wT, d, Lt, 2 * d, d, e, 0, st));
+    } else {
+      DF_L(gemm_simt(cp, 0, d, 0, Lw[l].ckv_wT, d, ptmp, 2 * d, Lt, 2 * d, d, nullptr, ACT_NONE, st));
+      DF_L(epi_rows(ptmp, e, 1, st));
+    }
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ one block (a3-a10)
+cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t st) {
+  const int d = c.d, f = c.ffn, Lt = c.L_txt;
+  const int of = f32() ? 1 : 0;
+  const LayerW& w = Lw[l];
+  const float* md = mods + size_t(l) * 6 * d;  // sh1, sc1, g1, sh2, sc2, g2
+  const size_t per = size_t(c.heads) * Lt * dhp * act_bytes();
+  // a4: h = RMSNorm(r)(1 + sc1) + sh1
+  DF_L(rmsnorm_mod(res, h, of, N, d, md + 0 * d, md + 1 * d, nullptr, c.eps, st));
+  // a5: q,k,v = heads(h Wqkv + b); qk-RMSNorm * g; RoPE3 on q, k
+  {
+    Epi e = heads_epi(N, 3, w.qkv_b, q, w.g_q, 1, k, w.g_k, 1, v, nullptr, 0);
+    DF_TRY(gemm(h, d, w.qkv_wT, d, N, 3 * d, d, e, of, st));
+  }
+  // a6: self-attention
+  DF_TRY(attn(q, k, v, o, N, N, st));
+  // a7: r += g1 * (o Wo + bo)
+  {
+    Epi e = epi_base(EPI_GRES, N, d);
+    e.bias = w.o_b;
+    e.resid = res;
+    e.ldr = d;
+    e.gate = md + 2 * d;
+    DF_TRY(gemm(o, d, w.o_wT, d, N, d, d, e, of, st));
+  }
+  // a8: cross-attention: hc = RMSNorm(r) g_n3; qc = headRMS(hc Wcq + b) g_cq; r += attn Wco + b
+  DF_L(rmsnorm_mod(res, h, of, N, d, nullptr, nullptr, w.g_n3, c.eps, st));
+  {
+    Epi e = heads_epi(N, 1, w.cq_b, qc, w.g_cq, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
+    DF_TRY(gemm(h, d, w.cq_wT, d, N, d, d, e, of, st));
+  }
+  DF_TRY(attn(qc, (const char*)cd.kc + l * per, (const char*)cd.vc + l * per, o, N, Lt, st));
+  {
+    Epi e = epi_base(EPI_GRES, N, d);
+    e.bias = w.co_b;
+    e.resid = res;
+    e.ldr = d;
+    DF_TRY(gemm(o, d, w.co_wT, d, N, d, d, e, of, st));
+  }
+  // a9: h2 = RMSNorm(r)(1 + sc2) + sh2
+  DF_L(rmsnorm_mod(res, h, of, N, d, md + 3 * d, md + 4 * d, nullptr, c.eps, st));
+  // a10: a = SiLU(h2 W1 + b1) * (h2 W3 + b3);  r += g2 * (a W2 + b2)
+  {
+    Epi e = epi_base(EPI_SWIGLU, N, 2 * f);
+    e.bias = w.b13;
+    e.out = a;
+    e.ldo = f;
+    DF_TRY(gemm(h, d, w.w13T, d, N, 2 * f, d, e, of, st));
+  }
+  {
+    Epi e = epi_base(EPI_GRES, N, d);
+    e.bias = w.b2;
+    e.resid = res;
+    e.ldr = d;
+    e.gate = md + 5 * d;
+    DF_TRY(gemm(a, f, w.w2T, f, N, d, f, e, of, st));
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ one step (a2-a12)
+cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStream_t st) {
+  const int d = c.d;
+  const int of = f32() ? 1 : 0;
+  DF_L(modulations(cd.e6 + size_t(i) * 6 * d, cd.e + size_t(i) * d, layer_mods.data(), c.layers, head_mod, d, mods,
+                   headmod, st));
+  // a2: r = patchify(x) Wpe + bpe   (fp32 residual)
+  DF_L(patchify(x, X, of, c.C, c.F, c.H, c.W, c.pt, c.ph, c.pw, st));
+  {
+    Epi e = epi_base(EPI_STORE, N, d);
+    e.bias = patch_b;
+    e.out = r;
+    e.ldo = d;
+    DF_TRY(gemm(X, P, patch_wT, P, N, d, P, e, 1, st));
+  }
+  for (int l = 0; l < c.layers; ++l) DF_TRY(block(cd, i, l, r, st));
+  // a11 + a12: head modulation, projection, unpatchify, Euler update fused in the epilogue
+  DF_L(rmsnorm_mod(r, h, of, N, d, headmod, headmod + d, nullptr, c.eps, st));
+  {
+    Epi e = epi_base(EPI_EULER, N, P);
+    e.bias = head_b;
+    e.x_lat = x;
+    e.v_out = v_out;
+    e.dsig = float(double(cd.sig[i + 1]) - double(cd.sig[i]));
+    e.C = c.C; e.pt = c.pt; e.ph = c.ph; e.pw = c.pw; e.Hl = c.H; e.Wl = c.W; e.Fl = c.F;
+    e.Hp = Hp; e.Wp = Wp;
+    DF_TRY(gemm(h, d, head_wT, d, N, P, d, e, 1, st));
+  }
+  return cudaSuccess;
+}
+
+cudaError_t Model::layer(const Cond& cd, int i, int l, float* r_io, cudaStream_t st) {
+  DF_L(modulations(cd.e6 + size_t(i) * 6 * c.d, cd.e + size_t(i) * c.d, layer_mods.data(), c.layers, head_mod, c.d,
+                   mods, headmod, st));
+  return block(cd, i, l, r_io, st);
+}
+
+// ------------------------------------------------------------------ E stand-in
+cudaError_t Model::encode(const int32_t* ids, void* ctx_out, cudaStream_t st) {
+  const int Lt = c.L_txt, dt = c.d_txt, fe = c.enc_ffn;
+  const int of = f32() ? 1 : 0;
+  DF_L(embed_rows(ids, emb, ez, Lt, dt, st));
+  DF_L(rmsnorm_mod(ez, ea, of, Lt, dt, nullptr, nullptr, g_a, c.eps, st));
+  Epi e1 = epi_base(EPI_SWIGLU, Lt, 2 * fe);
+  e1.out = ef;
+  e1.ldo = fe;
+  Epi e2 = epi_base(EPI_GRES, Lt, dt);
+  e2.resid = ez;
+  e2.ldr = dt;
+  if (!f32()) {
+    DF_L(gemm_tc((const bf16*)ea, dt, e_w13T, dt, Lt, 2 * fe, dt, e1, 0, st));
+    DF_L(gemm_tc((const bf16*)ef, fe, e_w2T, fe, Lt, dt, fe, e2, 0, st));
+  } else {
+    DF_L(gemm_simt(ea, 0, dt, 0, e_w13T, dt, etmp, 2 * fe, Lt, 2 * fe, dt, nullptr, ACT_NONE, st));
+    DF_L(epi_rows(etmp, e1, 1, st));
+    DF_L(gemm_simt(ef, 0, fe, 0, e_w2T, fe, etmp, dt, Lt, dt, fe, nullptr, ACT_NONE, st));
+    DF_L(epi_rows(etmp, e2, 1, st));
+  }
+  // ctx = bf16_RNE(RMSNorm(z) g_f): the payload is bf16 by definition (R21)
+  DF_L(rmsnorm_mod(ez, ctx_out, 0, Lt, dt, nullptr, nullptr, g_f, c.eps, st));
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ D stand-in
+cudaError_t Model::decode(const float* x, float* out, cudaStream_t st) {
+  DF_L(decode_latent(x, out, c.C, c.F, c.H, c.W, c.dec_width, d1_w, d1_b, d2f_w, d2f_b, d2r_w, d2r_b, st));
+  return cudaSuccess;
+}
+
+}  // namespace df

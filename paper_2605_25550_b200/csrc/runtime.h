@@ -1,0 +1,133 @@
+// Internal runtime of libdf: per-instance weights, workspaces and the stage
+// programs (E stand-in, DiT prologue/step/layer, D stand-in).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../include/df.h"
+#include "kernels.h"
+
+namespace df {
+
+extern thread_local std::string tls_err;
+// Counts launches issued by this library (bench "gpu_launches").
+extern std::atomic<uint64_t>* g_launches;
+
+#define DF_TRY(expr)                                                             \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      df::tls_err = std::string(#expr) + ": " + cudaGetErrorString(_e);          \
+      return _e;                                                                 \
+    }                                                                            \
+  } while (0)
+
+// Tensor ids (DESIGN.md parameter table; restated from the doc, not shared with the oracle).
+enum : uint32_t {
+  T_PATCH_W = 0, T_PATCH_B, T_TXT1_W, T_TXT1_B, T_TXT2_W, T_TXT2_B, T_TEMB1_W, T_TEMB1_B, T_TEMB2_W, T_TEMB2_B,
+  T_TMOD_W, T_TMOD_B, T_HEAD_MOD, T_HEAD_W, T_HEAD_B,
+  T_LAYER_BASE = 64, T_LAYER_STRIDE = 32,
+  L_MOD = 0, L_QKV_W, L_QKV_B, L_G_Q, L_G_K, L_O_W, L_O_B, L_G_N3, L_CQ_W, L_CQ_B, L_CK_W, L_CK_B, L_CV_W, L_CV_B,
+  L_G_CQ, L_G_CK, L_CO_W, L_CO_B, L_W1, L_B1, L_W3, L_B3, L_W2, L_B2,
+  T_ENC_BASE = 1u << 20, E_EMB = 0, E_G_A, E_W1, E_W3, E_W2, E_G_F,
+  T_DEC_BASE = 1u << 21, D_W1 = 0, D_B1, D_W2F, D_B2F, D_W2R, D_B2R,
+};
+
+struct LayerW {
+  bf16 *mod, *qkv_wT, *qkv_b, *g_q, *g_k, *o_wT, *o_b, *g_n3, *cq_wT, *cq_b, *ckv_wT, *ckv_b, *g_cq, *g_ck, *co_wT,
+      *co_b, *w13T, *b13, *w2T, *b2;
+};
+
+// Where a logical tensor lives on the device (for df_weight_bits).
+struct TensorLoc {
+  uint32_t tid;
+  bf16* base;
+  int in, out, layout, ld, row_off;
+};
+
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  cudaError_t reserve(size_t bytes);
+  void* take(size_t bytes);
+  void release();
+};
+
+struct DitModel;  // weights of all stages for one device
+
+// Per-request conditioning handle (df_cond).
+struct Cond {
+  int S = 0;
+  std::vector<float> sig;   // host sigma schedule, S+1
+  float* sig_dev = nullptr;
+  void* kc = nullptr;       // [layers][H][L][dhp]
+  void* vc = nullptr;
+  float* e = nullptr;       // [S, d]
+  float* e6 = nullptr;      // [S, 6d]
+  Arena mem;
+  int device = 0;
+};
+
+struct Model {
+  df_dit_cfg c{};
+  int precision = DF_BF16;
+  int device = 0;
+  int stage = DF_T;
+  uint64_t seed = 0;
+  int max_steps = 0;
+  // derived
+  int N = 0, P = 0, dh = 0, dhp = 0, Fp = 0, Hp = 0, Wp = 0;
+  Arena wmem, ws;
+  std::vector<TensorLoc> locs;
+  // global DiT weights
+  bf16 *patch_wT = nullptr, *patch_b = nullptr, *txt1_wT = nullptr, *txt1_b = nullptr, *txt2_wT = nullptr,
+       *txt2_b = nullptr, *temb1_wT = nullptr, *temb1_b = nullptr, *temb2_wT = nullptr, *temb2_b = nullptr,
+       *tmod_wT = nullptr, *tmod_b = nullptr, *head_mod = nullptr, *head_wT = nullptr, *head_b = nullptr;
+  std::vector<LayerW> Lw;
+  // encoder / decoder
+  bf16 *emb = nullptr, *g_a = nullptr, *e_w13T = nullptr, *e_w2T = nullptr, *g_f = nullptr;
+  bf16 *d1_w = nullptr, *d1_b = nullptr, *d2f_w = nullptr, *d2f_b = nullptr, *d2r_w = nullptr, *d2r_b = nullptr;
+  // workspace (T)
+  float* r = nullptr;       // residual [N, d]
+  void* h = nullptr;        // [N, d] bf16 | f32
+  void* q = nullptr;        // [H][N][dhp]
+  void* k = nullptr;
+  void* v = nullptr;
+  void* qc = nullptr;
+  void* o = nullptr;        // [N, d]
+  void* a = nullptr;        // [N, f]
+  void* X = nullptr;        // [N, P]
+  float* tmp = nullptr;     // fp32 build: raw GEMM out [N, max(3d, 2f)]
+  float* mods = nullptr;    // [layers][6][d]
+  float* headmod = nullptr; // [2][d]
+  float2* rope = nullptr;
+  // encoder workspace
+  float* ez = nullptr;      // [L, d_txt]
+  void* ea = nullptr;       // [L, d_txt]
+  void* ef = nullptr;       // [L, f_e]
+  float* etmp = nullptr;    // [L, 2 f_e]
+  std::vector<const bf16*> layer_mods;
+
+  cudaError_t create(const df_dit_cfg& cfg, int precision, int device, int stage, uint64_t seed, int max_steps);
+  void destroy();
+  bool f32() const { return precision == DF_FP32_VALIDATION; }
+  size_t act_bytes() const { return f32() ? 4 : 2; }
+
+  cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out);
+  cudaError_t step(const Cond& c, int i, float* x, float* v_out, cudaStream_t st);
+  cudaError_t layer(const Cond& c, int i, int l, float* r_io, cudaStream_t st);
+  cudaError_t encode(const int32_t* ids, void* ctx_bf16, cudaStream_t st);
+  cudaError_t decode(const float* x, float* out, cudaStream_t st);
+
+  // helpers
+  cudaError_t gemm(const void* A, int lda, const bf16* W, int ldw, int M, int Nn, int K, const Epi& e, int out_f32,
+                   cudaStream_t st);
+  cudaError_t attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st);
+  Epi heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0, int rope0, void* o1, const bf16* g1,
+                int rope1, void* o2, const bf16* g2, int rope2) const;
+  cudaError_t block(const Cond& c, int i, int l, float* r, cudaStream_t st);
+  cudaError_t init_weights(cudaStream_t st);
+};
+
+}  // namespace df

@@ -1,0 +1,142 @@
+"""DiT step / trajectory / per-layer parity against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star): one bf16 step rel-L2 <= 1e-2, a full
+trajectory <= 3e-2; fp32 validation build <= 1e-4."""
+import numpy as np
+import pytest
+
+from oracle import params as OP, dit, stages
+from synth import inputs
+from synth.configs import TINY, MID, IMAGE, VIDEO, with_layers
+from gpu_util import rel_l2, bf16_tensor_from_bits, make_ctx
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+BF16, FP32 = 0, 1
+TOL_STEP = {BF16: 1e-2, FP32: 1e-4}
+TOL_TRAJ = {BF16: 3e-2, FP32: 1e-4}
+
+
+def _gpu_step(c, cfg, x, ctx_bits, i, S, shift):
+    sig = dit.sigmas(S, shift).astype(np.float32)
+    ctx_t = bf16_tensor_from_bits(ctx_bits)
+    cond = c.dit_prepare(1, ctx_t, sig)
+    xt = torch.from_numpy(x).cuda()
+    vt = torch.zeros_like(xt)
+    c.dit_step(1, cond, i, xt, vt)
+    torch.cuda.synchronize()
+    c.cond_release(cond)
+    return xt.cpu().numpy(), vt.cpu().numpy()
+
+
+def _oracle_step(cfg, x, ctx_bits, i, S, shift, seed=0):
+    P = OP.Params(cfg, seed)
+    sig = dit.sigmas(S, shift).astype(np.float32).astype(np.float64)
+    cond = dit.prologue(P, cfg, inputs.bf16_bits_to_f64(ctx_bits), sig)
+    x1, v = dit.step(P, cfg, x.astype(np.float64), i, cond, sig)
+    return x1, v
+
+
+@pytest.mark.parametrize("prec", [BF16, FP32])
+@pytest.mark.parametrize("cfg,i", [(TINY, 0), (TINY, 2), (MID, 3)])
+def test_single_step_parity(cfg, i, prec):
+    x = inputs.latent(cfg, 11)
+    ctx_bits = inputs.ctx_bf16(cfg, 12)
+    with make_ctx(cfg, precision=prec) as c:
+        gx, gv = _gpu_step(c, cfg, x, ctx_bits, i, cfg.steps, cfg.shift)
+    ox, ov = _oracle_step(cfg, x, ctx_bits, i, cfg.steps, cfg.shift)
+    assert rel_l2(gv, ov) <= TOL_STEP[prec], rel_l2(gv, ov)
+    assert rel_l2(gx, ox) <= TOL_STEP[prec]
+
+
+@pytest.mark.parametrize("prec", [BF16, FP32])
+@pytest.mark.parametrize("cfg", [TINY, MID])
+def test_trajectory_parity(cfg, prec):
+    x0 = inputs.latent(cfg, 21)
+    ctx_bits = inputs.ctx_bf16(cfg, 22)
+    S, shift = cfg.steps, cfg.shift
+    sig = dit.sigmas(S, shift).astype(np.float32)
+    with make_ctx(cfg, precision=prec) as c:
+        cond = c.dit_prepare(1, bf16_tensor_from_bits(ctx_bits), sig)
+        xt = torch.from_numpy(x0).cuda()
+        for i in range(S):
+            c.dit_step(1, cond, i, xt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        gx = xt.cpu().numpy()
+    P = OP.Params(cfg, 0)
+    ox = dit.trajectory(P, cfg, x0.astype(np.float64), inputs.bf16_bits_to_f64(ctx_bits), steps=S, shift=shift)
+    # oracle uses the fp32-rounded schedule the GPU is given
+    err = rel_l2(gx, ox)
+    assert err <= TOL_TRAJ[prec], err
+
+
+def test_step_deterministic_bitwise():
+    """Same inputs twice -> identical bytes (fixed tile order, no atomics; R18)."""
+    cfg = MID
+    x = inputs.latent(cfg, 5)
+    ctx_bits = inputs.ctx_bf16(cfg, 6)
+    with make_ctx(cfg) as c:
+        a = _gpu_step(c, cfg, x, ctx_bits, 1, cfg.steps, cfg.shift)
+        b = _gpu_step(c, cfg, x, ctx_bits, 1, cfg.steps, cfg.shift)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def _layer_parity(cfg, rows, i=3, seed=0):
+    x_r = inputs.residual(cfg, 31)
+    ctx_bits = inputs.ctx_bf16(cfg, 32)
+    S, shift = cfg.steps, cfg.shift
+    sig = dit.sigmas(S, shift).astype(np.float32)
+    with make_ctx(cfg) as c:
+        cond = c.dit_prepare(1, bf16_tensor_from_bits(ctx_bits), sig)
+        rt = torch.from_numpy(x_r).cuda()
+        c.dit_layer(1, cond, i, 0, rt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        got = rt.cpu().numpy()[rows]
+    P = OP.Params(cfg, seed)
+    ctx = inputs.bf16_bits_to_f64(ctx_bits)
+    ctxp = dit.text_projection(P, cfg, ctx)
+    kv = dit.cross_kv(P, cfg, 0, ctxp)
+    _, e6 = dit.time_embedding(P, cfg, float(sig[i]))
+    want = dit.block_rows(P, cfg, 0, x_r.astype(np.float64), e6, kv, dit.token_positions(cfg), rows)
+    # compare the block's update (r' - r), the strict quantity
+    d_got = got - x_r[rows]
+    d_want = want - x_r[rows]
+    return rel_l2(d_got, d_want)
+
+
+def test_layer_parity_image_shape():
+    cfg = with_layers(IMAGE, 1)
+    rows = np.sort(np.random.default_rng(0).choice(cfg.N, 64, replace=False))
+    assert _layer_parity(cfg, rows) <= 1e-2
+
+
+@pytest.mark.slow
+def test_layer_parity_video_shape():
+    cfg = with_layers(VIDEO, 1)
+    rows = np.concatenate([np.sort(np.random.default_rng(1).choice(cfg.N - 120, 48, replace=False)),
+                           np.arange(cfg.N - 16, cfg.N)])  # includes the 120-row tail tile
+    assert _layer_parity(cfg, rows) <= 1e-2
+
+
+@pytest.mark.parametrize("prec", [BF16, FP32])
+def test_encoder_decoder_parity(prec):
+    cfg = MID
+    P = OP.Params(cfg, 0)
+    ids = stages.tokens_from_seed(cfg, 3)
+    with make_ctx(cfg, precision=prec) as c:
+        idt = torch.from_numpy(ids).cuda()
+        ctx_t = torch.empty((cfg.L_txt, cfg.d_txt), device="cuda", dtype=torch.bfloat16)
+        c.encode(0, idt, ctx_t)
+        lat = inputs.latent(cfg, 4)
+        out = torch.empty(cfg.out_shape, device="cuda")
+        c.decode(2, torch.from_numpy(lat).cuda(), out)
+        torch.cuda.synchronize()
+        got_ctx = ctx_t.float().cpu().numpy()
+        got_out = out.cpu().numpy()
+    want_ctx, _ = stages.encoder(P, cfg, ids)
+    assert rel_l2(got_ctx, want_ctx) <= (1e-2 if prec == BF16 else 4e-3)
+    want_out = stages.decoder(P, cfg, lat.astype(np.float64))
+    assert rel_l2(got_out, want_out) <= 1e-5

@@ -1,0 +1,133 @@
+"""Kernel-level parity (through the C ABI) against the oracle and closed forms."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import params as OP, stages, capacity as cap, dit
+from synth import inputs
+from synth.configs import TINY, MID, with_layers
+from gpu_util import rel_l2, bf16_tensor_from_bits, bf16_bits_of, make_ctx
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tiny_ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    c = make_ctx(TINY)
+    yield c
+    c.close()
+
+
+def test_weight_bytes_equal_oracle_tiny(tiny_ctx):
+    """Parity check 0 (P12): every parameter's bf16 bits == the oracle's."""
+    P = OP.Params(TINY, 0)
+    tab = OP.tensor_table(TINY)
+    inst_of = {"E": 0, "D": 2}
+    for tid, name, kind, shape in tab:
+        inst = inst_of.get(name[0], 1) if name[:2] in ("E.", "D.") else 1
+        got = tiny_ctx.weight_bits(inst, tid, int(np.prod(shape)))
+        want = P.bits(name).reshape(-1)
+        assert np.array_equal(got, want), name
+
+
+def test_weight_bytes_equal_oracle_mid_layer():
+    cfg = with_layers(MID, 1)
+    P = OP.Params(cfg, 7)
+    with make_ctx(cfg, seed=7) as c:
+        for name in ("L0.qkv_w", "L0.w1", "L0.w3", "L0.b3", "L0.g_ck", "L0.cv_w", "tmod_w", "head_w"):
+            tid = P.tid(name)
+            shape = P[name].shape
+            got = c.weight_bits(1, tid, int(np.prod(shape)))
+            assert np.array_equal(got, P.bits(name).reshape(-1)), name
+
+
+@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("M,N,K", [(16, 64, 64), (200, 320, 200), (384, 512, 4096), (130, 16, 64)])
+def test_gemm_integer_bit_exact(tiny_ctx, tc, M, N, K):
+    """P11: integer-valued bf16 operands -> exact fp32 accumulation; tails in M, N, K."""
+    A = inputs.int_matrix((M, K), -8, 8, seed=M + K)
+    W = inputs.int_matrix((N, K), -8, 8, seed=N + 3)
+    At = torch.from_numpy(A).cuda().to(torch.bfloat16)
+    Wt = torch.from_numpy(W).cuda().to(torch.bfloat16)
+    out = torch.full((M, N), float("nan"), device="cuda")
+    tiny_ctx.op_gemm(At, Wt, out, tc=tc)
+    torch.cuda.synchronize()
+    want = A.astype(np.float64) @ W.astype(np.float64).T
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), want)
+
+
+@pytest.mark.parametrize("H,Nq,Nk,dh,dhp", [(2, 300, 260, 128, 128), (3, 128, 128, 64, 64), (4, 16, 16, 16, 64),
+                                            (2, 257, 8, 128, 128), (1, 1000, 512, 128, 128)])
+def test_attention_vs_bruteforce(tiny_ctx, H, Nq, Nk, dh, dhp):
+    """P5: flash attention vs fp64 softmax on the same bf16 inputs (with dh padding)."""
+    r = np.random.default_rng(Nq + Nk)
+    q = np.zeros((H, Nq, dhp), np.float32)
+    k = np.zeros((H, Nk, dhp), np.float32)
+    v = np.zeros((H, Nk, dhp), np.float32)
+    q[..., :dh] = r.standard_normal((H, Nq, dh)) * 1.5
+    k[..., :dh] = r.standard_normal((H, Nk, dh)) * 1.5
+    v[..., :dh] = r.standard_normal((H, Nk, dh))
+    Q, K, V = (torch.from_numpy(t).cuda().to(torch.bfloat16) for t in (q, k, v))
+    O = torch.zeros((Nq, H * dh), device="cuda", dtype=torch.bfloat16)
+    tiny_ctx.op_attention(Q, K, V, O, H, Nq, Nk, dh, dhp, 1.0 / math.sqrt(dh))
+    torch.cuda.synchronize()
+    qd, kd, vd = (t.float().cpu().numpy().astype(np.float64)[..., :dh] for t in (Q, K, V))
+    want = dit.softmax_attention(qd, kd, vd).transpose(1, 0, 2).reshape(Nq, H * dh)
+    got = O.float().cpu().numpy()
+    assert rel_l2(got, want) < 1e-2
+
+
+def test_attention_special_cases(tiny_ctx):
+    """N_kv = 1 -> V; q = 0 -> mean(V)."""
+    H, Nq, dh = 2, 130, 128
+    v1 = torch.randn(H, 1, dh, device="cuda").to(torch.bfloat16)
+    Q = torch.randn(H, Nq, dh, device="cuda").to(torch.bfloat16)
+    O = torch.zeros(Nq, H * dh, device="cuda", dtype=torch.bfloat16)
+    tiny_ctx.op_attention(Q, torch.randn(H, 1, dh, device="cuda").to(torch.bfloat16), v1, O, H, Nq, 1, dh, dh, 0.1)
+    torch.cuda.synchronize()
+    want = v1.float().permute(1, 0, 2).reshape(1, H * dh).expand(Nq, -1)
+    assert torch.equal(O.float(), want)
+    V = torch.randn(H, 300, dh, device="cuda").to(torch.bfloat16)
+    tiny_ctx.op_attention(torch.zeros_like(Q), torch.randn(H, 300, dh, device="cuda").to(torch.bfloat16), V, O, H,
+                          Nq, 300, dh, dh, 0.1)
+    torch.cuda.synchronize()
+    want = V.double().mean(dim=1).reshape(1, H * dh).expand(Nq, -1)
+    assert rel_l2(O.double().cpu().numpy(), want.cpu().numpy()) < 4e-3
+
+
+def test_rmsnorm_mod_closed_form(tiny_ctx):
+    M, d = 333, 3072
+    x = torch.randn(M, d, device="cuda") * 3
+    sh = torch.randn(d, device="cuda") * 0.1
+    sc = torch.randn(d, device="cuda") * 0.1
+    out = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
+    tiny_ctx.op_rmsnorm_mod(x, out, sh, sc, 1e-6)
+    torch.cuda.synchronize()
+    xd = x.double().cpu().numpy()
+    want = dit.rms_norm(xd, 1e-6) * (1 + sc.double().cpu().numpy()) + sh.double().cpu().numpy()
+    assert rel_l2(out.double().cpu().numpy(), want) < 4e-3
+
+
+def test_noise_and_tokens_equal_oracle(tiny_ctx):
+    x = torch.empty(TINY.latent_shape, device="cuda")
+    tiny_ctx.noise(1, 12345, x)
+    ids = torch.empty(TINY.L_txt, device="cuda", dtype=torch.int32)
+    tiny_ctx.tokens(0, 12345, ids)
+    torch.cuda.synchronize()
+    want = stages.noise(TINY, 12345)
+    got = x.cpu().numpy()
+    # fp64 libm vs CUDA log/cos may differ by 1 ulp before the fp32 rounding
+    assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-3)) < 2.5e-7
+    assert np.array_equal(ids.cpu().numpy(), stages.tokens_from_seed(TINY, 12345))
+
+
+@pytest.mark.parametrize("nbytes", [8, 1000, 4194304, 8386560])
+def test_payload_hash_equals_oracle(tiny_ctx, nbytes):
+    buf = inputs.payload_bytes(nbytes, seed=nbytes)
+    t = torch.from_numpy(buf).cuda()
+    assert tiny_ctx.payload_hash(0, t, nbytes) == cap.payload_hash(buf)

@@ -219,3 +219,17 @@ def test_cross_attention_uses_text():
     vc2 = vc.copy(); vc2[0] += 1.0
     c = dit.block(P, cfg, 0, r0, e6, (kc, vc2), pos)
     assert np.abs(c - a).max() > 1e-6
+
+
+def test_block_rows_matches_block():
+    # the row-restricted evaluation is the same definition (pins block_rows to block)
+    cfg = with_layers(MID, 1)
+    P = OP.Params(cfg, 0)
+    rr = np.random.default_rng(9)
+    r0 = rr.normal(size=(cfg.N, cfg.d))
+    e6 = rr.normal(size=(6, cfg.d)) * 0.1
+    kv = (rr.normal(size=(cfg.L_txt, cfg.d)), rr.normal(size=(cfg.L_txt, cfg.d)))
+    pos = dit.token_positions(cfg)
+    full = dit.block(P, cfg, 0, r0, e6, kv, pos)
+    rows = np.array([0, 5, 511, 1023])
+    np.testing.assert_allclose(dit.block_rows(P, cfg, 0, r0, e6, kv, pos, rows), full[rows], rtol=1e-12, atol=1e-12)
