@@ -191,6 +191,15 @@ df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void*
 df_status df_op_rmsnorm_mod(df_ctx* ctx, const float* x, void* out, int32_t M, int32_t d, const float* shift,
                             const float* scale, float eps, void* stream);
 
+/* Per-launch timing of the DiT step's kernel classes (bench.py roofline): when
+ * enabled, every GEMM / attention / RMSNorm launch of the T instances is bracketed
+ * by CUDA events on its own stream (no host sync on the launch path).  Kinds:
+ * 0 QKV, 1 self-attn, 2 O-proj, 3 RMSNorm, 4 cross-Q, 5 cross-attn, 6 cross-O,
+ * 7 MLP up (SwiGLU), 8 MLP down, 9 head+Euler, 10 patch embed. */
+df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset);
+df_status df_kernel_stats(df_ctx* ctx, uint32_t kind, uint64_t* launches, double* total_ms, double* flops,
+                          double* bytes);
+
 /* Number of kernel launches this context issued so far (bench "gpu_launches"). */
 uint64_t df_launch_count(const df_ctx* ctx);
 

@@ -96,6 +96,9 @@ _SIGS = {
     "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
     "df_launch_count": (C.c_uint64, [C.c_void_p]),
+    "df_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    "df_kernel_stats": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -294,6 +297,20 @@ class Context:
         M, d = x.shape
         self._ck(self.lib.df_op_rmsnorm_mod(self.h, _ptr(x), _ptr(out), M, d, _ptr(shift), _ptr(scale), float(eps),
                                             _stream(stream)))
+
+    KINDS = ("qkv", "attn_self", "o_proj", "rmsnorm", "cross_q", "attn_cross", "cross_o", "mlp_up", "mlp_down",
+             "head_euler", "patch_embed")
+
+    def profile(self, enable=True, reset=True):
+        self._ck(self.lib.df_profile(self.h, int(enable), int(reset)))
+
+    def kernel_stats(self):
+        out = {}
+        for k, name in enumerate(self.KINDS):
+            n, ms, fl, by = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
+            self._ck(self.lib.df_kernel_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
+            out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+        return out
 
     def launch_count(self):
         return int(self.lib.df_launch_count(self.h))

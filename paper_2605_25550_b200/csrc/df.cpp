@@ -185,6 +185,7 @@ struct df_ctx {
   std::atomic<uint64_t> assigned_t{0}, assigned_d{0};
   size_t ctx_bytes = 0, lat_bytes = 0, out_bytes = 0;
   std::vector<float*> sched_dev;
+  Prof prof;
 };
 
 namespace {
@@ -457,6 +458,7 @@ void t_worker(df_ctx* ctx, Inst* me) {
     WK(cudaEventRecord(me->xsent[b], me->comm));
     // the cond cache must outlive the queued steps: free it once the compute stream passes
     WK(cudaStreamSynchronize(me->compute));
+    if (me->m.prof) me->m.prof->harvest();
     cd.mem.release();
     rs->t_end[1] = now_s();
     me->served++;
@@ -481,7 +483,8 @@ void d_worker(df_ctx* ctx, Inst* me) {
     WK(me->m.decode((const float*)me->slots.slots[rs->slot[1]].buf, me->dout, me->compute));
     WK(cudaEventRecord(me->slots.slots[rs->slot[1]].consumed, me->compute));
     WK(cudaEventRecord(rs->ev[5], me->compute));
-    WK(cudaMemcpyAsync(me->stage_host, me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
+    if (rs->req.out_host)
+      WK(cudaMemcpyAsync(me->stage_host, me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
     WK(cudaStreamSynchronize(me->compute));
     if (x1->t_hash) WK(cudaEventSynchronize(x1->t_hash));
     me->slots.release(rs->slot[1]);
@@ -548,6 +551,26 @@ const char* df_last_error(const df_ctx* ctx) {
 }
 
 uint64_t df_launch_count(const df_ctx*) { return g_launches->load(); }
+
+df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset) {
+  if (!ctx) return DF_ERR_INVALID;
+  for (auto& ip : ctx->inst)
+    if (ip->stage == DF_T) ip->m.prof = enable ? &ctx->prof : nullptr;
+  if (reset) ctx->prof.reset();
+  return DF_OK;
+}
+
+df_status df_kernel_stats(df_ctx* ctx, uint32_t kind, uint64_t* launches, double* total_ms, double* flops,
+                          double* bytes) {
+  if (!ctx || kind >= K_COUNT) return DF_ERR_INVALID;
+  ctx->prof.harvest();
+  std::lock_guard<std::mutex> lk(ctx->prof.mu);
+  if (launches) *launches = ctx->prof.count[kind];
+  if (total_ms) *total_ms = ctx->prof.ms[kind];
+  if (flops) *flops = ctx->prof.flops[kind];
+  if (bytes) *bytes = ctx->prof.bytes[kind];
+  return DF_OK;
+}
 
 df_status df_init(const df_graph* g, df_ctx** out) {
   if (!g || !out) return fail(nullptr, "df_init: null argument", DF_ERR_INVALID);

@@ -41,6 +41,63 @@ void Arena::release() {
 
 static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 
+cudaEvent_t Prof::get() {
+  if (pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = pool.back();
+  pool.pop_back();
+  return e;
+}
+void Prof::harvest() {
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& p : pending) {
+    float t = 0.f;
+    cudaEventSynchronize(p.b);
+    if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+      count[p.kind]++;
+      ms[p.kind] += t;
+      flops[p.kind] += p.flops;
+      bytes[p.kind] += p.bytes;
+    }
+    cudaGetLastError();
+    pool.push_back(p.a);
+    pool.push_back(p.b);
+  }
+  pending.clear();
+}
+void Prof::reset() {
+  harvest();
+  std::lock_guard<std::mutex> lk(mu);
+  for (int k = 0; k < K_COUNT; ++k) count[k] = 0, ms[k] = flops[k] = bytes[k] = 0;
+}
+
+// Brackets one launch with profiler events when profiling is on.
+struct ProfScope {
+  Prof* p;
+  cudaStream_t st;
+  int kind;
+  double fl, by;
+  cudaEvent_t a = nullptr;
+  ProfScope(Prof* p_, cudaStream_t s, int k, double f, double b) : p(p_), st(s), kind(k), fl(f), by(b) {
+    if (p) {
+      std::lock_guard<std::mutex> lk(p->mu);
+      a = p->get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (p) {
+      std::lock_guard<std::mutex> lk(p->mu);
+      cudaEvent_t b = p->get();
+      cudaEventRecord(b, st);
+      p->pending.push_back({kind, a, b, fl, by});
+    }
+  }
+};
+
 // ------------------------------------------------------------------ create / init
 cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uint64_t sd, int msteps) {
   c = cfg;
@@ -244,6 +301,7 @@ cudaError_t Model::init_weights(cudaStream_t st) {
 // ------------------------------------------------------------------ helpers
 cudaError_t Model::gemm(const void* A, int lda, const bf16* Wt, int ldw, int M, int Nn, int K, const Epi& e,
                         int out_f32, cudaStream_t st) {
+  ProfScope ps(prof, st, cur_kind, 2.0 * M * Nn * K, 0.0);
   if (!f32()) {
     DF_L(gemm_tc(static_cast<const bf16*>(A), lda, Wt, ldw, M, Nn, K, e, out_f32, st));
   } else {
@@ -255,6 +313,7 @@ cudaError_t Model::gemm(const void* A, int lda, const bf16* Wt, int ldw, int M, 
 
 cudaError_t Model::attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st) {
   const float scale = 1.0f / std::sqrt(float(dh));
+  ProfScope ps(prof, st, cur_kind, 4.0 * Nq * double(Nk) * dh * c.heads, 0.0);
   if (!f32()) {
     DF_L(attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, c.heads, Nq, Nk, dh, dhp, scale, st));
   } else {
@@ -289,6 +348,13 @@ Epi Model::heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0
   e.Df2 = c.rope_axes[0] / 2; e.Dh2 = c.rope_axes[1] / 2; e.Dw2 = c.rope_axes[2] / 2;
   e.eps = c.eps;
   return e;
+}
+
+cudaError_t Model::norm(const float* x, void* out, int M, int dd, const float* shift, const float* scale,
+                        const bf16* gain, cudaStream_t st) {
+  ProfScope ps(prof, st, K_NORM, 0.0, double(M) * dd * (4.0 + act_bytes()));
+  DF_L(rmsnorm_mod(x, out, f32() ? 1 : 0, M, dd, shift, scale, gain, c.eps, st));
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ prologue (a1)
@@ -367,43 +433,50 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
   const float* md = mods + size_t(l) * 6 * d;  // sh1, sc1, g1, sh2, sc2, g2
   const size_t per = size_t(c.heads) * Lt * dhp * act_bytes();
   // a4: h = RMSNorm(r)(1 + sc1) + sh1
-  DF_L(rmsnorm_mod(res, h, of, N, d, md + 0 * d, md + 1 * d, nullptr, c.eps, st));
+  DF_TRY(norm(res, h, N, d, md + 0 * d, md + 1 * d, nullptr, st));
   // a5: q,k,v = heads(h Wqkv + b); qk-RMSNorm * g; RoPE3 on q, k
   {
     Epi e = heads_epi(N, 3, w.qkv_b, q, w.g_q, 1, k, w.g_k, 1, v, nullptr, 0);
+    cur_kind = K_QKV;
     DF_TRY(gemm(h, d, w.qkv_wT, d, N, 3 * d, d, e, of, st));
   }
   // a6: self-attention
+  cur_kind = K_ATTN_SELF;
   DF_TRY(attn(q, k, v, o, N, N, st));
   // a7: r += g1 * (o Wo + bo)
   {
     Epi e = epi_base(EPI_GRES, N, d);
     e.bias = w.o_b;
+    cur_kind = K_O;
     e.resid = res;
     e.ldr = d;
     e.gate = md + 2 * d;
     DF_TRY(gemm(o, d, w.o_wT, d, N, d, d, e, of, st));
   }
   // a8: cross-attention: hc = RMSNorm(r) g_n3; qc = headRMS(hc Wcq + b) g_cq; r += attn Wco + b
-  DF_L(rmsnorm_mod(res, h, of, N, d, nullptr, nullptr, w.g_n3, c.eps, st));
+  DF_TRY(norm(res, h, N, d, nullptr, nullptr, w.g_n3, st));
   {
     Epi e = heads_epi(N, 1, w.cq_b, qc, w.g_cq, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
+    cur_kind = K_CQ;
     DF_TRY(gemm(h, d, w.cq_wT, d, N, d, d, e, of, st));
   }
+  cur_kind = K_ATTN_CROSS;
   DF_TRY(attn(qc, (const char*)cd.kc + l * per, (const char*)cd.vc + l * per, o, N, Lt, st));
   {
     Epi e = epi_base(EPI_GRES, N, d);
     e.bias = w.co_b;
+    cur_kind = K_CO;
     e.resid = res;
     e.ldr = d;
     DF_TRY(gemm(o, d, w.co_wT, d, N, d, d, e, of, st));
   }
   // a9: h2 = RMSNorm(r)(1 + sc2) + sh2
-  DF_L(rmsnorm_mod(res, h, of, N, d, md + 3 * d, md + 4 * d, nullptr, c.eps, st));
+  DF_TRY(norm(res, h, N, d, md + 3 * d, md + 4 * d, nullptr, st));
   // a10: a = SiLU(h2 W1 + b1) * (h2 W3 + b3);  r += g2 * (a W2 + b2)
   {
     Epi e = epi_base(EPI_SWIGLU, N, 2 * f);
     e.bias = w.b13;
+    cur_kind = K_UP;
     e.out = a;
     e.ldo = f;
     DF_TRY(gemm(h, d, w.w13T, d, N, 2 * f, d, e, of, st));
@@ -411,6 +484,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
   {
     Epi e = epi_base(EPI_GRES, N, d);
     e.bias = w.b2;
+    cur_kind = K_DOWN;
     e.resid = res;
     e.ldr = d;
     e.gate = md + 5 * d;
@@ -430,16 +504,18 @@ cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStrea
   {
     Epi e = epi_base(EPI_STORE, N, d);
     e.bias = patch_b;
+    cur_kind = K_PATCH;
     e.out = r;
     e.ldo = d;
     DF_TRY(gemm(X, P, patch_wT, P, N, d, P, e, 1, st));
   }
   for (int l = 0; l < c.layers; ++l) DF_TRY(block(cd, i, l, r, st));
   // a11 + a12: head modulation, projection, unpatchify, Euler update fused in the epilogue
-  DF_L(rmsnorm_mod(r, h, of, N, d, headmod, headmod + d, nullptr, c.eps, st));
+  DF_TRY(norm(r, h, N, d, headmod, headmod + d, nullptr, st));
   {
     Epi e = epi_base(EPI_EULER, N, P);
     e.bias = head_b;
+    cur_kind = K_HEAD;
     e.x_lat = x;
     e.v_out = v_out;
     e.dsig = float(double(cd.sig[i + 1]) - double(cd.sig[i]));

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <atomic>
 #include <cuda_runtime.h>
 #include "../../include/df.h"
 #include "kernels.h"
@@ -54,7 +56,25 @@ struct Arena {
   void release();
 };
 
-struct DitModel;  // weights of all stages for one device
+// Kernel classes timed by the optional per-launch profiler (df_profile / df_kernel_stats).
+enum KernelKind : int {
+  K_QKV = 0, K_ATTN_SELF, K_O, K_NORM, K_CQ, K_ATTN_CROSS, K_CO, K_UP, K_DOWN, K_HEAD, K_PATCH, K_PROLOGUE,
+  K_MISC, K_COUNT
+};
+
+// Records a CUDA event pair around each launch of a class; harvested after the stream
+// passes them (no host synchronisation on the launch path).
+struct Prof {
+  std::mutex mu;
+  std::vector<cudaEvent_t> pool;
+  struct Pending { int kind; cudaEvent_t a, b; double flops, bytes; };
+  std::vector<Pending> pending;
+  uint64_t count[K_COUNT] = {};
+  double ms[K_COUNT] = {}, flops[K_COUNT] = {}, bytes[K_COUNT] = {};
+  cudaEvent_t get();
+  void harvest();   // consumes completed pairs (blocks on each pending pair)
+  void reset();
+};
 
 // Per-request conditioning handle (df_cond).
 struct Cond {
@@ -108,6 +128,9 @@ struct Model {
   void* ef = nullptr;       // [L, f_e]
   float* etmp = nullptr;    // [L, 2 f_e]
   std::vector<const bf16*> layer_mods;
+  Prof* prof = nullptr;
+  int cur_kind = K_MISC;
+  double cur_flops = 0, cur_bytes = 0;
 
   cudaError_t create(const df_dit_cfg& cfg, int precision, int device, int stage, uint64_t seed, int max_steps);
   void destroy();
@@ -127,6 +150,8 @@ struct Model {
   Epi heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0, int rope0, void* o1, const bf16* g1,
                 int rope1, void* o2, const bf16* g2, int rope2) const;
   cudaError_t block(const Cond& c, int i, int l, float* r, cudaStream_t st);
+  cudaError_t norm(const float* x, void* out, int M, int dd, const float* shift, const float* scale, const bf16* gain,
+                   cudaStream_t st);
   cudaError_t init_weights(cudaStream_t st);
 };
 

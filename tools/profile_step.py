@@ -1,0 +1,49 @@
+"""Drive a short, ncu-friendly slice of the hot path: prologue + `--steps` DiT steps
+(first step = warm-up) of one request at a BASELINE workload shape, through the C ABI.
+
+    ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file launches.csv \
+        python tools/profile_step.py --config image --steps 2
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_25550_b200 import binding as B  # noqa: E402
+from synth.configs import CONFIGS, with_layers  # noqa: E402
+from synth import inputs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="image")
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=2)
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    if a.layers:
+        cfg = with_layers(cfg, a.layers)
+    g = B.make_graph(cfg, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)], max_steps=cfg.steps)
+    with B.Context(g) as c:
+        ctx = torch.from_numpy(inputs.ctx_bf16(cfg, 1).view(np.int16)).cuda().view(torch.bfloat16)
+        s = np.linspace(1, 0, cfg.steps + 1).astype(np.float32)
+        cond = c.dit_prepare(1, ctx, s)
+        x = torch.from_numpy(inputs.latent(cfg, 2)).cuda()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+        ev[0].record()
+        for i in range(a.steps):
+            c.dit_step(1, cond, i, x)
+            ev[i + 1].record()
+        torch.cuda.synchronize()
+        ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
+        fl = cfg.flops_per_step()
+        print({"config": cfg.name, "layers": cfg.layers, "step_ms": ms,
+               "tflops": [fl / (m / 1e3) / 1e12 for m in ms]})
+        c.cond_release(cond)
+
+
+if __name__ == "__main__":
+    main()
