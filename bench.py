@@ -103,12 +103,15 @@ class Clocks:
 
 # ------------------------------------------------------------------ oracle timing (reference arm / cpu_baseline)
 def oracle_sample(cfg, reps=1):
-    """Time the fp64 oracle on one DiT block at the full workload shape (weights generated
-    beforehand, untimed); extrapolate to requests/s = 1 / (t_block * layers * steps)."""
+    """Time the fp64 oracle on ONE DiT block with the workload's width (d, heads, f,
+    L_txt) on a bounded token count (a 32x32 latent, N = 1024: ~10-30 s of CPU work);
+    weights are generated beforehand (untimed).  Extrapolate by algorithmic FLOP:
+    requests/s = (oracle FLOP/s on the sample) / (FLOP per request of the workload)."""
+    import dataclasses
     import numpy as np
     from oracle import params as OP, dit
     from synth import inputs
-    c1 = with_layers(cfg, 1)
+    c1 = dataclasses.replace(with_layers(cfg, 1), F=1, H=min(cfg.H, 64), W=min(cfg.W, 64))
     P = OP.Params(c1, 0)
     for n in ("L0.mod", "L0.qkv_w", "L0.qkv_b", "L0.g_q", "L0.g_k", "L0.o_w", "L0.o_b", "L0.g_n3", "L0.cq_w",
               "L0.cq_b", "L0.g_cq", "L0.co_w", "L0.co_b", "L0.w1", "L0.b1", "L0.w3", "L0.b3", "L0.w2", "L0.b2"):
@@ -124,15 +127,17 @@ def oracle_sample(cfg, reps=1):
         dit.block(P, c1, 0, r, e6, kv, pos)
         times.append(time.perf_counter() - t0)
     t = min(times)
-    per_req = t * cfg.layers * cfg.steps
+    block_flops = (c1.flops_per_step() - 4 * c1.N * c1.P * c1.d) / c1.layers
+    rate = block_flops / t
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    return {"t_block_s": t, "value": 1.0 / per_req, "cores": cores,
-            "sample": f"1 DiT block of the {cfg.name} workload at full shape (N={cfg.N}, d={cfg.d}, f={cfg.ffn}, "
-                      f"L_txt={cfg.L_txt}), fp64 numpy oracle, extrapolated x{cfg.layers} layers x{cfg.steps} steps"}
+    return {"t_block_s": t, "value": rate / cfg.flops_per_request(), "cores": cores, "gflops": rate / 1e9,
+            "sample": f"1 DiT block at the {cfg.name} width (d={cfg.d}, heads={cfg.heads}, f={cfg.ffn}, "
+                      f"L_txt={cfg.L_txt}) on N={c1.N} tokens, fp64 numpy oracle ({rate / 1e9:.1f} GFLOP/s), "
+                      f"extrapolated by FLOP to one {cfg.name} request ({cfg.flops_per_request():.3e} FLOP)"}
 
 
 def run_reference(args, cfg):

@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cmath>
+#include <cstdlib>
 #include "kernels.h"
 
 namespace df {
@@ -251,9 +252,253 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ------------------------------------------------------------------ attn_tc2: 2 Q tiles / CTA
+// Two 128-query tiles of one head share every K/V block (halving L2->SMEM traffic per
+// FLOP).  TMEM (512 cols): S0 [0,128), S1 [128,256), O0 [256, 256+DH), O1 [256+DH, ..).
+// P_i (bf16, 2 per column) is written by softmax group i over the first 64 columns of
+// S_i and consumed from TMEM as the A operand of PV.  MMA issue order per key block j:
+//   PV0_j, QK0_{j+1}, PV1_j, QK1_{j+1}
+// so the tensor core always has the other tile's work while a softmax group runs, and
+// in-order execution guarantees PV_i_j has read P_i before QK_i_{j+1} overwrites S_i.
+template <int DH>
+struct Attn2Cfg {
+  static constexpr int ATOMS = DH / 64;
+  static constexpr int TILE = 128 * 128;
+  static constexpr int Q_BYTES = ATOMS * TILE;     // one 128-query tile
+  static constexpr int KV_BYTES = ATOMS * TILE;    // one K or V block of 128 keys
+  static constexpr int OFF_Q = 0;                  // Q0, Q1
+  static constexpr int OFF_K = 2 * Q_BYTES;        // K[2]
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;  // V[2]
+  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t O_COL = 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(384, 1)
+    attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                    int dh_real, float scale_log2) {
+  using Cfg = Attn2Cfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2] per Q tile
+  uint64_t* p_full = bars + 7;    // [2] per Q tile
+  uint64_t* o_done = bars + 9;    // [2] per Q tile (after the last PV)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int h = blockIdx.y;
+  const int q0 = blockIdx.x * 256;
+  const int nkb = (Nk + 127) / 128;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * Cfg::Q_BYTES);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int a = 0; a < Cfg::ATOMS; ++a)
+          tma_load_3d(sQ + t * Cfg::Q_BYTES + a * Cfg::TILE, &tmQ, q_full, a * 64, q0 + t * 128, h);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Cfg::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < Cfg::ATOMS; ++a) {
+          tma_load_3d(sK + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmK, &kv_full[st], a * 64, j * 128, h);
+          tma_load_3d(sV + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmV, &kv_full[st], a * 64, j * 128, h);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(128, DH, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_qk = [&](int t, int j) {
+        const uint32_t k_addr = smem_u32(sK + (j & 1) * Cfg::KV_BYTES);
+        const uint32_t qa = q_addr + t * Cfg::Q_BYTES;
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const uint32_t off = (k >> 2) * Cfg::TILE + (k & 3) * 32;
+          tc_mma_bf16(tmem + t * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), idesc_qk,
+                      k > 0);
+        }
+        tc_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t v_addr = smem_u32(sV + (j & 1) * Cfg::KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // 128 keys / 16; P_t columns k*8.. of S_t
+          tc_mma_bf16_ts(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, sdesc_sw128(v_addr + k * 2048, Cfg::TILE, 1024),
+                         idesc_pv, (j > 0 || k > 0));
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      for (int j = 0; j < nkb; ++j) {
+        const bool more = j + 1 < nkb;
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (j + 1 == nkb) tc_commit(&o_done[0]);
+        if (more) {
+          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_qk(0, j + 1);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j);
+        tc_commit(&kv_empty[j & 1]);
+        if (j + 1 == nkb) tc_commit(&o_done[1]);
+        if (more) issue_qk(1, j + 1);
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;        // Q tile of this softmax group
+    const int ew = (warp - 4) & 3;        // TMEM lane quarter
+    const int r = ew * 32 + lane;         // query row within the tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const uint32_t ts = tmem + lane_off + t * 128;
+    const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
+      tc_wait_ld();
+      const int valid = Nk - j * 128;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        s[c] = (c < valid) ? s[c] * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[c]);
+      }
+      const bool need = mx > m_used + 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_used;
+        if (j > 0) {
+          // s_full for block j implies PV_{j-1} (issued earlier) completed: O_t is stable
+          const float alpha = exp2f(m_used - m_new);
+          l *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < DH; c += 32) {
+            float o[32];
+            tmem_ld32(to + c, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(to + c, o);
+          }
+        }
+        m_used = m_new;
+      }
+      float lsum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float p0 = exp2f(s[c + 2 * i] - m_used), p1 = exp2f(s[c + 2 * i + 1] - m_used);
+          lsum += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(ts + c / 2, pk);
+      }
+      l += lsum;
+      tc_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&o_done[t], 0);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    const int q = q0 + t * 128 + r;
+    bf16* orow = O + size_t(q) * H * dh_real + size_t(h) * dh_real;
+#pragma unroll 1
+    for (int c = 0; c < DH; c += 32) {
+      float o[32];
+      tmem_ld32(to + c, o);
+      tc_wait_ld();
+      if (q < Nq && c < dh_real) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] *= inv;
+        if (dh_real - c >= 32) store_vec<32>(orow + c, o);
+        else
+          for (int i = 0; i < dh_real - c; ++i) orow[c + i] = __float2bfloat16_rn(o[i]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int g_attn_impl = 2;
+
+template <int DH>
+static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, bf16* O, int H,
+                                int Nq, int Nk, int dh, float scale, cudaStream_t st) {
+  using Cfg = Attn2Cfg<DH>;
+  auto kern = attn_tc2_kernel<DH>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((Nq + 255) / 256, H);
+  kern<<<grid, 384, Cfg::SMEM, st>>>(tq, tk, tv, O, H, Nq, Nk, dh, scale * 1.4426950408889634f);
+  return cudaGetLastError();
+}
+
 template <int DH>
 static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
                                float scale, cudaStream_t st) {
+  if (g_attn_impl == 2) {
+    CUtensorMap tq, tk, tv;
+    if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
+        !make_tmap_3d(&tv, V, H, Nk, DH, 128))
+      return cudaErrorInvalidValue;
+    return launch_attn2<DH>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st);
+  }
   using Cfg = AttnCfg<DH>;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
@@ -273,6 +518,11 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
 
 cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
                     float scale, cudaStream_t st) {
+  static const int impl_env = [] {
+    const char* e = getenv("DF_ATTN_IMPL");  // 1: one Q tile per CTA (round-1 kernel), 2: two (default)
+    return e ? atoi(e) : 2;
+  }();
+  g_attn_impl = impl_env;
   if (Nq <= 0) return cudaSuccess;
   if (Nk <= 0 || dh > dh_pad) return cudaErrorInvalidValue;
   if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st);

@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include "kernels.h"
 
 namespace df {
@@ -61,6 +62,8 @@ bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, u
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+int g_disable_pair = 0;
 
 int num_sms() {
   static int n = 0;
@@ -244,6 +247,183 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ 2-CTA (cta_group::2) GEMM
+// A CTA pair computes a 256 x 256 tile: CTA r loads A rows [r*128, r*128+128) and W rows
+// [r*128, r*128+128) of the tile (half the operand bytes of a 1-CTA 128x256 tile per
+// unit of work); the leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) whose
+// accumulator rows r*128.. live in CTA r's TMEM; each CTA's epilogue drains its own rows.
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * GBK * 2;
+constexpr int P_B_BYTES = 128 * GBK * 2;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+template <int CW, typename OutT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, const __grid_constant__ Epi epi) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P_STAGES * P_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + P_STAGES;
+  uint64_t* tfull = bars + 2 * P_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int num_m = (M + 255) / 256;
+  const int num_n = (N + 255) / 256;
+  const int tiles = num_m * num_n;
+  const int KB = (K + GBK - 1) / GBK;
+  const int cid = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 2);    // leader: own expect_tx + the peer's remote arrive
+      mbar_init(&empty[s], 1);   // multicast commit from the leader's MMA
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);   // multicast commit
+      mbar_init(&tempty[s], 256);  // 128 epilogue threads of each CTA (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < tiles; t += nclusters) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          else mbar_arrive_cluster(&full[stage], 0);
+          tma_load_2d_pair(sA + stage * P_A_BYTES, &tmA, &full[stage], kb * GBK, mb * 256 + rank * 128);
+          tma_load_2d_pair(sB + stage * P_B_BYTES, &tmB, &full[stage], kb * GBK, nb * 256 + rank * 128);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16(256, 256, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cid; t < tiles; t += nclusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a0 = smem_u32(sA + stage * P_A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * P_B_BYTES);
+#pragma unroll
+            for (int k = 0; k < GBK / 16; ++k)
+              tc_mma_bf16_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                               (kb | k) != 0);
+            tc_commit_pair(&empty[stage], 0x3);
+            if (kb == KB - 1) tc_commit_pair(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    float v[CW];
+    for (int t = cid; t < tiles; t += nclusters) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + rank * 128 + ew * 32 + lane;
+      const uint32_t trow = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int c = 0; c < 256; c += CW) {
+        const int n0 = nb * 256 + c;
+        if (n0 >= N) break;
+#pragma unroll
+        for (int q = 0; q < CW; q += 16) tmem_ld16(trow + c + q, v + q);
+        tc_wait_ld();
+        epi_apply<CW, OutT>(epi, row, n0, v);
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(&tempty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+template <int CW, typename OutT>
+static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
+                              cudaStream_t st) {
+  auto kern = gemm_tc2_kernel<CW, OutT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  int pairs = num_sms() / 2;
+  int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, 256, P_SMEM, st>>>(ta, tb, M, N, K, epi);
+  return cudaGetLastError();
+}
+
+static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
+                                int out_f32, cudaStream_t st) {
+  if (epi.kind == EPI_HEADS) {
+    if (out_f32) return cudaErrorInvalidValue;
+    switch (epi.dh) {
+      case 16: return launch_tc2<16, bf16>(ta, tb, M, N, K, epi, st);
+      case 64: return launch_tc2<64, bf16>(ta, tb, M, N, K, epi, st);
+      case 128: return launch_tc2<128, bf16>(ta, tb, M, N, K, epi, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return out_f32 ? launch_tc2<32, float>(ta, tb, M, N, K, epi, st) : launch_tc2<32, bf16>(ta, tb, M, N, K, epi, st);
+}
+
 template <int BN>
 static cudaError_t dispatch_cw(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
                                int out_f32, cudaStream_t st) {
@@ -263,9 +443,19 @@ cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N
                     cudaStream_t st, int bn) {
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
   if ((lda * 2) % 16 || (ldw * 2) % 16) return cudaErrorInvalidValue;
+  static const int pair_env = [] {
+    const char* e = getenv("DF_GEMM_PAIR");  // 0: 1-CTA 128x256 tiles only
+    return e ? atoi(e) : 1;
+  }();
+  if (!pair_env) g_disable_pair = 1;
   if (bn == 256 && N <= 128) bn = N <= 64 ? 64 : 128;
   if (epi.kind == EPI_HEADS && bn < epi.dh) bn = 128;
   CUtensorMap ta, tb;
+  if (bn == 256 && M >= 256 && N >= 256 && !g_disable_pair) {  // CTA-pair 256x256 tiles
+    if (!make_tmap_2d(&ta, A, M, K, lda, 128)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&tb, W, N, K, ldw, 128)) return cudaErrorInvalidValue;
+    return dispatch_tc2(ta, tb, M, N, K, epi, out_f32, st);
+  }
   if (!make_tmap_2d(&ta, A, M, K, lda, GBM)) return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tb, W, N, K, ldw, bn)) return cudaErrorInvalidValue;
   if (bn == 256) return dispatch_cw<256>(ta, tb, M, N, K, epi, out_f32, st);

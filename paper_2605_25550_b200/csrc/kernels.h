@@ -8,6 +8,7 @@
 namespace df {
 
 int num_sms();
+extern int g_disable_pair;  // 1: never use the CTA-pair GEMM (tests)
 
 // ---- tensor-core GEMM: out = epilogue(A[M,K] (bf16, row-major, lda) x W[N,K]^T (bf16, ldw)).
 // BN in {64, 128, 256}.  Returns cudaError_t of the launch.

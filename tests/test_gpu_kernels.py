@@ -47,7 +47,8 @@ def test_weight_bytes_equal_oracle_mid_layer():
 
 
 @pytest.mark.parametrize("tc", [1, 0])
-@pytest.mark.parametrize("M,N,K", [(16, 64, 64), (200, 320, 200), (384, 512, 4096), (130, 16, 64)])
+@pytest.mark.parametrize("M,N,K", [(16, 64, 64), (200, 320, 200), (384, 512, 4096), (130, 16, 64),
+                                   (300, 512, 200), (512, 320, 128), (1000, 768, 3072)])
 def test_gemm_integer_bit_exact(tiny_ctx, tc, M, N, K):
     """P11: integer-valued bf16 operands -> exact fp32 accumulation; tails in M, N, K."""
     A = inputs.int_matrix((M, K), -8, 8, seed=M + K)
