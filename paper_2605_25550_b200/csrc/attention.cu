@@ -266,10 +266,12 @@ struct Attn2Cfg {
   static constexpr int TILE = 128 * 128;
   static constexpr int Q_BYTES = ATOMS * TILE;     // one 128-query tile
   static constexpr int KV_BYTES = ATOMS * TILE;    // one K or V block of 128 keys
+  static constexpr int KST = 3;                    // K ring depth (K_j is needed one PV earlier than V_j)
+  static constexpr int VST = 2;                    // V ring depth
   static constexpr int OFF_Q = 0;                  // Q0, Q1
-  static constexpr int OFF_K = 2 * Q_BYTES;        // K[2]
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;  // V[2]
-  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
+  static constexpr int OFF_K = 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VST * KV_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t O_COL = 256;
 };
@@ -287,12 +289,14 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = smem + Cfg::OFF_V;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2] per Q tile
-  uint64_t* p_full = bars + 7;    // [2] per Q tile
-  uint64_t* o_done = bars + 9;    // [2] per Q tile (after the last PV)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* k_full = bars + 1;    // [KST]
+  uint64_t* k_empty = bars + 4;   // [KST]
+  uint64_t* v_full = bars + 7;    // [VST]
+  uint64_t* v_empty = bars + 9;   // [VST]
+  uint64_t* s_full = bars + 11;   // [2] per Q tile
+  uint64_t* p_full = bars + 13;   // [2] per Q tile
+  uint64_t* o_done = bars + 15;   // [2] per Q tile (after the last PV)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -305,9 +309,15 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
+    for (int s = 0; s < Cfg::KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 128);
       mbar_init(&o_done[s], 1);
@@ -328,14 +338,25 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int a = 0; a < Cfg::ATOMS; ++a)
           tma_load_3d(sQ + t * Cfg::Q_BYTES + a * Cfg::TILE, &tmQ, q_full, a * 64, q0 + t * 128, h);
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], 2 * Cfg::KV_BYTES);
+      // K runs ahead of V by up to KST blocks; interleave so neither ring starves
+      int jk = 0, jv = 0;
+      while (jv < nkb) {
+        if (jk < nkb && jk <= jv + 1) {
+          const int st = jk % Cfg::KST;
+          mbar_wait(&k_empty[st], ((jk / Cfg::KST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], Cfg::KV_BYTES);
 #pragma unroll
-        for (int a = 0; a < Cfg::ATOMS; ++a) {
-          tma_load_3d(sK + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmK, &kv_full[st], a * 64, j * 128, h);
-          tma_load_3d(sV + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmV, &kv_full[st], a * 64, j * 128, h);
+          for (int a = 0; a < Cfg::ATOMS; ++a)
+            tma_load_3d(sK + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmK, &k_full[st], a * 64, jk * 128, h);
+          ++jk;
+        } else {
+          const int st = jv % Cfg::VST;
+          mbar_wait(&v_empty[st], ((jv / Cfg::VST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], Cfg::KV_BYTES);
+#pragma unroll
+          for (int a = 0; a < Cfg::ATOMS; ++a)
+            tma_load_3d(sV + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmV, &v_full[st], a * 64, jv * 128, h);
+          ++jv;
         }
       }
     }
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idesc_pv = idesc_bf16(128, DH, false, true);
       const uint32_t q_addr = smem_u32(sQ);
       auto issue_qk = [&](int t, int j) {
-        const uint32_t k_addr = smem_u32(sK + (j & 1) * Cfg::KV_BYTES);
+        const uint32_t k_addr = smem_u32(sK + (j % Cfg::KST) * Cfg::KV_BYTES);
         const uint32_t qa = q_addr + t * Cfg::Q_BYTES;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
@@ -356,34 +377,41 @@ __global__ void __launch_bounds__(384, 1)
         tc_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {
-        const uint32_t v_addr = smem_u32(sV + (j & 1) * Cfg::KV_BYTES);
+        const uint32_t v_addr = smem_u32(sV + (j % Cfg::VST) * Cfg::KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)  // 128 keys / 16; P_t columns k*8.. of S_t
-          tc_mma_bf16_ts(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, sdesc_sw128(v_addr + k * 2048, Cfg::TILE, 1024),
-                         idesc_pv, (j > 0 || k > 0));
+        for (int k = 0; k < 8; ++k)  // 128 keys / 16; P_t = columns k*8.. of S_t
+          tc_mma_bf16_ts(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8,
+                         sdesc_sw128(v_addr + k * 2048, Cfg::TILE, 1024), idesc_pv, (j > 0 || k > 0));
+      };
+      auto wait_k = [&](int j) {
+        mbar_wait(&k_full[j % Cfg::KST], (j / Cfg::KST) & 1);
+        tc_fence_after();
       };
       mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
-      tc_fence_after();
+      wait_k(0);
       issue_qk(0, 0);
       issue_qk(1, 0);
+      tc_commit(&k_empty[0]);
       for (int j = 0; j < nkb; ++j) {
         const bool more = j + 1 < nkb;
+        mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
         mbar_wait(&p_full[0], j & 1);
         tc_fence_after();
         issue_pv(0, j);
-        if (j + 1 == nkb) tc_commit(&o_done[0]);
+        if (!more) tc_commit(&o_done[0]);
         if (more) {
-          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          tc_fence_after();
+          wait_k(j + 1);
           issue_qk(0, j + 1);
         }
         mbar_wait(&p_full[1], j & 1);
         tc_fence_after();
         issue_pv(1, j);
-        tc_commit(&kv_empty[j & 1]);
-        if (j + 1 == nkb) tc_commit(&o_done[1]);
-        if (more) issue_qk(1, j + 1);
+        tc_commit(&v_empty[j % Cfg::VST]);
+        if (!more) tc_commit(&o_done[1]);
+        if (more) {
+          issue_qk(1, j + 1);
+          tc_commit(&k_empty[(j + 1) % Cfg::KST]);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -402,12 +430,15 @@ __global__ void __launch_bounds__(384, 1)
       for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
       tc_wait_ld();
       const int valid = Nk - j * 128;
+      if (valid < 128) {  // ragged last key block (warp-uniform)
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) s[c] = -INFINITY;
+      }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        s[c] = (c < valid) ? s[c] * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[c]);
-      }
+      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      mx *= scale_log2;
       const bool need = mx > m_used + 8.0f;
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? mx : m_used;
@@ -433,7 +464,8 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float p0 = exp2f(s[c + 2 * i] - m_used), p1 = exp2f(s[c + 2 * i + 1] - m_used);
+          float p0 = exp2f(fmaf(s[c + 2 * i], scale_log2, -m_used));
+          float p1 = exp2f(fmaf(s[c + 2 * i + 1], scale_log2, -m_used));
           lsum += p0 + p1;
           pk[i] = pack_bf16x2(p0, p1);
         }

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--config", default="image")
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--kstats", action="store_true")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     if a.layers:
@@ -31,6 +32,8 @@ def main():
         ctx = torch.from_numpy(inputs.ctx_bf16(cfg, 1).view(np.int16)).cuda().view(torch.bfloat16)
         s = np.linspace(1, 0, cfg.steps + 1).astype(np.float32)
         cond = c.dit_prepare(1, ctx, s)
+        if a.kstats:
+            c.profile(True, True)
         x = torch.from_numpy(inputs.latent(cfg, 2)).cuda()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
         ev[0].record()
@@ -42,6 +45,15 @@ def main():
         fl = cfg.flops_per_step()
         print({"config": cfg.name, "layers": cfg.layers, "step_ms": ms,
                "tflops": [fl / (m / 1e3) / 1e12 for m in ms]})
+        if a.kstats:
+            ks = c.kernel_stats()
+            tot = sum(v["ms"] for v in ks.values())
+            for k, v in ks.items():
+                if v["launches"]:
+                    avg = v["ms"] / v["launches"]
+                    print(f"  {k:12s} share {v['ms'] / tot:6.3f}  avg {avg * 1e3:8.1f} us  "
+                          f"{(v['flops'] / v['ms'] / 1e9) if v['flops'] else (v['bytes'] / v['ms'] / 1e6):8.1f} "
+                          f"{'TFLOP/s' if v['flops'] else 'GB/s'}")
         c.cond_release(cond)
 
 
