@@ -276,7 +276,13 @@ struct Attn2Cfg {
   static constexpr uint32_t O_COL = 256;
 };
 
-template <int DH>
+DF_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int DH, bool POLY>
 __global__ void __launch_bounds__(384, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
@@ -324,7 +330,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -415,8 +421,8 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp >= 4) {
-    const int t = (warp - 4) >> 2;        // Q tile of this softmax group
-    const int ew = (warp - 4) & 3;        // TMEM lane quarter
+    const int t = (warp - 4) >> 2;        // Q tile of this softmax group (warps 4-7, 8-11)
+    const int ew = warp & 3;              // TMEM lane quarter = warp id mod 4
     const int r = ew * 32 + lane;         // query row within the tile
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
     const uint32_t ts = tmem + lane_off + t * 128;
@@ -425,19 +431,23 @@ __global__ void __launch_bounds__(384, 1)
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
-      tc_wait_ld();
+      // pass 1: row max, 64 columns in flight (S stays in TMEM; low register pressure)
       const int valid = Nk - j * 128;
-      if (valid < 128) {  // ragged last key block (warp-uniform)
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c >= valid) s[c] = -INFINITY;
-      }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      for (int c = 0; c < 128; c += 64) {
+        float s[64];
+        tmem_ld32(ts + c, s);
+        tmem_ld32(ts + c + 32, s + 32);
+        tc_wait_ld();
+        if (valid < 128) {  // ragged last key block (warp-uniform)
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (c + i >= valid) s[i] = -INFINITY;
+        }
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mx = fmaxf(mx, s[i]);
+      }
       mx *= scale_log2;
       const bool need = mx > m_used + 8.0f;
       if (__any_sync(0xffffffffu, need)) {
@@ -458,20 +468,42 @@ __global__ void __launch_bounds__(384, 1)
         }
         m_used = m_new;
       }
-      float lsum = 0.f;
+      // p = 2^(s*scale - m): FFMA2 for the affine part; 3/8 of the exponentials on the
+      // FMA/ALU pipes (polynomial), 5/8 on MUFU.EX2, so neither unit paces the tile.
+      float2 lsum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
+      const float2 nm2 = make_float2(-m_used, -m_used);
+      // pass 2: p = 2^(s*scale - m) -> bf16 pairs over the first half of S (= P_t)
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t pk[16];
+      for (int c = 0; c < 128; c += 64) {
+        float s[64];
+        tmem_ld32(ts + c, s);
+        tmem_ld32(ts + c + 32, s + 32);
+        tc_wait_ld();
+        if (valid < 128) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float p0 = exp2f(fmaf(s[c + 2 * i], scale_log2, -m_used));
-          float p1 = exp2f(fmaf(s[c + 2 * i + 1], scale_log2, -m_used));
-          lsum += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
+          for (int i = 0; i < 64; ++i)
+            if (c + i >= valid) s[i] = -INFINITY;
         }
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+          float2 p;
+          if (POLY && (i & 7) >= 5) {
+            p = exp2_poly2(x);
+          } else {
+            p.x = ex2_approx(x.x);
+            p.y = ex2_approx(x.y);
+          }
+          lsum2 = fadd2(lsum2, p);
+          pk[i] = pack_bf16x2(p.x, p.y);
+        }
+        // columns c/2 .. c/2+31 hold keys c .. c+63; they alias S columns already consumed
         tmem_st16(ts + c / 2, pk);
+        tmem_st16(ts + c / 2 + 16, pk + 16);
       }
-      l += lsum;
+      l += lsum2.x + lsum2.y;
       tc_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[t]);
@@ -497,7 +529,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -505,11 +537,11 @@ __global__ void __launch_bounds__(384, 1)
 
 int g_attn_impl = 2;
 
-template <int DH>
+template <int DH, bool POLY>
 static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, bf16* O, int H,
                                 int Nq, int Nk, int dh, float scale, cudaStream_t st) {
   using Cfg = Attn2Cfg<DH>;
-  auto kern = attn_tc2_kernel<DH>;
+  auto kern = attn_tc2_kernel<DH, POLY>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -529,7 +561,12 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
     if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
         !make_tmap_3d(&tv, V, H, Nk, DH, 128))
       return cudaErrorInvalidValue;
-    return launch_attn2<DH>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st);
+    static const int poly = [] {
+      const char* e = getenv("DF_ATTN_POLY");  // 1: 3/8 of the exponentials by polynomial on the FMA pipe
+      return e ? atoi(e) : 0;
+    }();
+    return poly ? launch_attn2<DH, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st)
+                : launch_attn2<DH, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st);
   }
   using Cfg = AttnCfg<DH>;
   CUtensorMap tq, tk, tv;

@@ -279,3 +279,36 @@ DF_DEV void tmem_st16(uint32_t taddr, const uint32_t* v) {
       : "memory");
 }
 }  // namespace df
+
+namespace df {
+// ---- packed fp32x2 (FFMA2 / FADD2 on sm_100)
+DF_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r, x = *reinterpret_cast<unsigned long long*>(&a), y = *reinterpret_cast<unsigned long long*>(&b),
+                        z = *reinterpret_cast<unsigned long long*>(&c);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(y), "l"(z));
+  return *reinterpret_cast<float2*>(&r);
+}
+DF_DEV float2 fadd2(float2 a, float2 b) {
+  unsigned long long r, x = *reinterpret_cast<unsigned long long*>(&a), y = *reinterpret_cast<unsigned long long*>(&b);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return *reinterpret_cast<float2*>(&r);
+}
+// 2^x for a pair on the FMA/ALU pipes (no MUFU): x = n + f, n = rint(x) via the 1.5*2^23
+// magic add, f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (rel. err 1.5e-4 <<
+// bf16 spacing), exponent added as an integer.  Inputs are clamped at -125.
+DF_DEV float2 exp2_poly2(float2 x) {
+  const float2 lo = make_float2(-125.f, -125.f);
+  x.x = fmaxf(x.x, lo.x);
+  x.y = fmaxf(x.y, lo.y);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);                                  // low mantissa bits = rint(x)
+  const float2 rn = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-rn.x, -rn.y));
+  // 2^f on [-0.5, 0.5]
+  float2 p = ffma2(make_float2(0.05534055f, 0.05534055f), f, make_float2(0.24302744f, 0.24302744f));
+  p = ffma2(p, f, make_float2(0.69324487f, 0.69324487f));
+  p = ffma2(p, f, make_float2(0.99986315f, 0.99986315f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+}  // namespace df
