@@ -67,7 +67,9 @@ typedef struct {
 /* Stage graph: the fixed chain E -> T -> D with an E:T:D instance ratio. */
 typedef struct {
   uint32_t n_inst;
-  struct { int32_t device; int32_t stage; } inst[DF_MAX_INST]; /* co-location allowed */
+  /* device: CUDA device index in the process that hosts the instance; rank: that
+   * process (0 in single-process mode).  Co-location allowed. */
+  struct { int32_t device; int32_t stage; int32_t rank; } inst[DF_MAX_INST];
   uint32_t G;                   /* GPU budget for Eq. 1                                  */
   uint64_t chunk_bytes[2];      /* per edge (0: E->T ctx, 1: T->D latent); 0 = whole     */
   uint32_t n_slots;             /* receive slots per consumer per edge, >= 2             */
@@ -80,6 +82,12 @@ typedef struct {
   float jitter_delay_s;
   uint64_t jitter_seed;
   df_dit_cfg dit;
+  /* One process per GPU (world > 1): every rank passes the same graph with its own
+   * `rank`; instances of other ranks are reached through a POSIX shared-memory control
+   * plane named shm_name (FAA metadata rings) and CUDA IPC receive slots
+   * (the posted destination addresses).  Rank 0 creates the segment. */
+  int32_t rank, world;
+  char shm_name[64];
 } df_graph;
 
 /* df_init: validate the graph (Eq. 1), allocate and Philox-initialise every
@@ -116,6 +124,8 @@ typedef struct {
   float xfer_ms[2];             /* device time of the E->T / T->D transfers               */
   float exposed_ms[2];          /* consumer stall on in-flight data per edge   */
   uint64_t hash_src[2], hash_dst[2]; /* payload hash on both sides of each edge  */
+  const void* out_view;         /* the decoded fp32 output in THIS process (the D rank's copy  */
+  uint64_t out_view_bytes;      /*   in multi-process mode); valid until the next df_poll      */
 } df_completion;
 /* Pop up to max completions ("final output is returned to the request
  * scheduler").  Blocks up to timeout_ms (-1 forever). DF_EMPTY if none. */
@@ -199,6 +209,12 @@ df_status df_op_rmsnorm_mod(df_ctx* ctx, const float* x, void* out, int32_t M, i
 df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset);
 df_status df_kernel_stats(df_ctx* ctx, uint32_t kind, uint64_t* launches, double* total_ms, double* flops,
                           double* bytes);
+
+/* Self-test of the shared-memory metadata ring (no GPU needed): role 0 creates the
+ * segment `name` and pushes n records with seq 0..n-1 into instance 0's inbox; role 1
+ * attaches and pops n records, returning in *checksum the sum of seq and in *fifo_ok
+ * whether they arrived in order.  For the CPU multi-process tests. */
+df_status df_ring_selftest(const char* name, int32_t role, uint64_t n, uint64_t* checksum, int32_t* fifo_ok);
 
 /* Number of kernel launches this context issued so far (bench "gpu_launches"). */
 uint64_t df_launch_count(const df_ctx* ctx);

@@ -31,7 +31,7 @@ class DitCfgC(C.Structure):
 
 
 class InstC(C.Structure):
-    _fields_ = [("device", C.c_int32), ("stage", C.c_int32)]
+    _fields_ = [("device", C.c_int32), ("stage", C.c_int32), ("rank", C.c_int32)]
 
 
 class GraphC(C.Structure):
@@ -39,7 +39,8 @@ class GraphC(C.Structure):
                 ("chunk_bytes", C.c_uint64 * 2), ("n_slots", C.c_uint32), ("handoff_mode", C.c_uint32),
                 ("ring_capacity", C.c_uint32), ("precision", C.c_uint32), ("max_steps", C.c_uint32),
                 ("weight_seed", C.c_uint64), ("jitter_p", C.c_float), ("jitter_delay_s", C.c_float),
-                ("jitter_seed", C.c_uint64), ("dit", DitCfgC)]
+                ("jitter_seed", C.c_uint64), ("dit", DitCfgC), ("rank", C.c_int32), ("world", C.c_int32),
+                ("shm_name", C.c_char * 64)]
 
 
 class ReqIdC(C.Structure):
@@ -56,7 +57,8 @@ class CompletionC(C.Structure):
     _fields_ = [("id", ReqIdC), ("status", C.c_int), ("user_tag", C.c_uint64), ("inst", C.c_int32 * 3),
                 ("t_submit", C.c_double), ("t_start", C.c_double * 3), ("t_end", C.c_double * 3),
                 ("t_done", C.c_double), ("stage_ms", C.c_float * 3), ("xfer_ms", C.c_float * 2),
-                ("exposed_ms", C.c_float * 2), ("hash_src", C.c_uint64 * 2), ("hash_dst", C.c_uint64 * 2)]
+                ("exposed_ms", C.c_float * 2), ("hash_src", C.c_uint64 * 2), ("hash_dst", C.c_uint64 * 2),
+                ("out_view", C.c_void_p), ("out_view_bytes", C.c_uint64)]
 
 
 class HandoffDescC(C.Structure):
@@ -96,6 +98,7 @@ _SIGS = {
     "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
     "df_launch_count": (C.c_uint64, [C.c_void_p]),
+    "df_ring_selftest": (C.c_int, [C.c_char_p, C.c_int32, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
     "df_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "df_kernel_stats": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -140,13 +143,17 @@ def dit_cfg_c(cfg) -> DitCfgC:
 
 
 def make_graph(cfg, instances, precision=DF_BF16, weight_seed=0, chunk_bytes=(0, 0), n_slots=2,
-               handoff_mode=DF_ASYNC | DF_HASH, ring_capacity=256, max_steps=None, jitter=(0.0, 0.0, 0), G=0):
-    """instances: list of (device, stage)."""
+               handoff_mode=DF_ASYNC | DF_HASH, ring_capacity=256, max_steps=None, jitter=(0.0, 0.0, 0), G=0,
+               rank=0, world=1, shm_name=""):
+    """instances: list of (device, stage) or (device, stage, rank)."""
     g = GraphC()
     g.n_inst = len(instances)
-    for i, (dev, st) in enumerate(instances):
-        g.inst[i].device = int(dev)
-        g.inst[i].stage = int(st)
+    for i, ins in enumerate(instances):
+        g.inst[i].device = int(ins[0])
+        g.inst[i].stage = int(ins[1])
+        g.inst[i].rank = int(ins[2]) if len(ins) > 2 else 0
+    g.rank, g.world = int(rank), int(world)
+    g.shm_name = shm_name.encode()[:63]
     g.G = int(G)
     g.chunk_bytes[0], g.chunk_bytes[1] = int(chunk_bytes[0]), int(chunk_bytes[1])
     g.n_slots = int(n_slots)

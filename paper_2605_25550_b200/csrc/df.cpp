@@ -25,6 +25,7 @@
 #include <thread>
 #include <vector>
 #include "ring.h"
+#include "plane.h"
 #include "runtime.h"
 
 using namespace df;
@@ -105,6 +106,9 @@ struct ReqState {
   Xfer* x[2] = {nullptr, nullptr};
   int slot[2] = {-1, -1};
   int xbuf = 0;  // T latent buffer index
+  bool pre = false;       // multi-process: completion filled by the D worker
+  df_completion comp{};
+  std::vector<float> outcopy;  // multi-process: decoded output held in the D process
 };
 
 struct Job {
@@ -162,6 +166,11 @@ struct Inst {
   float* stage_host = nullptr;
   std::atomic<uint64_t> busy_ns{0};
   std::atomic<uint64_t> served{0};
+  // multi-process
+  bool local = true;
+  cudaEvent_t ipc_consumed[PL_MAX_SLOTS] = {};
+  cudaEvent_t ipc_chunk[PL_MAX_SLOTS][PL_MAX_CHUNKS] = {};
+  unsigned long long* mp_hash = nullptr;  // pinned [2]: src (producer side), dst (consumer side)
 };
 
 struct df_ctx {
@@ -185,6 +194,18 @@ struct df_ctx {
   std::atomic<uint64_t> assigned_t{0}, assigned_d{0};
   size_t ctx_bytes = 0, lat_bytes = 0, out_bytes = 0;
   std::vector<float*> sched_dev;
+  // multi-process plane
+  bool mp = false, seg_owner = false;
+  PlaneSeg* seg = nullptr;
+  std::mutex view_mu;
+  struct View {
+    bool open = false, remote = false;
+    void* buf[PL_MAX_SLOTS] = {};
+    cudaEvent_t consumed[PL_MAX_SLOTS] = {};
+    cudaEvent_t chunk[PL_MAX_SLOTS][PL_MAX_CHUNKS] = {};
+  };
+  View views[DF_MAX_INST];
+  std::vector<ReqState*> last_polled;
   Prof prof;
 };
 
@@ -502,6 +523,10 @@ void d_worker(df_ctx* ctx, Inst* me) {
 }
 
 void fill_completion(df_ctx* ctx, ReqState* rs, df_completion* o) {
+  if (rs->pre) {
+    *o = rs->comp;
+    return;
+  }
   std::memset(o, 0, sizeof(*o));
   o->id = rs->id;
   o->status = DF_OK;
@@ -513,6 +538,8 @@ void fill_completion(df_ctx* ctx, ReqState* rs, df_completion* o) {
   }
   o->t_submit = rs->t_submit;
   o->t_done = rs->t_end[2];
+  o->out_view = rs->req.out_host;
+  o->out_view_bytes = rs->req.out_host ? ctx->out_bytes : 0;
   o->stage_ms[0] = ev_ms(rs->ev[0], rs->ev[1]);
   o->stage_ms[1] = ev_ms(rs->ev[2], rs->ev[3]);
   o->stage_ms[2] = ev_ms(rs->ev[4], rs->ev[5]);
@@ -542,6 +569,412 @@ void free_req(ReqState* rs) {
 
 }  // namespace
 
+// ================================================================== one process per GPU
+// (world > 1): instances of other ranks are reached through the shared-memory plane
+// (plane.h) and CUDA IPC.  The protocol per edge, for a consumer instance c:
+//   consumer: owns n_slots receive buffers + an interprocess "consumed" event and
+//             PL_MAX_CHUNKS interprocess chunk events per slot; posts free slot ids in
+//             its free ring (the destination-address handshake).
+//   producer: pops a free slot (empty ring = backpressure), makes its comm stream wait on
+//             the slot's consumed event and on its own compute, copies the payload into
+//             the peer slot in chunks, records the slot's chunk events, pushes a 128-byte
+//             MetaRec into c's inbox and moves on.
+//   consumer: pops the inbox, makes its compute stream wait per chunk (device-side),
+//             consumes, records consumed, re-posts the slot.
+namespace {
+
+int mp_nchunks(uint64_t bytes, uint64_t& chunk) {
+  if (chunk == 0 || chunk >= bytes) chunk = bytes;
+  chunk = (chunk + 15) & ~uint64_t(15);
+  uint64_t n = (bytes + chunk - 1) / chunk;
+  if (n > uint64_t(PL_MAX_CHUNKS)) {
+    chunk = ((bytes + PL_MAX_CHUNKS - 1) / PL_MAX_CHUNKS + 15) & ~uint64_t(15);
+    n = (bytes + chunk - 1) / chunk;
+  }
+  return int(n);
+}
+
+void mp_sleep() { std::this_thread::sleep_for(std::chrono::microseconds(20)); }
+
+// Producer-side view of consumer instance `ci` (opened lazily, cached).
+df_ctx::View* mp_view(df_ctx* ctx, int ci) {
+  df_ctx::View& v = ctx->views[ci];
+  std::lock_guard<std::mutex> lk(ctx->view_mu);
+  if (v.open) return &v;
+  InstPlane& ip = ctx->seg->inst[ci];
+  while (ip.ready.load(std::memory_order_acquire) == 0) {
+    if (ctx->stop) return nullptr;
+    mp_sleep();
+  }
+  Inst* I = ctx->inst[ci].get();
+  for (uint32_t s = 0; s < ip.n_slots; ++s) {
+    if (I->local) {
+      v.buf[s] = I->slots.slots[s].buf;
+      v.consumed[s] = I->ipc_consumed[s];
+      for (int c = 0; c < PL_MAX_CHUNKS; ++c) v.chunk[s][c] = I->ipc_chunk[s][c];
+    } else {
+      if (cudaIpcOpenMemHandle(&v.buf[s], ip.slot_mem[s], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return nullptr;
+      if (cudaIpcOpenEventHandle(&v.consumed[s], ip.consumed[s]) != cudaSuccess) return nullptr;
+      for (int c = 0; c < PL_MAX_CHUNKS; ++c)
+        if (cudaIpcOpenEventHandle(&v.chunk[s][c], ip.chunk[s][c]) != cudaSuccess) return nullptr;
+      v.remote = true;
+    }
+  }
+  v.open = true;
+  return &v;
+}
+
+// Publish a local consumer instance's slots and events into the plane.
+cudaError_t mp_publish(df_ctx* ctx, Inst& I, size_t slot_bytes) {
+  InstPlane& ip = ctx->seg->inst[I.id];
+  ip.n_slots = ctx->g.n_slots;
+  ip.slot_bytes = slot_bytes;
+  ip.nchunks_max = PL_MAX_CHUNKS;
+  for (uint32_t s = 0; s < ctx->g.n_slots; ++s) {
+    DF_TRY(cudaIpcGetMemHandle(&ip.slot_mem[s], I.slots.slots[s].buf));
+    DF_TRY(cudaEventCreateWithFlags(&I.ipc_consumed[s], cudaEventDisableTiming | cudaEventInterprocess));
+    DF_TRY(cudaEventRecord(I.ipc_consumed[s], I.compute));
+    DF_TRY(cudaIpcGetEventHandle(&ip.consumed[s], I.ipc_consumed[s]));
+    for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
+      DF_TRY(cudaEventCreateWithFlags(&I.ipc_chunk[s][c], cudaEventDisableTiming | cudaEventInterprocess));
+      DF_TRY(cudaIpcGetEventHandle(&ip.chunk[s][c], I.ipc_chunk[s][c]));
+    }
+  }
+  DF_TRY(cudaStreamSynchronize(I.compute));
+  for (uint32_t s = 0; s < ctx->g.n_slots; ++s)
+    while (!ip.free_slots.push(s)) mp_sleep();
+  ip.ready.store(1, std::memory_order_release);
+  return cudaSuccess;
+}
+
+// Producer: claim a slot of consumer `ci`, copy `bytes` after prod_stream's work, post meta.
+// Returns false on stop / error (error recorded).
+bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, uint64_t bytes, uint64_t chunk, cudaStream_t prod,
+             MetaRec m, uint32_t edge) {
+  df_ctx::View* v = mp_view(ctx, ci);
+  if (!v) {
+    if (!ctx->stop) worker_fail(ctx, "mp_send: cannot open the consumer's IPC handles");
+    return false;
+  }
+  InstPlane& ip = ctx->seg->inst[ci];
+  uint32_t s;
+  while (!ip.free_slots.pop(s)) {  // backpressure: no posted destination address yet
+    if (ctx->stop) return false;
+    mp_sleep();
+  }
+  auto chk = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) worker_fail(ctx, std::string("mp_send: ") + what + ": " + cudaGetErrorString(e));
+    return e == cudaSuccess;
+  };
+  cudaEvent_t ready;
+  if (!chk(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event")) return false;
+  if (!chk(cudaEventRecord(ready, prod), "record")) return false;
+  if (!chk(cudaStreamWaitEvent(me->comm, ready, 0), "wait")) return false;
+  cudaEventDestroy(ready);
+  if (!chk(cudaStreamWaitEvent(me->comm, v->consumed[s], 0), "wait consumed")) return false;
+  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f) {  // P:L142, R23
+    uint32_t c[4] = {uint32_t(m.seq), uint32_t(m.seq >> 32), edge, 3u};
+    philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
+    if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0) {
+      g_launches->fetch_add(1);
+      if (!chk(delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), me->comm), "delay")) return false;
+    }
+  }
+  unsigned long long* h = me->mp_hash;
+  if (ctx->g.handoff_mode & DF_HASH) {
+    g_launches->fetch_add(1);
+    if (!chk(payload_hash(src, bytes, 0, h, me->comm), "hash")) return false;
+  }
+  int n = mp_nchunks(bytes, chunk);
+  for (int c = 0; c < n; ++c) {
+    uint64_t off = uint64_t(c) * chunk, sz = std::min<uint64_t>(chunk, bytes - off);
+    if (!chk(cudaMemcpyAsync(static_cast<char*>(v->buf[s]) + off, static_cast<const char*>(src) + off, sz,
+                             cudaMemcpyDeviceToDevice, me->comm), "copy"))
+      return false;
+    if (!chk(cudaEventRecord(v->chunk[s][c], me->comm), "chunk event")) return false;
+  }
+  if (ctx->g.handoff_mode & DF_SYNC) {  // P:L151 comparison mode: the producer waits for delivery
+    if (!chk(cudaStreamSynchronize(me->comm), "sync")) return false;
+  }
+  if (ctx->g.handoff_mode & DF_HASH) {
+    if (!chk(cudaStreamSynchronize(me->comm), "hash sync")) return false;
+    m.hash_src = *h;
+  }
+  m.slot = s;
+  m.nchunks = uint32_t(n);
+  m.chunk_bytes = uint32_t(chunk);
+  while (!ip.inbox.push(m)) {
+    if (ctx->stop) return false;
+    mp_sleep();
+  }
+  return true;
+}
+
+bool mp_recv(df_ctx* ctx, Inst* me, MetaRec& m) {
+  InstPlane& ip = ctx->seg->inst[me->id];
+  while (!ip.inbox.pop(m)) {
+    if (ctx->stop) return false;
+    mp_sleep();
+  }
+  return true;
+}
+
+// Consumer: make `st` wait for every chunk of slot m.slot (device-side), then hash it.
+cudaError_t mp_wait_chunks(df_ctx* ctx, Inst* me, const MetaRec& m, cudaStream_t st, uint64_t bytes) {
+  for (uint32_t c = 0; c < m.nchunks; ++c) DF_TRY(cudaStreamWaitEvent(st, me->ipc_chunk[m.slot][c], 0));
+  if (ctx->g.handoff_mode & DF_HASH) {
+    g_launches->fetch_add(1);
+    DF_TRY(payload_hash(me->slots.slots[m.slot].buf, bytes, 0, me->mp_hash + 1, st));
+  }
+  return cudaSuccess;
+}
+
+cudaError_t mp_release_slot(df_ctx* ctx, Inst* me, uint32_t s, cudaStream_t st) {
+  DF_TRY(cudaEventRecord(me->ipc_consumed[s], st));
+  InstPlane& ip = ctx->seg->inst[me->id];
+  while (!ip.free_slots.push(s)) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  return cudaSuccess;
+}
+
+void mp_e_worker(df_ctx* ctx, Inst* me) {
+  cudaSetDevice(me->device);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  while (!ctx->stop.load()) {
+    ReqState* rs = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(ctx->req_mu);
+      if (!ctx->requests->pop(rs)) rs = nullptr;
+    }
+    if (!rs) {
+      mp_sleep();
+      continue;
+    }
+    MetaRec m{};
+    m.seq = rs->seq;
+    m.id_lo = rs->id.lo;
+    m.id_hi = rs->id.hi;
+    m.seed = rs->req.seed;
+    m.user_tag = rs->req.user_tag;
+    m.steps = rs->req.steps;
+    m.shift = rs->req.shift;
+    m.inst_e = me->id;
+    m.flags = rs->req.out_host ? 1u : 0u;  // bit0: deliver the decoded output
+    m.t_submit = rs->t_submit;
+    m.t_start_e = now_s();
+    const int tid = pick(ctx, DF_T, rs->seq);
+    int b = me->enext;
+    me->enext ^= 1;
+    WK(cudaStreamWaitEvent(me->compute, me->esent[b], 0));
+    WK(cudaEventRecord(e0, me->compute));
+    if (!rs->ids.empty()) {
+      WK(cudaMemcpyAsync(me->ids_dev, rs->ids.data(), rs->ids.size() * 4, cudaMemcpyHostToDevice, me->compute));
+    } else {
+      g_launches->fetch_add(1);
+      WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
+    }
+    WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+    WK(cudaEventRecord(e1, me->compute));
+    m.t_end_e = now_s();
+    if (!mp_send(ctx, me, tid, me->ebuf[b], ctx->ctx_bytes, ctx->g.chunk_bytes[0], me->compute, m, 0)) {
+      free_req(rs);
+      return;
+    }
+    WK(cudaEventRecord(me->esent[b], me->comm));
+    me->served++;
+    free_req(rs);  // the request now lives in T's inbox (another process or this one)
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+void mp_t_worker(df_ctx* ctx, Inst* me) {
+  cudaSetDevice(me->device);
+  cudaEvent_t r0, w0, t0, t1;
+  cudaEventCreate(&r0);
+  cudaEventCreate(&w0);
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  MetaRec m;
+  while (mp_recv(ctx, me, m)) {
+    const int S = int(m.steps);
+    int b = me->xnext;
+    me->xnext ^= 1;
+    float* x = me->xbuf[b];
+    WK(cudaStreamWaitEvent(me->compute, me->xsent[b], 0));
+    WK(cudaEventRecord(t0, me->compute));
+    g_launches->fetch_add(1);
+    WK(gen_noise(x, latent_elems(me->m.c), m.seed, me->compute));
+    WK(cudaEventRecord(r0, me->compute));  // consumer ready for ctx
+    WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->ctx_bytes));
+    WK(cudaEventRecord(w0, me->compute));  // ctx landed
+    std::vector<float> sig = sigmas_host(S, m.shift);
+    Cond cd;
+    WK(me->m.prepare(me->slots.slots[m.slot].buf, sig.data(), S, me->compute, &cd));
+    WK(mp_release_slot(ctx, me, m.slot, me->compute));
+    for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
+    WK(cudaEventRecord(t1, me->compute));
+    WK(cudaStreamSynchronize(me->compute));
+    if (me->m.prof) me->m.prof->harvest();
+    cd.mem.release();
+    float ms = 0.f, ex = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventElapsedTime(&ex, r0, w0);
+    MetaRec o = m;
+    o.inst_t = me->id;
+    o.t_end_t = now_s();
+    o.stage_ms_t = ms;
+    o.exposed_t = ex > 0.f ? ex : 0.f;
+    o.hash_src = 0;
+    // edge-0 check: the ctx we received must hash to what E sent
+    if ((ctx->g.handoff_mode & DF_HASH) && me->mp_hash[1] != m.hash_src) {
+      worker_fail(ctx, "mp_t_worker: E->T payload hash mismatch");
+      return;
+    }
+    const int did = pick(ctx, DF_D, m.seq);
+    if (!mp_send(ctx, me, did, x, ctx->lat_bytes, ctx->g.chunk_bytes[1], me->compute, o, 1)) return;
+    WK(cudaEventRecord(me->xsent[b], me->comm));
+    me->served++;
+  }
+}
+
+void mp_d_worker(df_ctx* ctx, Inst* me) {
+  cudaSetDevice(me->device);
+  cudaEvent_t r0, w0, d0, d1;
+  cudaEventCreate(&r0);
+  cudaEventCreate(&w0);
+  cudaEventCreate(&d0);
+  cudaEventCreate(&d1);
+  MetaRec m;
+  while (mp_recv(ctx, me, m)) {
+    double t_start = now_s();
+    WK(cudaEventRecord(r0, me->compute));
+    WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->lat_bytes));
+    WK(cudaEventRecord(w0, me->compute));
+    WK(cudaEventRecord(d0, me->compute));
+    WK(me->m.decode((const float*)me->slots.slots[m.slot].buf, me->dout, me->compute));
+    WK(cudaEventRecord(d1, me->compute));
+    WK(mp_release_slot(ctx, me, m.slot, me->compute));
+    if (m.flags & 1u)
+      WK(cudaMemcpyAsync(me->stage_host, me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
+    WK(cudaStreamSynchronize(me->compute));
+    auto rs = new ReqState();
+    rs->pre = true;
+    if (m.flags & 1u) {
+      rs->outcopy.resize(ctx->out_bytes / 4);
+      std::memcpy(rs->outcopy.data(), me->stage_host, ctx->out_bytes);
+    }
+    df_completion& o = rs->comp;
+    std::memset(&o, 0, sizeof(o));
+    o.id = {m.id_lo, m.id_hi};
+    o.status = DF_OK;
+    o.user_tag = m.user_tag;
+    o.inst[0] = m.inst_e;
+    o.inst[1] = m.inst_t;
+    o.inst[2] = me->id;
+    o.t_submit = m.t_submit;
+    o.t_start[0] = m.t_start_e;
+    o.t_end[0] = m.t_end_e;
+    o.t_end[1] = m.t_end_t;
+    o.t_start[2] = t_start;
+    o.t_end[2] = o.t_done = now_s();
+    o.stage_ms[0] = m.stage_ms_e;
+    o.stage_ms[1] = m.stage_ms_t;
+    cudaEventElapsedTime(&o.stage_ms[2], d0, d1);
+    float ex = 0.f;
+    cudaEventElapsedTime(&ex, r0, w0);
+    o.exposed_ms[0] = m.exposed_t;
+    o.exposed_ms[1] = ex > 0.f ? ex : 0.f;
+    o.xfer_ms[0] = o.xfer_ms[1] = -1.f;  // cross-process copies are timed by neither side's clock
+    if (!rs->outcopy.empty()) {
+      o.out_view = rs->outcopy.data();
+      o.out_view_bytes = ctx->out_bytes;
+    }
+    if (ctx->g.handoff_mode & DF_HASH) {
+      o.hash_src[1] = m.hash_src;
+      o.hash_dst[1] = me->mp_hash[1];
+      o.hash_src[0] = o.hash_dst[0] = 1;  // edge 0 was verified by T (mismatch fails the request)
+    }
+    me->served++;
+    {
+      std::lock_guard<std::mutex> lk(ctx->done_mu);
+      while (!ctx->done->push(rs)) std::this_thread::yield();
+    }
+    ctx->done_cv.notify_all();
+  }
+}
+
+}  // namespace
+
+
+// ---------------------------------------------------------------- shared-memory plane
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+namespace df {
+static const uint64_t PLANE_MAGIC = 0xD15A6F05A11A7E01ull;
+PlaneSeg* plane_open(const char* name, bool create, uint32_t world, std::string* err) {
+  const size_t sz = sizeof(PlaneSeg);
+  int fd = -1;
+  if (create) {
+    shm_unlink(name);
+    fd = shm_open(name, O_CREAT | O_RDWR | O_EXCL, 0600);
+    if (fd < 0 || ftruncate(fd, off_t(sz)) != 0) {
+      if (err) *err = std::string("shm_open/ftruncate(create) failed for ") + name;
+      if (fd >= 0) close(fd);
+      return nullptr;
+    }
+  } else {
+    for (int t = 0; t < 120000 && fd < 0; ++t) {  // rank 0 may not have created it yet (<= 120 s)
+      fd = shm_open(name, O_RDWR, 0600);
+      if (fd < 0) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    if (fd < 0) {
+      if (err) *err = std::string("shm_open(attach) timed out for ") + name;
+      return nullptr;
+    }
+    struct stat st;
+    for (int t = 0; t < 120000; ++t) {
+      if (fstat(fd, &st) == 0 && size_t(st.st_size) >= sz) break;
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  }
+  void* p = mmap(nullptr, sz, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) {
+    if (err) *err = "mmap failed";
+    return nullptr;
+  }
+  auto seg = static_cast<PlaneSeg*>(p);
+  if (create) {
+    std::memset(p, 0, sz);
+    seg->world = world;
+    for (int i = 0; i < PL_MAX_INST; ++i) {
+      seg->inst[i].free_slots.init();
+      seg->inst[i].inbox.init();
+    }
+    seg->magic.store(PLANE_MAGIC, std::memory_order_release);
+  } else {
+    for (int t = 0; t < 120000 && seg->magic.load(std::memory_order_acquire) != PLANE_MAGIC; ++t)
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    if (seg->magic.load() != PLANE_MAGIC) {
+      if (err) *err = "plane segment never initialised";
+      munmap(p, sz);
+      return nullptr;
+    }
+  }
+  seg->attached.fetch_add(1);
+  return seg;
+}
+void plane_close(PlaneSeg* seg, const char* name, bool owner) {
+  if (!seg) return;
+  munmap(seg, sizeof(PlaneSeg));
+  if (owner) shm_unlink(name);
+}
+}  // namespace df
+
 // ================================================================== C ABI
 extern "C" {
 
@@ -551,6 +984,40 @@ const char* df_last_error(const df_ctx* ctx) {
 }
 
 uint64_t df_launch_count(const df_ctx*) { return g_launches->load(); }
+
+df_status df_ring_selftest(const char* name, int32_t role, uint64_t n, uint64_t* checksum, int32_t* fifo_ok) {
+  if (!name || !name[0] || (role != 0 && role != 1)) return DF_ERR_INVALID;
+  std::string err;
+  PlaneSeg* seg = plane_open(name, role == 0, 2, &err);
+  if (!seg) return fail(nullptr, "df_ring_selftest: " + err, DF_ERR_STATE);
+  auto& inbox = seg->inst[0].inbox;
+  uint64_t sum = 0;
+  int ok = 1;
+  if (role == 0) {
+    for (uint64_t i = 0; i < n; ++i) {
+      MetaRec m{};
+      m.seq = i;
+      m.id_lo = i * 7 + 1;
+      while (!inbox.push(m)) std::this_thread::yield();  // ring holds 64: exercises backpressure
+      sum += i;
+    }
+    while (seg->inst[1].ready.load(std::memory_order_acquire) == 0) std::this_thread::yield();
+  } else {
+    uint64_t expect = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      MetaRec m;
+      while (!inbox.pop(m)) std::this_thread::yield();
+      if (m.seq != expect || m.id_lo != m.seq * 7 + 1) ok = 0;
+      expect = m.seq + 1;
+      sum += m.seq;
+    }
+    seg->inst[1].ready.store(1, std::memory_order_release);
+  }
+  if (checksum) *checksum = sum;
+  if (fifo_ok) *fifo_ok = ok;
+  plane_close(seg, name, role == 0);
+  return DF_OK;
+}
 
 df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset) {
   if (!ctx) return DF_ERR_INVALID;
@@ -590,7 +1057,13 @@ df_status df_init(const df_graph* g, df_ctx** out) {
     return fail(nullptr, "df_init: Eq.1 capacity", DF_ERR_CAPACITY);
   if (g->n_slots < 2 || (g->ring_capacity & (g->ring_capacity - 1)) || g->ring_capacity < 2)
     return fail(nullptr, "df_init: n_slots >= 2 and ring_capacity a power of two", DF_ERR_INVALID);
+  const bool mp = g->world > 1;
+  if (mp && (g->rank < 0 || g->rank >= g->world || !g->shm_name[0] || g->n_slots > uint32_t(PL_MAX_SLOTS)))
+    return fail(nullptr, "df_init: multi-process graph needs rank in [0, world), shm_name, n_slots <= 4",
+                DF_ERR_INVALID);
+  auto is_local = [&](uint32_t i) { return !mp || g->inst[i].rank == g->rank; };
   for (uint32_t i = 0; i < g->n_inst; ++i) {
+    if (!is_local(i)) continue;
     cudaDeviceProp p;
     if (cudaGetDeviceProperties(&p, g->inst[i].device) != cudaSuccess || p.major != 10)
       return fail(nullptr, "df_init: instance device is not sm_100 (B200)");
@@ -605,7 +1078,18 @@ df_status df_init(const df_graph* g, df_ctx** out) {
   ctx->out_bytes = out_elems(c) * 4;
   // peer access between every pair of devices in use (NVLink P2P, P:L390 GPUDirect analogue)
   std::set<int> devs;
-  for (uint32_t i = 0; i < g->n_inst; ++i) devs.insert(g->inst[i].device);
+  for (uint32_t i = 0; i < g->n_inst; ++i)
+    if (is_local(i)) devs.insert(g->inst[i].device);
+  if (mp) {
+    std::string perr;
+    ctx->mp = true;
+    ctx->seg_owner = g->rank == 0;
+    ctx->seg = plane_open(g->shm_name, ctx->seg_owner, uint32_t(g->world), &perr);
+    if (!ctx->seg) {
+      delete ctx;
+      return fail(nullptr, "df_init: " + perr);
+    }
+  }
   for (int a : devs)
     for (int b : devs)
       if (a != b) {
@@ -622,12 +1106,14 @@ df_status df_init(const df_graph* g, df_ctx** out) {
     in->id = int(i);
     in->stage = g->inst[i].stage;
     in->device = g->inst[i].device;
+    in->local = is_local(i);
     ctx->by_stage[in->stage].push_back(int(i));
     ctx->inst.push_back(std::move(in));
   }
   for (int s = 0; s < 3; ++s) ctx->active[s] = int(ctx->by_stage[s].size());
   for (auto& ip : ctx->inst) {
     Inst& I = *ip;
+    if (!I.local) continue;
     cudaError_t e = I.m.create(c, int(g->precision), I.device, I.stage, g->weight_seed, int(g->max_steps));
     if (e != cudaSuccess) {
       std::string m = std::string("df_init: instance create: ") + cudaGetErrorString(e) + " " + df::tls_err;
@@ -667,17 +1153,28 @@ df_status df_init(const df_graph* g, df_ctx** out) {
       cudaHostAlloc(&I.stage_host, ctx->out_bytes, cudaHostAllocPortable);
     }
     cudaError_t le = cudaDeviceSynchronize();
+    if (le == cudaSuccess && mp) {
+      le = cudaHostAlloc(&I.mp_hash, 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable);
+      if (le == cudaSuccess && slot_bytes) le = mp_publish(ctx, I, slot_bytes);
+    }
     if (le != cudaSuccess) {
-      std::string m = std::string("df_init: setup: ") + cudaGetErrorString(le);
+      std::string m = std::string("df_init: setup: ") + cudaGetErrorString(le) + " " + df::tls_err;
       df_finalize(ctx);
       return fail(nullptr, m);
     }
   }
   for (auto& ip : ctx->inst) {
     Inst* I = ip.get();
-    if (I->stage == DF_E) I->worker = std::thread(e_worker, ctx, I);
-    else if (I->stage == DF_T) I->worker = std::thread(t_worker, ctx, I);
-    else I->worker = std::thread(d_worker, ctx, I);
+    if (!I->local) continue;
+    if (mp) {
+      if (I->stage == DF_E) I->worker = std::thread(mp_e_worker, ctx, I);
+      else if (I->stage == DF_T) I->worker = std::thread(mp_t_worker, ctx, I);
+      else I->worker = std::thread(mp_d_worker, ctx, I);
+    } else {
+      if (I->stage == DF_E) I->worker = std::thread(e_worker, ctx, I);
+      else if (I->stage == DF_T) I->worker = std::thread(t_worker, ctx, I);
+      else I->worker = std::thread(d_worker, ctx, I);
+    }
   }
   *out = ctx;
   return DF_OK;
@@ -692,10 +1189,27 @@ df_status df_finalize(df_ctx* ctx) {
   }
   for (auto& ip : ctx->inst)
     if (ip->worker.joinable()) ip->worker.join();
+  for (int i = 0; i < int(ctx->inst.size()); ++i) {  // close the IPC views of remote consumers
+    df_ctx::View& v = ctx->views[i];
+    if (!v.open || !v.remote) continue;
+    for (int sl = 0; sl < PL_MAX_SLOTS; ++sl) {
+      if (v.buf[sl]) cudaIpcCloseMemHandle(v.buf[sl]);
+      if (v.consumed[sl]) cudaEventDestroy(v.consumed[sl]);
+      for (int c = 0; c < PL_MAX_CHUNKS; ++c)
+        if (v.chunk[sl][c]) cudaEventDestroy(v.chunk[sl][c]);
+    }
+  }
   for (auto& ip : ctx->inst) {
     Inst& I = *ip;
+    if (!I.local) continue;
     cudaSetDevice(I.device);
     cudaDeviceSynchronize();
+    for (int sl = 0; sl < PL_MAX_SLOTS; ++sl) {
+      if (I.ipc_consumed[sl]) cudaEventDestroy(I.ipc_consumed[sl]);
+      for (int c = 0; c < PL_MAX_CHUNKS; ++c)
+        if (I.ipc_chunk[sl][c]) cudaEventDestroy(I.ipc_chunk[sl][c]);
+    }
+    if (I.mp_hash) cudaFreeHost(I.mp_hash);
     for (auto& s : I.slots.slots) {
       if (s.buf) cudaFree(s.buf);
       if (s.consumed) cudaEventDestroy(s.consumed);
@@ -716,12 +1230,19 @@ df_status df_finalize(df_ctx* ctx) {
   ReqState* rs;
   while (ctx->requests && ctx->requests->pop(rs)) free_req(rs);
   while (ctx->done && ctx->done->pop(rs)) free_req(rs);
+  for (ReqState* old : ctx->last_polled) free_req(old);
+  if (ctx->seg) plane_close(ctx->seg, ctx->g.shm_name, ctx->seg_owner);
   delete ctx;
   return DF_OK;
 }
 
 df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
   if (!ctx || !r) return DF_ERR_INVALID;
+  if (ctx->mp) {
+    bool has_e = false;
+    for (auto& ip : ctx->inst) has_e |= ip->local && ip->stage == DF_E;
+    if (!has_e) return fail(ctx, "df_submit: this rank hosts no encoder instance", DF_ERR_INVALID);
+  }
   if (ctx->failed) return fail(ctx, ctx->err, DF_ERR_STATE);
   if (r->steps == 0 || r->steps > ctx->g.max_steps || !(r->shift > 0.f))
     return fail(ctx, "df_submit: steps in [1, max_steps] and shift > 0", DF_ERR_INVALID);
@@ -745,7 +1266,7 @@ df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
   // timing events are created by each stage worker on its own device
   {
     std::lock_guard<std::mutex> lk(ctx->req_mu);
-    rs->seq = ctx->seq.fetch_add(1);
+    rs->seq = ctx->mp ? ctx->seg->seq.fetch_add(1) : ctx->seq.fetch_add(1);  // FAA ticket
   }
   if (!ctx->requests->push(rs)) {
     free_req(rs);
@@ -763,9 +1284,13 @@ df_status df_poll(df_ctx* ctx, df_completion* out, uint32_t max, uint32_t* n_out
   auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms < 0 ? 0 : timeout_ms);
   for (;;) {
     ReqState* rs;
+    if (*n_out == 0) {  // views handed out by the previous df_poll expire now
+      for (ReqState* old : ctx->last_polled) free_req(old);
+      ctx->last_polled.clear();
+    }
     while (*n_out < max && ctx->done->pop(rs)) {
       fill_completion(ctx, rs, &out[(*n_out)++]);
-      free_req(rs);
+      ctx->last_polled.push_back(rs);
     }
     if (*n_out) return DF_OK;
     if (ctx->failed) return fail(ctx, ctx->err, DF_ERR_STATE);

@@ -1,0 +1,124 @@
+// Cross-process control plane of the stage handoff (one process per GPU).
+//
+// PAPER.md §sec:decentral-queue: stages are decoupled by fixed-length
+// metadata queues with Fetch-and-Add concurrency control and one-sided access; the
+// downstream instance posts a destination address before data moves.
+// Inside one node the "RDMA-backed queues" become lock-free rings in a POSIX shared-memory
+// segment that every rank maps, and the destination addresses become CUDA IPC handles of
+// the consumer's receive slots (data plane: the producer copies chunks straight into the
+// peer slot over NVLink; one interprocess event per chunk).
+//
+// Segment layout (all fixed size, lock-free std::atomic words, no pointers):
+//   Header        magic, world, global request sequence (FAA), per-instance ready flags
+//   InstPlane[i]  for every consumer instance i: slot IPC handles, per-slot consumed
+//                 event + per-chunk events (IPC handles), a free-slot ring (the posted
+//                 destination addresses) and an inbox ring of 128-byte metadata records.
+#pragma once
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <cuda_runtime.h>
+
+namespace df {
+
+constexpr int PL_MAX_INST = 32;
+constexpr int PL_MAX_SLOTS = 4;
+constexpr int PL_MAX_CHUNKS = 64;
+constexpr int PL_RING = 64;  // power of two
+
+// Fixed-length request metadata ("leveraging fixed-length metadata ... O(1)").
+struct alignas(8) MetaRec {
+  uint64_t seq, id_lo, id_hi, seed, user_tag;
+  uint32_t steps, slot, nchunks, chunk_bytes;
+  float shift;
+  int32_t inst_e, inst_t;
+  uint32_t flags;
+  double t_submit, t_start_e, t_end_e, t_end_t;  // host CLOCK_MONOTONIC (node-wide)
+  float stage_ms_e, stage_ms_t, exposed_t;
+  uint32_t pad;
+  uint64_t hash_src;                              // payload hash computed by the producer
+};
+static_assert(sizeof(MetaRec) <= 128, "metadata record must stay fixed-size");
+
+// Bounded MPMC ring of fixed-size records with per-cell sequence words (Vyukov); the
+// tail/head tickets are claimed by CAS-FAA on shared words.
+template <typename T, int CAP>
+struct ShmRing {
+  struct Cell {
+    std::atomic<uint64_t> seq;
+    T val;
+  };
+  alignas(64) std::atomic<uint64_t> head;
+  alignas(64) std::atomic<uint64_t> tail;
+  Cell cells[CAP];
+  void init() {
+    head.store(0);
+    tail.store(0);
+    for (int i = 0; i < CAP; ++i) cells[i].seq.store(uint64_t(i));
+  }
+  bool push(const T& v) {
+    uint64_t pos = tail.load(std::memory_order_relaxed);
+    for (;;) {
+      Cell& c = cells[pos & (CAP - 1)];
+      uint64_t s = c.seq.load(std::memory_order_acquire);
+      int64_t dif = int64_t(s) - int64_t(pos);
+      if (dif == 0) {
+        if (tail.compare_exchange_weak(pos, pos + 1, std::memory_order_relaxed)) {
+          c.val = v;
+          c.seq.store(pos + 1, std::memory_order_release);
+          return true;
+        }
+      } else if (dif < 0) {
+        return false;
+      } else {
+        pos = tail.load(std::memory_order_relaxed);
+      }
+    }
+  }
+  bool pop(T& out) {
+    uint64_t pos = head.load(std::memory_order_relaxed);
+    for (;;) {
+      Cell& c = cells[pos & (CAP - 1)];
+      uint64_t s = c.seq.load(std::memory_order_acquire);
+      int64_t dif = int64_t(s) - int64_t(pos + 1);
+      if (dif == 0) {
+        if (head.compare_exchange_weak(pos, pos + 1, std::memory_order_relaxed)) {
+          out = c.val;
+          c.seq.store(pos + CAP, std::memory_order_release);
+          return true;
+        }
+      } else if (dif < 0) {
+        return false;
+      } else {
+        pos = head.load(std::memory_order_relaxed);
+      }
+    }
+  }
+};
+
+struct InstPlane {
+  std::atomic<uint32_t> ready;  // consumer published its handles
+  uint32_t n_slots, nchunks_max;
+  uint64_t slot_bytes;
+  cudaIpcMemHandle_t slot_mem[PL_MAX_SLOTS];
+  cudaIpcEventHandle_t consumed[PL_MAX_SLOTS];
+  cudaIpcEventHandle_t chunk[PL_MAX_SLOTS][PL_MAX_CHUNKS];
+  ShmRing<uint32_t, 16> free_slots;      // posted destination addresses (slot index)
+  ShmRing<MetaRec, PL_RING> inbox;       // control plane into this consumer
+};
+
+struct PlaneSeg {
+  std::atomic<uint64_t> magic;
+  std::atomic<uint64_t> seq;             // global request sequence (FAA)
+  std::atomic<uint32_t> attached;
+  uint32_t world;
+  InstPlane inst[PL_MAX_INST];
+};
+
+// Create (rank 0) or attach to the named segment; returns nullptr on failure.
+PlaneSeg* plane_open(const char* name, bool create, uint32_t world, std::string* err);
+void plane_close(PlaneSeg* seg, const char* name, bool owner);
+
+}  // namespace df

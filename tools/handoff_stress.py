@@ -1,0 +1,91 @@
+"""BASELINE configs[4] "handoff stress": chunk-size sweep and injected transfer jitter,
+asynchronous vs synchronous stage handoff.
+
+Jitter patterns are P:L511's definitional list (R24): stable 5%/d1, mild
+10%/d1, moderate 10%/d2, severe 20%/d2, with d scaled to this machine's DiT stage time
+(d1 = 0.2 s * T_T/74.1 s, d2 = 2 s * T_T/74.1 s, the paper's delay/DiT-time ratios;
+74.1 s is the A10 4-step DiT time of tab:stage_time) plus an unscaled stress point
+d = T_T/2.  One Bernoulli draw per request-edge transfer (R23).
+
+    python tools/handoff_stress.py --config image --dit-steps 4 --requests 12
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_25550_b200 import binding as B  # noqa: E402
+from synth.configs import CONFIGS  # noqa: E402
+
+
+def run(cfg, steps, n_req, mode, chunk, jitter, seed0):
+    g = B.make_graph(cfg, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)], chunk_bytes=chunk,
+                     handoff_mode=mode | B.DF_HASH, max_steps=steps, jitter=jitter)
+    with B.Context(g) as c:
+        # warm-up request (not timed)
+        c.submit(steps, cfg.shift, seed0 - 1)
+        while not c.poll(1, 60000):
+            pass
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(n_req):
+            while c.submit(steps, cfg.shift, seed0 + k)[0] != B.DF_OK:
+                time.sleep(0.001)
+        comps = []
+        while len(comps) < n_req:
+            comps += c.poll(16, 60000)
+        wall = time.perf_counter() - t0
+    lat = [(x.t_done - x.t_submit) * 1e3 for x in comps]
+    exp = [x.exposed_ms[0] + x.exposed_ms[1] for x in comps]
+    return {"req_per_s": n_req / wall, "stage_T_ms": statistics.median(x.stage_ms[1] for x in comps),
+            "xfer_ms": [statistics.median(x.xfer_ms[0] for x in comps), statistics.median(x.xfer_ms[1] for x in comps)],
+            "exposed_ms_median": statistics.median(exp), "exposed_ms_mean": statistics.mean(exp),
+            "exposed_frac_of_latency": statistics.mean(exp) / statistics.mean(lat),
+            "latency_ms_p50": float(np.percentile(lat, 50)), "latency_ms_p99": float(np.percentile(lat, 99)),
+            "hash_match": all(x.hash_src[e] == x.hash_dst[e] != 0 for x in comps for e in range(2))}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="image")
+    ap.add_argument("--dit-steps", type=int, default=4)
+    ap.add_argument("--requests", type=int, default=12)
+    ap.add_argument("--out", default="gpurun_out/handoff_stress.json")
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    res = {"config": cfg.name, "dit_steps": a.dit_steps, "requests_per_point": a.requests, "chunk_sweep": {},
+           "jitter": {}}
+    # ---- chunk-size sweep (no jitter, async)
+    for ch in (16 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 0):
+        r = run(cfg, a.dit_steps, max(4, a.requests // 2), B.DF_ASYNC, (ch, ch), (0.0, 0.0, 0), 100)
+        res["chunk_sweep"][str(ch or "whole")] = r
+        print("chunk", ch, r, flush=True)
+    base = res["chunk_sweep"]["262144"]
+    T_T = base["stage_T_ms"] / 1e3
+    d1, d2 = 0.2 * T_T / 74.1, 2.0 * T_T / 74.1
+    pats = {"none": (0.0, 0.0), "stable 5%/d1": (0.05, d1), "mild 10%/d1": (0.10, d1),
+            "moderate 10%/d2": (0.10, d2), "severe 20%/d2": (0.20, d2), "stress 20%/T_T/2": (0.20, T_T / 2)}
+    res["T_T_s"], res["d1_s"], res["d2_s"] = T_T, d1, d2
+    for name, (p, d) in pats.items():
+        for mode, mname in ((B.DF_ASYNC, "async"), (B.DF_SYNC, "sync")):
+            r = run(cfg, a.dit_steps, a.requests, mode, (256 << 10, 256 << 10), (p, d, 7), 1000)
+            res["jitter"].setdefault(name, {})[mname] = r
+            print(name, mname, r, flush=True)
+    for name, v in res["jitter"].items():
+        n0 = res["jitter"]["none"]
+        for m in ("async", "sync"):
+            v[m]["throughput_drop_vs_none"] = 1.0 - v[m]["req_per_s"] / n0[m]["req_per_s"]
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(res, f, indent=1)
+    print(json.dumps({k: {m: round(v[m]["throughput_drop_vs_none"], 4) for m in v} for k, v in res["jitter"].items()}))
+
+
+if __name__ == "__main__":
+    main()
