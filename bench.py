@@ -9,9 +9,12 @@ configs[1] workload: text-to-image 1024x1024 -> 4096 latent tokens, DiT hidden 3
 layers, 28 steps, bf16, random-init weights, synthetic requests.
 
 N=1: E, T and D co-resident on GPU 0 (layout 1:1:1), requests pipelined through the async
-handoff.  N>1 (torchrun, one process per GPU): every rank runs a co-located 1:1:1 pipeline
-on its own GPU over its own request stream (requests are independent units; no
-data-path collective) -> "scaling": "weak".
+handoff.  N>1 (torchrun, one process per GPU): stage-partitioned, E on GPU 0, D on GPU N-1
+and a DiT instance on every GPU (1:N:1; --exclusive gives E and D GPUs of their own, the
+paper's 1:6:1 at N=8); requests cross GPUs through the asynchronous chunked handoff
+(shared-memory FAA metadata rings + CUDA IPC receive slots, copies over NVLink).  K
+requests per DiT instance -> "scaling": "weak".  The process group (NCCL; gloo with
+DF_BENCH_BACKEND=gloo) is plumbing only: barriers and the max-over-ranks reduction.
 
 Prints ONE JSON line (rank 0).  --impl reference times the fp64 CPU oracle (the
 reference arm for this tier) on a bounded sample of the same workload.
@@ -177,54 +180,81 @@ def run_ours(args, cfg):
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2605_25550_b200 import binding as B
+    from paper_2605_25550_b200 import binding as B, layouts
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("DF_BENCH_DEVICE", local))  # tests: several ranks on one GPU
+    backend = os.environ.get("DF_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        if backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, init_method="env://")
     torch.cuda.set_device(local)
-    dev = local
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     peaks = load_peaks()
 
-    inst = [(dev, B.DF_E), (dev, B.DF_T), (dev, B.DF_D)]
+    # Layout: N = 1 -> E+T+D on GPU 0; N > 1 -> one process per GPU, a DiT
+    # instance on every GPU, E on GPU 0 and D on GPU N-1 (E:T:D = 1:N:1), requests cross
+    # GPUs through the async chunked handoff (shared-memory rings + CUDA IPC over NVLink).
+    inst = [(local if i[2] == rank else 0, i[1], i[2]) for i in layouts.partitioned(world, args.exclusive)]
+    shm = f"/df_bench_{os.environ.get('MASTER_PORT', '0')}_{os.getuid()}"
     g = B.make_graph(cfg, inst, precision=B.DF_BF16, weight_seed=0,
                      chunk_bytes=(args.chunk_ctx, args.chunk_lat), n_slots=2,
-                     handoff_mode=B.DF_ASYNC | B.DF_HASH, ring_capacity=256, max_steps=cfg.steps)
+                     handoff_mode=B.DF_ASYNC | B.DF_HASH, ring_capacity=256, max_steps=cfg.steps,
+                     rank=rank, world=world, shm_name=shm if world > 1 else "")
     ctx = B.Context(g)
     stream = torch.cuda.current_stream()
+    e_rank, d_rank = layouts.ranks_of(inst, B.DF_E)[0], layouts.ranks_of(inst, B.DF_D)[0]
+    n_t = layouts.ratio(inst)[1]
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
-    def run_batch(n, seed0, out_bufs=None, ids=None):
-        comps = []
-        for k in range(n):
-            ob = out_bufs[k] if out_bufs is not None else None
-            while True:
-                st, _ = ctx.submit(cfg.steps, cfg.shift, seed0 + k, out_host=ob,
-                                   token_ids=ids[k] if ids is not None else None, user_tag=seed0 + k)
-                if st == B.DF_OK:
-                    break
-                comps += ctx.poll(16, timeout_ms=10)
-        while len(comps) < n:
-            comps += ctx.poll(16, timeout_ms=1000)
+    def run_batch(n, seed0, with_host_io=False):
+        """Submit n requests on the E rank; collect n completions on the D rank."""
+        comps, outs = [], []
+        if rank == e_rank:
+            rng = np.random.default_rng(seed0)
+            dummy = np.empty(cfg.out_shape, np.float32) if with_host_io else None
+            for k in range(n):
+                ids = rng.integers(0, cfg.vocab, cfg.L_txt, dtype=np.int32) if with_host_io else None
+                while True:
+                    st, _ = ctx.submit(cfg.steps, cfg.shift, seed0 + k, out_host=dummy, token_ids=ids,
+                                       user_tag=seed0 + k)
+                    if st == B.DF_OK:
+                        break
+                    if rank == d_rank:
+                        comps += ctx.poll(16, timeout_ms=5)
+                    else:
+                        time.sleep(0.002)
+        if rank == d_rank:
+            while len(comps) < n:
+                got = ctx.poll(16, timeout_ms=1000)
+                if with_host_io:  # the decoded images are host-resident on this rank
+                    for x in got:
+                        outs.append(np.ctypeslib.as_array(
+                            (np.ctypeslib.ctypes.c_float * (x.out_view_bytes // 4)).from_address(x.out_view)).sum())
+                comps += got
         return comps
 
-    # warm-up
-    run_batch(args.warmup, 1000 + rank * 100000)
+    n_total = args.steps * n_t          # weak scaling: K requests per DiT instance
+    run_batch(args.warmup * n_t, 1000)
     barrier()
-    # ---- timed region (device-resident inputs: tokens/noise from seeds on device)
+    # ---- timed region (inputs device-resident: tokens and noise from seeds on the device)
     ctx.profile(True, True)
     l0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(dev) as clk:
+    with Clocks(local) as clk:
         barrier()
         ev0.record(stream)
-        comps = run_batch(args.steps, 2000 + rank * 100000)
+        comps = run_batch(n_total, 2000)
+        if world > 1:
+            dist.barrier()  # the D rank's completion of the last request ends the region
         ev1.record(stream)
         ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -233,50 +263,59 @@ def run_ours(args, cfg):
     ctx.profile(False, False)
     # ---- e2e: host token ids in, host images out, through the public API
     out_bytes = int(np.prod(cfg.out_shape)) * 4
-    outs = [np.empty(cfg.out_shape, np.float32) for _ in range(args.steps)]
-    rng = np.random.default_rng(rank)
-    ids = [rng.integers(0, cfg.vocab, cfg.L_txt, dtype=np.int32) for _ in range(args.steps)]
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    ecomps = run_batch(args.steps, 3000 + rank * 100000, out_bufs=outs, ids=ids)
+    ecomps = run_batch(n_total, 3000, with_host_io=True)
+    if world > 1:
+        dist.barrier()
     e1.record(stream)
     e1.synchronize()
     ems = e0.elapsed_time(e1)
 
-    # ---- max over ranks
-    t = torch.tensor([ms, ems], device="cuda", dtype=torch.float64)
+    # ---- max over ranks; completions live on the D rank
+    t = torch.tensor([ms, ems], device=red_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, ems = float(t[0]), float(t[1])
-    total = args.steps * world
-    value = total / (ms / 1000.0)
-    e2e = total / (ems / 1000.0)
-
-    # ---- per-request accounting
-    t_ms = [c.stage_ms[1] for c in comps]
-    lat = [(c.t_done - c.t_submit) * 1000.0 for c in comps]
-    exposed = [c.exposed_ms[0] + c.exposed_ms[1] for c in comps]
-    xfer = [(c.xfer_ms[0], c.xfer_ms[1]) for c in comps]
-    hash_ok = all(c.hash_src[e] == c.hash_dst[e] != 0 for c in comps + ecomps for e in range(2))
+    launches_t = torch.tensor([launches], device=red_dev, dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(launches_t)
+    summary = None
+    if rank == d_rank:
+        lat = [(c.t_done - c.t_submit) * 1000.0 for c in comps]
+        exposed = [c.exposed_ms[0] + c.exposed_ms[1] for c in comps]
+        summary = {
+            "t_ms": statistics.median(c.stage_ms[1] for c in comps),
+            "lat": statistics.median(lat), "exp_med": statistics.median(exposed), "exp_max": max(exposed),
+            "exp_frac": statistics.median(exposed) / statistics.median(lat),
+            "xfer": [statistics.median(c.xfer_ms[0] for c in comps), statistics.median(c.xfer_ms[1] for c in comps)],
+            "hash_ok": all(c.hash_src[e] == c.hash_dst[e] != 0 for c in comps + ecomps for e in range(2)),
+            "n": len(comps), "t_inst": sorted({int(c.inst[1]) for c in comps})}
+    if world > 1:
+        objs = [None] * world
+        dist.all_gather_object(objs, summary)
+        summary = objs[d_rank]
+    value = n_total / (ms / 1000.0)
+    e2e = n_total / (ems / 1000.0)
     dit_tflop = cfg.flops_per_request() / 1e12
-    dit_tflops = dit_tflop / (statistics.median(t_ms) / 1000.0)
-    # ---- roofline of the dominant kernel class (largest share of measured kernel time)
+    dit_tflops = dit_tflop / (summary["t_ms"] / 1000.0)
+    # ---- roofline of the dominant kernel class (this rank's DiT instance, timed live)
     dom = max(kstats, key=lambda k: kstats[k]["ms"])
     ks = kstats[dom]
     avg_ms = ks["ms"] / max(ks["launches"], 1)
     if ks["flops"] > 0:
         ach = (ks["flops"] / ks["launches"]) / (avg_ms / 1000.0) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
-                "frac": ach / peaks["bf16_sus"], "traffic": None, "kernel": dom,
+                "frac": ach / peaks["bf16_sus"], "traffic": args.traffic, "kernel": dom,
                 "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
                 "peak_note": f"{peaks['src']} sustained cuBLAS bf16 (kernel timed inside a long step)"}
     else:
         ach = (ks["bytes"] / ks["launches"]) / (avg_ms / 1000.0) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
-                "traffic": None, "kernel": dom, "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
+                "traffic": args.traffic, "kernel": dom, "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
                 "peak_note": f"{peaks['src']} HBM copy"}
-    tot_kms = sum(v["ms"] for v in kstats.values())
+    tot_kms = sum(v["ms"] for v in kstats.values()) or 1.0
     shares = {k: round(v["ms"] / tot_kms, 4) for k, v in kstats.items() if v["ms"] > 0}
     tput_kind = {k: round((v["flops"] / v["ms"] / 1e9), 1) for k, v in kstats.items() if v["ms"] > 0 and v["flops"] > 0}
 
@@ -290,27 +329,32 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         s = oracle_sample(cfg)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "oracle", "sample": s["sample"]}
+    gE, gT, gD = layouts.ratio(inst)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / n_total, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "layout": f"E+T+D co-resident per GPU (E:T:D = {world}:{world}:{world})",
-                   "requests_per_rank": args.steps, "steps_per_request": cfg.steps,
-                   "chunk_bytes": [args.chunk_ctx, args.chunk_lat],
+        "config": {"workload": workload_name(cfg),
+                   "layout": ("E+T+D co-resident on GPU 0" if world == 1 else
+                              f"stage-partitioned, one process per GPU: E on GPU 0, D on GPU {world - 1}, "
+                              f"a DiT instance on {'every' if not args.exclusive else 'each other'} GPU; "
+                              "cross-GPU handoff via shared-memory FAA rings + CUDA IPC slots"),
+                   "E:T:D": f"{gE}:{gT}:{gD}", "requests": n_total, "requests_per_dit_instance": args.steps,
+                   "steps_per_request": cfg.steps, "chunk_bytes": [args.chunk_ctx, args.chunk_lat],
                    "l2": "inputs larger than L2: the DiT streams 8.5 GB of weights per denoising step"
                          if cfg.name == "image" else "weights per step exceed L2"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": cfg.L_txt * 4, "d2h_bytes_per_step": out_bytes},
-        "gpu_launches": launches,
+        "gpu_launches": int(launches_t.item()),
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        "dit_step": {"tflop_per_request": dit_tflop, "t_stage_ms_median": statistics.median(t_ms),
+        "dit_step": {"tflop_per_request": dit_tflop, "t_stage_ms_median": summary["t_ms"],
                      "achieved_tflops": dit_tflops, "frac_of_sustained_peak": dit_tflops / peaks["bf16_sus"],
                      "frac_of_burst_peak": dit_tflops / peaks["bf16"]},
-        "handoff": {"exposed_ms_median": statistics.median(exposed), "exposed_ms_max": max(exposed),
-                    "exposed_frac_of_latency": statistics.median(exposed) / statistics.median(lat),
-                    "xfer_ms_median": [statistics.median(x[0] for x in xfer), statistics.median(x[1] for x in xfer)],
-                    "latency_ms_median": statistics.median(lat), "hash_match": hash_ok},
+        "handoff": {"exposed_ms_median": summary["exp_med"], "exposed_ms_max": summary["exp_max"],
+                    "exposed_frac_of_latency": summary["exp_frac"], "xfer_ms_median": summary["xfer"],
+                    "latency_ms_median": summary["lat"], "hash_match": summary["hash_ok"],
+                    "dit_instances_used": summary["t_inst"]},
         "kernel_time_share": shares,
         "kernel_gflops": tput_kind,
     }
@@ -331,6 +375,9 @@ def main():
     ap.add_argument("--chunk-ctx", type=int, default=512 * 1024)
     ap.add_argument("--chunk-lat", type=int, default=256 * 1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exclusive", action="store_true", help="N>1: E and D on GPUs of their own (1:N-2:1)")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
