@@ -210,6 +210,35 @@ df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset);
 df_status df_kernel_stats(df_ctx* ctx, uint32_t kind, uint64_t* launches, double* total_ms, double* flops,
                           double* bytes);
 
+/* ------------------------------------------------------------------ hybrid instance scheduler
+ * Alg. 1 (§sec:hybrid-scheduling): every delta seconds collect per-stage
+ * metrics m = {u_s, q_s, d_s}; if the workload changed (modal request key of the recent
+ * 25% of the history differs from the rest) apply the predicted ratio (the Eq. 6 planner
+ * over measured stage times) and skip the reactive rule; otherwise scale
+ * service s out iff u_s > U_high and q_s > Q_high and d_s rises, in iff u_s < U_low and
+ * q_s = 0.  Defaults: delta 2 s, U_high 0.8, Q_high 5, U_low 0.2. */
+typedef struct { float delta_s, U_high, U_low; uint32_t Q_high; int32_t move_budget; uint32_t G; } df_sched_cfg;
+typedef struct { float u[3]; uint32_t q[3]; float d[3]; } df_sched_metrics;
+typedef struct {
+  double t;                     /* host monotonic seconds                              */
+  int32_t action;               /* 0 none, 1 scale-out, 2 scale-in, 3 reconfigure       */
+  int32_t stage;                /* for 1/2                                              */
+  uint32_t g[3];                /* allocation after the decision                        */
+  df_sched_metrics m;
+} df_sched_event;
+/* Pure functions (no GPU, no context): the Eq. 6 planner (exhaustive; cur/budget limit
+ * the L1 instance moves from cur, budget < 0 = unlimited; ties -> fewer GPUs, then
+ * larger g_T, then larger g_D), Alg. 1's reactive rule per stage (out[s] in {-1,0,+1};
+ * prev NULL = first tick), and the workload-change detector. */
+df_status df_plan_ratio(uint32_t G, const double T[3], const uint32_t* cur, int32_t budget, uint32_t out[3]);
+df_status df_sched_react(const df_sched_cfg* cfg, const df_sched_metrics* now, const df_sched_metrics* prev,
+                         const uint32_t g[3], int32_t out[3]);
+int32_t df_sched_changed(const uint32_t* keys, uint32_t n);
+/* Controller thread on a live context (single-process). */
+df_status df_sched_start(df_ctx* ctx, const df_sched_cfg* cfg);
+df_status df_sched_stop(df_ctx* ctx);
+df_status df_sched_log(df_ctx* ctx, df_sched_event* out, uint32_t max, uint32_t* n_out);
+
 /* Self-test of the shared-memory metadata ring (no GPU needed): role 0 creates the
  * segment `name` and pushes n records with seq 0..n-1 into instance 0's inbox; role 1
  * attaches and pops n records, returning in *checksum the sum of seq and in *fifo_ok

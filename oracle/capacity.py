@@ -36,19 +36,54 @@ def feasible(g, G) -> bool:
     return min(g) >= 1 and sum(g) <= G
 
 
-def plan(G: int, T):
-    """Exhaustive Eq. 6 maximiser over all feasible allocations."""
+def plan(G: int, T, cur=None, budget=None):
+    """Exhaustive Eq. 6 maximiser over all feasible allocations; with `cur` and `budget`,
+    only allocations within `budget` instance moves (L1 distance) of `cur`."""
     if G < 3:
         raise ValueError("G < 3: no feasible allocation")
     best, key = None, None
     for gE in range(1, G - 1):
         for gT in range(1, G - gE):
             for gD in range(1, G - gE - gT + 1):
+                if cur is not None and budget is not None and budget >= 0 and \
+                        abs(gE - cur[0]) + abs(gT - cur[1]) + abs(gD - cur[2]) > budget:
+                    continue
                 q, _ = qps((gE, gT, gD), T)
                 k = (round(q, 12), -(gE + gT + gD), gT, gD)
                 if key is None or k > key:
                     best, key = (gE, gT, gD), k
     return best
+
+
+def reactive(u, q, d, d_prev, g_s, g_total, G, U_high=0.8, Q_high=5, U_low=0.2):
+    """Alg. 1 lines 11-17 for one service s with g_s instances: +1 (ScaleOut)
+    iff u > U_high and q > Q_high and d > d' (previous window; the first tick has none)
+    and a GPU is free (g_total < G, Eq. 1); -1 (ScaleIn) iff u < U_low and q = 0, never
+    below one instance; else 0."""
+    if u > U_high and q > Q_high and d_prev is not None and d > d_prev:
+        return 1 if g_total < G else 0
+    if u < U_low and q == 0:
+        return -1 if g_s >= 2 else 0
+    return 0
+
+
+def changed(keys) -> bool:
+    """Changed(H) (Alg. 1 line 6; "identifying the most frequent workload in H"):
+    the modal key of the most recent 25% differs from the modal key of the rest; a tie
+    for the mode in either part means no change (SPEC S:L490 reading)."""
+    n = len(keys)
+    if n < 4:
+        return False
+    cut = n - max(1, n // 4)
+
+    def mode(xs):
+        from collections import Counter
+        c = Counter(xs).most_common()
+        if len(c) > 1 and c[0][1] == c[1][1]:
+            return None
+        return c[0][0]
+    a, b = mode(keys[:cut]), mode(keys[cut:])
+    return a is not None and b is not None and a != b
 
 
 def splitmix64(z: np.ndarray) -> np.ndarray:

@@ -61,6 +61,20 @@ class CompletionC(C.Structure):
                 ("out_view", C.c_void_p), ("out_view_bytes", C.c_uint64)]
 
 
+class SchedCfgC(C.Structure):
+    _fields_ = [("delta_s", C.c_float), ("U_high", C.c_float), ("U_low", C.c_float), ("Q_high", C.c_uint32),
+                ("move_budget", C.c_int32), ("G", C.c_uint32)]
+
+
+class SchedMetricsC(C.Structure):
+    _fields_ = [("u", C.c_float * 3), ("q", C.c_uint32 * 3), ("d", C.c_float * 3)]
+
+
+class SchedEventC(C.Structure):
+    _fields_ = [("t", C.c_double), ("action", C.c_int32), ("stage", C.c_int32), ("g", C.c_uint32 * 3),
+                ("m", SchedMetricsC)]
+
+
 class HandoffDescC(C.Structure):
     _fields_ = [("src_inst", C.c_int32), ("dst_inst", C.c_int32), ("src", C.c_void_p), ("dst", C.c_void_p),
                 ("bytes", C.c_uint64), ("chunk_bytes", C.c_uint64), ("flags", C.c_uint32),
@@ -98,6 +112,14 @@ _SIGS = {
     "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
     "df_launch_count": (C.c_uint64, [C.c_void_p]),
+    "df_plan_ratio": (C.c_int, [C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.c_int32,
+                                C.POINTER(C.c_uint32)]),
+    "df_sched_react": (C.c_int, [C.POINTER(SchedCfgC), C.POINTER(SchedMetricsC), C.POINTER(SchedMetricsC),
+                                 C.POINTER(C.c_uint32), C.POINTER(C.c_int32)]),
+    "df_sched_changed": (C.c_int32, [C.POINTER(C.c_uint32), C.c_uint32]),
+    "df_sched_start": (C.c_int, [C.c_void_p, C.POINTER(SchedCfgC)]),
+    "df_sched_stop": (C.c_int, [C.c_void_p]),
+    "df_sched_log": (C.c_int, [C.c_void_p, C.POINTER(SchedEventC), C.c_uint32, C.POINTER(C.c_uint32)]),
     "df_ring_selftest": (C.c_int, [C.c_char_p, C.c_int32, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
     "df_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "df_kernel_stats": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
@@ -165,6 +187,42 @@ def make_graph(cfg, instances, precision=DF_BF16, weight_seed=0, chunk_bytes=(0,
     g.jitter_p, g.jitter_delay_s, g.jitter_seed = float(jitter[0]), float(jitter[1]), int(jitter[2])
     g.dit = dit_cfg_c(cfg)
     return g
+
+
+def sched_cfg(delta_s=2.0, U_high=0.8, U_low=0.2, Q_high=5, move_budget=-1, G=0) -> SchedCfgC:
+    """Alg. 1 defaults."""
+    return SchedCfgC(float(delta_s), float(U_high), float(U_low), int(Q_high), int(move_budget), int(G))
+
+
+def plan_ratio(G, T, cur=None, budget=-1):
+    lib = load()
+    Tc = (C.c_double * 3)(*T)
+    out = (C.c_uint32 * 3)()
+    curc = (C.c_uint32 * 3)(*cur) if cur is not None else None
+    st = lib.df_plan_ratio(int(G), Tc, curc, int(budget), out)
+    if st != DF_OK:
+        raise DFError(st, "df_plan_ratio")
+    return tuple(out)
+
+
+def sched_react(cfg, now, prev, g):
+    lib = load()
+    def mk(m):
+        if m is None:
+            return None
+        u, q, d = m
+        return C.byref(SchedMetricsC((C.c_float * 3)(*u), (C.c_uint32 * 3)(*q), (C.c_float * 3)(*d)))
+    out = (C.c_int32 * 3)()
+    st = lib.df_sched_react(C.byref(cfg), mk(now), mk(prev), (C.c_uint32 * 3)(*g), out)
+    if st != DF_OK:
+        raise DFError(st, "df_sched_react")
+    return tuple(out)
+
+
+def sched_changed(keys):
+    lib = load()
+    arr = (C.c_uint32 * max(1, len(keys)))(*keys)
+    return bool(lib.df_sched_changed(arr, len(keys)))
 
 
 def _ptr(t):
@@ -318,6 +376,19 @@ class Context:
             self._ck(self.lib.df_kernel_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
             out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
         return out
+
+    def sched_start(self, cfg):
+        self._ck(self.lib.df_sched_start(self.h, C.byref(cfg)))
+
+    def sched_stop(self):
+        self._ck(self.lib.df_sched_stop(self.h))
+
+    def sched_log(self):
+        n = C.c_uint32()
+        self._ck(self.lib.df_sched_log(self.h, None, 0, C.byref(n)))
+        arr = (SchedEventC * max(1, n.value))()
+        self._ck(self.lib.df_sched_log(self.h, arr, n.value, C.byref(n)))
+        return [arr[i] for i in range(n.value)]
 
     def launch_count(self):
         return int(self.lib.df_launch_count(self.h))

@@ -21,6 +21,8 @@
 #include <memory>
 #include <mutex>
 #include <set>
+#include <map>
+#include <cmath>
 #include <string>
 #include <thread>
 #include <vector>
@@ -206,6 +208,15 @@ struct df_ctx {
   };
   View views[DF_MAX_INST];
   std::vector<ReqState*> last_polled;
+  // hybrid scheduler (Alg. 1)
+  std::thread sched;
+  std::atomic<bool> sched_stop{false};
+  df_sched_cfg sched_cfg{};
+  std::mutex sched_mu;
+  std::deque<uint32_t> hist;               // workload keys (steps) of admitted requests
+  std::map<uint32_t, double> stage_s[3];   // measured seconds per request per instance (EMA)
+  std::atomic<uint64_t> qd_ns[3], qd_count[3];  // queueing delay accumulators per stage
+  std::vector<df_sched_event> sched_log;
   Prof prof;
 };
 
@@ -347,6 +358,15 @@ int pick(df_ctx* ctx, int stage, uint64_t seq) {
   return v[seq % uint64_t(std::min<int>(n, int(v.size())))];
 }
 
+// Stage-time profile for the Eq. 6 planner: EMA of seconds per request per instance, keyed by
+// the workload (steps for T; E and D do not depend on steps, tab:stage_time).
+void sched_note(df_ctx* ctx, int stage, uint32_t key, double sec) {
+  std::lock_guard<std::mutex> lk(ctx->sched_mu);
+  auto it = ctx->stage_s[stage].find(key);
+  if (it == ctx->stage_s[stage].end()) ctx->stage_s[stage][key] = sec;
+  else it->second = 0.7 * it->second + 0.3 * sec;
+}
+
 void worker_fail(df_ctx* ctx, const std::string& m) {
   std::lock_guard<std::mutex> lk(ctx->done_mu);
   ctx->err = m;
@@ -378,6 +398,8 @@ void e_worker(df_ctx* ctx, Inst* me) {
     }
     rs->inst[0] = me->id;
     rs->t_start[0] = now_s();
+    ctx->qd_ns[0] += uint64_t((rs->t_start[0] - rs->t_submit) * 1e9);
+    ctx->qd_count[0]++;
     WK(cudaEventCreate(&rs->ev[0]));
     WK(cudaEventCreate(&rs->ev[1]));
     const int tid = pick(ctx, DF_T, rs->seq);
@@ -419,6 +441,8 @@ void e_worker(df_ctx* ctx, Inst* me) {
     WK(cudaEventRecord(me->esent[b], me->comm));
     rs->t_end[0] = now_s();
     me->served++;
+    me->busy_ns += uint64_t((rs->t_end[0] - rs->t_start[0]) * 1e9);
+    sched_note(ctx, 0, 0u, rs->t_end[0] - rs->t_start[0]);
     T->inbox.push(Job{rs});  // E moves on immediately
   }
 }
@@ -429,6 +453,8 @@ void t_worker(df_ctx* ctx, Inst* me) {
   while (me->inbox.pop(j, ctx->stop)) {
     ReqState* rs = j.rs;
     rs->t_start[1] = now_s();
+    ctx->qd_ns[1] += uint64_t(std::max(0.0, rs->t_start[1] - rs->t_end[0]) * 1e9);
+    ctx->qd_count[1]++;
     WK(cudaEventCreate(&rs->ev[2]));
     WK(cudaEventCreate(&rs->ev[3]));
     WK(cudaEventCreate(&rs->ev[6]));
@@ -483,6 +509,8 @@ void t_worker(df_ctx* ctx, Inst* me) {
     cd.mem.release();
     rs->t_end[1] = now_s();
     me->served++;
+    me->busy_ns += uint64_t((rs->t_end[1] - rs->t_start[1]) * 1e9);
+    sched_note(ctx, 1, rs->req.steps, rs->t_end[1] - rs->t_start[1]);
     D->inbox.push(Job{rs});  // T dequeues its next request without waiting for the send
   }
 }
@@ -494,6 +522,8 @@ void d_worker(df_ctx* ctx, Inst* me) {
   while (me->inbox.pop(j, ctx->stop)) {
     ReqState* rs = j.rs;
     rs->t_start[2] = now_s();
+    ctx->qd_ns[2] += uint64_t(std::max(0.0, rs->t_start[2] - rs->t_end[1]) * 1e9);
+    ctx->qd_count[2]++;
     WK(cudaEventCreate(&rs->ev[4]));
     WK(cudaEventCreate(&rs->ev[5]));
     WK(cudaEventCreate(&rs->ev[7]));
@@ -513,6 +543,8 @@ void d_worker(df_ctx* ctx, Inst* me) {
       std::memcpy(rs->req.out_host, me->stage_host, ctx->out_bytes);
     rs->t_end[2] = now_s();
     me->served++;
+    me->busy_ns += uint64_t((rs->t_end[2] - rs->t_start[2]) * 1e9);
+    sched_note(ctx, 2, 0u, rs->t_end[2] - rs->t_start[2]);
     {
       std::lock_guard<std::mutex> lk(ctx->done_mu);
       while (!ctx->done->push(rs)) std::this_thread::yield();
@@ -975,6 +1007,180 @@ void plane_close(PlaneSeg* seg, const char* name, bool owner) {
 }
 }  // namespace df
 
+// ================================================================== hybrid scheduler (Alg. 1)
+namespace {
+
+double eq6(const uint32_t g[3], const double T[3]) {
+  double q = 1e300;
+  for (int s = 0; s < 3; ++s) q = std::min(q, double(g[s]) / T[s]);
+  return q;
+}
+
+bool plan_ratio(uint32_t G, const double T[3], const uint32_t* cur, int32_t budget, const uint32_t* cap,
+                uint32_t out[3]) {
+  bool found = false;
+  double bq = 0;
+  uint32_t best[3] = {0, 0, 0};
+  for (uint32_t e = 1; e + 2 <= G; ++e)
+    for (uint32_t t = 1; e + t + 1 <= G; ++t)
+      for (uint32_t d = 1; e + t + d <= G; ++d) {
+        if (cap && (e > cap[0] || t > cap[1] || d > cap[2])) continue;
+        if (cur && budget >= 0) {
+          int64_t mv = std::llabs(int64_t(e) - cur[0]) + std::llabs(int64_t(t) - cur[1]) + std::llabs(int64_t(d) - cur[2]);
+          if (mv > budget) continue;
+        }
+        uint32_t g[3] = {e, t, d};
+        double q = eq6(g, T);
+        // ties (to 1e-12 relative): fewer GPUs, then larger g_T, then larger g_D
+        bool better = !found || q > bq * (1 + 1e-12);
+        if (!better && found && std::fabs(q - bq) <= bq * 1e-12) {
+          uint32_t sn = e + t + d, sb = best[0] + best[1] + best[2];
+          better = sn < sb || (sn == sb && (t > best[1] || (t == best[1] && d > best[2])));
+        }
+        if (better) {
+          found = true;
+          bq = q;
+          best[0] = e, best[1] = t, best[2] = d;
+        }
+      }
+  if (found) std::memcpy(out, best, sizeof(best));
+  return found;
+}
+
+void react(const df_sched_cfg& c, const df_sched_metrics& now, const df_sched_metrics* prev, const uint32_t g[3],
+           int32_t out[3]) {
+  const uint32_t total = g[0] + g[1] + g[2];
+  for (int s = 0; s < 3; ++s) {
+    out[s] = 0;
+    if (now.u[s] > c.U_high && now.q[s] > c.Q_high && prev && now.d[s] > prev->d[s]) {
+      out[s] = (c.G == 0 || total < c.G) ? 1 : 0;
+    } else if (now.u[s] < c.U_low && now.q[s] == 0) {
+      out[s] = g[s] >= 2 ? -1 : 0;
+    }
+  }
+}
+
+bool changed(const uint32_t* k, uint32_t n) {
+  if (n < 4) return false;
+  uint32_t cut = n - std::max<uint32_t>(1, n / 4);
+  auto mode = [&](uint32_t a, uint32_t b, bool& tie) {
+    std::map<uint32_t, uint32_t> cnt;
+    for (uint32_t i = a; i < b; ++i) cnt[k[i]]++;
+    uint32_t bk = 0, bc = 0, second = 0;
+    for (auto& kv : cnt) {
+      if (kv.second > bc) {
+        second = bc;
+        bc = kv.second;
+        bk = kv.first;
+      } else if (kv.second > second) {
+        second = kv.second;
+      }
+    }
+    tie = cnt.size() > 1 && second == bc;
+    return bk;
+  };
+  bool t1 = false, t2 = false;
+  uint32_t a = mode(0, cut, t1), b = mode(cut, n, t2);
+  return !t1 && !t2 && a != b;
+}
+
+// Controller: every delta, measure u/q/d per stage from the live pipeline and apply Alg. 1.
+void sched_loop(df_ctx* ctx) {
+  df_sched_cfg c = ctx->sched_cfg;
+  df_sched_metrics prev{};
+  bool have_prev = false;
+  std::vector<uint64_t> busy0(ctx->inst.size());
+  for (size_t i = 0; i < ctx->inst.size(); ++i) busy0[i] = ctx->inst[i]->busy_ns.load();
+  double t_prev = now_s();
+  while (!ctx->sched_stop.load()) {
+    for (int k = 0; k < int(c.delta_s * 100) && !ctx->sched_stop.load(); ++k)
+      std::this_thread::sleep_for(std::chrono::milliseconds(10));
+    if (ctx->sched_stop.load()) break;
+    const double t = now_s(), win = std::max(1e-6, t - t_prev);
+    t_prev = t;
+    df_sched_metrics m{};
+    uint32_t g[3];
+    for (int s = 0; s < 3; ++s) g[s] = uint32_t(ctx->active[s].load());
+    for (int s = 0; s < 3; ++s) {
+      const auto& ids = ctx->by_stage[s];
+      double busy = 0;
+      for (size_t j = 0; j < ids.size(); ++j) {
+        Inst& I = *ctx->inst[ids[j]];
+        uint64_t b = I.busy_ns.load();
+        if (j < g[s]) busy += double(b - busy0[ids[j]]) * 1e-9;
+        busy0[ids[j]] = b;
+        if (j < g[s] && s != DF_E) m.q[s] += uint32_t(I.inbox.size());
+      }
+      if (s == DF_E) m.q[s] = uint32_t(ctx->requests->size_approx());
+      m.u[s] = float(std::min(1.0, busy / (double(g[s]) * win)));
+      uint64_t n = ctx->qd_count[s].exchange(0);
+      uint64_t tot = ctx->qd_ns[s].exchange(0);
+      m.d[s] = n ? float(double(tot) * 1e-9 / double(n)) : 0.f;
+    }
+    df_sched_event ev{};
+    ev.t = t;
+    ev.m = m;
+    // workload change -> predictive reconfiguration (Alg. 1 lines 6-10)
+    std::vector<uint32_t> keys;
+    {
+      std::lock_guard<std::mutex> lk(ctx->sched_mu);
+      keys.assign(ctx->hist.begin(), ctx->hist.end());
+    }
+    bool reconf = false;
+    if (changed(keys.data(), uint32_t(keys.size()))) {
+      uint32_t key = keys.back();
+      double T[3];
+      bool ok = true;
+      {
+        std::lock_guard<std::mutex> lk(ctx->sched_mu);
+        for (int s = 0; s < 3; ++s) {
+          auto it = ctx->stage_s[s].find(s == DF_T ? key : 0u);
+          if (it == ctx->stage_s[s].end()) ok = false;
+          else T[s] = std::max(1e-6, it->second);
+        }
+      }
+      uint32_t capn[3] = {uint32_t(ctx->by_stage[0].size()), uint32_t(ctx->by_stage[1].size()),
+                          uint32_t(ctx->by_stage[2].size())};
+      uint32_t G = c.G ? c.G : capn[0] + capn[1] + capn[2];
+      uint32_t tgt[3];
+      if (ok && plan_ratio(G, T, g, c.move_budget, capn, tgt) && std::memcmp(tgt, g, sizeof(g)) != 0) {
+        df_set_ratio(ctx, tgt[0], tgt[1], tgt[2]);
+        ev.action = 3;
+        std::memcpy(ev.g, tgt, sizeof(tgt));
+        reconf = true;
+        std::lock_guard<std::mutex> lk(ctx->sched_mu);
+        ctx->hist.clear();  // the new regime starts a fresh history
+      }
+    }
+    if (!reconf) {  // reactive rule (lines 11-17); one action per tick
+      int32_t dlt[3];
+      df_sched_cfg cc = c;
+      if (!cc.G) cc.G = uint32_t(ctx->inst.size());
+      react(cc, m, have_prev ? &prev : nullptr, g, dlt);
+      uint32_t ng[3] = {g[0], g[1], g[2]};
+      for (int s = 0; s < 3 && ev.action == 0; ++s) {
+        if (dlt[s] > 0 && ng[s] < ctx->by_stage[s].size()) {
+          ng[s]++;
+          ev.action = 1;
+          ev.stage = s;
+        } else if (dlt[s] < 0) {
+          ng[s]--;
+          ev.action = 2;
+          ev.stage = s;
+        }
+      }
+      if (ev.action) df_set_ratio(ctx, ng[0], ng[1], ng[2]);
+      std::memcpy(ev.g, ng, sizeof(ng));
+    }
+    prev = m;
+    have_prev = true;
+    std::lock_guard<std::mutex> lk(ctx->sched_mu);
+    ctx->sched_log.push_back(ev);
+  }
+}
+
+}  // namespace
+
 // ================================================================== C ABI
 extern "C" {
 
@@ -984,6 +1190,46 @@ const char* df_last_error(const df_ctx* ctx) {
 }
 
 uint64_t df_launch_count(const df_ctx*) { return g_launches->load(); }
+
+df_status df_plan_ratio(uint32_t G, const double T[3], const uint32_t* cur, int32_t budget, uint32_t out[3]) {
+  if (!T || !out || G < 3 || !(T[0] > 0 && T[1] > 0 && T[2] > 0)) return DF_ERR_INVALID;
+  return plan_ratio(G, T, cur, cur ? budget : -1, nullptr, out) ? DF_OK : DF_ERR_CAPACITY;
+}
+
+df_status df_sched_react(const df_sched_cfg* cfg, const df_sched_metrics* now, const df_sched_metrics* prev,
+                         const uint32_t g[3], int32_t out[3]) {
+  if (!cfg || !now || !g || !out) return DF_ERR_INVALID;
+  react(*cfg, *now, prev, g, out);
+  return DF_OK;
+}
+
+int32_t df_sched_changed(const uint32_t* keys, uint32_t n) { return keys && changed(keys, n) ? 1 : 0; }
+
+df_status df_sched_start(df_ctx* ctx, const df_sched_cfg* cfg) {
+  if (!ctx || !cfg || !(cfg->delta_s > 0.f) || !(cfg->U_low < cfg->U_high)) return DF_ERR_INVALID;
+  if (ctx->mp) return fail(ctx, "df_sched_start: single-process contexts only", DF_ERR_INVALID);
+  if (ctx->sched.joinable()) return fail(ctx, "df_sched_start: already running", DF_ERR_STATE);
+  ctx->sched_cfg = *cfg;
+  ctx->sched_stop = false;
+  ctx->sched = std::thread(sched_loop, ctx);
+  return DF_OK;
+}
+
+df_status df_sched_stop(df_ctx* ctx) {
+  if (!ctx) return DF_ERR_INVALID;
+  ctx->sched_stop = true;
+  if (ctx->sched.joinable()) ctx->sched.join();
+  return DF_OK;
+}
+
+df_status df_sched_log(df_ctx* ctx, df_sched_event* out, uint32_t max, uint32_t* n_out) {
+  if (!ctx || !n_out) return DF_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(ctx->sched_mu);
+  uint32_t n = std::min<uint32_t>(max, uint32_t(ctx->sched_log.size()));
+  for (uint32_t i = 0; i < n && out; ++i) out[i] = ctx->sched_log[i];
+  *n_out = out ? n : uint32_t(ctx->sched_log.size());
+  return DF_OK;
+}
 
 df_status df_ring_selftest(const char* name, int32_t role, uint64_t n, uint64_t* checksum, int32_t* fifo_ok) {
   if (!name || !name[0] || (role != 0 && role != 1)) return DF_ERR_INVALID;
@@ -1182,6 +1428,8 @@ df_status df_init(const df_graph* g, df_ctx** out) {
 
 df_status df_finalize(df_ctx* ctx) {
   if (!ctx) return DF_ERR_INVALID;
+  ctx->sched_stop = true;
+  if (ctx->sched.joinable()) ctx->sched.join();
   ctx->stop = true;
   for (auto& ip : ctx->inst) {
     ip->inbox.cv.notify_all();
@@ -1267,6 +1515,11 @@ df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
   {
     std::lock_guard<std::mutex> lk(ctx->req_mu);
     rs->seq = ctx->mp ? ctx->seg->seq.fetch_add(1) : ctx->seq.fetch_add(1);  // FAA ticket
+  }
+  {
+    std::lock_guard<std::mutex> lk(ctx->sched_mu);
+    ctx->hist.push_back(r->steps);
+    while (ctx->hist.size() > 64) ctx->hist.pop_front();
   }
   if (!ctx->requests->push(rs)) {
     free_req(rs);

@@ -133,3 +133,26 @@ def test_pipeline_request_tiny_runs():
     out = stages.request(P, TINY, seed=1)
     assert out["latent"].dtype == np.float32 and np.all(np.isfinite(out["out"]))
     assert out["out"].shape == TINY.out_shape
+
+
+def test_planner_move_budget_spec_example():
+    # 1-step stage times, current (1,6,1), <= 2 instance moves -> (1,5,2)
+    assert cap.plan(8, T1, cur=(1, 6, 1), budget=2) == (1, 5, 2)
+    assert cap.plan(8, T1) == (2, 4, 2)                   # unconstrained optimum differs (R25)
+    assert cap.plan(8, T4, cur=(1, 5, 2), budget=8) == (1, 6, 1)
+
+
+def test_reactive_rule_spec_examples():
+    # S:L489-491
+    assert cap.reactive(0.95, 7, 4.8, 3.1, 6, 8 - 1, 8) == 1       # ScaleOut(T), one GPU free
+    assert cap.reactive(0.95, 7, 4.8, 3.1, 6, 8, 8) == 0           # no free GPU: capacity
+    assert cap.reactive(0.10, 0, 0.0, 0.0, 2, 8, 8) == -1          # ScaleIn(D)
+    assert cap.reactive(0.10, 0, 0.0, 0.0, 1, 8, 8) == 0           # never below one instance
+    assert cap.reactive(0.50, 2, 1.0, 0.5, 1, 8, 8) == 0           # NoOp
+    assert cap.reactive(0.95, 7, 4.8, None, 6, 7, 8) == 0          # first tick: no d'
+
+
+def test_change_detector_spec_examples():
+    assert not cap.changed([4] * 20)
+    assert cap.changed([4] * 15 + [1] * 5)
+    assert not cap.changed([4] * 12 + [1, 1, 4, 4])   # tie in the recent window -> no change
