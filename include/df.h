@@ -108,6 +108,10 @@ typedef struct {
   uint64_t out_bytes;           /*   until df_poll returns this request (MPI Irecv rule)  */
   uint64_t user_tag;
   df_req_id id;                 /* {0,0} = assign one                                    */
+  float guidance;               /* classifier-free guidance scale; 0 or 1 = off (NEXT-2). When
+                                   on, E also encodes the negative prompt (tokens from the seed's
+                                   negative stream or neg_token_ids) and T runs a batch of 2.  */
+  const int32_t* neg_token_ids; /* host [L_txt] or NULL; copied                          */
 } df_request;
 /* Admit a request ("request scheduler inserts the request into the global
  * request buffer").  MT-safe.  DF_AGAIN if the ring is full, DF_ERR_DUPLICATE if
@@ -141,6 +145,11 @@ df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD);
 typedef struct df_cond df_cond;   /* per-request conditioning: cross K/V of every layer, e/e6 of every step */
 /* Request prologue on T instance t_inst from a device bf16 ctx
  * [L_txt, d_txt]; sigmas = host float[S+1] schedule.  *out is caller-owned. */
+/* Classifier-free guidance variant (NEXT-2; "negative prompts"): ctx_neg_dev is the
+ * negative prompt's bf16 ctx; every df_dit_step then runs the conditional and negative
+ * samples as one batch of 2 and updates x with v = v_u + guidance (v_c - v_u). */
+df_status df_dit_prepare_cfg(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const void* ctx_neg_dev,
+                             float guidance, const float* sigmas, uint32_t S, void* stream, df_cond** out);
 df_status df_dit_prepare(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const float* sigmas, uint32_t S,
                          void* stream, df_cond** out);
 /* One denoising step i (a2-a12): x_dev fp32 [C,F,H,W] updated in place,

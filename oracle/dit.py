@@ -258,18 +258,32 @@ def velocity(P, cfg, x: np.ndarray, i: int, cond, cross: bool = True, trace=None
     return head(P, cfg, r, cond["e"][i])
 
 
+def velocity_cfg(P, cfg, x, i, cond, cond_neg, guidance: float) -> np.ndarray:
+    """Classifier-free guidance (NEXT-2; "negative prompts"): the DiT runs on the
+    conditional and the negative-prompt conditioning; v = v_u + g (v_c - v_u).  g = 1 is the
+    conditional velocity (R20)."""
+    v_c = velocity(P, cfg, x, i, cond)
+    v_u = velocity(P, cfg, x, i, cond_neg)
+    return v_u + guidance * (v_c - v_u)
+
+
 def step(P, cfg, x, i, cond, sig):
     """One denoising step: returns (x_{i+1}, v_i)."""
     v = velocity(P, cfg, x, i, cond)
     return euler_update(np.asarray(x, dtype=np.float64), v, sig[i], sig[i + 1]), v
 
 
-def trajectory(P, cfg, x0, ctx, steps=None, shift=None):
-    """x_S from x_0 and the bf16 ctx payload (values as fp64)."""
+def trajectory(P, cfg, x0, ctx, steps=None, shift=None, ctx_neg=None, guidance: float = 1.0):
+    """x_S from x_0 and the bf16 ctx payload (values as fp64); with ctx_neg, classifier-free
+    guidance with scale `guidance`."""
     S = cfg.steps if steps is None else steps
     sig = sigmas(S, cfg.shift if shift is None else shift)
     cond = prologue(P, cfg, ctx, sig)
+    cond_neg = prologue(P, cfg, ctx_neg, sig) if ctx_neg is not None else None
     x = np.asarray(x0, dtype=np.float64)
     for i in range(S):
-        x, _ = step(P, cfg, x, i, cond, sig)
+        if cond_neg is None:
+            x, _ = step(P, cfg, x, i, cond, sig)
+        else:
+            x = euler_update(x, velocity_cfg(P, cfg, x, i, cond, cond_neg, guidance), sig[i], sig[i + 1])
     return x

@@ -37,8 +37,9 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
     return bf16_bits_to_f64(bits), bits
 
 
-def tokens_from_seed(cfg, seed: int) -> np.ndarray:
-    return (stream_words(seed, cfg.L_txt, 0, 2) % np.uint32(cfg.vocab)).astype(np.int32)
+def tokens_from_seed(cfg, seed: int, negative: bool = False) -> np.ndarray:
+    """Prompt token ids (stream c3=2) or the negative prompt's (stream c3=4)."""
+    return (stream_words(seed, cfg.L_txt, 0, 4 if negative else 2) % np.uint32(cfg.vocab)).astype(np.int32)
 
 
 def noise(cfg, seed: int) -> np.ndarray:
@@ -80,13 +81,18 @@ def decoder(P, cfg, x: np.ndarray) -> np.ndarray:
     return out
 
 
-def request(P, cfg, seed: int, ids=None, steps=None, shift=None):
-    """Serial E -> T -> D for one request (the pipeline's exact result)."""
+def request(P, cfg, seed: int, ids=None, steps=None, shift=None, guidance: float = 1.0):
+    """Serial E -> T -> D for one request (the pipeline's exact result).  guidance != 1 adds
+    the negative prompt (tokens from stream c3=4) and classifier-free guidance (NEXT-2)."""
     if ids is None:
         ids = tokens_from_seed(cfg, seed)
     ctx, ctx_bits = encoder(P, cfg, ids)
+    ctx_neg = None
+    if guidance != 1.0:
+        ctx_neg, _ = encoder(P, cfg, tokens_from_seed(cfg, seed, negative=True))
     x0 = noise(cfg, seed)
-    xS = dit.trajectory(P, cfg, x0.astype(np.float64), ctx, steps=steps, shift=shift)
+    xS = dit.trajectory(P, cfg, x0.astype(np.float64), ctx, steps=steps, shift=shift, ctx_neg=ctx_neg,
+                        guidance=guidance)
     lat = xS.astype(np.float32)                      # T->D payload is fp32 (R21)
     return {"ids": ids, "ctx": ctx, "ctx_bits": ctx_bits, "x0": x0, "latent": lat,
             "out": decoder(P, cfg, lat.astype(np.float64))}

@@ -50,7 +50,8 @@ class ReqIdC(C.Structure):
 class RequestC(C.Structure):
     _fields_ = [("steps", C.c_uint32), ("shift", C.c_float), ("seed", C.c_uint64),
                 ("token_ids", C.POINTER(C.c_int32)), ("out_host", C.c_void_p), ("out_bytes", C.c_uint64),
-                ("user_tag", C.c_uint64), ("id", ReqIdC)]
+                ("user_tag", C.c_uint64), ("id", ReqIdC), ("guidance", C.c_float),
+                ("neg_token_ids", C.POINTER(C.c_int32))]
 
 
 class CompletionC(C.Structure):
@@ -92,6 +93,8 @@ _SIGS = {
     "df_set_ratio": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32]),
     "df_dit_prepare": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.c_void_p,
                                  C.POINTER(C.c_void_p)]),
+    "df_dit_prepare_cfg": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_float, C.POINTER(C.c_float),
+                                     C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "df_dit_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_dit_layer": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "df_cond_release": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -264,9 +267,14 @@ class Context:
         self.close()
 
     # ---- serving
-    def submit(self, steps, shift, seed, out_host=None, token_ids=None, user_tag=0, req_id=None):
+    def submit(self, steps, shift, seed, out_host=None, token_ids=None, user_tag=0, req_id=None, guidance=1.0,
+               neg_token_ids=None):
         r = RequestC()
         r.steps, r.shift, r.seed, r.user_tag = int(steps), float(shift), int(seed), int(user_tag)
+        r.guidance = float(guidance)
+        if neg_token_ids is not None:
+            self._nids = (C.c_int32 * len(neg_token_ids))(*[int(x) for x in neg_token_ids])
+            r.neg_token_ids = C.cast(self._nids, C.POINTER(C.c_int32))
         if token_ids is not None:
             self._ids = (C.c_int32 * len(token_ids))(*[int(x) for x in token_ids])
             r.token_ids = C.cast(self._ids, C.POINTER(C.c_int32))
@@ -296,6 +304,13 @@ class Context:
         out = C.c_void_p()
         self._ck(self.lib.df_dit_prepare(self.h, t_inst, _ptr(ctx_dev), sig, len(sigmas) - 1, _stream(stream),
                                          C.byref(out)))
+        return out
+
+    def dit_prepare_cfg(self, t_inst, ctx_dev, ctx_neg_dev, guidance, sigmas, stream=None):
+        sig = (C.c_float * len(sigmas))(*[float(s) for s in sigmas])
+        out = C.c_void_p()
+        self._ck(self.lib.df_dit_prepare_cfg(self.h, t_inst, _ptr(ctx_dev), _ptr(ctx_neg_dev), float(guidance), sig,
+                                             len(sigmas) - 1, _stream(stream), C.byref(out)))
         return out
 
     def dit_step(self, t_inst, cond, i, x_dev, v_dev=None, stream=None):

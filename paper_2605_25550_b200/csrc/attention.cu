@@ -282,11 +282,11 @@ DF_DEV float ex2_approx(float x) {
   return y;
 }
 
-template <int DH, bool POLY>
+template <int DH, bool POLY, bool SP>
 __global__ void __launch_bounds__(384, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
-                    int dh_real, float scale_log2) {
+                    int dh_real, float scale_log2, int Hs) {
   using Cfg = Attn2Cfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -335,6 +335,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -427,13 +429,18 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
     const uint32_t ts = tmem + lane_off + t * 128;
     const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH;
-    float m_used = -INFINITY, l = 0.f;
+    // SP (single pass): the max in use starts at 0 (log2 units) and is only raised when a
+    // block's logits exceed it by > 2^30, so no max pre-pass is needed; P is clamped at 2^64
+    // before that (rare) rescale, which is exact for logits within 2^64 of the max in use
+    // (far beyond the range of this model's RMS-normalised q, k: |s| log2e <= sqrt(dh) max|g|^2).
+    float m_used = SP ? 0.f : -INFINITY, l = 0.f;
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      // pass 1: row max, 64 columns in flight (S stays in TMEM; low register pressure)
       const int valid = Nk - j * 128;
       float mx = -INFINITY;
+      if (!SP) {
+      // pass 1: row max, 64 columns in flight (S stays in TMEM; low register pressure)
 #pragma unroll
       for (int c = 0; c < 128; c += 64) {
         float s[64];
@@ -468,6 +475,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         m_used = m_new;
       }
+      }  // !SP
       // p = 2^(s*scale - m): FFMA2 for the affine part; 3/8 of the exponentials on the
       // FMA/ALU pipes (polynomial), 5/8 on MUFU.EX2, so neither unit paces the tile.
       float2 lsum2 = make_float2(0.f, 0.f);
@@ -489,6 +497,11 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+          if (SP) {
+            mx = fmaxf(mx, fmaxf(s[2 * i], s[2 * i + 1]));
+            x.x = fminf(x.x, 64.f);
+            x.y = fminf(x.y, 64.f);
+          }
           float2 p;
           if (POLY && (i & 7) >= 5) {
             p = exp2_poly2(x);
@@ -503,6 +516,41 @@ __global__ void __launch_bounds__(384, 1)
         tmem_st16(ts + c / 2, pk);
         tmem_st16(ts + c / 2 + 16, pk + 16);
       }
+      if (SP && __any_sync(0xffffffffu, mx * scale_log2 > m_used + 30.0f)) {
+        // rare: raise the max in use; rescale O_t (stable: s_full for block j implies
+        // PV_{j-1} completed), l, this block's sum and its P (in place, p' = p * alpha)
+        tc_wait_st();
+        const float m_new = fmaxf(m_used, mx * scale_log2);
+        const float alpha = exp2f(m_used - m_new);
+        l *= alpha;
+        lsum2.x *= alpha;
+        lsum2.y *= alpha;
+        if (j > 0) {
+#pragma unroll 1
+          for (int c = 0; c < DH; c += 32) {
+            float o[32];
+            tmem_ld32(to + c, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(to + c, o);
+          }
+        }
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 16) {
+          float pf[16];
+          uint32_t pk[16];
+          tmem_ld16(ts + c, pf);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            uint32_t u = __float_as_uint(pf[i]);
+            pk[i] = pack_bf16x2(__uint_as_float(u << 16) * alpha, __uint_as_float(u & 0xFFFF0000u) * alpha);
+          }
+          tmem_st16(ts + c, pk);
+        }
+        m_used = m_new;
+      }
       l += lsum2.x + lsum2.y;
       tc_wait_st();
       tc_fence_before();
@@ -512,7 +560,9 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const float inv = 1.0f / l;
     const int q = q0 + t * 128 + r;
-    bf16* orow = O + size_t(q) * H * dh_real + size_t(h) * dh_real;
+    // heads of a stacked batch: head h belongs to sample h / Hs; token-major rows b*Nq + q
+    const int hb = h / Hs, hl = h - hb * Hs;
+    bf16* orow = O + (size_t(hb) * Nq + q) * Hs * dh_real + size_t(hl) * dh_real;
 #pragma unroll 1
     for (int c = 0; c < DH; c += 32) {
       float o[32];
@@ -537,11 +587,11 @@ __global__ void __launch_bounds__(384, 1)
 
 int g_attn_impl = 2;
 
-template <int DH, bool POLY>
+template <int DH, bool POLY, bool SP>
 static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, bf16* O, int H,
-                                int Nq, int Nk, int dh, float scale, cudaStream_t st) {
+                                int Nq, int Nk, int dh, float scale, cudaStream_t st, int hs) {
   using Cfg = Attn2Cfg<DH>;
-  auto kern = attn_tc2_kernel<DH, POLY>;
+  auto kern = attn_tc2_kernel<DH, POLY, SP>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -549,14 +599,16 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
     attr = true;
   }
   dim3 grid((Nq + 255) / 256, H);
-  kern<<<grid, 384, Cfg::SMEM, st>>>(tq, tk, tv, O, H, Nq, Nk, dh, scale * 1.4426950408889634f);
-  return cudaGetLastError();
+  float sl2 = scale * 1.4426950408889634f;
+  void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,
+                  (void*)&Nq, (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs};
+  return launch_ex((const void*)kern, grid, dim3(384), Cfg::SMEM, st, args);
 }
 
 template <int DH>
 static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
-                               float scale, cudaStream_t st) {
-  if (g_attn_impl == 2) {
+                               float scale, cudaStream_t st, int hs) {
+  if (g_attn_impl == 2 || hs != H) {
     CUtensorMap tq, tk, tv;
     if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
         !make_tmap_3d(&tv, V, H, Nk, DH, 128))
@@ -565,8 +617,14 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
       const char* e = getenv("DF_ATTN_POLY");  // 1: 3/8 of the exponentials by polynomial on the FMA pipe
       return e ? atoi(e) : 0;
     }();
-    return poly ? launch_attn2<DH, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st)
-                : launch_attn2<DH, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st);
+    static const int sp = [] {
+      const char* e = getenv("DF_ATTN_SP");  // 1: single-pass softmax (lazy max from 0)
+      return e ? atoi(e) : 0;
+    }();
+    if (sp) return poly ? launch_attn2<DH, true, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
+                        : launch_attn2<DH, false, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    return poly ? launch_attn2<DH, true, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
+                : launch_attn2<DH, false, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
   }
   using Cfg = AttnCfg<DH>;
   CUtensorMap tq, tk, tv;
@@ -586,23 +644,24 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
 }
 
 cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
-                    float scale, cudaStream_t st) {
+                    float scale, cudaStream_t st, int heads_per_sample) {
   static const int impl_env = [] {
     const char* e = getenv("DF_ATTN_IMPL");  // 1: one Q tile per CTA (round-1 kernel), 2: two (default)
     return e ? atoi(e) : 2;
   }();
   g_attn_impl = impl_env;
+  const int hs = heads_per_sample > 0 ? heads_per_sample : H;
   if (Nq <= 0) return cudaSuccess;
-  if (Nk <= 0 || dh > dh_pad) return cudaErrorInvalidValue;
-  if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st);
-  if (dh_pad == 128) return launch_attn<128>(Q, K, V, O, H, Nq, Nk, dh, scale, st);
+  if (Nk <= 0 || dh > dh_pad || H % hs) return cudaErrorInvalidValue;
+  if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+  if (dh_pad == 128) return launch_attn<128>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
   return cudaErrorInvalidValue;
 }
 
 // ------------------------------------------------------------------ fp32 SIMT attention
 __global__ void attn_simt_kernel(const float* __restrict__ Q, const float* __restrict__ K,
                                  const float* __restrict__ V, float* __restrict__ O, int H, int Nq, int Nk, int dh,
-                                 float scale) {
+                                 float scale, int hs) {
   const int warps = blockDim.x / 32;
   const int q = blockIdx.x * warps + threadIdx.x / 32;
   const int h = blockIdx.y;
@@ -629,18 +688,20 @@ __global__ void attn_simt_kernel(const float* __restrict__ Q, const float* __res
       if (lane + 32 * i < dh) ov[i] = ov[i] * corr + pj * vr[lane + 32 * i];
     m = mn;
   }
-  float* orow = O + size_t(q) * H * dh + size_t(h) * dh;
+  const int hb = h / hs, hl = h - hb * hs;
+  float* orow = O + (size_t(hb) * Nq + q) * hs * dh + size_t(hl) * dh;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (lane + 32 * i < dh) orow[lane + 32 * i] = ov[i] / l;
 }
 
 cudaError_t attn_simt(const float* Q, const float* K, const float* V, float* O, int H, int Nq, int Nk, int dh,
-                      float scale, cudaStream_t st) {
+                      float scale, cudaStream_t st, int heads_per_sample) {
+  const int hs = heads_per_sample > 0 ? heads_per_sample : H;
   if (Nq <= 0) return cudaSuccess;
-  if (Nk <= 0 || dh > 128) return cudaErrorInvalidValue;
+  if (Nk <= 0 || dh > 128 || H % hs) return cudaErrorInvalidValue;
   dim3 grid((Nq + 3) / 4, H);
-  attn_simt_kernel<<<grid, 128, 0, st>>>(Q, K, V, O, H, Nq, Nk, dh, scale);
+  attn_simt_kernel<<<grid, 128, 0, st>>>(Q, K, V, O, H, Nq, Nk, dh, scale, hs);
   return cudaGetLastError();
 }
 

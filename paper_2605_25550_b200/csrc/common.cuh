@@ -312,3 +312,11 @@ DF_DEV float2 exp2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 }  // namespace df
+
+namespace df {
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor drains; it must call
+// pdl_wait() before reading or writing anything the predecessor produces or consumes.
+DF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DF_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+}  // namespace df

@@ -101,7 +101,7 @@ struct ReqState {
   df_request req{};
   df_req_id id{};
   uint64_t seq = 0;
-  std::vector<int32_t> ids;
+  std::vector<int32_t> ids, neg_ids;
   int inst[3] = {-1, -1, -1};
   double t_submit = 0, t_start[3] = {0, 0, 0}, t_end[3] = {0, 0, 0};
   cudaEvent_t ev[10] = {};  // 0,1 E start/end; 2,3 T start/end; 4,5 D start/end; 6 T ready; 7 D ready
@@ -240,6 +240,7 @@ df_status fail(df_ctx* c, const std::string& m, df_status s = DF_ERR_CUDA) {
   } while (0)
 
 size_t latent_elems(const df_dit_cfg& c) { return size_t(c.C) * c.F * c.H * c.W; }
+bool cfg_on(float g) { return g != 0.f && g != 1.f; }
 size_t out_elems(const df_dit_cfg& c) { return size_t(3) * (1 + 4 * (c.F - 1)) * 8 * c.H * 8 * c.W; }
 
 std::vector<float> sigmas_host(int S, float shift) {
@@ -383,6 +384,20 @@ void worker_fail(df_ctx* ctx, const std::string& m) {
     }                                                                             \
   } while (0)
 
+// Negative prompt (CFG): tokens from the caller or the seed's negative stream, encoded into
+// the second half of the send buffer.
+cudaError_t encode_negative(df_ctx* ctx, Inst* me, ReqState* rs, void* ebuf) {
+  const size_t L = ctx->g.dit.L_txt;
+  int32_t* nid = me->ids_dev + L;
+  if (!rs->neg_ids.empty()) {
+    DF_TRY(cudaMemcpyAsync(nid, rs->neg_ids.data(), L * 4, cudaMemcpyHostToDevice, me->compute));
+  } else {
+    g_launches->fetch_add(1);
+    DF_TRY(gen_tokens(nid, int(L), int(me->m.c.vocab), rs->req.seed, me->compute, 4));
+  }
+  return me->m.encode(nid, static_cast<char*>(ebuf) + ctx->ctx_bytes, me->compute);
+}
+
 void e_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
   while (!ctx->stop.load()) {
@@ -416,6 +431,8 @@ void e_worker(df_ctx* ctx, Inst* me) {
       WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
     }
     WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+    const bool cfgr = cfg_on(rs->req.guidance);
+    if (cfgr) WK(encode_negative(ctx, me, rs, me->ebuf[b]));
     WK(cudaEventRecord(rs->ev[1], me->compute));
     // handshake: claim a receive slot on T (its posted destination address)
     int s = T->slots.acquire(ctx->stop);
@@ -427,7 +444,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
     d.dst_inst = tid;
     d.src = me->ebuf[b];
     d.dst = T->slots.slots[s].buf;
-    d.bytes = ctx->ctx_bytes;
+    d.bytes = (cfgr ? 2 : 1) * ctx->ctx_bytes;
     d.chunk_bytes = ctx->g.chunk_bytes[0];
     d.flags = (ctx->g.handoff_mode & (DF_SYNC | DF_HASH));
     d.seq = rs->seq;
@@ -473,7 +490,10 @@ void t_worker(df_ctx* ctx, Inst* me) {
     for (uint32_t c = 0; c < x0->nchunks; ++c) WK(cudaStreamWaitEvent(me->compute, x0->chunk_ev[c], 0));
     std::vector<float> sig = sigmas_host(S, rs->req.shift);
     Cond cd;
-    WK(me->m.prepare(me->slots.slots[rs->slot[0]].buf, sig.data(), S, me->compute, &cd));
+    const void* cbuf = me->slots.slots[rs->slot[0]].buf;
+    const bool cfgr = cfg_on(rs->req.guidance);
+    WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->ctx_bytes : nullptr,
+                     cfgr ? rs->req.guidance : 1.f));
     WK(cudaEventRecord(me->slots.slots[rs->slot[0]].consumed, me->compute));
     me->slots.release(rs->slot[0]);  // producer's comm stream waits on `consumed` before reuse
     for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
@@ -807,9 +827,13 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
       WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
     }
     WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+    const bool cfgr = cfg_on(rs->req.guidance);
+    if (cfgr) WK(encode_negative(ctx, me, rs, me->ebuf[b]));
+    m.guidance = cfgr ? rs->req.guidance : 1.f;
     WK(cudaEventRecord(e1, me->compute));
     m.t_end_e = now_s();
-    if (!mp_send(ctx, me, tid, me->ebuf[b], ctx->ctx_bytes, ctx->g.chunk_bytes[0], me->compute, m, 0)) {
+    if (!mp_send(ctx, me, tid, me->ebuf[b], (cfgr ? 2 : 1) * ctx->ctx_bytes, ctx->g.chunk_bytes[0], me->compute, m,
+                 0)) {
       free_req(rs);
       return;
     }
@@ -839,11 +863,14 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     g_launches->fetch_add(1);
     WK(gen_noise(x, latent_elems(me->m.c), m.seed, me->compute));
     WK(cudaEventRecord(r0, me->compute));  // consumer ready for ctx
-    WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->ctx_bytes));
+    const bool cfgr = cfg_on(m.guidance);
+    WK(mp_wait_chunks(ctx, me, m, me->compute, (cfgr ? 2 : 1) * ctx->ctx_bytes));
     WK(cudaEventRecord(w0, me->compute));  // ctx landed
     std::vector<float> sig = sigmas_host(S, m.shift);
     Cond cd;
-    WK(me->m.prepare(me->slots.slots[m.slot].buf, sig.data(), S, me->compute, &cd));
+    const void* cbuf = me->slots.slots[m.slot].buf;
+    WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->ctx_bytes : nullptr,
+                     cfgr ? m.guidance : 1.f));
     WK(mp_release_slot(ctx, me, m.slot, me->compute));
     for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
     WK(cudaEventRecord(t1, me->compute));
@@ -1371,7 +1398,8 @@ df_status df_init(const df_graph* g, df_ctx** out) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, I.stage == DF_T ? lo : hi);
     cudaStreamCreateWithPriority(&I.comm, cudaStreamNonBlocking, hi);
-    size_t slot_bytes = I.stage == DF_T ? ctx->ctx_bytes : (I.stage == DF_D ? ctx->lat_bytes : 0);
+    // T receive slots and E send buffers hold up to two ctx (prompt + negative prompt, CFG)
+    size_t slot_bytes = I.stage == DF_T ? 2 * ctx->ctx_bytes : (I.stage == DF_D ? ctx->lat_bytes : 0);
     if (slot_bytes) {
       I.slots.slots.resize(g->n_slots);
       for (uint32_t s = 0; s < g->n_slots; ++s) {
@@ -1389,11 +1417,11 @@ df_status df_init(const df_graph* g, df_ctx** out) {
       }
     } else if (I.stage == DF_E) {
       for (int b = 0; b < 2; ++b) {
-        cudaMalloc(&I.ebuf[b], ctx->ctx_bytes);
+        cudaMalloc(&I.ebuf[b], 2 * ctx->ctx_bytes);
         cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming);
         cudaEventRecord(I.esent[b], I.comm);
       }
-      cudaMalloc(&I.ids_dev, size_t(c.L_txt) * 4);
+      cudaMalloc(&I.ids_dev, 2 * size_t(c.L_txt) * 4);
     } else {
       cudaMalloc(&I.dout, ctx->out_bytes);
       cudaHostAlloc(&I.stage_host, ctx->out_bytes, cudaHostAllocPortable);
@@ -1511,6 +1539,7 @@ df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
   rs->id = id;
   rs->t_submit = now_s();
   if (r->token_ids) rs->ids.assign(r->token_ids, r->token_ids + ctx->g.dit.L_txt);
+  if (r->neg_token_ids) rs->neg_ids.assign(r->neg_token_ids, r->neg_token_ids + ctx->g.dit.L_txt);
   // timing events are created by each stage worker on its own device
   {
     std::lock_guard<std::mutex> lk(ctx->req_mu);
@@ -1591,6 +1620,24 @@ df_status df_dit_prepare(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const
     c->c.mem.release();
     delete c;
     return fail(ctx, std::string("df_dit_prepare: ") + cudaGetErrorString(e) + " " + df::tls_err);
+  }
+  *out = c;
+  return DF_OK;
+}
+
+df_status df_dit_prepare_cfg(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const void* ctx_neg_dev,
+                             float guidance, const float* sigmas, uint32_t S, void* stream, df_cond** out) {
+  Inst* I = get_inst(ctx, t_inst, DF_T);
+  if (!I || !ctx_dev || !ctx_neg_dev || !sigmas || !S || !out)
+    return fail(ctx, "df_dit_prepare_cfg: invalid", DF_ERR_INVALID);
+  if (ctx->failed) return DF_ERR_STATE;
+  auto c = new df_cond();
+  c->inst = t_inst;
+  cudaError_t e = I->m.prepare(ctx_dev, sigmas, int(S), (cudaStream_t)stream, &c->c, ctx_neg_dev, guidance);
+  if (e != cudaSuccess) {
+    c->c.mem.release();
+    delete c;
+    return fail(ctx, std::string("df_dit_prepare_cfg: ") + cudaGetErrorString(e) + " " + df::tls_err);
   }
   *out = c;
   return DF_OK;

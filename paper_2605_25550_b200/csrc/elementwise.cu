@@ -95,12 +95,13 @@ cudaError_t gen_noise(float* x, size_t n, uint64_t seed, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-__global__ void tokens_kernel(int32_t* ids, int n, int vocab, uint64_t seed) {
+__global__ void tokens_kernel(int32_t* ids, int n, int vocab, uint64_t seed, uint32_t c3) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) ids[j] = int32_t(philox_word(seed, j, 0, 2) % uint32_t(vocab));
+  if (j < n) ids[j] = int32_t(philox_word(seed, j, 0, c3) % uint32_t(vocab));
 }
-cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st) {
-  tokens_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, vocab, seed);
+// stream c3 = 2: prompt tokens; c3 = 4: negative-prompt tokens
+cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st, uint32_t stream_c3) {
+  tokens_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, vocab, seed, stream_c3);
   return cudaGetLastError();
 }
 
@@ -110,6 +111,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
                                                       const float* __restrict__ shift, const float* __restrict__ scale,
                                                       const bf16* __restrict__ gain, float eps) {
   // one CTA per row; each thread holds up to 8 float4 (d <= 8192)
+  pdl_wait();
+  pdl_launch_dependents();
   const int row = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
   const int nv = d / 4;
@@ -165,9 +168,9 @@ cudaError_t rmsnorm_mod(const float* x, void* out, int out_f32, int M, int d, co
                         const bf16* gain, float eps, cudaStream_t st) {
   if (d % 4 || d > 8192) return cudaErrorInvalidValue;
   if (M <= 0) return cudaSuccess;
-  if (out_f32) rmsnorm_kernel<float><<<M, 256, 0, st>>>(x, (float*)out, d, shift, scale, gain, eps);
-  else rmsnorm_kernel<bf16><<<M, 256, 0, st>>>(x, (bf16*)out, d, shift, scale, gain, eps);
-  return cudaGetLastError();
+  void* args[] = {(void*)&x, (void*)&out, (void*)&d, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
+  if (out_f32) return launch_ex((const void*)rmsnorm_kernel<float>, dim3(M), dim3(256), 0, st, args);
+  return launch_ex((const void*)rmsnorm_kernel<bf16>, dim3(M), dim3(256), 0, st, args);
 }
 
 // ------------------------------------------------------------------ patchify
@@ -238,6 +241,24 @@ cudaError_t modulations(const float* e6, const float* e, const bf16* const* laye
     modulations_kernel<<<grid, 256, 0, st>>>(e6, e, mp, l0, nl, head_mod, d, mods, l0 == 0 ? head : nullptr);
   }
   return cudaGetLastError();
+}
+
+__global__ void cfg_euler_kernel(float* __restrict__ x, const float* __restrict__ vb, float* __restrict__ v_out,
+                                 size_t n, float g, float dsig) {
+  pdl_wait();
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float vc = vb[i], vu = vb[n + i];
+    const float v = vu + g * (vc - vu);  // classifier-free guidance (NEXT-2)
+    if (v_out) v_out[i] = v;
+    x[i] += dsig * v;
+  }
+}
+cudaError_t cfg_euler(float* x, const float* v_batch, float* v_out, size_t n, float guidance, float dsig,
+                      cudaStream_t st) {
+  unsigned b = unsigned((n + 255) / 256);
+  if (b > 148 * 8) b = 148 * 8;
+  void* args[] = {(void*)&x, (void*)&v_batch, (void*)&v_out, (void*)&n, (void*)&guidance, (void*)&dsig};
+  return launch_ex((const void*)cfg_euler_kernel, dim3(b), dim3(256), 0, st, args);
 }
 
 __global__ void silu_kernel(float* x, size_t n) {

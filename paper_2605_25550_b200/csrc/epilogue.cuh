@@ -42,6 +42,11 @@ struct Epi {
   float* v_out;
   float dsig;
   int C, pt, ph, pw, Hl, Wl, Fl;  // latent geometry
+  // batch of samples stacked along M (classifier-free guidance: conditional, negative):
+  // rows per sample; HEADS writes sample-major [b][heads][Mper][dh_pad]; EULER with
+  // v_batch stores v of sample b at v_batch[b * latent_elems + idx] instead of updating x.
+  int Mper;
+  float* v_batch;
 };
 
 DF_DEV float bias_at(const Epi& e, int n) { return e.bias ? bf2f(e.bias[n]) : 0.0f; }
@@ -149,6 +154,9 @@ DF_DEV void epi_apply(const Epi& e, int m, int n0, float* v) {
     if (n0 >= e.N) return;
     const int sec = n0 / e.d;
     const int hd = (n0 - sec * e.d) / e.dh;
+    const int mper = e.Mper > 0 ? e.Mper : e.M;
+    const int bsm = m / mper;     // sample of the stacked batch
+    m -= bsm * mper;              // token within the sample (RoPE position, row)
 #pragma unroll
     for (int i = 0; i < CW; ++i) v[i] += bias_at(e, n0 + i);
     const bf16* g = e.sec_gain[sec];
@@ -170,10 +178,13 @@ DF_DEV void epi_apply(const Epi& e, int m, int n0, float* v) {
         v[2 * p + 1] = a * cs.y + b * cs.x;
       }
     }
-    OutT* o = reinterpret_cast<OutT*>(e.sec_out[sec]) + (size_t(hd) * e.M + m) * e.dh_pad;
+    OutT* o = reinterpret_cast<OutT*>(e.sec_out[sec]) + ((size_t(bsm) * e.heads + hd) * mper + m) * e.dh_pad;
     store_vec<CW>(o, v);
   } else if (e.kind == EPI_EULER) {
     // token m = (f*Hp + hh)*Wp + ww ; column p = ((c*pt + i)*ph + j)*pw + k
+    const int mper = e.Mper > 0 ? e.Mper : e.M;
+    const int bsm = m / mper;
+    m -= bsm * mper;
     int hw = e.Hp * e.Wp;
     int f = m / hw, rem = m - f * hw;
     int hh = rem / e.Wp, ww = rem - hh * e.Wp;
@@ -187,6 +198,10 @@ DF_DEV void epi_apply(const Epi& e, int m, int n0, float* v) {
         int c = t / e.pt;
         size_t idx = ((size_t(c) * e.Fl + (f * e.pt + ii)) * e.Hl + (hh * e.ph + j)) * e.Wl + (ww * e.pw + k);
         float vel = v[i] + bias_at(e, p);
+        if (e.v_batch) {
+          e.v_batch[size_t(bsm) * e.C * e.Fl * e.Hl * e.Wl + idx] = vel;
+          continue;
+        }
         if (e.v_out) e.v_out[idx] = vel;
         e.x_lat[idx] += e.dsig * vel;
       }

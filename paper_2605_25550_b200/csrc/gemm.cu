@@ -64,6 +64,25 @@ bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, u
 }
 
 int g_disable_pair = 0;
+int g_pdl = -1;
+
+cudaError_t launch_ex(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void** args) {
+  if (g_pdl < 0) {
+    const char* e = getenv("DF_PDL");
+    g_pdl = e ? atoi(e) : 0;  // measured: no gain on the image step, off by default
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
 
 int num_sms() {
   static int n = 0;
@@ -142,6 +161,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -243,8 +264,8 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M
   }
   int tiles = ((M + GBM - 1) / GBM) * ((N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, epi);
-  return cudaGetLastError();
+  void* args[] = {(void*)&ta, (void*)&tb, (void*)&M, (void*)&N, (void*)&K, (void*)&epi};
+  return launch_ex((const void*)kern, dim3(grid), dim3(256), Cfg::SMEM, st, args);
 }
 
 
@@ -303,6 +324,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -406,8 +429,8 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int 
   int tiles = ((M + 255) / 256) * ((N + 255) / 256);
   int pairs = num_sms() / 2;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, 256, P_SMEM, st>>>(ta, tb, M, N, K, epi);
-  return cudaGetLastError();
+  void* args[] = {(void*)&ta, (void*)&tb, (void*)&M, (void*)&N, (void*)&K, (void*)&epi};
+  return launch_ex((const void*)kern, dim3(grid), dim3(256), P_SMEM, st, args);
 }
 
 static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,

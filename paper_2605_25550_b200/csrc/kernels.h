@@ -8,6 +8,9 @@
 namespace df {
 
 int num_sms();
+extern int g_pdl;  // 1: launch the hot kernels with programmatic dependent launch (DF_PDL=1; default off)
+// Launch helper: cudaLaunchKernelEx with optional PDL attribute.
+cudaError_t launch_ex(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void** args);
 extern int g_disable_pair;  // 1: never use the CTA-pair GEMM (tests)
 
 // ---- tensor-core GEMM: out = epilogue(A[M,K] (bf16, row-major, lda) x W[N,K]^T (bf16, ldw)).
@@ -23,11 +26,15 @@ cudaError_t epi_rows(const float* tmp, const Epi& epi, int out_f32, cudaStream_t
 
 // ---- attention: O[n, h*dh + c] = softmax(Q_h K_h^T * scale) V_h
 // Q/K/V head-major [H][Nq|Nk][dh_pad] bf16; O token-major [Nq, H*dh] bf16.
+// heads_per_sample (0 = H): H counts the heads of a stacked batch (B = H / heads_per_sample
+// samples, sample-major [b][h]); O rows are b*Nq + q with heads_per_sample*dh columns.
 cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
-                    float scale, cudaStream_t st);
+                    float scale, cudaStream_t st, int heads_per_sample = 0);
 // fp32 validation build: same layout with float and dh_pad == dh.
 cudaError_t attn_simt(const float* Q, const float* K, const float* V, float* O, int H, int Nq, int Nk, int dh,
-                      float scale, cudaStream_t st);
+                      float scale, cudaStream_t st, int heads_per_sample = 0);
+// x += dsig * (v_u + g (v_c - v_u)) with v_batch = [v_c | v_u]; v_out (optional) gets the guided v
+cudaError_t cfg_euler(float* x, const float* v_batch, float* v_out, size_t n, float guidance, float dsig, cudaStream_t st);
 
 // ---- elementwise
 // out[m, :] = RMSNorm(x[m, :]) * (1 + scale) + shift     (mode 0; scale/shift fp32 [d])
@@ -61,7 +68,7 @@ struct InitSpec {
 };
 cudaError_t init_tensor(bf16* dst, const InitSpec& s, cudaStream_t st);
 cudaError_t gen_noise(float* x, size_t n, uint64_t seed, cudaStream_t st);
-cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st);
+cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st, uint32_t stream_c3 = 2);
 
 // ---- E / D stand-ins
 cudaError_t embed_rows(const int32_t* ids, const bf16* emb, float* z, int L, int dt, cudaStream_t st);

@@ -161,26 +161,31 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
   size_t wsb = 0;
   const size_t Nn = N;
   if (stage == DF_T) {
-    size_t hd = size_t(c.heads) * Nn * dhp * ab;
-    wsb = al(Nn * d * 4) + al(Nn * d * ab) + 4 * al(hd) + al(Nn * d * ab) + al(Nn * f * ab) + al(Nn * P * ab) +
-          al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8);
-    if (f32()) wsb += al(Nn * std::max(3 * d, 2 * f) * 4);
+    // activations sized for a batch of 2 (classifier-free guidance stacks cond + negative)
+    const size_t N2 = 2 * Nn;
+    size_t hd = size_t(c.heads) * N2 * dhp * ab;
+    wsb = al(N2 * d * 4) + al(N2 * d * ab) + 4 * al(hd) + al(N2 * d * ab) + al(N2 * f * ab) + al(Nn * P * ab) +
+          al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
+          al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
+    if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
   } else if (stage == DF_E) {
     wsb = al(L * dt * 4) + al(L * dt * ab) + al(L * fe * ab) + al(L * 2 * fe * 4);
   }
   DF_TRY(ws.reserve(wsb + 4096));
   if (stage == DF_T) {
-    size_t hd = size_t(c.heads) * Nn * dhp * ab;
-    r = (float*)ws.take(Nn * d * 4);
-    h = ws.take(Nn * d * ab);
+    const size_t N2 = 2 * Nn;
+    size_t hd = size_t(c.heads) * N2 * dhp * ab;
+    r = (float*)ws.take(N2 * d * 4);
+    h = ws.take(N2 * d * ab);
     q = ws.take(hd); k = ws.take(hd); v = ws.take(hd); qc = ws.take(hd);
-    o = ws.take(Nn * d * ab);
-    a = ws.take(Nn * f * ab);
+    o = ws.take(N2 * d * ab);
+    a = ws.take(N2 * f * ab);
     X = ws.take(Nn * P * ab);
+    vbatch = (float*)ws.take(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
     headmod = (float*)ws.take(2 * d * 4);
     rope = (float2*)ws.take(size_t(Fp + Hp + Wp) * dh / 2 * 8 + 64);
-    if (f32()) tmp = (float*)ws.take(Nn * std::max(3 * d, 2 * f) * 4);
+    if (f32()) tmp = (float*)ws.take(N2 * std::max(3 * d, 2 * f) * 4);
     // zero the head-major buffers once: the dh..dhp padding must stay 0 (TMA reads it)
     DF_TRY(cudaMemset(q, 0, 4 * al(hd)));
     // RoPE table in fp64 -> fp32 (R7): (cos, sin)(pos_a * theta^(-2j/D_a))
@@ -311,13 +316,15 @@ cudaError_t Model::gemm(const void* A, int lda, const bf16* Wt, int ldw, int M, 
   return cudaSuccess;
 }
 
-cudaError_t Model::attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st) {
+cudaError_t Model::attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st,
+                        int B) {
   const float scale = 1.0f / std::sqrt(float(dh));
-  ProfScope ps(prof, st, cur_kind, 4.0 * Nq * double(Nk) * dh * c.heads, 0.0);
+  const int Ht = B * int(c.heads);  // a stacked batch is B x heads sample-major heads
+  ProfScope ps(prof, st, cur_kind, 4.0 * Nq * double(Nk) * dh * Ht, 0.0);
   if (!f32()) {
-    DF_L(attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, c.heads, Nq, Nk, dh, dhp, scale, st));
+    DF_L(attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, Ht, Nq, Nk, dh, dhp, scale, st, c.heads));
   } else {
-    DF_L(attn_simt((const float*)Q, (const float*)K, (const float*)V, (float*)O, c.heads, Nq, Nk, dh, scale, st));
+    DF_L(attn_simt((const float*)Q, (const float*)K, (const float*)V, (float*)O, Ht, Nq, Nk, dh, scale, st, c.heads));
   }
   return cudaSuccess;
 }
@@ -332,8 +339,9 @@ static Epi epi_base(int kind, int M, int N) {
 }
 
 Epi Model::heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0, int rope0, void* o1,
-                     const bf16* g1, int rope1, void* o2, const bf16* g2, int rope2) const {
+                     const bf16* g1, int rope1, void* o2, const bf16* g2, int rope2, int Mper) const {
   Epi e = epi_base(EPI_HEADS, M, nsec * c.d);
+  e.Mper = Mper > 0 ? Mper : M;
   e.bias = bias;
   e.d = c.d;
   e.heads = c.heads;
@@ -358,17 +366,20 @@ cudaError_t Model::norm(const float* x, void* out, int M, int dd, const float* s
 }
 
 // ------------------------------------------------------------------ prologue (a1)
-cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out) {
+cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
+                           const void* ctx_neg_bf16, float guidance) {
   const int d = c.d, Lt = c.L_txt, dt = c.d_txt, fd = c.freq_dim;
   const size_t ab = act_bytes();
   Cond& cd = *out;
   cd.S = S;
   cd.device = device;
+  cd.B = ctx_neg_bf16 ? 2 : 1;
+  cd.guidance = guidance;
   cd.sig.assign(sig_host, sig_host + S + 1);
-  size_t kvb = size_t(c.layers) * c.heads * Lt * dhp * ab;
+  size_t kvb = size_t(c.layers) * cd.B * c.heads * Lt * dhp * ab;
   size_t need = al((S + 1) * 4) + 2 * al(kvb) + al(size_t(S) * d * 4) + al(size_t(S) * 6 * d * 4) +
                 al(size_t(S) * fd * 4) + al(size_t(S) * d * 4) + 2 * al(size_t(Lt) * d * ab) +
-                al(size_t(Lt) * dt * 4) + (f32() ? al(size_t(Lt) * 2 * d * 4) : 0) + 4096;
+                (f32() ? al(size_t(Lt) * 2 * d * 4) : 0) + 4096;
   DF_TRY(cd.mem.reserve(need));
   cd.sig_dev = (float*)cd.mem.take((S + 1) * 4);
   cd.kc = cd.mem.take(kvb);
@@ -379,9 +390,8 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   float* t1 = (float*)cd.mem.take(size_t(S) * d * 4);
   void* c1 = cd.mem.take(size_t(Lt) * d * ab);
   void* cp = cd.mem.take(size_t(Lt) * d * ab);
-  float* ctx32 = (float*)cd.mem.take(size_t(Lt) * dt * 4);
   float* ptmp = f32() ? (float*)cd.mem.take(size_t(Lt) * 2 * d * 4) : nullptr;
-  if (!cd.e6) return cudaErrorMemoryAllocation;
+  if (!cp) return cudaErrorMemoryAllocation;
   if (!f32()) DF_TRY(cudaMemsetAsync(cd.kc, 0, 2 * al(kvb), st));  // dh padding = 0
   DF_TRY(cudaMemcpyAsync(cd.sig_dev, sig_host, (S + 1) * 4, cudaMemcpyHostToDevice, st));
   // time conditioning for all S steps (R4, R5), fp32 SIMT: the M = S rows are GEMV-like
@@ -389,117 +399,122 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   DF_L(gemm_simt(s, 0, fd, ACT_NONE, temb1_wT, fd, t1, d, S, d, fd, temb1_b, ACT_SILU, st));
   DF_L(gemm_simt(t1, 0, d, ACT_NONE, temb2_wT, d, cd.e, d, S, d, d, temb2_b, ACT_NONE, st));
   DF_L(gemm_simt(cd.e, 0, d, ACT_SILU, tmod_wT, d, cd.e6, 6 * d, S, 6 * d, d, tmod_b, ACT_NONE, st));
-  // text projection ctx' = GELU(ctx W1 + b1) W2 + b2
-  Epi e1 = epi_base(EPI_STORE, Lt, d);
-  e1.bias = txt1_b;
-  e1.act = ACT_GELU;
-  e1.out = c1;
-  e1.ldo = d;
-  Epi e2 = epi_base(EPI_STORE, Lt, d);
-  e2.bias = txt2_b;
-  e2.out = cp;
-  e2.ldo = d;
-  if (!f32()) {
-    DF_L(gemm_tc((const bf16*)ctx_bf16, dt, txt1_wT, dt, Lt, d, dt, e1, 0, st));
-    DF_L(gemm_tc((const bf16*)c1, d, txt2_wT, d, Lt, d, d, e2, 0, st));
-  } else {
-    DF_L(gemm_simt(ctx_bf16, 1, dt, 0, txt1_wT, dt, ptmp, d, Lt, d, dt, nullptr, ACT_NONE, st));
-    DF_L(epi_rows(ptmp, e1, 1, st));
-    DF_L(gemm_simt(c1, 0, d, 0, txt2_wT, d, ptmp, d, Lt, d, d, nullptr, ACT_NONE, st));
-    DF_L(epi_rows(ptmp, e2, 1, st));
-  }
-  (void)ctx32;
-  // cross K/V for every layer: [K | V] = ctx' [Wck | Wcv]^T; K <- headRMS * g_ck
-  const size_t per = size_t(c.heads) * Lt * dhp * ab;
-  for (int l = 0; l < c.layers; ++l) {
-    void* kl = (char*)cd.kc + l * per;
-    void* vl = (char*)cd.vc + l * per;
-    Epi e = heads_epi(Lt, 2, Lw[l].ckv_b, kl, Lw[l].g_ck, 0, vl, nullptr, 0, nullptr, nullptr, 0);
+  // per context b (0: prompt, 1: negative prompt): ctx' = GELU(ctx W1 + b1) W2 + b2, then
+  // [K | V] = ctx' [Wck | Wcv]^T per layer, K <- headRMS * g_ck, into sample-major heads
+  const size_t per = size_t(cd.B) * c.heads * Lt * dhp * ab;     // one layer
+  const size_t per_b = size_t(c.heads) * Lt * dhp * ab;          // one sample of one layer
+  for (int b = 0; b < cd.B; ++b) {
+    const void* ctxb = b == 0 ? ctx_bf16 : ctx_neg_bf16;
+    Epi e1 = epi_base(EPI_STORE, Lt, d);
+    e1.bias = txt1_b;
+    e1.act = ACT_GELU;
+    e1.out = c1;
+    e1.ldo = d;
+    Epi e2 = epi_base(EPI_STORE, Lt, d);
+    e2.bias = txt2_b;
+    e2.out = cp;
+    e2.ldo = d;
     if (!f32()) {
-      DF_L(gemm_tc((const bf16*)cp, d, Lw[l].ckv_wT, d, Lt, 2 * d, d, e, 0, st));
+      DF_L(gemm_tc((const bf16*)ctxb, dt, txt1_wT, dt, Lt, d, dt, e1, 0, st));
+      DF_L(gemm_tc((const bf16*)c1, d, txt2_wT, d, Lt, d, d, e2, 0, st));
     } else {
-      DF_L(gemm_simt(cp, 0, d, 0, Lw[l].ckv_wT, d, ptmp, 2 * d, Lt, 2 * d, d, nullptr, ACT_NONE, st));
-      DF_L(epi_rows(ptmp, e, 1, st));
+      DF_L(gemm_simt(ctxb, 1, dt, 0, txt1_wT, dt, ptmp, d, Lt, d, dt, nullptr, ACT_NONE, st));
+      DF_L(epi_rows(ptmp, e1, 1, st));
+      DF_L(gemm_simt(c1, 0, d, 0, txt2_wT, d, ptmp, d, Lt, d, d, nullptr, ACT_NONE, st));
+      DF_L(epi_rows(ptmp, e2, 1, st));
+    }
+    for (int l = 0; l < c.layers; ++l) {
+      void* kl = (char*)cd.kc + l * per + b * per_b;
+      void* vl = (char*)cd.vc + l * per + b * per_b;
+      Epi e = heads_epi(Lt, 2, Lw[l].ckv_b, kl, Lw[l].g_ck, 0, vl, nullptr, 0, nullptr, nullptr, 0);
+      if (!f32()) {
+        DF_L(gemm_tc((const bf16*)cp, d, Lw[l].ckv_wT, d, Lt, 2 * d, d, e, 0, st));
+      } else {
+        DF_L(gemm_simt(cp, 0, d, 0, Lw[l].ckv_wT, d, ptmp, 2 * d, Lt, 2 * d, d, nullptr, ACT_NONE, st));
+        DF_L(epi_rows(ptmp, e, 1, st));
+      }
     }
   }
   return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ one block (a3-a10)
+// res holds B x N rows (sample-major); every GEMM runs over all B*N rows, the heads are
+// sample-major [b][h][N][dh] so attention treats the batch as B*H heads.
 cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t st) {
-  const int d = c.d, f = c.ffn, Lt = c.L_txt;
+  const int d = c.d, f = c.ffn, Lt = c.L_txt, B = cd.B, M = B * N;
   const int of = f32() ? 1 : 0;
   const LayerW& w = Lw[l];
   const float* md = mods + size_t(l) * 6 * d;  // sh1, sc1, g1, sh2, sc2, g2
-  const size_t per = size_t(c.heads) * Lt * dhp * act_bytes();
+  const size_t per = size_t(B) * c.heads * Lt * dhp * act_bytes();
   // a4: h = RMSNorm(r)(1 + sc1) + sh1
-  DF_TRY(norm(res, h, N, d, md + 0 * d, md + 1 * d, nullptr, st));
+  DF_TRY(norm(res, h, M, d, md + 0 * d, md + 1 * d, nullptr, st));
   // a5: q,k,v = heads(h Wqkv + b); qk-RMSNorm * g; RoPE3 on q, k
   {
-    Epi e = heads_epi(N, 3, w.qkv_b, q, w.g_q, 1, k, w.g_k, 1, v, nullptr, 0);
+    Epi e = heads_epi(M, 3, w.qkv_b, q, w.g_q, 1, k, w.g_k, 1, v, nullptr, 0, N);
     cur_kind = K_QKV;
-    DF_TRY(gemm(h, d, w.qkv_wT, d, N, 3 * d, d, e, of, st));
+    DF_TRY(gemm(h, d, w.qkv_wT, d, M, 3 * d, d, e, of, st));
   }
-  // a6: self-attention
+  // a6: self-attention (per sample)
   cur_kind = K_ATTN_SELF;
-  DF_TRY(attn(q, k, v, o, N, N, st));
+  DF_TRY(attn(q, k, v, o, N, N, st, B));
   // a7: r += g1 * (o Wo + bo)
   {
-    Epi e = epi_base(EPI_GRES, N, d);
+    Epi e = epi_base(EPI_GRES, M, d);
     e.bias = w.o_b;
     cur_kind = K_O;
     e.resid = res;
     e.ldr = d;
     e.gate = md + 2 * d;
-    DF_TRY(gemm(o, d, w.o_wT, d, N, d, d, e, of, st));
+    DF_TRY(gemm(o, d, w.o_wT, d, M, d, d, e, of, st));
   }
   // a8: cross-attention: hc = RMSNorm(r) g_n3; qc = headRMS(hc Wcq + b) g_cq; r += attn Wco + b
-  DF_TRY(norm(res, h, N, d, nullptr, nullptr, w.g_n3, st));
+  DF_TRY(norm(res, h, M, d, nullptr, nullptr, w.g_n3, st));
   {
-    Epi e = heads_epi(N, 1, w.cq_b, qc, w.g_cq, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
+    Epi e = heads_epi(M, 1, w.cq_b, qc, w.g_cq, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, N);
     cur_kind = K_CQ;
-    DF_TRY(gemm(h, d, w.cq_wT, d, N, d, d, e, of, st));
+    DF_TRY(gemm(h, d, w.cq_wT, d, M, d, d, e, of, st));
   }
   cur_kind = K_ATTN_CROSS;
-  DF_TRY(attn(qc, (const char*)cd.kc + l * per, (const char*)cd.vc + l * per, o, N, Lt, st));
+  DF_TRY(attn(qc, (const char*)cd.kc + l * per, (const char*)cd.vc + l * per, o, N, Lt, st, B));
   {
-    Epi e = epi_base(EPI_GRES, N, d);
+    Epi e = epi_base(EPI_GRES, M, d);
     e.bias = w.co_b;
     cur_kind = K_CO;
     e.resid = res;
     e.ldr = d;
-    DF_TRY(gemm(o, d, w.co_wT, d, N, d, d, e, of, st));
+    DF_TRY(gemm(o, d, w.co_wT, d, M, d, d, e, of, st));
   }
   // a9: h2 = RMSNorm(r)(1 + sc2) + sh2
-  DF_TRY(norm(res, h, N, d, md + 3 * d, md + 4 * d, nullptr, st));
+  DF_TRY(norm(res, h, M, d, md + 3 * d, md + 4 * d, nullptr, st));
   // a10: a = SiLU(h2 W1 + b1) * (h2 W3 + b3);  r += g2 * (a W2 + b2)
   {
-    Epi e = epi_base(EPI_SWIGLU, N, 2 * f);
+    Epi e = epi_base(EPI_SWIGLU, M, 2 * f);
     e.bias = w.b13;
     cur_kind = K_UP;
     e.out = a;
     e.ldo = f;
-    DF_TRY(gemm(h, d, w.w13T, d, N, 2 * f, d, e, of, st));
+    DF_TRY(gemm(h, d, w.w13T, d, M, 2 * f, d, e, of, st));
   }
   {
-    Epi e = epi_base(EPI_GRES, N, d);
+    Epi e = epi_base(EPI_GRES, M, d);
     e.bias = w.b2;
     cur_kind = K_DOWN;
     e.resid = res;
     e.ldr = d;
     e.gate = md + 5 * d;
-    DF_TRY(gemm(a, f, w.w2T, f, N, d, f, e, of, st));
+    DF_TRY(gemm(a, f, w.w2T, f, M, d, f, e, of, st));
   }
   return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ one step (a2-a12)
 cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStream_t st) {
-  const int d = c.d;
+  const int d = c.d, B = cd.B, M = B * N;
   const int of = f32() ? 1 : 0;
   DF_L(modulations(cd.e6 + size_t(i) * 6 * d, cd.e + size_t(i) * d, layer_mods.data(), c.layers, head_mod, d, mods,
                    headmod, st));
-  // a2: r = patchify(x) Wpe + bpe   (fp32 residual)
+  // a2: r = patchify(x) Wpe + bpe   (fp32 residual); a CFG batch starts both samples from it
   DF_L(patchify(x, X, of, c.C, c.F, c.H, c.W, c.pt, c.ph, c.pw, st));
   {
     Epi e = epi_base(EPI_STORE, N, d);
@@ -509,11 +524,12 @@ cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStrea
     e.ldo = d;
     DF_TRY(gemm(X, P, patch_wT, P, N, d, P, e, 1, st));
   }
+  if (B == 2) DF_TRY(cudaMemcpyAsync(r + size_t(N) * d, r, size_t(N) * d * 4, cudaMemcpyDeviceToDevice, st));
   for (int l = 0; l < c.layers; ++l) DF_TRY(block(cd, i, l, r, st));
   // a11 + a12: head modulation, projection, unpatchify, Euler update fused in the epilogue
-  DF_TRY(norm(r, h, N, d, headmod, headmod + d, nullptr, st));
+  DF_TRY(norm(r, h, M, d, headmod, headmod + d, nullptr, st));
   {
-    Epi e = epi_base(EPI_EULER, N, P);
+    Epi e = epi_base(EPI_EULER, M, P);
     e.bias = head_b;
     cur_kind = K_HEAD;
     e.x_lat = x;
@@ -521,7 +537,11 @@ cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStrea
     e.dsig = float(double(cd.sig[i + 1]) - double(cd.sig[i]));
     e.C = c.C; e.pt = c.pt; e.ph = c.ph; e.pw = c.pw; e.Hl = c.H; e.Wl = c.W; e.Fl = c.F;
     e.Hp = Hp; e.Wp = Wp;
-    DF_TRY(gemm(h, d, head_wT, d, N, P, d, e, 1, st));
+    e.Mper = N;
+    if (B == 2) e.v_batch = vbatch;  // v of both samples; guidance + Euler below
+    DF_TRY(gemm(h, d, head_wT, d, M, P, d, e, 1, st));
+    if (B == 2)
+      DF_L(cfg_euler(x, vbatch, v_out, size_t(c.C) * c.F * c.H * c.W, cd.guidance, e.dsig, st));
   }
   return cudaSuccess;
 }

@@ -37,7 +37,7 @@ struct alignas(8) MetaRec {
   uint32_t flags;
   double t_submit, t_start_e, t_end_e, t_end_t;  // host CLOCK_MONOTONIC (node-wide)
   float stage_ms_e, stage_ms_t, exposed_t;
-  uint32_t pad;
+  float guidance;                                 // CFG scale (payload holds 2 ctx when on)
   uint64_t hash_src;                              // payload hash computed by the producer
 };
 static_assert(sizeof(MetaRec) <= 128, "metadata record must stay fixed-size");

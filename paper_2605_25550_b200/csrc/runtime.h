@@ -87,6 +87,8 @@ struct Cond {
   float* e6 = nullptr;      // [S, 6d]
   Arena mem;
   int device = 0;
+  int B = 1;                // 2: classifier-free guidance (conditional, negative prompt)
+  float guidance = 1.f;
 };
 
 struct Model {
@@ -122,6 +124,7 @@ struct Model {
   float* mods = nullptr;    // [layers][6][d]
   float* headmod = nullptr; // [2][d]
   float2* rope = nullptr;
+  float* vbatch = nullptr;  // [2][C,F,H,W] velocities of a CFG batch
   // encoder workspace
   float* ez = nullptr;      // [L, d_txt]
   void* ea = nullptr;       // [L, d_txt]
@@ -137,7 +140,8 @@ struct Model {
   bool f32() const { return precision == DF_FP32_VALIDATION; }
   size_t act_bytes() const { return f32() ? 4 : 2; }
 
-  cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out);
+  cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
+                      const void* ctx_neg_bf16 = nullptr, float guidance = 1.f);
   cudaError_t step(const Cond& c, int i, float* x, float* v_out, cudaStream_t st);
   cudaError_t layer(const Cond& c, int i, int l, float* r_io, cudaStream_t st);
   cudaError_t encode(const int32_t* ids, void* ctx_bf16, cudaStream_t st);
@@ -146,9 +150,9 @@ struct Model {
   // helpers
   cudaError_t gemm(const void* A, int lda, const bf16* W, int ldw, int M, int Nn, int K, const Epi& e, int out_f32,
                    cudaStream_t st);
-  cudaError_t attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st);
+  cudaError_t attn(const void* Q, const void* K, const void* V, void* O, int Nq, int Nk, cudaStream_t st, int B = 1);
   Epi heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0, int rope0, void* o1, const bf16* g1,
-                int rope1, void* o2, const bf16* g2, int rope2) const;
+                int rope1, void* o2, const bf16* g2, int rope2, int Mper = 0) const;
   cudaError_t block(const Cond& c, int i, int l, float* r, cudaStream_t st);
   cudaError_t norm(const float* x, void* out, int M, int dd, const float* shift, const float* scale, const bf16* gain,
                    cudaStream_t st);

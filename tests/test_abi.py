@@ -14,7 +14,7 @@ LIB = os.path.join(ROOT, "paper_2605_25550_b200", "libdf.so")
 
 def _declared():
     txt = open(HDR).read()
-    return sorted(set(re.findall(r"^\s*(?:df_status|const char\*|uint64_t)\s+(df_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:df_status|const char\*|uint64_t|int32_t)\s+(df_\w+)\s*\(", txt, re.M)))
 
 
 @pytest.fixture(scope="module")

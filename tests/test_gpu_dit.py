@@ -140,3 +140,32 @@ def test_encoder_decoder_parity(prec):
     assert rel_l2(got_ctx, want_ctx) <= (1e-2 if prec == BF16 else 4e-3)
     want_out = stages.decoder(P, cfg, lat.astype(np.float64))
     assert rel_l2(got_out, want_out) <= 1e-5
+
+
+@pytest.mark.parametrize("prec", [BF16, FP32])
+@pytest.mark.parametrize("cfg", [TINY, MID])
+def test_cfg_step_parity(cfg, prec):
+    """NEXT-2: one guided step = batch-2 DiT pass, v = v_u + g (v_c - v_u)."""
+    g = 4.5
+    x = inputs.latent(cfg, 41)
+    cb, nb = inputs.ctx_bf16(cfg, 42), inputs.ctx_bf16(cfg, 43)
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32)
+    i = 1
+    with make_ctx(cfg, precision=prec) as c:
+        cond = c.dit_prepare_cfg(1, bf16_tensor_from_bits(cb), bf16_tensor_from_bits(nb), g, sig)
+        xt = torch.from_numpy(x).cuda()
+        vt = torch.zeros_like(xt)
+        c.dit_step(1, cond, i, xt, vt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        gx, gv = xt.cpu().numpy(), vt.cpu().numpy()
+    P = OP.Params(cfg, 0)
+    s64 = sig.astype(np.float64)
+    c1 = dit.prologue(P, cfg, inputs.bf16_bits_to_f64(cb), s64)
+    c0 = dit.prologue(P, cfg, inputs.bf16_bits_to_f64(nb), s64)
+    ov = dit.velocity_cfg(P, cfg, x.astype(np.float64), i, c1, c0, g)
+    ox = dit.euler_update(x.astype(np.float64), ov, s64[i], s64[i + 1])
+    # the guided velocity amplifies the difference of two rounded velocities by g
+    tol = {BF16: 3e-2, FP32: 1e-4}[prec]
+    assert rel_l2(gv, ov) <= tol, rel_l2(gv, ov)
+    assert rel_l2(gx, ox) <= tol

@@ -88,3 +88,20 @@ def test_duplicate_and_backpressure():
     with make_ctx(cfg) as c:
         assert c.set_ratio(1, 2, 1) == B.DF_ERR_CAPACITY
         assert c.set_ratio(1, 1, 1) == B.DF_OK
+
+
+def test_pipeline_cfg_matches_oracle():
+    """NEXT-2 end to end: E encodes prompt + negative prompt, T runs the guided batch."""
+    cfg = TINY
+    P = OP.Params(cfg, 0)
+    with make_ctx(cfg) as c:
+        outs = {s: np.zeros(cfg.out_shape, np.float32) for s in (5, 6)}
+        for s in (5, 6):
+            c.submit(cfg.steps, cfg.shift, s, out_host=outs[s], user_tag=s, guidance=3.0)
+        comps = []
+        while len(comps) < 2:
+            comps += c.poll(8, 60000)
+    for x in comps:
+        assert x.hash_src[0] == x.hash_dst[0] != 0
+        want = stages.request(P, cfg, seed=int(x.user_tag), guidance=3.0)["out"]
+        assert rel_l2(outs[x.user_tag], want) <= 3e-2

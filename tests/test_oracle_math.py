@@ -233,3 +233,21 @@ def test_block_rows_matches_block():
     full = dit.block(P, cfg, 0, r0, e6, kv, pos)
     rows = np.array([0, 5, 511, 1023])
     np.testing.assert_allclose(dit.block_rows(P, cfg, 0, r0, e6, kv, pos, rows), full[rows], rtol=1e-12, atol=1e-12)
+
+
+def test_cfg_guidance_pins():
+    # g = 1 -> the conditional velocity; g = 0 -> the unconditional one; v(g) affine in g
+    cfg = with_layers(TINY, 2)
+    P = OP.Params(cfg, 0)
+    r = np.random.default_rng(11)
+    sig = dit.sigmas(cfg.steps, cfg.shift)
+    c1 = dit.prologue(P, cfg, r.normal(size=(cfg.L_txt, cfg.d_txt)), sig)
+    c0 = dit.prologue(P, cfg, r.normal(size=(cfg.L_txt, cfg.d_txt)), sig)
+    x = r.normal(size=cfg.latent_shape)
+    v1 = dit.velocity(P, cfg, x, 1, c1)
+    v0 = dit.velocity(P, cfg, x, 1, c0)
+    np.testing.assert_allclose(dit.velocity_cfg(P, cfg, x, 1, c1, c0, 1.0), v1, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(dit.velocity_cfg(P, cfg, x, 1, c1, c0, 0.0), v0, rtol=0, atol=1e-13)
+    a, b, c = (dit.velocity_cfg(P, cfg, x, 1, c1, c0, g) for g in (2.0, 5.0, 8.0))
+    np.testing.assert_allclose(c - b, b - a, atol=1e-11)       # affine in g
+    assert np.linalg.norm(v1 - v0) > 1e-3 * np.linalg.norm(v1)  # the negative prompt matters

@@ -1,0 +1,63 @@
+"""Attention microbenchmark through df_op_attention (no model): TFLOP/s of the tcgen05
+flash-attention kernel at the workload shapes.  Variants are selected by env vars
+(DF_ATTN_IMPL, DF_ATTN_POLY, DF_ATTN_SP) read once per process.
+
+    python tools/attn_bench.py --shape video
+"""
+import argparse
+import math
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_25550_b200 import binding as B  # noqa: E402
+from synth.configs import TINY  # noqa: E402
+
+SHAPES = {"video": (40, 32760, 32760), "image": (24, 4096, 4096), "cross_video": (40, 32760, 512),
+          "cross_image": (24, 4096, 512)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="video")
+    ap.add_argument("--iters", type=int, default=5)
+    a = ap.parse_args()
+    H, Nq, Nk = SHAPES[a.shape]
+    dh = 128
+    g = B.make_graph(TINY, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)])
+    with B.Context(g) as c:
+        torch.manual_seed(0)
+
+        def rmsn(t):  # RMS-normalised rows like the model's qk-norm (R6)
+            return t * torch.rsqrt(t.float().pow(2).mean(-1, keepdim=True)).to(t.dtype)
+        Q = rmsn(torch.randn(H, Nq, dh, device="cuda")).to(torch.bfloat16)
+        K = rmsn(torch.randn(H, Nk, dh, device="cuda")).to(torch.bfloat16)
+        V = torch.randn(H, Nk, dh, device="cuda").to(torch.bfloat16)
+        O = torch.empty(Nq, H * dh, device="cuda", dtype=torch.bfloat16)
+        sc = 1.0 / math.sqrt(dh)
+        c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ms = []
+        for _ in range(a.iters):
+            ev[0].record()
+            c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms.append(ev[0].elapsed_time(ev[1]))
+        rows = torch.arange(0, Nq, max(1, Nq // 7), device="cuda")[:8]
+        qf, kf, vf = Q[:, rows].float(), K.float(), V.float()
+        ref = torch.softmax(qf @ kf.transpose(1, 2) * sc, -1) @ vf
+        got = O[rows].float().view(len(rows), H, dh).transpose(0, 1)
+        err = ((got - ref).norm() / ref.norm()).item()
+        fl = 4.0 * H * Nq * Nk * dh
+        best = min(ms)
+        print({"shape": a.shape, "impl": os.environ.get("DF_ATTN_IMPL", "2"), "poly": os.environ.get("DF_ATTN_POLY", "0"),
+               "sp": os.environ.get("DF_ATTN_SP", "0"), "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
+               "rel_l2_vs_torch": f"{err:.2e}"})
+
+
+if __name__ == "__main__":
+    main()
