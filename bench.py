@@ -199,7 +199,8 @@ def run_ours(args, cfg):
     # Layout: N = 1 -> E+T+D on GPU 0; N > 1 -> one process per GPU, a DiT
     # instance on every GPU, E on GPU 0 and D on GPU N-1 (E:T:D = 1:N:1), requests cross
     # GPUs through the async chunked handoff (shared-memory rings + CUDA IPC over NVLink).
-    inst = [(local if i[2] == rank else 0, i[1], i[2]) for i in layouts.partitioned(world, args.exclusive)]
+    inst = [(local if i[2] == rank else 0, i[1], i[2])
+            for i in layouts.partitioned(world, args.exclusive, args.t_per_gpu)]
     shm = f"/df_bench_{os.environ.get('MASTER_PORT', '0')}_{os.getuid()}"
     g = B.make_graph(cfg, inst, precision=B.DF_BF16, weight_seed=0,
                      chunk_bytes=(args.chunk_ctx, args.chunk_lat), n_slots=2,
@@ -376,6 +377,7 @@ def main():
     ap.add_argument("--chunk-lat", type=int, default=256 * 1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exclusive", action="store_true", help="N>1: E and D on GPUs of their own (1:N-2:1)")
+    ap.add_argument("--t-per-gpu", type=int, default=1, help="DiT instances per GPU")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     args = ap.parse_args()

@@ -320,3 +320,29 @@ namespace df {
 DF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 DF_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 }  // namespace df
+
+namespace df {
+// ---- TMA bulk stores from shared memory (epilogue): one elected lane issues; the staging
+// buffer may be rewritten after cp.async.bulk.wait_group.read.
+DF_DEV void tma_store_2d(const void* desc, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(desc),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+DF_DEV void tma_store_3d(const void* desc, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(desc),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+// global[box] += smem[box] (element type of the tensor map, here f32), performed by the TMA unit
+DF_DEV void tma_reduce_add_2d(const void* desc, const void* src, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(desc),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+DF_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+DF_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+DF_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// 16-byte chunk j (0..7) of row r in a 128B-swizzled [rows x 128 B] staging tile
+DF_DEV uint8_t* swz128(uint8_t* base, int r, int j) { return base + r * 128 + ((j ^ (r & 7)) << 4); }
+}  // namespace df

@@ -81,6 +81,65 @@ DF_DEV float2 rope_cs(const Epi& e, int m, int pair) {
   return e.rope_tab[e.Fp * e.Df2 + e.Hp * e.Dh2 + ww * e.Dw2 + pair];
 }
 
+// EPI_HEADS math on one head: bias, per-head RMSNorm * gain (if the section has a gain),
+// RoPE (if the section rotates); m is the token within its sample (RoPE position).
+template <int CW>
+DF_DEV void heads_math(const Epi& e, int m, int n0, int sec, int hd, float* v) {
+#pragma unroll
+  for (int i = 0; i < CW; ++i) v[i] += bias_at(e, n0 + i);
+  const bf16* g = e.sec_gain[sec];
+  if (g) {
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) ss += v[i] * v[i];
+    float inv = rsqrtf(ss / float(CW) + e.eps);
+    const bf16* gg = g + hd * e.dh;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) v[i] = v[i] * inv * bf2f(gg[i]);
+  }
+  if (e.sec_rope[sec]) {
+#pragma unroll
+    for (int p = 0; p < CW / 2; ++p) {
+      float2 cs = rope_cs(e, m, p);
+      float a = v[2 * p], b = v[2 * p + 1];
+      v[2 * p] = a * cs.x - b * cs.y;
+      v[2 * p + 1] = a * cs.y + b * cs.x;
+    }
+  }
+}
+
+// heads_math with the head's bias and gain already staged as fp32 (shared memory); same
+// arithmetic in the same order.
+template <int CW>
+DF_DEV void heads_math_s(const Epi& e, int m, int sec, const float* sb, const float* sg, float* v) {
+#pragma unroll
+  for (int i = 0; i < CW; i += 4) {
+    const float4 b4 = *reinterpret_cast<const float4*>(sb + i);
+    v[i] += b4.x, v[i + 1] += b4.y, v[i + 2] += b4.z, v[i + 3] += b4.w;
+  }
+  if (sg) {
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) ss += v[i] * v[i];
+    float inv = rsqrtf(ss / float(CW) + e.eps);
+#pragma unroll
+    for (int i = 0; i < CW; i += 4) {
+      const float4 g4 = *reinterpret_cast<const float4*>(sg + i);
+      v[i] = v[i] * inv * g4.x, v[i + 1] = v[i + 1] * inv * g4.y;
+      v[i + 2] = v[i + 2] * inv * g4.z, v[i + 3] = v[i + 3] * inv * g4.w;
+    }
+  }
+  if (e.sec_rope[sec]) {
+#pragma unroll
+    for (int p = 0; p < CW / 2; ++p) {
+      float2 cs = rope_cs(e, m, p);
+      float a = v[2 * p], b = v[2 * p + 1];
+      v[2 * p] = a * cs.x - b * cs.y;
+      v[2 * p + 1] = a * cs.y + b * cs.x;
+    }
+  }
+}
+
 // Columns are processed in chunks of CW; for EPI_HEADS CW must equal dh.
 template <int CW, typename OutT>
 DF_DEV void epi_apply(const Epi& e, int m, int n0, float* v) {
@@ -157,27 +216,7 @@ DF_DEV void epi_apply(const Epi& e, int m, int n0, float* v) {
     const int mper = e.Mper > 0 ? e.Mper : e.M;
     const int bsm = m / mper;     // sample of the stacked batch
     m -= bsm * mper;              // token within the sample (RoPE position, row)
-#pragma unroll
-    for (int i = 0; i < CW; ++i) v[i] += bias_at(e, n0 + i);
-    const bf16* g = e.sec_gain[sec];
-    if (g) {
-      float ss = 0.f;
-#pragma unroll
-      for (int i = 0; i < CW; ++i) ss += v[i] * v[i];
-      float inv = rsqrtf(ss / float(CW) + e.eps);
-      const bf16* gg = g + hd * e.dh;
-#pragma unroll
-      for (int i = 0; i < CW; ++i) v[i] = v[i] * inv * bf2f(gg[i]);
-    }
-    if (e.sec_rope[sec]) {
-#pragma unroll
-      for (int p = 0; p < CW / 2; ++p) {
-        float2 cs = rope_cs(e, m, p);
-        float a = v[2 * p], b = v[2 * p + 1];
-        v[2 * p] = a * cs.x - b * cs.y;
-        v[2 * p + 1] = a * cs.y + b * cs.x;
-      }
-    }
+    heads_math<CW>(e, m, n0, sec, hd, v);
     OutT* o = reinterpret_cast<OutT*>(e.sec_out[sec]) + ((size_t(bsm) * e.heads + hd) * mper + m) * e.dh_pad;
     store_vec<CW>(o, v);
   } else if (e.kind == EPI_EULER) {

@@ -18,6 +18,7 @@
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include "kernels.h"
 
 namespace df {
@@ -60,6 +61,25 @@ bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, u
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Generic tiled tensor map (128B swizzle; box inner extent must be 128 B).
+bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
+               const uint64_t* strides_bytes, const uint32_t* box) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  (void)esize;
+  CUresult r = enc(m, dt, rank, const_cast<void*>(base), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -274,21 +294,32 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M
 // [r*128, r*128+128) of the tile (half the operand bytes of a 1-CTA 128x256 tile per
 // unit of work); the leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) whose
 // accumulator rows r*128.. live in CTA r's TMEM; each CTA's epilogue drains its own rows.
-constexpr int P_STAGES = 6;
+constexpr int P_STAGES = 5;
 constexpr int P_A_BYTES = 128 * GBK * 2;
 constexpr int P_B_BYTES = 128 * GBK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
-constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_OFF_BAR = P_STAGES * P_STAGE_BYTES;
+constexpr int P_OFF_STG = P_OFF_BAR + 1024;        // 4 epilogue warps x 2 x 4 KB staging tiles
+constexpr int P_OFF_PRM = P_OFF_STG + 4 * 2 * 4096;  // 4 epilogue warps x (256 bias + 256 gate/gain) fp32
+constexpr int P_SMEM = P_OFF_PRM + 4 * 2048 + 1024;
 
-template <int CW, typename OutT>
+// Epilogue variants of the pair kernel (compile-time): TK_DIRECT = per-thread stores via
+// epi_apply; the others stage each warp's 32-row slice in a 128B-swizzled 4 KB shared tile
+// and write it with one bulk TMA store (TK_GRES: a TMA reduce-add into the fp32 residual,
+// so the residual is never read by the SMs).
+enum : int { TK_DIRECT = 0, TK_STORE_F32 = 1, TK_STORE_BF16 = 2, TK_GRES = 3, TK_SWIGLU = 4, TK_HEADS = 5 };
+
+template <int CW, typename OutT, int TK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, const __grid_constant__ Epi epi) {
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
+                    const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const __grid_constant__ Epi epi,
+                    int epi_skip) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + P_STAGES * P_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P_OFF_BAR);
   uint64_t* full = bars;
   uint64_t* empty = bars + P_STAGES;
   uint64_t* tfull = bars + 2 * P_STAGES;
@@ -309,12 +340,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (TK != TK_DIRECT) tma_prefetch_desc(&tmO0);
     for (int s = 0; s < P_STAGES; ++s) {
       mbar_init(&full[s], 2);    // leader: own expect_tx + the peer's remote arrive
       mbar_init(&empty[s], 1);   // multicast commit from the leader's MMA
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);   // multicast commit
+      mbar_init(&tfull[s], 1);     // multicast commit
       mbar_init(&tempty[s], 256);  // 128 epilogue threads of each CTA (leader's copy is used)
     }
     fence_mbar_init();
@@ -383,30 +415,265 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
+    uint8_t* stg0 = smem + P_OFF_STG + ew * 8192;
+    float* s_bias = reinterpret_cast<float*>(smem + P_OFF_PRM + ew * 2048);  // this tile's 256 columns
+    float* s_aux = s_bias + 256;  // GRES: gate (1 if none); HEADS: per-head RMSNorm gain
+    int sb = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     float v[CW];
+    // staging buffer handshake: before refilling buffer sb, the bulk store issued from it two
+    // stores ago must have finished reading shared memory
+    auto stage_acquire = [&]() -> uint8_t* {
+      if (lane == 0) bulk_wait_read1();
+      __syncwarp();
+      return stg0 + sb * 4096;
+    };
+    auto stage_release = [&]() {
+      fence_proxy_async_smem();
+      __syncwarp();
+    };
     for (int t = cid; t < tiles; t += nclusters) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
+      if (TK != TK_DIRECT) {
+        // per-column epilogue parameters of the tile, loaded once (coalesced) while the
+        // accumulator is still being produced; read back as broadcast shared loads
+        __syncwarp();
+#pragma unroll 1
+        for (int i = lane; i < 256; i += 32) {
+          const int n = nb * 256 + i;
+          const bool ok = n < N;
+          s_bias[i] = (ok && epi.bias) ? bf2f(epi.bias[n]) : 0.f;
+          float g = 1.f;
+          if (TK == TK_GRES) {
+            g = ok ? (epi.gate ? epi.gate[n] : 1.f) : 0.f;
+          } else if (TK == TK_HEADS && ok) {
+            const int sec = n / epi.d;
+            const bf16* gs = epi.sec_gain[sec];
+            g = gs ? bf2f(gs[n - sec * epi.d]) : 1.f;
+          }
+          s_aux[i] = g;
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * 256 + rank * 128 + ew * 32 + lane;
+      const int row0 = mb * 256 + rank * 128 + ew * 32;
+      const int row = row0 + lane;
       const uint32_t trow = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
+      if (TK == TK_DIRECT || epi_skip) {
 #pragma unroll 1
-      for (int c = 0; c < 256; c += CW) {
-        const int n0 = nb * 256 + c;
-        if (n0 >= N) break;
+        for (int c = 0; c < 256; c += CW) {
+          const int n0 = nb * 256 + c;
+          if (n0 >= N) break;
 #pragma unroll
-        for (int q = 0; q < CW; q += 16) tmem_ld16(trow + c + q, v + q);
-        tc_wait_ld();
-        epi_apply<CW, OutT>(epi, row, n0, v);
+          for (int q = 0; q < CW; q += 16) tmem_ld16(trow + c + q, v + q);
+          tc_wait_ld();
+          if (!epi_skip) epi_apply<CW, OutT>(epi, row, n0, v);
+        }
+      } else if (TK == TK_STORE_F32 || TK == TK_GRES) {
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 32) {
+          const int n0 = nb * 256 + c;
+          if (n0 >= N) break;
+          tmem_ld32(trow + c, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(s_bias + c + i);
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+            float gg[4] = {1.f, 1.f, 1.f, 1.f};
+            if (TK == TK_GRES) {
+              const float4 g4 = *reinterpret_cast<const float4*>(s_aux + c + i);
+              gg[0] = g4.x, gg[1] = g4.y, gg[2] = g4.z, gg[3] = g4.w;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              float z = v[i + u] + bb[u];
+              if (TK == TK_STORE_F32) {
+                if (epi.act == ACT_GELU) z = gelu_tanh_f(z);
+                else if (epi.act == ACT_SILU) z = silu_f(z);
+              } else if (epi.gate) {
+                z *= gg[u];
+              }
+              v[i + u] = z;
+            }
+          }
+          uint8_t* buf = stage_acquire();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(swz128(buf, lane, j)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          stage_release();
+          if (lane == 0) {
+            if (TK == TK_GRES) tma_reduce_add_2d(&tmO0, buf, n0, row0);
+            else tma_store_2d(&tmO0, buf, n0, row0);
+            bulk_commit();
+          }
+          sb ^= 1;
+        }
+      } else if (TK == TK_STORE_BF16) {
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 64) {
+          const int n0 = nb * 256 + c;
+          if (n0 >= N) break;
+          float w[64];
+          tmem_ld32(trow + c, w);
+          tmem_ld32(trow + c + 32, w + 32);
+          tc_wait_ld();
+          uint8_t* buf = stage_acquire();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float z[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              z[i] = w[8 * j + i] + s_bias[c + 8 * j + i];
+              if (epi.act == ACT_GELU) z[i] = gelu_tanh_f(z[i]);
+              else if (epi.act == ACT_SILU) z[i] = silu_f(z[i]);
+            }
+            uint4 u;
+            u.x = pack_bf16x2(z[0], z[1]);
+            u.y = pack_bf16x2(z[2], z[3]);
+            u.z = pack_bf16x2(z[4], z[5]);
+            u.w = pack_bf16x2(z[6], z[7]);
+            *reinterpret_cast<uint4*>(swz128(buf, lane, j)) = u;
+          }
+          stage_release();
+          if (lane == 0) {
+            tma_store_2d(&tmO0, buf, n0, row0);
+            bulk_commit();
+          }
+          sb ^= 1;
+        }
+      } else if (TK == TK_SWIGLU) {
+        // 128 accumulator columns (4 x (16 W1 | 16 W3)) -> 64 output columns = one 128 B box row
+#pragma unroll 1
+        for (int g = 0; g < 256; g += 128) {
+          const int n0 = nb * 256 + g;
+          if (n0 >= N) break;
+          uint8_t* buf = stage_acquire();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float a[32];
+            tmem_ld32(trow + g + 32 * q, a);
+            tc_wait_ld();
+            float w[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float a1 = a[i] + s_bias[g + 32 * q + i];
+              float a3 = a[16 + i] + s_bias[g + 32 * q + 16 + i];
+              w[i] = silu_f(a1) * a3;
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              uint4 u;
+              u.x = pack_bf16x2(w[8 * j + 0], w[8 * j + 1]);
+              u.y = pack_bf16x2(w[8 * j + 2], w[8 * j + 3]);
+              u.z = pack_bf16x2(w[8 * j + 4], w[8 * j + 5]);
+              u.w = pack_bf16x2(w[8 * j + 6], w[8 * j + 7]);
+              *reinterpret_cast<uint4*>(swz128(buf, lane, 2 * q + j)) = u;
+            }
+          }
+          stage_release();
+          if (lane == 0) {
+            tma_store_2d(&tmO0, buf, n0 / 2, row0);
+            bulk_commit();
+          }
+          sb ^= 1;
+        }
+      } else if (TK == TK_HEADS) {
+        // one 128-wide head per chunk, two passes over TMEM to bound register pressure:
+        // pass 1 the per-head sum of squares, pass 2 per 64 columns bias, RMSNorm * gain, RoPE,
+        // then a 64-column box into the sample-major head layout [b][heads][Mper][128]
+        // (same arithmetic, same order as heads_math)
+        const int mper = epi.Mper > 0 ? epi.Mper : epi.M;
+        const int rlast = min(row0 + 31, M - 1);
+        const int b0 = row0 / mper;
+        const bool straddle = (rlast / mper) != b0;  // warp rows span two samples (rare): per-lane stores
+        const int rowc = min(row, M - 1);            // lanes past M: any valid position (TMA clips them)
+        const int bl = straddle ? rowc / mper : b0;
+        const int mloc = rowc - bl * mper;
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 128) {
+          const int n0 = nb * 256 + c;
+          if (n0 >= N || row0 >= M) break;
+          const int sec = n0 / epi.d;
+          const int hd = (n0 - sec * epi.d) / epi.dh;
+          const bool norm = epi.sec_gain[sec] != nullptr;
+          const bool rope = epi.sec_rope[sec] != 0;
+          float inv = 1.f;
+          if (norm) {
+            float ss = 0.f;
+#pragma unroll 1
+            for (int q = 0; q < 128; q += 32) {
+              float a[32];
+              tmem_ld32(trow + c + q, a);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float z = a[i] + s_bias[c + q + i];
+                ss += z * z;
+              }
+            }
+            inv = rsqrtf(ss / 128.f + epi.eps);
+          }
+          const CUtensorMap* map = sec == 0 ? &tmO0 : (sec == 1 ? &tmO1 : &tmO2);
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {
+            float w[64];
+            tmem_ld32(trow + c + 64 * hf, w);
+            tmem_ld32(trow + c + 64 * hf + 32, w + 32);
+            tc_wait_ld();
+            const float* pb = s_bias + c + 64 * hf;
+            const float* pg = s_aux + c + 64 * hf;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+              w[i] += pb[i];
+              if (norm) w[i] = w[i] * inv * pg[i];
+            }
+            if (rope) {
+#pragma unroll
+              for (int p = 0; p < 32; ++p) {
+                const float2 cs = rope_cs(epi, mloc, 32 * hf + p);
+                const float x0 = w[2 * p], x1 = w[2 * p + 1];
+                w[2 * p] = x0 * cs.x - x1 * cs.y;
+                w[2 * p + 1] = x0 * cs.y + x1 * cs.x;
+              }
+            }
+            if (straddle) {
+              if (row < M)
+                store_vec<64>(reinterpret_cast<bf16*>(epi.sec_out[sec]) +
+                                  ((size_t(bl) * epi.heads + hd) * mper + mloc) * 128 + 64 * hf,
+                              w);
+              continue;
+            }
+            uint8_t* buf = stage_acquire();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float* z = w + 8 * j;
+              uint4 u;
+              u.x = pack_bf16x2(z[0], z[1]);
+              u.y = pack_bf16x2(z[2], z[3]);
+              u.z = pack_bf16x2(z[4], z[5]);
+              u.w = pack_bf16x2(z[6], z[7]);
+              *reinterpret_cast<uint4*>(swz128(buf, lane, j)) = u;
+            }
+            stage_release();
+            if (lane == 0) {
+              tma_store_3d(map, buf, 64 * hf, row0 - b0 * mper, b0 * epi.heads + hd);
+              bulk_commit();
+            }
+            sb ^= 1;
+          }
+        }
       }
       tc_fence_before();
       mbar_arrive_cluster(&tempty[acc], 0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (TK != TK_DIRECT && lane == 0) bulk_wait_all();  // stores complete before exit
   }
   tc_fence_before();
   cluster_sync_all();
@@ -416,10 +683,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
-template <int CW, typename OutT>
-static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
-                              cudaStream_t st) {
-  auto kern = gemm_tc2_kernel<CW, OutT>;
+template <int CW, typename OutT, int TK>
+static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap* to, int M, int N, int K,
+                              const Epi& epi, cudaStream_t st) {
+  auto kern = gemm_tc2_kernel<CW, OutT, TK>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
@@ -429,22 +696,67 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int 
   int tiles = ((M + 255) / 256) * ((N + 255) / 256);
   int pairs = num_sms() / 2;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
-  void* args[] = {(void*)&ta, (void*)&tb, (void*)&M, (void*)&N, (void*)&K, (void*)&epi};
+  static const int skip = [] {  // debug: DF_GEMM_NOEPI=1 drops the epilogue work (timing experiments only)
+    const char* e = getenv("DF_GEMM_NOEPI");
+    return e ? atoi(e) : 0;
+  }();
+  int sk = skip;
+  void* args[] = {(void*)&ta,     (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2], (void*)&M,
+                  (void*)&N,      (void*)&K,  (void*)&epi,   (void*)&sk};
   return launch_ex((const void*)kern, dim3(grid), dim3(256), P_SMEM, st, args);
 }
 
+bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
+               const uint64_t* strides_bytes, const uint32_t* box);
+
 static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
                                 int out_f32, cudaStream_t st) {
+  static const int tma_epi = [] {  // DF_GEMM_TMA_EPI=0: per-thread epilogue stores (A/B)
+    const char* e = getenv("DF_GEMM_TMA_EPI");
+    return e ? atoi(e) : 1;
+  }();
+  CUtensorMap to[3];
+  std::memset(to, 0, sizeof(to));
+  if (tma_epi) {
+    const uint32_t box_f32[2] = {32, 32}, box_bf16[2] = {64, 32};
+    if (epi.kind == EPI_STORE && out_f32 && (epi.ldo % 4) == 0) {
+      const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 4};
+      if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box_f32))
+        return launch_tc2<32, float, TK_STORE_F32>(ta, tb, to, M, N, K, epi, st);
+    } else if (epi.kind == EPI_STORE && !out_f32 && (epi.ldo % 8) == 0) {
+      const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 2};
+      if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box_bf16))
+        return launch_tc2<32, bf16, TK_STORE_BF16>(ta, tb, to, M, N, K, epi, st);
+    } else if (epi.kind == EPI_GRES && (epi.ldr % 4) == 0) {
+      const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldr) * 4};
+      if (make_tmap(&to[0], epi.resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box_f32))
+        return launch_tc2<32, float, TK_GRES>(ta, tb, to, M, N, K, epi, st);
+    } else if (epi.kind == EPI_SWIGLU && !out_f32 && (epi.ldo % 8) == 0) {
+      const uint64_t dims[2] = {uint64_t(N / 2), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 2};
+      if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box_bf16))
+        return launch_tc2<32, bf16, TK_SWIGLU>(ta, tb, to, M, N, K, epi, st);
+    } else if (epi.kind == EPI_HEADS && !out_f32 && epi.dh == 128 && epi.dh_pad == 128) {
+      const int mper = epi.Mper > 0 ? epi.Mper : M;
+      const uint64_t dims[3] = {128, uint64_t(mper), uint64_t(M / mper) * epi.heads};
+      const uint64_t str[2] = {128 * 2, uint64_t(mper) * 128 * 2};
+      const uint32_t box[3] = {64, 32, 1};
+      bool ok = true;
+      for (int s = 0; s < epi.nsec; ++s)
+        ok = ok && make_tmap(&to[s], epi.sec_out[s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, dims, str, box);
+      if (ok) return launch_tc2<128, bf16, TK_HEADS>(ta, tb, to, M, N, K, epi, st);
+    }
+  }
   if (epi.kind == EPI_HEADS) {
     if (out_f32) return cudaErrorInvalidValue;
     switch (epi.dh) {
-      case 16: return launch_tc2<16, bf16>(ta, tb, M, N, K, epi, st);
-      case 64: return launch_tc2<64, bf16>(ta, tb, M, N, K, epi, st);
-      case 128: return launch_tc2<128, bf16>(ta, tb, M, N, K, epi, st);
+      case 16: return launch_tc2<16, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+      case 64: return launch_tc2<64, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+      case 128: return launch_tc2<128, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
       default: return cudaErrorInvalidValue;
     }
   }
-  return out_f32 ? launch_tc2<32, float>(ta, tb, M, N, K, epi, st) : launch_tc2<32, bf16>(ta, tb, M, N, K, epi, st);
+  return out_f32 ? launch_tc2<32, float, TK_DIRECT>(ta, tb, to, M, N, K, epi, st)
+                 : launch_tc2<32, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
 }
 
 template <int BN>

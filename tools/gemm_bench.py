@@ -1,0 +1,60 @@
+"""GEMM microbenchmark: libdf's tcgen05 CTA-pair GEMM (df_op_gemm, fp32 output) against
+cuBLAS bf16 (torch.matmul, bf16 output) on the same shapes, same run — separates the
+mainloop from the fused epilogues measured inside the DiT step.
+
+    python tools/gemm_bench.py
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_25550_b200 import binding as B  # noqa: E402
+from synth.configs import TINY  # noqa: E402
+
+SHAPES = [("square8192", 8192, 8192, 8192), ("image_qkv", 4096, 9216, 3072), ("image_up", 4096, 16384, 3072),
+          ("image_o", 4096, 3072, 3072), ("image_down", 4096, 3072, 8192), ("video_up", 32760, 27648, 5120)]
+
+
+def timeit(fn, iters=10):
+    fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    best = 1e30
+    for _ in range(iters):
+        ev[0].record()
+        fn()
+        ev[1].record()
+        torch.cuda.synchronize()
+        best = min(best, ev[0].elapsed_time(ev[1]))
+    return best
+
+
+def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--no-cublas", action="store_true")
+    a = ap.parse_args()
+    g = B.make_graph(TINY, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)])
+    with B.Context(g) as c:
+        for name, M, N, K in SHAPES:
+            if a.only and name != a.only:
+                continue
+            A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+            W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+            out = torch.empty(M, N, device="cuda")
+            ms_ours = timeit(lambda: c.op_gemm(A, W, out, tc=1))
+            ms_cublas = ms_ours if a.no_cublas else timeit(lambda: torch.matmul(A, W.t()))
+            fl = 2.0 * M * N * K
+            ref = (A.float() @ W.float().t())
+            err = ((out - ref).norm() / ref.norm()).item()
+            print({"shape": name, "M": M, "N": N, "K": K, "ours_tflops": round(fl / ms_ours / 1e9, 1),
+                   "cublas_tflops": round(fl / ms_cublas / 1e9, 1), "ratio": round(ms_cublas / ms_ours, 3),
+                   "rel_err": f"{err:.1e}"}, flush=True)
+            del A, W, out, ref
+
+
+if __name__ == "__main__":
+    main()
