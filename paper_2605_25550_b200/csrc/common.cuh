@@ -15,6 +15,9 @@ typedef __nv_bfloat16 bf16;
 
 // ------------------------------------------------------------------ numerics
 DF_DEV float bf2f(bf16 v) { return __bfloat162float(v); }
+// low / high bf16 of a packed pair, widened exactly (bf16 = the top 16 bits of an fp32)
+DF_DEV float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+DF_DEV float bf_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 DF_DEV float bfbits2f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 DF_DEV uint16_t f2bfbits(float f) {  // RNE (cvt.rn.bf16.f32)
   bf16 h = __float2bfloat16_rn(f);

@@ -164,10 +164,82 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   }
 }
 
+// One warp per row (d = 128 * VPT): every lane has VPT independent 16-byte loads in flight
+// and the reduction is warp shuffles only. Rows up to 24 float4 per lane stay in registers;
+// wider rows re-read x (an L1 hit) in the second pass.
+template <int VPT, typename OutT>
+__global__ void __launch_bounds__(128) rmsnorm_warp_kernel(const float* __restrict__ x, OutT* __restrict__ out, int M,
+                                                           const float* __restrict__ shift,
+                                                           const float* __restrict__ scale,
+                                                           const bf16* __restrict__ gain, float eps) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  constexpr int d = 128 * VPT;
+  constexpr bool KEEP = VPT <= 24;
+  const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
+  float4 v[KEEP ? VPT : 1];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const float4 t = xr[lane + 32 * i];
+    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+    if constexpr (KEEP) v[i] = t;
+  }
+  ss = warp_sum(ss);
+  const float inv = rsqrtf(ss / float(d) + eps);
+  OutT* orow = out + size_t(row) * d;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = lane + 32 * i;
+    float4 t;
+    if constexpr (KEEP) t = v[i];
+    else t = xr[c];
+    float y[4] = {t.x * inv, t.y * inv, t.z * inv, t.w * inv};
+    if (gain) {
+      const uint2 g = reinterpret_cast<const uint2*>(gain)[c];
+      y[0] *= bf_lo(g.x), y[1] *= bf_hi(g.x), y[2] *= bf_lo(g.y), y[3] *= bf_hi(g.y);
+    } else {
+      const float4 sc = reinterpret_cast<const float4*>(scale)[c];
+      const float4 sh = reinterpret_cast<const float4*>(shift)[c];
+      y[0] = y[0] * (1.f + sc.x) + sh.x;
+      y[1] = y[1] * (1.f + sc.y) + sh.y;
+      y[2] = y[2] * (1.f + sc.z) + sh.z;
+      y[3] = y[3] * (1.f + sc.w) + sh.w;
+    }
+    if constexpr (sizeof(OutT) == 2) {
+      uint2 u;
+      u.x = pack_bf16x2(y[0], y[1]);
+      u.y = pack_bf16x2(y[2], y[3]);
+      reinterpret_cast<uint2*>(orow)[c] = u;
+    } else {
+      reinterpret_cast<float4*>(orow)[c] = make_float4(y[0], y[1], y[2], y[3]);
+    }
+  }
+}
+
+template <int VPT>
+static cudaError_t launch_rms_warp(const float* x, void* out, int out_f32, int M, const float* shift,
+                                   const float* scale, const bf16* gain, float eps, cudaStream_t st) {
+  void* args[] = {(void*)&x, (void*)&out, (void*)&M, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
+  dim3 grid((M + 3) / 4);
+  if (out_f32) return launch_ex((const void*)rmsnorm_warp_kernel<VPT, float>, grid, dim3(128), 0, st, args);
+  return launch_ex((const void*)rmsnorm_warp_kernel<VPT, bf16>, grid, dim3(128), 0, st, args);
+}
+
 cudaError_t rmsnorm_mod(const float* x, void* out, int out_f32, int M, int d, const float* shift, const float* scale,
                         const bf16* gain, float eps, cudaStream_t st) {
   if (d % 4 || d > 8192) return cudaErrorInvalidValue;
   if (M <= 0) return cudaSuccess;
+  switch (d) {  // the model widths (mid, image, text encoder, video)
+    case 256: return launch_rms_warp<2>(x, out, out_f32, M, shift, scale, gain, eps, st);
+    case 3072: return launch_rms_warp<24>(x, out, out_f32, M, shift, scale, gain, eps, st);
+    case 4096: return launch_rms_warp<32>(x, out, out_f32, M, shift, scale, gain, eps, st);
+    case 5120: return launch_rms_warp<40>(x, out, out_f32, M, shift, scale, gain, eps, st);
+    default: break;
+  }
   void* args[] = {(void*)&x, (void*)&out, (void*)&d, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
   if (out_f32) return launch_ex((const void*)rmsnorm_kernel<float>, dim3(M), dim3(256), 0, st, args);
   return launch_ex((const void*)rmsnorm_kernel<bf16>, dim3(M), dim3(256), 0, st, args);

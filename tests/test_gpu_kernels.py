@@ -101,8 +101,9 @@ def test_attention_special_cases(tiny_ctx):
     assert rel_l2(O.double().cpu().numpy(), want.cpu().numpy()) < 4e-3
 
 
-def test_rmsnorm_mod_closed_form(tiny_ctx):
-    M, d = 333, 3072
+@pytest.mark.parametrize("d", [200, 3072, 4096, 5120])
+def test_rmsnorm_mod_closed_form(tiny_ctx, d):
+    M = 333  # not a multiple of the 4 rows per CTA
     x = torch.randn(M, d, device="cuda") * 3
     sh = torch.randn(d, device="cuda") * 0.1
     sc = torch.randn(d, device="cuda") * 0.1
