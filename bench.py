@@ -307,15 +307,32 @@ def run_ours(args, cfg):
     avg_ms = ks["ms"] / max(ks["launches"], 1)
     if ks["flops"] > 0:
         ach = (ks["flops"] / ks["launches"]) / (avg_ms / 1000.0) / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
-                "frac": ach / peaks["bf16_sus"], "traffic": args.traffic, "kernel": dom,
-                "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
-                "peak_note": f"{peaks['src']} sustained cuBLAS bf16 (kernel timed inside a long step)"}
+        # the sustained figure (cuBLAS 8192^3 back to back, deepest power-cap clocks) is the
+        # denominator for a kernel timed inside a long step unless the kernel beats it; then the
+        # burst figure is the ceiling that still holds
+        if ach <= peaks["bf16_sus"]:
+            pk, note = peaks["bf16_sus"], f"{peaks['src']} sustained cuBLAS bf16 (kernel timed inside a long step)"
+        else:
+            pk = peaks["bf16"]
+            note = (f"{peaks['src']} burst cuBLAS bf16: the kernel exceeds the sustained figure "
+                    f"({peaks['bf16_sus']:.1f}), which was measured at lower power-capped clocks")
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "traffic": args.traffic, "kernel": dom,
+                "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"], "peak_note": note}
     else:
         ach = (ks["bytes"] / ks["launches"]) / (avg_ms / 1000.0) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
                 "traffic": args.traffic, "kernel": dom, "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
                 "peak_note": f"{peaks['src']} HBM copy"}
+    if roof["traffic"] is None:  # committed ncu capture of this kernel at this config, if any
+        try:
+            tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
+            ent = tj.get(args.config, {}).get(dom)
+            if ent:
+                roof["traffic"] = ent["bytes"]
+                roof["traffic_source"] = ent["source"]
+        except (OSError, ValueError):
+            pass
     tot_kms = sum(v["ms"] for v in kstats.values()) or 1.0
     shares = {k: round(v["ms"] / tot_kms, 4) for k, v in kstats.items() if v["ms"] > 0}
     tput_kind = {k: round((v["flops"] / v["ms"] / 1e9), 1) for k, v in kstats.items() if v["ms"] > 0 and v["flops"] > 0}

@@ -7,6 +7,9 @@
 #include <cmath>
 #include "kernels.h"
 
+#include <atomic>
+#include <mutex>
+
 namespace df {
 
 // ------------------------------------------------------------------ Philox4x32-10
@@ -413,10 +416,12 @@ DF_DEV unsigned long long splitmix64(unsigned long long z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+// acc[0] = running sum, acc[1] = arrival counter; both back to 0 when the kernel ends, so a
+// slot is reusable by the next hash on any stream once this one finished.
 __global__ void hash_kernel(const uint8_t* __restrict__ buf, size_t nbytes, size_t word_off,
-                            unsigned long long* out) {
+                            unsigned long long* acc, unsigned long long* out) {
   size_t nw = (nbytes + 7) / 8;
-  unsigned long long acc = 0;
+  unsigned long long h = 0;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nw; i += size_t(gridDim.x) * blockDim.x) {
     unsigned long long w = 0;
     size_t b0 = i * 8;
@@ -426,22 +431,56 @@ __global__ void hash_kernel(const uint8_t* __restrict__ buf, size_t nbytes, size
       for (int k = 0; k < 8; ++k)
         if (b0 + k < nbytes) w |= (unsigned long long)buf[b0 + k] << (8 * k);
     }
-    acc += splitmix64(w ^ ((word_off + i) * 0x9E3779B97F4A7C15ull));
+    h += splitmix64(w ^ ((word_off + i) * 0x9E3779B97F4A7C15ull));
   }
-  // sum mod 2^64 is order-independent: warp reduce then one atomic per warp
+  // sum mod 2^64 is order-independent: warp reduce, one device atomic per warp; the last
+  // block to arrive publishes the total with one store (out may be host-mapped memory)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc, h);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(acc + 1, 1ull) == gridDim.x - 1) {
+      __threadfence();
+      *out = atomicExch(acc, 0ull);
+      acc[1] = 0;
+    }
+  }
 }
+
+// Per-device pool of accumulator slots (zeroed once; every hash returns its slot zeroed).
+// Slots are handed out round robin: up to kHashSlots hashes may be in flight per device.
+static constexpr int kHashSlots = 1024;
+static unsigned long long* hash_slots(int dev) {
+  static std::mutex mu;
+  static unsigned long long* pool[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!pool[dev]) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, kHashSlots * 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, kHashSlots * 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    pool[dev] = static_cast<unsigned long long*>(p);
+  }
+  return pool[dev];
+}
+
 cudaError_t payload_hash(const void* buf, size_t nbytes, size_t word_offset, unsigned long long* out,
                          cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
-  if (e != cudaSuccess) return e;
   size_t nw = (nbytes + 7) / 8;
   unsigned blocks = unsigned((nw + 255) / 256);
   if (blocks > 296) blocks = 296;
-  if (!blocks) return cudaSuccess;
-  hash_kernel<<<blocks, 256, 0, st>>>((const uint8_t*)buf, nbytes, word_offset, out);
+  if (!blocks) return cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  unsigned long long* pool = hash_slots(dev);
+  if (!pool) return cudaErrorMemoryAllocation;
+  static std::atomic<unsigned> next{0};
+  unsigned long long* acc = pool + 2 * (next.fetch_add(1) % kHashSlots);
+  hash_kernel<<<blocks, 256, 0, st>>>((const uint8_t*)buf, nbytes, word_offset, acc, out);
   return cudaGetLastError();
 }
 
