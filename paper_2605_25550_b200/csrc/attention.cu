@@ -282,7 +282,7 @@ DF_DEV float ex2_approx(float x) {
   return y;
 }
 
-template <int DH, bool POLY, bool SP>
+template <int DH, bool POLY, int DBG = 0>
 __global__ void __launch_bounds__(384, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
@@ -429,33 +429,38 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
     const uint32_t ts = tmem + lane_off + t * 128;
     const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH;
-    // SP (single pass): the max in use starts at 0 (log2 units) and is only raised when a
-    // block's logits exceed it by > 2^30, so no max pre-pass is needed; P is clamped at 2^64
-    // before that (rare) rescale, which is exact for logits within 2^64 of the max in use
-    // (far beyond the range of this model's RMS-normalised q, k: |s| log2e <= sqrt(dh) max|g|^2).
-    float m_used = SP ? 0.f : -INFINITY, l = 0.f;
+    // One TMEM read of S per key block: the 128 logits of this row stay in registers for
+    // the max and the exponentials (TMEM reads are 64 B/clk and the tensor core's own operand
+    // reads share them; a second pass over S costs as much TMEM bandwidth as the first).
+    float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const int valid = Nk - j * 128;
-      float mx = -INFINITY;
-      if (!SP) {
-      // pass 1: row max, 64 columns in flight (S stays in TMEM; low register pressure)
-#pragma unroll
-      for (int c = 0; c < 128; c += 64) {
-        float s[64];
-        tmem_ld32(ts + c, s);
-        tmem_ld32(ts + c + 32, s + 32);
-        tc_wait_ld();
-        if (valid < 128) {  // ragged last key block (warp-uniform)
-#pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (c + i >= valid) s[i] = -INFINITY;
-        }
-#pragma unroll
-        for (int i = 0; i < 64; ++i) mx = fmaxf(mx, s[i]);
+      if (DBG == 2) {  // profiling knob: tensor + synchronisation only (no softmax)
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
+        continue;
       }
-      mx *= scale_log2;
+      const int valid = Nk - j * 128;
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
+      tc_wait_ld();
+      if (valid < 128) {  // ragged last key block (warp-uniform)
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i >= valid) s[i] = -INFINITY;
+      }
+      // row max: four independent FMNMX3 chains
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 128; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], fmaxf(s[i + 2 * u], s[i + 2 * u + 1]));
+      }
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+      // lazy rescale: the max in use moves only when a row's max exceeds it by > 8 (log2),
+      // so p <= 2^8 and the O correction is rare after the first blocks
       const bool need = mx > m_used + 8.0f;
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? mx : m_used;
@@ -464,46 +469,32 @@ __global__ void __launch_bounds__(384, 1)
           const float alpha = exp2f(m_used - m_new);
           l *= alpha;
 #pragma unroll 1
-          for (int c = 0; c < DH; c += 32) {
-            float o[32];
-            tmem_ld32(to + c, o);
+          for (int c = 0; c < DH; c += 16) {
+            float o[16];
+            tmem_ld16(to + c, o);
             tc_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st32(to + c, o);
+            for (int i = 0; i < 16; ++i) o[i] *= alpha;
+            tmem_st16(to + c, reinterpret_cast<uint32_t*>(o));
           }
         }
         m_used = m_new;
       }
-      }  // !SP
-      // p = 2^(s*scale - m): FFMA2 for the affine part; 3/8 of the exponentials on the
-      // FMA/ALU pipes (polynomial), 5/8 on MUFU.EX2, so neither unit paces the tile.
+      // p = 2^(s*scale - m) -> bf16 pairs into the first 64 columns of S (= P_t); FFMA2 for
+      // the affine part; with POLY 3/8 of the exponentials on the FMA pipe (polynomial)
       float2 lsum2 = make_float2(0.f, 0.f);
       const float2 sc2 = make_float2(scale_log2, scale_log2);
       const float2 nm2 = make_float2(-m_used, -m_used);
-      // pass 2: p = 2^(s*scale - m) -> bf16 pairs over the first half of S (= P_t)
 #pragma unroll
-      for (int c = 0; c < 128; c += 64) {
-        float s[64];
-        tmem_ld32(ts + c, s);
-        tmem_ld32(ts + c + 32, s + 32);
-        tc_wait_ld();
-        if (valid < 128) {
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (c + i >= valid) s[i] = -INFINITY;
-        }
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
-          if (SP) {
-            mx = fmaxf(mx, fmaxf(s[2 * i], s[2 * i + 1]));
-            x.x = fminf(x.x, 64.f);
-            x.y = fminf(x.y, 64.f);
-          }
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = ffma2(make_float2(s[32 * q + 2 * i], s[32 * q + 2 * i + 1]), sc2, nm2);
           float2 p;
-          if (POLY && (i & 7) >= 5) {
+          if (DBG == 1) {
+            p = ffma2(x, sc2, nm2);
+          } else if (POLY && (i & 7) >= 5) {
             p = exp2_poly2(x);
           } else {
             p.x = ex2_approx(x.x);
@@ -512,44 +503,8 @@ __global__ void __launch_bounds__(384, 1)
           lsum2 = fadd2(lsum2, p);
           pk[i] = pack_bf16x2(p.x, p.y);
         }
-        // columns c/2 .. c/2+31 hold keys c .. c+63; they alias S columns already consumed
-        tmem_st16(ts + c / 2, pk);
-        tmem_st16(ts + c / 2 + 16, pk + 16);
-      }
-      if (SP && __any_sync(0xffffffffu, mx * scale_log2 > m_used + 30.0f)) {
-        // rare: raise the max in use; rescale O_t (stable: s_full for block j implies
-        // PV_{j-1} completed), l, this block's sum and its P (in place, p' = p * alpha)
-        tc_wait_st();
-        const float m_new = fmaxf(m_used, mx * scale_log2);
-        const float alpha = exp2f(m_used - m_new);
-        l *= alpha;
-        lsum2.x *= alpha;
-        lsum2.y *= alpha;
-        if (j > 0) {
-#pragma unroll 1
-          for (int c = 0; c < DH; c += 32) {
-            float o[32];
-            tmem_ld32(to + c, o);
-            tc_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st32(to + c, o);
-          }
-        }
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 16) {
-          float pf[16];
-          uint32_t pk[16];
-          tmem_ld16(ts + c, pf);
-          tc_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            uint32_t u = __float_as_uint(pf[i]);
-            pk[i] = pack_bf16x2(__uint_as_float(u << 16) * alpha, __uint_as_float(u & 0xFFFF0000u) * alpha);
-          }
-          tmem_st16(ts + c, pk);
-        }
-        m_used = m_new;
+        // columns 16q .. 16q+15 hold keys 32q .. 32q+31 (S is already in registers)
+        tmem_st16(ts + 16 * q, pk);
       }
       l += lsum2.x + lsum2.y;
       tc_wait_st();
@@ -587,11 +542,11 @@ __global__ void __launch_bounds__(384, 1)
 
 int g_attn_impl = 2;
 
-template <int DH, bool POLY, bool SP>
+template <int DH, bool POLY, int DBG = 0>
 static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, bf16* O, int H,
                                 int Nq, int Nk, int dh, float scale, cudaStream_t st, int hs) {
   using Cfg = Attn2Cfg<DH>;
-  auto kern = attn_tc2_kernel<DH, POLY, SP>;
+  auto kern = attn_tc2_kernel<DH, POLY, DBG>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -617,14 +572,14 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
       const char* e = getenv("DF_ATTN_POLY");  // 1: 3/8 of the exponentials by polynomial on the FMA pipe
       return e ? atoi(e) : 0;
     }();
-    static const int sp = [] {
-      const char* e = getenv("DF_ATTN_SP");  // 1: single-pass softmax (lazy max from 0)
+    static const int dbg = [] {
+      const char* e = getenv("DF_ATTN_DBG");  // profiling only: 1 = FMA instead of ex2, 2 = no softmax (wrong results)
       return e ? atoi(e) : 0;
     }();
-    if (sp) return poly ? launch_attn2<DH, true, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
-                        : launch_attn2<DH, false, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
-    return poly ? launch_attn2<DH, true, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
-                : launch_attn2<DH, false, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    if (dbg == 1) return launch_attn2<DH, false, 1>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    if (dbg == 2) return launch_attn2<DH, false, 2>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    return poly ? launch_attn2<DH, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
+                : launch_attn2<DH, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
   }
   using Cfg = AttnCfg<DH>;
   CUtensorMap tq, tk, tv;

@@ -1,6 +1,6 @@
 """Attention microbenchmark through df_op_attention (no model): TFLOP/s of the tcgen05
 flash-attention kernel at the workload shapes.  Variants are selected by env vars
-(DF_ATTN_IMPL, DF_ATTN_POLY, DF_ATTN_SP) read once per process.
+(DF_ATTN_IMPL, DF_ATTN_POLY) read once per process.
 
     python tools/attn_bench.py --shape video
 """
@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="video")
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--lib", action="store_true", help="also time torch SDPA (cuDNN / flash backends) on the same inputs")
     a = ap.parse_args()
     H, Nq, Nk = SHAPES[a.shape]
     dh = 128
@@ -55,8 +56,28 @@ def main():
         fl = 4.0 * H * Nq * Nk * dh
         best = min(ms)
         print({"shape": a.shape, "impl": os.environ.get("DF_ATTN_IMPL", "2"), "poly": os.environ.get("DF_ATTN_POLY", "0"),
-               "sp": os.environ.get("DF_ATTN_SP", "0"), "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
+               "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
                "rel_l2_vs_torch": f"{err:.2e}"})
+        if a.lib:  # library reference point (not on the product path)
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+            q4, k4, v4 = Q.unsqueeze(0), K.unsqueeze(0), V.unsqueeze(0)
+            for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION):
+                try:
+                    with sdpa_kernel(be):
+                        f = lambda: torch.nn.functional.scaled_dot_product_attention(q4, k4, v4, scale=sc)
+                        f()
+                        torch.cuda.synchronize()
+                        lm = []
+                        for _ in range(a.iters):
+                            ev[0].record()
+                            f()
+                            ev[1].record()
+                            torch.cuda.synchronize()
+                            lm.append(ev[0].elapsed_time(ev[1]))
+                    print({"shape": a.shape, "lib": str(be), "ms": round(min(lm), 3),
+                           "tflops": round(fl / min(lm) / 1e9, 1)}, flush=True)
+                except Exception as ex:  # backend not available for this shape / build
+                    print({"shape": a.shape, "lib": str(be), "error": str(ex)[:120]}, flush=True)
 
 
 if __name__ == "__main__":
