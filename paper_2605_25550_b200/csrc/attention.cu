@@ -443,9 +443,34 @@ __global__ void __launch_bounds__(384, 1)
       }
       const int valid = Nk - j * 128;
       float s[128];
+      if (DBG == 4) {
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
-      tc_wait_ld();
+        for (int c = 0; c < 128; ++c) s[c] = float(c & 7) * 0.01f;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
+        tc_wait_ld();
+      }
+      if (DBG == 6) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = __float_as_uint(s[i]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_st16(ts + 16 * q, pk);
+        tc_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
+        continue;
+      }
+      if (DBG == 3) {
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) acc += s[c];
+        l += acc;
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
+        continue;
+      }
       if (valid < 128) {  // ragged last key block (warp-uniform)
 #pragma unroll
         for (int i = 0; i < 128; ++i)
@@ -504,7 +529,11 @@ __global__ void __launch_bounds__(384, 1)
           pk[i] = pack_bf16x2(p.x, p.y);
         }
         // columns 16q .. 16q+15 hold keys 32q .. 32q+31 (S is already in registers)
-        tmem_st16(ts + 16 * q, pk);
+        if (DBG == 5) {
+          l += __uint_as_float(pk[0] ^ pk[5] ^ pk[11] ^ pk[15]) * 1e-30f;
+        } else {
+          tmem_st16(ts + 16 * q, pk);
+        }
       }
       l += lsum2.x + lsum2.y;
       tc_wait_st();
@@ -560,10 +589,316 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
   return launch_ex((const void*)kern, grid, dim3(384), Cfg::SMEM, st, args);
 }
 
+// ------------------------------------------------------------------ attn_pair: CTA-pair (cta_group::2)
+// A cluster of two CTAs runs M = 256 MMAs: query tile t of the pair is 256 rows, 128 in each
+// CTA's shared memory and TMEM. Each CTA stages HALF of every K/V block (K: 64 of the 128
+// keys, all of dh; V: all 128 keys, 64 of the 128 dh columns), so per SM the shared-memory
+// operand reads of QK^T and PV and the TMA writes halve against attn_tc2 (whose SS-mode
+// M=128 QK^T alone saturates the 128 B/clk shared-memory port). The leader CTA's MMA thread
+// issues for both; ring barriers live on the leader (count 2: its expect_tx + the peer's
+// arrive), MMA completions are multicast to both CTAs. Softmax is per CTA over its own 128
+// rows, exactly as in attn_tc2 (P written into TMEM, consumed as the A operand of PV).
+struct AttnPairCfg {
+  static constexpr int DH = 128;
+  static constexpr int ATOM = 64 * 128;              // SW128 atom of 64 rows (8 KB)
+  static constexpr int Q_BYTES = 2 * 128 * 128;      // one 128-row Q tile (2 dh atoms of 16 KB)
+  static constexpr int K_BYTES = 64 * 128 * 2;       // half K block: 64 keys x 128 dh
+  static constexpr int V_BYTES = 128 * 64 * 2;       // half V block: 128 keys x 64 dh
+  static constexpr int KST = 4;
+  static constexpr int VST = 4;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * K_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VST * V_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t O_COL = 256;
+};
+
+template <bool POLY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                     int dh_real, float scale_log2, int Hs) {
+  using Cfg = AttnPairCfg;
+  constexpr int DH = Cfg::DH;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;                 // [KST]  leader
+  uint64_t* k_empty = k_full + Cfg::KST;       // [KST]  both (multicast commit)
+  uint64_t* v_full = k_empty + Cfg::KST;       // [VST]  leader
+  uint64_t* v_empty = v_full + Cfg::VST;       // [VST]  both
+  uint64_t* s_full = v_empty + Cfg::VST;       // [2]    both
+  uint64_t* p_full = s_full + 2;               // [2]    leader: 4 softmax warps x 2 CTAs
+  uint64_t* o_done = p_full + 2;               // [2]    both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int h = blockIdx.y;
+  const int qp = (blockIdx.x >> 1) * 512;      // first query row of the pair
+  const int nkb = (Nk + 127) / 128;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 2);
+    for (int s = 0; s < Cfg::KST; ++s) {
+      mbar_init(&k_full[s], 2);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::VST; ++s) {
+      mbar_init(&v_full[s], 2);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 8);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // this CTA's rows of tile t: qp + t*256 + rank*128
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * Cfg::Q_BYTES);
+      else mbar_arrive_cluster(q_full, 0);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_pair(sQ + t * Cfg::Q_BYTES + a * 2 * Cfg::ATOM, &tmQ, q_full, a * 64,
+                           qp + t * 256 + int(rank) * 128, h);
+      int jk = 0, jv = 0;
+      while (jv < nkb) {
+        if (jk < nkb && jk <= jv + 2) {
+          const int st = jk % Cfg::KST;
+          mbar_wait(&k_empty[st], ((jk / Cfg::KST) & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(&k_full[st], 2 * Cfg::K_BYTES);
+          else mbar_arrive_cluster(&k_full[st], 0);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)  // keys jk*128 + rank*64 .. +64, dh atom a
+            tma_load_3d_pair(sK + st * Cfg::K_BYTES + a * Cfg::ATOM, &tmK, &k_full[st], a * 64,
+                             jk * 128 + int(rank) * 64, h);
+          ++jk;
+        } else {
+          const int st = jv % Cfg::VST;
+          mbar_wait(&v_empty[st], ((jv / Cfg::VST) & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(&v_full[st], 2 * Cfg::V_BYTES);
+          else mbar_arrive_cluster(&v_full[st], 0);
+          // keys jv*128 .. +128, dh columns rank*64 .. +64
+          tma_load_3d_pair(sV + st * Cfg::V_BYTES, &tmV, &v_full[st], int(rank) * 64, jv * 128, h);
+          ++jv;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(256, DH, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_qk = [&](int t, int j) {
+        const uint32_t k_addr = smem_u32(sK + (j % Cfg::KST) * Cfg::K_BYTES);
+        const uint32_t qa = q_addr + t * Cfg::Q_BYTES;
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          // A: 128 rows per CTA, dh atoms of 16 KB; B: 64 keys per CTA, dh atoms of 8 KB
+          tc_mma_bf16_pair(tmem + t * 128, sdesc_sw128(qa + (k >> 2) * 2 * Cfg::ATOM + (k & 3) * 32, 16, 1024),
+                           sdesc_sw128(k_addr + (k >> 2) * Cfg::ATOM + (k & 3) * 32, 16, 1024), idesc_qk, k > 0);
+        }
+        tc_commit_pair(&s_full[t], 0x3);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t v_addr = smem_u32(sV + (j % Cfg::VST) * Cfg::V_BYTES);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // 128 keys / 16; P_t = TMEM columns k*8.. of S_t
+          tc_mma_bf16_ts_pair(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8,
+                              sdesc_sw128(v_addr + k * 2048, Cfg::V_BYTES, 1024), idesc_pv, (j > 0 || k > 0));
+      };
+      auto wait_k = [&](int j) {
+        mbar_wait(&k_full[j % Cfg::KST], (j / Cfg::KST) & 1);
+        tc_fence_after();
+      };
+      mbar_wait(q_full, 0);
+      wait_k(0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      tc_commit_pair(&k_empty[0], 0x3);
+      for (int j = 0; j < nkb; ++j) {
+        const bool more = j + 1 < nkb;
+        mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (!more) tc_commit_pair(&o_done[0], 0x3);
+        if (more) {
+          wait_k(j + 1);
+          issue_qk(0, j + 1);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j);
+        tc_commit_pair(&v_empty[j % Cfg::VST], 0x3);
+        if (!more) tc_commit_pair(&o_done[1], 0x3);
+        if (more) {
+          issue_qk(1, j + 1);
+          tc_commit_pair(&k_empty[(j + 1) % Cfg::KST], 0x3);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;        // Q tile of this softmax group (warps 4-7, 8-11)
+    const int ew = warp & 3;              // TMEM lane quarter = warp id mod 4
+    const int r = ew * 32 + lane;         // query row within this CTA's half of the tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const uint32_t ts = tmem + lane_off + t * 128;
+    const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      const int valid = Nk - j * 128;
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) tmem_ld32(ts + c, s + c);
+      tc_wait_ld();
+      if (valid < 128) {  // ragged last key block (warp-uniform)
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i >= valid) s[i] = -INFINITY;
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 128; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], fmaxf(s[i + 2 * u], s[i + 2 * u + 1]));
+      }
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+      const bool need = mx > m_used + 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_used;
+        if (j > 0) {
+          // s_full for block j implies PV_{j-1} (issued earlier) completed: O_t is stable
+          const float alpha = exp2f(m_used - m_new);
+          l *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < DH; c += 16) {
+            float o[16];
+            tmem_ld16(to + c, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= alpha;
+            tmem_st16(to + c, reinterpret_cast<uint32_t*>(o));
+          }
+        }
+        m_used = m_new;
+      }
+      float2 lsum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
+      const float2 nm2 = make_float2(-m_used, -m_used);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = ffma2(make_float2(s[32 * q + 2 * i], s[32 * q + 2 * i + 1]), sc2, nm2);
+          float2 p;
+          if (POLY && (i & 7) >= 5) {
+            p = exp2_poly2(x);
+          } else {
+            p.x = ex2_approx(x.x);
+            p.y = ex2_approx(x.y);
+          }
+          lsum2 = fadd2(lsum2, p);
+          pk[i] = pack_bf16x2(p.x, p.y);
+        }
+        tmem_st16(ts + 16 * q, pk);
+      }
+      l += lsum2.x + lsum2.y;
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&p_full[t], 0);  // one arrive per warp, on the leader
+    }
+    mbar_wait(&o_done[t], 0);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    const int q = qp + t * 256 + int(rank) * 128 + r;
+    const int hb = h / Hs, hl = h - hb * Hs;
+    bf16* orow = O + (size_t(hb) * Nq + q) * Hs * dh_real + size_t(hl) * dh_real;
+#pragma unroll 1
+    for (int c = 0; c < DH; c += 32) {
+      float o[32];
+      tmem_ld32(to + c, o);
+      tc_wait_ld();
+      if (q < Nq && c < dh_real) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] *= inv;
+        if (dh_real - c >= 32) store_vec<32>(orow + c, o);
+        else
+          for (int i = 0; i < dh_real - c; ++i) orow[c + i] = __float2bfloat16_rn(o[i]);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+template <bool POLY>
+static cudaError_t launch_attn_pair(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk,
+                                    int dh, float scale, cudaStream_t st, int hs) {
+  using Cfg = AttnPairCfg;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
+      !make_tmap_3d(&tv, V, H, Nk, 128, 128))
+    return cudaErrorInvalidValue;
+  auto kern = attn_pair_kernel<POLY>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(2 * ((Nq + 511) / 512), H);
+  float sl2 = scale * 1.4426950408889634f;
+  void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,
+                  (void*)&Nq, (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs};
+  return launch_ex((const void*)kern, grid, dim3(384), Cfg::SMEM, st, args);
+}
+
 template <int DH>
 static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
                                float scale, cudaStream_t st, int hs) {
-  if (g_attn_impl == 2 || hs != H) {
+  if constexpr (DH == 128) {
+    if (g_attn_impl == 3) {
+      static const int poly = [] {
+        const char* e = getenv("DF_ATTN_POLY");
+        return e ? atoi(e) : 0;
+      }();
+      return poly ? launch_attn_pair<true>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs)
+                  : launch_attn_pair<false>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+    }
+  }
+  if (g_attn_impl >= 2 || hs != H) {
     CUtensorMap tq, tk, tv;
     if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
         !make_tmap_3d(&tv, V, H, Nk, DH, 128))
@@ -578,6 +913,10 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
     }();
     if (dbg == 1) return launch_attn2<DH, false, 1>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
     if (dbg == 2) return launch_attn2<DH, false, 2>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    if (dbg == 3) return launch_attn2<DH, false, 3>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    if (dbg == 4) return launch_attn2<DH, false, 4>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    if (dbg == 5) return launch_attn2<DH, false, 5>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    if (dbg == 6) return launch_attn2<DH, false, 6>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
     return poly ? launch_attn2<DH, true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
                 : launch_attn2<DH, false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
   }

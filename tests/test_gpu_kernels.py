@@ -133,3 +133,18 @@ def test_payload_hash_equals_oracle(tiny_ctx, nbytes):
     buf = inputs.payload_bytes(nbytes, seed=nbytes)
     t = torch.from_numpy(buf).cuda()
     assert tiny_ctx.payload_hash(0, t, nbytes) == cap.payload_hash(buf)
+
+
+@pytest.mark.parametrize("impl", ["1", "3"])
+def test_attention_kernel_variants(impl):
+    """The non-default attention kernels (1: one Q tile per CTA; 3: CTA-pair cta_group::2)
+    pass the same brute-force and special-case checks; the variant is chosen once per
+    process (DF_ATTN_IMPL), so they run in a child pytest."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DF_ATTN_IMPL=impl)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_kernels.py"), "-q", "-x",
+                        "-k", "bruteforce or special_cases"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
