@@ -14,6 +14,7 @@
 //               a stale max (exact after the final 1/l normalisation).
 // attn_simt: fp32 warp-per-row reference-grade kernel for the fp32 validation build.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 #include <cmath>
 #include <cstdlib>
@@ -589,6 +590,294 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
   return launch_ex((const void*)kern, grid, dim3(384), Cfg::SMEM, st, args);
 }
 
+// ------------------------------------------------------------------ attn_tc3: 2 threads per query row
+// Same tensor-core schedule and TMEM map as attn_tc2 (two 128-query tiles per CTA, S/P/O in
+// TMEM, PV0_j, QK0_{j+1}, PV1_j, QK1_{j+1}), but each query row's softmax is shared by two
+// threads of two warps with the same TMEM lane quarter: thread (t, hc, r) owns key columns
+// [64 hc, 64 hc + 64) of S_t row r and output columns [64 hc, 64 hc + 64) of O_t.  The
+// softmax of one tile is on the critical path between its QK and its PV (P aliases S), so
+// halving the per-thread chain (and doubling the warps that hide its latencies) shortens
+// every key-block period.  The two halves agree on the row max through shared memory: each
+// writes its local max rounded UP to fp16 (any common upper bound is a valid stabiliser and
+// both threads then compute the same m), one named barrier per tile and block.
+// Warps 0-15 softmax (tile = w >> 3, half = (w >> 2) & 1, lane quarter = w & 3), warp 16
+// TMA, warp 17 MMA + TMEM allocation.
+constexpr int ATTN3_THREADS = 18 * 32;
+
+DF_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <bool POLY>
+__global__ void __launch_bounds__(ATTN3_THREADS, 1)
+    attn_tc3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                    int dh_real, float scale_log2, int Hs) {
+  constexpr int DH = 128;
+  using Cfg = Attn2Cfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;    // [KST]
+  uint64_t* k_empty = bars + 4;   // [KST]
+  uint64_t* v_full = bars + 7;    // [VST]
+  uint64_t* v_empty = bars + 9;   // [VST]
+  uint64_t* s_full = bars + 11;   // [2] per Q tile
+  uint64_t* p_full = bars + 13;   // [2] per Q tile (256 arrivals)
+  uint64_t* o_done = bars + 15;   // [2] per Q tile (after the last PV)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  __half* red = reinterpret_cast<__half*>(smem + Cfg::OFF_BAR + 256);  // [2 tiles][2 halves][128 rows]
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int h = blockIdx.y;
+  const int q0 = blockIdx.x * 256;
+  const int nkb = (Nk + 127) / 128;
+
+  if (warp == 16 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < Cfg::KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 256);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 17) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 16) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * Cfg::Q_BYTES);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int a = 0; a < Cfg::ATOMS; ++a)
+          tma_load_3d(sQ + t * Cfg::Q_BYTES + a * Cfg::TILE, &tmQ, q_full, a * 64, q0 + t * 128, h);
+      int jk = 0, jv = 0;
+      while (jv < nkb) {
+        if (jk < nkb && jk <= jv + 1) {
+          const int st = jk % Cfg::KST;
+          mbar_wait(&k_empty[st], ((jk / Cfg::KST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], Cfg::KV_BYTES);
+#pragma unroll
+          for (int a = 0; a < Cfg::ATOMS; ++a)
+            tma_load_3d(sK + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmK, &k_full[st], a * 64, jk * 128, h);
+          ++jk;
+        } else {
+          const int st = jv % Cfg::VST;
+          mbar_wait(&v_empty[st], ((jv / Cfg::VST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], Cfg::KV_BYTES);
+#pragma unroll
+          for (int a = 0; a < Cfg::ATOMS; ++a)
+            tma_load_3d(sV + st * Cfg::KV_BYTES + a * Cfg::TILE, &tmV, &v_full[st], a * 64, jv * 128, h);
+          ++jv;
+        }
+      }
+    }
+  } else if (warp == 17) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(128, DH, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_qk = [&](int t, int j) {
+        const uint32_t k_addr = smem_u32(sK + (j % Cfg::KST) * Cfg::KV_BYTES);
+        const uint32_t qa = q_addr + t * Cfg::Q_BYTES;
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const uint32_t off = (k >> 2) * Cfg::TILE + (k & 3) * 32;
+          tc_mma_bf16(tmem + t * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), idesc_qk,
+                      k > 0);
+        }
+        tc_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t v_addr = smem_u32(sV + (j % Cfg::VST) * Cfg::KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc_mma_bf16_ts(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8,
+                         sdesc_sw128(v_addr + k * 2048, Cfg::TILE, 1024), idesc_pv, (j > 0 || k > 0));
+      };
+      auto wait_k = [&](int j) {
+        mbar_wait(&k_full[j % Cfg::KST], (j / Cfg::KST) & 1);
+        tc_fence_after();
+      };
+      mbar_wait(q_full, 0);
+      wait_k(0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      tc_commit(&k_empty[0]);
+      for (int j = 0; j < nkb; ++j) {
+        const bool more = j + 1 < nkb;
+        mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (!more) tc_commit(&o_done[0]);
+        if (more) {
+          wait_k(j + 1);
+          issue_qk(0, j + 1);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j);
+        tc_commit(&v_empty[j % Cfg::VST]);
+        if (!more) tc_commit(&o_done[1]);
+        if (more) {
+          issue_qk(1, j + 1);
+          tc_commit(&k_empty[(j + 1) % Cfg::KST]);
+        }
+      }
+    }
+  } else {
+    const int t = warp >> 3;              // Q tile
+    const int hc = (warp >> 2) & 1;       // key / output column half
+    const int ew = warp & 3;              // TMEM lane quarter
+    const int r = ew * 32 + lane;         // query row within the tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const uint32_t ts = tmem + lane_off + t * 128;
+    const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH + 64 * hc;
+    __half* red_own = red + (t * 2 + hc) * 128 + r;
+    const __half* red_oth = red + (t * 2 + (hc ^ 1)) * 128 + r;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      float s[64];
+      tmem_ld32(ts + 64 * hc, s);
+      tmem_ld32(ts + 64 * hc + 32, s + 32);
+      tc_wait_ld();
+      const int valid = Nk - j * 128 - 64 * hc;
+      if (valid < 64) {  // ragged last key block (warp-uniform)
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= valid) s[i] = -INFINITY;
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], fmaxf(s[i + 2 * u], s[i + 2 * u + 1]));
+      }
+      // both halves must use the same stabiliser: exchange maxima rounded up to fp16
+      const __half hm = __float2half_ru(fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2);
+      *red_own = hm;
+      named_bar_sync(1 + t, 256);
+      const float mx = fmaxf(__half2float(hm), __half2float(*red_oth));
+      const bool need = mx > m_used + 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_used;
+        if (j > 0) {
+          const float alpha = exp2f(m_used - m_new);
+          l *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < 64; c += 16) {
+            float o[16];
+            tmem_ld16(to + c, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= alpha;
+            tmem_st16(to + c, reinterpret_cast<uint32_t*>(o));
+          }
+        }
+        m_used = m_new;
+      }
+      float2 lsum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
+      const float2 nm2 = make_float2(-m_used, -m_used);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = ffma2(make_float2(s[32 * q + 2 * i], s[32 * q + 2 * i + 1]), sc2, nm2);
+          float2 p;
+          if (POLY && (i & 7) >= 5) {
+            p = exp2_poly2(x);
+          } else {
+            p.x = ex2_approx(x.x);
+            p.y = ex2_approx(x.y);
+          }
+          lsum2 = fadd2(lsum2, p);
+          pk[i] = pack_bf16x2(p.x, p.y);
+        }
+        // keys 64 hc + 32 q .. +32 -> packed P columns 32 hc + 16 q .. +16 (S was read by
+        // both halves before the named barrier)
+        tmem_st16(ts + 32 * hc + 16 * q, pk);
+      }
+      l += lsum2.x + lsum2.y;
+      tc_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&o_done[t], 0);
+    tc_fence_after();
+    // row sum = both halves' partial sums; Q_t's shared memory is free once O_t is final
+    float* lred = reinterpret_cast<float*>(sQ + t * Cfg::Q_BYTES);
+    lred[hc * 128 + r] = l;
+    named_bar_sync(1 + t, 256);
+    const float inv = 1.0f / (l + lred[(hc ^ 1) * 128 + r]);
+    const int q = q0 + t * 128 + r;
+    const int hb = h / Hs, hl = h - hb * Hs;
+    bf16* orow = O + (size_t(hb) * Nq + q) * Hs * dh_real + size_t(hl) * dh_real + 64 * hc;
+#pragma unroll 1
+    for (int c = 0; c < 64; c += 32) {
+      float o[32];
+      tmem_ld32(to + c, o);
+      tc_wait_ld();
+      if (q < Nq) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] *= inv;
+        store_vec<32>(orow + c, o);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 17) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <bool POLY>
+static cudaError_t launch_attn3(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, bf16* O, int H,
+                                int Nq, int Nk, int dh, float scale, cudaStream_t st, int hs) {
+  using Cfg = Attn2Cfg<128>;
+  constexpr int SMEM = Cfg::SMEM + 1024;  // + the fp16 max exchange (1 KB) after the barriers
+  static_assert(SMEM <= 232448, "attn_tc3 shared memory");
+  auto kern = attn_tc3_kernel<POLY>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((Nq + 255) / 256, H);
+  float sl2 = scale * 1.4426950408889634f;
+  void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,
+                  (void*)&Nq, (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs};
+  return launch_ex((const void*)kern, grid, dim3(ATTN3_THREADS), SMEM, st, args);
+}
+
 // ------------------------------------------------------------------ attn_pair: CTA-pair (cta_group::2)
 // A cluster of two CTAs runs M = 256 MMAs: query tile t of the pair is 256 rows, 128 in each
 // CTA's shared memory and TMEM. Each CTA stages HALF of every K/V block (K: 64 of the 128
@@ -898,6 +1187,20 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
                   : launch_attn_pair<false>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
     }
   }
+  if constexpr (DH == 128) {
+    if (g_attn_impl == 4 && dh == 128) {
+      static const int poly = [] {
+        const char* e = getenv("DF_ATTN_POLY");
+        return e ? atoi(e) : 0;
+      }();
+      CUtensorMap tq, tk, tv;
+      if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
+          !make_tmap_3d(&tv, V, H, Nk, DH, 128))
+        return cudaErrorInvalidValue;
+      return poly ? launch_attn3<true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
+                  : launch_attn3<false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+    }
+  }
   if (g_attn_impl >= 2 || hs != H) {
     CUtensorMap tq, tk, tv;
     if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
@@ -940,8 +1243,11 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
 cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
                     float scale, cudaStream_t st, int heads_per_sample) {
   static const int impl_env = [] {
-    const char* e = getenv("DF_ATTN_IMPL");  // 1: one Q tile per CTA (round-1 kernel), 2: two (default)
-    return e ? atoi(e) : 2;
+    // 1: one Q tile per CTA (round-1 kernel); 2: two Q tiles, one softmax thread per row;
+    // 3: CTA pair (cta_group::2); 4 (default): two Q tiles, two softmax threads per row
+    // (dh = 128; other head sizes take variant 2)
+    const char* e = getenv("DF_ATTN_IMPL");
+    return e ? atoi(e) : 4;
   }();
   g_attn_impl = impl_env;
   const int hs = heads_per_sample > 0 ? heads_per_sample : H;

@@ -129,6 +129,13 @@ struct Inbox {
     }
     cv.notify_one();
   }
+  bool try_pop(T& out) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (q.empty()) return false;
+    out = q.front();
+    q.pop_front();
+    return true;
+  }
   bool pop(T& out, std::atomic<bool>& stop) {
     std::unique_lock<std::mutex> lk(mu);
     cv.wait(lk, [&] { return !q.empty() || stop.load(); });
@@ -464,10 +471,38 @@ void e_worker(df_ctx* ctx, Inst* me) {
   }
 }
 
+// T finishes a request once its compute has drained on the device: stage time from the
+// device events, profiler harvest, hand the job to D (whose stream already waits on the
+// T->D chunk events, so D may enqueue its decode right away).
+void t_finish(df_ctx* ctx, Inst* me, ReqState* rs, Inst* D) {
+  WK(cudaEventSynchronize(rs->ev[3]));
+  if (me->m.prof) me->m.prof->harvest();
+  rs->t_end[1] = now_s();
+  const double dev_s = ev_ms(rs->ev[2], rs->ev[3]) * 1e-3;
+  me->served++;
+  me->busy_ns += uint64_t(dev_s * 1e9);
+  sched_note(ctx, 1, rs->req.steps, dev_s);
+  D->inbox.push(Job{rs});
+}
+
+// One T instance.  The host enqueues request r's whole prologue + S steps + T->D send,
+// then finishes request r-1 (waits for its device completion): the compute stream always
+// holds the next request's work, so no host round trip sits between two requests on the
+// device (T starts the next request without waiting).  The conditioning cache is
+// one persistent buffer reused in stream order (no cudaMalloc/cudaFree per request).
 void t_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
-  Job j;
-  while (me->inbox.pop(j, ctx->stop)) {
+  Cond cd;  // persistent: Model::prepare reuses its arena when it is large enough
+  ReqState* pend = nullptr;
+  Inst* pendD = nullptr;
+  for (;;) {
+    Job j;
+    if (pend && !me->inbox.try_pop(j)) {  // nothing queued: finish the request in flight first
+      t_finish(ctx, me, pend, pendD);
+      pend = nullptr;
+      continue;
+    }
+    if (!pend && !me->inbox.pop(j, ctx->stop)) break;
     ReqState* rs = j.rs;
     rs->t_start[1] = now_s();
     ctx->qd_ns[1] += uint64_t(std::max(0.0, rs->t_start[1] - rs->t_end[0]) * 1e9);
@@ -489,7 +524,6 @@ void t_worker(df_ctx* ctx, Inst* me) {
     Xfer* x0 = rs->x[0];
     for (uint32_t c = 0; c < x0->nchunks; ++c) WK(cudaStreamWaitEvent(me->compute, x0->chunk_ev[c], 0));
     std::vector<float> sig = sigmas_host(S, rs->req.shift);
-    Cond cd;
     const void* cbuf = me->slots.slots[rs->slot[0]].buf;
     const bool cfgr = cfg_on(rs->req.guidance);
     WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->ctx_bytes : nullptr,
@@ -498,6 +532,11 @@ void t_worker(df_ctx* ctx, Inst* me) {
     me->slots.release(rs->slot[0]);  // producer's comm stream waits on `consumed` before reuse
     for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
     WK(cudaEventRecord(rs->ev[3], me->compute));
+    // r-1 drains while r is already queued behind it; finishing it before claiming a D slot
+    // means this worker never holds an unsent D slot while it blocks (no slot deadlock with
+    // several T instances sharing one D)
+    if (pend) t_finish(ctx, me, pend, pendD);
+    pend = nullptr;
     // T -> D: claim a D slot, send the final latent in per-frame chunks
     const int did = pick(ctx, DF_D, rs->seq);
     Inst* D = ctx->inst[did].get();
@@ -523,16 +562,12 @@ void t_worker(df_ctx* ctx, Inst* me) {
     }
     rs->x[1] = xx;
     WK(cudaEventRecord(me->xsent[b], me->comm));
-    // the cond cache must outlive the queued steps: free it once the compute stream passes
-    WK(cudaStreamSynchronize(me->compute));
-    if (me->m.prof) me->m.prof->harvest();
-    cd.mem.release();
-    rs->t_end[1] = now_s();
-    me->served++;
-    me->busy_ns += uint64_t((rs->t_end[1] - rs->t_start[1]) * 1e9);
-    sched_note(ctx, 1, rs->req.steps, rs->t_end[1] - rs->t_start[1]);
-    D->inbox.push(Job{rs});  // T dequeues its next request without waiting for the send
+    pend = rs;
+    pendD = D;
   }
+  if (pend) t_finish(ctx, me, pend, pendD);
+  WK(cudaStreamSynchronize(me->compute));
+  cd.mem.release();
 }
 
 void d_worker(df_ctx* ctx, Inst* me) {
@@ -1297,6 +1332,10 @@ df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset) {
   for (auto& ip : ctx->inst)
     if (ip->stage == DF_T) ip->m.prof = enable ? &ctx->prof : nullptr;
   if (reset) ctx->prof.reset();
+  // one video request launches ~22k kernels (two events each) between
+  // harvests; creating events inside the timed region would put cudaEventCreate on the
+  // launch path
+  if (enable) ctx->prof.reserve(1 << 16);
   return DF_OK;
 }
 

@@ -70,15 +70,27 @@ DF_DEV void store_vec(float* o, const float* v) {
   for (int i = 0; i < CW; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
 }
 
-DF_DEV float2 rope_cs(const Epi& e, int m, int pair) {
-  int hw = e.Hp * e.Wp;
-  int f = m / hw, rem = m - f * hw;
-  int hh = rem / e.Wp, ww = rem - hh * e.Wp;
-  if (pair < e.Df2) return e.rope_tab[f * e.Df2 + pair];
-  pair -= e.Df2;
-  if (pair < e.Dh2) return e.rope_tab[e.Fp * e.Df2 + hh * e.Dh2 + pair];
-  pair -= e.Dh2;
-  return e.rope_tab[e.Fp * e.Df2 + e.Hp * e.Dh2 + ww * e.Dw2 + pair];
+
+// rope_cs with the token's grid coordinates decoded once: per-axis table rows, indexed
+// by the pair number within the head (the f rows cover pairs [0, Df2), h [Df2, Df2+Dh2),
+// w the rest; the h and w bases are pre-offset so the pair index is used unchanged)
+struct RopeRow {
+  const float2* f;
+  const float2* h;
+  const float2* w;
+};
+DF_DEV RopeRow rope_row(const Epi& e, int m) {
+  const int hw = e.Hp * e.Wp;
+  const int f = m / hw, rem = m - f * hw;
+  const int hh = rem / e.Wp, ww = rem - hh * e.Wp;
+  RopeRow r;
+  r.f = e.rope_tab + f * e.Df2;
+  r.h = e.rope_tab + e.Fp * e.Df2 + hh * e.Dh2 - e.Df2;
+  r.w = e.rope_tab + e.Fp * e.Df2 + e.Hp * e.Dh2 + ww * e.Dw2 - e.Df2 - e.Dh2;
+  return r;
+}
+DF_DEV float2 rope_at(const Epi& e, const RopeRow& r, int pair) {
+  return pair < e.Df2 ? r.f[pair] : (pair < e.Df2 + e.Dh2 ? r.h[pair] : r.w[pair]);
 }
 
 // EPI_HEADS math on one head: bias, per-head RMSNorm * gain (if the section has a gain),
@@ -98,9 +110,10 @@ DF_DEV void heads_math(const Epi& e, int m, int n0, int sec, int hd, float* v) {
     for (int i = 0; i < CW; ++i) v[i] = v[i] * inv * bf2f(gg[i]);
   }
   if (e.sec_rope[sec]) {
+    const RopeRow rr = rope_row(e, m);
 #pragma unroll
     for (int p = 0; p < CW / 2; ++p) {
-      float2 cs = rope_cs(e, m, p);
+      float2 cs = rope_at(e, rr, p);
       float a = v[2 * p], b = v[2 * p + 1];
       v[2 * p] = a * cs.x - b * cs.y;
       v[2 * p + 1] = a * cs.y + b * cs.x;
@@ -130,9 +143,10 @@ DF_DEV void heads_math_s(const Epi& e, int m, int sec, const float* sb, const fl
     }
   }
   if (e.sec_rope[sec]) {
+    const RopeRow rr = rope_row(e, m);
 #pragma unroll
     for (int p = 0; p < CW / 2; ++p) {
-      float2 cs = rope_cs(e, m, p);
+      float2 cs = rope_at(e, rr, p);
       float a = v[2 * p], b = v[2 * p + 1];
       v[2 * p] = a * cs.x - b * cs.y;
       v[2 * p + 1] = a * cs.y + b * cs.x;

@@ -594,6 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const int rowc = min(row, M - 1);            // lanes past M: any valid position (TMA clips them)
         const int bl = straddle ? rowc / mper : b0;
         const int mloc = rowc - bl * mper;
+        const RopeRow rrow = rope_row(epi, mloc);  // integer divisions once per row, not per pair
 #pragma unroll 1
         for (int c = 0; c < 256; c += 128) {
           const int n0 = nb * 256 + c;
@@ -635,7 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             if (rope) {
 #pragma unroll
               for (int p = 0; p < 32; ++p) {
-                const float2 cs = rope_cs(epi, mloc, 32 * hf + p);
+                const float2 cs = rope_at(epi, rrow, 32 * hf + p);
                 const float x0 = w[2 * p], x1 = w[2 * p + 1];
                 w[2 * p] = x0 * cs.x - x1 * cs.y;
                 w[2 * p + 1] = x0 * cs.y + x1 * cs.x;

@@ -51,6 +51,14 @@ cudaEvent_t Prof::get() {
   pool.pop_back();
   return e;
 }
+void Prof::reserve(size_t n) {
+  std::lock_guard<std::mutex> lk(mu);
+  while (pool.size() < n) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    pool.push_back(e);
+  }
+}
 void Prof::harvest() {
   std::lock_guard<std::mutex> lk(mu);
   for (auto& p : pending) {
@@ -380,7 +388,12 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   size_t need = al((S + 1) * 4) + 2 * al(kvb) + al(size_t(S) * d * 4) + al(size_t(S) * 6 * d * 4) +
                 al(size_t(S) * fd * 4) + al(size_t(S) * d * 4) + 2 * al(size_t(Lt) * d * ab) +
                 (f32() ? al(size_t(Lt) * 2 * d * 4) : 0) + 4096;
-  DF_TRY(cd.mem.reserve(need));
+  if (cd.mem.base && cd.mem.cap >= need) {
+    cd.mem.used = 0;  // persistent cache of a T worker: reused in stream order
+  } else {
+    cd.mem.release();
+    DF_TRY(cd.mem.reserve(need));
+  }
   cd.sig_dev = (float*)cd.mem.take((S + 1) * 4);
   cd.kc = cd.mem.take(kvb);
   cd.vc = cd.mem.take(kvb);

@@ -72,6 +72,7 @@ struct Prof {
   uint64_t count[K_COUNT] = {};
   double ms[K_COUNT] = {}, flops[K_COUNT] = {}, bytes[K_COUNT] = {};
   cudaEvent_t get();
+  void reserve(size_t n);  // pre-create events so the launch path never calls cudaEventCreate
   void harvest();   // consumes completed pairs (blocks on each pending pair)
   void reset();
 };
