@@ -200,7 +200,10 @@ df_status df_payload_hash(df_ctx* ctx, int32_t inst, const void* buf_dev, uint64
 /* Parity check 0: copy the bf16 bits of parameter `tensor_id` (logical [in,out]
  * row-major, DESIGN.md parameter table) of instance inst into host `dst`. */
 df_status df_weight_bits(df_ctx* ctx, int32_t inst, uint32_t tensor_id, uint16_t* dst, uint64_t n);
-/* out = A[M,K] (bf16) x W[N,K]^T (bf16), fp32 out [M,N]; tensor-core kernel (tc=1) or SIMT (tc=0). */
+/* out = A[M,K] (bf16) x W[N,K]^T (bf16), fp32 out [M,N]; tensor-core kernel (tc=1), tensor cores
+ * with the stream-K schedule (tc=2: uses the workspace of the first T instance, taken when whole-tile
+ * waves would leave > 8 % of the CTA pairs idle; DF_ERR_STATE without a T instance), or
+ * SIMT (tc=0).  Device pointers; stream-ordered. */
 df_status df_op_gemm(df_ctx* ctx, const void* A, const void* W, float* out, int32_t M, int32_t N, int32_t K,
                      int32_t tc, void* stream);
 /* O[Nq, H*dh] = softmax(Q K^T * scale) V, head-major bf16 Q/K/V [H][N][dh_pad]. */

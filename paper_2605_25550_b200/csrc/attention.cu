@@ -590,6 +590,29 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
   return launch_ex((const void*)kern, grid, dim3(384), Cfg::SMEM, st, args);
 }
 
+// p = 2^x for a pair of logits, packed to bf16x2 for P; adds the pair to the row sum.
+// EXPM 0: MUFU ex2 (fp32); 1: 3 of 8 pairs by polynomial on the FMA pipe; 2: 1 of 4 pairs;
+// 3: one MUFU ex2.bf16x2 per pair (input rounded to bf16: coarser, profiling only).
+template <int EXPM>
+DF_DEV uint32_t softmax_exp2(float2 x, int i, float2& lsum2) {
+  if (EXPM == 3) {
+    const uint32_t xb = pack_bf16x2(x.x, x.y);
+    uint32_t pb;
+    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(pb) : "r"(xb));
+    lsum2 = fadd2(lsum2, make_float2(__uint_as_float(pb << 16), __uint_as_float(pb & 0xffff0000u)));
+    return pb;
+  }
+  float2 p;
+  if ((EXPM == 1 && (i & 7) >= 5) || (EXPM == 2 && (i & 3) == 3)) {
+    p = exp2_poly2(x);
+  } else {
+    p.x = ex2_approx(x.x);
+    p.y = ex2_approx(x.y);
+  }
+  lsum2 = fadd2(lsum2, p);
+  return pack_bf16x2(p.x, p.y);
+}
+
 // ------------------------------------------------------------------ attn_tc3: 2 threads per query row
 // Same tensor-core schedule and TMEM map as attn_tc2 (two 128-query tiles per CTA, S/P/O in
 // TMEM, PV0_j, QK0_{j+1}, PV1_j, QK1_{j+1}), but each query row's softmax is shared by two
@@ -605,8 +628,20 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
 constexpr int ATTN3_THREADS = 18 * 32;
 
 DF_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+DF_DEV void sts_u16(uint32_t a, unsigned short v) { asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory"); }
+DF_DEV unsigned short lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+DF_DEV void sts_f32(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
+DF_DEV float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
 
-template <bool POLY>
+template <int EXPM>
 __global__ void __launch_bounds__(ATTN3_THREADS, 1)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
@@ -625,7 +660,10 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
   uint64_t* v_full = bars + 7;    // [VST]
   uint64_t* v_empty = bars + 9;   // [VST]
   uint64_t* s_full = bars + 11;   // [2] per Q tile
-  uint64_t* p_full = bars + 13;   // [2] per Q tile (256 arrivals)
+  // P of tile t is published in key quarters (32 keys each; quarter 2 hc + q is written by
+  // the 4 warps of half hc, chunk q): PV starts on the first quarter while the rest is
+  // still being exponentiated
+  uint64_t* p_q = bars + 18;      // [2 tiles][4 quarters], one arrive per warp
   uint64_t* o_done = bars + 15;   // [2] per Q tile (after the last PV)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   __half* red = reinterpret_cast<__half*>(smem + Cfg::OFF_BAR + 256);  // [2 tiles][2 halves][128 rows]
@@ -651,7 +689,7 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 256);
+      for (int u = 0; u < 4; ++u) mbar_init(&p_q[s * 4 + u], 4);
       mbar_init(&o_done[s], 1);
     }
     fence_mbar_init();
@@ -694,57 +732,79 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
       }
     }
   } else if (warp == 17) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
-      constexpr uint32_t idesc_pv = idesc_bf16(128, DH, false, true);
-      const uint32_t q_addr = smem_u32(sQ);
-      auto issue_qk = [&](int t, int j) {
-        const uint32_t k_addr = smem_u32(sK + (j % Cfg::KST) * Cfg::KV_BYTES);
-        const uint32_t qa = q_addr + t * Cfg::Q_BYTES;
+    // the whole warp runs the schedule (warp-uniform values live in uniform registers and
+    // descriptors are base + constant offsets); one elected lane issues each MMA batch
+    constexpr uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idesc_pv = idesc_bf16(128, DH, false, true);
+    const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+    const uint64_t dv = sdesc_sw128(smem_u32(sV), Cfg::TILE, 1024);
+    auto issue_qk = [&](int t, int j) {
+      const uint64_t a0 = dq + uint64_t((t * Cfg::Q_BYTES) >> 4);
+      const uint64_t b0 = dk + uint64_t(((j % Cfg::KST) * Cfg::KV_BYTES) >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
-          const uint32_t off = (k >> 2) * Cfg::TILE + (k & 3) * 32;
-          tc_mma_bf16(tmem + t * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), idesc_qk,
-                      k > 0);
+          const uint32_t off = ((k >> 2) * Cfg::TILE + (k & 3) * 32) >> 4;
+          tc_mma_bf16(tmem + t * 128, a0 + off, b0 + off, idesc_qk, k > 0);
         }
         tc_commit(&s_full[t]);
-      };
-      auto issue_pv = [&](int t, int j) {
-        const uint32_t v_addr = smem_u32(sV + (j % Cfg::VST) * Cfg::KV_BYTES);
+      }
+      __syncwarp();
+    };
+    // PV of tile t, key quarter u (k-steps 2u, 2u+1); quarters are issued in the order
+    // 0, 2, 1, 3 (both halves' first chunks first); the first MMA of block 0 overwrites O
+    auto issue_pv = [&](int t, int j, int u, bool first) {
+      const uint64_t b0 = dv + uint64_t(((j % Cfg::VST) * Cfg::KV_BYTES) >> 4);
+      if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          tc_mma_bf16_ts(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8,
-                         sdesc_sw128(v_addr + k * 2048, Cfg::TILE, 1024), idesc_pv, (j > 0 || k > 0));
-      };
-      auto wait_k = [&](int j) {
-        mbar_wait(&k_full[j % Cfg::KST], (j / Cfg::KST) & 1);
-        tc_fence_after();
-      };
-      mbar_wait(q_full, 0);
-      wait_k(0);
-      issue_qk(0, 0);
-      issue_qk(1, 0);
-      tc_commit(&k_empty[0]);
-      for (int j = 0; j < nkb; ++j) {
-        const bool more = j + 1 < nkb;
-        mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        issue_pv(0, j);
-        if (!more) tc_commit(&o_done[0]);
-        if (more) {
-          wait_k(j + 1);
-          issue_qk(0, j + 1);
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k = 2 * u + kk;
+          tc_mma_bf16_ts(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, b0 + uint64_t((k * 2048) >> 4), idesc_pv,
+                         !(first && kk == 0));
         }
-        mbar_wait(&p_full[1], j & 1);
+      }
+      __syncwarp();
+    };
+    auto pv_tile = [&](int t, int j, bool last) {
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        const int u = (n >> 1) | ((n & 1) << 1);  // 0, 2, 1, 3
+        mbar_wait(&p_q[t * 4 + u], j & 1);
         tc_fence_after();
-        issue_pv(1, j);
-        tc_commit(&v_empty[j % Cfg::VST]);
-        if (!more) tc_commit(&o_done[1]);
-        if (more) {
-          issue_qk(1, j + 1);
-          tc_commit(&k_empty[(j + 1) % Cfg::KST]);
-        }
+        issue_pv(t, j, u, j == 0 && n == 0);
+      }
+      if (elect_one()) {
+        if (t == 1) tc_commit(&v_empty[j % Cfg::VST]);
+        if (last) tc_commit(&o_done[t]);
+      }
+      __syncwarp();
+    };
+    auto commit1 = [&](uint64_t* bar) {
+      if (elect_one()) tc_commit(bar);
+      __syncwarp();
+    };
+    auto wait_k = [&](int j) {
+      mbar_wait(&k_full[j % Cfg::KST], (j / Cfg::KST) & 1);
+      tc_fence_after();
+    };
+    mbar_wait(q_full, 0);
+    wait_k(0);
+    issue_qk(0, 0);
+    issue_qk(1, 0);
+    commit1(&k_empty[0]);
+    for (int j = 0; j < nkb; ++j) {
+      const bool more = j + 1 < nkb;
+      mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
+      pv_tile(0, j, !more);
+      if (more) {
+        wait_k(j + 1);
+        issue_qk(0, j + 1);
+      }
+      pv_tile(1, j, !more);
+      if (more) {
+        issue_qk(1, j + 1);
+        commit1(&k_empty[(j + 1) % Cfg::KST]);
       }
     }
   } else {
@@ -755,12 +815,21 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
     const uint32_t ts = tmem + lane_off + t * 128;
     const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH + 64 * hc;
-    __half* red_own = red + (t * 2 + hc) * 128 + r;
-    const __half* red_oth = red + (t * 2 + (hc ^ 1)) * 128 + r;
+    const uint32_t red_own = smem_u32(red + (t * 2 + hc) * 128 + r);
+    const uint32_t red_oth = smem_u32(red + (t * 2 + (hc ^ 1)) * 128 + r);
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
+      if (EXPM == 9) {  // profiling only: tensor cores + synchronisation, no softmax (wrong results)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&p_q[t * 4 + 2 * hc]);
+          mbar_arrive(&p_q[t * 4 + 2 * hc + 1]);
+        }
+        continue;
+      }
       float s[64];
       tmem_ld32(ts + 64 * hc, s);
       tmem_ld32(ts + 64 * hc + 32, s + 32);
@@ -779,9 +848,9 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
       }
       // both halves must use the same stabiliser: exchange maxima rounded up to fp16
       const __half hm = __float2half_ru(fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2);
-      *red_own = hm;
+      sts_u16(red_own, __half_as_ushort(hm));
       named_bar_sync(1 + t, 256);
-      const float mx = fmaxf(__half2float(hm), __half2float(*red_oth));
+      const float mx = fmaxf(__half2float(hm), __half2float(__ushort_as_half(lds_u16(red_oth))));
       const bool need = mx > m_used + 8.0f;
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? mx : m_used;
@@ -803,30 +872,26 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
       float2 lsum2 = make_float2(0.f, 0.f);
       const float2 sc2 = make_float2(scale_log2, scale_log2);
       const float2 nm2 = make_float2(-m_used, -m_used);
+      // keys 64 hc + 32 q .. +32 -> packed P columns 32 hc + 16 q .. +16 (S was read by both
+      // halves before the named barrier); chunk 0's store drains while chunk 1 is computed
+      uint32_t pk[16];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        uint32_t pk[16];
+      for (int i = 0; i < 16; ++i)
+        pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2), i, lsum2);
+      tmem_st16(ts + 32 * hc, pk);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float2 x = ffma2(make_float2(s[32 * q + 2 * i], s[32 * q + 2 * i + 1]), sc2, nm2);
-          float2 p;
-          if (POLY && (i & 7) >= 5) {
-            p = exp2_poly2(x);
-          } else {
-            p.x = ex2_approx(x.x);
-            p.y = ex2_approx(x.y);
-          }
-          lsum2 = fadd2(lsum2, p);
-          pk[i] = pack_bf16x2(p.x, p.y);
-        }
-        // keys 64 hc + 32 q .. +32 -> packed P columns 32 hc + 16 q .. +16 (S was read by
-        // both halves before the named barrier)
-        tmem_st16(ts + 32 * hc + 16 * q, pk);
-      }
+      for (int i = 0; i < 16; ++i)
+        pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[32 + 2 * i], s[32 + 2 * i + 1]), sc2, nm2), i, lsum2);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_q[t * 4 + 2 * hc]);
+      tmem_st16(ts + 32 * hc + 16, pk);
       l += lsum2.x + lsum2.y;
       tc_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_q[t * 4 + 2 * hc + 1]);
     }
     mbar_wait(&o_done[t], 0);
     tc_fence_after();
@@ -858,13 +923,13 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
   }
 }
 
-template <bool POLY>
+template <int EXPM>
 static cudaError_t launch_attn3(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, bf16* O, int H,
                                 int Nq, int Nk, int dh, float scale, cudaStream_t st, int hs) {
   using Cfg = Attn2Cfg<128>;
   constexpr int SMEM = Cfg::SMEM + 1024;  // + the fp16 max exchange (1 KB) after the barriers
   static_assert(SMEM <= 232448, "attn_tc3 shared memory");
-  auto kern = attn_tc3_kernel<POLY>;
+  auto kern = attn_tc3_kernel<EXPM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -1152,6 +1217,296 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
+// ------------------------------------------------------------------ attn_pair3: CTA pair + 2 threads per row
+// attn_pair's tensor-core schedule (M = 256 over a CTA pair: per SM the QK^T shared-memory
+// operand reads drop from 8 KB to 6 KB per 64-clock K step and the PV B reads halve, so the
+// 128 B/clk shared-memory port stops pacing the MMAs) with attn_tc3's softmax (two threads
+// per query row).  The row maxima are exchanged exactly (fp32) through shared memory.
+template <int EXPM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
+    attn_pair3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                      int dh_real, float scale_log2, int Hs) {
+  using Cfg = AttnPairCfg;
+  constexpr int DH = Cfg::DH;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;                 // [KST]  leader
+  uint64_t* k_empty = k_full + Cfg::KST;       // [KST]  both (multicast commit)
+  uint64_t* v_full = k_empty + Cfg::KST;       // [VST]  leader
+  uint64_t* v_empty = v_full + Cfg::VST;       // [VST]  both
+  uint64_t* s_full = v_empty + Cfg::VST;       // [2]    both
+  uint64_t* p_full = s_full + 2;               // [2]    leader: 8 softmax warps x 2 CTAs
+  uint64_t* o_done = p_full + 2;               // [2]    both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  float* red = reinterpret_cast<float*>(smem + Cfg::OFF_BAR + 256);  // [2 tiles][2 halves][128 rows]
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int h = blockIdx.y;
+  const int qp = (blockIdx.x >> 1) * 512;      // first query row of the pair
+  const int nkb = (Nk + 127) / 128;
+
+  if (warp == 16 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 2);
+    for (int s = 0; s < Cfg::KST; ++s) {
+      mbar_init(&k_full[s], 2);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::VST; ++s) {
+      mbar_init(&v_full[s], 2);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 16);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 17) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 16) {
+    if (lane == 0) {
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * Cfg::Q_BYTES);
+      else mbar_arrive_cluster(q_full, 0);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_pair(sQ + t * Cfg::Q_BYTES + a * 2 * Cfg::ATOM, &tmQ, q_full, a * 64,
+                           qp + t * 256 + int(rank) * 128, h);
+      int jk = 0, jv = 0;
+      while (jv < nkb) {
+        if (jk < nkb && jk <= jv + 2) {
+          const int st = jk % Cfg::KST;
+          mbar_wait(&k_empty[st], ((jk / Cfg::KST) & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(&k_full[st], 2 * Cfg::K_BYTES);
+          else mbar_arrive_cluster(&k_full[st], 0);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+            tma_load_3d_pair(sK + st * Cfg::K_BYTES + a * Cfg::ATOM, &tmK, &k_full[st], a * 64,
+                             jk * 128 + int(rank) * 64, h);
+          ++jk;
+        } else {
+          const int st = jv % Cfg::VST;
+          mbar_wait(&v_empty[st], ((jv / Cfg::VST) & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(&v_full[st], 2 * Cfg::V_BYTES);
+          else mbar_arrive_cluster(&v_full[st], 0);
+          tma_load_3d_pair(sV + st * Cfg::V_BYTES, &tmV, &v_full[st], int(rank) * 64, jv * 128, h);
+          ++jv;
+        }
+      }
+    }
+  } else if (warp == 17) {
+    if (leader) {  // whole warp runs the schedule; one elected lane issues each MMA batch
+      constexpr uint32_t idesc_qk = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(256, DH, false, true);
+      const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(sV), Cfg::V_BYTES, 1024);
+      auto issue_qk = [&](int t, int j) {
+        const uint64_t a0 = dq + uint64_t((t * Cfg::Q_BYTES) >> 4);
+        const uint64_t b0 = dk + uint64_t(((j % Cfg::KST) * Cfg::K_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k)
+            tc_mma_bf16_pair(tmem + t * 128, a0 + uint64_t(((k >> 2) * 2 * Cfg::ATOM + (k & 3) * 32) >> 4),
+                             b0 + uint64_t(((k >> 2) * Cfg::ATOM + (k & 3) * 32) >> 4), idesc_qk, k > 0);
+          tc_commit_pair(&s_full[t], 0x3);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int j, bool last) {
+        const uint64_t b0 = dv + uint64_t(((j % Cfg::VST) * Cfg::V_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc_mma_bf16_ts_pair(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, b0 + uint64_t((k * 2048) >> 4),
+                                idesc_pv, (j > 0 || k > 0));
+          if (t == 1) tc_commit_pair(&v_empty[j % Cfg::VST], 0x3);
+          if (last) tc_commit_pair(&o_done[t], 0x3);
+        }
+        __syncwarp();
+      };
+      auto commit1 = [&](uint64_t* bar) {
+        if (elect_one()) tc_commit_pair(bar, 0x3);
+        __syncwarp();
+      };
+      auto wait_k = [&](int j) {
+        mbar_wait(&k_full[j % Cfg::KST], (j / Cfg::KST) & 1);
+        tc_fence_after();
+      };
+      mbar_wait(q_full, 0);
+      wait_k(0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      commit1(&k_empty[0]);
+      for (int j = 0; j < nkb; ++j) {
+        const bool more = j + 1 < nkb;
+        mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j, !more);
+        if (more) {
+          wait_k(j + 1);
+          issue_qk(0, j + 1);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j, !more);
+        if (more) {
+          issue_qk(1, j + 1);
+          commit1(&k_empty[(j + 1) % Cfg::KST]);
+        }
+      }
+    }
+  } else {
+    const int t = warp >> 3;              // Q tile
+    const int hc = (warp >> 2) & 1;       // key / output column half
+    const int ew = warp & 3;              // TMEM lane quarter
+    const int r = ew * 32 + lane;         // query row within this CTA's half of the tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const uint32_t ts = tmem + lane_off + t * 128;
+    const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH + 64 * hc;
+    const uint32_t red_own = smem_u32(red + (t * 2 + hc) * 128 + r);
+    const uint32_t red_oth = smem_u32(red + (t * 2 + (hc ^ 1)) * 128 + r);
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      if (EXPM == 9) {  // profiling only: tensor cores + synchronisation, no softmax (wrong results)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&p_full[t], 0);
+        continue;
+      }
+      float s[64];
+      tmem_ld32(ts + 64 * hc, s);
+      tmem_ld32(ts + 64 * hc + 32, s + 32);
+      tc_wait_ld();
+      const int valid = Nk - j * 128 - 64 * hc;
+      if (valid < 64) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= valid) s[i] = -INFINITY;
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], fmaxf(s[i + 2 * u], s[i + 2 * u + 1]));
+      }
+      const float mloc = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+      sts_f32(red_own, mloc);
+      named_bar_sync(1 + t, 256);
+      const float mx = fmaxf(mloc, lds_f32(red_oth));
+      const bool need = mx > m_used + 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_used;
+        if (j > 0) {
+          const float alpha = exp2f(m_used - m_new);
+          l *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < 64; c += 16) {
+            float o[16];
+            tmem_ld16(to + c, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= alpha;
+            tmem_st16(to + c, reinterpret_cast<uint32_t*>(o));
+          }
+        }
+        m_used = m_new;
+      }
+      float2 lsum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
+      const float2 nm2 = make_float2(-m_used, -m_used);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = ffma2(make_float2(s[32 * q + 2 * i], s[32 * q + 2 * i + 1]), sc2, nm2);
+          pk[i] = softmax_exp2<EXPM>(x, i, lsum2);
+        }
+        tmem_st16(ts + 32 * hc + 16 * q, pk);
+      }
+      l += lsum2.x + lsum2.y;
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&p_full[t], 0);  // one arrive per warp, on the leader
+    }
+    mbar_wait(&o_done[t], 0);
+    tc_fence_after();
+    float* lred = reinterpret_cast<float*>(sQ + t * Cfg::Q_BYTES);  // Q_t is free once O_t is final
+    lred[hc * 128 + r] = l;
+    named_bar_sync(1 + t, 256);
+    const float inv = 1.0f / (l + lred[(hc ^ 1) * 128 + r]);
+    const int q = qp + t * 256 + int(rank) * 128 + r;
+    const int hb = h / Hs, hl = h - hb * Hs;
+    bf16* orow = O + (size_t(hb) * Nq + q) * Hs * dh_real + size_t(hl) * dh_real + 64 * hc;
+#pragma unroll 1
+    for (int c = 0; c < 64; c += 32) {
+      float o[32];
+      tmem_ld32(to + c, o);
+      tc_wait_ld();
+      if (q < Nq) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] *= inv;
+        store_vec<32>(orow + c, o);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 17) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+template <int EXPM>
+static cudaError_t launch_attn_pair3(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk,
+                                     int dh, float scale, cudaStream_t st, int hs) {
+  using Cfg = AttnPairCfg;
+  constexpr int SMEM = Cfg::SMEM + 2048;  // + fp32 max exchange after the barriers
+  static_assert(SMEM <= 232448, "attn_pair3 shared memory");
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
+      !make_tmap_3d(&tv, V, H, Nk, 128, 128))
+    return cudaErrorInvalidValue;
+  auto kern = attn_pair3_kernel<EXPM>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(2 * ((Nq + 511) / 512), H);
+  float sl2 = scale * 1.4426950408889634f;
+  void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,
+                  (void*)&Nq, (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs};
+  return launch_ex((const void*)kern, grid, dim3(ATTN3_THREADS), SMEM, st, args);
+}
+
 template <bool POLY>
 static cudaError_t launch_attn_pair(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk,
                                     int dh, float scale, cudaStream_t st, int hs) {
@@ -1188,17 +1543,35 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
     }
   }
   if constexpr (DH == 128) {
-    if (g_attn_impl == 4 && dh == 128) {
+    if (g_attn_impl == 5 && dh == 128) {
       static const int poly = [] {
         const char* e = getenv("DF_ATTN_POLY");
         return e ? atoi(e) : 0;
+      }();
+      switch (poly) {  // DF_ATTN_POLY: exponential mode (softmax_exp2)
+        case 1: return launch_attn_pair3<1>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 2: return launch_attn_pair3<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 3: return launch_attn_pair3<3>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 9: return launch_attn_pair3<9>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        default: return launch_attn_pair3<0>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+      }
+    }
+    if (g_attn_impl == 4 && dh == 128) {
+      static const int poly = [] {  // default 2: a quarter of the exponentials on the FMA pipe
+        const char* e = getenv("DF_ATTN_POLY");
+        return e ? atoi(e) : 2;
       }();
       CUtensorMap tq, tk, tv;
       if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||
           !make_tmap_3d(&tv, V, H, Nk, DH, 128))
         return cudaErrorInvalidValue;
-      return poly ? launch_attn3<true>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs)
-                  : launch_attn3<false>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+      switch (poly) {  // DF_ATTN_POLY: exponential mode (softmax_exp2)
+        case 1: return launch_attn3<1>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+        case 2: return launch_attn3<2>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+        case 3: return launch_attn3<3>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+        case 9: return launch_attn3<9>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+        default: return launch_attn3<0>(tq, tk, tv, O, H, Nq, Nk, dh, scale, st, hs);
+      }
     }
   }
   if (g_attn_impl >= 2 || hs != H) {
@@ -1244,8 +1617,8 @@ cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H,
                     float scale, cudaStream_t st, int heads_per_sample) {
   static const int impl_env = [] {
     // 1: one Q tile per CTA (round-1 kernel); 2: two Q tiles, one softmax thread per row;
-    // 3: CTA pair (cta_group::2); 4 (default): two Q tiles, two softmax threads per row
-    // (dh = 128; other head sizes take variant 2)
+    // 3: CTA pair (cta_group::2); 4 (default): two Q tiles, two softmax threads per row;
+    // 5: CTA pair, two softmax threads per row (4 and 5: dh = 128; other head sizes take 2)
     const char* e = getenv("DF_ATTN_IMPL");
     return e ? atoi(e) : 4;
   }();

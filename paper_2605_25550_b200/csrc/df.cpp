@@ -1840,6 +1840,16 @@ df_status df_op_gemm(df_ctx* ctx, const void* A, const void* W, float* out, int3
   e.out = out;
   e.ldo = N;
   g_launches->fetch_add(1);
+  if (tc == 2) {  // tensor cores with the stream-K workspace of the first T instance (tests)
+    for (auto& ip : ctx->inst)
+      if (ip->stage == DF_T && ip->m.sk_ws) {
+        e.sk_ws = ip->m.sk_ws;
+        e.sk_flag = ip->m.sk_flag;
+        e.sk_force = 1;
+        break;
+      }
+    if (!e.sk_ws) return fail(ctx, "df_op_gemm: no stream-K workspace", DF_ERR_STATE);
+  }
   cudaError_t r = tc ? gemm_tc((const bf16*)A, K, (const bf16*)W, K, M, N, K, e, 1, (cudaStream_t)stream)
                      : gemm_simt(A, 1, K, 0, (const bf16*)W, K, out, N, M, N, K, nullptr, ACT_NONE, (cudaStream_t)stream);
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_gemm: ") + cudaGetErrorString(r));

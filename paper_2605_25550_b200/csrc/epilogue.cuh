@@ -47,6 +47,13 @@ struct Epi {
   // v_batch stores v of sample b at v_batch[b * latent_elems + idx] instead of updating x.
   int Mper;
   float* v_batch;
+  // stream-K (CTA-pair GEMM only; null = data-parallel tiles): partial-tile workspace
+  // [pairs][2 CTAs][256 cols][128 rows] fp32, one ready flag per (pair, CTA) holding the
+  // epoch of the launch that wrote it
+  float* sk_ws;
+  unsigned* sk_flag;
+  unsigned sk_epoch;
+  int sk_force;  // host: take stream-K whenever the tile count allows it (tests)
 };
 
 DF_DEV float bias_at(const Epi& e, int n) { return e.bias ? bf2f(e.bias[n]) : 0.0f; }

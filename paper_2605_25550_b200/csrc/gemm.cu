@@ -1,3 +1,4 @@
+#include <atomic>
 // Dense contractions of the DiT step.
 //
 // gemm_tc: persistent, warp-specialised tcgen05 GEMM for sm_100a.
@@ -309,6 +310,55 @@ constexpr int P_SMEM = P_OFF_PRM + 4 * 2048 + 1024;
 // so the residual is never read by the SMs).
 enum : int { TK_DIRECT = 0, TK_STORE_F32 = 1, TK_STORE_BF16 = 2, TK_GRES = 3, TK_SWIGLU = 4, TK_HEADS = 5 };
 
+// Work units of one CTA pair.  Data-parallel: whole 256x256 tiles cid, cid + pairs, ...
+// Stream-K (epi.sk_ws set; needs tiles >= pairs): the tiles x KB k-blocks are cut into
+// `pairs` equal contiguous ranges, so every pair gets the same MMA work; a tile cut between
+// pair p (its first k-blocks, the LAST unit of p) and pair p + 1 (the rest, the FIRST unit
+// of p + 1) is finished by p: p + 1 stores its raw partial accumulator in slot p + 1 of the
+// workspace and publishes it with an epoch flag long before p gets there; p adds it to its
+// own accumulator before the epilogue.  One fp32 add of two fixed partials: deterministic.
+struct PairSched {
+  int tiles, KB, pairs, cid;
+  bool sk;
+  long long u, e;  // stream-K cursor / end (k-block units)
+  int t;           // data-parallel cursor
+  DF_DEV PairSched(int tiles_, int KB_, int pairs_, int cid_, bool sk_)
+      : tiles(tiles_), KB(KB_), pairs(pairs_), cid(cid_), sk(sk_) {
+    const long long total = (long long)tiles * KB;
+    u = total * cid / pairs;
+    e = total * (cid + 1) / pairs;
+    t = cid;
+  }
+  // next unit: tile, k-block range [k0, k1)
+  DF_DEV bool next(int& tile, int& k0, int& k1) {
+    if (!sk) {
+      if (t >= tiles) return false;
+      tile = t;
+      k0 = 0;
+      k1 = KB;
+      t += pairs;
+      return true;
+    }
+    if (u >= e) return false;
+    tile = int(u / KB);
+    k0 = int(u - (long long)tile * KB);
+    const long long left = e - u;
+    k1 = left < (long long)(KB - k0) ? k0 + int(left) : KB;
+    u += k1 - k0;
+    return true;
+  }
+};
+
+DF_DEV void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+DF_DEV unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+DF_DEV void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 epilogue warps
+
 template <int CW, typename OutT, int TK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -336,6 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int KB = (K + GBK - 1) / GBK;
   const int cid = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
+  const bool sk = epi.sk_ws != nullptr;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -363,10 +414,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < tiles; t += nclusters) {
+      PairSched ps(tiles, KB, nclusters, cid, sk);
+      int t, k0, k1;
+      while (ps.next(t, k0, k1)) {
         int mb, nb;
         tile_coords(t, num_m, num_n, mb, nb);
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
           else mbar_arrive_cluster(&full[stage], 0);
@@ -386,11 +439,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cid; t < tiles; t += nclusters) {
+      PairSched ps(tiles, KB, nclusters, cid, sk);
+      int t, k0, k1;
+      while (ps.next(t, k0, k1)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
@@ -399,9 +454,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
             for (int k = 0; k < GBK / 16; ++k)
               tc_mma_bf16_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
-                               (kb | k) != 0);
+                               (kb > k0 || k > 0));
             tc_commit_pair(&empty[stage], 0x3);
-            if (kb == KB - 1) tc_commit_pair(&tfull[acc], 0x3);
+            if (kb == k1 - 1) tc_commit_pair(&tfull[acc], 0x3);
           }
           __syncwarp();
           if (++stage == P_STAGES) {
@@ -433,9 +488,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       fence_proxy_async_smem();
       __syncwarp();
     };
-    for (int t = cid; t < tiles; t += nclusters) {
+    PairSched ps(tiles, KB, nclusters, cid, sk);
+    int t, k0, k1;
+    while (ps.next(t, k0, k1)) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
+      const uint32_t trow_u = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
+      if (k0 > 0) {
+        // stream-K: the later k-blocks of a tile another pair finishes. Publish the raw
+        // partial (column-major per CTA, so each store is one coalesced 128 B row of lanes).
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        float* wsp = epi.sk_ws + (size_t(cid) * 2 + rank) * 256 * 128 + ew * 32 + lane;
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 32) {
+          tmem_ld32(trow_u + c, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) __stcg(wsp + (c + i) * 128, v[i]);
+        }
+        __threadfence();
+        epi_bar_sync();
+        if (ew == 0 && lane == 0) st_release_u32(epi.sk_flag + cid * 2 + rank, epi.sk_epoch);
+        tc_fence_before();
+        mbar_arrive_cluster(&tempty[acc], 0);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
+      // stream-K: this pair holds the first k-blocks of a tile whose rest pair cid+1 computed
+      const bool fix = k1 < KB;
+      const float* wfix = fix ? epi.sk_ws + (size_t(cid + 1) * 2 + rank) * 256 * 128 + ew * 32 + lane : nullptr;
+      auto fixup = [&](float* vv, int col, int n) {
+#pragma unroll
+        for (int i = 0; i < n; ++i) vv[i] += __ldcg(wfix + (col + i) * 128);
+      };
       if (TK != TK_DIRECT) {
         // per-column epilogue parameters of the tile, loaded once (coalesced) while the
         // accumulator is still being produced; read back as broadcast shared loads
@@ -459,6 +546,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (fix) {
+        if (ew == 0 && lane == 0)
+          while (ld_acquire_u32(epi.sk_flag + (cid + 1) * 2 + rank) != epi.sk_epoch) __nanosleep(64);
+        epi_bar_sync();
+      }
       const int row0 = mb * 256 + rank * 128 + ew * 32;
       const int row = row0 + lane;
       const uint32_t trow = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
@@ -470,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
           for (int q = 0; q < CW; q += 16) tmem_ld16(trow + c + q, v + q);
           tc_wait_ld();
+          if (fix) fixup(v, c, CW);
           if (!epi_skip) epi_apply<CW, OutT>(epi, row, n0, v);
         }
       } else if (TK == TK_STORE_F32 || TK == TK_GRES) {
@@ -479,6 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (n0 >= N) break;
           tmem_ld32(trow + c, v);
           tc_wait_ld();
+          if (fix) fixup(v, c, 32);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             const float4 b4 = *reinterpret_cast<const float4*>(s_bias + c + i);
@@ -522,6 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           tmem_ld32(trow + c, w);
           tmem_ld32(trow + c + 32, w + 32);
           tc_wait_ld();
+          if (fix) fixup(w, c, 64);
           uint8_t* buf = stage_acquire();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -558,6 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             float a[32];
             tmem_ld32(trow + g + 32 * q, a);
             tc_wait_ld();
+            if (fix) fixup(a, g + 32 * q, 32);
             float w[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -611,6 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
               float a[32];
               tmem_ld32(trow + c + q, a);
               tc_wait_ld();
+              if (fix) fixup(a, c + q, 32);
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 const float z = a[i] + s_bias[c + q + i];
@@ -626,6 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             tmem_ld32(trow + c + 64 * hf, w);
             tmem_ld32(trow + c + 64 * hf + 32, w + 32);
             tc_wait_ld();
+            if (fix) fixup(w, c + 64 * hf, 64);
             const float* pb = s_bias + c + 64 * hf;
             const float* pg = s_aux + c + 64 * hf;
 #pragma unroll
@@ -695,15 +793,57 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
     attr_set = true;
   }
   int tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  int pairs = num_sms() / 2;
+  // persistent grid = the CTA pairs that can be co-resident (a GPC with an odd number of
+  // usable SMs strands one SM, so this can be < SMs / 2); stream-K relies on every pair
+  // being resident (a pair may wait for its successor's partial)
+  static const int max_pairs = [&] {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = P_SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / 2;
+    }
+    if (getenv("DF_GEMM_VERBOSE")) fprintf(stderr, "gemm_tc2: %d co-resident CTA pairs\n", n);
+    return n < num_sms() / 2 ? n : num_sms() / 2;
+  }();
+  int pairs = max_pairs;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
+  // stream-K when whole-tile waves would leave > 8 % of the pairs idle on the last wave
+  // (image: 192 tiles on 74 pairs = 2.59 waves -> 86 % busy). Measured slower than the
+  // data-parallel schedule on the image shapes, so opt-in: DF_GEMM_SK=1
+  static const int sk_env = [] {
+    const char* e = getenv("DF_GEMM_SK");
+    return e ? atoi(e) : 0;
+  }();
+  Epi ep = epi;
+  const int waves = (tiles + pairs - 1) / pairs;
+  const bool use_sk = (sk_env || epi.sk_force) && epi.sk_ws && epi.sk_flag && tiles >= pairs && tiles % pairs &&
+                      double(tiles) / (double(waves) * pairs) < 0.92;
+  if (use_sk) {
+    static std::atomic<unsigned> epoch{0};
+    ep.sk_epoch = ++epoch;
+    if (ep.sk_epoch == 0) ep.sk_epoch = ++epoch;  // flags start at 0
+  } else {
+    ep.sk_ws = nullptr;
+    ep.sk_flag = nullptr;
+  }
   static const int skip = [] {  // debug: DF_GEMM_NOEPI=1 drops the epilogue work (timing experiments only)
     const char* e = getenv("DF_GEMM_NOEPI");
     return e ? atoi(e) : 0;
   }();
   int sk = skip;
   void* args[] = {(void*)&ta,     (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2], (void*)&M,
-                  (void*)&N,      (void*)&K,  (void*)&epi,   (void*)&sk};
+                  (void*)&N,      (void*)&K,  (void*)&ep,    (void*)&sk};
   return launch_ex((const void*)kern, dim3(grid), dim3(256), P_SMEM, st, args);
 }
 

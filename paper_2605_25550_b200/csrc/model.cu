@@ -176,6 +176,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
+    else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // stream-K partials + flags
   } else if (stage == DF_E) {
     wsb = al(L * dt * 4) + al(L * dt * ab) + al(L * fe * ab) + al(L * 2 * fe * 4);
   }
@@ -193,7 +194,13 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
     headmod = (float*)ws.take(2 * d * 4);
     rope = (float2*)ws.take(size_t(Fp + Hp + Wp) * dh / 2 * 8 + 64);
-    if (f32()) tmp = (float*)ws.take(N2 * std::max(3 * d, 2 * f) * 4);
+    if (f32()) {
+      tmp = (float*)ws.take(N2 * std::max(3 * d, 2 * f) * 4);
+    } else {
+      sk_ws = (float*)ws.take(size_t(num_sms()) * 128 * 256 * 4);
+      sk_flag = (unsigned*)ws.take(size_t(num_sms()) * 4);
+      DF_TRY(cudaMemset(sk_flag, 0, size_t(num_sms()) * 4));
+    }
     // zero the head-major buffers once: the dh..dhp padding must stay 0 (TMA reads it)
     DF_TRY(cudaMemset(q, 0, 4 * al(hd)));
     // RoPE table in fp64 -> fp32 (R7): (cos, sin)(pos_a * theta^(-2j/D_a))
@@ -316,6 +323,13 @@ cudaError_t Model::gemm(const void* A, int lda, const bf16* Wt, int ldw, int M, 
                         int out_f32, cudaStream_t st) {
   ProfScope ps(prof, st, cur_kind, 2.0 * M * Nn * K, 0.0);
   if (!f32()) {
+    if (sk_ws && !e.sk_ws) {  // offer this instance's stream-K workspace (gemm_tc decides)
+      Epi es = e;
+      es.sk_ws = sk_ws;
+      es.sk_flag = sk_flag;
+      DF_L(gemm_tc(static_cast<const bf16*>(A), lda, Wt, ldw, M, Nn, K, es, out_f32, st));
+      return cudaSuccess;
+    }
     DF_L(gemm_tc(static_cast<const bf16*>(A), lda, Wt, ldw, M, Nn, K, e, out_f32, st));
   } else {
     DF_L(gemm_simt(A, 0, lda, 0, Wt, ldw, tmp, Nn, M, Nn, K, nullptr, ACT_NONE, st));

@@ -122,6 +122,8 @@ struct Model {
   void* a = nullptr;        // [N, f]
   void* X = nullptr;        // [N, P]
   float* tmp = nullptr;     // fp32 build: raw GEMM out [N, max(3d, 2f)]
+  float* sk_ws = nullptr;   // bf16 build: stream-K partial tiles [SMs/2][2][256][128] fp32
+  unsigned* sk_flag = nullptr;  // [SMs] epochs
   float* mods = nullptr;    // [layers][6][d]
   float* headmod = nullptr; // [2][d]
   float2* rope = nullptr;

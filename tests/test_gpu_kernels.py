@@ -62,6 +62,26 @@ def test_gemm_integer_bit_exact(tiny_ctx, tc, M, N, K):
     assert np.array_equal(out.cpu().numpy().astype(np.float64), want)
 
 
+@pytest.mark.parametrize("M,N,K", [(4096, 3072, 320), (2300, 2250, 3072), (2304, 2304, 1000), (4096, 9216, 128)])
+def test_gemm_stream_k_bit_exact(tiny_ctx, M, N, K):
+    """P11 through the stream-K schedule (tiles cut between CTA pairs, partials fixed up in
+    a workspace): integer-valued operands stay bit-exact, ragged M/N/K included; the result
+    is identical to the data-parallel schedule and to a second stream-K run."""
+    A = inputs.int_matrix((M, K), -8, 8, seed=M + K)
+    W = inputs.int_matrix((N, K), -8, 8, seed=N + 3)
+    At = torch.from_numpy(A).cuda().to(torch.bfloat16)
+    Wt = torch.from_numpy(W).cuda().to(torch.bfloat16)
+    want = A.astype(np.float64) @ W.astype(np.float64).T
+    outs = []
+    for tc in (2, 1, 2):
+        out = torch.full((M, N), float("nan"), device="cuda")
+        tiny_ctx.op_gemm(At, Wt, out, tc=tc)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0].astype(np.float64), want)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
 @pytest.mark.parametrize("H,Nq,Nk,dh,dhp", [(2, 300, 260, 128, 128), (3, 128, 128, 64, 64), (4, 16, 16, 16, 64),
                                             (2, 257, 8, 128, 128), (1, 1000, 512, 128, 128)])
 def test_attention_vs_bruteforce(tiny_ctx, H, Nq, Nk, dh, dhp):
@@ -135,9 +155,10 @@ def test_payload_hash_equals_oracle(tiny_ctx, nbytes):
     assert tiny_ctx.payload_hash(0, t, nbytes) == cap.payload_hash(buf)
 
 
-@pytest.mark.parametrize("impl", ["1", "2", "3"])
+@pytest.mark.parametrize("impl", ["1", "2", "3", "5"])
 def test_attention_kernel_variants(impl):
-    """The non-default attention kernels (1: one Q tile per CTA; 2: two Q tiles, one softmax thread per row; 3: CTA pair)
+    """The non-default attention kernels (1: one Q tile per CTA; 2: two Q tiles, one softmax thread per row; 3: CTA pair;
+    5: CTA pair, two softmax threads per row)
     pass the same brute-force and special-case checks; the variant is chosen once per
     process (DF_ATTN_IMPL), so they run in a child pytest."""
     import os

@@ -36,6 +36,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--tc", type=int, default=1, help="2: allow the stream-K schedule")
     a = ap.parse_args()
     g = B.make_graph(TINY, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)])
     with B.Context(g) as c:
@@ -45,12 +46,12 @@ def main():
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
             out = torch.empty(M, N, device="cuda")
-            ms_ours = timeit(lambda: c.op_gemm(A, W, out, tc=1))
+            ms_ours = timeit(lambda: c.op_gemm(A, W, out, tc=a.tc))
             ms_cublas = ms_ours if a.no_cublas else timeit(lambda: torch.matmul(A, W.t()))
             fl = 2.0 * M * N * K
             ref = (A.float() @ W.float().t())
             err = ((out - ref).norm() / ref.norm()).item()
-            print({"shape": name, "M": M, "N": N, "K": K, "ours_tflops": round(fl / ms_ours / 1e9, 1),
+            print({"shape": name, "tc": a.tc, "M": M, "N": N, "K": K, "ours_tflops": round(fl / ms_ours / 1e9, 1),
                    "cublas_tflops": round(fl / ms_cublas / 1e9, 1), "ratio": round(ms_cublas / ms_ours, 3),
                    "rel_err": f"{err:.1e}"}, flush=True)
             del A, W, out, ref
