@@ -1244,6 +1244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
   uint64_t* p_full = s_full + 2;               // [2]    leader: 8 softmax warps x 2 CTAs
   uint64_t* o_done = p_full + 2;               // [2]    both
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* p_q = o_done + 3;                  // [2 tiles][4 key quarters] leader: 4 warps x 2 CTAs
   float* red = reinterpret_cast<float*>(smem + Cfg::OFF_BAR + 256);  // [2 tiles][2 halves][128 rows]
 
   const int warp = warp_id();
@@ -1270,6 +1271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 16);
+      for (int u = 0; u < 4; ++u) mbar_init(&p_q[s * 4 + u], 8);
       mbar_init(&o_done[s], 1);
     }
     fence_mbar_init();
@@ -1333,13 +1335,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
         }
         __syncwarp();
       };
-      auto issue_pv = [&](int t, int j, bool last) {
+      // PV per key quarter (order 0, 2, 1, 3), as in attn_tc3
+      auto issue_pv = [&](int t, int j, int u, bool first) {
         const uint64_t b0 = dv + uint64_t(((j % Cfg::VST) * Cfg::V_BYTES) >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
+          for (int kk = 0; kk < 2; ++kk) {
+            const int k = 2 * u + kk;
             tc_mma_bf16_ts_pair(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, b0 + uint64_t((k * 2048) >> 4),
-                                idesc_pv, (j > 0 || k > 0));
+                                idesc_pv, !(first && kk == 0));
+          }
+        }
+        __syncwarp();
+      };
+      auto pv_tile = [&](int t, int j, bool last) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const int u = (n >> 1) | ((n & 1) << 1);
+          mbar_wait(&p_q[t * 4 + u], j & 1);
+          tc_fence_after();
+          issue_pv(t, j, u, j == 0 && n == 0);
+        }
+        if (elect_one()) {
           if (t == 1) tc_commit_pair(&v_empty[j % Cfg::VST], 0x3);
           if (last) tc_commit_pair(&o_done[t], 0x3);
         }
@@ -1361,16 +1378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       for (int j = 0; j < nkb; ++j) {
         const bool more = j + 1 < nkb;
         mbar_wait(&v_full[j % Cfg::VST], (j / Cfg::VST) & 1);
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        issue_pv(0, j, !more);
+        pv_tile(0, j, !more);
         if (more) {
           wait_k(j + 1);
           issue_qk(0, j + 1);
         }
-        mbar_wait(&p_full[1], j & 1);
-        tc_fence_after();
-        issue_pv(1, j, !more);
+        pv_tile(1, j, !more);
         if (more) {
           issue_qk(1, j + 1);
           commit1(&k_empty[(j + 1) % Cfg::KST]);
@@ -1394,7 +1407,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       if (EXPM == 9) {  // profiling only: tensor cores + synchronisation, no softmax (wrong results)
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&p_full[t], 0);
+        if (lane == 0) {
+          mbar_arrive_cluster(&p_q[t * 4 + 2 * hc], 0);
+          mbar_arrive_cluster(&p_q[t * 4 + 2 * hc + 1], 0);
+        }
         continue;
       }
       float s[64];
@@ -1438,21 +1454,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       float2 lsum2 = make_float2(0.f, 0.f);
       const float2 sc2 = make_float2(scale_log2, scale_log2);
       const float2 nm2 = make_float2(-m_used, -m_used);
+      uint32_t pk[16];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        uint32_t pk[16];
+      for (int i = 0; i < 16; ++i)
+        pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2), i, lsum2);
+      tmem_st16(ts + 32 * hc, pk);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float2 x = ffma2(make_float2(s[32 * q + 2 * i], s[32 * q + 2 * i + 1]), sc2, nm2);
-          pk[i] = softmax_exp2<EXPM>(x, i, lsum2);
-        }
-        tmem_st16(ts + 32 * hc + 16 * q, pk);
-      }
+      for (int i = 0; i < 16; ++i)
+        pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[32 + 2 * i], s[32 + 2 * i + 1]), sc2, nm2), i, lsum2);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&p_q[t * 4 + 2 * hc], 0);  // one arrive per warp, on the leader
+      tmem_st16(ts + 32 * hc + 16, pk);
       l += lsum2.x + lsum2.y;
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&p_full[t], 0);  // one arrive per warp, on the leader
+      if (lane == 0) mbar_arrive_cluster(&p_q[t * 4 + 2 * hc + 1], 0);
     }
     mbar_wait(&o_done[t], 0);
     tc_fence_after();
@@ -1546,7 +1565,7 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
     if (g_attn_impl == 5 && dh == 128) {
       static const int poly = [] {
         const char* e = getenv("DF_ATTN_POLY");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 2;
       }();
       switch (poly) {  // DF_ATTN_POLY: exponential mode (softmax_exp2)
         case 1: return launch_attn_pair3<1>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
@@ -1617,10 +1636,11 @@ cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H,
                     float scale, cudaStream_t st, int heads_per_sample) {
   static const int impl_env = [] {
     // 1: one Q tile per CTA (round-1 kernel); 2: two Q tiles, one softmax thread per row;
-    // 3: CTA pair (cta_group::2); 4 (default): two Q tiles, two softmax threads per row;
-    // 5: CTA pair, two softmax threads per row (4 and 5: dh = 128; other head sizes take 2)
+    // 3: CTA pair (cta_group::2); 4: two Q tiles, two softmax threads per row;
+    // 5 (default): CTA pair, two softmax threads per row (4 and 5: dh = 128; other head
+    // sizes take 2)
     const char* e = getenv("DF_ATTN_IMPL");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 5;
   }();
   g_attn_impl = impl_env;
   const int hs = heads_per_sample > 0 ? heads_per_sample : H;

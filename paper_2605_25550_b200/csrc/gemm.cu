@@ -312,22 +312,37 @@ enum : int { TK_DIRECT = 0, TK_STORE_F32 = 1, TK_STORE_BF16 = 2, TK_GRES = 3, TK
 
 // Work units of one CTA pair.  Data-parallel: whole 256x256 tiles cid, cid + pairs, ...
 // Stream-K (epi.sk_ws set; needs tiles >= pairs): the tiles x KB k-blocks are cut into
-// `pairs` equal contiguous ranges, so every pair gets the same MMA work; a tile cut between
-// pair p (its first k-blocks, the LAST unit of p) and pair p + 1 (the rest, the FIRST unit
-// of p + 1) is finished by p: p + 1 stores its raw partial accumulator in slot p + 1 of the
-// workspace and publishes it with an epoch flag long before p gets there; p adds it to its
-// own accumulator before the epilogue.  One fp32 add of two fixed partials: deterministic.
+// `pairs` equal contiguous ranges, so every pair gets the same MMA work.  A tile cut
+// between pair p (its first k-blocks, the "head") and pair p + 1 (the rest, the "tail") is
+// finished by p + 1.  Each pair runs its partial units FIRST: the head (raw partial to
+// workspace slot p, published with an epoch flag), then the tail (waits for slot p - 1's
+// flag, adds that partial to its own accumulator, normal epilogue), then its whole tiles.
+// The fix-up therefore overlaps the whole-tile mainloops instead of sitting at the end,
+// and it is one fp32 add of two fixed partials: deterministic.
 struct PairSched {
   int tiles, KB, pairs, cid;
   bool sk;
-  long long u, e;  // stream-K cursor / end (k-block units)
   int t;           // data-parallel cursor
+  int n, i;        // stream-K: unit count, cursor
+  int ut[3], u0[3], u1[3];
+  int full0, full1;  // stream-K whole tiles [full0, full1)
   DF_DEV PairSched(int tiles_, int KB_, int pairs_, int cid_, bool sk_)
-      : tiles(tiles_), KB(KB_), pairs(pairs_), cid(cid_), sk(sk_) {
+      : tiles(tiles_), KB(KB_), pairs(pairs_), cid(cid_), sk(sk_), t(cid_), n(0), i(0) {
+    if (!sk) return;
     const long long total = (long long)tiles * KB;
-    u = total * cid / pairs;
-    e = total * (cid + 1) / pairs;
-    t = cid;
+    const long long b = total * cid / pairs, e = total * (cid + 1) / pairs;
+    const int ta = int(b / KB), ka = int(b % KB);  // first tile, offset
+    const int tb = int(e / KB), kb = int(e % KB);  // last tile (exclusive when kb == 0), end offset
+    full0 = ka ? ta + 1 : ta;
+    full1 = tb;
+    if (kb) {  // head: first kb k-blocks of tile tb
+      ut[n] = tb, u0[n] = 0, u1[n] = kb;
+      ++n;
+    }
+    if (ka) {  // tail: k-blocks [ka, KB) of tile ta
+      ut[n] = ta, u0[n] = ka, u1[n] = KB;
+      ++n;
+    }
   }
   // next unit: tile, k-block range [k0, k1)
   DF_DEV bool next(int& tile, int& k0, int& k1) {
@@ -339,12 +354,15 @@ struct PairSched {
       t += pairs;
       return true;
     }
-    if (u >= e) return false;
-    tile = int(u / KB);
-    k0 = int(u - (long long)tile * KB);
-    const long long left = e - u;
-    k1 = left < (long long)(KB - k0) ? k0 + int(left) : KB;
-    u += k1 - k0;
+    if (i < n) {
+      tile = ut[i], k0 = u0[i], k1 = u1[i];
+      ++i;
+      return true;
+    }
+    if (full0 >= full1) return false;
+    tile = full0++;
+    k0 = 0;
+    k1 = KB;
     return true;
   }
 };
@@ -494,8 +512,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const uint32_t trow_u = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
-      if (k0 > 0) {
-        // stream-K: the later k-blocks of a tile another pair finishes. Publish the raw
+      if (k1 < KB) {
+        // stream-K head: the first k-blocks of a tile the next pair finishes. Publish the raw
         // partial (column-major per CTA, so each store is one coalesced 128 B row of lanes).
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -516,9 +534,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (acc == 0) acc_phase ^= 1;
         continue;
       }
-      // stream-K: this pair holds the first k-blocks of a tile whose rest pair cid+1 computed
-      const bool fix = k1 < KB;
-      const float* wfix = fix ? epi.sk_ws + (size_t(cid + 1) * 2 + rank) * 256 * 128 + ew * 32 + lane : nullptr;
+      // stream-K tail: the previous pair published this tile's first k-blocks in its slot
+      const bool fix = k0 > 0;
+      const float* wfix = fix ? epi.sk_ws + (size_t(cid - 1) * 2 + rank) * 256 * 128 + ew * 32 + lane : nullptr;
       auto fixup = [&](float* vv, int col, int n) {
 #pragma unroll
         for (int i = 0; i < n; ++i) vv[i] += __ldcg(wfix + (col + i) * 128);
@@ -548,7 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       if (fix) {
         if (ew == 0 && lane == 0)
-          while (ld_acquire_u32(epi.sk_flag + (cid + 1) * 2 + rank) != epi.sk_epoch) __nanosleep(64);
+          while (ld_acquire_u32(epi.sk_flag + (cid - 1) * 2 + rank) != epi.sk_epoch) __nanosleep(64);
         epi_bar_sync();
       }
       const int row0 = mb * 256 + rank * 128 + ew * 32;
@@ -819,16 +837,19 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
   int pairs = max_pairs;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
   // stream-K when whole-tile waves would leave > 8 % of the pairs idle on the last wave
-  // (image: 192 tiles on 74 pairs = 2.59 waves -> 86 % busy). Measured slower than the
-  // data-parallel schedule on the image shapes, so opt-in: DF_GEMM_SK=1
+  // (image: 192 tiles on 74 pairs = 2.59 waves -> 86 % busy)
   static const int sk_env = [] {
     const char* e = getenv("DF_GEMM_SK");
     return e ? atoi(e) : 0;
   }();
   Epi ep = epi;
   const int waves = (tiles + pairs - 1) / pairs;
-  const bool use_sk = (sk_env || epi.sk_force) && epi.sk_ws && epi.sk_flag && tiles >= pairs && tiles % pairs &&
-                      double(tiles) / (double(waves) * pairs) < 0.92;
+  // measured (image): a gain on the long-K residual GEMM (MLP down, K = 8192),
+  // neutral to negative on K = 3072 and on the two-pass head epilogue -> default on for
+  // EPI_GRES with >= 96 k-blocks only; DF_GEMM_SK=1 takes it wherever the waves are ragged
+  const bool sk_auto = epi.kind == EPI_GRES && (K + GBK - 1) / GBK >= 96;
+  const bool use_sk = (sk_env || epi.sk_force || sk_auto) && epi.sk_ws && epi.sk_flag && tiles >= pairs &&
+                      tiles % pairs && double(tiles) / (double(waves) * pairs) < 0.92;
   if (use_sk) {
     static std::atomic<unsigned> epoch{0};
     ep.sk_epoch = ++epoch;
