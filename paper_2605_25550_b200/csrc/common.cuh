@@ -364,6 +364,7 @@ DF_DEV void tma_reduce_add_2d(const void* desc, const void* src, int x, int y) {
 }
 DF_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 DF_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+DF_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 DF_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // 16-byte chunk j (0..7) of row r in a 128B-swizzled [rows x 128 B] staging tile
 DF_DEV uint8_t* swz128(uint8_t* base, int r, int j) { return base + r * 128 + ((j ^ (r & 7)) << 4); }

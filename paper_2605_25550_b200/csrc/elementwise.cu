@@ -168,10 +168,12 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 }
 
 // One warp per row (d = 128 * VPT): every lane has VPT independent 16-byte loads in flight
-// and the reduction is warp shuffles only. Rows up to 24 float4 per lane stay in registers;
-// wider rows re-read x (an L1 hit) in the second pass.
+// and the reduction is warp shuffles only. The second pass re-reads x (L1 / L2 hits) rather
+// than holding the row in registers: at 24 float4 per lane the kernel needed 148 registers,
+// 3 CTAs (12 warps) per SM, and sat at 2.5 TB/s; without the row in registers every CTA of
+// the grid is resident at once.  Rows of <= 8 float4 per lane stay in registers.
 template <int VPT, typename OutT>
-__global__ void __launch_bounds__(128) rmsnorm_warp_kernel(const float* __restrict__ x, OutT* __restrict__ out, int M,
+__global__ void __launch_bounds__(128, 8) rmsnorm_warp_kernel(const float* __restrict__ x, OutT* __restrict__ out, int M,
                                                            const float* __restrict__ shift,
                                                            const float* __restrict__ scale,
                                                            const bf16* __restrict__ gain, float eps) {
@@ -181,20 +183,31 @@ __global__ void __launch_bounds__(128) rmsnorm_warp_kernel(const float* __restri
   const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (row >= M) return;
   constexpr int d = 128 * VPT;
-  constexpr bool KEEP = VPT <= 24;
+  constexpr bool KEEP = VPT <= 8;
   const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
   float4 v[KEEP ? VPT : 1];
   float ss = 0.f;
+  if constexpr (KEEP) {
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const float4 t = xr[lane + 32 * i];
-    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
-    if constexpr (KEEP) v[i] = t;
+    for (int i = 0; i < VPT; ++i) {
+      v[i] = xr[lane + 32 * i];
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+  } else {
+    // 8 independent 16-byte loads in flight per lane and chunk
+#pragma unroll 1
+    for (int b = 0; b < VPT; b += 8) {
+      float4 t[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = (b + i < VPT) ? xr[lane + 32 * (b + i)] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += t[i].x * t[i].x + t[i].y * t[i].y + t[i].z * t[i].z + t[i].w * t[i].w;
+    }
   }
   ss = warp_sum(ss);
   const float inv = rsqrtf(ss / float(d) + eps);
   OutT* orow = out + size_t(row) * d;
-#pragma unroll
+#pragma unroll 8
   for (int i = 0; i < VPT; ++i) {
     const int c = lane + 32 * i;
     float4 t;

@@ -300,9 +300,15 @@ constexpr int P_A_BYTES = 128 * GBK * 2;
 constexpr int P_B_BYTES = 128 * GBK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_OFF_BAR = P_STAGES * P_STAGE_BYTES;
-constexpr int P_OFF_STG = P_OFF_BAR + 1024;        // 4 epilogue warps x 2 x 4 KB staging tiles
-constexpr int P_OFF_PRM = P_OFF_STG + 4 * 2 * 4096;  // 4 epilogue warps x (256 bias + 256 gate/gain) fp32
-constexpr int P_SMEM = P_OFF_PRM + 4 * 2048 + 1024;
+// Epilogue: 8 warps, two per TMEM lane quarter; warp 4 + 4 h + q drains lanes 32q.. of the
+// accumulator, columns [128 h, 128 h + 128) (one head of the QKV/cross-Q epilogue).  Two warps
+// per SM sub-partition hide each other's TMEM-load / store latencies: with one, the head
+// epilogue (bias, per-head RMSNorm, RoPE) outlasted the K = 3072 mainloop of the next tile.
+constexpr int P_EPI_WARPS = 8;
+constexpr int P_THREADS = 128 + 32 * P_EPI_WARPS;
+constexpr int P_OFF_STG = P_OFF_BAR + 1024;                    // 8 epilogue warps x 4 KB staging tile
+constexpr int P_OFF_PRM = P_OFF_STG + P_EPI_WARPS * 4096;      // 8 warps x (128 bias + 128 gate/gain) fp32
+constexpr int P_SMEM = P_OFF_PRM + P_EPI_WARPS * 1024 + 1024;
 
 // Epilogue variants of the pair kernel (compile-time): TK_DIRECT = per-thread stores via
 // epi_apply; the others stage each warp's 32-row slice in a 128B-swizzled 4 KB shared tile
@@ -375,10 +381,10 @@ DF_DEV unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-DF_DEV void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 epilogue warps
+DF_DEV void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 epilogue warps
 
 template <int CW, typename OutT, int TK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
                     const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const __grid_constant__ Epi epi,
@@ -416,7 +422,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);     // multicast commit
-      mbar_init(&tempty[s], 256);  // 128 epilogue threads of each CTA (leader's copy is used)
+      mbar_init(&tempty[s], 2 * 32 * P_EPI_WARPS);  // epilogue threads of both CTAs (leader's copy is used)
     }
     fence_mbar_init();
   }
@@ -487,20 +493,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
-    uint8_t* stg0 = smem + P_OFF_STG + ew * 8192;
-    float* s_bias = reinterpret_cast<float*>(smem + P_OFF_PRM + ew * 2048);  // this tile's 256 columns
-    float* s_aux = s_bias + 256;  // GRES: gate (1 if none); HEADS: per-head RMSNorm gain
-    int sb = 0;
+    const int ew = warp & 3;              // TMEM lane quarter
+    const int eh = (warp - 4) >> 2;       // column half of the tile
+    const int c_lo = 128 * eh, c_hi = c_lo + 128;
+    uint8_t* stg0 = smem + P_OFF_STG + (warp - 4) * 4096;
+    // this warp's 128 columns; indexed with tile columns c in [c_lo, c_hi)
+    float* s_bias = reinterpret_cast<float*>(smem + P_OFF_PRM + (warp - 4) * 1024) - c_lo;
+    float* s_aux = s_bias + 128;  // GRES: gate (1 if none); HEADS: per-head RMSNorm gain
     int acc = 0;
     uint32_t acc_phase = 0;
     float v[CW];
-    // staging buffer handshake: before refilling buffer sb, the bulk store issued from it two
-    // stores ago must have finished reading shared memory
+    // staging handshake: before refilling the (single) staging tile, the bulk store issued
+    // from it must have finished reading shared memory (the other warp of this SM
+    // sub-partition runs meanwhile)
     auto stage_acquire = [&]() -> uint8_t* {
-      if (lane == 0) bulk_wait_read1();
+      if (lane == 0) bulk_wait_read0();
       __syncwarp();
-      return stg0 + sb * 4096;
+      return stg0;
     };
     auto stage_release = [&]() {
       fence_proxy_async_smem();
@@ -519,7 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         tc_fence_after();
         float* wsp = epi.sk_ws + (size_t(cid) * 2 + rank) * 256 * 128 + ew * 32 + lane;
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 32) {
+        for (int c = c_lo; c < c_hi; c += 32) {
           tmem_ld32(trow_u + c, v);
           tc_wait_ld();
 #pragma unroll
@@ -527,7 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         }
         __threadfence();
         epi_bar_sync();
-        if (ew == 0 && lane == 0) st_release_u32(epi.sk_flag + cid * 2 + rank, epi.sk_epoch);
+        if (warp == 4 && lane == 0) st_release_u32(epi.sk_flag + cid * 2 + rank, epi.sk_epoch);
         tc_fence_before();
         mbar_arrive_cluster(&tempty[acc], 0);
         acc ^= 1;
@@ -546,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         // accumulator is still being produced; read back as broadcast shared loads
         __syncwarp();
 #pragma unroll 1
-        for (int i = lane; i < 256; i += 32) {
+        for (int i = c_lo + lane; i < c_hi; i += 32) {
           const int n = nb * 256 + i;
           const bool ok = n < N;
           s_bias[i] = (ok && epi.bias) ? bf2f(epi.bias[n]) : 0.f;
@@ -565,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (fix) {
-        if (ew == 0 && lane == 0)
+        if (warp == 4 && lane == 0)
           while (ld_acquire_u32(epi.sk_flag + (cid - 1) * 2 + rank) != epi.sk_epoch) __nanosleep(64);
         epi_bar_sync();
       }
@@ -574,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const uint32_t trow = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
       if (TK == TK_DIRECT || epi_skip) {
 #pragma unroll 1
-        for (int c = 0; c < 256; c += CW) {
+        for (int c = c_lo; c < c_hi; c += CW) {
           const int n0 = nb * 256 + c;
           if (n0 >= N) break;
 #pragma unroll
@@ -585,7 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         }
       } else if (TK == TK_STORE_F32 || TK == TK_GRES) {
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 32) {
+        for (int c = c_lo; c < c_hi; c += 32) {
           const int n0 = nb * 256 + c;
           if (n0 >= N) break;
           tmem_ld32(trow + c, v);
@@ -623,11 +632,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             else tma_store_2d(&tmO0, buf, n0, row0);
             bulk_commit();
           }
-          sb ^= 1;
         }
       } else if (TK == TK_STORE_BF16) {
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 64) {
+        for (int c = c_lo; c < c_hi; c += 64) {
           const int n0 = nb * 256 + c;
           if (n0 >= N) break;
           float w[64];
@@ -657,12 +665,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             tma_store_2d(&tmO0, buf, n0, row0);
             bulk_commit();
           }
-          sb ^= 1;
         }
       } else if (TK == TK_SWIGLU) {
         // 128 accumulator columns (4 x (16 W1 | 16 W3)) -> 64 output columns = one 128 B box row
 #pragma unroll 1
-        for (int g = 0; g < 256; g += 128) {
+        for (int g = c_lo; g < c_hi; g += 128) {
           const int n0 = nb * 256 + g;
           if (n0 >= N) break;
           uint8_t* buf = stage_acquire();
@@ -694,7 +701,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             tma_store_2d(&tmO0, buf, n0 / 2, row0);
             bulk_commit();
           }
-          sb ^= 1;
         }
       } else if (TK == TK_HEADS) {
         // one 128-wide head per chunk, two passes over TMEM to bound register pressure:
@@ -710,7 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const int mloc = rowc - bl * mper;
         const RopeRow rrow = rope_row(epi, mloc);  // integer divisions once per row, not per pair
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 128) {
+        for (int c = c_lo; c < c_hi; c += 128) {
           const int n0 = nb * 256 + c;
           if (n0 >= N || row0 >= M) break;
           const int sec = n0 / epi.d;
@@ -781,8 +787,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
               tma_store_3d(map, buf, 64 * hf, row0 - b0 * mper, b0 * epi.heads + hd);
               bulk_commit();
             }
-            sb ^= 1;
-          }
+            }
         }
       }
       tc_fence_before();
@@ -817,7 +822,7 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
   static const int max_pairs = [&] {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms());
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(P_THREADS);
     cfg.dynamicSmemBytes = P_SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -865,7 +870,7 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
   int sk = skip;
   void* args[] = {(void*)&ta,     (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2], (void*)&M,
                   (void*)&N,      (void*)&K,  (void*)&ep,    (void*)&sk};
-  return launch_ex((const void*)kern, dim3(grid), dim3(256), P_SMEM, st, args);
+  return launch_ex((const void*)kern, dim3(grid), dim3(P_THREADS), P_SMEM, st, args);
 }
 
 bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
