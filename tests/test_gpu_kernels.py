@@ -155,10 +155,11 @@ def test_payload_hash_equals_oracle(tiny_ctx, nbytes):
     assert tiny_ctx.payload_hash(0, t, nbytes) == cap.payload_hash(buf)
 
 
-@pytest.mark.parametrize("impl", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("impl", ["1", "2", "3", "4", "5"])
 def test_attention_kernel_variants(impl):
     """The non-default attention kernels (1: one Q tile per CTA; 2: two Q tiles, one softmax thread per row; 3: CTA pair,
-    one softmax thread per row; 4: two Q tiles, two softmax threads per row)
+    one softmax thread per row; 4: two Q tiles, two softmax threads per row; 5: CTA pair, two softmax threads per row,
+    one work item per launch slot)
     pass the same brute-force and special-case checks; the variant is chosen once per
     process (DF_ATTN_IMPL), so they run in a child pytest."""
     import os
