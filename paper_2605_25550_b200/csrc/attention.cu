@@ -1717,12 +1717,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     const uint32_t red_oth = smem_u32(red + (t * 2 + (hc ^ 1)) * 128 + r);
     const uint32_t lred_own = smem_u32(lred + (t * 2 + hc) * 128 + r);
     const uint32_t lred_oth = smem_u32(lred + (t * 2 + (hc ^ 1)) * 128 + r);
-    int g = 0, n = 0;
-    for (int it = cid; it < items; it += npairs, ++n, g += nkb) {
-      const int h = it / nqp, qp = (it - h * nqp) * 512;
+    // one loop-carried counter (n); item and block indices are recomputed from it, which
+    // keeps the 96-register budget of 18 warps free of spills
+    const int my_items = cid < items ? (items - 1 - cid) / npairs + 1 : 0;
+    for (int n = 0; n < my_items; ++n) {
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkb; ++j) {
-        const int jg = g + j;
+        const int jg = n * nkb + j;
         mbar_wait(&s_full[t], jg & 1);
         tc_fence_after();
         float s[64];
@@ -1790,6 +1791,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       sts_f32(lred_own, l);
       named_bar_sync(1 + t, 256);
       const float inv = 1.0f / (l + lds_f32(lred_oth));
+      const int it = cid + n * npairs;
+      const int h = it / nqp, qp = (it - h * nqp) * 512;
       const int q = qp + t * 256 + int(rank) * 128 + r;
       const int hb = h / Hs, hl = h - hb * Hs;
       bf16* orow = O + (size_t(hb) * Nq + q) * Hs * dh_real + size_t(hl) * dh_real + 64 * hc;

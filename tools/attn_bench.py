@@ -55,7 +55,7 @@ def main():
         err = ((got - ref).norm() / ref.norm()).item()
         fl = 4.0 * H * Nq * Nk * dh
         best = min(ms)
-        print({"shape": a.shape, "impl": os.environ.get("DF_ATTN_IMPL", "2"), "poly": os.environ.get("DF_ATTN_POLY", "0"),
+        print({"shape": a.shape, "impl": os.environ.get("DF_ATTN_IMPL", "default"), "poly": os.environ.get("DF_ATTN_POLY", "default"),
                "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
                "rel_l2_vs_torch": f"{err:.2e}"})
         if a.lib:  # library reference point (not on the product path)
