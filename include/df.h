@@ -62,6 +62,10 @@ typedef struct {
   uint32_t vocab, enc_ffn, dec_width; /* E / D stand-ins (R17)                          */
   float eps, rope_theta;
   uint32_t rope_axes[3];        /* (D_f, D_h, D_w), sum = d/heads                        */
+  /* image-to-video conditioning (NEXT-3; R27): C_y > 0 makes the patch embedding
+   * read concat(x, y) (y [C_y, F, H, W] fp32: first-frame mask + VAE latent) and adds a
+   * cross-attention over L_img image tokens of width d_img per block; 0 = text only. */
+  uint32_t C_y, L_img, d_img;
 } df_dit_cfg;
 
 /* Stage graph: the fixed chain E -> T -> D with an E:T:D instance ratio. */
@@ -152,6 +156,15 @@ df_status df_dit_prepare_cfg(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, c
                              float guidance, const float* sigmas, uint32_t S, void* stream, df_cond** out);
 df_status df_dit_prepare(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const float* sigmas, uint32_t S,
                          void* stream, df_cond** out);
+/* Image-to-video prologue (NEXT-3; "Encoder produces latent tensors"):
+ * for a graph with dit.C_y > 0.  clip_dev: device bf16 [L_img, d_img] image tokens; y_dev:
+ * device fp32 [C_y, F, H, W] (first-frame mask + VAE latent), copied into the conditioning
+ * (the caller may reuse it once the stream passes).  ctx_neg_dev (optional) adds classifier-
+ * free guidance as in df_dit_prepare_cfg.  DF_ERR_INVALID for a text-only graph;
+ * df_dit_prepare refuses an I2V graph (it has no image inputs). */
+df_status df_dit_prepare_i2v(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const void* clip_dev,
+                             const float* y_dev, const void* ctx_neg_dev, float guidance, const float* sigmas,
+                             uint32_t S, void* stream, df_cond** out);
 /* One denoising step i (a2-a12): x_dev fp32 [C,F,H,W] updated in place,
  * x <- x + (sigma_{i+1} - sigma_i) v; v_dev (optional, fp32 [C,F,H,W]) gets v. */
 df_status df_dit_step(df_ctx* ctx, int32_t t_inst, const df_cond* c, uint32_t i, float* x_dev, float* v_dev,

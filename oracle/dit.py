@@ -77,10 +77,11 @@ def sinusoid(t: float, freq_dim: int = 256) -> np.ndarray:
 # ---------------------------------------------------------------- geometry
 def patchify(x: np.ndarray, cfg) -> np.ndarray:
     """X[n,p] = x[c, f*pt+i, hh*ph+j, ww*pw+k]; n = (f*Hp+hh)*Wp+ww,
-    p = ((c*pt+i)*ph+j)*pw+k  (Conv3d flatten order, R11)."""
-    C, pt, ph, pw = cfg.C, cfg.pt, cfg.ph, cfg.pw
+    p = ((c*pt+i)*ph+j)*pw+k  (Conv3d flatten order, R11).  The channel count is x's
+    (C for the latent, C + C_y for the I2V input concat(x, y))."""
+    C, pt, ph, pw = x.shape[0], cfg.pt, cfg.ph, cfg.pw
     Fp, Hp, Wp = cfg.Fp, cfg.Hp, cfg.Wp
-    X = np.empty((cfg.N, cfg.P), dtype=np.float64)
+    X = np.empty((cfg.N, C * pt * ph * pw), dtype=np.float64)
     for f in range(Fp):
         for hh in range(Hp):
             for ww in range(Wp):
@@ -160,13 +161,32 @@ def cross_kv(P, cfg, l: int, ctxp: np.ndarray):
     return k, v
 
 
-def prologue(P, cfg, ctx: np.ndarray, sig: np.ndarray):
+def image_projection(P, cfg, clip: np.ndarray) -> np.ndarray:
+    """I2V (NEXT-3, reading R27): img' = GELU_tanh(clip W_i1 + b_i1) W_i2 + b_i2 -> [L_img, d]
+    (the text projection's form; Wan's MLPProj adds LayerNorms)."""
+    return gelu_tanh(clip @ P["img1_w"] + P["img1_b"]) @ P["img2_w"] + P["img2_b"]
+
+
+def image_kv(P, cfg, l: int, imgp: np.ndarray):
+    """Ki_l = headRMS(img' W_ki + b_ki) * g_ki;  Vi_l = img' W_vi + b_vi  (as cross_kv)."""
+    k = head_rms_norm(imgp @ P.layer(l, "ki_w") + P.layer(l, "ki_b"), cfg.heads, cfg.eps) * P.layer(l, "g_ki")
+    v = imgp @ P.layer(l, "vi_w") + P.layer(l, "vi_b")
+    return k, v
+
+
+def prologue(P, cfg, ctx: np.ndarray, sig: np.ndarray, clip=None, y=None):
     """Per-request conditioning: cross K/V for every layer and
-    (e_i, e6_i) for every step i < S."""
+    (e_i, e6_i) for every step i < S.  I2V (cfg.C_y > 0): also the image-token K/V of
+    every layer from clip [L_img, d_img], and y [C_y, F, H, W] for the patch embedding."""
     ctxp = text_projection(P, cfg, ctx)
     kv = [cross_kv(P, cfg, l, ctxp) for l in range(cfg.layers)]
     te = [time_embedding(P, cfg, float(sig[i])) for i in range(len(sig) - 1)]
-    return {"ctxp": ctxp, "kv": kv, "e": [t[0] for t in te], "e6": [t[1] for t in te]}
+    cond = {"ctxp": ctxp, "kv": kv, "e": [t[0] for t in te], "e6": [t[1] for t in te], "kvi": None, "y": None}
+    if cfg.i2v:
+        imgp = image_projection(P, cfg, np.asarray(clip, dtype=np.float64))
+        cond["kvi"] = [image_kv(P, cfg, l, imgp) for l in range(cfg.layers)]
+        cond["y"] = np.asarray(y, dtype=np.float64)
+    return cond
 
 
 def _heads(z: np.ndarray, H: int) -> np.ndarray:
@@ -181,9 +201,10 @@ def _unheads(z: np.ndarray) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- one block
-def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = True) -> np.ndarray:
+def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = True, kvi=None) -> np.ndarray:
     """One DiT block (Wan2.1 order, R1): adaLN self-attention, cross-attention,
-    adaLN gated MLP.  r [N, d] fp64 -> r' [N, d]."""
+    adaLN gated MLP.  r [N, d] fp64 -> r' [N, d].  I2V: the cross-attention output is the
+    text term plus the image-token term softmax(qc Ki^T / sqrt(dh)) Vi (Wan I2V, R27)."""
     d, H, eps = cfg.d, cfg.heads, cfg.eps
     sh1, sc1, g1, sh2, sc2, g2 = (e6 + P.layer(l, "mod"))  # rows 0..5 (R4)
     # --- self-attention (a4-a7)
@@ -202,6 +223,8 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
         qc = head_rms_norm(hc @ P.layer(l, "cq_w") + P.layer(l, "cq_b"), H, eps) * P.layer(l, "g_cq")
         kc, vc = kv
         oc = softmax_attention(_heads(qc, H), _heads(kc, H), _heads(vc, H))
+        if kvi is not None:
+            oc = oc + softmax_attention(_heads(qc, H), _heads(kvi[0], H), _heads(kvi[1], H))
         r = r + (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))
     # --- gated MLP (a9-a10): SwiGLU with biases (R9)
     h2 = rms_norm(r, eps) * (1.0 + sc2) + sh2
@@ -210,7 +233,7 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
     return r
 
 
-def block_rows(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, rows) -> np.ndarray:
+def block_rows(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, rows, kvi=None) -> np.ndarray:
     """block() evaluated only at output rows `rows` (production-shape parity).
     Same definition: self-attention keys/values use ALL tokens; every other
     operation is row-wise, so restricting the query rows changes nothing."""
@@ -231,6 +254,8 @@ def block_rows(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, rows) -> 
     qc = head_rms_norm(hc @ P.layer(l, "cq_w") + P.layer(l, "cq_b"), H, eps) * P.layer(l, "g_cq")
     kc, vc = kv
     oc = softmax_attention(_heads(qc, H), _heads(kc, H), _heads(vc, H))
+    if kvi is not None:
+        oc = oc + softmax_attention(_heads(qc, H), _heads(kvi[0], H), _heads(kvi[1], H))
     rr = rr + (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))
     h2 = rms_norm(rr, eps) * (1.0 + sc2) + sh2
     a = silu(h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * (h2 @ P.layer(l, "w3") + P.layer(l, "b3"))
@@ -248,11 +273,16 @@ def head(P, cfg, r: np.ndarray, e: np.ndarray) -> np.ndarray:
 def velocity(P, cfg, x: np.ndarray, i: int, cond, cross: bool = True, trace=None) -> np.ndarray:
     """v(x_i, sigma_i): patch embed -> blocks -> head (a2-a11)."""
     pos = token_positions(cfg)
-    r = patchify(np.asarray(x, dtype=np.float64), cfg) @ P["patch_w"] + P["patch_b"]
+    xin = np.asarray(x, dtype=np.float64)
+    if cfg.i2v:  # concat(x, y) along channels before patchify (Wan I2V in_dim = C + C_y)
+        xin = np.concatenate([xin, cond["y"]], axis=0)
+    r = patchify(xin, cfg) @ P["patch_w"] + P["patch_b"]
     if trace is not None:
         trace.append(r.copy())
+    kvi = cond.get("kvi")
     for l in range(cfg.layers):
-        r = block(P, cfg, l, r, cond["e6"][i], cond["kv"][l], pos, cross=cross)
+        r = block(P, cfg, l, r, cond["e6"][i], cond["kv"][l], pos, cross=cross,
+                  kvi=kvi[l] if kvi is not None else None)
         if trace is not None:
             trace.append(r.copy())
     return head(P, cfg, r, cond["e"][i])
@@ -273,13 +303,13 @@ def step(P, cfg, x, i, cond, sig):
     return euler_update(np.asarray(x, dtype=np.float64), v, sig[i], sig[i + 1]), v
 
 
-def trajectory(P, cfg, x0, ctx, steps=None, shift=None, ctx_neg=None, guidance: float = 1.0):
+def trajectory(P, cfg, x0, ctx, steps=None, shift=None, ctx_neg=None, guidance: float = 1.0, clip=None, y=None):
     """x_S from x_0 and the bf16 ctx payload (values as fp64); with ctx_neg, classifier-free
-    guidance with scale `guidance`."""
+    guidance with scale `guidance`; I2V configs also take clip and y."""
     S = cfg.steps if steps is None else steps
     sig = sigmas(S, cfg.shift if shift is None else shift)
-    cond = prologue(P, cfg, ctx, sig)
-    cond_neg = prologue(P, cfg, ctx_neg, sig) if ctx_neg is not None else None
+    cond = prologue(P, cfg, ctx, sig, clip=clip, y=y)
+    cond_neg = prologue(P, cfg, ctx_neg, sig, clip=clip, y=y) if ctx_neg is not None else None
     x = np.asarray(x0, dtype=np.float64)
     for i in range(S):
         if cond_neg is None:

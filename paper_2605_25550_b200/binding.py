@@ -27,7 +27,8 @@ class DitCfgC(C.Structure):
                 ("d", C.c_uint32), ("heads", C.c_uint32), ("ffn", C.c_uint32), ("layers", C.c_uint32),
                 ("d_txt", C.c_uint32), ("L_txt", C.c_uint32), ("freq_dim", C.c_uint32),
                 ("vocab", C.c_uint32), ("enc_ffn", C.c_uint32), ("dec_width", C.c_uint32),
-                ("eps", C.c_float), ("rope_theta", C.c_float), ("rope_axes", C.c_uint32 * 3)]
+                ("eps", C.c_float), ("rope_theta", C.c_float), ("rope_axes", C.c_uint32 * 3),
+                ("C_y", C.c_uint32), ("L_img", C.c_uint32), ("d_img", C.c_uint32)]
 
 
 class InstC(C.Structure):
@@ -95,6 +96,8 @@ _SIGS = {
                                  C.POINTER(C.c_void_p)]),
     "df_dit_prepare_cfg": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_float, C.POINTER(C.c_float),
                                      C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "df_dit_prepare_i2v": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float,
+                                     C.POINTER(C.c_float), C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "df_dit_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_dit_layer": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "df_cond_release": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -157,7 +160,7 @@ def dit_cfg_c(cfg) -> DitCfgC:
     """synth.configs.DitCfg -> df_dit_cfg."""
     c = DitCfgC()
     for k in ("C", "F", "H", "W", "pt", "ph", "pw", "d", "heads", "ffn", "layers", "d_txt", "L_txt", "freq_dim",
-              "vocab", "dec_width"):
+              "vocab", "dec_width", "C_y", "L_img", "d_img"):
         setattr(c, k, int(getattr(cfg, k)))
     c.enc_ffn = int(cfg.f_e)
     c.eps = float(cfg.eps)
@@ -311,6 +314,14 @@ class Context:
         out = C.c_void_p()
         self._ck(self.lib.df_dit_prepare_cfg(self.h, t_inst, _ptr(ctx_dev), _ptr(ctx_neg_dev), float(guidance), sig,
                                              len(sigmas) - 1, _stream(stream), C.byref(out)))
+        return out
+
+    def dit_prepare_i2v(self, t_inst, ctx_dev, clip_dev, y_dev, sigmas, ctx_neg_dev=None, guidance=1.0, stream=None):
+        sig = (C.c_float * len(sigmas))(*[float(s) for s in sigmas])
+        out = C.c_void_p()
+        self._ck(self.lib.df_dit_prepare_i2v(self.h, t_inst, _ptr(ctx_dev), _ptr(clip_dev), _ptr(y_dev),
+                                             _ptr(ctx_neg_dev), float(guidance), sig, len(sigmas) - 1,
+                                             _stream(stream), C.byref(out)))
         return out
 
     def dit_step(self, t_inst, cond, i, x_dev, v_dev=None, stream=None):

@@ -37,6 +37,8 @@ DF_DEV float gelu_tanh_f(float z) {
 template <typename T> DF_DEV void store_val(T* p, float v);
 template <> DF_DEV void store_val<float>(float* p, float v) { *p = v; }
 template <> DF_DEV void store_val<bf16>(bf16* p, float v) { *p = __float2bfloat16_rn(v); }
+DF_DEV float load_val(const float* p) { return *p; }
+DF_DEV float load_val(const bf16* p) { return __bfloat162float(*p); }
 
 // ------------------------------------------------------------------ smem / mbarrier
 DF_DEV uint32_t smem_u32(const void* p) {

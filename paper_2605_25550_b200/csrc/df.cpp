@@ -1682,6 +1682,26 @@ df_status df_dit_prepare_cfg(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, c
   return DF_OK;
 }
 
+df_status df_dit_prepare_i2v(df_ctx* ctx, int32_t t_inst, const void* ctx_dev, const void* clip_dev,
+                             const float* y_dev, const void* ctx_neg_dev, float guidance, const float* sigmas,
+                             uint32_t S, void* stream, df_cond** out) {
+  Inst* I = get_inst(ctx, t_inst, DF_T);
+  if (!I || !ctx_dev || !clip_dev || !y_dev || !sigmas || !S || !out || !I->m.i2v())
+    return fail(ctx, "df_dit_prepare_i2v: invalid", DF_ERR_INVALID);
+  if (ctx->failed) return DF_ERR_STATE;
+  auto c = new df_cond();
+  c->inst = t_inst;
+  cudaError_t e = I->m.prepare(ctx_dev, sigmas, int(S), (cudaStream_t)stream, &c->c, ctx_neg_dev,
+                               ctx_neg_dev ? guidance : 1.f, clip_dev, y_dev);
+  if (e != cudaSuccess) {
+    c->c.mem.release();
+    delete c;
+    return fail(ctx, std::string("df_dit_prepare_i2v: ") + cudaGetErrorString(e) + " " + df::tls_err);
+  }
+  *out = c;
+  return DF_OK;
+}
+
 df_status df_dit_step(df_ctx* ctx, int32_t t_inst, const df_cond* c, uint32_t i, float* x_dev, float* v_dev,
                       void* stream) {
   Inst* I = get_inst(ctx, t_inst, DF_T);

@@ -262,10 +262,11 @@ cudaError_t rmsnorm_mod(const float* x, void* out, int out_f32, int M, int d, co
 }
 
 // ------------------------------------------------------------------ patchify
+// I2V: channels c >= C come from y (concat(x, y) along channels, Wan's in_dim = C + C_y)
 template <typename OutT>
-__global__ void patchify_kernel(const float* __restrict__ x, OutT* __restrict__ X, int C, int F, int H, int W, int pt,
-                                int ph, int pw, size_t total) {
-  const int P = C * pt * ph * pw;
+__global__ void patchify_kernel(const float* __restrict__ x, const float* __restrict__ y, int Cy, OutT* __restrict__ X,
+                                int C, int F, int H, int W, int pt, int ph, int pw, size_t total) {
+  const int P = (C + Cy) * pt * ph * pw;
   const int Hp = H / ph, Wp = W / pw;
   for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
     int p = int(t % P);
@@ -276,17 +277,37 @@ __global__ void patchify_kernel(const float* __restrict__ x, OutT* __restrict__ 
     r /= ph;
     int i = r % pt;
     int c = r / pt;
-    float v = x[((size_t(c) * F + f * pt + i) * H + hh * ph + j) * W + ww * pw + k];
+    const size_t sp = (size_t(f * pt + i) * H + hh * ph + j) * W + ww * pw + k;
+    const float v = c < C ? x[size_t(c) * F * H * W + sp] : y[size_t(c - C) * F * H * W + sp];
     store_val<OutT>(X + t, v);
   }
 }
-cudaError_t patchify(const float* x, void* X, int out_f32, int C, int F, int H, int W, int pt, int ph, int pw,
-                     cudaStream_t st) {
-  size_t total = size_t(C) * F * H * W;
+cudaError_t patchify(const float* x, const float* y, int Cy, void* X, int out_f32, int C, int F, int H, int W, int pt,
+                     int ph, int pw, cudaStream_t st) {
+  if (Cy > 0 && !y) return cudaErrorInvalidValue;
+  size_t total = size_t(C + (Cy > 0 ? Cy : 0)) * F * H * W;
+  const int cy = Cy > 0 ? Cy : 0;
   unsigned blocks = unsigned((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  if (out_f32) patchify_kernel<float><<<blocks, 256, 0, st>>>(x, (float*)X, C, F, H, W, pt, ph, pw, total);
-  else patchify_kernel<bf16><<<blocks, 256, 0, st>>>(x, (bf16*)X, C, F, H, W, pt, ph, pw, total);
+  if (out_f32) patchify_kernel<float><<<blocks, 256, 0, st>>>(x, y, cy, (float*)X, C, F, H, W, pt, ph, pw, total);
+  else patchify_kernel<bf16><<<blocks, 256, 0, st>>>(x, y, cy, (bf16*)X, C, F, H, W, pt, ph, pw, total);
+  return cudaGetLastError();
+}
+
+// o += oi elementwise (I2V: text + image cross-attention outputs), in the activation dtype
+template <typename T>
+__global__ void add_into_kernel(T* __restrict__ o, const T* __restrict__ oi, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float v = load_val(o + i) + load_val(oi + i);
+    store_val<T>(o + i, v);
+  }
+}
+cudaError_t add_into(void* o, const void* oi, size_t n, int f32, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  unsigned blocks = unsigned((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (f32) add_into_kernel<float><<<blocks, 256, 0, st>>>((float*)o, (const float*)oi, n);
+  else add_into_kernel<bf16><<<blocks, 256, 0, st>>>((bf16*)o, (const bf16*)oi, n);
   return cudaGetLastError();
 }
 

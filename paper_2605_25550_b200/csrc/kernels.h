@@ -41,9 +41,11 @@ cudaError_t cfg_euler(float* x, const float* v_batch, float* v_out, size_t n, fl
 //           = RMSNorm(x[m, :]) * gain                     (mode 1; gain bf16 [d])
 cudaError_t rmsnorm_mod(const float* x, void* out, int out_f32, int M, int d, const float* shift, const float* scale,
                         const bf16* gain, float eps, cudaStream_t st);
-// X[n, p] = patchify(x)   (bf16 or fp32 out)
-cudaError_t patchify(const float* x, void* X, int out_f32, int C, int F, int H, int W, int pt, int ph, int pw,
-                     cudaStream_t st);
+// X[n, p] = patchify(concat(x, y))   (bf16 or fp32 out; y [Cy, F, H, W] only for I2V, Cy = 0 otherwise)
+cudaError_t patchify(const float* x, const float* y, int Cy, void* X, int out_f32, int C, int F, int H, int W, int pt,
+                     int ph, int pw, cudaStream_t st);
+// o += oi (bf16 or fp32, n elements)
+cudaError_t add_into(void* o, const void* oi, size_t n, int f32, cudaStream_t st);
 // sinusoid rows s[i, :] = [cos(1000 sig_i w) | sin(1000 sig_i w)], i < S
 cudaError_t sinusoid(const float* sig_dev, float* s, int S, int freq_dim, cudaStream_t st);
 // mods[l][k][:] = e6[k][:] + M_l[k][:] for k < 6, all layers; head[0..1][:] = head_mod + e

@@ -120,22 +120,27 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
   Wp = c.W / c.pw;
   N = Fp * Hp * Wp;
   P = c.C * c.pt * c.ph * c.pw;
+  Pin = (c.C + c.C_y) * c.pt * c.ph * c.pw;
   dh = c.d / c.heads;
   dhp = f32() ? dh : (dh <= 64 ? 64 : 128);
   if (c.d % c.heads || dh > 128 || c.ffn % 16 || c.d % 4 || c.enc_ffn % 16 ||
-      c.rope_axes[0] + c.rope_axes[1] + c.rope_axes[2] != uint32_t(dh))
+      c.rope_axes[0] + c.rope_axes[1] + c.rope_axes[2] != uint32_t(dh) ||
+      (c.C_y > 0 && (c.L_img == 0 || c.d_img == 0 || c.d_img % 8)))
     return cudaErrorInvalidValue;
   const size_t d = c.d, f = c.ffn, L = c.L_txt, dt = c.d_txt, fe = c.enc_ffn, ab = act_bytes();
   // ---- weights
   size_t wb = 0;
   if (stage == DF_T) {
-    wb += al(d * P * 2) + al(d * 2) + al(d * dt * 2) + al(d * 2) + al(d * d * 2) + al(d * 2) + al(d * c.freq_dim * 2) +
+    wb += al(d * Pin * 2) + al(d * 2) + al(d * dt * 2) + al(d * 2) + al(d * d * 2) + al(d * 2) + al(d * c.freq_dim * 2) +
           al(d * 2) + al(d * d * 2) + al(d * 2) + al(6 * d * d * 2) + al(6 * d * 2) + al(2 * d * 2) + al(P * d * 2) +
           al(P * 2);
     size_t per = al(6 * d * 2) + al(3 * d * d * 2) + al(3 * d * 2) + 3 * al(d * 2) + al(d * d * 2) + al(d * 2) +
                  al(d * d * 2) + al(d * 2) + al(2 * d * d * 2) + al(2 * d * 2) + 2 * al(d * 2) + al(d * d * 2) +
                  al(d * 2) + al(2 * f * d * 2) + al(2 * f * 2) + al(d * f * 2) + al(d * 2);
     wb += per * c.layers;
+    if (i2v())  // image projection + per layer image-token K | V and K gain
+      wb += al(d * c.d_img * 2) + al(d * 2) + al(d * d * 2) + al(d * 2) +
+            size_t(c.layers) * (al(2 * d * d * 2) + al(2 * d * 2) + al(d * 2));
   } else if (stage == DF_E) {
     wb += al(size_t(c.vocab) * dt * 2) + 2 * al(dt * 2) + al(2 * fe * dt * 2) + al(dt * fe * 2);
   } else {
@@ -145,7 +150,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
   DF_TRY(wmem.reserve(wb + 4096));
   auto W = [&](size_t n) { return static_cast<bf16*>(wmem.take(n * 2)); };
   if (stage == DF_T) {
-    patch_wT = W(d * P); patch_b = W(d);
+    patch_wT = W(d * Pin); patch_b = W(d);
     txt1_wT = W(d * dt); txt1_b = W(d); txt2_wT = W(d * d); txt2_b = W(d);
     temb1_wT = W(d * c.freq_dim); temb1_b = W(d); temb2_wT = W(d * d); temb2_b = W(d);
     tmod_wT = W(6 * d * d); tmod_b = W(6 * d); head_mod = W(2 * d); head_wT = W(P * d); head_b = W(P);
@@ -155,6 +160,12 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
       l.o_wT = W(d * d); l.o_b = W(d); l.g_n3 = W(d); l.cq_wT = W(d * d); l.cq_b = W(d);
       l.ckv_wT = W(2 * d * d); l.ckv_b = W(2 * d); l.g_cq = W(d); l.g_ck = W(d); l.co_wT = W(d * d); l.co_b = W(d);
       l.w13T = W(2 * f * d); l.b13 = W(2 * f); l.w2T = W(d * f); l.b2 = W(d);
+    }
+    if (i2v()) {
+      img1_wT = W(d * c.d_img); img1_b = W(d); img2_wT = W(d * d); img2_b = W(d);
+      for (auto& l : Lw) {
+        l.ckvi_wT = W(2 * d * d); l.ckvi_b = W(2 * d); l.g_ki = W(d);
+      }
     }
     layer_mods.clear();
     for (auto& l : Lw) layer_mods.push_back(l.mod);
@@ -172,7 +183,8 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     // activations sized for a batch of 2 (classifier-free guidance stacks cond + negative)
     const size_t N2 = 2 * Nn;
     size_t hd = size_t(c.heads) * N2 * dhp * ab;
-    wsb = al(N2 * d * 4) + al(N2 * d * ab) + 4 * al(hd) + al(N2 * d * ab) + al(N2 * f * ab) + al(Nn * P * ab) +
+    wsb = al(N2 * d * 4) + al(N2 * d * ab) + 4 * al(hd) + al(N2 * d * ab) + al(N2 * f * ab) + al(Nn * Pin * ab) +
+          (i2v() ? al(N2 * d * ab) : 0) +
           al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
@@ -189,7 +201,8 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     q = ws.take(hd); k = ws.take(hd); v = ws.take(hd); qc = ws.take(hd);
     o = ws.take(N2 * d * ab);
     a = ws.take(N2 * f * ab);
-    X = ws.take(Nn * P * ab);
+    X = ws.take(Nn * Pin * ab);
+    if (i2v()) oi = ws.take(N2 * d * ab);
     vbatch = (float*)ws.take(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
     headmod = (float*)ws.take(2 * d * 4);
@@ -256,7 +269,7 @@ cudaError_t Model::init_weights(cudaStream_t st) {
   auto vec = [&](bf16* dst, uint32_t tid, double sd, int n) { return go(dst, tid, 0, sd, 1, n, 0, n, 0); };
   auto gain = [&](bf16* dst, uint32_t tid, int n) { return go(dst, tid, 1, 0.1, 1, n, 0, n, 0); };
   if (stage == DF_T) {
-    DF_TRY(lin(patch_wT, T_PATCH_W, P, d));
+    DF_TRY(lin(patch_wT, T_PATCH_W, Pin, d));
     DF_TRY(vec(patch_b, T_PATCH_B, 0.02, d));
     DF_TRY(lin(txt1_wT, T_TXT1_W, dt, d));
     DF_TRY(vec(txt1_b, T_TXT1_B, 0.02, d));
@@ -271,6 +284,12 @@ cudaError_t Model::init_weights(cudaStream_t st) {
     DF_TRY(go(head_mod, T_HEAD_MOD, 0, 0.1, 2, d, 0, d, 0));
     DF_TRY(lin(head_wT, T_HEAD_W, d, P));
     DF_TRY(vec(head_b, T_HEAD_B, 0.02, P));
+    if (i2v()) {
+      DF_TRY(lin(img1_wT, T_IMG1_W, c.d_img, d));
+      DF_TRY(vec(img1_b, T_IMG1_B, 0.02, d));
+      DF_TRY(lin(img2_wT, T_IMG2_W, d, d));
+      DF_TRY(vec(img2_b, T_IMG2_B, 0.02, d));
+    }
     for (int l = 0; l < c.layers; ++l) {
       const uint32_t b = T_LAYER_BASE + T_LAYER_STRIDE * l;
       LayerW& w = Lw[l];
@@ -298,6 +317,13 @@ cudaError_t Model::init_weights(cudaStream_t st) {
       DF_TRY(go(w.b13, b + L_B3, 0, 0.02, 1, f, 2, 1, 1));
       DF_TRY(lin(w.w2T, b + L_W2, f, d));
       DF_TRY(vec(w.b2, b + L_B2, 0.02, d));
+      if (i2v()) {  // image-token K | V stacked like the text K | V, K gain
+        DF_TRY(go(w.ckvi_wT, b + L_KI_W, 0, 1.0 / std::sqrt(double(d)), d, d, 1, d, 0));
+        DF_TRY(vec(w.ckvi_b, b + L_KI_B, 0.02, d));
+        DF_TRY(go(w.ckvi_wT, b + L_VI_W, 0, 1.0 / std::sqrt(double(d)), d, d, 1, d, d));
+        DF_TRY(vec(w.ckvi_b + d, b + L_VI_B, 0.02, d));
+        DF_TRY(gain(w.g_ki, b + L_G_KI, d));
+      }
     }
   } else if (stage == DF_E) {
     DF_TRY(go(emb, T_ENC_BASE + E_EMB, 0, 1.0, c.vocab, dt, 0, dt, 0));
@@ -389,8 +415,10 @@ cudaError_t Model::norm(const float* x, void* out, int M, int dd, const float* s
 
 // ------------------------------------------------------------------ prologue (a1)
 cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
-                           const void* ctx_neg_bf16, float guidance) {
+                           const void* ctx_neg_bf16, float guidance, const void* clip_bf16, const float* y_in) {
   const int d = c.d, Lt = c.L_txt, dt = c.d_txt, fd = c.freq_dim;
+  const int Li = int(c.L_img), di = int(c.d_img);
+  if (i2v() != (clip_bf16 != nullptr && y_in != nullptr)) return cudaErrorInvalidValue;  // I2V needs both
   const size_t ab = act_bytes();
   Cond& cd = *out;
   cd.S = S;
@@ -399,9 +427,12 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   cd.guidance = guidance;
   cd.sig.assign(sig_host, sig_host + S + 1);
   size_t kvb = size_t(c.layers) * cd.B * c.heads * Lt * dhp * ab;
+  const size_t kvbi = size_t(c.layers) * cd.B * c.heads * Li * dhp * ab;         // I2V image-token K (V)
+  const size_t yel = size_t(c.C_y) * c.F * c.H * c.W;
+  const int Lmax = Lt > Li ? Lt : Li;
   size_t need = al((S + 1) * 4) + 2 * al(kvb) + al(size_t(S) * d * 4) + al(size_t(S) * 6 * d * 4) +
-                al(size_t(S) * fd * 4) + al(size_t(S) * d * 4) + 2 * al(size_t(Lt) * d * ab) +
-                (f32() ? al(size_t(Lt) * 2 * d * 4) : 0) + 4096;
+                al(size_t(S) * fd * 4) + al(size_t(S) * d * 4) + 2 * al(size_t(Lmax) * d * ab) +
+                (f32() ? al(size_t(Lmax) * 2 * d * 4) : 0) + (i2v() ? 2 * al(kvbi) + al(yel * 4) : 0) + 4096;
   if (cd.mem.base && cd.mem.cap >= need) {
     cd.mem.used = 0;  // persistent cache of a T worker: reused in stream order
   } else {
@@ -415,11 +446,22 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   cd.e6 = (float*)cd.mem.take(size_t(S) * 6 * d * 4);
   float* s = (float*)cd.mem.take(size_t(S) * fd * 4);
   float* t1 = (float*)cd.mem.take(size_t(S) * d * 4);
-  void* c1 = cd.mem.take(size_t(Lt) * d * ab);
-  void* cp = cd.mem.take(size_t(Lt) * d * ab);
-  float* ptmp = f32() ? (float*)cd.mem.take(size_t(Lt) * 2 * d * 4) : nullptr;
-  if (!cp) return cudaErrorMemoryAllocation;
+  void* c1 = cd.mem.take(size_t(Lmax) * d * ab);
+  void* cp = cd.mem.take(size_t(Lmax) * d * ab);
+  float* ptmp = f32() ? (float*)cd.mem.take(size_t(Lmax) * 2 * d * 4) : nullptr;
+  cd.kci = cd.vci = nullptr;
+  cd.y = nullptr;
+  if (i2v()) {
+    cd.kci = cd.mem.take(kvbi);
+    cd.vci = cd.mem.take(kvbi);
+    cd.y = (float*)cd.mem.take(yel * 4);
+  }
+  if (!cp || (i2v() && !cd.y)) return cudaErrorMemoryAllocation;
   if (!f32()) DF_TRY(cudaMemsetAsync(cd.kc, 0, 2 * al(kvb), st));  // dh padding = 0
+  if (i2v()) {
+    if (!f32()) DF_TRY(cudaMemsetAsync(cd.kci, 0, 2 * al(kvbi), st));
+    DF_TRY(cudaMemcpyAsync(cd.y, y_in, yel * 4, cudaMemcpyDeviceToDevice, st));
+  }
   DF_TRY(cudaMemcpyAsync(cd.sig_dev, sig_host, (S + 1) * 4, cudaMemcpyHostToDevice, st));
   // time conditioning for all S steps (R4, R5), fp32 SIMT: the M = S rows are GEMV-like
   DF_L(sinusoid(cd.sig_dev, s, S, fd, st));
@@ -458,6 +500,39 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
         DF_L(gemm_tc((const bf16*)cp, d, Lw[l].ckv_wT, d, Lt, 2 * d, d, e, 0, st));
       } else {
         DF_L(gemm_simt(cp, 0, d, 0, Lw[l].ckv_wT, d, ptmp, 2 * d, Lt, 2 * d, d, nullptr, ACT_NONE, st));
+        DF_L(epi_rows(ptmp, e, 1, st));
+      }
+    }
+    if (!i2v()) continue;
+    // I2V (NEXT-3, R27): img' = GELU(clip W_i1 + b_i1) W_i2 + b_i2; [Ki | Vi] = img' [Wki | Wvi]^T
+    // per layer, Ki <- headRMS * g_ki (the same image conditioning for both CFG samples)
+    Epi i1 = epi_base(EPI_STORE, Li, d);
+    i1.bias = img1_b;
+    i1.act = ACT_GELU;
+    i1.out = c1;
+    i1.ldo = d;
+    Epi i2 = epi_base(EPI_STORE, Li, d);
+    i2.bias = img2_b;
+    i2.out = cp;
+    i2.ldo = d;
+    if (!f32()) {
+      DF_L(gemm_tc((const bf16*)clip_bf16, di, img1_wT, di, Li, d, di, i1, 0, st));
+      DF_L(gemm_tc((const bf16*)c1, d, img2_wT, d, Li, d, d, i2, 0, st));
+    } else {
+      DF_L(gemm_simt(clip_bf16, 1, di, 0, img1_wT, di, ptmp, d, Li, d, di, nullptr, ACT_NONE, st));
+      DF_L(epi_rows(ptmp, i1, 1, st));
+      DF_L(gemm_simt(c1, 0, d, 0, img2_wT, d, ptmp, d, Li, d, d, nullptr, ACT_NONE, st));
+      DF_L(epi_rows(ptmp, i2, 1, st));
+    }
+    const size_t peri = size_t(cd.B) * c.heads * Li * dhp * ab, peri_b = size_t(c.heads) * Li * dhp * ab;
+    for (int l = 0; l < c.layers; ++l) {
+      void* kl = (char*)cd.kci + l * peri + b * peri_b;
+      void* vl = (char*)cd.vci + l * peri + b * peri_b;
+      Epi e = heads_epi(Li, 2, Lw[l].ckvi_b, kl, Lw[l].g_ki, 0, vl, nullptr, 0, nullptr, nullptr, 0);
+      if (!f32()) {
+        DF_L(gemm_tc((const bf16*)cp, d, Lw[l].ckvi_wT, d, Li, 2 * d, d, e, 0, st));
+      } else {
+        DF_L(gemm_simt(cp, 0, d, 0, Lw[l].ckvi_wT, d, ptmp, 2 * d, Li, 2 * d, d, nullptr, ACT_NONE, st));
         DF_L(epi_rows(ptmp, e, 1, st));
       }
     }
@@ -504,6 +579,11 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
   }
   cur_kind = K_ATTN_CROSS;
   DF_TRY(attn(qc, (const char*)cd.kc + l * per, (const char*)cd.vc + l * per, o, N, Lt, st, B));
+  if (i2v()) {  // I2V: + softmax(qc Ki^T / sqrt(dh)) Vi over the image tokens (R27)
+    const size_t peri = size_t(B) * c.heads * c.L_img * dhp * act_bytes();
+    DF_TRY(attn(qc, (const char*)cd.kci + l * peri, (const char*)cd.vci + l * peri, oi, N, int(c.L_img), st, B));
+    DF_L(add_into(o, oi, size_t(M) * d, of, st));
+  }
   {
     Epi e = epi_base(EPI_GRES, M, d);
     e.bias = w.co_b;
@@ -542,14 +622,14 @@ cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStrea
   DF_L(modulations(cd.e6 + size_t(i) * 6 * d, cd.e + size_t(i) * d, layer_mods.data(), c.layers, head_mod, d, mods,
                    headmod, st));
   // a2: r = patchify(x) Wpe + bpe   (fp32 residual); a CFG batch starts both samples from it
-  DF_L(patchify(x, X, of, c.C, c.F, c.H, c.W, c.pt, c.ph, c.pw, st));
+  DF_L(patchify(x, cd.y, int(c.C_y), X, of, c.C, c.F, c.H, c.W, c.pt, c.ph, c.pw, st));  // I2V: concat(x, y)
   {
     Epi e = epi_base(EPI_STORE, N, d);
     e.bias = patch_b;
     cur_kind = K_PATCH;
     e.out = r;
     e.ldo = d;
-    DF_TRY(gemm(X, P, patch_wT, P, N, d, P, e, 1, st));
+    DF_TRY(gemm(X, Pin, patch_wT, Pin, N, d, Pin, e, 1, st));
   }
   if (B == 2) DF_TRY(cudaMemcpyAsync(r + size_t(N) * d, r, size_t(N) * d * 4, cudaMemcpyDeviceToDevice, st));
   for (int l = 0; l < c.layers; ++l) DF_TRY(block(cd, i, l, r, st));

@@ -29,9 +29,11 @@ extern std::atomic<uint64_t>* g_launches;
 enum : uint32_t {
   T_PATCH_W = 0, T_PATCH_B, T_TXT1_W, T_TXT1_B, T_TXT2_W, T_TXT2_B, T_TEMB1_W, T_TEMB1_B, T_TEMB2_W, T_TEMB2_B,
   T_TMOD_W, T_TMOD_B, T_HEAD_MOD, T_HEAD_W, T_HEAD_B,
+  T_IMG1_W = 15, T_IMG1_B, T_IMG2_W, T_IMG2_B,  // image-to-video (NEXT-3) only
   T_LAYER_BASE = 64, T_LAYER_STRIDE = 32,
   L_MOD = 0, L_QKV_W, L_QKV_B, L_G_Q, L_G_K, L_O_W, L_O_B, L_G_N3, L_CQ_W, L_CQ_B, L_CK_W, L_CK_B, L_CV_W, L_CV_B,
   L_G_CQ, L_G_CK, L_CO_W, L_CO_B, L_W1, L_B1, L_W3, L_B3, L_W2, L_B2,
+  L_KI_W = 24, L_KI_B, L_VI_W, L_VI_B, L_G_KI,  // image-to-video (NEXT-3) only
   T_ENC_BASE = 1u << 20, E_EMB = 0, E_G_A, E_W1, E_W3, E_W2, E_G_F,
   T_DEC_BASE = 1u << 21, D_W1 = 0, D_B1, D_W2F, D_B2F, D_W2R, D_B2R,
 };
@@ -39,6 +41,7 @@ enum : uint32_t {
 struct LayerW {
   bf16 *mod, *qkv_wT, *qkv_b, *g_q, *g_k, *o_wT, *o_b, *g_n3, *cq_wT, *cq_b, *ckv_wT, *ckv_b, *g_cq, *g_ck, *co_wT,
       *co_b, *w13T, *b13, *w2T, *b2;
+  bf16 *ckvi_wT = nullptr, *ckvi_b = nullptr, *g_ki = nullptr;  // I2V image-token K | V, K gain
 };
 
 // Where a logical tensor lives on the device (for df_weight_bits).
@@ -90,6 +93,9 @@ struct Cond {
   int device = 0;
   int B = 1;                // 2: classifier-free guidance (conditional, negative prompt)
   float guidance = 1.f;
+  void* kci = nullptr;      // I2V: image-token K/V [layers][B][H][L_img][dhp]
+  void* vci = nullptr;
+  float* y = nullptr;       // I2V: y [C_y, F, H, W] (mask + first-frame latent), per request
 };
 
 struct Model {
@@ -101,12 +107,14 @@ struct Model {
   int max_steps = 0;
   // derived
   int N = 0, P = 0, dh = 0, dhp = 0, Fp = 0, Hp = 0, Wp = 0;
+  int Pin = 0;              // patch-embedding input width ((C + C_y) pt ph pw)
   Arena wmem, ws;
   std::vector<TensorLoc> locs;
   // global DiT weights
   bf16 *patch_wT = nullptr, *patch_b = nullptr, *txt1_wT = nullptr, *txt1_b = nullptr, *txt2_wT = nullptr,
        *txt2_b = nullptr, *temb1_wT = nullptr, *temb1_b = nullptr, *temb2_wT = nullptr, *temb2_b = nullptr,
        *tmod_wT = nullptr, *tmod_b = nullptr, *head_mod = nullptr, *head_wT = nullptr, *head_b = nullptr;
+  bf16 *img1_wT = nullptr, *img1_b = nullptr, *img2_wT = nullptr, *img2_b = nullptr;  // I2V image projection
   std::vector<LayerW> Lw;
   // encoder / decoder
   bf16 *emb = nullptr, *g_a = nullptr, *e_w13T = nullptr, *e_w2T = nullptr, *g_f = nullptr;
@@ -120,6 +128,7 @@ struct Model {
   void* qc = nullptr;
   void* o = nullptr;        // [N, d]
   void* a = nullptr;        // [N, f]
+  void* oi = nullptr;       // I2V: image cross-attention output [N, d]
   void* X = nullptr;        // [N, P]
   float* tmp = nullptr;     // fp32 build: raw GEMM out [N, max(3d, 2f)]
   float* sk_ws = nullptr;   // bf16 build: stream-K partial tiles [SMs/2][2][256][128] fp32
@@ -144,7 +153,9 @@ struct Model {
   size_t act_bytes() const { return f32() ? 4 : 2; }
 
   cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
-                      const void* ctx_neg_bf16 = nullptr, float guidance = 1.f);
+                      const void* ctx_neg_bf16 = nullptr, float guidance = 1.f, const void* clip_bf16 = nullptr,
+                      const float* y = nullptr);
+  bool i2v() const { return c.C_y > 0; }
   cudaError_t step(const Cond& c, int i, float* x, float* v_out, cudaStream_t st);
   cudaError_t layer(const Cond& c, int i, int l, float* r_io, cudaStream_t st);
   cudaError_t encode(const int32_t* ids, void* ctx_bf16, cudaStream_t st);

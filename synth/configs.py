@@ -54,6 +54,13 @@ class DitCfg:
     vocab: int = 32768
     enc_ffn: int = 0       # 0 -> 2*d_txt
     dec_width: int = 256   # c_dec
+    # image-to-video conditioning (NEXT-3; C_y = 0: text only).  E also ships
+    # y [C_y, F, H, W] fp32 (mask + VAE latent of the first frame, concatenated to the
+    # noisy latent along channels before patchify) and clip [L_img, d_img] bf16 image tokens
+    # (a second cross-attention per block); Wan I2V: C_y = 4 + C = 20, L_img = 257, d_img = 1280
+    C_y: int = 0
+    L_img: int = 0
+    d_img: int = 0
 
     # ---- derived by counting ----
     @property
@@ -79,6 +86,19 @@ class DitCfg:
     @property
     def P(self) -> int:
         return self.C * self.pt * self.ph * self.pw
+
+    @property
+    def i2v(self) -> bool:
+        return self.C_y > 0
+
+    @property
+    def P_in(self) -> int:
+        """Patch-embedding input width: the noisy latent and y, concatenated along channels."""
+        return (self.C + self.C_y) * self.pt * self.ph * self.pw
+
+    @property
+    def y_shape(self):
+        return (self.C_y, self.F, self.H, self.W)
 
     @property
     def rope_axes(self):
@@ -112,13 +132,15 @@ class DitCfg:
                      + 4 * N * N * d        # self-attn QK^T + PV
                      + 2 * N * d * d        # O
                      + 4 * N * d * d        # cross Q + cross O
-                     + 4 * N * L * d        # cross attn
+                     + 4 * N * (L + self.L_img) * d  # cross attn (text + image tokens)
                      + 6 * N * d * f)       # gated MLP (up 2f + down)
-        return float(self.layers * per_layer + 2 * N * P * d + 2 * N * d * P)
+        return float(self.layers * per_layer + 2 * N * self.P_in * d + 2 * N * d * P)
 
     def flops_prologue(self) -> float:
         L, d, dt = self.L_txt, self.d, self.d_txt
+        Li, di = self.L_img, self.d_img
         return float(2 * L * dt * d + 2 * L * d * d + self.layers * 4 * L * d * d
+                     + 2 * Li * di * d + 2 * Li * d * d + self.layers * 4 * Li * d * d
                      + self.steps * (2 * self.freq_dim * d + 2 * d * d + 12 * d * d))
 
     def flops_per_request(self) -> float:
@@ -141,7 +163,12 @@ VIDEO = DitCfg(name="video", C=16, F=21, H=60, W=104, d=5120, heads=40,
                ffn=_ffn(5120, 256), layers=40, d_txt=4096, L_txt=512, steps=50,
                shift=5.0)
 
-CONFIGS = {c.name: c for c in (TINY, MID, IMAGE, VIDEO)}
+# image-to-video parity configs (NEXT-3): the tiny / mid shapes plus y and image tokens;
+# a 2-frame latent so the first-frame mask is not trivially all ones
+TINY_I2V = replace(TINY, name="tiny-i2v", F=2, C_y=4 + 4, L_img=5, d_img=24)
+MID_I2V = replace(MID, name="mid-i2v", F=2, H=32, W=32, C_y=4 + 16, L_img=257, d_img=128)
+
+CONFIGS = {c.name: c for c in (TINY, MID, IMAGE, VIDEO, TINY_I2V, MID_I2V)}
 
 
 def with_layers(cfg: DitCfg, layers: int, steps: int | None = None) -> DitCfg:

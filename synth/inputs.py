@@ -36,6 +36,21 @@ def ctx_bf16(cfg, seed: int) -> np.ndarray:
     return f32_to_bf16_bits_trunc(rng(seed).standard_normal((cfg.L_txt, cfg.d_txt), dtype=np.float32))
 
 
+def clip_bf16(cfg, seed: int) -> np.ndarray:
+    """I2V image tokens (E->T payload) [L_img, d_img] as bf16 bits, values ~N(0,1)."""
+    return f32_to_bf16_bits_trunc(rng(seed).standard_normal((cfg.L_img, cfg.d_img), dtype=np.float32))
+
+
+def y_cond(cfg, seed: int) -> np.ndarray:
+    """I2V conditioning y [C_y, F, H, W] fp32 (Wan layout): channels 0..3 the first-frame
+    mask (1 on latent frame 0, 0 elsewhere), channels 4.. a VAE-like latent of the conditioning
+    image on frame 0 (N(0,1)) and zeros on the later frames."""
+    y = np.zeros(cfg.y_shape, dtype=np.float32)
+    y[:4, 0] = 1.0
+    y[4:, 0] = rng(seed).standard_normal((cfg.C_y - 4, cfg.H, cfg.W), dtype=np.float32)
+    return y
+
+
 def residual(cfg, seed: int, scale: float = 1.0) -> np.ndarray:
     """A DiT residual stream r [N, d] fp32 (input of one block)."""
     return (scale * rng(seed).standard_normal((cfg.N, cfg.d), dtype=np.float32)).astype(np.float32)

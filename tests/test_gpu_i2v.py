@@ -1,0 +1,114 @@
+"""Image-to-video conditioning (NEXT-3; R27) against the fp64
+oracle: the patch embedding reads concat(x, y) and every block adds a cross-attention
+over the image tokens.  Same tolerances as the text-to-video path (BASELINE.json
+north_star): one bf16 step rel-L2 <= 1e-2, a trajectory <= 3e-2, fp32 build <= 1e-4."""
+import numpy as np
+import pytest
+
+from oracle import params as OP, dit
+from synth import inputs
+from synth.configs import TINY_I2V, MID_I2V
+from gpu_util import rel_l2, bf16_tensor_from_bits, make_ctx
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+BF16, FP32 = 0, 1
+TOL_STEP = {BF16: 1e-2, FP32: 1e-4}
+TOL_TRAJ = {BF16: 3e-2, FP32: 1e-4}
+
+
+def _inputs(cfg, seed):
+    return (inputs.latent(cfg, seed), inputs.ctx_bf16(cfg, seed + 1), inputs.clip_bf16(cfg, seed + 2),
+            inputs.y_cond(cfg, seed + 3))
+
+
+def _oracle_cond(P, cfg, ctx_bits, clip_bits, y, sig):
+    return dit.prologue(P, cfg, inputs.bf16_bits_to_f64(ctx_bits), sig, clip=inputs.bf16_bits_to_f64(clip_bits),
+                        y=y.astype(np.float64))
+
+
+def test_i2v_weight_bits():
+    """Parity check 0 for the I2V tensors: the wider patch embedding and the image paths."""
+    cfg = TINY_I2V
+    P = OP.Params(cfg, 7)
+    with make_ctx(cfg, seed=7) as c:
+        for name in ("patch_w", "img1_w", "img2_b", "L0.ki_w", "L1.vi_w", "L1.vi_b", "L0.g_ki"):
+            got = c.weight_bits(1, P.tid(name), int(np.prod(P[name].shape)))
+            assert np.array_equal(got, P.bits(name).reshape(-1)), name
+
+
+@pytest.mark.parametrize("prec", [BF16, FP32])
+@pytest.mark.parametrize("cfg,i", [(TINY_I2V, 0), (TINY_I2V, 3), (MID_I2V, 2)])
+def test_i2v_step_parity(cfg, i, prec):
+    x, ctx_bits, clip_bits, y = _inputs(cfg, 30)
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32)
+    with make_ctx(cfg, precision=prec) as c:
+        cond = c.dit_prepare_i2v(1, bf16_tensor_from_bits(ctx_bits), bf16_tensor_from_bits(clip_bits),
+                                 torch.from_numpy(y).cuda(), sig)
+        xt = torch.from_numpy(x).cuda()
+        vt = torch.zeros_like(xt)
+        c.dit_step(1, cond, i, xt, vt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        gx, gv = xt.cpu().numpy(), vt.cpu().numpy()
+    P = OP.Params(cfg, 0)
+    sig64 = sig.astype(np.float64)
+    ox, ov = dit.step(P, cfg, x.astype(np.float64), i, _oracle_cond(P, cfg, ctx_bits, clip_bits, y, sig64), sig64)
+    assert rel_l2(gv, ov) <= TOL_STEP[prec], rel_l2(gv, ov)
+    assert rel_l2(gx, ox) <= TOL_STEP[prec]
+
+
+@pytest.mark.parametrize("prec", [BF16, FP32])
+def test_i2v_trajectory_parity(prec):
+    cfg = TINY_I2V
+    x0, ctx_bits, clip_bits, y = _inputs(cfg, 40)
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32)
+    with make_ctx(cfg, precision=prec) as c:
+        cond = c.dit_prepare_i2v(1, bf16_tensor_from_bits(ctx_bits), bf16_tensor_from_bits(clip_bits),
+                                 torch.from_numpy(y).cuda(), sig)
+        xt = torch.from_numpy(x0).cuda()
+        for i in range(cfg.steps):
+            c.dit_step(1, cond, i, xt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        gx = xt.cpu().numpy()
+    P = OP.Params(cfg, 0)
+    ox = dit.trajectory(P, cfg, x0.astype(np.float64), inputs.bf16_bits_to_f64(ctx_bits),
+                        clip=inputs.bf16_bits_to_f64(clip_bits), y=y.astype(np.float64))
+    assert rel_l2(gx, ox) <= TOL_TRAJ[prec], rel_l2(gx, ox)
+
+
+def test_i2v_cfg_step_parity():
+    """I2V with classifier-free guidance: the negative sample keeps the image conditioning."""
+    cfg = TINY_I2V
+    x, ctx_bits, clip_bits, y = _inputs(cfg, 50)
+    neg_bits = inputs.ctx_bf16(cfg, 55)
+    g = 4.0
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32)
+    with make_ctx(cfg) as c:
+        cond = c.dit_prepare_i2v(1, bf16_tensor_from_bits(ctx_bits), bf16_tensor_from_bits(clip_bits),
+                                 torch.from_numpy(y).cuda(), sig, ctx_neg_dev=bf16_tensor_from_bits(neg_bits),
+                                 guidance=g)
+        xt = torch.from_numpy(x).cuda()
+        vt = torch.zeros_like(xt)
+        c.dit_step(1, cond, 1, xt, vt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        gv = vt.cpu().numpy()
+    P = OP.Params(cfg, 0)
+    sig64 = sig.astype(np.float64)
+    cc = _oracle_cond(P, cfg, ctx_bits, clip_bits, y, sig64)
+    cn = _oracle_cond(P, cfg, neg_bits, clip_bits, y, sig64)
+    ov = dit.velocity_cfg(P, cfg, x.astype(np.float64), 1, cc, cn, g)
+    assert rel_l2(gv, ov) <= TOL_STEP[BF16], rel_l2(gv, ov)
+
+
+def test_i2v_needs_image_inputs():
+    """The text-only prologue refuses an I2V graph (it has no image inputs)."""
+    from paper_2605_25550_b200.binding import DFError
+    cfg = TINY_I2V
+    ctx_bits = inputs.ctx_bf16(cfg, 60)
+    with make_ctx(cfg) as c:
+        with pytest.raises(DFError):
+            c.dit_prepare(1, bf16_tensor_from_bits(ctx_bits), dit.sigmas(cfg.steps, cfg.shift).astype(np.float32))

@@ -251,3 +251,104 @@ def test_cfg_guidance_pins():
     a, b, c = (dit.velocity_cfg(P, cfg, x, 1, c1, c0, g) for g in (2.0, 5.0, 8.0))
     np.testing.assert_allclose(c - b, b - a, atol=1e-11)       # affine in g
     assert np.linalg.norm(v1 - v0) > 1e-3 * np.linalg.norm(v1)  # the negative prompt matters
+
+
+# ---------------------------------------------------------------- I2V (NEXT-3)
+def _i2v_cfg():
+    from synth.configs import TINY_I2V
+    return with_layers(TINY_I2V, 1)
+
+
+def test_i2v_patch_input_is_channel_concat():
+    # the first P patch features are the noisy latent's, the rest y's (Conv3d order over
+    # the C + C_y channels): catches a swapped or interleaved concatenation
+    from synth import inputs
+    cfg = _i2v_cfg()
+    x = np.random.default_rng(21).normal(size=cfg.latent_shape)
+    y = inputs.y_cond(cfg, 3).astype(np.float64)
+    X = dit.patchify(np.concatenate([x, y], 0), cfg)
+    assert X.shape == (cfg.N, cfg.P_in)
+    np.testing.assert_array_equal(X[:, :cfg.P], dit.patchify(x, cfg))
+    np.testing.assert_array_equal(X[:, cfg.P:], dit.patchify(y, cfg))
+    # y's first-frame mask reaches exactly the frame-0 tokens
+    ppf = cfg.pt * cfg.ph * cfg.pw
+    mask_cols = X[:, cfg.P:cfg.P + 4 * ppf]
+    f = dit.token_positions(cfg)[:, 0]
+    assert np.all(mask_cols[f == 0] == 1.0) and np.all(mask_cols[f > 0] == 0.0)
+
+
+def _cross_only_block(P, cfg, r0, e6):
+    mod = P.layer(0, "mod").copy()
+    mod[2] = -e6[2]  # g1 = 0: no self-attention
+    mod[5] = -e6[5]  # g2 = 0: no MLP
+    P.set("L0.mod", mod)
+
+
+def test_i2v_single_image_token_adds_its_value_row():
+    # L_img = 1: softmax over one key is 1, so the image term is Vi[0] for every query and
+    # the block (self-attention and MLP gated off) moves by exactly Vi[0] W_co on every row
+    cfg = _i2v_cfg()
+    P = OP.Params(cfg, 0)
+    rr = np.random.default_rng(22)
+    r0 = rr.normal(size=(cfg.N, cfg.d))
+    e6 = rr.normal(size=(6, cfg.d)) * 0.1
+    _cross_only_block(P, cfg, r0, e6)
+    kv = (rr.normal(size=(cfg.L_txt, cfg.d)), rr.normal(size=(cfg.L_txt, cfg.d)))
+    ki, vi = rr.normal(size=(1, cfg.d)), rr.normal(size=(1, cfg.d))
+    pos = dit.token_positions(cfg)
+    a = dit.block(P, cfg, 0, r0, e6, kv, pos)
+    b = dit.block(P, cfg, 0, r0, e6, kv, pos, kvi=(ki, vi))
+    want = np.broadcast_to(vi[0] @ P.layer(0, "co_w"), (cfg.N, cfg.d))
+    np.testing.assert_allclose(b - a, want, rtol=0, atol=1e-12)
+
+
+def test_i2v_image_tokens_are_a_set():
+    # permuting image tokens leaves the block invariant; changing one token's value does not
+    cfg = _i2v_cfg()
+    P = OP.Params(cfg, 0)
+    rr = np.random.default_rng(23)
+    r0 = rr.normal(size=(cfg.N, cfg.d))
+    e6 = rr.normal(size=(6, cfg.d)) * 0.1
+    kv = (rr.normal(size=(cfg.L_txt, cfg.d)), rr.normal(size=(cfg.L_txt, cfg.d)))
+    ki, vi = rr.normal(size=(cfg.L_img, cfg.d)), rr.normal(size=(cfg.L_img, cfg.d))
+    pos = dit.token_positions(cfg)
+    a = dit.block(P, cfg, 0, r0, e6, kv, pos, kvi=(ki, vi))
+    perm = rr.permutation(cfg.L_img)
+    b = dit.block(P, cfg, 0, r0, e6, kv, pos, kvi=(ki[perm], vi[perm]))
+    np.testing.assert_allclose(a, b, atol=1e-12)
+    vi2 = vi.copy(); vi2[1] += 1.0
+    assert np.abs(dit.block(P, cfg, 0, r0, e6, kv, pos, kvi=(ki, vi2)) - a).max() > 1e-6
+
+
+def test_i2v_reduces_to_t2v_when_image_paths_are_zero():
+    # zero y's patch weights and the image values: the I2V velocity equals the text-only
+    # model's with the same (shared tensor-id) weights -> pins the whole I2V wiring to the
+    # T2V path and its own pins
+    import dataclasses
+    from synth import inputs
+    cfg = with_layers(_i2v_cfg(), 2)
+    t2v = dataclasses.replace(cfg, C_y=0, L_img=0, d_img=0, name="tiny-i2v-as-t2v")
+    P = OP.Params(cfg, 0)
+    Pt = OP.Params(t2v, 0)
+    pw = P["patch_w"].copy(); pw[cfg.P:] = 0.0
+    P.set("patch_w", pw)
+    Pt.set("patch_w", pw[:cfg.P])
+    for l in range(cfg.layers):
+        P.set(f"L{l}.vi_w", np.zeros((cfg.d, cfg.d)))
+        P.set(f"L{l}.vi_b", np.zeros(cfg.d))
+    sig = dit.sigmas(cfg.steps, cfg.shift)
+    ctx = np.random.default_rng(24).normal(size=(cfg.L_txt, cfg.d_txt))
+    clip = np.random.default_rng(25).normal(size=(cfg.L_img, cfg.d_img))
+    y = inputs.y_cond(cfg, 4).astype(np.float64)
+    x = np.random.default_rng(26).normal(size=cfg.latent_shape)
+    ci = dit.prologue(P, cfg, ctx, sig, clip=clip, y=y)
+    ct = dit.prologue(Pt, t2v, ctx, sig)
+    np.testing.assert_allclose(dit.velocity(P, cfg, x, 1, ci), dit.velocity(Pt, t2v, x, 1, ct), rtol=0, atol=1e-12)
+    # and with the real weights both conditioning paths matter
+    P2 = OP.Params(cfg, 0)
+    ci2 = dit.prologue(P2, cfg, ctx, sig, clip=clip, y=y)
+    v = dit.velocity(P2, cfg, x, 1, ci2)
+    ci3 = dit.prologue(P2, cfg, ctx, sig, clip=clip * 0.0, y=y)
+    ci4 = dit.prologue(P2, cfg, ctx, sig, clip=clip, y=y * 0.0)
+    assert np.linalg.norm(dit.velocity(P2, cfg, x, 1, ci3) - v) > 1e-3 * np.linalg.norm(v)
+    assert np.linalg.norm(dit.velocity(P2, cfg, x, 1, ci4) - v) > 1e-3 * np.linalg.norm(v)
