@@ -182,6 +182,10 @@ df_status df_decode(df_ctx* ctx, int32_t d_inst, const float* x_dev, float* out_
 /* x0 ~ N(0,1) and token ids from a request seed. */
 df_status df_noise(df_ctx* ctx, int32_t inst, uint64_t seed, float* x_dev, void* stream);
 df_status df_tokens(df_ctx* ctx, int32_t inst, uint64_t seed, int32_t* ids_dev, void* stream);
+/* I2V E stand-in (NEXT-3, R27): the image conditioning of request `seed` — clip_dev
+ * bf16 [L_img, d_img] and y_dev fp32 [C_y, F, H, W] (device, caller-owned); DF_ERR_INVALID for
+ * a text-only graph. */
+df_status df_image_cond(df_ctx* ctx, int32_t inst, uint64_t seed, void* clip_dev, float* y_dev, void* stream);
 
 /* Chunked stage handoff: copy bytes from src (device of
  * src_inst) into dst (device of dst_inst) in ceil(bytes/chunk_bytes) chunks on the

@@ -53,6 +53,29 @@ def noise(cfg, seed: int) -> np.ndarray:
     return z.astype(np.float32).reshape(cfg.latent_shape)
 
 
+def image_encoder(cfg, seed: int):
+    """I2V E stand-in (NEXT-3, R27): the conditioning image's CLIP tokens and VAE latent.
+    No trained encoders exist here (OUT), so both are drawn from the request seed with the
+    weights' exact uniform recipe (r = (u >> 8) 2^-24; v = fp32_RNE((2r - 1) * fp32(sqrt 3)),
+    unit variance): clip[j] = bf16_RNE(v_j) from stream (seed; 0, 5); y channels 0..3 = the
+    first-frame mask (1 on latent frame 0), channels 4.. of frame 0 = v_j from stream
+    (seed; 0, 6) in [C_y - 4, H, W] row-major order, later frames 0.
+    Returns (clip bf16 bits [L_img, d_img], y fp32 [C_y, F, H, W])."""
+    a = np.float32(math.sqrt(3.0))
+
+    def uni(n, c3):
+        u = stream_words(seed, n, 0, c3)
+        r = (u >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+        return ((np.float32(2.0) * r - np.float32(1.0)).astype(np.float32) * a).astype(np.float32)
+
+    from .params import f32_to_bf16_rne_bits
+    clip = f32_to_bf16_rne_bits(uni(cfg.L_img * cfg.d_img, 5)).reshape(cfg.L_img, cfg.d_img)
+    y = np.zeros(cfg.y_shape, dtype=np.float32)
+    y[:4, 0] = 1.0
+    y[4:, 0] = uni((cfg.C_y - 4) * cfg.H * cfg.W, 6).reshape(cfg.C_y - 4, cfg.H, cfg.W)
+    return clip, y
+
+
 def encoder(P, cfg, ids: np.ndarray):
     """E stand-in; returns (ctx values fp64, ctx bf16 bits)."""
     eps = cfg.eps
@@ -90,9 +113,14 @@ def request(P, cfg, seed: int, ids=None, steps=None, shift=None, guidance: float
     ctx_neg = None
     if guidance != 1.0:
         ctx_neg, _ = encoder(P, cfg, tokens_from_seed(cfg, seed, negative=True))
+    clip = y = clip_bits = None
+    if cfg.i2v:  # the image conditioning rides the E->T payload after ctx (NEXT-3)
+        clip_bits, y = image_encoder(cfg, seed)
+        clip = (clip_bits.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+        y = y.astype(np.float64)
     x0 = noise(cfg, seed)
     xS = dit.trajectory(P, cfg, x0.astype(np.float64), ctx, steps=steps, shift=shift, ctx_neg=ctx_neg,
-                        guidance=guidance)
+                        guidance=guidance, clip=clip, y=y)
     lat = xS.astype(np.float32)                      # T->D payload is fp32 (R21)
-    return {"ids": ids, "ctx": ctx, "ctx_bits": ctx_bits, "x0": x0, "latent": lat,
+    return {"ids": ids, "ctx": ctx, "ctx_bits": ctx_bits, "x0": x0, "latent": lat, "clip_bits": clip_bits,
             "out": decoder(P, cfg, lat.astype(np.float64))}

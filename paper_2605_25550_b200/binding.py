@@ -105,6 +105,7 @@ _SIGS = {
     "df_decode": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_noise": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
     "df_tokens": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "df_image_cond": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_handoff": (C.c_int, [C.c_void_p, C.POINTER(HandoffDescC), C.c_void_p, C.POINTER(C.c_void_p)]),
     "df_handoff_wait": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "df_handoff_query": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]),
@@ -344,6 +345,9 @@ class Context:
 
     def tokens(self, inst, seed, ids_dev, stream=None):
         self._ck(self.lib.df_tokens(self.h, inst, seed, _ptr(ids_dev), _stream(stream)))
+
+    def image_cond(self, inst, seed, clip_dev, y_dev, stream=None):
+        self._ck(self.lib.df_image_cond(self.h, inst, seed, _ptr(clip_dev), _ptr(y_dev), _stream(stream)))
 
     def handoff(self, src_inst, dst_inst, src, dst, nbytes, chunk_bytes, flags=0, seq=0, edge=0, stream=None):
         d = HandoffDescC(src_inst, dst_inst, C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), int(nbytes),

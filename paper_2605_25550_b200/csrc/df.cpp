@@ -202,6 +202,12 @@ struct df_ctx {
   std::mutex req_mu;   // E workers share the request ring; assignment counters below
   std::atomic<uint64_t> assigned_t{0}, assigned_d{0};
   size_t ctx_bytes = 0, lat_bytes = 0, out_bytes = 0;
+  // E->T payload: [ctx | clip | y | ctx_neg]; clip/y only for image-to-video graphs (NEXT-3),
+  // ctx_neg only for classifier-free-guidance requests (NEXT-2)
+  size_t clip_bytes = 0, y_bytes = 0;
+  size_t img_bytes() const { return clip_bytes + y_bytes; }
+  size_t neg_off() const { return ctx_bytes + img_bytes(); }
+  size_t payload(bool cfgr) const { return ctx_bytes + img_bytes() + (cfgr ? ctx_bytes : 0); }
   std::vector<float*> sched_dev;
   // multi-process plane
   bool mp = false, seg_owner = false;
@@ -393,6 +399,26 @@ void worker_fail(df_ctx* ctx, const std::string& m) {
 
 // Negative prompt (CFG): tokens from the caller or the seed's negative stream, encoded into
 // the second half of the send buffer.
+// I2V (NEXT-3): the conditioning image's CLIP tokens and VAE latent (stand-in, R27) right
+// after the prompt's ctx in the send buffer
+cudaError_t encode_image(df_ctx* ctx, Inst* me, uint64_t seed, void* ebuf) {
+  if (!ctx->clip_bytes) return cudaSuccess;
+  const df_dit_cfg& c = me->m.c;
+  char* p = static_cast<char*>(ebuf) + ctx->ctx_bytes;
+  g_launches->fetch_add(1);
+  return gen_image_cond(seed, reinterpret_cast<bf16*>(p), size_t(c.L_img) * c.d_img,
+                        reinterpret_cast<float*>(p + ctx->clip_bytes), int(c.C_y), int(c.F), int(c.H), int(c.W),
+                        me->compute);
+}
+const void* i2v_clip(const df_ctx* ctx, const void* cbuf) {
+  return ctx->clip_bytes ? static_cast<const char*>(cbuf) + ctx->ctx_bytes : nullptr;
+}
+const float* i2v_y(const df_ctx* ctx, const void* cbuf) {
+  return ctx->clip_bytes ? reinterpret_cast<const float*>(static_cast<const char*>(cbuf) + ctx->ctx_bytes +
+                                                          ctx->clip_bytes)
+                         : nullptr;
+}
+
 cudaError_t encode_negative(df_ctx* ctx, Inst* me, ReqState* rs, void* ebuf) {
   const size_t L = ctx->g.dit.L_txt;
   int32_t* nid = me->ids_dev + L;
@@ -402,7 +428,7 @@ cudaError_t encode_negative(df_ctx* ctx, Inst* me, ReqState* rs, void* ebuf) {
     g_launches->fetch_add(1);
     DF_TRY(gen_tokens(nid, int(L), int(me->m.c.vocab), rs->req.seed, me->compute, 4));
   }
-  return me->m.encode(nid, static_cast<char*>(ebuf) + ctx->ctx_bytes, me->compute);
+  return me->m.encode(nid, static_cast<char*>(ebuf) + ctx->neg_off(), me->compute);
 }
 
 void e_worker(df_ctx* ctx, Inst* me) {
@@ -438,6 +464,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
       WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
     }
     WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+    WK(encode_image(ctx, me, rs->req.seed, me->ebuf[b]));
     const bool cfgr = cfg_on(rs->req.guidance);
     if (cfgr) WK(encode_negative(ctx, me, rs, me->ebuf[b]));
     WK(cudaEventRecord(rs->ev[1], me->compute));
@@ -451,7 +478,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
     d.dst_inst = tid;
     d.src = me->ebuf[b];
     d.dst = T->slots.slots[s].buf;
-    d.bytes = (cfgr ? 2 : 1) * ctx->ctx_bytes;
+    d.bytes = ctx->payload(cfgr);
     d.chunk_bytes = ctx->g.chunk_bytes[0];
     d.flags = (ctx->g.handoff_mode & (DF_SYNC | DF_HASH));
     d.seq = rs->seq;
@@ -526,8 +553,8 @@ void t_worker(df_ctx* ctx, Inst* me) {
     std::vector<float> sig = sigmas_host(S, rs->req.shift);
     const void* cbuf = me->slots.slots[rs->slot[0]].buf;
     const bool cfgr = cfg_on(rs->req.guidance);
-    WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->ctx_bytes : nullptr,
-                     cfgr ? rs->req.guidance : 1.f));
+    WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->neg_off() : nullptr,
+                     cfgr ? rs->req.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf)));
     WK(cudaEventRecord(me->slots.slots[rs->slot[0]].consumed, me->compute));
     me->slots.release(rs->slot[0]);  // producer's comm stream waits on `consumed` before reuse
     for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
@@ -862,12 +889,13 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
       WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
     }
     WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+    WK(encode_image(ctx, me, rs->req.seed, me->ebuf[b]));
     const bool cfgr = cfg_on(rs->req.guidance);
     if (cfgr) WK(encode_negative(ctx, me, rs, me->ebuf[b]));
     m.guidance = cfgr ? rs->req.guidance : 1.f;
     WK(cudaEventRecord(e1, me->compute));
     m.t_end_e = now_s();
-    if (!mp_send(ctx, me, tid, me->ebuf[b], (cfgr ? 2 : 1) * ctx->ctx_bytes, ctx->g.chunk_bytes[0], me->compute, m,
+    if (!mp_send(ctx, me, tid, me->ebuf[b], ctx->payload(cfgr), ctx->g.chunk_bytes[0], me->compute, m,
                  0)) {
       free_req(rs);
       return;
@@ -899,13 +927,13 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     WK(gen_noise(x, latent_elems(me->m.c), m.seed, me->compute));
     WK(cudaEventRecord(r0, me->compute));  // consumer ready for ctx
     const bool cfgr = cfg_on(m.guidance);
-    WK(mp_wait_chunks(ctx, me, m, me->compute, (cfgr ? 2 : 1) * ctx->ctx_bytes));
+    WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->payload(cfgr)));
     WK(cudaEventRecord(w0, me->compute));  // ctx landed
     std::vector<float> sig = sigmas_host(S, m.shift);
     Cond cd;
     const void* cbuf = me->slots.slots[m.slot].buf;
-    WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->ctx_bytes : nullptr,
-                     cfgr ? m.guidance : 1.f));
+    WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->neg_off() : nullptr,
+                     cfgr ? m.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf)));
     WK(mp_release_slot(ctx, me, m.slot, me->compute));
     for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
     WK(cudaEventRecord(t1, me->compute));
@@ -1386,6 +1414,10 @@ df_status df_init(const df_graph* g, df_ctx** out) {
   ctx->done.reset(new FaaRing<ReqState*>(std::max<uint32_t>(g->ring_capacity, 1024)));
   const df_dit_cfg& c = g->dit;
   ctx->ctx_bytes = size_t(c.L_txt) * c.d_txt * 2;
+  if (c.C_y > 0) {
+    ctx->clip_bytes = (size_t(c.L_img) * c.d_img * 2 + 15) & ~size_t(15);
+    ctx->y_bytes = size_t(c.C_y) * c.F * c.H * c.W * 4;
+  }
   ctx->lat_bytes = latent_elems(c) * 4;
   ctx->out_bytes = out_elems(c) * 4;
   // peer access between every pair of devices in use (NVLink P2P, P:L390 GPUDirect analogue)
@@ -1438,7 +1470,7 @@ df_status df_init(const df_graph* g, df_ctx** out) {
     cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, I.stage == DF_T ? lo : hi);
     cudaStreamCreateWithPriority(&I.comm, cudaStreamNonBlocking, hi);
     // T receive slots and E send buffers hold up to two ctx (prompt + negative prompt, CFG)
-    size_t slot_bytes = I.stage == DF_T ? 2 * ctx->ctx_bytes : (I.stage == DF_D ? ctx->lat_bytes : 0);
+    size_t slot_bytes = I.stage == DF_T ? ctx->payload(true) : (I.stage == DF_D ? ctx->lat_bytes : 0);
     if (slot_bytes) {
       I.slots.slots.resize(g->n_slots);
       for (uint32_t s = 0; s < g->n_slots; ++s) {
@@ -1456,7 +1488,7 @@ df_status df_init(const df_graph* g, df_ctx** out) {
       }
     } else if (I.stage == DF_E) {
       for (int b = 0; b < 2; ++b) {
-        cudaMalloc(&I.ebuf[b], 2 * ctx->ctx_bytes);
+        cudaMalloc(&I.ebuf[b], ctx->payload(true));
         cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming);
         cudaEventRecord(I.esent[b], I.comm);
       }
@@ -1759,6 +1791,16 @@ df_status df_tokens(df_ctx* ctx, int32_t inst, uint64_t seed, int32_t* ids_dev, 
   if (!I || !ids_dev) return fail(ctx, "df_tokens: invalid", DF_ERR_INVALID);
   g_launches->fetch_add(1);
   cudaError_t e = gen_tokens(ids_dev, int(ctx->g.dit.L_txt), int(ctx->g.dit.vocab), seed, (cudaStream_t)stream);
+  return e == cudaSuccess ? DF_OK : fail(ctx, cudaGetErrorString(e));
+}
+
+df_status df_image_cond(df_ctx* ctx, int32_t inst, uint64_t seed, void* clip_dev, float* y_dev, void* stream) {
+  Inst* I = get_inst(ctx, inst, -1);
+  const df_dit_cfg& c = ctx ? ctx->g.dit : df_dit_cfg{};
+  if (!I || !clip_dev || !y_dev || c.C_y == 0) return fail(ctx, "df_image_cond: invalid", DF_ERR_INVALID);
+  g_launches->fetch_add(1);
+  cudaError_t e = gen_image_cond(seed, static_cast<bf16*>(clip_dev), size_t(c.L_img) * c.d_img, y_dev, int(c.C_y),
+                                 int(c.F), int(c.H), int(c.W), (cudaStream_t)stream);
   return e == cudaSuccess ? DF_OK : fail(ctx, cudaGetErrorString(e));
 }
 

@@ -103,6 +103,36 @@ __global__ void tokens_kernel(int32_t* ids, int n, int vocab, uint64_t seed, uin
   if (j < n) ids[j] = int32_t(philox_word(seed, j, 0, c3) % uint32_t(vocab));
 }
 // stream c3 = 2: prompt tokens; c3 = 4: negative-prompt tokens
+// I2V E stand-in (R27): clip [L_img, d_img] bf16 from stream (seed; 0, 5) and
+// y [C_y, F, H, W] fp32 (mask channels 0..3 = 1 on frame 0; channels 4.. of frame 0 from
+// stream (seed; 0, 6)), each value fp32((2r - 1) * fp32(sqrt 3)) with r = (u >> 8) 2^-24
+DF_DEV float unit_uniform(uint32_t u) {
+  const float r = float(u >> 8) * 5.9604644775390625e-08f;  // 2^-24, exact
+  return __fmul_rn(__fsub_rn(__fmul_rn(2.0f, r), 1.0f), 1.7320508075688772f);
+}
+__global__ void image_cond_kernel(uint64_t seed, bf16* clip, size_t n_clip, float* y, int Cy, int F, int H, int W) {
+  const size_t hw = size_t(H) * W, n_y = size_t(Cy) * F * hw;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_clip + n_y; i += size_t(gridDim.x) * blockDim.x) {
+    if (i < n_clip) {
+      clip[i] = __float2bfloat16_rn(unit_uniform(philox_word(seed, i, 0, 5)));
+    } else {
+      const size_t j = i - n_clip;
+      const size_t c = j / (size_t(F) * hw), rem = j - c * size_t(F) * hw, f = rem / hw, p = rem - f * hw;
+      float v = 0.f;
+      if (f == 0) v = c < 4 ? 1.f : unit_uniform(philox_word(seed, (c - 4) * hw + p, 0, 6));
+      y[j] = v;
+    }
+  }
+}
+cudaError_t gen_image_cond(uint64_t seed, bf16* clip, size_t n_clip, float* y, int Cy, int F, int H, int W,
+                           cudaStream_t st) {
+  const size_t n = n_clip + size_t(Cy) * F * H * W;
+  unsigned blocks = unsigned((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  image_cond_kernel<<<blocks, 256, 0, st>>>(seed, clip, n_clip, y, Cy, F, H, W);
+  return cudaGetLastError();
+}
+
 cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st, uint32_t stream_c3) {
   tokens_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, vocab, seed, stream_c3);
   return cudaGetLastError();

@@ -70,6 +70,9 @@ struct InitSpec {
 };
 cudaError_t init_tensor(bf16* dst, const InitSpec& s, cudaStream_t st);
 cudaError_t gen_noise(float* x, size_t n, uint64_t seed, cudaStream_t st);
+// I2V E stand-in: clip tokens (bf16) and y (fp32) of request `seed` (R27)
+cudaError_t gen_image_cond(uint64_t seed, bf16* clip, size_t n_clip, float* y, int Cy, int F, int H, int W,
+                           cudaStream_t st);
 cudaError_t gen_tokens(int32_t* ids, int n, int vocab, uint64_t seed, cudaStream_t st, uint32_t stream_c3 = 2);
 
 // ---- E / D stand-ins

@@ -112,3 +112,44 @@ def test_i2v_needs_image_inputs():
     with make_ctx(cfg) as c:
         with pytest.raises(DFError):
             c.dit_prepare(1, bf16_tensor_from_bits(ctx_bits), dit.sigmas(cfg.steps, cfg.shift).astype(np.float32))
+
+
+def test_i2v_image_encoder_equals_oracle():
+    """The E stand-in's image conditioning (clip bf16, y fp32) is bit-exact with the oracle's."""
+    from oracle import stages
+    from synth.configs import TINY_I2V
+    cfg = TINY_I2V
+    with make_ctx(cfg) as c:
+        clip = torch.zeros((cfg.L_img, cfg.d_img), device="cuda", dtype=torch.bfloat16)
+        y = torch.zeros(cfg.y_shape, device="cuda")
+        c.image_cond(0, 987, clip, y)
+        torch.cuda.synchronize()
+        want_clip, want_y = stages.image_encoder(cfg, 987)
+        got_clip = clip.view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(got_clip, want_clip)
+        assert np.array_equal(y.cpu().numpy(), want_y)
+
+
+@pytest.mark.parametrize("guidance", [1.0, 3.0])
+def test_i2v_pipeline_matches_oracle(guidance):
+    """E -> T -> D with the image conditioning in the E->T payload ([ctx | clip | y | ctx_neg],
+    chunked, hashed): outputs within the trajectory tolerance of the serial oracle request."""
+    from oracle import stages, capacity as cap
+    from paper_2605_25550_b200 import binding as B
+    cfg = TINY_I2V
+    P = OP.Params(cfg, 0)
+    seeds = [5, 6]
+    with make_ctx(cfg, handoff_mode=B.DF_ASYNC | B.DF_HASH, chunk_bytes=(96, 256)) as c:
+        outs = {s: np.zeros(cfg.out_shape, np.float32) for s in seeds}
+        for s in seeds:
+            st, _ = c.submit(cfg.steps, cfg.shift, s, out_host=outs[s], user_tag=s, guidance=guidance)
+            assert st == B.DF_OK
+        comps = []
+        while len(comps) < len(seeds):
+            comps += c.poll(16, timeout_ms=60000)
+    assert sorted(x.user_tag for x in comps) == seeds
+    for x in comps:
+        for e in range(2):
+            assert x.hash_src[e] == x.hash_dst[e] != 0
+        want = stages.request(P, cfg, seed=int(x.user_tag), guidance=guidance)
+        assert rel_l2(outs[x.user_tag], want["out"]) <= 3e-2

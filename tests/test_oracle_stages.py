@@ -156,3 +156,25 @@ def test_change_detector_spec_examples():
     assert not cap.changed([4] * 20)
     assert cap.changed([4] * 15 + [1] * 5)
     assert not cap.changed([4] * 12 + [1, 1, 4, 4])   # tie in the recent window -> no change
+
+
+def test_image_encoder_stand_in_invariants():
+    """I2V E stand-in (R27): unit-variance uniform tokens bounded by sqrt(3), the first-frame
+    mask exactly 1 on latent frame 0 and y zero on later frames, seed-determined."""
+    from synth.configs import TINY_I2V, MID_I2V
+    cfg = MID_I2V
+    clip_bits, y = stages.image_encoder(cfg, 11)
+    clip = (clip_bits.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+    assert clip.shape == (cfg.L_img, cfg.d_img) and y.shape == cfg.y_shape and y.dtype == np.float32
+    assert np.abs(clip).max() <= np.sqrt(3.0) * (1 + 2 ** -8)
+    n = clip.size
+    assert abs(clip.mean()) < 5 / np.sqrt(n) and abs(clip.var() - 1.0) < 0.05
+    assert np.all(y[:4, 0] == 1.0) and np.all(y[:, 1:] == 0.0)
+    lat = y[4:, 0].astype(np.float64)
+    assert abs(lat.mean()) < 5 / np.sqrt(lat.size) and abs(lat.var() - 1.0) < 0.05
+    c2, y2 = stages.image_encoder(cfg, 11)
+    c3, y3 = stages.image_encoder(cfg, 12)
+    assert np.array_equal(c2, clip_bits) and np.array_equal(y2, y)
+    assert not np.array_equal(c3, clip_bits) and not np.array_equal(y3, y)
+    ct, yt = stages.image_encoder(TINY_I2V, 11)
+    assert ct.shape == (TINY_I2V.L_img, TINY_I2V.d_img) and yt.shape == TINY_I2V.y_shape
