@@ -172,6 +172,9 @@ def workload_name(cfg):
         return "text-to-image 1024x1024 -> 4096 latent tokens, DiT hidden 3072 x28 layers, 28 Euler steps (BASELINE configs[1])"
     if cfg.name == "video":
         return "text-to-video 81x480x832 -> 32760 latent tokens, DiT hidden 5120 x40 layers, 50 Euler steps (BASELINE configs[2])"
+    if cfg.name == "video_i2v":
+        return (f"image-to-video 81x480x832 -> 32760 latent tokens (+ y 20 channels, 257 CLIP tokens), DiT hidden "
+                f"5120 x40 layers, {cfg.steps} Euler steps (the paper's Wan2.2 I2V workload, P:L441; not a BASELINE config)")
     return f"{cfg.name}: N={cfg.N} d={cfg.d} layers={cfg.layers} steps={cfg.steps}"
 
 
@@ -397,8 +400,13 @@ def main():
     ap.add_argument("--t-per-gpu", type=int, default=1, help="DiT instances per GPU")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
+    ap.add_argument("--dit-steps", type=int, default=0,
+                    help="Euler steps per request (0: the config's); for the few-step I2V / workload-shift runs")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.dit_steps:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, steps=args.dit_steps)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -168,7 +168,11 @@ VIDEO = DitCfg(name="video", C=16, F=21, H=60, W=104, d=5120, heads=40,
 TINY_I2V = replace(TINY, name="tiny-i2v", F=2, C_y=4 + 4, L_img=5, d_img=24)
 MID_I2V = replace(MID, name="mid-i2v", F=2, H=32, W=32, C_y=4 + 16, L_img=257, d_img=128)
 
-CONFIGS = {c.name: c for c in (TINY, MID, IMAGE, VIDEO, TINY_I2V, MID_I2V)}
+# the paper's Wan2.2 I2V workload at 480p / 81 frames (tab:quality: I2V 40/8/4/1-step):
+# the video shape plus y (4 mask + 16 latent channels) and 257 CLIP tokens of width 1280
+VIDEO_I2V = replace(VIDEO, name="video_i2v", steps=40, C_y=4 + 16, L_img=257, d_img=1280)
+
+CONFIGS = {c.name: c for c in (TINY, MID, IMAGE, VIDEO, TINY_I2V, MID_I2V, VIDEO_I2V)}
 
 
 def with_layers(cfg: DitCfg, layers: int, steps: int | None = None) -> DitCfg:
