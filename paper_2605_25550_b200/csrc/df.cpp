@@ -304,10 +304,8 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_str
   if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f) {
     uint32_t c[4] = {uint32_t(d->seq), uint32_t(d->seq >> 32), d->edge, 3u};
     philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
-    if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0) {
-      g_launches->fetch_add(1);
-      CK(ctx, delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), S.comm));
-    }
+    if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0)
+      CK(ctx, delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), S.comm));  // host function, no kernel
   }
   CK(ctx, cudaEventRecord(x->t0, S.comm));
   std::vector<uint32_t> order(x->nchunks);
@@ -790,7 +788,6 @@ bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, uint64_t bytes, uin
     uint32_t c[4] = {uint32_t(m.seq), uint32_t(m.seq >> 32), edge, 3u};
     philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
     if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0) {
-      g_launches->fetch_add(1);
       if (!chk(delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), me->comm), "delay")) return false;
     }
   }

@@ -1,3 +1,5 @@
+#include <chrono>
+#include <thread>
 // HBM-bound kernels of the DiT step and the request prologue, plus parameter init
 // (Philox4x32-10) and the E/D stand-in stages.
 //
@@ -548,18 +550,15 @@ cudaError_t payload_hash(const void* buf, size_t nbytes, size_t word_offset, uns
   return cudaGetLastError();
 }
 
-__global__ void delay_kernel(uint64_t ns) {
-  uint64_t t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  uint64_t t = t0;
-  while (t - t0 < ns) {
-    __nanosleep(1000);
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  }
+// Injected transfer delay (P:L142 jitter, R23): a host function on the comm stream, so the
+// delay holds back the stream's later copies without occupying an SM (a spinning 1-thread
+// kernel had pinned one SM for the whole delay and stalled the persistent kernels' last pair).
+static void CUDART_CB delay_host_fn(void* p) {
+  std::this_thread::sleep_for(std::chrono::nanoseconds(reinterpret_cast<uintptr_t>(p)));
 }
 cudaError_t delay_ns(uint64_t ns, cudaStream_t st) {
-  delay_kernel<<<1, 1, 0, st>>>(ns);
-  return cudaGetLastError();
+  if (ns == 0) return cudaSuccess;
+  return cudaLaunchHostFunc(st, delay_host_fn, reinterpret_cast<void*>(uintptr_t(ns)));
 }
 
 }  // namespace df

@@ -105,3 +105,18 @@ def test_pipeline_cfg_matches_oracle():
         assert x.hash_src[0] == x.hash_dst[0] != 0
         want = stages.request(P, cfg, seed=int(x.user_tag), guidance=3.0)["out"]
         assert rel_l2(outs[x.user_tag], want) <= 3e-2
+
+
+def test_jitter_delays_the_transfer_not_the_data():
+    """Injected transfer jitter (R23) with p = 1: every E->T transfer is held back by d
+    on the comm stream, the (tiny, fast) DiT stage waits for it (exposed >= d on edge 0), and
+    the outputs are unchanged (the delay is a host function, no kernel and no SM taken)."""
+    cfg = TINY
+    P = OP.Params(cfg, 0)
+    d = 0.05
+    with make_ctx(cfg, handoff_mode=B.DF_ASYNC | B.DF_HASH, jitter=(1.0, d, 5)) as c:
+        outs, comps = _run_requests(c, cfg, [7, 8], cfg.steps, cfg.shift)
+    for x in comps:
+        assert x.exposed_ms[0] >= 0.8 * d * 1e3, x.exposed_ms[0]
+        assert x.hash_src[0] == x.hash_dst[0] != 0
+        assert rel_l2(outs[x.user_tag], stages.request(P, cfg, seed=int(x.user_tag))["out"]) <= 3e-2

@@ -24,8 +24,11 @@ def main():
     ap.add_argument("--shape", default="video")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--lib", action="store_true", help="also time torch SDPA (cuDNN / flash backends) on the same inputs")
+    ap.add_argument("--H", type=int, default=0, help="override the head count (work-item scaling experiments)")
     a = ap.parse_args()
     H, Nq, Nk = SHAPES[a.shape]
+    if a.H:
+        H = a.H
     dh = 128
     g = B.make_graph(TINY, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)])
     with B.Context(g) as c:
@@ -55,7 +58,7 @@ def main():
         err = ((got - ref).norm() / ref.norm()).item()
         fl = 4.0 * H * Nq * Nk * dh
         best = min(ms)
-        print({"shape": a.shape, "impl": os.environ.get("DF_ATTN_IMPL", "default"), "poly": os.environ.get("DF_ATTN_POLY", "default"),
+        print({"shape": a.shape, "H": H, "impl": os.environ.get("DF_ATTN_IMPL", "default"), "poly": os.environ.get("DF_ATTN_POLY", "default"),
                "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
                "rel_l2_vs_torch": f"{err:.2e}"})
         if a.lib:  # library reference point (not on the product path)
