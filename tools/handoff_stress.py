@@ -24,6 +24,9 @@ from paper_2605_25550_b200 import binding as B  # noqa: E402
 from synth.configs import CONFIGS  # noqa: E402
 
 
+SLOTS = 2
+
+
 def run(cfg, steps, n_req, mode, chunk, jitter, seed0, reps=3):
     """Best of `reps` repetitions (host-side hiccups only ever slow a run down)."""
     best = None
@@ -36,7 +39,7 @@ def run(cfg, steps, n_req, mode, chunk, jitter, seed0, reps=3):
 
 def run_once(cfg, steps, n_req, mode, chunk, jitter, seed0):
     g = B.make_graph(cfg, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)], chunk_bytes=chunk,
-                     handoff_mode=mode | B.DF_HASH, max_steps=steps, jitter=jitter)
+                     handoff_mode=mode | B.DF_HASH, max_steps=steps, jitter=jitter, n_slots=SLOTS)
     with B.Context(g) as c:
         # warm-up request (not timed)
         c.submit(steps, cfg.shift, seed0 - 1)
@@ -67,12 +70,16 @@ def main():
     ap.add_argument("--dit-steps", type=int, default=8)
     ap.add_argument("--requests", type=int, default=24)
     ap.add_argument("--out", default="gpurun_out/handoff_stress.json")
+    ap.add_argument("--slots", type=int, default=2, help="receive slots per consumer per edge")
+    ap.add_argument("--jitter-only", action="store_true", help="skip the chunk sweep (chunk 256 KiB)")
     a = ap.parse_args()
+    global SLOTS
+    SLOTS = a.slots
     cfg = CONFIGS[a.config]
-    res = {"config": cfg.name, "dit_steps": a.dit_steps, "requests_per_point": a.requests, "chunk_sweep": {},
-           "jitter": {}}
+    res = {"config": cfg.name, "dit_steps": a.dit_steps, "requests_per_point": a.requests, "slots": a.slots,
+           "chunk_sweep": {}, "jitter": {}}
     # ---- chunk-size sweep (no jitter, async)
-    for ch in (16 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 0):
+    for ch in ((256 << 10,) if a.jitter_only else (16 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 0)):
         r = run(cfg, a.dit_steps, max(4, a.requests // 2), B.DF_ASYNC, (ch, ch), (0.0, 0.0, 0), 100)
         res["chunk_sweep"][str(ch or "whole")] = r
         print("chunk", ch, r, flush=True)
