@@ -153,3 +153,32 @@ def test_i2v_pipeline_matches_oracle(guidance):
             assert x.hash_src[e] == x.hash_dst[e] != 0
         want = stages.request(P, cfg, seed=int(x.user_tag), guidance=guidance)
         assert rel_l2(outs[x.user_tag], want["out"]) <= 3e-2
+
+
+def test_i2v_layer_parity_production_widths():
+    """One I2V block at the video model's widths (d = 5120, 40 heads, 257 image tokens of
+    width 1280 -> 3 key blocks with a ragged tail, C_y = 20 -> a 144-wide patch input) on a
+    2-frame 480x832 latent, 64 sampled rows plus the ragged last rows, vs oracle.block_rows."""
+    import dataclasses
+    from synth.configs import VIDEO_I2V, with_layers
+    cfg = dataclasses.replace(with_layers(VIDEO_I2V, 1), F=2)
+    x_r = inputs.residual(cfg, 71)
+    ctx_bits, clip_bits, y = inputs.ctx_bf16(cfg, 72), inputs.clip_bf16(cfg, 73), inputs.y_cond(cfg, 74)
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32)
+    i = 5
+    rows = np.concatenate([np.sort(np.random.default_rng(2).choice(cfg.N - 40, 48, replace=False)),
+                           np.arange(cfg.N - 16, cfg.N)])
+    with make_ctx(cfg) as c:
+        cond = c.dit_prepare_i2v(1, bf16_tensor_from_bits(ctx_bits), bf16_tensor_from_bits(clip_bits),
+                                 torch.from_numpy(y).cuda(), sig)
+        rt = torch.from_numpy(x_r).cuda()
+        c.dit_layer(1, cond, i, 0, rt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        got = rt.cpu().numpy()[rows]
+    P = OP.Params(cfg, 0)
+    kv = dit.cross_kv(P, cfg, 0, dit.text_projection(P, cfg, inputs.bf16_bits_to_f64(ctx_bits)))
+    kvi = dit.image_kv(P, cfg, 0, dit.image_projection(P, cfg, inputs.bf16_bits_to_f64(clip_bits)))
+    _, e6 = dit.time_embedding(P, cfg, float(sig[i]))
+    want = dit.block_rows(P, cfg, 0, x_r.astype(np.float64), e6, kv, dit.token_positions(cfg), rows, kvi=kvi)
+    assert rel_l2(got - x_r[rows], want - x_r[rows]) <= 1e-2
