@@ -1,3 +1,4 @@
+#include <atomic>
 // Self- and cross-attention of the DiT block (PAPER.md P:L118
 // "attention is O(T^2 D)"): O_h = softmax(Q_h K_h^T / sqrt(dh)) V_h, no mask, fp32
 // online softmax.
@@ -1861,6 +1862,507 @@ static cudaError_t launch_attn_pp(const bf16* Q, const bf16* K, const bf16* V, b
   return launch_ex((const void*)kern, grid, dim3(ATTN3_THREADS), SMEM, st, args);
 }
 
+DF_DEV void st_release_u32_attn(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+DF_DEV unsigned ld_acquire_u32_attn(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------------ attn_ppsk: persistent CTA pair + stream-K
+// attn_pair3's MMA schedule and softmax, but each CTA pair loops over work units instead of
+// one item per launch slot (an item = 512 query rows of one head; items head-major so
+// consecutive items reuse K/V in L2): the TMEM allocation and barrier set-up happen once,
+// the next unit's Q is loaded while the current unit's last blocks run (q_empty is committed
+// after its last QK), and the next unit's QKs start while the softmax warps normalise and
+// store the previous O (the first PV of a unit waits for o_free, the epilogue's release of
+// O_t).  All barrier phases run on counters that continue across units.
+//
+// Stream-K (sk.ws set; the image shape's 192 items on 74 pairs would otherwise leave 30
+// pairs idle for the last third): the items x key blocks are cut into equal contiguous
+// ranges per pair.  An item cut between pair p (its first key blocks, the "head") and
+// pair p + 1 (the rest, the "tail") is finished by p + 1: every pair runs its head unit
+// first and publishes the unnormalised O, the row max in use m and the half-row sums l
+// (fp32) in its workspace slot with an epoch flag; its tail unit then waits for slot
+// p - 1, merges O = O_a 2^(m_a - m) + O_b 2^(m_b - m) (m = max), l likewise, and
+// normalises.  The split points depend only on the shape and the pair count: deterministic.
+struct AttnSK {
+  float* ws;          // [pairs][2 CTAs] slots of SK_SLOT floats
+  unsigned* flag;     // [pairs][2 CTAs] epochs
+  unsigned epoch;
+};
+constexpr int SK_SLOT = 2 * 2 * 64 * 128 + 2 * 128 + 2 * 2 * 128;  // O [t][hc][64][128], m [t][128], l [t][hc][128]
+
+struct AttnSched {
+  int nkb, step;
+  int hd_it, hd_k;        // stream-K head unit: item, block count (0 = none)
+  int tl_it, tl_k;        // stream-K tail unit: item, first block (0 = none)
+  int full0, full1;       // whole items [full0, full1) in steps of `step`
+  int state;              // 0: head next, 1: tail next, 2: whole items
+  DF_DEV AttnSched(int items, int nkb_, int npairs, int cid, bool sk)
+      : nkb(nkb_), step(sk ? 1 : npairs), hd_it(0), hd_k(0), tl_it(0), tl_k(0), full0(cid), full1(items),
+        state(sk ? 0 : 2) {
+    if (!sk) return;
+    const long long total = (long long)items * nkb;
+    const long long b = total * cid / npairs, e = total * (cid + 1) / npairs;
+    const int ta = int(b / nkb), ka = int(b % nkb);
+    const int tb = int(e / nkb), kb = int(e % nkb);
+    full0 = ka ? ta + 1 : ta;
+    full1 = tb;
+    hd_it = tb, hd_k = kb;  // head: first kb blocks of item tb (published for pair cid + 1)
+    tl_it = ta, tl_k = ka;  // tail: blocks [ka, nkb) of item ta (merged with pair cid - 1's head)
+  }
+  DF_DEV bool next(int& it, int& j0, int& j1) {
+    if (state == 0) {
+      state = 1;
+      if (hd_k) {
+        it = hd_it, j0 = 0, j1 = hd_k;
+        return true;
+      }
+    }
+    if (state == 1) {
+      state = 2;
+      if (tl_k) {
+        it = tl_it, j0 = tl_k, j1 = nkb;
+        return true;
+      }
+    }
+    if (full0 >= full1) return false;
+    it = full0;
+    j0 = 0;
+    j1 = nkb;
+    full0 += step;
+    return true;
+  }
+};
+
+template <int EXPM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
+    attn_ppsk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                   int dh_real, float scale_log2, int Hs, const __grid_constant__ AttnSK sk) {
+  using Cfg = AttnPairCfg;
+  constexpr int DH = Cfg::DH;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;                 // leader
+  uint64_t* q_empty = bars + 1;                // both (multicast commit after the unit's last QK)
+  uint64_t* k_full = bars + 2;                 // [KST]  leader
+  uint64_t* k_empty = k_full + Cfg::KST;       // [KST]  both
+  uint64_t* v_full = k_empty + Cfg::KST;       // [VST]  leader
+  uint64_t* v_empty = v_full + Cfg::VST;       // [VST]  both
+  uint64_t* s_full = v_empty + Cfg::VST;       // [2]    both
+  uint64_t* o_done = s_full + 2;               // [2]    both
+  uint64_t* o_free = o_done + 2;               // [2]    leader: 8 softmax warps x 2 CTAs
+  uint64_t* p_q = o_free + 2;                  // [2][4] leader: 4 warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_q + 8);
+  float* red = reinterpret_cast<float*>(smem + Cfg::OFF_BAR + 512);    // [2 tiles][2 halves][128] row max
+  float* lred = red + 512;                                              // [2 tiles][2 halves][128] row sum
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int nkb = (Nk + 127) / 128;
+  const int nqp = (Nq + 511) / 512;
+  const int items = nqp * H;
+  const int cid = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const bool use_sk = sk.ws != nullptr;
+
+  if (warp == 16 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 2);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < Cfg::KST; ++s) {
+      mbar_init(&k_full[s], 2);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::VST; ++s) {
+      mbar_init(&v_full[s], 2);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&o_done[s], 1);
+      mbar_init(&o_free[s], 16);
+      for (int u = 0; u < 4; ++u) mbar_init(&p_q[s * 4 + u], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 17) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 16) {
+    if (lane == 0) {
+      int jk = 0, jv = 0;  // running K / V block counters (ring slots and phases)
+      int n = 0;           // units done by this pair
+      AttnSched sc(items, nkb, npairs, cid, use_sk);
+      int it, j0, j1;
+      while (sc.next(it, j0, j1)) {
+        const int h = it / nqp, qp = (it - h * nqp) * 512;
+        if (n > 0) mbar_wait(q_empty, (n - 1) & 1);  // previous unit's QKs no longer read Q
+        if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * Cfg::Q_BYTES);
+        else mbar_arrive_cluster(q_full, 0);
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+            tma_load_3d_pair(sQ + t * Cfg::Q_BYTES + a * 2 * Cfg::ATOM, &tmQ, q_full, a * 64,
+                             qp + t * 256 + int(rank) * 128, h);
+        const int nb = j1 - j0;
+        const int k_end = jk + nb, v_end = jv + nb;
+        while (jv < v_end) {
+          if (jk < k_end && jk <= jv + 2) {
+            const int st = jk % Cfg::KST;
+            mbar_wait(&k_empty[st], ((jk / Cfg::KST) & 1) ^ 1);
+            if (leader) mbar_arrive_expect_tx(&k_full[st], 2 * Cfg::K_BYTES);
+            else mbar_arrive_cluster(&k_full[st], 0);
+            const int kb = j0 + jk - (k_end - nb);
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+              tma_load_3d_pair(sK + st * Cfg::K_BYTES + a * Cfg::ATOM, &tmK, &k_full[st], a * 64,
+                               kb * 128 + int(rank) * 64, h);
+            ++jk;
+          } else {
+            const int st = jv % Cfg::VST;
+            mbar_wait(&v_empty[st], ((jv / Cfg::VST) & 1) ^ 1);
+            if (leader) mbar_arrive_expect_tx(&v_full[st], 2 * Cfg::V_BYTES);
+            else mbar_arrive_cluster(&v_full[st], 0);
+            const int vb = j0 + jv - (v_end - nb);
+            tma_load_3d_pair(sV + st * Cfg::V_BYTES, &tmV, &v_full[st], int(rank) * 64, vb * 128, h);
+            ++jv;
+          }
+        }
+        ++n;
+      }
+    }
+  } else if (warp == 17) {
+    if (leader) {  // whole warp runs the schedule; one elected lane issues each MMA batch
+      constexpr uint32_t idesc_qk = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(256, DH, false, true);
+      const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(sV), Cfg::V_BYTES, 1024);
+      auto issue_qk = [&](int t, int jg) {
+        const uint64_t a0 = dq + uint64_t((t * Cfg::Q_BYTES) >> 4);
+        const uint64_t b0 = dk + uint64_t(((jg % Cfg::KST) * Cfg::K_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k)
+            tc_mma_bf16_pair(tmem + t * 128, a0 + uint64_t(((k >> 2) * 2 * Cfg::ATOM + (k & 3) * 32) >> 4),
+                             b0 + uint64_t(((k >> 2) * Cfg::ATOM + (k & 3) * 32) >> 4), idesc_qk, k > 0);
+          tc_commit_pair(&s_full[t], 0x3);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int jg, int u, bool first) {
+        const uint64_t b0 = dv + uint64_t(((jg % Cfg::VST) * Cfg::V_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int k = 2 * u + kk;
+            tc_mma_bf16_ts_pair(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, b0 + uint64_t((k * 2048) >> 4),
+                                idesc_pv, !(first && kk == 0));
+          }
+        }
+        __syncwarp();
+      };
+      auto commit1 = [&](uint64_t* bar) {
+        if (elect_one()) tc_commit_pair(bar, 0x3);
+        __syncwarp();
+      };
+      auto wait_k = [&](int jg) {
+        mbar_wait(&k_full[jg % Cfg::KST], (jg / Cfg::KST) & 1);
+        tc_fence_after();
+      };
+      int g = 0;  // running key-block counter (ring slots, S/P phases)
+      int n = 0;
+      AttnSched sc(items, nkb, npairs, cid, use_sk);
+      int it, j0, j1;
+      while (sc.next(it, j0, j1)) {
+        const int nb = j1 - j0;
+        auto pv_tile = [&](int t, int j) {
+          const int jg = g + j;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int u = (m >> 1) | ((m & 1) << 1);  // quarters 0, 2, 1, 3
+            mbar_wait(&p_q[t * 4 + u], jg & 1);
+            tc_fence_after();
+            issue_pv(t, jg, u, j == 0 && m == 0);
+          }
+          if (elect_one()) {
+            if (t == 1) tc_commit_pair(&v_empty[jg % Cfg::VST], 0x3);
+            if (j == nb - 1) tc_commit_pair(&o_done[t], 0x3);
+          }
+          __syncwarp();
+        };
+        mbar_wait(q_full, n & 1);
+        wait_k(g);
+        issue_qk(0, g);
+        issue_qk(1, g);
+        commit1(&k_empty[g % Cfg::KST]);
+        if (nb == 1) commit1(q_empty);
+        for (int j = 0; j < nb; ++j) {
+          const bool more = j + 1 < nb;
+          mbar_wait(&v_full[(g + j) % Cfg::VST], ((g + j) / Cfg::VST) & 1);
+          if (j == 0 && n > 0) {  // O_0 of the previous unit has been read out
+            mbar_wait(&o_free[0], (n - 1) & 1);
+            tc_fence_after();
+          }
+          pv_tile(0, j);
+          if (more) {
+            wait_k(g + j + 1);
+            issue_qk(0, g + j + 1);
+          }
+          if (j == 0 && n > 0) {
+            mbar_wait(&o_free[1], (n - 1) & 1);
+            tc_fence_after();
+          }
+          pv_tile(1, j);
+          if (more) {
+            issue_qk(1, g + j + 1);
+            commit1(&k_empty[(g + j + 1) % Cfg::KST]);
+            if (j + 2 == nb) commit1(q_empty);  // the unit's last QK is issued: Q may be reloaded
+          }
+        }
+        g += nb;
+        ++n;
+      }
+    }
+  } else {
+    const int t = warp >> 3;              // Q tile
+    const int hc = (warp >> 2) & 1;       // key / output column half
+    const int ew = warp & 3;              // TMEM lane quarter
+    const int r = ew * 32 + lane;         // query row within this CTA's half of the tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const uint32_t ts = tmem + lane_off + t * 128;
+    const uint32_t to = tmem + lane_off + Cfg::O_COL + t * DH + 64 * hc;
+    const uint32_t red_own = smem_u32(red + (t * 2 + hc) * 128 + r);
+    const uint32_t red_oth = smem_u32(red + (t * 2 + (hc ^ 1)) * 128 + r);
+    const uint32_t lred_own = smem_u32(lred + (t * 2 + hc) * 128 + r);
+    const uint32_t lred_oth = smem_u32(lred + (t * 2 + (hc ^ 1)) * 128 + r);
+    int g = 0, n = 0;
+    AttnSched sc(items, nkb, npairs, cid, use_sk);
+    int it, j0, j1;
+    while (sc.next(it, j0, j1)) {
+      const int nb = j1 - j0;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nb; ++j) {
+        const int jg = g + j;
+        mbar_wait(&s_full[t], jg & 1);
+        tc_fence_after();
+        float s[64];
+        tmem_ld32(ts + 64 * hc, s);
+        tmem_ld32(ts + 64 * hc + 32, s + 32);
+        tc_wait_ld();
+        const int valid = Nk - (j0 + j) * 128 - 64 * hc;
+        if (valid < 64) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i >= valid) s[i] = -INFINITY;
+        }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int i = 0; i < 64; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], fmaxf(s[i + 2 * u], s[i + 2 * u + 1]));
+        }
+        const float mloc = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+        sts_f32(red_own, mloc);
+        named_bar_sync(1 + t, 256);
+        const float mx = fmaxf(mloc, lds_f32(red_oth));
+        const bool need = mx > m_used + 8.0f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? mx : m_used;
+          if (j > 0) {
+            const float alpha = exp2f(m_used - m_new);
+            l *= alpha;
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 16) {
+              float o[16];
+              tmem_ld16(to + c, o);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] *= alpha;
+              tmem_st16(to + c, reinterpret_cast<uint32_t*>(o));
+            }
+          }
+          m_used = m_new;
+        }
+        float2 lsum2 = make_float2(0.f, 0.f);
+        const float2 sc2 = make_float2(scale_log2, scale_log2);
+        const float2 nm2 = make_float2(-m_used, -m_used);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2), i, lsum2);
+        tmem_st16(ts + 32 * hc, pk);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[32 + 2 * i], s[32 + 2 * i + 1]), sc2, nm2), i, lsum2);
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&p_q[t * 4 + 2 * hc], 0);
+        tmem_st16(ts + 32 * hc + 16, pk);
+        l += lsum2.x + lsum2.y;
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&p_q[t * 4 + 2 * hc + 1], 0);
+      }
+      mbar_wait(&o_done[t], n & 1);
+      tc_fence_after();
+      if (use_sk && j1 < nkb) {
+        // head unit: publish the unnormalised O (column-major slot: one coalesced 128 B row of
+        // lanes per column), the max in use and this half's row sum; the next pair finishes
+        float* slot = sk.ws + size_t(cid * 2 + int(rank)) * SK_SLOT;
+        float* po = slot + ((t * 2 + hc) * 64) * 128 + r;
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 32) {
+          float o[32];
+          tmem_ld32(to + c, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) __stcg(po + (c + i) * 128, o[i]);
+        }
+        if (hc == 0) __stcg(slot + 2 * 2 * 64 * 128 + t * 128 + r, m_used);
+        __stcg(slot + 2 * 2 * 64 * 128 + 2 * 128 + (t * 2 + hc) * 128 + r, l);
+        __threadfence();
+        named_bar_sync(3, 512);  // all 16 softmax warps of this CTA have published
+        if (warp == 0 && lane == 0) st_release_u32_attn(sk.flag + cid * 2 + int(rank), sk.epoch);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&o_free[t], 0);
+        g += nb;
+        ++n;
+        continue;
+      }
+      float sa = 0.f, sb = 1.f;
+      const float* pa = nullptr;
+      if (use_sk && j0 > 0) {
+        // tail unit: merge the previous pair's head partial of this item (same rows: same rank)
+        const float* slot = sk.ws + size_t((cid - 1) * 2 + int(rank)) * SK_SLOT;
+        if (lane == 0)
+          while (ld_acquire_u32_attn(sk.flag + (cid - 1) * 2 + int(rank)) != sk.epoch) __nanosleep(100);
+        __syncwarp();
+        const float ma = __ldcg(slot + 2 * 2 * 64 * 128 + t * 128 + r);
+        const float la = __ldcg(slot + 2 * 2 * 64 * 128 + 2 * 128 + (t * 2 + hc) * 128 + r);
+        const float m = fmaxf(ma, m_used);  // both factors <= 1
+        sa = exp2f(ma - m);
+        sb = exp2f(m_used - m);
+        l = la * sa + l * sb;
+        pa = slot + ((t * 2 + hc) * 64) * 128 + r;
+      }
+      sts_f32(lred_own, l);
+      named_bar_sync(1 + t, 256);
+      const float inv = 1.0f / (l + lds_f32(lred_oth));
+      const int h = it / nqp, qp = (it - h * nqp) * 512;
+      const int q = qp + t * 256 + int(rank) * 128 + r;
+      const int hb = h / Hs, hl = h - hb * Hs;
+      bf16* orow = O + (size_t(hb) * Nq + q) * Hs * dh_real + size_t(hl) * dh_real + 64 * hc;
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        float o[32];
+        tmem_ld32(to + c, o);
+        tc_wait_ld();
+        if (pa) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __ldcg(pa + (c + i) * 128) * sa + o[i] * sb;
+        }
+        if (q < Nq) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= inv;
+          store_vec<32>(orow + c, o);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&o_free[t], 0);  // O_t may be overwritten by the next unit
+      g += nb;
+      ++n;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 17) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+template <int EXPM>
+static cudaError_t launch_attn_ppsk(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
+                                  float scale, cudaStream_t st, int hs, float* sk_ws, unsigned* sk_flag) {
+  using Cfg = AttnPairCfg;
+  constexpr int SMEM = Cfg::OFF_BAR + 512 + 4096 + 1024;
+  static_assert(SMEM <= 232448, "attn_ppsk shared memory");
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
+      !make_tmap_3d(&tv, V, H, Nk, 128, 128))
+    return cudaErrorInvalidValue;
+  auto kern = attn_ppsk_kernel<EXPM>;
+  static int max_pairs = 0;
+  if (!max_pairs) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(ATTN3_THREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / 2;
+    }
+    max_pairs = n < num_sms() / 2 ? n : num_sms() / 2;
+  }
+  const int items = ((Nq + 511) / 512) * H;
+  const int nkb = (Nk + 127) / 128;
+  const int pairs = items < max_pairs ? items : max_pairs;
+  dim3 grid(2 * pairs);
+  // stream-K when whole items would leave > 8 % of the pairs idle on the last round and
+  // every pair's share spans at least one whole item (DF_ATTN_SK=0 turns it off)
+  static const int sk_env = [] {
+    const char* e = getenv("DF_ATTN_SK");
+    return e ? atoi(e) : 1;
+  }();
+  AttnSK sk = {nullptr, nullptr, 0};
+  const int rounds = (items + pairs - 1) / pairs;
+  if (sk_env && sk_ws && sk_flag && items > pairs && items % pairs && nkb >= 8 &&
+      double(items) / (double(rounds) * pairs) < 0.92) {
+    static std::atomic<unsigned> epoch{0};
+    sk.ws = sk_ws;
+    sk.flag = sk_flag;
+    sk.epoch = ++epoch;
+    if (sk.epoch == 0) sk.epoch = ++epoch;
+  }
+  float sl2 = scale * 1.4426950408889634f;
+  void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,  (void*)&Nq,
+                  (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs, (void*)&sk};
+  return launch_ex((const void*)kern, grid, dim3(ATTN3_THREADS), SMEM, st, args);
+}
+
 template <int EXPM>
 static cudaError_t launch_attn_pair3(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk,
                                      int dh, float scale, cudaStream_t st, int hs) {
@@ -1909,7 +2411,7 @@ static cudaError_t launch_attn_pair(const bf16* Q, const bf16* K, const bf16* V,
 
 template <int DH>
 static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
-                               float scale, cudaStream_t st, int hs) {
+                               float scale, cudaStream_t st, int hs, float* sk_ws, unsigned* sk_flag) {
   if constexpr (DH == 128) {
     if (g_attn_impl == 3) {
       static const int poly = [] {
@@ -1921,6 +2423,14 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
     }
   }
   if constexpr (DH == 128) {
+    if (g_attn_impl == 7 && dh == 128) {  // persistent + stream-K split of ragged rounds
+      static const int poly = [] {
+        const char* e = getenv("DF_ATTN_POLY");
+        return e ? atoi(e) : 2;
+      }();
+      return poly == 0 ? launch_attn_ppsk<0>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs, sk_ws, sk_flag)
+                       : launch_attn_ppsk<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs, sk_ws, sk_flag);
+    }
     if (g_attn_impl == 6 && dh == 128) {
       static const int poly = [] {
         const char* e = getenv("DF_ATTN_POLY");
@@ -2000,12 +2510,13 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
 }
 
 cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
-                    float scale, cudaStream_t st, int heads_per_sample) {
+                    float scale, cudaStream_t st, int heads_per_sample, float* sk_ws, unsigned* sk_flag) {
   static const int impl_env = [] {
     // 1: one Q tile per CTA (round-1 kernel); 2: two Q tiles, one softmax thread per row;
     // 3: CTA pair (cta_group::2); 4: two Q tiles, two softmax threads per row;
     // 5: CTA pair, two softmax threads per row; 6 (default): 5 made persistent over work
-    // items (4-6: dh = 128; other head sizes take 2)
+    // items; 7: 6 with the stream-K split of ragged rounds (4-7: dh = 128; other head sizes
+    // take 2)
     const char* e = getenv("DF_ATTN_IMPL");
     return e ? atoi(e) : 6;
   }();
@@ -2013,8 +2524,8 @@ cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H,
   const int hs = heads_per_sample > 0 ? heads_per_sample : H;
   if (Nq <= 0) return cudaSuccess;
   if (Nk <= 0 || dh > dh_pad || H % hs) return cudaErrorInvalidValue;
-  if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
-  if (dh_pad == 128) return launch_attn<128>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+  if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs, nullptr, nullptr);
+  if (dh_pad == 128) return launch_attn<128>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs, sk_ws, sk_flag);
   return cudaErrorInvalidValue;
 }
 

@@ -1918,8 +1918,17 @@ df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void*
                           int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream) {
   if (!ctx || !Q || !K || !V || !O) return DF_ERR_INVALID;
   g_launches->fetch_add(1);
+  // the first T instance's attention stream-K workspace (taken only for ragged rounds)
+  float* skw = nullptr;
+  unsigned* skf = nullptr;
+  for (auto& ip : ctx->inst)
+    if (ip->stage == DF_T && ip->m.attn_sk_ws) {
+      skw = ip->m.attn_sk_ws;
+      skf = ip->m.attn_sk_flag;
+      break;
+    }
   cudaError_t r = attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, H, Nq, Nk, dh, dh_pad, scale,
-                          (cudaStream_t)stream);
+                          (cudaStream_t)stream, 0, skw, skf);
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_attention: ") + cudaGetErrorString(r));
 }
 

@@ -155,7 +155,7 @@ def test_payload_hash_equals_oracle(tiny_ctx, nbytes):
     assert tiny_ctx.payload_hash(0, t, nbytes) == cap.payload_hash(buf)
 
 
-@pytest.mark.parametrize("impl", ["1", "2", "3", "4", "5"])
+@pytest.mark.parametrize("impl", ["1", "2", "3", "4", "5", "7"])
 def test_attention_kernel_variants(impl):
     """The non-default attention kernels (1: one Q tile per CTA; 2: two Q tiles, one softmax thread per row; 3: CTA pair,
     one softmax thread per row; 4: two Q tiles, two softmax threads per row; 5: CTA pair, two softmax threads per row,
@@ -168,5 +168,29 @@ def test_attention_kernel_variants(impl):
     env = dict(os.environ, DF_ATTN_IMPL=impl)
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_kernels.py"), "-q", "-x",
-                        "-k", "bruteforce or special_cases"], env=env, capture_output=True, text=True, timeout=600)
+                        "-k", "bruteforce or special_cases or stream_k"], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_attention_stream_k_ragged_rounds(tiny_ctx):
+    """A ragged last round (96 items of 512 queries on 74 CTA pairs) against fp64 softmax on
+    sampled rows, bit-identical across runs; under DF_ATTN_IMPL=7 (child run of the variants
+    test) this is the stream-K split, items cut between pairs merged from (O, m, l) partials."""
+    H, Nq, Nk, dh = 12, 4096, 4096, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Q = (torch.randn(H, Nq, dh, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    K = (torch.randn(H, Nk, dh, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    V = torch.randn(H, Nk, dh, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for _ in range(2):
+        O = torch.zeros((Nq, H * dh), device="cuda", dtype=torch.bfloat16)
+        tiny_ctx.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, 1.0 / math.sqrt(dh))
+        torch.cuda.synchronize()
+        outs.append(O.clone())
+    assert torch.equal(outs[0], outs[1])
+    rows = np.unique(np.concatenate([np.arange(0, Nq, 97), np.arange(Nq - 8, Nq)]))
+    qd = Q.float().cpu().numpy().astype(np.float64)[:, rows]
+    kd, vd = (t.float().cpu().numpy().astype(np.float64) for t in (K, V))
+    want = dit.softmax_attention(qd, kd, vd).transpose(1, 0, 2).reshape(len(rows), H * dh)
+    got = outs[0].float().cpu().numpy()[rows]
+    assert rel_l2(got, want) < 1e-2
