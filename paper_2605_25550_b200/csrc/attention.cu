@@ -1,3 +1,4 @@
+#include <cstring>
 #include <atomic>
 // Self- and cross-attention of the DiT block (PAPER.md P:L118
 // "attention is O(T^2 D)"): O_h = softmax(Q_h K_h^T / sqrt(dh)) V_h, no mask, fp32
@@ -1888,10 +1889,16 @@ DF_DEV unsigned ld_acquire_u32_attn(const unsigned* p) {
 // (fp32) in its workspace slot with an epoch flag; its tail unit then waits for slot
 // p - 1, merges O = O_a 2^(m_a - m) + O_b 2^(m_b - m) (m = max), l likewise, and
 // normalises.  The split points depend only on the shape and the pair count: deterministic.
+constexpr int SK_MAX_PAIRS = 80;
 struct AttnSK {
   float* ws;          // [pairs][2 CTAs] slots of SK_SLOT floats
   unsigned* flag;     // [pairs][2 CTAs] epochs
   unsigned epoch;
+  // per-pair schedule computed on the host (kernel parameters are read with uniform loads,
+  // so the MMA warp's unit loop stays in uniform registers): head item / block count, tail
+  // item / first block, whole items [full0, full1)
+  short hd_it[SK_MAX_PAIRS], hd_k[SK_MAX_PAIRS], tl_it[SK_MAX_PAIRS], tl_k[SK_MAX_PAIRS];
+  short full0[SK_MAX_PAIRS], full1[SK_MAX_PAIRS];
 };
 constexpr int SK_SLOT = 2 * 2 * 64 * 128 + 2 * 128 + 2 * 2 * 128;  // O [t][hc][64][128], m [t][128], l [t][hc][128]
 
@@ -1901,18 +1908,14 @@ struct AttnSched {
   int tl_it, tl_k;        // stream-K tail unit: item, first block (0 = none)
   int full0, full1;       // whole items [full0, full1) in steps of `step`
   int state;              // 0: head next, 1: tail next, 2: whole items
-  DF_DEV AttnSched(int items, int nkb_, int npairs, int cid, bool sk)
-      : nkb(nkb_), step(sk ? 1 : npairs), hd_it(0), hd_k(0), tl_it(0), tl_k(0), full0(cid), full1(items),
-        state(sk ? 0 : 2) {
-    if (!sk) return;
-    const long long total = (long long)items * nkb;
-    const long long b = total * cid / npairs, e = total * (cid + 1) / npairs;
-    const int ta = int(b / nkb), ka = int(b % nkb);
-    const int tb = int(e / nkb), kb = int(e % nkb);
-    full0 = ka ? ta + 1 : ta;
-    full1 = tb;
-    hd_it = tb, hd_k = kb;  // head: first kb blocks of item tb (published for pair cid + 1)
-    tl_it = ta, tl_k = ka;  // tail: blocks [ka, nkb) of item ta (merged with pair cid - 1's head)
+  DF_DEV AttnSched(int items, int nkb_, int npairs, int cid, const AttnSK& sk)
+      : nkb(nkb_), step(npairs), hd_it(0), hd_k(0), tl_it(0), tl_k(0), full0(cid), full1(items), state(2) {
+    if (!sk.ws) return;
+    step = 1;
+    state = 0;
+    hd_it = sk.hd_it[cid], hd_k = sk.hd_k[cid];
+    tl_it = sk.tl_it[cid], tl_k = sk.tl_k[cid];
+    full0 = sk.full0[cid], full1 = sk.full1[cid];
   }
   DF_DEV bool next(int& it, int& j0, int& j1) {
     if (state == 0) {
@@ -2009,7 +2012,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     if (lane == 0) {
       int jk = 0, jv = 0;  // running K / V block counters (ring slots and phases)
       int n = 0;           // units done by this pair
-      AttnSched sc(items, nkb, npairs, cid, use_sk);
+      AttnSched sc(items, nkb, npairs, cid, sk);
       int it, j0, j1;
       while (sc.next(it, j0, j1)) {
         const int h = it / nqp, qp = (it - h * nqp) * 512;
@@ -2090,12 +2093,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       };
       int g = 0;  // running key-block counter (ring slots, S/P phases)
       int n = 0;
-      AttnSched sc(items, nkb, npairs, cid, use_sk);
+      AttnSched sc(items, nkb, npairs, cid, sk);
       int it, j0, j1;
       while (sc.next(it, j0, j1)) {
         const int nb = j1 - j0;
-        auto pv_tile = [&](int t, int j) {
-          const int jg = g + j;
+        auto pv_tile = [&](int t, int j, int nb_, int g_) {
+          const int jg = g_ + j;
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
             const int u = (m >> 1) | ((m & 1) << 1);  // quarters 0, 2, 1, 3
@@ -2105,7 +2108,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
           }
           if (elect_one()) {
             if (t == 1) tc_commit_pair(&v_empty[jg % Cfg::VST], 0x3);
-            if (j == nb - 1) tc_commit_pair(&o_done[t], 0x3);
+            if (j == nb_ - 1) tc_commit_pair(&o_done[t], 0x3);
           }
           __syncwarp();
         };
@@ -2122,7 +2125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
             mbar_wait(&o_free[0], (n - 1) & 1);
             tc_fence_after();
           }
-          pv_tile(0, j);
+          pv_tile(0, j, nb, g);
           if (more) {
             wait_k(g + j + 1);
             issue_qk(0, g + j + 1);
@@ -2131,7 +2134,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
             mbar_wait(&o_free[1], (n - 1) & 1);
             tc_fence_after();
           }
-          pv_tile(1, j);
+          pv_tile(1, j, nb, g);
           if (more) {
             issue_qk(1, g + j + 1);
             commit1(&k_empty[(g + j + 1) % Cfg::KST]);
@@ -2155,7 +2158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     const uint32_t lred_own = smem_u32(lred + (t * 2 + hc) * 128 + r);
     const uint32_t lred_oth = smem_u32(lred + (t * 2 + (hc ^ 1)) * 128 + r);
     int g = 0, n = 0;
-    AttnSched sc(items, nkb, npairs, cid, use_sk);
+    AttnSched sc(items, nkb, npairs, cid, sk);
     int it, j0, j1;
     while (sc.next(it, j0, j1)) {
       const int nb = j1 - j0;
@@ -2347,15 +2350,24 @@ static cudaError_t launch_attn_ppsk(const bf16* Q, const bf16* K, const bf16* V,
     const char* e = getenv("DF_ATTN_SK");
     return e ? atoi(e) : 1;
   }();
-  AttnSK sk = {nullptr, nullptr, 0};
+  AttnSK sk;
+  std::memset(&sk, 0, sizeof(sk));
   const int rounds = (items + pairs - 1) / pairs;
-  if (sk_env && sk_ws && sk_flag && items > pairs && items % pairs && nkb >= 8 &&
-      double(items) / (double(rounds) * pairs) < 0.92) {
+  if (sk_env && sk_ws && sk_flag && items > pairs && items % pairs && nkb >= 8 && pairs <= SK_MAX_PAIRS &&
+      items < 32768 && double(items) / (double(rounds) * pairs) < 0.92) {
     static std::atomic<unsigned> epoch{0};
     sk.ws = sk_ws;
     sk.flag = sk_flag;
     sk.epoch = ++epoch;
     if (sk.epoch == 0) sk.epoch = ++epoch;
+    const long long total = (long long)items * nkb;
+    for (int p = 0; p < pairs; ++p) {  // equal contiguous ranges of items x key blocks
+      const long long b = total * p / pairs, e = total * (p + 1) / pairs;
+      const int ta = int(b / nkb), ka = int(b % nkb), tb = int(e / nkb), kb = int(e % nkb);
+      sk.hd_it[p] = short(tb), sk.hd_k[p] = short(kb);
+      sk.tl_it[p] = short(ta), sk.tl_k[p] = short(ka);
+      sk.full0[p] = short(ka ? ta + 1 : ta), sk.full1[p] = short(tb);
+    }
   }
   float sl2 = scale * 1.4426950408889634f;
   void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,  (void*)&Nq,
