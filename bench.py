@@ -250,7 +250,9 @@ def run_ours(args, cfg):
     run_batch(args.warmup * n_t, 1000)
     barrier()
     # ---- timed region (inputs device-resident: tokens and noise from seeds on the device)
-    ctx.profile(True, True)
+    # per-kernel CUDA events on every 4th denoising step of the timed region (every step's
+    # ~300 event pairs would otherwise add their own GPU commands to the measured time)
+    ctx.profile(4, True)
     l0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:

@@ -234,7 +234,9 @@ df_status df_op_rmsnorm_mod(df_ctx* ctx, const float* x, void* out, int32_t M, i
  * enabled, every GEMM / attention / RMSNorm launch of the T instances is bracketed
  * by CUDA events on its own stream (no host sync on the launch path).  Kinds:
  * 0 QKV, 1 self-attn, 2 O-proj, 3 RMSNorm, 4 cross-Q, 5 cross-attn, 6 cross-O,
- * 7 MLP up (SwiGLU), 8 MLP down, 9 head+Euler, 10 patch embed. */
+ * 7 MLP up (SwiGLU), 8 MLP down, 9 head+Euler, 10 patch embed.  enable = n > 1 samples
+ * every n-th denoising step (each event pair is a GPU command between two kernels; the
+ * unsampled steps run exactly as with profiling off). */
 df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset);
 df_status df_kernel_stats(df_ctx* ctx, uint32_t kind, uint64_t* launches, double* total_ms, double* flops,
                           double* bytes);

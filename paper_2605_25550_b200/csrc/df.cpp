@@ -1355,7 +1355,10 @@ df_status df_ring_selftest(const char* name, int32_t role, uint64_t n, uint64_t*
 df_status df_profile(df_ctx* ctx, int32_t enable, int32_t reset) {
   if (!ctx) return DF_ERR_INVALID;
   for (auto& ip : ctx->inst)
-    if (ip->stage == DF_T) ip->m.prof = enable ? &ctx->prof : nullptr;
+    if (ip->stage == DF_T) {
+      ip->m.prof = enable ? &ctx->prof : nullptr;
+      ip->m.prof_every = enable > 1 ? enable : 1;
+    }
   if (reset) ctx->prof.reset();
   // one video request launches ~22k kernels (two events each) between
   // harvests; creating events inside the timed region would put cudaEventCreate on the

@@ -622,6 +622,13 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
 
 // ------------------------------------------------------------------ one step (a2-a12)
 cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStream_t st) {
+  if (prof && prof_every > 1 && i % prof_every) {  // sampled profiling: this step runs unbracketed
+    Prof* p = prof;
+    prof = nullptr;
+    cudaError_t e = step(cd, i, x, v_out, st);
+    prof = p;
+    return e;
+  }
   const int d = c.d, B = cd.B, M = B * N;
   const int of = f32() ? 1 : 0;
   DF_L(modulations(cd.e6 + size_t(i) * 6 * d, cd.e + size_t(i) * d, layer_mods.data(), c.layers, head_mod, d, mods,

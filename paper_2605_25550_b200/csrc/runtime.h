@@ -146,6 +146,7 @@ struct Model {
   float* etmp = nullptr;    // [L, 2 f_e]
   std::vector<const bf16*> layer_mods;
   Prof* prof = nullptr;
+  int prof_every = 1;       // profile the launches of every prof_every-th denoising step
   int cur_kind = K_MISC;
   double cur_flops = 0, cur_bytes = 0;
 
