@@ -120,3 +120,33 @@ def test_jitter_delays_the_transfer_not_the_data():
         assert x.exposed_ms[0] >= 0.8 * d * 1e3, x.exposed_ms[0]
         assert x.hash_src[0] == x.hash_dst[0] != 0
         assert rel_l2(outs[x.user_tag], stages.request(P, cfg, seed=int(x.user_tag))["out"]) <= 3e-2
+
+
+def test_pipeline_soak_bit_identical_under_reordering():
+    """R18 under load: 32 requests (half with classifier-free guidance) through E x1, T x2,
+    D x1 with small chunks, submitted in two different orders (the second run with transfer
+    jitter) -> every request's decoded output is byte-identical across the runs; completions
+    conserve the submission set.  Exercises the T worker's enqueue-ahead pipelining, the
+    persistent conditioning arena reused across CFG and non-CFG requests, and slot reuse."""
+    cfg = MID
+    inst = [(0, B.DF_E), (0, B.DF_T), (0, B.DF_T), (0, B.DF_D)]
+    seeds = list(range(300, 332))
+    guid = {s: (3.0 if s % 2 else 1.0) for s in seeds}
+
+    def run(order, jitter):
+        outs = {s: np.zeros(cfg.out_shape, np.float32) for s in seeds}
+        with make_ctx(cfg, instances=inst, chunk_bytes=(4096, 16384), jitter=jitter) as c:
+            comps = []
+            for s in order:
+                while c.submit(3, 3.0, s, out_host=outs[s], user_tag=s, guidance=guid[s])[0] != B.DF_OK:
+                    comps += c.poll(16, 5)
+            while len(comps) < len(seeds):
+                comps += c.poll(16, 60000)
+        assert sorted(x.user_tag for x in comps) == seeds
+        assert all(x.hash_src[e] == x.hash_dst[e] != 0 for x in comps for e in range(2))
+        return outs
+
+    a = run(seeds, (0.0, 0.0, 0))
+    b = run(list(reversed(seeds)), (0.3, 0.004, 9))
+    for s in seeds:
+        assert np.array_equal(a[s], b[s]), s
