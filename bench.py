@@ -353,6 +353,10 @@ def run_ours(args, cfg):
         s = oracle_sample(cfg)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "oracle", "sample": s["sample"]}
     gE, gT, gD = layouts.ratio(inst)
+    # per-request payloads of the two edges (E->T: ctx [| clip | y]; T->D: the fp32 latent)
+    e2t_bytes = cfg.L_txt * cfg.d_txt * 2 + (((cfg.L_img * cfg.d_img * 2 + 15) // 16) * 16 +
+                                              cfg.C_y * cfg.F * cfg.H * cfg.W * 4 if cfg.C_y else 0)
+    t2d_bytes = cfg.latent_elems * 4
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / n_total, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -376,6 +380,9 @@ def run_ours(args, cfg):
                      "frac_of_burst_peak": dit_tflops / peaks["bf16"]},
         "handoff": {"exposed_ms_median": summary["exp_med"], "exposed_ms_max": summary["exp_max"],
                     "exposed_frac_of_latency": summary["exp_frac"], "xfer_ms_median": summary["xfer"],
+                    "payload_bytes": [e2t_bytes, t2d_bytes],
+                    "xfer_gbps": [e2t_bytes / max(summary["xfer"][0], 1e-9) / 1e6,
+                                  t2d_bytes / max(summary["xfer"][1], 1e-9) / 1e6],
                     "latency_ms_median": summary["lat"], "hash_match": summary["hash_ok"],
                     "dit_instances_used": summary["t_inst"]},
         "kernel_time_share": shares,
