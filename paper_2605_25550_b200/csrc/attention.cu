@@ -2448,8 +2448,11 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
         const char* e = getenv("DF_ATTN_POLY");
         return e ? atoi(e) : 2;
       }();
-      return poly == 0 ? launch_attn_pp<0>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs)
-                       : launch_attn_pp<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+      switch (poly) {  // DF_ATTN_POLY: share of exponentials on the FMA pipe (softmax_exp2)
+        case 0: return launch_attn_pp<0>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 1: return launch_attn_pp<1>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        default: return launch_attn_pp<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+      }
     }
     if (g_attn_impl == 5 && dh == 128) {
       static const int poly = [] {
