@@ -913,6 +913,7 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   MetaRec m;
+  Cond cd;  // persistent conditioning arena, reused in stream order (as in t_worker)
   while (mp_recv(ctx, me, m)) {
     const int S = int(m.steps);
     int b = me->xnext;
@@ -927,7 +928,6 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->payload(cfgr)));
     WK(cudaEventRecord(w0, me->compute));  // ctx landed
     std::vector<float> sig = sigmas_host(S, m.shift);
-    Cond cd;
     const void* cbuf = me->slots.slots[m.slot].buf;
     WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->neg_off() : nullptr,
                      cfgr ? m.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf)));
@@ -936,7 +936,6 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     WK(cudaEventRecord(t1, me->compute));
     WK(cudaStreamSynchronize(me->compute));
     if (me->m.prof) me->m.prof->harvest();
-    cd.mem.release();
     float ms = 0.f, ex = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
     cudaEventElapsedTime(&ex, r0, w0);
@@ -956,6 +955,8 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     WK(cudaEventRecord(me->xsent[b], me->comm));
     me->served++;
   }
+  cudaStreamSynchronize(me->compute);
+  cd.mem.release();
 }
 
 void mp_d_worker(df_ctx* ctx, Inst* me) {
