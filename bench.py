@@ -381,8 +381,9 @@ def run_ours(args, cfg):
         "handoff": {"exposed_ms_median": summary["exp_med"], "exposed_ms_max": summary["exp_max"],
                     "exposed_frac_of_latency": summary["exp_frac"], "xfer_ms_median": summary["xfer"],
                     "payload_bytes": [e2t_bytes, t2d_bytes],
-                    "xfer_gbps": [e2t_bytes / max(summary["xfer"][0], 1e-9) / 1e6,
-                                  t2d_bytes / max(summary["xfer"][1], 1e-9) / 1e6],
+                    # (the cross-process path does not time its copies: xfer_ms = -1 -> null)
+                    "xfer_gbps": [(e2t_bytes / summary["xfer"][0] / 1e6) if summary["xfer"][0] > 0 else None,
+                                  (t2d_bytes / summary["xfer"][1] / 1e6) if summary["xfer"][1] > 0 else None],
                     "latency_ms_median": summary["lat"], "hash_match": summary["hash_ok"],
                     "dit_instances_used": summary["t_inst"]},
         "kernel_time_share": shares,
