@@ -268,11 +268,99 @@ __global__ void __launch_bounds__(128, 8) rmsnorm_warp_kernel(const float* __res
   }
 }
 
+// Bulk-copy variant: one elected thread moves the CTA's 4 rows of x into shared memory with
+// cp.async.bulk (one mbarrier, no per-thread load instructions in flight), then each warp
+// reduces and normalises its row from shared memory.  DF_RMS_BULK=1 selects it (A/B).
+DF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+template <int VPT, typename OutT>
+__global__ void __launch_bounds__(128) rmsnorm_bulk_kernel(const float* __restrict__ x, OutT* __restrict__ out, int M,
+                                                          const float* __restrict__ shift,
+                                                          const float* __restrict__ scale,
+                                                          const bf16* __restrict__ gain, float eps) {
+  constexpr int d = 128 * VPT;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float4* rows = reinterpret_cast<float4*>(sm + 16);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row0 = blockIdx.x * 4;
+  const int nrows = min(4, M - row0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, uint32_t(nrows) * d * 4);
+    for (int r = 0; r < nrows; ++r) bulk_g2s(rows + r * (d / 4), x + size_t(row0 + r) * d, d * 4, bar);
+  }
+  __syncthreads();
+  if (w >= nrows) return;
+  mbar_wait(bar, 0);
+  const float4* xr = rows + w * (d / 4);
+  float ss = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < VPT; ++i) {
+    const float4 t = xr[lane + 32 * i];
+    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+  }
+  ss = warp_sum(ss);
+  const float inv = rsqrtf(ss / float(d) + eps);
+  OutT* orow = out + size_t(row0 + w) * d;
+#pragma unroll 8
+  for (int i = 0; i < VPT; ++i) {
+    const int c = lane + 32 * i;
+    const float4 t = xr[c];
+    float y[4] = {t.x * inv, t.y * inv, t.z * inv, t.w * inv};
+    if (gain) {
+      const uint2 g = reinterpret_cast<const uint2*>(gain)[c];
+      y[0] *= bf_lo(g.x), y[1] *= bf_hi(g.x), y[2] *= bf_lo(g.y), y[3] *= bf_hi(g.y);
+    } else {
+      const float4 sc = reinterpret_cast<const float4*>(scale)[c];
+      const float4 sh = reinterpret_cast<const float4*>(shift)[c];
+      y[0] = y[0] * (1.f + sc.x) + sh.x;
+      y[1] = y[1] * (1.f + sc.y) + sh.y;
+      y[2] = y[2] * (1.f + sc.z) + sh.z;
+      y[3] = y[3] * (1.f + sc.w) + sh.w;
+    }
+    if constexpr (sizeof(OutT) == 2) {
+      uint2 u;
+      u.x = pack_bf16x2(y[0], y[1]);
+      u.y = pack_bf16x2(y[2], y[3]);
+      reinterpret_cast<uint2*>(orow)[c] = u;
+    } else {
+      reinterpret_cast<float4*>(orow)[c] = make_float4(y[0], y[1], y[2], y[3]);
+    }
+  }
+}
+
 template <int VPT>
 static cudaError_t launch_rms_warp(const float* x, void* out, int out_f32, int M, const float* shift,
                                    const float* scale, const bf16* gain, float eps, cudaStream_t st) {
   void* args[] = {(void*)&x, (void*)&out, (void*)&M, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
   dim3 grid((M + 3) / 4);
+  static const int bulk = [] {
+    const char* e = getenv("DF_RMS_BULK");
+    return e ? atoi(e) : 0;
+  }();
+  if (bulk) {
+    const size_t smem = 16 + size_t(4) * 128 * VPT * 4;
+    const void* kern = out_f32 ? (const void*)rmsnorm_bulk_kernel<VPT, float> : (const void*)rmsnorm_bulk_kernel<VPT, bf16>;
+    static bool attr = false;
+    if (!attr) {  // both output types
+      cudaError_t e = cudaFuncSetAttribute((const void*)rmsnorm_bulk_kernel<VPT, float>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)rmsnorm_bulk_kernel<VPT, bf16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return launch_ex(kern, grid, dim3(128), smem, st, args);
+  }
   if (out_f32) return launch_ex((const void*)rmsnorm_warp_kernel<VPT, float>, grid, dim3(128), 0, st, args);
   return launch_ex((const void*)rmsnorm_warp_kernel<VPT, bf16>, grid, dim3(128), 0, st, args);
 }
