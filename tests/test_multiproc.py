@@ -86,3 +86,21 @@ def test_layouts():
     assert sum(L.ratio(inst)) <= 8                            # Eq. 1
     with pytest.raises(ValueError):
         L.partitioned(2, exclusive=True)
+
+
+def test_layouts_colocated_dit_instances():
+    """Several DiT instances per GPU (bench --t-per-gpu): every GPU gets t instances of T,
+    E stays on GPU 0 and D on the last GPU; ratios follow."""
+    from paper_2605_25550_b200 import layouts as L
+    from paper_2605_25550_b200.binding import DF_E, DF_T, DF_D
+    inst = L.partitioned(1, t_per_gpu=2)
+    assert L.ratio(inst) == (1, 2, 1) and all(i[2] == 0 for i in inst)
+    inst = L.partitioned(4, t_per_gpu=3)
+    assert L.ratio(inst) == (1, 12, 1)
+    assert sorted({i[2] for i in inst if i[1] == DF_T}) == [0, 1, 2, 3]
+    assert all(sum(1 for i in inst if i[1] == DF_T and i[2] == r) == 3 for r in range(4))
+    assert L.ranks_of(inst, DF_E) == [0] and L.ranks_of(inst, DF_D) == [3]
+    inst = L.partitioned(8, exclusive=True, t_per_gpu=2)
+    assert L.ratio(inst) == (1, 12, 1) and L.ranks_of(inst, DF_T) == list(range(1, 7))
+    with pytest.raises(ValueError):
+        L.partitioned(2, t_per_gpu=0)
