@@ -267,6 +267,52 @@ std::vector<float> sigmas_host(int S, float shift) {
 }
 
 // ---------------------------------------------------------------- handoff
+// Edges that draw injected jitter (bit 0: E->T, bit 1: T->D); DF_JITTER_EDGES narrows the
+// handoff-stress experiments to one edge (default both).
+static unsigned jitter_edges() {
+  static const unsigned m = [] {
+    const char* e = getenv("DF_JITTER_EDGES");
+    return e ? unsigned(atoi(e)) : 3u;
+  }();
+  return m;
+}
+
+void free_xfer(Xfer* x);
+
+// Mapped host slots for the payload hashes, a (src, dst) pair per transfer, pooled
+// process-wide (cudaHostAllocPortable: valid on every device).  A cudaHostAlloc/cudaFreeHost
+// pair per transfer costs an implicit device synchronisation in the polling thread, which
+// held the producer's enqueue behind any in-flight injected delay (the
+// handoff-stress point).  Blocks are never returned to the driver (4 KiB each).
+class HashPool {
+  std::mutex mu_;
+  std::vector<unsigned long long*> free_;
+
+ public:
+  unsigned long long* get() {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (free_.empty()) {
+      constexpr int kPairs = 256;
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, kPairs * 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) !=
+          cudaSuccess)
+        return nullptr;
+      for (int i = kPairs - 1; i >= 0; --i) free_.push_back(static_cast<unsigned long long*>(p) + 2 * i);
+    }
+    unsigned long long* p = free_.back();
+    free_.pop_back();
+    return p;
+  }
+  void put(unsigned long long* p) {
+    std::lock_guard<std::mutex> lk(mu_);
+    free_.push_back(p);
+  }
+};
+HashPool& hash_pool() {
+  static HashPool* pool = new HashPool;  // intentionally leaked: no CUDA calls at exit
+  return *pool;
+}
+
 df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_stream, Xfer** out) {
   if (!d || d->src_inst < 0 || d->dst_inst < 0 || d->src_inst >= int(ctx->inst.size()) ||
       d->dst_inst >= int(ctx->inst.size()) || !d->src || !d->dst || !d->bytes)
@@ -294,14 +340,18 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_str
   CK(ctx, cudaEventDestroy(ready));
   const bool hash = (d->flags & DF_HASH) != 0;
   if (hash) {
-    CK(ctx, cudaHostAlloc(&x->hash_dev, 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
+    x->hash_dev = hash_pool().get();
+    if (!x->hash_dev) {
+      free_xfer(x);
+      return fail(ctx, "df_handoff: cudaHostAlloc (hash slots) failed", DF_ERR_CUDA);
+    }
     x->hash_dev[0] = x->hash_dev[1] = 0;
     x->hashed = true;
     g_launches->fetch_add(1);
     CK(ctx, payload_hash(d->src, d->bytes, 0, x->hash_dev, S.comm));
   }
   // jitter: one Bernoulli draw per request-edge transfer (R23)
-  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f) {
+  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f && (jitter_edges() >> d->edge & 1u)) {
     uint32_t c[4] = {uint32_t(d->seq), uint32_t(d->seq >> 32), d->edge, 3u};
     philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
     if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0)
@@ -349,7 +399,7 @@ void free_xfer(Xfer* x) {
   if (x->t0) cudaEventDestroy(x->t0);
   if (x->t1) cudaEventDestroy(x->t1);
   if (x->t_hash) cudaEventDestroy(x->t_hash);
-  if (x->hash_dev) cudaFreeHost(x->hash_dev);
+  if (x->hash_dev) hash_pool().put(x->hash_dev);
   delete x;
 }
 
@@ -784,7 +834,7 @@ bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, uint64_t bytes, uin
   if (!chk(cudaStreamWaitEvent(me->comm, ready, 0), "wait")) return false;
   cudaEventDestroy(ready);
   if (!chk(cudaStreamWaitEvent(me->comm, v->consumed[s], 0), "wait consumed")) return false;
-  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f) {  // P:L142, R23
+  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f && (jitter_edges() >> edge & 1u)) {  // P:L142, R23
     uint32_t c[4] = {uint32_t(m.seq), uint32_t(m.seq >> 32), edge, 3u};
     philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
     if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0) {

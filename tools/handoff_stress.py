@@ -48,7 +48,7 @@ def run_once(cfg, steps, n_req, mode, chunk, jitter, seed0):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for k in range(n_req):
-            while c.submit(steps, cfg.shift, seed0 + k)[0] != B.DF_OK:
+            while c.submit(steps, cfg.shift, seed0 + k, user_tag=k)[0] != B.DF_OK:
                 time.sleep(0.001)
         comps = []
         while len(comps) < n_req:
@@ -61,7 +61,12 @@ def run_once(cfg, steps, n_req, mode, chunk, jitter, seed0):
             "exposed_ms_median": statistics.median(exp), "exposed_ms_mean": statistics.mean(exp),
             "exposed_frac_of_latency": statistics.mean(exp) / statistics.mean(lat),
             "latency_ms_p50": float(np.percentile(lat, 50)), "latency_ms_p99": float(np.percentile(lat, 99)),
-            "hash_match": all(x.hash_src[e] == x.hash_dst[e] != 0 for x in comps for e in range(2))}
+            "hash_match": all(x.hash_src[e] == x.hash_dst[e] != 0 for x in comps for e in range(2)),
+            "trace": [{"tag": x.user_tag, "submit": round(x.t_submit - t0, 4),
+                       "start": [round(x.t_start[k] - t0, 4) for k in range(3)],
+                       "end": [round(x.t_end[k] - t0, 4) for k in range(3)],
+                       "stage_ms": [round(v, 2) for v in x.stage_ms], "xfer_ms": [round(v, 2) for v in x.xfer_ms]}
+                      for x in sorted(comps, key=lambda x: x.t_end[1])]}
 
 
 def main():
@@ -72,6 +77,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/handoff_stress.json")
     ap.add_argument("--slots", type=int, default=2, help="receive slots per consumer per edge")
     ap.add_argument("--jitter-only", action="store_true", help="skip the chunk sweep (chunk 256 KiB)")
+    ap.add_argument("--stress-only", action="store_true", help="only the none / T_T/2 stress jitter points")
     a = ap.parse_args()
     global SLOTS
     SLOTS = a.slots
@@ -88,6 +94,8 @@ def main():
     d1, d2 = 0.2 * T_T / 74.1, 2.0 * T_T / 74.1
     pats = {"none": (0.0, 0.0), "stable 5%/d1": (0.05, d1), "mild 10%/d1": (0.10, d1),
             "moderate 10%/d2": (0.10, d2), "severe 20%/d2": (0.20, d2), "stress 20%/T_T/2": (0.20, T_T / 2)}
+    if a.stress_only:
+        pats = {k: pats[k] for k in ("none", "stress 20%/T_T/2")}
     res["T_T_s"], res["d1_s"], res["d2_s"] = T_T, d1, d2
     for name, (p, d) in pats.items():
         for mode, mname in ((B.DF_ASYNC, "async"), (B.DF_SYNC, "sync")):
