@@ -223,6 +223,18 @@ df_status df_weight_bits(df_ctx* ctx, int32_t inst, uint32_t tensor_id, uint16_t
  * SIMT (tc=0).  Device pointers; stream-ordered. */
 df_status df_op_gemm(df_ctx* ctx, const void* A, const void* W, float* out, int32_t M, int32_t N, int32_t K,
                      int32_t tc, void* stream);
+/* FP8 (P:L116 names quantisation as a serving optimisation, the paper fixes
+ * no format -- DESIGN.md R28): per-tensor e4m3 quantisation of n bf16 values x (device),
+ * s = amax|x| / 448 (1 if every x is 0), q[i] = e4m3 bits of RNE_satfinite(x[i] / s) with the
+ * division rounded in fp32.  q: n bytes (device); scale: one fp32 (device, overwritten).
+ * Three stream-ordered launches; DF_ERR_INVALID on null pointers. */
+df_status df_op_quant_e4m3(df_ctx* ctx, const void* x, uint64_t n, void* q, float* scale, void* stream);
+/* out[M,N] = sa * sb * (qa[M,K] . qb[N,K]^T): e4m3 operands (row-major, K contiguous,
+ * K % 16 == 0, M and N >= 256), scales sa/sb device fp32 pointers (as df_op_quant_e4m3 writes
+ * them), fp32 accumulation on the tensor cores (tcgen05 kind::f8f6f4, CTA pairs), out fp32
+ * (out_f32 = 1) or bf16, row stride N.  Device pointers; stream-ordered. */
+df_status df_op_gemm_e4m3(df_ctx* ctx, const void* qa, const void* qb, const float* sa, const float* sb, int32_t M,
+                          int32_t N, int32_t K, void* out, int32_t out_f32, void* stream);
 /* O[Nq, H*dh] = softmax(Q K^T * scale) V, head-major bf16 Q/K/V [H][N][dh_pad]. */
 df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t H, int32_t Nq,
                           int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream);

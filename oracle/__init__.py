@@ -24,4 +24,6 @@ Parity status per function (pins in tests/test_oracle_*.py):
                index check; encoder composition parity unpinned
   capacity.qps / plan  pinned: the paper's QPM points
   capacity.payload_hash pinned: splitmix64 published first output, chunk additivity
+  fp8 (NEXT-4, R28) pinned: E4M3 closed forms, 256-code round trip, ties-to-even,
+               saturation, torch float8_e4m3fn cast, brute-force GEMM
 """

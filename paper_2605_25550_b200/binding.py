@@ -116,6 +116,9 @@ _SIGS = {
                              C.c_int32, C.c_void_p]),
     "df_op_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p]),
+    "df_op_quant_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "df_op_gemm_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
     "df_launch_count": (C.c_uint64, [C.c_void_p]),
@@ -383,6 +386,18 @@ class Context:
         M, K = A.shape
         N = W.shape[0]
         self._ck(self.lib.df_op_gemm(self.h, _ptr(A), _ptr(W), _ptr(out), M, N, K, int(tc), _stream(stream)))
+
+    def op_quant_e4m3(self, x, q, scale, stream=None):
+        """x: bf16 (any shape, contiguous); q: uint8 of x.numel(); scale: fp32 [1] (device)."""
+        self._ck(self.lib.df_op_quant_e4m3(self.h, _ptr(x), int(x.numel()), _ptr(q), _ptr(scale), _stream(stream)))
+
+    def op_gemm_e4m3(self, qa, qb, sa, sb, out, stream=None):
+        """qa uint8 [M,K], qb uint8 [N,K], sa/sb fp32 [1] (device), out fp32 or bf16 [M,N]."""
+        M, K = qa.shape
+        N = qb.shape[0]
+        out_f32 = int(str(out.dtype) == "torch.float32")
+        self._ck(self.lib.df_op_gemm_e4m3(self.h, _ptr(qa), _ptr(qb), _ptr(sa), _ptr(sb), M, N, K, _ptr(out), out_f32,
+                                          _stream(stream)))
 
     def op_attention(self, Q, K, V, O, H, Nq, Nk, dh, dh_pad, scale, stream=None):
         self._ck(self.lib.df_op_attention(self.h, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), H, Nq, Nk, dh, dh_pad,

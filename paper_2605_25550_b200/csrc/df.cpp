@@ -1994,4 +1994,22 @@ df_status df_op_rmsnorm_mod(df_ctx* ctx, const float* x, void* out, int32_t M, i
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_rmsnorm_mod: ") + cudaGetErrorString(r));
 }
 
+df_status df_op_quant_e4m3(df_ctx* ctx, const void* x, uint64_t n, void* q, float* scale, void* stream) {
+  if (!ctx || (n && (!x || !q)) || !scale) return DF_ERR_INVALID;
+  g_launches->fetch_add(n ? 3 : 1);
+  cudaError_t r = quant_e4m3(static_cast<const bf16*>(x), size_t(n), static_cast<uint8_t*>(q), scale,
+                             (cudaStream_t)stream);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_quant_e4m3: ") + cudaGetErrorString(r));
+}
+
+df_status df_op_gemm_e4m3(df_ctx* ctx, const void* qa, const void* qb, const float* sa, const float* sb, int32_t M,
+                          int32_t N, int32_t K, void* out, int32_t out_f32, void* stream) {
+  if (!ctx || !qa || !qb || !sa || !sb || !out) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = gemm_e4m3(static_cast<const uint8_t*>(qa), static_cast<const uint8_t*>(qb), sa, sb, M, N, K, out, N,
+                            out_f32, (cudaStream_t)stream);
+  if (r == cudaErrorInvalidValue) return fail(ctx, "df_op_gemm_e4m3: unsupported shape", DF_ERR_INVALID);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_gemm_e4m3: ") + cudaGetErrorString(r));
+}
+
 }  // extern "C"

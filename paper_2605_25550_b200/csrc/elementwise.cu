@@ -8,6 +8,7 @@
 // traffic per row: 4d bytes read + 2d bytes written (bf16 out).
 #include <cmath>
 #include "kernels.h"
+#include <cuda_fp8.h>
 
 #include <atomic>
 #include <mutex>
@@ -647,6 +648,74 @@ static void CUDART_CB delay_host_fn(void* p) {
 cudaError_t delay_ns(uint64_t ns, cudaStream_t st) {
   if (ns == 0) return cudaSuccess;
   return cudaLaunchHostFunc(st, delay_host_fn, reinterpret_cast<void*>(uintptr_t(ns)));
+}
+
+// ---------------------------------------------------------------- e4m3 quantiser (NEXT-4)
+// Per-tensor current scaling (R28): s = amax|x| / 448 (1 when x == 0) and
+// q = RNE_satfinite_e4m3(x / s), the division correctly rounded in fp32, so x ~= s * q.
+// Three stream-ordered launches: amax (one atomicMax per warp on the float bits -- valid for
+// non-negative floats), the scale (one thread, in place), the quantisation (8 per thread).
+__global__ void __launch_bounds__(256) e4m3_amax_kernel(const bf16* __restrict__ x, size_t n, unsigned* amax) {
+  float m = 0.f;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  const size_t n8 = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / 8;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(x) + i);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      m = fmaxf(m, fabsf(__uint_as_float(w[k] << 16)));
+      m = fmaxf(m, fabsf(__uint_as_float(w[k] & 0xFFFF0000u)));
+    }
+  }
+  for (size_t i = n8 * 8 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    m = fmaxf(m, fabsf(bf2f(x[i])));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+}
+__global__ void e4m3_scale_kernel(float* s) {
+  const float a = __uint_as_float(*reinterpret_cast<const unsigned*>(s));
+  *s = a > 0.f ? __fdiv_rn(a, 448.f) : 1.f;
+}
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d, float s) {
+  const uint32_t q0 = __nv_cvt_float_to_fp8(__fdiv_rn(a, s), __NV_SATFINITE, __NV_E4M3);
+  const uint32_t q1 = __nv_cvt_float_to_fp8(__fdiv_rn(b, s), __NV_SATFINITE, __NV_E4M3);
+  const uint32_t q2 = __nv_cvt_float_to_fp8(__fdiv_rn(c, s), __NV_SATFINITE, __NV_E4M3);
+  const uint32_t q3 = __nv_cvt_float_to_fp8(__fdiv_rn(d, s), __NV_SATFINITE, __NV_E4M3);
+  return q0 | (q1 << 8) | (q2 << 16) | (q3 << 24);
+}
+__global__ void __launch_bounds__(256) e4m3_quant_kernel(const bf16* __restrict__ x, size_t n,
+                                                         const float* __restrict__ sp, uint8_t* __restrict__ q) {
+  const float s = __ldg(sp);
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  const bool vec = !((reinterpret_cast<uintptr_t>(x) & 15) | (reinterpret_cast<uintptr_t>(q) & 7));
+  const size_t n8 = vec ? n / 8 : 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(x) + i);
+    uint2 o;
+    o.x = e4m3x4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                 __uint_as_float(u.y & 0xFFFF0000u), s);
+    o.y = e4m3x4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u), __uint_as_float(u.w << 16),
+                 __uint_as_float(u.w & 0xFFFF0000u), s);
+    reinterpret_cast<uint2*>(q)[i] = o;
+  }
+  for (size_t i = n8 * 8 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    q[i] = uint8_t(__nv_cvt_float_to_fp8(__fdiv_rn(bf2f(x[i]), s), __NV_SATFINITE, __NV_E4M3));
+}
+cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaStream_t st) {
+  cudaError_t e0 = cudaMemsetAsync(scale, 0, sizeof(float), st);
+  if (e0 != cudaSuccess) return e0;
+  if (n == 0) {
+    e4m3_scale_kernel<<<1, 1, 0, st>>>(scale);
+    return cudaGetLastError();
+  }
+  const size_t per = 256 * 8;
+  const unsigned grid = unsigned(std::min<size_t>((n + per - 1) / per, size_t(num_sms()) * 8));
+  e4m3_amax_kernel<<<grid, 256, 0, st>>>(x, n, reinterpret_cast<unsigned*>(scale));
+  e4m3_scale_kernel<<<1, 1, 0, st>>>(scale);
+  e4m3_quant_kernel<<<grid, 256, 0, st>>>(x, n, scale, q);
+  return cudaGetLastError();
 }
 
 }  // namespace df

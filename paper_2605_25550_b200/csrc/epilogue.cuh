@@ -54,6 +54,9 @@ struct Epi {
   unsigned* sk_flag;
   unsigned sk_epoch;
   int sk_force;  // host: take stream-K whenever the tile count allows it (tests)
+  // FP8 (e4m3) operands (NEXT-4): device pointers to the per-tensor dequantisation scales of
+  // A and B; the accumulator is multiplied by *f8_scale[0] * *f8_scale[1] before the epilogue
+  const float* f8_scale[2];
 };
 
 DF_DEV float bias_at(const Epi& e, int n) { return e.bias ? bf2f(e.bias[n]) : 0.0f; }

@@ -383,7 +383,11 @@ DF_DEV unsigned ld_acquire_u32(const unsigned* p) {
 }
 DF_DEV void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 epilogue warps
 
-template <int CW, typename OutT, int TK>
+// F8: e4m3 operands (NEXT-4) -- a 128-byte swizzled row holds 128 k-elements instead of
+// 64, and an 8-bit MMA consumes 32 of them (32 bytes) per instruction, so the smem tiles,
+// descriptors and stage bytes are those of the bf16 kernel; only the k-block extent, the
+// MMA kind and the dequantisation scale in the epilogue change.
+template <int CW, typename OutT, int TK, bool F8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
@@ -407,7 +411,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   const int num_m = (M + 255) / 256;
   const int num_n = (N + 255) / 256;
   const int tiles = num_m * num_n;
-  const int KB = (K + GBK - 1) / GBK;
+  constexpr int BKE = F8 ? 128 : GBK;  // k-elements per 128-byte smem row
+  const int KB = (K + BKE - 1) / BKE;
   const int cid = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
   const bool sk = epi.sk_ws != nullptr;
@@ -447,8 +452,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
           else mbar_arrive_cluster(&full[stage], 0);
-          tma_load_2d_pair(sA + stage * P_A_BYTES, &tmA, &full[stage], kb * GBK, mb * 256 + rank * 128);
-          tma_load_2d_pair(sB + stage * P_B_BYTES, &tmB, &full[stage], kb * GBK, nb * 256 + rank * 128);
+          tma_load_2d_pair(sA + stage * P_A_BYTES, &tmA, &full[stage], kb * BKE, mb * 256 + rank * 128);
+          tma_load_2d_pair(sB + stage * P_B_BYTES, &tmB, &full[stage], kb * BKE, nb * 256 + rank * 128);
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -458,7 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader) {
-      constexpr uint32_t idesc = idesc_bf16(256, 256, false, false);
+      constexpr uint32_t idesc = F8 ? idesc_e4m3(256, 256) : idesc_bf16(256, 256, false, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -476,9 +481,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             const uint32_t a0 = smem_u32(sA + stage * P_A_BYTES);
             const uint32_t b0 = smem_u32(sB + stage * P_B_BYTES);
 #pragma unroll
-            for (int k = 0; k < GBK / 16; ++k)
-              tc_mma_bf16_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+            for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of each 128-byte row
+              if (F8)
+                tc_mma_f8_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                                (kb > k0 || k > 0));
+              else
+                tc_mma_bf16_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024),
+                                 idesc, (kb > k0 || k > 0));
+            }
             tc_commit_pair(&empty[stage], 0x3);
             if (kb == k1 - 1) tc_commit_pair(&tfull[acc], 0x3);
           }
@@ -550,6 +560,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < n; ++i) vv[i] += __ldcg(wfix + (col + i) * 128);
       };
+      const float f8a = F8 ? __ldg(epi.f8_scale[0]) * __ldg(epi.f8_scale[1]) : 1.f;  // dequantisation
+      auto f8_scale_acc = [&](float* vv, int n) {
+#pragma unroll
+        for (int i = 0; i < n; ++i) vv[i] *= f8a;
+      };
       if (TK != TK_DIRECT) {
         // per-column epilogue parameters of the tile, loaded once (coalesced) while the
         // accumulator is still being produced; read back as broadcast shared loads
@@ -600,6 +615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tmem_ld32(trow + c, v);
           tc_wait_ld();
           if (fix) fixup(v, c, 32);
+          if (F8) f8_scale_acc(v, 32);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             const float4 b4 = *reinterpret_cast<const float4*>(s_bias + c + i);
@@ -643,6 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tmem_ld32(trow + c + 32, w + 32);
           tc_wait_ld();
           if (fix) fixup(w, c, 64);
+          if (F8) f8_scale_acc(w, 64);
           uint8_t* buf = stage_acquire();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -805,10 +822,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   }
 }
 
-template <int CW, typename OutT, int TK>
+template <int CW, typename OutT, int TK, bool F8 = false>
 static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap* to, int M, int N, int K,
                               const Epi& epi, cudaStream_t st) {
-  auto kern = gemm_tc2_kernel<CW, OutT, TK>;
+  auto kern = gemm_tc2_kernel<CW, OutT, TK, F8>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
@@ -924,6 +941,43 @@ static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, in
   }
   return out_f32 ? launch_tc2<32, float, TK_DIRECT>(ta, tb, to, M, N, K, epi, st)
                  : launch_tc2<32, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+}
+
+// e4m3 x e4m3 GEMM (NEXT-4): out[M, N] = sa * sb * (qa[M, K] . qb[N, K]^T), fp32
+// accumulation in TMEM, fp32 or bf16 out through the TMA-store epilogue.  K-major 8-bit
+// operands; row strides K bytes (K % 16 == 0 for TMA); M, N >= 256 (CTA-pair tiles).
+cudaError_t gemm_e4m3(const uint8_t* qa, const uint8_t* qb, const float* sa, const float* sb, int M, int N, int K,
+                      void* out, int ldo, int out_f32, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if (K % 16 || M < 256 || N < 256 || !sa || !sb || !out || ldo < N) return cudaErrorInvalidValue;
+  if ((out_f32 && ldo % 4) || (!out_f32 && ldo % 8)) return cudaErrorInvalidValue;
+  CUtensorMap ta, tb, to[3];
+  std::memset(to, 0, sizeof(to));
+  const uint32_t box_q[2] = {128, 128};
+  const uint64_t da[2] = {uint64_t(K), uint64_t(M)}, db[2] = {uint64_t(K), uint64_t(N)}, sq[1] = {uint64_t(K)};
+  if (!make_tmap(&ta, qa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, da, sq, box_q)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tb, qb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, db, sq, box_q)) return cudaErrorInvalidValue;
+  Epi epi;
+  std::memset(&epi, 0, sizeof(epi));
+  epi.kind = EPI_STORE;
+  epi.M = M;
+  epi.N = N;
+  epi.act = ACT_NONE;
+  epi.out = out;
+  epi.ldo = ldo;
+  epi.f8_scale[0] = sa;
+  epi.f8_scale[1] = sb;
+  const uint64_t dims[2] = {uint64_t(N), uint64_t(M)};
+  if (out_f32) {
+    const uint32_t box[2] = {32, 32};
+    const uint64_t str[1] = {uint64_t(ldo) * 4};
+    if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box)) return cudaErrorInvalidValue;
+    return launch_tc2<32, float, TK_STORE_F32, true>(ta, tb, to, M, N, K, epi, st);
+  }
+  const uint32_t box[2] = {64, 32};
+  const uint64_t str[1] = {uint64_t(ldo) * 2};
+  if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box)) return cudaErrorInvalidValue;
+  return launch_tc2<32, bf16, TK_STORE_BF16, true>(ta, tb, to, M, N, K, epi, st);
 }
 
 template <int BN>

@@ -15,6 +15,10 @@ extern int g_disable_pair;  // 1: never use the CTA-pair GEMM (tests)
 
 // ---- tensor-core GEMM: out = epilogue(A[M,K] (bf16, row-major, lda) x W[N,K]^T (bf16, ldw)).
 // BN in {64, 128, 256}.  Returns cudaError_t of the launch.
+// e4m3 (NEXT-4): per-tensor quantiser (3 launches) and the CTA-pair e4m3 GEMM
+cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaStream_t st);
+cudaError_t gemm_e4m3(const uint8_t* qa, const uint8_t* qb, const float* sa, const float* sb, int M, int N, int K,
+                      void* out, int ldo, int out_f32, cudaStream_t st);
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& epi,
                     int out_f32, cudaStream_t st, int bn = 256);
 

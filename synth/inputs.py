@@ -67,3 +67,13 @@ def int_matrix(shape, lo: int, hi: int, seed: int) -> np.ndarray:
 
 def payload_bytes(nbytes: int, seed: int) -> np.ndarray:
     return rng(seed).integers(0, 256, size=nbytes, dtype=np.uint8)
+
+
+def activation_bf16(shape, seed: int, outlier_frac: float = 1e-3, outlier_scale: float = 24.0) -> np.ndarray:
+    """bf16 bits of an activation-like matrix: N(0,1) with a sparse set of large-magnitude
+    outliers (the channel outliers that make per-tensor FP8 scaling lossy, NEXT-4)."""
+    g = rng(seed)
+    a = g.standard_normal(shape, dtype=np.float32)
+    m = g.random(shape) < outlier_frac
+    a[m] *= np.float32(outlier_scale)
+    return f32_to_bf16_bits_trunc(a)

@@ -1,0 +1,81 @@
+"""NEXT-4 parity: the e4m3 quantiser (bit-exact codes and scale) and the CTA-pair e4m3
+GEMM (fp32-accumulation bound) against oracle/fp8.py, through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import fp8
+from synth import inputs
+from synth.configs import TINY
+from gpu_util import bf16_tensor_from_bits, make_ctx
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    with make_ctx(TINY) as c:
+        yield c
+
+
+def _quant_gpu(ctx, bits, offset=0):
+    x = bf16_tensor_from_bits(np.concatenate([np.zeros(offset, np.uint16), bits.reshape(-1)]))[offset:]
+    q = torch.full((bits.size + offset,), 0xAB, dtype=torch.uint8, device="cuda")[offset:]
+    s = torch.full((1,), float("nan"), device="cuda")
+    ctx.op_quant_e4m3(x, q, s)
+    torch.cuda.synchronize()
+    return q.cpu().numpy(), np.float32(s.item())
+
+
+@pytest.mark.parametrize("shape,offset", [((1,), 0), ((7,), 0), ((1000003,), 0), ((1000003,), 1), ((4096, 3072), 0),
+                                          ((512, 40), 3)])
+def test_quant_bit_exact(ctx, shape, offset):
+    bits = inputs.activation_bf16(shape, seed=int(np.prod(shape)) + offset)
+    q, s = _quant_gpu(ctx, bits, offset)
+    q_ref, s_ref = fp8.quantize_per_tensor(inputs.bf16_bits_to_f64(bits).astype(np.float32))
+    assert s == s_ref
+    assert np.array_equal(q, q_ref.reshape(-1))
+
+
+def test_quant_zero_tensor(ctx):
+    q, s = _quant_gpu(ctx, np.zeros(4099, np.uint16))
+    assert s == 1.0 and not q.any()
+
+
+def _gemm_case(ctx, M, N, K, out_dtype, seed):
+    a = inputs.bf16_bits_to_f64(inputs.activation_bf16((M, K), seed=seed)).astype(np.float32)
+    b = inputs.bf16_bits_to_f64(inputs.activation_bf16((N, K), seed=seed + 1, outlier_frac=0.0)).astype(np.float32)
+    qa, sa = fp8.quantize_per_tensor(a)
+    qb, sb = fp8.quantize_per_tensor(b)
+    want = fp8.gemm_e4m3(qa, qb, sa, sb)
+    bound = float(sa) * float(sb) * (np.abs(fp8.e4m3_decode(qa)) @ np.abs(fp8.e4m3_decode(qb)).T)
+    out = torch.full((M, N), float("nan"), dtype=out_dtype, device="cuda")
+    ctx.op_gemm_e4m3(torch.from_numpy(qa).cuda(), torch.from_numpy(qb).cuda(),
+                     torch.tensor([sa], device="cuda"), torch.tensor([sb], device="cuda"), out)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy().astype(np.float64), want, bound
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (512, 768, 3072), (300, 520, 208), (4096, 3072, 3072),
+                                   (4096, 12288, 3072), (4096, 3072, 8192)])
+def test_gemm_e4m3_fp32_out(ctx, M, N, K):
+    """Products of e4m3 values are exact in fp32; the only error is the fp32 accumulation
+    order (R28: |err| <= 2^-17 * sa sb sum|a||b|, K <= 8192)."""
+    got, want, bound = _gemm_case(ctx, M, N, K, torch.float32, seed=M + N + K)
+    assert np.all(np.isfinite(got))
+    print("fp8 gemm", M, N, K, "max |err|/bound = %.3g" % float(np.max(np.abs(got - want) / np.maximum(bound, 1e-300))))
+    assert np.all(np.abs(got - want) <= 2.0 ** -17 * bound + 1e-30)
+
+
+def test_gemm_e4m3_bf16_out(ctx):
+    got, want, bound = _gemm_case(ctx, 512, 512, 1024, torch.bfloat16, seed=9)
+    assert np.all(np.abs(got - want) <= 2.0 ** -8 * np.abs(want) + 2.0 ** -17 * bound + 1e-30)
+
+
+def test_gemm_e4m3_rejects_bad_shapes(ctx):
+    from paper_2605_25550_b200 import binding as B
+    q = torch.zeros((256, 200), dtype=torch.uint8, device="cuda")  # K % 16 != 0
+    s = torch.ones(1, device="cuda")
+    out = torch.empty((256, 256), device="cuda")
+    with pytest.raises(B.DFError):
+        ctx.op_gemm_e4m3(q, torch.zeros((256, 200), dtype=torch.uint8, device="cuda"), s, s, out)

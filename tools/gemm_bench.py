@@ -31,12 +31,35 @@ def timeit(fn, iters=10):
     return best
 
 
+def fp8_shape(c, name, A, W, M, N, K, no_cublas):
+    """NEXT-4: per-tensor e4m3 operands (quantised by df_op_quant_e4m3), bf16 output."""
+    qa = torch.empty(M, K, dtype=torch.uint8, device="cuda")
+    qb = torch.empty(N, K, dtype=torch.uint8, device="cuda")
+    sa = torch.empty(1, device="cuda")
+    sb = torch.empty(1, device="cuda")
+    ms_q = timeit(lambda: c.op_quant_e4m3(A, qa, sa))
+    c.op_quant_e4m3(W, qb, sb)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    ms_ours = timeit(lambda: c.op_gemm_e4m3(qa, qb, sa, sb, out))
+    fl = 2.0 * M * N * K
+    row = {"shape": name, "dtype": "e4m3", "M": M, "N": N, "K": K, "ours_tflops": round(fl / ms_ours / 1e9, 1),
+           "quant_A_gbs": round(A.numel() * 3 / ms_q / 1e6, 1)}
+    if not no_cublas:
+        fa, fb = qa.view(torch.float8_e4m3fn), qb.view(torch.float8_e4m3fn)
+        ms_lib = timeit(lambda: torch._scaled_mm(fa, fb.t(), scale_a=sa, scale_b=sb, out_dtype=torch.bfloat16))
+        ref = torch._scaled_mm(fa, fb.t(), scale_a=sa, scale_b=sb, out_dtype=torch.bfloat16).float()
+        row.update({"cublaslt_tflops": round(fl / ms_lib / 1e9, 1), "ratio": round(ms_lib / ms_ours, 3),
+                    "rel_err_vs_cublaslt": f"{((out.float() - ref).norm() / ref.norm()).item():.1e}"})
+    print(row, flush=True)
+
+
 def main():
     import argparse
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--tc", type=int, default=1, help="2: allow the stream-K schedule")
+    ap.add_argument("--fp8", action="store_true", help="e4m3 GEMM (df_op_gemm_e4m3) vs cuBLASLt torch._scaled_mm")
     a = ap.parse_args()
     g = B.make_graph(TINY, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)])
     with B.Context(g) as c:
@@ -45,6 +68,10 @@ def main():
                 continue
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+            if a.fp8:
+                fp8_shape(c, name, A, W, M, N, K, a.no_cublas)
+                del A, W
+                continue
             out = torch.empty(M, N, device="cuda")
             ms_ours = timeit(lambda: c.op_gemm(A, W, out, tc=a.tc))
             ms_cublas = ms_ours if a.no_cublas else timeit(lambda: torch.matmul(A, W.t()))
