@@ -605,6 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           for (int q = 0; q < CW; q += 16) tmem_ld16(trow + c + q, v + q);
           tc_wait_ld();
           if (fix) fixup(v, c, CW);
+          if (F8) f8_scale_acc(v, CW);
           if (!epi_skip) epi_apply<CW, OutT>(epi, row, n0, v);
         }
       } else if (TK == TK_STORE_F32 || TK == TK_GRES) {
@@ -974,6 +975,11 @@ cudaError_t gemm_e4m3(const uint8_t* qa, const uint8_t* qb, const float* sa, con
     if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box)) return cudaErrorInvalidValue;
     return launch_tc2<32, float, TK_STORE_F32, true>(ta, tb, to, M, N, K, epi, st);
   }
+  static const int tma_epi = [] {  // DF_GEMM_TMA_EPI=0: per-thread epilogue stores (A/B)
+    const char* e = getenv("DF_GEMM_TMA_EPI");
+    return e ? atoi(e) : 1;
+  }();
+  if (!tma_epi) return launch_tc2<32, bf16, TK_DIRECT, true>(ta, tb, to, M, N, K, epi, st);
   const uint32_t box[2] = {64, 32};
   const uint64_t str[1] = {uint64_t(ldo) * 2};
   if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box)) return cudaErrorInvalidValue;
