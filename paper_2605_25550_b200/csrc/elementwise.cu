@@ -659,20 +659,34 @@ __global__ void __launch_bounds__(256) e4m3_amax_kernel(const bf16* __restrict__
   float m = 0.f;
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   const size_t n8 = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / 8;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(x) + i);
+  auto acc = [&](const uint4 u) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       m = fmaxf(m, fabsf(__uint_as_float(w[k] << 16)));
       m = fmaxf(m, fabsf(__uint_as_float(w[k] & 0xFFFF0000u)));
     }
+  };
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n8; i += 4 * stride) {  // four 16-byte loads in flight per thread
+    const uint4 u0 = __ldg(xv + i), u1 = __ldg(xv + i + stride), u2 = __ldg(xv + i + 2 * stride),
+                u3 = __ldg(xv + i + 3 * stride);
+    acc(u0), acc(u1), acc(u2), acc(u3);
   }
+  for (; i < n8; i += stride) acc(__ldg(xv + i));
   for (size_t i = n8 * 8 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
     m = fmaxf(m, fabsf(bf2f(x[i])));
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+  __shared__ float wm[8];  // block max, then one atomic per block
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, wm[w]);
+    if (m > 0.f) atomicMax(amax, __float_as_uint(m));
+  }
 }
 __global__ void e4m3_scale_kernel(float* s) {
   const float a = __uint_as_float(*reinterpret_cast<const unsigned*>(s));
@@ -691,15 +705,22 @@ __global__ void __launch_bounds__(256) e4m3_quant_kernel(const bf16* __restrict_
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   const bool vec = !((reinterpret_cast<uintptr_t>(x) & 15) | (reinterpret_cast<uintptr_t>(q) & 7));
   const size_t n8 = vec ? n / 8 : 0;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(x) + i);
+  auto cvt = [&](const uint4 u, size_t i) {
     uint2 o;
     o.x = e4m3x4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
                  __uint_as_float(u.y & 0xFFFF0000u), s);
     o.y = e4m3x4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u), __uint_as_float(u.w << 16),
                  __uint_as_float(u.w & 0xFFFF0000u), s);
     reinterpret_cast<uint2*>(q)[i] = o;
+  };
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n8; i += 4 * stride) {  // four 16-byte loads in flight per thread
+    const uint4 u0 = __ldg(xv + i), u1 = __ldg(xv + i + stride), u2 = __ldg(xv + i + 2 * stride),
+                u3 = __ldg(xv + i + 3 * stride);
+    cvt(u0, i), cvt(u1, i + stride), cvt(u2, i + 2 * stride), cvt(u3, i + 3 * stride);
   }
+  for (; i < n8; i += stride) cvt(__ldg(xv + i), i);
   for (size_t i = n8 * 8 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
     q[i] = uint8_t(__nv_cvt_float_to_fp8(__fdiv_rn(bf2f(x[i]), s), __NV_SATFINITE, __NV_E4M3));
 }
@@ -710,8 +731,8 @@ cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaSt
     e4m3_scale_kernel<<<1, 1, 0, st>>>(scale);
     return cudaGetLastError();
   }
-  const size_t per = 256 * 8;
-  const unsigned grid = unsigned(std::min<size_t>((n + per - 1) / per, size_t(num_sms()) * 8));
+  const size_t per = 256 * 8 * 4;  // four 8-element vectors per thread
+  const unsigned grid = unsigned(std::max<size_t>(1, std::min<size_t>((n + per - 1) / per, size_t(num_sms()) * 8)));
   e4m3_amax_kernel<<<grid, 256, 0, st>>>(x, n, reinterpret_cast<unsigned*>(scale));
   e4m3_scale_kernel<<<1, 1, 0, st>>>(scale);
   e4m3_quant_kernel<<<grid, 256, 0, st>>>(x, n, scale, q);
