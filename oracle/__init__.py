@@ -7,7 +7,9 @@ the two meet only through synth/ (seeded inputs and shapes, no method
 arithmetic).  Every function cites the PAPER.md passage or DESIGN.md reading it
 follows.
 
-Parity status per function (pins in tests/test_oracle_*.py):
+Parity status per function (pins in tests/test_oracle_*.py; every pin
+is checked to fail under one-line mutations of the oracle by tools/mutate_oracle.py,
+38/38 killed, profiles/r02_oracle_mutations.txt):
   philox       pinned: Random123 known-answer vectors
   params       pinned: uniform-recipe invariants (range, exactness, moments)
   dit.sigmas   pinned: worked values S=4, shifts 1/3/5 (closed form)
@@ -17,11 +19,18 @@ Parity status per function (pins in tests/test_oracle_*.py):
   dit.rms_norm pinned: scale invariance, unit rms
   dit.patchify pinned: round trip, hand-indexed elements
   dit.sinusoid pinned: t=0 closed form
-  dit.block    pinned: adaLN-zero identity, loop re-derivation on a tiny case
-  dit (full composition) — parity unpinned by the paper (no printed values);
-               rests on the per-component pins and the vacuity guard
-  stages.encoder / decoder — stand-ins (R17); decoder pinned by pixel-shuffle
-               index check; encoder composition parity unpinned
+  dit.time_embedding pinned: identity-like W_e1/W_e2/W_m closed form at sigma = 0.37 and 0
+  dit.text_projection pinned: one-hot W_t1, shifted W_t2 closed form (GELU side, b_t1 inside)
+  dit.cross_kv pinned: per-head RMS of K = |g_ck| at any per-head scale, V un-normalised
+  dit.head     pinned: shift-only / scale-only hand-indexed outputs
+  dit.velocity pinned (wiring): zero-layer DiT = head(patch embed, e) closed form
+  dit.block    pinned: adaLN-zero identity; modulation rows 0/1 (uniform self-attention
+               closed form), rows 3/4 and the SwiGLU sides (linear / SiLU special cases),
+               gates, cross-attention ungated and unmodulated, cross query path closed form
+  dit (full composition) -- parity unpinned by the paper (no printed values);
+               rests on the per-function pins above and the vacuity guard
+  stages.encoder pinned: one-token closed form (SiLU side, residual, gains)
+  stages.decoder pinned: pixel-shuffle index check
   capacity.qps / plan  pinned: the paper's QPM points
   capacity.payload_hash pinned: splitmix64 published first output, chunk additivity
   fp8 (NEXT-4, R28) pinned: E4M3 closed forms, 256-code round trip, ties-to-even,

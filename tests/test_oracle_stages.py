@@ -128,6 +128,20 @@ def test_vacuity_guard(cfg):
     assert dcross >= 5e-2, dcross
 
 
+@pytest.mark.parametrize("name", ["image", "video"])
+def test_vacuity_guard_production_width(name):
+    """The guard at the C2 / C3 widths (d, heads, f, L_txt, the weights' std table) on one
+    latent frame of 16x16 (N = 64) and one block; the full depths (28 / 40 blocks) are run
+    by tools/vacuity_full_depth.py (profiles/r02_vacuity_*_full_depth.json)."""
+    import dataclasses
+    from synth.configs import CONFIGS
+    cfg = dataclasses.replace(with_layers(CONFIGS[name], 1), F=1, H=16, W=16)
+    rho, vx, dcross = _vacuity(cfg)
+    assert all(1e-2 <= r <= 1.0 for r in rho), rho
+    assert 0.1 <= vx <= 10.0, vx
+    assert dcross >= 5e-2, dcross
+
+
 def test_pipeline_request_tiny_runs():
     P = OP.Params(TINY, 0)
     out = stages.request(P, TINY, seed=1)
