@@ -45,12 +45,14 @@ def philox4x32_10(c0, c1, c2, c3, k0: int, k1: int):
     return (c0.astype(np.uint32), c1.astype(np.uint32), c2.astype(np.uint32), c3.astype(np.uint32))
 
 
-def stream_words(seed: int, n: int, c2: int, c3: int) -> np.ndarray:
-    """Words w_i, i < n, of the stream (seed; c2, c3) per DESIGN.md §RNG:
+def stream_words(seed: int, n: int, c2: int, c3: int, first: int = 0) -> np.ndarray:
+    """Words w_i, first <= i < first + n, of the stream (seed; c2, c3) per DESIGN.md §RNG:
     counter (lo32(i>>2), hi32(i>>2), c2, c3), key (lo32(seed), hi32(seed)),
-    output word i & 3."""
+    output word i & 3.  `first` must be a multiple of 4 (a slice of whole blocks, so a
+    large tensor can be generated piecewise)."""
+    assert first % 4 == 0
     nb = (n + 3) // 4
-    blk = np.arange(nb, dtype=np.uint64)
+    blk = np.arange(first // 4, first // 4 + nb, dtype=np.uint64)
     lo = blk & MASK32
     hi = blk >> np.uint64(32)
     z = np.full(nb, c2 & 0xFFFFFFFF, dtype=np.uint64)

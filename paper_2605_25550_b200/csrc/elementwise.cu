@@ -517,15 +517,18 @@ cudaError_t embed_rows(const int32_t* ids, const bf16* emb, float* z, int L, int
 // ------------------------------------------------------------------ D stand-in
 // One CTA per (latent frame, 8 latent pixels): u = SiLU(x W1 + b1) in smem, then
 // o = tanh(u W2 + b2) scattered by the pixel shuffle.
+// One CTA per 8 latent pixels of one latent frame; the launch covers frames [f0, f0 + gridDim.y)
+// and pixels [p_begin, p_end) of each (a T->D chunk when D decodes chunk by chunk).
 __global__ void decode_kernel(const float* __restrict__ x, float* __restrict__ out, int C, int F, int H, int W,
                               int cdec, const bf16* __restrict__ w1, const bf16* __restrict__ b1,
                               const bf16* __restrict__ w2f, const bf16* __restrict__ b2f,
-                              const bf16* __restrict__ w2r, const bf16* __restrict__ b2r) {
+                              const bf16* __restrict__ w2r, const bf16* __restrict__ b2r, int f0, int p_begin,
+                              int p_end) {
   extern __shared__ float sh[];  // [8][cdec]
-  const int phi = blockIdx.y;
-  const int pix0 = blockIdx.x * 8;
+  const int phi = f0 + blockIdx.y;
+  const int pix0 = p_begin + blockIdx.x * 8;
   const int HW = H * W;
-  const int npix = min(8, HW - pix0);
+  const int npix = min(8, p_end - pix0);
   for (int t = threadIdx.x; t < 8 * cdec; t += blockDim.x) {
     int q = t / cdec, u = t % cdec;
     float acc = 0.f;
@@ -559,8 +562,15 @@ __global__ void decode_kernel(const float* __restrict__ x, float* __restrict__ o
 cudaError_t decode_latent(const float* x, float* out, int C, int F, int H, int W, int cdec, const bf16* w1,
                           const bf16* b1, const bf16* w2f, const bf16* b2f, const bf16* w2r, const bf16* b2r,
                           cudaStream_t st) {
-  dim3 grid((H * W + 7) / 8, F);
-  decode_kernel<<<grid, 256, 8 * cdec * sizeof(float), st>>>(x, out, C, F, H, W, cdec, w1, b1, w2f, b2f, w2r, b2r);
+  return decode_latent_region(x, out, C, F, H, W, cdec, w1, b1, w2f, b2f, w2r, b2r, 0, F, 0, H * W, st);
+}
+cudaError_t decode_latent_region(const float* x, float* out, int C, int F, int H, int W, int cdec, const bf16* w1,
+                                 const bf16* b1, const bf16* w2f, const bf16* b2f, const bf16* w2r, const bf16* b2r,
+                                 int f0, int nf, int p_begin, int p_end, cudaStream_t st) {
+  if (nf <= 0 || p_end <= p_begin) return cudaSuccess;
+  dim3 grid((p_end - p_begin + 7) / 8, nf);
+  decode_kernel<<<grid, 256, 8 * cdec * sizeof(float), st>>>(x, out, C, F, H, W, cdec, w1, b1, w2f, b2f, w2r, b2r,
+                                                             f0, p_begin, p_end);
   return cudaGetLastError();
 }
 

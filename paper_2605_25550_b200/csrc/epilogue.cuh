@@ -42,6 +42,7 @@ struct Epi {
   float* v_out;
   float dsig;
   int C, pt, ph, pw, Hl, Wl, Fl;  // latent geometry
+  int m_base;              // EULER: token index of GEMM row 0 (the head run over one T->D chunk's tokens)
   // batch of samples stacked along M (classifier-free guidance: conditional, negative):
   // rows per sample; HEADS writes sample-major [b][heads][Mper][dh_pad]; EULER with
   // v_batch stores v of sample b at v_batch[b * latent_elems + idx] instead of updating x.
@@ -245,6 +246,7 @@ DF_DEV void epi_apply(const Epi& e, int m, int n0, float* v) {
     store_vec<CW>(o, v);
   } else if (e.kind == EPI_EULER) {
     // token m = (f*Hp + hh)*Wp + ww ; column p = ((c*pt + i)*ph + j)*pw + k
+    m += e.m_base;
     const int mper = e.Mper > 0 ? e.Mper : e.M;
     const int bsm = m / mper;
     m -= bsm * mper;

@@ -88,6 +88,9 @@ cudaError_t embed_rows(const int32_t* ids, const bf16* emb, float* z, int L, int
 cudaError_t decode_latent(const float* x, float* out, int C, int F, int H, int W, int cdec, const bf16* w1,
                           const bf16* b1, const bf16* w2f, const bf16* b2f, const bf16* w2r, const bf16* b2r,
                           cudaStream_t st);
+cudaError_t decode_latent_region(const float* x, float* out, int C, int F, int H, int W, int cdec, const bf16* w1,
+                                 const bf16* b1, const bf16* w2f, const bf16* b2f, const bf16* w2r, const bf16* b2r,
+                                 int f0, int nf, int p_begin, int p_end, cudaStream_t st);
 
 // ---- handoff helpers
 cudaError_t payload_hash(const void* buf, size_t nbytes, size_t word_offset, unsigned long long* out,

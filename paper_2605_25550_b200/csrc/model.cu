@@ -420,7 +420,8 @@ cudaError_t Model::norm(const float* x, void* out, int M, int dd, const float* s
 
 // ------------------------------------------------------------------ prologue (a1)
 cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
-                           const void* ctx_neg_bf16, float guidance, const void* clip_bf16, const float* y_in) {
+                           const void* ctx_neg_bf16, float guidance, const void* clip_bf16, const float* y_in,
+                           const ChunkHook* hook) {
   const int d = c.d, Lt = c.L_txt, dt = c.d_txt, fd = c.freq_dim;
   const int Li = int(c.L_img), di = int(c.d_img);
   if (i2v() != (clip_bf16 != nullptr && y_in != nullptr)) return cudaErrorInvalidValue;  // I2V needs both
@@ -462,11 +463,10 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
     cd.y = (float*)cd.mem.take(yel * 4);
   }
   if (!cp || (i2v() && !cd.y)) return cudaErrorMemoryAllocation;
+  // nothing above or in the time conditioning reads the E->T payload: with a chunk hook this
+  // part runs while the payload is still in flight
   if (!f32()) DF_TRY(cudaMemsetAsync(cd.kc, 0, 2 * al(kvb), st));  // dh padding = 0
-  if (i2v()) {
-    if (!f32()) DF_TRY(cudaMemsetAsync(cd.kci, 0, 2 * al(kvbi), st));
-    DF_TRY(cudaMemcpyAsync(cd.y, y_in, yel * 4, cudaMemcpyDeviceToDevice, st));
-  }
+  if (i2v() && !f32()) DF_TRY(cudaMemsetAsync(cd.kci, 0, 2 * al(kvbi), st));
   DF_TRY(cudaMemcpyAsync(cd.sig_dev, sig_host, (S + 1) * 4, cudaMemcpyHostToDevice, st));
   // time conditioning for all S steps (R4, R5), fp32 SIMT: the M = S rows are GEMV-like
   DF_L(sinusoid(cd.sig_dev, s, S, fd, st));
@@ -474,23 +474,28 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   DF_L(gemm_simt(t1, 0, d, ACT_NONE, temb2_wT, d, cd.e, d, S, d, d, temb2_b, ACT_NONE, st));
   DF_L(gemm_simt(cd.e, 0, d, ACT_SILU, tmod_wT, d, cd.e6, 6 * d, S, 6 * d, d, tmod_b, ACT_NONE, st));
   // per context b (0: prompt, 1: negative prompt): ctx' = GELU(ctx W1 + b1) W2 + b2, then
-  // [K | V] = ctx' [Wck | Wcv]^T per layer, K <- headRMS * g_ck, into sample-major heads
+  // [K | V] = ctx' [Wck | Wcv]^T per layer, K <- headRMS * g_ck, into sample-major heads.
+  // Every operation is row-wise, so rows [r0, r0 + rows) can be projected as soon as they land
+  // (bn = 128 keeps a chunk on the one-CTA tiles, whose head-major epilogue takes the row
+  // offset through the output pointer and the Lt-row head stride through Mper).
   const size_t per = size_t(cd.B) * c.heads * Lt * dhp * ab;     // one layer
   const size_t per_b = size_t(c.heads) * Lt * dhp * ab;          // one sample of one layer
-  for (int b = 0; b < cd.B; ++b) {
-    const void* ctxb = b == 0 ? ctx_bf16 : ctx_neg_bf16;
-    Epi e1 = epi_base(EPI_STORE, Lt, d);
+  auto project = [&](int b, const void* ctxb, int r0, int rows) -> cudaError_t {
+    const bool part = rows != Lt;
+    const int bn = part ? 128 : 256;
+    Epi e1 = epi_base(EPI_STORE, rows, d);
     e1.bias = txt1_b;
     e1.act = ACT_GELU;
-    e1.out = c1;
+    e1.out = (char*)c1 + size_t(r0) * d * ab;
     e1.ldo = d;
-    Epi e2 = epi_base(EPI_STORE, Lt, d);
+    Epi e2 = epi_base(EPI_STORE, rows, d);
     e2.bias = txt2_b;
-    e2.out = cp;
+    e2.out = (char*)cp + size_t(r0) * d * ab;
     e2.ldo = d;
+    const bf16* xr = (const bf16*)ctxb + size_t(r0) * dt;
     if (!f32()) {
-      DF_L(gemm_tc((const bf16*)ctxb, dt, txt1_wT, dt, Lt, d, dt, e1, 0, st));
-      DF_L(gemm_tc((const bf16*)c1, d, txt2_wT, d, Lt, d, d, e2, 0, st));
+      DF_L(gemm_tc(xr, dt, txt1_wT, dt, rows, d, dt, e1, 0, st, bn));
+      DF_L(gemm_tc((const bf16*)e1.out, d, txt2_wT, d, rows, d, d, e2, 0, st, bn));
     } else {
       DF_L(gemm_simt(ctxb, 1, dt, 0, txt1_wT, dt, ptmp, d, Lt, d, dt, nullptr, ACT_NONE, st));
       DF_L(epi_rows(ptmp, e1, 1, st));
@@ -498,19 +503,37 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
       DF_L(epi_rows(ptmp, e2, 1, st));
     }
     for (int l = 0; l < c.layers; ++l) {
-      void* kl = (char*)cd.kc + l * per + b * per_b;
-      void* vl = (char*)cd.vc + l * per + b * per_b;
-      Epi e = heads_epi(Lt, 2, Lw[l].ckv_b, kl, Lw[l].g_ck, 0, vl, nullptr, 0, nullptr, nullptr, 0);
+      char* kl = (char*)cd.kc + l * per + b * per_b + size_t(r0) * dhp * ab;
+      char* vl = (char*)cd.vc + l * per + b * per_b + size_t(r0) * dhp * ab;
+      Epi e = heads_epi(rows, 2, Lw[l].ckv_b, kl, Lw[l].g_ck, 0, vl, nullptr, 0, nullptr, nullptr, 0,
+                        part ? Lt : 0);
       if (!f32()) {
-        DF_L(gemm_tc((const bf16*)cp, d, Lw[l].ckv_wT, d, Lt, 2 * d, d, e, 0, st));
+        DF_L(gemm_tc((const bf16*)e2.out, d, Lw[l].ckv_wT, d, rows, 2 * d, d, e, 0, st, bn));
       } else {
         DF_L(gemm_simt(cp, 0, d, 0, Lw[l].ckv_wT, d, ptmp, 2 * d, Lt, 2 * d, d, nullptr, ACT_NONE, st));
         DF_L(epi_rows(ptmp, e, 1, st));
       }
     }
-    if (!i2v()) continue;
-    // I2V (NEXT-3, R27): img' = GELU(clip W_i1 + b_i1) W_i2 + b_i2; [Ki | Vi] = img' [Wki | Wvi]^T
-    // per layer, Ki <- headRMS * g_ki (the same image conditioning for both CFG samples)
+    return cudaSuccess;
+  };
+  // the prompt, chunk by chunk as it lands (bf16 path) or whole
+  const bool chunked = hook && hook->wait && !f32() && hook->rows_per_chunk > 0 && hook->rows_per_chunk < Lt;
+  int waited = 0;  // chunks [0, waited) already waited for
+  if (chunked) {
+    for (int r0 = 0; r0 < Lt; r0 += hook->rows_per_chunk, ++waited) {
+      DF_TRY(hook->wait(hook->user, waited));
+      DF_TRY(project(0, ctx_bf16, r0, std::min(hook->rows_per_chunk, Lt - r0)));
+    }
+  }
+  if (hook && hook->wait)
+    for (; waited < hook->nchunks; ++waited) DF_TRY(hook->wait(hook->user, waited));
+  if (!chunked) DF_TRY(project(0, ctx_bf16, 0, Lt));
+  if (cd.B == 2) DF_TRY(project(1, ctx_neg_bf16, 0, Lt));
+  if (!i2v()) return cudaSuccess;
+  DF_TRY(cudaMemcpyAsync(cd.y, y_in, yel * 4, cudaMemcpyDeviceToDevice, st));
+  // I2V (NEXT-3, R27): img' = GELU(clip W_i1 + b_i1) W_i2 + b_i2; [Ki | Vi] = img' [Wki | Wvi]^T
+  // per layer, Ki <- headRMS * g_ki (the same image conditioning for both CFG samples)
+  for (int b = 0; b < cd.B; ++b) {
     Epi i1 = epi_base(EPI_STORE, Li, d);
     i1.bias = img1_b;
     i1.act = ACT_GELU;
@@ -621,11 +644,11 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
 }
 
 // ------------------------------------------------------------------ one step (a2-a12)
-cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStream_t st) {
+cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStream_t st, const BlockHook* bh) {
   if (prof && prof_every > 1 && i % prof_every) {  // sampled profiling: this step runs unbracketed
     Prof* p = prof;
     prof = nullptr;
-    cudaError_t e = step(cd, i, x, v_out, st);
+    cudaError_t e = step(cd, i, x, v_out, st, bh);
     prof = p;
     return e;
   }
@@ -658,9 +681,28 @@ cudaError_t Model::step(const Cond& cd, int i, float* x, float* v_out, cudaStrea
     e.Hp = Hp; e.Wp = Wp;
     e.Mper = N;
     if (B == 2) e.v_batch = vbatch;  // v of both samples; guidance + Euler below
-    DF_TRY(gemm(h, d, head_wT, d, M, P, d, e, 1, st));
-    if (B == 2)
-      DF_L(cfg_euler(x, vbatch, v_out, size_t(c.C) * c.F * c.H * c.W, cd.guidance, e.dsig, st));
+    const bool blocks = bh && bh->done && B == 1 && c.pt == 1 && bh->lb.n > 1;
+    if (!blocks) {
+      DF_TRY(gemm(h, d, head_wT, d, M, P, d, e, 1, st));
+      if (B == 2)
+        DF_L(cfg_euler(x, vbatch, v_out, size_t(c.C) * c.F * c.H * c.W, cd.guidance, e.dsig, st));
+      if (bh && bh->done)
+        for (int k = 0; k < bh->lb.n; ++k) DF_TRY(bh->done(bh->user, k));
+    } else {
+      // the head + Euler epilogue once per T->D chunk: latent rows [h0, h1) of frame f are the
+      // tokens [(f Hp + h0/ph) Wp, (f Hp + h1/ph) Wp) (pt = 1); the chunk's send starts as soon
+      // as its block is final (a12 -> a14)
+      for (int k = 0; k < bh->lb.n; ++k) {
+        int f, h0, h1;
+        bh->lb.block(k, f, h0, h1);
+        const int m0 = (f * Hp + h0 / c.ph) * Wp, m1 = (f * Hp + (h1 + c.ph - 1) / c.ph) * Wp;
+        Epi eb = e;
+        eb.M = m1 - m0;
+        eb.m_base = m0;
+        DF_TRY(gemm((const char*)h + size_t(m0) * d * act_bytes(), d, head_wT, d, m1 - m0, P, d, eb, 1, st));
+        DF_TRY(bh->done(bh->user, k));
+      }
+    }
   }
   return cudaSuccess;
 }
@@ -700,6 +742,17 @@ cudaError_t Model::encode(const int32_t* ids, void* ctx_out, cudaStream_t st) {
 // ------------------------------------------------------------------ D stand-in
 cudaError_t Model::decode(const float* x, float* out, cudaStream_t st) {
   DF_L(decode_latent(x, out, c.C, c.F, c.H, c.W, c.dec_width, d1_w, d1_b, d2f_w, d2f_b, d2r_w, d2r_b, st));
+  return cudaSuccess;
+}
+
+// One T->D chunk (latent rows [h0, h1) of frame f): every latent pixel decodes on its own, so D
+// starts on the first chunk that lands (a14).
+cudaError_t Model::decode_block(const float* x, float* out, const LatentBlocks& lb, int k, cudaStream_t st) {
+  if (lb.n <= 1) return decode(x, out, st);
+  int f, h0, h1;
+  lb.block(k, f, h0, h1);
+  DF_L(decode_latent_region(x, out, c.C, c.F, c.H, c.W, c.dec_width, d1_w, d1_b, d2f_w, d2f_b, d2r_w, d2r_b, f, 1,
+                            h0 * int(c.W), h1 * int(c.W), st));
   return cudaSuccess;
 }
 

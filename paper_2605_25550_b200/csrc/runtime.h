@@ -80,6 +80,39 @@ struct Prof {
   void reset();
 };
 
+// T->D chunk plan over the fp32 latent [C, F, H, W] (R22): a chunk
+// is the block of latent rows [h0, h1) of one latent frame f, all C channels (C strided rows
+// of (h1 - h0) W floats).  Video: one frame per chunk; image (F = 1): blocks of hb rows.
+// Chunk k -> (f, h0, h1) with f = k / nbh.  n = 1 with hb = H, F = 1 is the whole latent.
+struct LatentBlocks {
+  int C = 0, F = 1, H = 0, W = 0, hb = 0, nbh = 1, n = 1;
+  void block(int k, int& f, int& h0, int& h1) const {
+    f = k / nbh;
+    h0 = (k % nbh) * hb;
+    h1 = h0 + hb < H ? h0 + hb : H;
+  }
+};
+
+// Chunk-wise consumption of the E->T payload by the request prologue (a1): the prompt ctx
+// arrives in chunks of rows_per_chunk rows; wait(c) makes the prologue's stream wait for chunk
+// c (device-side) before the rows of chunk c are projected.  Chunks past the prompt (negative
+// prompt, I2V image tokens) are all waited for before those parts are read.
+struct ChunkHook {
+  int rows_per_chunk = 0;
+  int nchunks = 0;
+  cudaError_t (*wait)(void* user, int c) = nullptr;
+  void* user = nullptr;
+};
+
+// Chunk-wise production of the final latent (a12 -> a14): on the step it is passed to, the
+// head + Euler epilogue runs once per latent block of `lb` and done(k) is called right after
+// block k is enqueued (the T->D send of chunk k waits on the event it records).
+struct BlockHook {
+  LatentBlocks lb;
+  cudaError_t (*done)(void* user, int k) = nullptr;
+  void* user = nullptr;
+};
+
 // Per-request conditioning handle (df_cond).
 struct Cond {
   int S = 0;
@@ -157,12 +190,13 @@ struct Model {
 
   cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
                       const void* ctx_neg_bf16 = nullptr, float guidance = 1.f, const void* clip_bf16 = nullptr,
-                      const float* y = nullptr);
+                      const float* y = nullptr, const ChunkHook* hook = nullptr);
   bool i2v() const { return c.C_y > 0; }
-  cudaError_t step(const Cond& c, int i, float* x, float* v_out, cudaStream_t st);
+  cudaError_t step(const Cond& c, int i, float* x, float* v_out, cudaStream_t st, const BlockHook* bh = nullptr);
   cudaError_t layer(const Cond& c, int i, int l, float* r_io, cudaStream_t st);
   cudaError_t encode(const int32_t* ids, void* ctx_bf16, cudaStream_t st);
   cudaError_t decode(const float* x, float* out, cudaStream_t st);
+  cudaError_t decode_block(const float* x, float* out, const LatentBlocks& lb, int k, cudaStream_t st);
 
   // helpers
   cudaError_t gemm(const void* A, int lda, const bf16* W, int ldw, int M, int Nn, int K, const Epi& e, int out_f32,

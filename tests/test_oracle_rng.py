@@ -76,3 +76,19 @@ def test_noise_moments_and_tokens():
     assert abs(float(x.mean())) < 0.02 and abs(float(x.std()) - 1.0) < 0.02
     ids = stages.tokens_from_seed(TINY, 3)
     assert ids.min() >= 0 and ids.max() < TINY.vocab and ids.shape == (TINY.L_txt,)
+
+
+def test_streaming_params_equal_cached_params():
+    """tests/oracle_big.StreamingParams (sliced Philox on a pool, no per-layer cache) yields
+    the same bf16 bits as oracle.params.Params for every tensor of the mid model."""
+    from oracle import params as OP
+    from oracle_big import StreamingParams
+    from synth.configs import MID
+    P, S = OP.Params(MID, 3), StreamingParams(MID, 3, procs=2, slice_words=4096)
+    try:
+        for _, name, _, _ in OP.tensor_table(MID):
+            if name.startswith("L1.") or name.startswith("L0.w") or not name.startswith("L"):
+                assert np.array_equal(P.bits(name), S.bits(name)), name
+                assert np.array_equal(P[name], S[name]), name
+    finally:
+        S.close()
