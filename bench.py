@@ -179,6 +179,148 @@ def workload_name(cfg):
 
 
 # ------------------------------------------------------------------ our arm
+def summarize(comps, ecomps=()):
+    """Per-request pipeline numbers from df_completion records (D rank)."""
+    lat = [(c.t_done - c.t_submit) * 1000.0 for c in comps]
+    exposed = [c.exposed_ms[0] + c.exposed_ms[1] for c in comps]
+    med = statistics.median
+
+    def pos(v):
+        v = [x for x in v if x > 0]
+        return med(v) if v else -1.0
+    return {
+        "t_ms": med(c.stage_ms[1] for c in comps),
+        "lat": med(lat), "exp_med": med(exposed), "exp_max": max(exposed),
+        "exp_frac": med(exposed) / med(lat),
+        "exp_edge": [med(c.exposed_ms[0] for c in comps), med(c.exposed_ms[1] for c in comps)],
+        "xfer": [pos([c.xfer_ms[0] for c in comps]), pos([c.xfer_ms[1] for c in comps])],
+        "overlap": [med(c.overlap_ms[0] for c in comps), med(c.overlap_ms[1] for c in comps)],
+        "hash_ok": all(c.hash_src[e] == c.hash_dst[e] != 0 for c in list(comps) + list(ecomps) for e in range(2)),
+        "n": len(comps), "t_inst": sorted({int(c.inst[1]) for c in comps})}
+
+
+def roofline(kstats, peaks, traffic, config):
+    """Roofline of the kernel class with the largest measured time share (this rank's DiT
+    instance, per-launch CUDA events on its stream)."""
+    dom = max(kstats, key=lambda k: kstats[k]["ms"])
+    ks = kstats[dom]
+    avg_ms = ks["ms"] / max(ks["launches"], 1)
+    if ks["flops"] > 0:
+        ach = (ks["flops"] / ks["launches"]) / (avg_ms / 1000.0) / 1e12
+        # the sustained figure (cuBLAS 8192^3 back to back, deepest power-cap clocks) is the
+        # denominator for a kernel timed inside a long step unless the kernel beats it; then the
+        # burst figure is the ceiling that still holds
+        if ach <= peaks["bf16_sus"]:
+            pk, note = peaks["bf16_sus"], f"{peaks['src']} sustained cuBLAS bf16 (kernel timed inside a long step)"
+        else:
+            pk = peaks["bf16"]
+            note = (f"{peaks['src']} burst cuBLAS bf16: the kernel exceeds the sustained figure "
+                    f"({peaks['bf16_sus']:.1f}), which was measured at lower power-capped clocks")
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "traffic": traffic, "kernel": dom,
+                "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"], "peak_note": note}
+    else:
+        ach = (ks["bytes"] / ks["launches"]) / (avg_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
+                "traffic": traffic, "kernel": dom, "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
+                "peak_note": f"{peaks['src']} HBM copy"}
+    if roof["traffic"] is None:  # committed ncu capture of this kernel at this config, if any
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            ent = tj.get(config, {}).get(dom)
+            if ent:
+                roof["traffic"] = ent["bytes"]
+                roof["traffic_source"] = ent["source"]
+        except (OSError, ValueError):
+            pass
+    return roof
+
+
+def kernel_tables(kstats):
+    tot = sum(v["ms"] for v in kstats.values()) or 1.0
+    shares = {k: round(v["ms"] / tot, 4) for k, v in kstats.items() if v["ms"] > 0}
+    gfl = {k: round((v["flops"] / v["ms"] / 1e9), 1) for k, v in kstats.items() if v["ms"] > 0 and v["flops"] > 0}
+    return shares, gfl
+
+
+def payload_bytes(cfg):
+    """Per-request payloads of the two edges (E->T: ctx [| clip | y]; T->D: the fp32 latent)."""
+    e2t = cfg.L_txt * cfg.d_txt * 2 + (((cfg.L_img * cfg.d_img * 2 + 15) // 16) * 16 +
+                                       cfg.C_y * cfg.F * cfg.H * cfg.W * 4 if cfg.C_y else 0)
+    return e2t, cfg.latent_elems * 4
+
+
+def handoff_record(cfg, summary):
+    e2t, t2d = payload_bytes(cfg)
+    return {"exposed_ms_median": summary["exp_med"], "exposed_ms_max": summary["exp_max"],
+            "exposed_ms_median_per_edge": summary["exp_edge"],
+            "exposed_frac_of_latency": summary["exp_frac"], "xfer_ms_median": summary["xfer"],
+            "payload_bytes": [e2t, t2d],
+            "xfer_gbps": [(e2t / summary["xfer"][0] / 1e6) if summary["xfer"][0] > 0 else None,
+                          (t2d / summary["xfer"][1] / 1e6) if summary["xfer"][1] > 0 else None],
+            "consumer_overlap_ms_median": summary["overlap"],
+            "latency_ms_median": summary["lat"], "hash_match": summary["hash_ok"],
+            "dit_instances_used": summary["t_inst"]}
+
+
+def video_record(args, peaks, local):
+    """The north_star's headline shape (BASELINE configs[2], C3): text-to-video 81x480x832 ->
+    32760 tokens, DiT 5120 x40 layers, 50 Euler steps, through the same E -> T -> D pipeline on
+    this GPU: 1 warm-up request (50 denoising steps) then `video_requests` timed requests,
+    inputs device-resident (tokens and noise from the seed), with the DiT step's roofline and
+    the clocks sampled during the timed region."""
+    import torch
+    from paper_2605_25550_b200 import binding as B, layouts
+    cfg = CONFIGS["video"]
+    inst = layouts.partitioned(1)
+    g = B.make_graph(cfg, inst, precision=B.DF_BF16, weight_seed=0, chunk_bytes=(args.chunk_ctx, args.chunk_lat),
+                     n_slots=2, handoff_mode=B.DF_ASYNC | B.DF_HASH, ring_capacity=64, max_steps=cfg.steps)
+    ctx = B.Context(g)
+    stream = torch.cuda.current_stream()
+
+    def batch(n, seed0):
+        for k in range(n):
+            while ctx.submit(cfg.steps, cfg.shift, seed0 + k, user_tag=seed0 + k)[0] != B.DF_OK:
+                time.sleep(0.01)
+        comps = []
+        while len(comps) < n:
+            comps += ctx.poll(16, timeout_ms=1000)
+        return comps
+
+    try:
+        batch(1, 5000)
+        torch.cuda.synchronize()
+        ctx.profile(4, True)
+        l0 = ctx.launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(local) as clk:
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            comps = batch(args.video_requests, 6000)
+            ev1.record(stream)
+            ev1.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        launches = ctx.launch_count() - l0
+        kstats = ctx.kernel_stats()
+        ctx.profile(False, False)
+    finally:
+        ctx.close()
+    summ = summarize(comps)
+    tflop = cfg.flops_per_request() / 1e12
+    tfs = tflop / (summ["t_ms"] / 1000.0)
+    shares, gfl = kernel_tables(kstats)
+    return {"workload": workload_name(cfg), "E:T:D": "1:1:1", "requests": args.video_requests, "warmup_requests": 1,
+            "value": args.video_requests / (ms / 1000.0), "unit": UNIT, "ms_per_request": ms / args.video_requests,
+            "gpu_launches": launches,
+            "dit_step": {"tflop_per_request": tflop, "tflop_per_step": cfg.flops_per_step() / 1e12,
+                         "t_stage_ms_median": summ["t_ms"], "achieved_tflops": tfs,
+                         "frac_of_sustained_peak": tfs / peaks["bf16_sus"], "frac_of_burst_peak": tfs / peaks["bf16"]},
+            "roofline": roofline(kstats, peaks, None, "video"),
+            "clocks": clk.summary(),
+            "handoff": handoff_record(cfg, summ),
+            "kernel_time_share": shares, "kernel_gflops": gfl}
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -287,17 +429,7 @@ def run_ours(args, cfg):
     launches_t = torch.tensor([launches], device=red_dev, dtype=torch.int64)
     if world > 1:
         dist.all_reduce(launches_t)
-    summary = None
-    if rank == d_rank:
-        lat = [(c.t_done - c.t_submit) * 1000.0 for c in comps]
-        exposed = [c.exposed_ms[0] + c.exposed_ms[1] for c in comps]
-        summary = {
-            "t_ms": statistics.median(c.stage_ms[1] for c in comps),
-            "lat": statistics.median(lat), "exp_med": statistics.median(exposed), "exp_max": max(exposed),
-            "exp_frac": statistics.median(exposed) / statistics.median(lat),
-            "xfer": [statistics.median(c.xfer_ms[0] for c in comps), statistics.median(c.xfer_ms[1] for c in comps)],
-            "hash_ok": all(c.hash_src[e] == c.hash_dst[e] != 0 for c in comps + ecomps for e in range(2)),
-            "n": len(comps), "t_inst": sorted({int(c.inst[1]) for c in comps})}
+    summary = summarize(comps, ecomps) if rank == d_rank else None
     if world > 1:
         objs = [None] * world
         dist.all_gather_object(objs, summary)
@@ -306,57 +438,23 @@ def run_ours(args, cfg):
     e2e = n_total / (ems / 1000.0)
     dit_tflop = cfg.flops_per_request() / 1e12
     dit_tflops = dit_tflop / (summary["t_ms"] / 1000.0)
-    # ---- roofline of the dominant kernel class (this rank's DiT instance, timed live)
-    dom = max(kstats, key=lambda k: kstats[k]["ms"])
-    ks = kstats[dom]
-    avg_ms = ks["ms"] / max(ks["launches"], 1)
-    if ks["flops"] > 0:
-        ach = (ks["flops"] / ks["launches"]) / (avg_ms / 1000.0) / 1e12
-        # the sustained figure (cuBLAS 8192^3 back to back, deepest power-cap clocks) is the
-        # denominator for a kernel timed inside a long step unless the kernel beats it; then the
-        # burst figure is the ceiling that still holds
-        if ach <= peaks["bf16_sus"]:
-            pk, note = peaks["bf16_sus"], f"{peaks['src']} sustained cuBLAS bf16 (kernel timed inside a long step)"
-        else:
-            pk = peaks["bf16"]
-            note = (f"{peaks['src']} burst cuBLAS bf16: the kernel exceeds the sustained figure "
-                    f"({peaks['bf16_sus']:.1f}), which was measured at lower power-capped clocks")
-        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
-                "frac": ach / pk, "traffic": args.traffic, "kernel": dom,
-                "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"], "peak_note": note}
-    else:
-        ach = (ks["bytes"] / ks["launches"]) / (avg_ms / 1000.0) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
-                "traffic": args.traffic, "kernel": dom, "avg_launch_us": avg_ms * 1000.0, "launches": ks["launches"],
-                "peak_note": f"{peaks['src']} HBM copy"}
-    if roof["traffic"] is None:  # committed ncu capture of this kernel at this config, if any
-        try:
-            tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
-            ent = tj.get(args.config, {}).get(dom)
-            if ent:
-                roof["traffic"] = ent["bytes"]
-                roof["traffic_source"] = ent["source"]
-        except (OSError, ValueError):
-            pass
-    tot_kms = sum(v["ms"] for v in kstats.values()) or 1.0
-    shares = {k: round(v["ms"] / tot_kms, 4) for k, v in kstats.items() if v["ms"] > 0}
-    tput_kind = {k: round((v["flops"] / v["ms"] / 1e9), 1) for k, v in kstats.items() if v["ms"] > 0 and v["flops"] > 0}
-
+    roof = roofline(kstats, peaks, args.traffic, args.config)
+    shares, tput_kind = kernel_tables(kstats)
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         ctx.close()
         return
+    ctx.close()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         s = oracle_sample(cfg)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "oracle", "sample": s["sample"]}
+    video = None
+    if world == 1 and args.config == "image" and args.video_requests > 0:
+        video = video_record(args, peaks, local)
     gE, gT, gD = layouts.ratio(inst)
-    # per-request payloads of the two edges (E->T: ctx [| clip | y]; T->D: the fp32 latent)
-    e2t_bytes = cfg.L_txt * cfg.d_txt * 2 + (((cfg.L_img * cfg.d_img * 2 + 15) // 16) * 16 +
-                                              cfg.C_y * cfg.F * cfg.H * cfg.W * 4 if cfg.C_y else 0)
-    t2d_bytes = cfg.latent_elems * 4
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / n_total, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -378,22 +476,16 @@ def run_ours(args, cfg):
         "dit_step": {"tflop_per_request": dit_tflop, "t_stage_ms_median": summary["t_ms"],
                      "achieved_tflops": dit_tflops, "frac_of_sustained_peak": dit_tflops / peaks["bf16_sus"],
                      "frac_of_burst_peak": dit_tflops / peaks["bf16"]},
-        "handoff": {"exposed_ms_median": summary["exp_med"], "exposed_ms_max": summary["exp_max"],
-                    "exposed_frac_of_latency": summary["exp_frac"], "xfer_ms_median": summary["xfer"],
-                    "payload_bytes": [e2t_bytes, t2d_bytes],
-                    # (the cross-process path does not time its copies: xfer_ms = -1 -> null)
-                    "xfer_gbps": [(e2t_bytes / summary["xfer"][0] / 1e6) if summary["xfer"][0] > 0 else None,
-                                  (t2d_bytes / summary["xfer"][1] / 1e6) if summary["xfer"][1] > 0 else None],
-                    "latency_ms_median": summary["lat"], "hash_match": summary["hash_ok"],
-                    "dit_instances_used": summary["t_inst"]},
+        "handoff": handoff_record(cfg, summary),
         "kernel_time_share": shares,
         "kernel_gflops": tput_kind,
     }
+    if video is not None:
+        line["video"] = video
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    ctx.close()
 
 
 def main():
@@ -410,6 +502,8 @@ def main():
     ap.add_argument("--t-per-gpu", type=int, default=1, help="DiT instances per GPU")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
+    ap.add_argument("--video-requests", type=int, default=1,
+                    help="N=1 image run: timed C3 (video) requests in the line's `video` sub-record (0: skip)")
     ap.add_argument("--dit-steps", type=int, default=0,
                     help="Euler steps per request (0: the config's); for the few-step I2V / workload-shift runs")
     args = ap.parse_args()

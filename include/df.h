@@ -45,7 +45,7 @@ typedef enum {
 
 typedef enum { DF_E = 0, DF_T = 1, DF_D = 2 } df_stage;
 enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1 };               /* df_graph.precision */
-enum { DF_ASYNC = 0, DF_SYNC = 1, DF_PERMUTE = 2, DF_HASH = 4 }; /* handoff flags   */
+enum { DF_ASYNC = 0, DF_SYNC = 1, DF_PERMUTE = 2, DF_HASH = 4, DF_LATENT_BLOCKS = 8 }; /* handoff flags */
 #define DF_ALL_CHUNKS 0xFFFFFFFFu
 #define DF_MAX_INST 32
 
@@ -92,6 +92,10 @@ typedef struct {
    * (the posted destination addresses).  Rank 0 creates the segment. */
   int32_t rank, world;
   char shm_name[64];
+  /* Chunk before which an injected delay is placed (0: before the first chunk; clamped to
+   * the last).  The delay holds back that chunk and the ones after it, so a consumer that
+   * works chunk by chunk is already busy on the earlier ones (handoff-stress tests). */
+  uint32_t jitter_chunk;
 } df_graph;
 
 /* df_init: validate the graph (Eq. 1), allocate and Philox-initialise every
@@ -129,11 +133,18 @@ typedef struct {
   int32_t inst[3];              /* E, T, D instance that served it                       */
   double t_submit, t_start[3], t_end[3], t_done; /* seconds, host monotonic clock        */
   float stage_ms[3];            /* device time of E, T, D compute                         */
-  float xfer_ms[2];             /* device time of the E->T / T->D transfers               */
-  float exposed_ms[2];          /* consumer stall on in-flight data per edge   */
+  float xfer_ms[2];             /* device time of the E->T / T->D transfers (first copy issued
+                                   -> last chunk landed)                                 */
+  float exposed_ms[2];          /* consumer stall on in-flight data per edge, on the consumer's
+                                   clock: sum over chunks c of max(0, A_c - max(R_c, P_c))
+                                                             */
   uint64_t hash_src[2], hash_dst[2]; /* payload hash on both sides of each edge  */
   const void* out_view;         /* the decoded fp32 output in THIS process (the D rank's copy  */
   uint64_t out_view_bytes;      /*   in multi-process mode); valid until the next df_poll      */
+  float overlap_ms[2];          /* per edge: how long before the last chunk landed the consumer
+                                   was already working on chunk 0 (chunk-wise consumption:
+                                   the prologue projects ctx rows as they land, D decodes
+                                   latent blocks as they land; north_star) */
 } df_completion;
 /* Pop up to max completions ("final output is returned to the request
  * scheduler").  Blocks up to timeout_ms (-1 forever). DF_EMPTY if none. */
@@ -188,11 +199,15 @@ df_status df_tokens(df_ctx* ctx, int32_t inst, uint64_t seed, int32_t* ids_dev, 
 df_status df_image_cond(df_ctx* ctx, int32_t inst, uint64_t seed, void* clip_dev, float* y_dev, void* stream);
 
 /* Chunked stage handoff: copy bytes from src (device of
- * src_inst) into dst (device of dst_inst) in ceil(bytes/chunk_bytes) chunks on the
- * library's comm stream after the work already queued on src_stream, one event per
- * chunk.  DF_SYNC also makes src_stream wait for the last chunk.  DF_PERMUTE issues
- * chunks in a seeded random order (tests).  DF_HASH hashes both sides.  Jitter per
- * the graph's jitter_p / jitter_delay_s.  *out is caller-owned. */
+ * src_inst) into dst (device of dst_inst) in ceil(bytes/chunk_bytes) chunks (chunk sizes
+ * rounded up to 16 bytes, at most 64 chunks) on the library's comm stream after the work
+ * already queued on src_stream, one event per chunk.  DF_LATENT_BLOCKS: bytes is the
+ * graph's fp32 latent [C,F,H,W] and a chunk is a block of latent rows of one frame (all
+ * channels; a video chunk is one latent frame), sized by chunk_bytes (R22).  DF_SYNC also
+ * makes src_stream wait for the last chunk.  DF_PERMUTE issues chunks in a seeded random
+ * order (tests).  DF_HASH hashes both sides (the destination on the destination's aux
+ * stream).  Jitter per the graph's jitter_p / jitter_delay_s / jitter_chunk.  Never blocks
+ * the host.  *out is caller-owned. */
 typedef struct {
   int32_t src_inst, dst_inst;
   const void* src;

@@ -16,7 +16,7 @@ DF_OK, DF_AGAIN, DF_EMPTY = 0, 1, 2
 DF_ERR_INVALID, DF_ERR_CAPACITY, DF_ERR_NOMEM, DF_ERR_DUPLICATE, DF_ERR_STATE = 10, 11, 12, 13, 14
 DF_E, DF_T, DF_D = 0, 1, 2
 DF_BF16, DF_FP32_VALIDATION = 0, 1
-DF_ASYNC, DF_SYNC, DF_PERMUTE, DF_HASH = 0, 1, 2, 4
+DF_ASYNC, DF_SYNC, DF_PERMUTE, DF_HASH, DF_LATENT_BLOCKS = 0, 1, 2, 4, 8
 DF_ALL_CHUNKS = 0xFFFFFFFF
 DF_MAX_INST = 32
 
@@ -41,7 +41,7 @@ class GraphC(C.Structure):
                 ("ring_capacity", C.c_uint32), ("precision", C.c_uint32), ("max_steps", C.c_uint32),
                 ("weight_seed", C.c_uint64), ("jitter_p", C.c_float), ("jitter_delay_s", C.c_float),
                 ("jitter_seed", C.c_uint64), ("dit", DitCfgC), ("rank", C.c_int32), ("world", C.c_int32),
-                ("shm_name", C.c_char * 64)]
+                ("shm_name", C.c_char * 64), ("jitter_chunk", C.c_uint32)]
 
 
 class ReqIdC(C.Structure):
@@ -60,7 +60,7 @@ class CompletionC(C.Structure):
                 ("t_submit", C.c_double), ("t_start", C.c_double * 3), ("t_end", C.c_double * 3),
                 ("t_done", C.c_double), ("stage_ms", C.c_float * 3), ("xfer_ms", C.c_float * 2),
                 ("exposed_ms", C.c_float * 2), ("hash_src", C.c_uint64 * 2), ("hash_dst", C.c_uint64 * 2),
-                ("out_view", C.c_void_p), ("out_view_bytes", C.c_uint64)]
+                ("out_view", C.c_void_p), ("out_view_bytes", C.c_uint64), ("overlap_ms", C.c_float * 2)]
 
 
 class SchedCfgC(C.Structure):
@@ -176,7 +176,7 @@ def dit_cfg_c(cfg) -> DitCfgC:
 
 def make_graph(cfg, instances, precision=DF_BF16, weight_seed=0, chunk_bytes=(0, 0), n_slots=2,
                handoff_mode=DF_ASYNC | DF_HASH, ring_capacity=256, max_steps=None, jitter=(0.0, 0.0, 0), G=0,
-               rank=0, world=1, shm_name=""):
+               rank=0, world=1, shm_name="", jitter_chunk=0):
     """instances: list of (device, stage) or (device, stage, rank)."""
     g = GraphC()
     g.n_inst = len(instances)
@@ -195,6 +195,7 @@ def make_graph(cfg, instances, precision=DF_BF16, weight_seed=0, chunk_bytes=(0,
     g.max_steps = int(max_steps if max_steps is not None else max(cfg.steps, 64))
     g.weight_seed = int(weight_seed)
     g.jitter_p, g.jitter_delay_s, g.jitter_seed = float(jitter[0]), float(jitter[1]), int(jitter[2])
+    g.jitter_chunk = int(jitter_chunk)
     g.dit = dit_cfg_c(cfg)
     return g
 

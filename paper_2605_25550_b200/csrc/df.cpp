@@ -35,9 +35,10 @@ using namespace df;
 struct df_xfer {
   int src_dev = 0, dst_dev = 0;
   uint32_t nchunks = 0;
-  std::vector<cudaEvent_t> chunk_ev;  // on the source comm stream (cross-device waits are legal)
-  cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing (source comm stream)
-  cudaEvent_t t_hash = nullptr;            // destination hash done (dst comm stream)
+  std::vector<cudaEvent_t> chunk_ev;  // source device, source comm stream: chunk c landed
+  std::vector<cudaEvent_t> ready_ev;  // source device, source comm stream: chunk c's data existed
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing (source comm stream): first copy issued / last landed
+  cudaEvent_t t_hash = nullptr;            // destination hash done (destination aux stream)
   unsigned long long* hash_dev = nullptr;  // [2] src, dst (pinned-mapped host)
   bool hashed = false;
   uint64_t bytes = 0;
@@ -104,10 +105,13 @@ struct ReqState {
   std::vector<int32_t> ids, neg_ids;
   int inst[3] = {-1, -1, -1};
   double t_submit = 0, t_start[3] = {0, 0, 0}, t_end[3] = {0, 0, 0};
-  cudaEvent_t ev[10] = {};  // 0,1 E start/end; 2,3 T start/end; 4,5 D start/end; 6 T ready; 7 D ready
+  cudaEvent_t ev[6] = {};  // 0,1 E start/end; 2,3 T start/end; 4,5 D start/end (each on its stage's device)
   Xfer* x[2] = {nullptr, nullptr};
   int slot[2] = {-1, -1};
   int xbuf = 0;  // T latent buffer index
+  // per edge, measured by the consumer on its own device clock once its work completed
+  float exposed[2] = {0, 0}, xfer[2] = {-1, -1}, overlap[2] = {0, 0};
+  float stage_ms[3] = {-1, -1, -1};
   bool pre = false;       // multi-process: completion filled by the D worker
   df_completion comp{};
   std::vector<float> outcopy;  // multi-process: decoded output held in the D process
@@ -154,32 +158,87 @@ struct Inbox {
 
 
 
+// Busy time of one instance for Alg. 1's utilisation u_s: accumulated busy intervals
+// plus the open one, so a sample taken mid-request credits the time already spent (a request
+// credited only at its completion made u_s jump between 0 and 1 from tick to tick).
+struct BusyClock {
+  std::mutex mu;
+  uint64_t acc = 0;
+  double since = -1;
+  void begin(double t) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (since < 0) since = t;
+  }
+  void end(double t) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (since >= 0) acc += uint64_t(std::max(0.0, t - since) * 1e9), since = -1;
+  }
+  uint64_t sample(double t) {
+    std::lock_guard<std::mutex> lk(mu);
+    return acc + (since >= 0 ? uint64_t(std::max(0.0, t - since) * 1e9) : 0);
+  }
+};
+
+// Consumer-side device timestamps of one in-flight transfer, all on the
+// consumer's device so every difference is one clock:
+//   R[c], A[c]  consumer compute stream, right before / after its wait on chunk c;
+//   P[c]        probe stream, when the producer's "chunk c exists" event fired;
+//   X0, X1      probe stream, when the first copy was issued / the last chunk landed.
+// exposed = sum_c max(0, A_c - max(R_c, P_c)): the consumer stalled on data in flight (injected
+// delays included), not on upstream compute.  overlap = max(0, X1 - A_0): how long before the
+// last chunk landed the consumer was already working on chunk 0.
+struct RecvClock {
+  int n = 0;
+  cudaStream_t probe = nullptr;
+  cudaEvent_t R[PL_MAX_CHUNKS] = {}, A[PL_MAX_CHUNKS] = {}, P[PL_MAX_CHUNKS] = {};
+  cudaEvent_t X0 = nullptr, X1 = nullptr;
+  unsigned long long* hash = nullptr;  // mapped pinned [2]: src (producer's, via the slot trailer), dst
+};
+
+// Producer-owned events of the transfers into one (consumer, slot) (multi-process).
+struct SendSet {
+  cudaEvent_t ready[PL_MAX_CHUNKS] = {}, start = nullptr, chunk[PL_MAX_CHUNKS] = {};
+  XferEvHandles h{};
+};
+// The consumer's handles on a producer's SendSet (opened over IPC, or the producer's own
+// events when it lives in this process).
+struct OpenSet {
+  bool open = false;
+  bool ipc = false;
+  cudaEvent_t ready[PL_MAX_CHUNKS] = {}, start = nullptr, chunk[PL_MAX_CHUNKS] = {};
+};
+
 struct Inst {
   int id = 0, stage = 0, device = 0;
   Model m;
   cudaStream_t compute = nullptr, comm = nullptr;
+  cudaStream_t aux = nullptr;  // destination hashes and slot release (never behind an outbound send)
   std::thread worker;
   Inbox<Job> inbox;
-  SlotPool slots;           // receive slots (T: ctx; D: latent)
-  // T: two latent buffers, each with a "send done" event
+  SlotPool slots;           // receive slots (T: ctx; D: latent); each has a 64-byte trailer
+  size_t slot_cap = 0;      // payload capacity of a slot (the trailer starts here)
+  // T: two latent buffers, each with a "send done" event, the per-chunk events of its last
+  // step's head blocks, and the receive clock of the E->T transfer it consumed
   float* xbuf[2] = {nullptr, nullptr};
   cudaEvent_t xsent[2] = {nullptr, nullptr};
+  cudaEvent_t hb_ev[2][PL_MAX_CHUNKS] = {};
+  RecvClock rclk[4];        // T: per latent buffer; D: per pending decode
   int xnext = 0;
   // E: two ctx send buffers
   void* ebuf[2] = {nullptr, nullptr};
   cudaEvent_t esent[2] = {nullptr, nullptr};
   int enext = 0;
   int32_t* ids_dev = nullptr;
-  // D: decoded output + pinned staging
+  // D: decoded output + pinned staging (one per pending decode)
   float* dout = nullptr;
-  float* stage_host = nullptr;
-  std::atomic<uint64_t> busy_ns{0};
+  float* stage_host[4] = {nullptr, nullptr, nullptr, nullptr};
+  BusyClock busy;
   std::atomic<uint64_t> served{0};
   // multi-process
   bool local = true;
   cudaEvent_t ipc_consumed[PL_MAX_SLOTS] = {};
-  cudaEvent_t ipc_chunk[PL_MAX_SLOTS][PL_MAX_CHUNKS] = {};
-  unsigned long long* mp_hash = nullptr;  // pinned [2]: src (producer side), dst (consumer side)
+  SendSet* sendset[PL_MAX_INST][PL_MAX_SLOTS] = {};  // producer: per (consumer, slot)
+  OpenSet opened[PL_MAX_INST][PL_MAX_SLOTS];          // consumer: per (producer, slot)
 };
 
 struct df_ctx {
@@ -215,9 +274,9 @@ struct df_ctx {
   std::mutex view_mu;
   struct View {
     bool open = false, remote = false;
+    uint64_t slot_bytes = 0;  // payload capacity; the 64-byte trailer follows
     void* buf[PL_MAX_SLOTS] = {};
     cudaEvent_t consumed[PL_MAX_SLOTS] = {};
-    cudaEvent_t chunk[PL_MAX_SLOTS][PL_MAX_CHUNKS] = {};
   };
   View views[DF_MAX_INST];
   std::vector<ReqState*> last_polled;
@@ -277,6 +336,107 @@ static unsigned jitter_edges() {
   return m;
 }
 
+// Jitter (R23): one seeded Bernoulli draw per request-edge transfer; the delay is a
+// host function on the comm stream placed before chunk min(jitter_chunk, n - 1).
+static bool jitter_draw(const df_ctx* ctx, uint64_t seq, uint32_t edge) {
+  if (!(ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f && (jitter_edges() >> edge & 1u))) return false;
+  uint32_t c[4] = {uint32_t(seq), uint32_t(seq >> 32), edge, 3u};
+  philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
+  return double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0;
+}
+
+// ---------------------------------------------------------------- chunk plans (R22)
+// A transfer is cut into n chunks: byte ranges (the E->T payload; the public df_handoff) or
+// latent blocks (T->D: rows [h0, h1) of one latent frame, all channels -> a 2-D copy of C
+// strided rows).  Both sides derive the same plan from the graph.
+struct ChunkPlan {
+  int n = 1;
+  bool blocks = false;
+  uint64_t bytes = 0, chunk = 0;
+  LatentBlocks lb;
+  void piece(int k, uint64_t& off, uint64_t& width, uint64_t& height, uint64_t& pitch) const {
+    if (!blocks) {
+      off = uint64_t(k) * chunk;
+      width = std::min<uint64_t>(chunk, bytes - off);
+      height = 1;
+      pitch = width;
+      return;
+    }
+    int f, h0, h1;
+    lb.block(k, f, h0, h1);
+    off = (uint64_t(f) * lb.H + h0) * lb.W * 4;
+    width = uint64_t(h1 - h0) * lb.W * 4;
+    height = uint64_t(lb.C);
+    pitch = uint64_t(lb.F) * lb.H * lb.W * 4;
+  }
+};
+
+ChunkPlan plan_bytes(uint64_t bytes, uint64_t chunk, uint64_t align) {
+  ChunkPlan p;
+  p.bytes = bytes;
+  if (chunk == 0 || chunk >= bytes) chunk = bytes;
+  chunk = (chunk + align - 1) / align * align;
+  if ((bytes + chunk - 1) / chunk > uint64_t(PL_MAX_CHUNKS))
+    chunk = ((bytes + PL_MAX_CHUNKS - 1) / PL_MAX_CHUNKS + align - 1) / align * align;
+  p.chunk = chunk;
+  p.n = int((bytes + chunk - 1) / chunk);
+  return p;
+}
+
+// T->D plan: blocks of hb = floor(chunk_bytes / (C W 4)) latent rows (a multiple of ph, at
+// least ph); a video chunk is one whole latent frame; chunk_bytes = 0 (or a block covering
+// the latent, or pt != 1) = one chunk.
+ChunkPlan plan_latent(const df_dit_cfg& c, uint64_t chunk_bytes) {
+  const uint64_t total = uint64_t(c.C) * c.F * c.H * c.W * 4;
+  ChunkPlan p = plan_bytes(total, 0, 16);
+  if (chunk_bytes == 0 || chunk_bytes >= total || c.pt != 1) return p;
+  LatentBlocks lb;
+  lb.C = int(c.C), lb.F = int(c.F), lb.H = int(c.H), lb.W = int(c.W);
+  int hb = int(chunk_bytes / (uint64_t(c.C) * c.W * 4));
+  hb = std::max<int>(int(c.ph), hb / int(c.ph) * int(c.ph));
+  if (c.F > 1 || hb >= int(c.H)) hb = int(c.H);
+  lb.hb = hb;
+  lb.nbh = (int(c.H) + hb - 1) / hb;
+  lb.n = int(c.F) * lb.nbh;
+  if (lb.n <= 1 || lb.n > PL_MAX_CHUNKS) return p;
+  p.blocks = true;
+  p.n = lb.n;
+  p.lb = lb;
+  return p;
+}
+
+// E->T plan: chunks of whole ctx rows (the prologue projects rows as they land).
+ChunkPlan plan_ctx(const df_ctx* ctx, uint64_t bytes) {
+  uint64_t row = uint64_t(ctx->g.dit.d_txt) * 2, a = 16;
+  while (a % row) a += 16;  // lcm(16, row bytes)
+  return plan_bytes(bytes, ctx->g.chunk_bytes[0], a);
+}
+
+int rows_per_chunk(const df_ctx* ctx, const ChunkPlan& p) {
+  return int(p.chunk / (uint64_t(ctx->g.dit.d_txt) * 2));
+}
+
+// One chunk on `st`.  peer_dev >= 0: a single-process copy to another device.
+cudaError_t copy_piece(const ChunkPlan& p, int k, void* dst, int dst_dev, const void* src, int src_dev,
+                       cudaStream_t st) {
+  uint64_t off, width, height, pitch;
+  p.piece(k, off, width, height, pitch);
+  char* d = static_cast<char*>(dst) + off;
+  const char* s = static_cast<const char*>(src) + off;
+  if (dst_dev == src_dev) {
+    if (height == 1) return cudaMemcpyAsync(d, s, width, cudaMemcpyDeviceToDevice, st);
+    return cudaMemcpy2DAsync(d, pitch, s, pitch, width, height, cudaMemcpyDeviceToDevice, st);
+  }
+  if (height == 1) return cudaMemcpyPeerAsync(d, dst_dev, s, src_dev, width, st);
+  cudaMemcpy3DPeerParms q{};
+  q.srcPtr = make_cudaPitchedPtr(const_cast<char*>(s), pitch, width, height);
+  q.srcDevice = src_dev;
+  q.dstPtr = make_cudaPitchedPtr(d, pitch, width, height);
+  q.dstDevice = dst_dev;
+  q.extent = make_cudaExtent(width, height, 1);
+  return cudaMemcpy3DPeerAsync(&q, st);
+}
+
 void free_xfer(Xfer* x);
 
 // Mapped host slots for the payload hashes, a (src, dst) pair per transfer, pooled
@@ -313,9 +473,14 @@ HashPool& hash_pool() {
   return *pool;
 }
 
-df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_stream, Xfer** out) {
+// Single-process transfer (df_handoff and the in-process pipeline edges).  The comm stream of
+// the source instance runs, per chunk c (in order, or a seeded permutation): wait for the
+// chunk's data (piece_ready[c], or the whole producer stream), record ready[c], [the injected
+// delay], copy, [source hash after the last copy], record chunk[c].  No host synchronisation.
+df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, const ChunkPlan& plan, cudaStream_t src_stream,
+                     const cudaEvent_t* piece_ready, Xfer** out) {
   if (!d || d->src_inst < 0 || d->dst_inst < 0 || d->src_inst >= int(ctx->inst.size()) ||
-      d->dst_inst >= int(ctx->inst.size()) || !d->src || !d->dst || !d->bytes)
+      d->dst_inst >= int(ctx->inst.size()) || !d->src || !d->dst || !d->bytes || plan.n < 1)
     return fail(ctx, "df_handoff: invalid descriptor", DF_ERR_INVALID);
   Inst& S = *ctx->inst[d->src_inst];
   Inst& D = *ctx->inst[d->dst_inst];
@@ -323,21 +488,21 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_str
   x->src_dev = S.device;
   x->dst_dev = D.device;
   x->bytes = d->bytes;
-  uint64_t cb = d->chunk_bytes;
-  if (cb == 0 || cb >= d->bytes) cb = d->bytes;
-  cb = (cb + 15) & ~uint64_t(15);  // 16-byte chunk granularity (R22)
-  x->nchunks = uint32_t((d->bytes + cb - 1) / cb);
+  x->nchunks = uint32_t(plan.n);
   CK(ctx, cudaSetDevice(S.device));
   x->chunk_ev.resize(x->nchunks);
+  x->ready_ev.resize(x->nchunks);
   for (auto& e : x->chunk_ev) CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : x->ready_ev) CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(ctx, cudaEventCreate(&x->t0));
   CK(ctx, cudaEventCreate(&x->t1));
-  // comm stream runs after the producer's queued work
-  cudaEvent_t ready;
-  CK(ctx, cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  CK(ctx, cudaEventRecord(ready, src_stream));
-  CK(ctx, cudaStreamWaitEvent(S.comm, ready, 0));
-  CK(ctx, cudaEventDestroy(ready));
+  if (!piece_ready) {  // comm stream runs after the producer's queued work
+    cudaEvent_t ready;
+    CK(ctx, cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(ctx, cudaEventRecord(ready, src_stream));
+    CK(ctx, cudaStreamWaitEvent(S.comm, ready, 0));
+    CK(ctx, cudaEventDestroy(ready));
+  }
   const bool hash = (d->flags & DF_HASH) != 0;
   if (hash) {
     x->hash_dev = hash_pool().get();
@@ -347,45 +512,41 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_str
     }
     x->hash_dev[0] = x->hash_dev[1] = 0;
     x->hashed = true;
-    g_launches->fetch_add(1);
-    CK(ctx, payload_hash(d->src, d->bytes, 0, x->hash_dev, S.comm));
   }
-  // jitter: one Bernoulli draw per request-edge transfer (R23)
-  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f && (jitter_edges() >> d->edge & 1u)) {
-    uint32_t c[4] = {uint32_t(d->seq), uint32_t(d->seq >> 32), d->edge, 3u};
-    philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
-    if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0)
-      CK(ctx, delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), S.comm));  // host function, no kernel
-  }
-  CK(ctx, cudaEventRecord(x->t0, S.comm));
-  std::vector<uint32_t> order(x->nchunks);
-  for (uint32_t i = 0; i < x->nchunks; ++i) order[i] = i;
+  const bool delay = jitter_draw(ctx, d->seq, d->edge);
+  const int jc = std::min<int>(int(ctx->g.jitter_chunk), plan.n - 1);
+  std::vector<int> order(plan.n);
+  for (int i = 0; i < plan.n; ++i) order[i] = i;
   if (d->flags & DF_PERMUTE) {
-    for (uint32_t i = x->nchunks; i > 1; --i) {  // seeded Fisher-Yates
-      uint32_t c[4] = {uint32_t(d->seq), i, 0x5045524Du, 4u};
+    for (int i = plan.n; i > 1; --i) {  // seeded Fisher-Yates
+      uint32_t c[4] = {uint32_t(d->seq), uint32_t(i), 0x5045524Du, 4u};
       philox_host(c, 0x1234567u, 0x89ABCDEFu);
-      std::swap(order[i - 1], order[c[0] % i]);
+      std::swap(order[i - 1], order[c[0] % uint32_t(i)]);
     }
   }
-  for (uint32_t k = 0; k < x->nchunks; ++k) {
-    uint32_t ci = order[k];
-    uint64_t off = uint64_t(ci) * cb;
-    uint64_t sz = std::min<uint64_t>(cb, d->bytes - off);
-    const char* sp = static_cast<const char*>(d->src) + off;
-    char* dp = static_cast<char*>(d->dst) + off;
-    if (S.device == D.device) CK(ctx, cudaMemcpyAsync(dp, sp, sz, cudaMemcpyDeviceToDevice, S.comm));
-    else CK(ctx, cudaMemcpyPeerAsync(dp, D.device, sp, S.device, sz, S.comm));
+  for (int k = 0; k < plan.n; ++k) {
+    const int ci = order[k];
+    if (piece_ready) CK(ctx, cudaStreamWaitEvent(S.comm, piece_ready[ci], 0));
+    CK(ctx, cudaEventRecord(x->ready_ev[ci], S.comm));
+    if (delay && k == jc) CK(ctx, delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), S.comm));
+    if (k == 0) CK(ctx, cudaEventRecord(x->t0, S.comm));
+    CK(ctx, copy_piece(plan, ci, d->dst, D.device, d->src, S.device, S.comm));
+    if (hash && k == plan.n - 1) {  // every piece is final here
+      g_launches->fetch_add(1);
+      CK(ctx, payload_hash(d->src, d->bytes, 0, x->hash_dev, S.comm));
+    }
     CK(ctx, cudaEventRecord(x->chunk_ev[ci], S.comm));
   }
   CK(ctx, cudaEventRecord(x->t1, S.comm));
   if (hash) {
-    // destination hash, on the destination device after the last chunk landed
+    // destination hash on the destination's aux stream (never queued behind that instance's
+    // own outbound sends and their injected delays)
     CK(ctx, cudaSetDevice(D.device));
-    CK(ctx, cudaStreamWaitEvent(D.comm, x->t1, 0));
+    CK(ctx, cudaStreamWaitEvent(D.aux, x->t1, 0));
     g_launches->fetch_add(1);
-    CK(ctx, payload_hash(d->dst, d->bytes, 0, x->hash_dev + 1, D.comm));
+    CK(ctx, payload_hash(d->dst, d->bytes, 0, x->hash_dev + 1, D.aux));
     CK(ctx, cudaEventCreateWithFlags(&x->t_hash, cudaEventDisableTiming));
-    CK(ctx, cudaEventRecord(x->t_hash, D.comm));
+    CK(ctx, cudaEventRecord(x->t_hash, D.aux));
     CK(ctx, cudaSetDevice(S.device));
   }
   if (d->flags & DF_SYNC) CK(ctx, cudaStreamWaitEvent(src_stream, x->t1, 0));
@@ -395,7 +556,9 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, cudaStream_t src_str
 
 void free_xfer(Xfer* x) {
   if (!x) return;
+  if (x->t_hash) cudaEventSynchronize(x->t_hash);  // the pooled hash slot is still being written
   for (auto e : x->chunk_ev) cudaEventDestroy(e);
+  for (auto e : x->ready_ev) cudaEventDestroy(e);
   if (x->t0) cudaEventDestroy(x->t0);
   if (x->t1) cudaEventDestroy(x->t1);
   if (x->t_hash) cudaEventDestroy(x->t_hash);
@@ -410,6 +573,88 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
     return -1.f;
   }
   return ms;
+}
+
+// ---------------------------------------------------------------- consumer clocks
+cudaError_t clock_create(RecvClock& rc) {
+  DF_TRY(cudaStreamCreateWithFlags(&rc.probe, cudaStreamNonBlocking));
+  for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
+    DF_TRY(cudaEventCreate(&rc.R[c]));
+    DF_TRY(cudaEventCreate(&rc.A[c]));
+    DF_TRY(cudaEventCreate(&rc.P[c]));
+  }
+  DF_TRY(cudaEventCreate(&rc.X0));
+  DF_TRY(cudaEventCreate(&rc.X1));
+  rc.hash = hash_pool().get();
+  return rc.hash ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
+void clock_destroy(RecvClock& rc) {
+  if (rc.probe) cudaStreamSynchronize(rc.probe);
+  for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
+    if (rc.R[c]) cudaEventDestroy(rc.R[c]);
+    if (rc.A[c]) cudaEventDestroy(rc.A[c]);
+    if (rc.P[c]) cudaEventDestroy(rc.P[c]);
+  }
+  if (rc.X0) cudaEventDestroy(rc.X0);
+  if (rc.X1) cudaEventDestroy(rc.X1);
+  if (rc.probe) cudaStreamDestroy(rc.probe);
+  if (rc.hash) hash_pool().put(rc.hash);
+  rc = RecvClock{};
+}
+
+// Probe stream: P_c when the producer's ready[c] fired, X0 at the first copy, X1 when the last
+// chunk landed (waits in the producer's own record order).
+cudaError_t clock_probe(RecvClock& rc, int n, const cudaEvent_t* ready, cudaEvent_t start, cudaEvent_t last) {
+  rc.n = n;
+  for (int c = 0; c < n; ++c) {
+    DF_TRY(cudaStreamWaitEvent(rc.probe, ready[c], 0));
+    DF_TRY(cudaEventRecord(rc.P[c], rc.probe));
+    if (c == 0) {
+      DF_TRY(cudaStreamWaitEvent(rc.probe, start, 0));
+      DF_TRY(cudaEventRecord(rc.X0, rc.probe));
+    }
+  }
+  DF_TRY(cudaStreamWaitEvent(rc.probe, last, 0));
+  return cudaEventRecord(rc.X1, rc.probe);
+}
+
+// Consumer stream `st` waits for chunk c (device-side), bracketed by R_c / A_c.
+cudaError_t clock_chunk(RecvClock& rc, int c, cudaStream_t st, cudaEvent_t chunk_ev) {
+  DF_TRY(cudaEventRecord(rc.R[c], st));
+  DF_TRY(cudaStreamWaitEvent(st, chunk_ev, 0));
+  return cudaEventRecord(rc.A[c], st);
+}
+
+// After the consumer's work on this transfer completed on the device.
+void clock_read(RecvClock& rc, float& exposed, float& xfer, float& overlap) {
+  cudaEventSynchronize(rc.X1);
+  double ex = 0;
+  for (int c = 0; c < rc.n; ++c) {
+    const float r = ev_ms(rc.R[0], rc.R[c]), a = ev_ms(rc.R[0], rc.A[c]), p = ev_ms(rc.R[0], rc.P[c]);
+    ex += std::max(0.f, a - std::max(r, p));
+  }
+  exposed = float(ex);
+  xfer = ev_ms(rc.X0, rc.X1);
+  overlap = std::max(0.f, ev_ms(rc.A[0], rc.X1));
+}
+
+struct ChunkWaitCtx {
+  RecvClock* rc;
+  cudaStream_t st;
+  const cudaEvent_t* chunk;
+};
+cudaError_t chunk_wait_cb(void* u, int c) {
+  auto* w = static_cast<ChunkWaitCtx*>(u);
+  return clock_chunk(*w->rc, c, w->st, w->chunk[c]);
+}
+struct BlockDoneCtx {
+  cudaEvent_t* ev;
+  cudaStream_t st;
+};
+cudaError_t block_done_cb(void* u, int k) {
+  auto* b = static_cast<BlockDoneCtx*>(u);
+  return cudaEventRecord(b->ev[k], b->st);
 }
 
 // ---------------------------------------------------------------- workers
@@ -467,16 +712,31 @@ const float* i2v_y(const df_ctx* ctx, const void* cbuf) {
                          : nullptr;
 }
 
-cudaError_t encode_negative(df_ctx* ctx, Inst* me, ReqState* rs, void* ebuf) {
+cudaError_t encode_negative(df_ctx* ctx, Inst* me, const int32_t* neg_ids_host, uint64_t seed, void* ebuf) {
   const size_t L = ctx->g.dit.L_txt;
   int32_t* nid = me->ids_dev + L;
-  if (!rs->neg_ids.empty()) {
-    DF_TRY(cudaMemcpyAsync(nid, rs->neg_ids.data(), L * 4, cudaMemcpyHostToDevice, me->compute));
+  if (neg_ids_host) {
+    DF_TRY(cudaMemcpyAsync(nid, neg_ids_host, L * 4, cudaMemcpyHostToDevice, me->compute));
   } else {
     g_launches->fetch_add(1);
-    DF_TRY(gen_tokens(nid, int(L), int(me->m.c.vocab), rs->req.seed, me->compute, 4));
+    DF_TRY(gen_tokens(nid, int(L), int(me->m.c.vocab), seed, me->compute, 4));
   }
   return me->m.encode(nid, static_cast<char*>(ebuf) + ctx->neg_off(), me->compute);
+}
+
+// E stand-in for one request into send buffer b (tokens from the caller or the seed).
+cudaError_t encode_request(df_ctx* ctx, Inst* me, ReqState* rs, int b) {
+  if (!rs->ids.empty()) {
+    DF_TRY(cudaMemcpyAsync(me->ids_dev, rs->ids.data(), rs->ids.size() * 4, cudaMemcpyHostToDevice, me->compute));
+  } else {
+    g_launches->fetch_add(1);
+    DF_TRY(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
+  }
+  DF_TRY(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
+  DF_TRY(encode_image(ctx, me, rs->req.seed, me->ebuf[b]));
+  if (cfg_on(rs->req.guidance))
+    DF_TRY(encode_negative(ctx, me, rs->neg_ids.empty() ? nullptr : rs->neg_ids.data(), rs->req.seed, me->ebuf[b]));
+  return cudaSuccess;
 }
 
 void e_worker(df_ctx* ctx, Inst* me) {
@@ -485,7 +745,6 @@ void e_worker(df_ctx* ctx, Inst* me) {
     ReqState* rs = nullptr;
     {
       std::lock_guard<std::mutex> lk(ctx->req_mu);
-      // only the E instance the request's sequence maps to takes it
       if (!ctx->requests->pop(rs)) rs = nullptr;
     }
     if (!rs) {
@@ -494,6 +753,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
     }
     rs->inst[0] = me->id;
     rs->t_start[0] = now_s();
+    me->busy.begin(rs->t_start[0]);
     ctx->qd_ns[0] += uint64_t((rs->t_start[0] - rs->t_submit) * 1e9);
     ctx->qd_count[0]++;
     WK(cudaEventCreate(&rs->ev[0]));
@@ -505,20 +765,17 @@ void e_worker(df_ctx* ctx, Inst* me) {
     me->enext ^= 1;
     WK(cudaStreamWaitEvent(me->compute, me->esent[b], 0));  // send buffer reuse
     WK(cudaEventRecord(rs->ev[0], me->compute));
-    if (!rs->ids.empty()) {
-      WK(cudaMemcpyAsync(me->ids_dev, rs->ids.data(), rs->ids.size() * 4, cudaMemcpyHostToDevice, me->compute));
-    } else {
-      g_launches->fetch_add(1);
-      WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
-    }
-    WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
-    WK(encode_image(ctx, me, rs->req.seed, me->ebuf[b]));
-    const bool cfgr = cfg_on(rs->req.guidance);
-    if (cfgr) WK(encode_negative(ctx, me, rs, me->ebuf[b]));
+    WK(encode_request(ctx, me, rs, b));
     WK(cudaEventRecord(rs->ev[1], me->compute));
-    // handshake: claim a receive slot on T (its posted destination address)
+    const bool cfgr = cfg_on(rs->req.guidance);
+    // handshake: claim a receive slot on T (its posted destination address); the wait
+    // for a free slot is backpressure, not E's work (Alg. 1's u_E)
+    const double tw = now_s();
+    me->busy.end(tw);
     int s = T->slots.acquire(ctx->stop);
     if (s < 0) return;
+    const double tw1 = now_s();
+    me->busy.begin(tw1);
     rs->slot[0] = s;
     WK(cudaStreamWaitEvent(me->comm, T->slots.slots[s].consumed, 0));
     df_handoff_desc d{};
@@ -532,30 +789,32 @@ void e_worker(df_ctx* ctx, Inst* me) {
     d.seq = rs->seq;
     d.edge = 0;
     Xfer* x = nullptr;
-    if (do_handoff(ctx, &d, me->compute, &x) != DF_OK) {
+    if (do_handoff(ctx, &d, plan_ctx(ctx, d.bytes), me->compute, nullptr, &x) != DF_OK) {
       worker_fail(ctx, ctx->err);
       return;
     }
     rs->x[0] = x;
     WK(cudaEventRecord(me->esent[b], me->comm));
     rs->t_end[0] = now_s();
+    me->busy.end(rs->t_end[0]);
     me->served++;
-    me->busy_ns += uint64_t((rs->t_end[0] - rs->t_start[0]) * 1e9);
-    sched_note(ctx, 0, 0u, rs->t_end[0] - rs->t_start[0]);
+    sched_note(ctx, 0, 0u, (rs->t_end[0] - rs->t_start[0]) - (tw1 - tw));
     T->inbox.push(Job{rs});  // E moves on immediately
   }
 }
 
-// T finishes a request once its compute has drained on the device: stage time from the
-// device events, profiler harvest, hand the job to D (whose stream already waits on the
-// T->D chunk events, so D may enqueue its decode right away).
+// T finishes a request once its compute has drained on the device: stage time and the E->T
+// receive clock from the device events, profiler harvest, hand the job to D (whose stream
+// waits on the T->D chunk events, so D may enqueue its decode right away).
 void t_finish(df_ctx* ctx, Inst* me, ReqState* rs, Inst* D) {
   WK(cudaEventSynchronize(rs->ev[3]));
   if (me->m.prof) me->m.prof->harvest();
   rs->t_end[1] = now_s();
   const double dev_s = ev_ms(rs->ev[2], rs->ev[3]) * 1e-3;
+  rs->stage_ms[1] = float(dev_s * 1e3);
+  clock_read(me->rclk[rs->xbuf], rs->exposed[0], rs->xfer[0], rs->overlap[0]);
+  rs->xfer[0] = ev_ms(rs->x[0]->t0, rs->x[0]->t1);  // exact: both on the producer's comm stream
   me->served++;
-  me->busy_ns += uint64_t(dev_s * 1e9);
   sched_note(ctx, 1, rs->req.steps, dev_s);
   D->inbox.push(Job{rs});
 }
@@ -563,28 +822,32 @@ void t_finish(df_ctx* ctx, Inst* me, ReqState* rs, Inst* D) {
 // One T instance.  The host enqueues request r's whole prologue + S steps + T->D send,
 // then finishes request r-1 (waits for its device completion): the compute stream always
 // holds the next request's work, so no host round trip sits between two requests on the
-// device (T starts the next request without waiting).  The conditioning cache is
+// device (T starts the next request without waiting).  The prologue consumes the
+// E->T payload chunk by chunk as it lands; the last step's head writes the latent block by
+// block and each T->D chunk is sent as soon as its block is final.  The conditioning cache is
 // one persistent buffer reused in stream order (no cudaMalloc/cudaFree per request).
 void t_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
   Cond cd;  // persistent: Model::prepare reuses its arena when it is large enough
   ReqState* pend = nullptr;
   Inst* pendD = nullptr;
+  const ChunkPlan lplan = plan_latent(ctx->g.dit, ctx->g.chunk_bytes[1]);
   for (;;) {
     Job j;
     if (pend && !me->inbox.try_pop(j)) {  // nothing queued: finish the request in flight first
       t_finish(ctx, me, pend, pendD);
       pend = nullptr;
+      if (me->inbox.size() == 0) me->busy.end(now_s());
       continue;
     }
     if (!pend && !me->inbox.pop(j, ctx->stop)) break;
     ReqState* rs = j.rs;
     rs->t_start[1] = now_s();
+    me->busy.begin(rs->t_start[1]);
     ctx->qd_ns[1] += uint64_t(std::max(0.0, rs->t_start[1] - rs->t_end[0]) * 1e9);
     ctx->qd_count[1]++;
     WK(cudaEventCreate(&rs->ev[2]));
     WK(cudaEventCreate(&rs->ev[3]));
-    WK(cudaEventCreate(&rs->ev[6]));
     const int S = int(rs->req.steps);
     int b = me->xnext;
     me->xnext ^= 1;
@@ -594,25 +857,44 @@ void t_worker(df_ctx* ctx, Inst* me) {
     WK(cudaEventRecord(rs->ev[2], me->compute));
     g_launches->fetch_add(1);
     WK(gen_noise(x, latent_elems(me->m.c), rs->req.seed, me->compute));  // x0 does not need ctx
-    // consumer ready for ctx; wait per chunk (device-side), then the prologue
-    WK(cudaEventRecord(rs->ev[6], me->compute));
+    // the prologue consumes ctx chunk by chunk as it lands (device-side waits)
     Xfer* x0 = rs->x[0];
-    for (uint32_t c = 0; c < x0->nchunks; ++c) WK(cudaStreamWaitEvent(me->compute, x0->chunk_ev[c], 0));
+    RecvClock& rc = me->rclk[b];
+    WK(clock_probe(rc, int(x0->nchunks), x0->ready_ev.data(), x0->t0, x0->t1));
+    const bool cfgr = cfg_on(rs->req.guidance);
+    const ChunkPlan cplan = plan_ctx(ctx, ctx->payload(cfgr));
+    ChunkWaitCtx wc{&rc, me->compute, x0->chunk_ev.data()};
+    ChunkHook hook;
+    hook.rows_per_chunk = rows_per_chunk(ctx, cplan);
+    hook.nchunks = int(x0->nchunks);
+    hook.wait = chunk_wait_cb;
+    hook.user = &wc;
     std::vector<float> sig = sigmas_host(S, rs->req.shift);
     const void* cbuf = me->slots.slots[rs->slot[0]].buf;
-    const bool cfgr = cfg_on(rs->req.guidance);
     WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->neg_off() : nullptr,
-                     cfgr ? rs->req.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf)));
-    WK(cudaEventRecord(me->slots.slots[rs->slot[0]].consumed, me->compute));
+                     cfgr ? rs->req.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf), &hook));
+    // the slot is free once the prologue and the destination hash (aux stream) both read it
+    {
+      cudaEvent_t& consumed = me->slots.slots[rs->slot[0]].consumed;
+      WK(cudaEventRecord(consumed, me->compute));
+      WK(cudaStreamWaitEvent(me->aux, consumed, 0));
+      if (x0->t_hash) WK(cudaStreamWaitEvent(me->aux, x0->t_hash, 0));
+      WK(cudaEventRecord(consumed, me->aux));
+    }
     me->slots.release(rs->slot[0]);  // producer's comm stream waits on `consumed` before reuse
-    for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
+    BlockDoneCtx bd{me->hb_ev[b], me->compute};
+    BlockHook bh;
+    bh.lb = lplan.lb;
+    bh.done = block_done_cb;
+    bh.user = &bd;
+    for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute, i == S - 1 ? &bh : nullptr));
     WK(cudaEventRecord(rs->ev[3], me->compute));
     // r-1 drains while r is already queued behind it; finishing it before claiming a D slot
     // means this worker never holds an unsent D slot while it blocks (no slot deadlock with
     // several T instances sharing one D)
     if (pend) t_finish(ctx, me, pend, pendD);
     pend = nullptr;
-    // T -> D: claim a D slot, send the final latent in per-frame chunks
+    // T -> D: claim a D slot, send the final latent chunk by chunk as its blocks are final
     const int did = pick(ctx, DF_D, rs->seq);
     Inst* D = ctx->inst[did].get();
     rs->inst[2] = did;
@@ -631,7 +913,7 @@ void t_worker(df_ctx* ctx, Inst* me) {
     d.seq = rs->seq;
     d.edge = 1;
     Xfer* xx = nullptr;
-    if (do_handoff(ctx, &d, me->compute, &xx) != DF_OK) {
+    if (do_handoff(ctx, &d, lplan, me->compute, lplan.n > 1 ? me->hb_ev[b] : nullptr, &xx) != DF_OK) {
       worker_fail(ctx, ctx->err);
       return;
     }
@@ -641,6 +923,7 @@ void t_worker(df_ctx* ctx, Inst* me) {
     pendD = D;
   }
   if (pend) t_finish(ctx, me, pend, pendD);
+  me->busy.end(now_s());
   WK(cudaStreamSynchronize(me->compute));
   cd.mem.release();
 }
@@ -648,39 +931,45 @@ void t_worker(df_ctx* ctx, Inst* me) {
 void d_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
   Job j;
-  const df_dit_cfg& c = me->m.c;
+  const ChunkPlan lplan = plan_latent(ctx->g.dit, ctx->g.chunk_bytes[1]);
   while (me->inbox.pop(j, ctx->stop)) {
     ReqState* rs = j.rs;
     rs->t_start[2] = now_s();
+    me->busy.begin(rs->t_start[2]);
     ctx->qd_ns[2] += uint64_t(std::max(0.0, rs->t_start[2] - rs->t_end[1]) * 1e9);
     ctx->qd_count[2]++;
     WK(cudaEventCreate(&rs->ev[4]));
     WK(cudaEventCreate(&rs->ev[5]));
-    WK(cudaEventCreate(&rs->ev[7]));
-    WK(cudaEventRecord(rs->ev[7], me->compute));
     Xfer* x1 = rs->x[1];
-    for (uint32_t k = 0; k < x1->nchunks; ++k) WK(cudaStreamWaitEvent(me->compute, x1->chunk_ev[k], 0));
+    RecvClock& rc = me->rclk[0];
+    WK(clock_probe(rc, int(x1->nchunks), x1->ready_ev.data(), x1->t0, x1->t1));
     WK(cudaEventRecord(rs->ev[4], me->compute));
-    WK(me->m.decode((const float*)me->slots.slots[rs->slot[1]].buf, me->dout, me->compute));
+    const float* lat = (const float*)me->slots.slots[rs->slot[1]].buf;
+    for (uint32_t k = 0; k < x1->nchunks; ++k) {  // D decodes each chunk as it lands (a14)
+      WK(clock_chunk(rc, int(k), me->compute, x1->chunk_ev[k]));
+      WK(me->m.decode_block(lat, me->dout, lplan.lb, int(k), me->compute));
+    }
     WK(cudaEventRecord(me->slots.slots[rs->slot[1]].consumed, me->compute));
     WK(cudaEventRecord(rs->ev[5], me->compute));
     if (rs->req.out_host)
-      WK(cudaMemcpyAsync(me->stage_host, me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
+      WK(cudaMemcpyAsync(me->stage_host[0], me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
     WK(cudaStreamSynchronize(me->compute));
     if (x1->t_hash) WK(cudaEventSynchronize(x1->t_hash));
     me->slots.release(rs->slot[1]);
     if (rs->req.out_host && rs->req.out_bytes >= ctx->out_bytes)
-      std::memcpy(rs->req.out_host, me->stage_host, ctx->out_bytes);
+      std::memcpy(rs->req.out_host, me->stage_host[0], ctx->out_bytes);
+    clock_read(rc, rs->exposed[1], rs->xfer[1], rs->overlap[1]);
+    rs->xfer[1] = ev_ms(x1->t0, x1->t1);
+    rs->stage_ms[2] = ev_ms(rs->ev[4], rs->ev[5]);
     rs->t_end[2] = now_s();
+    me->busy.end(rs->t_end[2]);
     me->served++;
-    me->busy_ns += uint64_t((rs->t_end[2] - rs->t_start[2]) * 1e9);
     sched_note(ctx, 2, 0u, rs->t_end[2] - rs->t_start[2]);
     {
       std::lock_guard<std::mutex> lk(ctx->done_mu);
       while (!ctx->done->push(rs)) std::this_thread::yield();
     }
     ctx->done_cv.notify_all();
-    (void)c;
   }
 }
 
@@ -703,22 +992,20 @@ void fill_completion(df_ctx* ctx, ReqState* rs, df_completion* o) {
   o->out_view = rs->req.out_host;
   o->out_view_bytes = rs->req.out_host ? ctx->out_bytes : 0;
   o->stage_ms[0] = ev_ms(rs->ev[0], rs->ev[1]);
-  o->stage_ms[1] = ev_ms(rs->ev[2], rs->ev[3]);
-  o->stage_ms[2] = ev_ms(rs->ev[4], rs->ev[5]);
+  o->stage_ms[1] = rs->stage_ms[1];
+  o->stage_ms[2] = rs->stage_ms[2];
   for (int e = 0; e < 2; ++e) {
     Xfer* x = rs->x[e];
     if (!x) continue;
-    o->xfer_ms[e] = ev_ms(x->t0, x->t1);
-    // exposed: consumer ready (R) -> last chunk landed (A), clamped at 0
-    float ex = ev_ms(rs->ev[e == 0 ? 6 : 7], x->t1);
-    o->exposed_ms[e] = ex > 0.f ? ex : 0.f;
+    o->xfer_ms[e] = rs->xfer[e];
+    o->exposed_ms[e] = rs->exposed[e];
+    o->overlap_ms[e] = rs->overlap[e];
     if (x->hashed) {
       if (x->t_hash) cudaEventSynchronize(x->t_hash);
       o->hash_src[e] = x->hash_dev[0];
       o->hash_dst[e] = x->hash_dev[1];
     }
   }
-  (void)ctx;
 }
 
 void free_req(ReqState* rs) {
@@ -734,27 +1021,21 @@ void free_req(ReqState* rs) {
 // ================================================================== one process per GPU
 // (world > 1): instances of other ranks are reached through the shared-memory plane
 // (plane.h) and CUDA IPC.  The protocol per edge, for a consumer instance c:
-//   consumer: owns n_slots receive buffers + an interprocess "consumed" event and
-//             PL_MAX_CHUNKS interprocess chunk events per slot; posts free slot ids in
-//             its free ring (the destination-address handshake).
-//   producer: pops a free slot (empty ring = backpressure), makes its comm stream wait on
-//             the slot's consumed event and on its own compute, copies the payload into
-//             the peer slot in chunks, records the slot's chunk events, pushes a 128-byte
-//             MetaRec into c's inbox and moves on.
+//   consumer: owns n_slots receive buffers (+ a 64-byte trailer each) and an interprocess
+//             "consumed" event per slot; posts free slot ids in its free ring (the
+//             destination-address handshake).
+//   producer: pops a free slot (empty ring = backpressure), publishes the IPC handles of its
+//             own ready / start / chunk events for (c, slot) into c's slot record, makes its
+//             comm stream wait on `consumed`, copies the payload into the peer slot chunk by
+//             chunk, hashes the source into the slot trailer (one peer store), and pushes a
+//             fixed-size MetaRec into c's inbox.  Nothing on this path synchronises the host:
+//             E pushes the record right away and moves on; T pushes it when its
+//             compute of the request has drained (it is already enqueued by then).
 //   consumer: pops the inbox, makes its compute stream wait per chunk (device-side),
-//             consumes, records consumed, re-posts the slot.
+//             consumes chunk by chunk, hashes the slot and reads the trailer on its stream,
+//             records consumed, re-posts the slot, and reads the clocks and hashes once its
+//             own completion event fired.
 namespace {
-
-int mp_nchunks(uint64_t bytes, uint64_t& chunk) {
-  if (chunk == 0 || chunk >= bytes) chunk = bytes;
-  chunk = (chunk + 15) & ~uint64_t(15);
-  uint64_t n = (bytes + chunk - 1) / chunk;
-  if (n > uint64_t(PL_MAX_CHUNKS)) {
-    chunk = ((bytes + PL_MAX_CHUNKS - 1) / PL_MAX_CHUNKS + 15) & ~uint64_t(15);
-    n = (bytes + chunk - 1) / chunk;
-  }
-  return int(n);
-}
 
 void mp_sleep() { std::this_thread::sleep_for(std::chrono::microseconds(20)); }
 
@@ -769,16 +1050,14 @@ df_ctx::View* mp_view(df_ctx* ctx, int ci) {
     mp_sleep();
   }
   Inst* I = ctx->inst[ci].get();
+  v.slot_bytes = ip.slot_bytes;
   for (uint32_t s = 0; s < ip.n_slots; ++s) {
     if (I->local) {
       v.buf[s] = I->slots.slots[s].buf;
       v.consumed[s] = I->ipc_consumed[s];
-      for (int c = 0; c < PL_MAX_CHUNKS; ++c) v.chunk[s][c] = I->ipc_chunk[s][c];
     } else {
       if (cudaIpcOpenMemHandle(&v.buf[s], ip.slot_mem[s], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return nullptr;
       if (cudaIpcOpenEventHandle(&v.consumed[s], ip.consumed[s]) != cudaSuccess) return nullptr;
-      for (int c = 0; c < PL_MAX_CHUNKS; ++c)
-        if (cudaIpcOpenEventHandle(&v.chunk[s][c], ip.chunk[s][c]) != cudaSuccess) return nullptr;
       v.remote = true;
     }
   }
@@ -786,7 +1065,7 @@ df_ctx::View* mp_view(df_ctx* ctx, int ci) {
   return &v;
 }
 
-// Publish a local consumer instance's slots and events into the plane.
+// Publish a local consumer instance's slots and consumed events into the plane.
 cudaError_t mp_publish(df_ctx* ctx, Inst& I, size_t slot_bytes) {
   InstPlane& ip = ctx->seg->inst[I.id];
   ip.n_slots = ctx->g.n_slots;
@@ -797,10 +1076,6 @@ cudaError_t mp_publish(df_ctx* ctx, Inst& I, size_t slot_bytes) {
     DF_TRY(cudaEventCreateWithFlags(&I.ipc_consumed[s], cudaEventDisableTiming | cudaEventInterprocess));
     DF_TRY(cudaEventRecord(I.ipc_consumed[s], I.compute));
     DF_TRY(cudaIpcGetEventHandle(&ip.consumed[s], I.ipc_consumed[s]));
-    for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
-      DF_TRY(cudaEventCreateWithFlags(&I.ipc_chunk[s][c], cudaEventDisableTiming | cudaEventInterprocess));
-      DF_TRY(cudaIpcGetEventHandle(&ip.chunk[s][c], I.ipc_chunk[s][c]));
-    }
   }
   DF_TRY(cudaStreamSynchronize(I.compute));
   for (uint32_t s = 0; s < ctx->g.n_slots; ++s)
@@ -809,10 +1084,59 @@ cudaError_t mp_publish(df_ctx* ctx, Inst& I, size_t slot_bytes) {
   return cudaSuccess;
 }
 
-// Producer: claim a slot of consumer `ci`, copy `bytes` after prod_stream's work, post meta.
-// Returns false on stop / error (error recorded).
-bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, uint64_t bytes, uint64_t chunk, cudaStream_t prod,
-             MetaRec m, uint32_t edge) {
+// The producer's events for (consumer ci, slot s): created on first use on the producer's
+// device (interprocess events must not time; the consumer times them on its own clock).
+SendSet* send_set(Inst* me, int ci, int s) {
+  SendSet*& ss = me->sendset[ci][s];
+  if (ss) return ss;
+  auto* n = new SendSet();
+  const unsigned fl = cudaEventDisableTiming | cudaEventInterprocess;
+  bool ok = true;
+  for (int c = 0; c < PL_MAX_CHUNKS && ok; ++c) {
+    ok = cudaEventCreateWithFlags(&n->ready[c], fl) == cudaSuccess &&
+         cudaEventCreateWithFlags(&n->chunk[c], fl) == cudaSuccess &&
+         cudaIpcGetEventHandle(&n->h.ready[c], n->ready[c]) == cudaSuccess &&
+         cudaIpcGetEventHandle(&n->h.chunk[c], n->chunk[c]) == cudaSuccess;
+  }
+  ok = ok && cudaEventCreateWithFlags(&n->start, fl) == cudaSuccess &&
+       cudaIpcGetEventHandle(&n->h.start, n->start) == cudaSuccess;
+  if (!ok) {
+    delete n;
+    return nullptr;
+  }
+  n->h.producer = me->id;
+  ss = n;
+  return ss;
+}
+
+// The consumer's handles on the events of the transfer in its slot s (published by producer p).
+OpenSet* open_set(df_ctx* ctx, Inst* me, int p, int s) {
+  OpenSet& os = me->opened[p][s];
+  if (os.open) return &os;
+  Inst* P = ctx->inst[p].get();
+  if (P->local) {  // same process: the producer's own events
+    SendSet* ss = P->sendset[me->id][s];
+    if (!ss) return nullptr;
+    for (int c = 0; c < PL_MAX_CHUNKS; ++c) os.ready[c] = ss->ready[c], os.chunk[c] = ss->chunk[c];
+    os.start = ss->start;
+  } else {
+    const XferEvHandles& h = ctx->seg->inst[me->id].xev[s];
+    for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
+      if (cudaIpcOpenEventHandle(&os.ready[c], h.ready[c]) != cudaSuccess) return nullptr;
+      if (cudaIpcOpenEventHandle(&os.chunk[c], h.chunk[c]) != cudaSuccess) return nullptr;
+    }
+    if (cudaIpcOpenEventHandle(&os.start, h.start) != cudaSuccess) return nullptr;
+    os.ipc = true;
+  }
+  os.open = true;
+  return &os;
+}
+
+// Producer: claim a slot of consumer `ci` and enqueue the chunked copy of `src` (after
+// prod's queued work, or chunk by chunk after piece_ready[c]) on the comm stream.  Fills
+// m.slot / nchunks / src; the caller posts m (mp_post).  Returns false on stop / error.
+bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, const ChunkPlan& plan, cudaStream_t prod,
+             const cudaEvent_t* piece_ready, MetaRec& m, uint32_t edge) {
   df_ctx::View* v = mp_view(ctx, ci);
   if (!v) {
     if (!ctx->stop) worker_fail(ctx, "mp_send: cannot open the consumer's IPC handles");
@@ -828,42 +1152,49 @@ bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, uint64_t bytes, uin
     if (e != cudaSuccess) worker_fail(ctx, std::string("mp_send: ") + what + ": " + cudaGetErrorString(e));
     return e == cudaSuccess;
   };
-  cudaEvent_t ready;
-  if (!chk(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event")) return false;
-  if (!chk(cudaEventRecord(ready, prod), "record")) return false;
-  if (!chk(cudaStreamWaitEvent(me->comm, ready, 0), "wait")) return false;
-  cudaEventDestroy(ready);
+  SendSet* ss = send_set(me, ci, int(s));
+  if (!ss) return chk(cudaErrorUnknown, "interprocess events");
+  ss->h.nchunks = uint32_t(plan.n);
+  std::memcpy(&ip.xev[s], &ss->h, sizeof(XferEvHandles));  // read by c after it pops m (release below)
   if (!chk(cudaStreamWaitEvent(me->comm, v->consumed[s], 0), "wait consumed")) return false;
-  if (ctx->g.jitter_p > 0.f && ctx->g.jitter_delay_s > 0.f && (jitter_edges() >> edge & 1u)) {  // P:L142, R23
-    uint32_t c[4] = {uint32_t(m.seq), uint32_t(m.seq >> 32), edge, 3u};
-    philox_host(c, uint32_t(ctx->g.jitter_seed), uint32_t(ctx->g.jitter_seed >> 32));
-    if (double(c[0]) < double(ctx->g.jitter_p) * 4294967296.0) {
-      if (!chk(delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), me->comm), "delay")) return false;
-    }
+  if (!piece_ready) {
+    cudaEvent_t ready;
+    if (!chk(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event")) return false;
+    if (!chk(cudaEventRecord(ready, prod), "record")) return false;
+    if (!chk(cudaStreamWaitEvent(me->comm, ready, 0), "wait")) return false;
+    cudaEventDestroy(ready);
   }
-  unsigned long long* h = me->mp_hash;
-  if (ctx->g.handoff_mode & DF_HASH) {
-    g_launches->fetch_add(1);
-    if (!chk(payload_hash(src, bytes, 0, h, me->comm), "hash")) return false;
-  }
-  int n = mp_nchunks(bytes, chunk);
-  for (int c = 0; c < n; ++c) {
-    uint64_t off = uint64_t(c) * chunk, sz = std::min<uint64_t>(chunk, bytes - off);
-    if (!chk(cudaMemcpyAsync(static_cast<char*>(v->buf[s]) + off, static_cast<const char*>(src) + off, sz,
-                             cudaMemcpyDeviceToDevice, me->comm), "copy"))
+  const bool delay = jitter_draw(ctx, m.seq, edge);
+  const int jc = std::min<int>(int(ctx->g.jitter_chunk), plan.n - 1);
+  char* dst = static_cast<char*>(v->buf[s]);
+  for (int c = 0; c < plan.n; ++c) {
+    if (piece_ready && !chk(cudaStreamWaitEvent(me->comm, piece_ready[c], 0), "wait piece")) return false;
+    if (!chk(cudaEventRecord(ss->ready[c], me->comm), "ready")) return false;
+    if (delay && c == jc &&
+        !chk(delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), me->comm), "delay"))  // P:L142, R23
       return false;
-    if (!chk(cudaEventRecord(v->chunk[s][c], me->comm), "chunk event")) return false;
+    if (c == 0 && !chk(cudaEventRecord(ss->start, me->comm), "start")) return false;
+    // IPC-mapped peer memory is addressed from this device: same-device copy kinds
+    if (!chk(copy_piece(plan, c, dst, me->device, src, me->device, me->comm), "copy")) return false;
+    if (c == plan.n - 1 && (ctx->g.handoff_mode & DF_HASH)) {  // source hash into the slot trailer
+      g_launches->fetch_add(1);
+      auto* trailer = reinterpret_cast<unsigned long long*>(dst + v->slot_bytes);
+      if (!chk(payload_hash(src, plan.bytes, 0, trailer, me->comm), "hash")) return false;
+    }
+    if (!chk(cudaEventRecord(ss->chunk[c], me->comm), "chunk event")) return false;
   }
-  if (ctx->g.handoff_mode & DF_SYNC) {  // P:L151 comparison mode: the producer waits for delivery
-    if (!chk(cudaStreamSynchronize(me->comm), "sync")) return false;
-  }
-  if (ctx->g.handoff_mode & DF_HASH) {
-    if (!chk(cudaStreamSynchronize(me->comm), "hash sync")) return false;
-    m.hash_src = *h;
-  }
+  if ((ctx->g.handoff_mode & DF_SYNC) &&  // P:L151 comparison mode: the producer waits for delivery
+      !chk(cudaStreamWaitEvent(prod, ss->chunk[plan.n - 1], 0), "sync"))
+    return false;
   m.slot = s;
-  m.nchunks = uint32_t(n);
-  m.chunk_bytes = uint32_t(chunk);
+  m.nchunks = uint32_t(plan.n);
+  m.chunk_bytes = uint32_t(plan.chunk);
+  m.src = me->id;
+  return true;
+}
+
+bool mp_post(df_ctx* ctx, int ci, const MetaRec& m) {
+  InstPlane& ip = ctx->seg->inst[ci];
   while (!ip.inbox.push(m)) {
     if (ctx->stop) return false;
     mp_sleep();
@@ -871,26 +1202,25 @@ bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, uint64_t bytes, uin
   return true;
 }
 
+bool mp_try_recv(df_ctx* ctx, Inst* me, MetaRec& m) { return ctx->seg->inst[me->id].inbox.pop(m); }
+
 bool mp_recv(df_ctx* ctx, Inst* me, MetaRec& m) {
-  InstPlane& ip = ctx->seg->inst[me->id];
-  while (!ip.inbox.pop(m)) {
+  while (!mp_try_recv(ctx, me, m)) {
     if (ctx->stop) return false;
     mp_sleep();
   }
   return true;
 }
 
-// Consumer: make `st` wait for every chunk of slot m.slot (device-side), then hash it.
-cudaError_t mp_wait_chunks(df_ctx* ctx, Inst* me, const MetaRec& m, cudaStream_t st, uint64_t bytes) {
-  for (uint32_t c = 0; c < m.nchunks; ++c) DF_TRY(cudaStreamWaitEvent(st, me->ipc_chunk[m.slot][c], 0));
+// Consumer, after its last read of slot s on `st`: verify inputs (destination hash into
+// rc.hash[1], the producer's hash from the trailer into rc.hash[0]), record consumed, re-post.
+cudaError_t mp_finish_slot(df_ctx* ctx, Inst* me, RecvClock& rc, uint32_t s, uint64_t bytes, cudaStream_t st) {
   if (ctx->g.handoff_mode & DF_HASH) {
+    const char* buf = static_cast<const char*>(me->slots.slots[s].buf);
     g_launches->fetch_add(1);
-    DF_TRY(payload_hash(me->slots.slots[m.slot].buf, bytes, 0, me->mp_hash + 1, st));
+    DF_TRY(payload_hash(buf, bytes, 0, rc.hash + 1, st));
+    DF_TRY(cudaMemcpyAsync(rc.hash, buf + me->slot_cap, 8, cudaMemcpyDeviceToHost, st));
   }
-  return cudaSuccess;
-}
-
-cudaError_t mp_release_slot(df_ctx* ctx, Inst* me, uint32_t s, cudaStream_t st) {
   DF_TRY(cudaEventRecord(me->ipc_consumed[s], st));
   InstPlane& ip = ctx->seg->inst[me->id];
   while (!ip.free_slots.push(s)) std::this_thread::sleep_for(std::chrono::microseconds(20));
@@ -899,9 +1229,6 @@ cudaError_t mp_release_slot(df_ctx* ctx, Inst* me, uint32_t s, cudaStream_t st) 
 
 void mp_e_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
   while (!ctx->stop.load()) {
     ReqState* rs = nullptr;
     {
@@ -924,154 +1251,278 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
     m.flags = rs->req.out_host ? 1u : 0u;  // bit0: deliver the decoded output
     m.t_submit = rs->t_submit;
     m.t_start_e = now_s();
+    me->busy.begin(m.t_start_e);
     const int tid = pick(ctx, DF_T, rs->seq);
     int b = me->enext;
     me->enext ^= 1;
     WK(cudaStreamWaitEvent(me->compute, me->esent[b], 0));
-    WK(cudaEventRecord(e0, me->compute));
-    if (!rs->ids.empty()) {
-      WK(cudaMemcpyAsync(me->ids_dev, rs->ids.data(), rs->ids.size() * 4, cudaMemcpyHostToDevice, me->compute));
-    } else {
-      g_launches->fetch_add(1);
-      WK(gen_tokens(me->ids_dev, int(me->m.c.L_txt), int(me->m.c.vocab), rs->req.seed, me->compute));
-    }
-    WK(me->m.encode(me->ids_dev, me->ebuf[b], me->compute));
-    WK(encode_image(ctx, me, rs->req.seed, me->ebuf[b]));
+    WK(encode_request(ctx, me, rs, b));
     const bool cfgr = cfg_on(rs->req.guidance);
-    if (cfgr) WK(encode_negative(ctx, me, rs, me->ebuf[b]));
     m.guidance = cfgr ? rs->req.guidance : 1.f;
-    WK(cudaEventRecord(e1, me->compute));
     m.t_end_e = now_s();
-    if (!mp_send(ctx, me, tid, me->ebuf[b], ctx->payload(cfgr), ctx->g.chunk_bytes[0], me->compute, m,
-                 0)) {
+    m.stage_ms_e = float((m.t_end_e - m.t_start_e) * 1e3);  // host enqueue time (E never waits)
+    me->busy.end(m.t_end_e);
+    const uint64_t bytes = ctx->payload(cfgr);
+    if (!mp_send(ctx, me, tid, me->ebuf[b], plan_ctx(ctx, bytes), me->compute, nullptr, m, 0)) {
       free_req(rs);
       return;
     }
     WK(cudaEventRecord(me->esent[b], me->comm));
+    if (!mp_post(ctx, tid, m)) {  // E moves on immediately
+      free_req(rs);
+      return;
+    }
     me->served++;
     free_req(rs);  // the request now lives in T's inbox (another process or this one)
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+}
+
+// Per in-flight request of a multi-process T worker (one per latent buffer).
+struct MpTReq {
+  MetaRec in{}, out{};
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int did = -1;
+  bool live = false;
+};
+
+// Finish request `r` (its compute and T->D copies are enqueued): wait for its compute, verify
+// the E->T hashes, then post its record to D (D's stream waits on the chunk events).
+bool mp_t_finish(df_ctx* ctx, Inst* me, MpTReq& r, int b) {
+  if (cudaEventSynchronize(r.t1) != cudaSuccess) {
+    worker_fail(ctx, "mp_t_worker: request compute failed");
+    return false;
+  }
+  if (me->m.prof) me->m.prof->harvest();
+  RecvClock& rc = me->rclk[b];
+  MetaRec& o = r.out;
+  clock_read(rc, o.exposed_e2t, o.xfer_e2t, o.overlap_e2t);
+  o.stage_ms_t = ev_ms(r.t0, r.t1);
+  o.t_end_t = now_s();
+  if (ctx->g.handoff_mode & DF_HASH) {  // edge-0 check: the ctx we consumed is what E sent
+    o.hash_src_e2t = rc.hash[0];
+    o.hash_dst_e2t = rc.hash[1];
+    if (rc.hash[0] != rc.hash[1]) {
+      worker_fail(ctx, "mp_t_worker: E->T payload hash mismatch");
+      return false;
+    }
+  }
+  sched_note(ctx, 1, o.steps, o.stage_ms_t * 1e-3);
+  me->served++;
+  r.live = false;
+  return mp_post(ctx, r.did, o);
 }
 
 void mp_t_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
-  cudaEvent_t r0, w0, t0, t1;
-  cudaEventCreate(&r0);
-  cudaEventCreate(&w0);
-  cudaEventCreate(&t0);
-  cudaEventCreate(&t1);
-  MetaRec m;
+  MpTReq req[2];
+  for (auto& r : req) {
+    cudaEventCreate(&r.t0);
+    cudaEventCreate(&r.t1);
+  }
   Cond cd;  // persistent conditioning arena, reused in stream order (as in t_worker)
-  while (mp_recv(ctx, me, m)) {
+  const ChunkPlan lplan = plan_latent(ctx->g.dit, ctx->g.chunk_bytes[1]);
+  int pend = -1;  // latent buffer of the request whose record is not posted yet
+  for (;;) {
+    MetaRec m;
+    if (pend >= 0 && !mp_try_recv(ctx, me, m)) {  // nothing queued: finish the one in flight
+      if (!mp_t_finish(ctx, me, req[pend], pend)) return;
+      pend = -1;
+      me->busy.end(now_s());
+      continue;
+    }
+    if (pend < 0 && !mp_recv(ctx, me, m)) break;
+    const double ts = now_s();
+    me->busy.begin(ts);
     const int S = int(m.steps);
-    int b = me->xnext;
+    const int b = me->xnext;
     me->xnext ^= 1;
+    MpTReq& r = req[b];
+    r.in = m;
     float* x = me->xbuf[b];
+    OpenSet* os = open_set(ctx, me, m.src, int(m.slot));
+    if (!os) {
+      worker_fail(ctx, "mp_t_worker: cannot open the producer's events");
+      return;
+    }
     WK(cudaStreamWaitEvent(me->compute, me->xsent[b], 0));
-    WK(cudaEventRecord(t0, me->compute));
+    WK(cudaEventRecord(r.t0, me->compute));
     g_launches->fetch_add(1);
     WK(gen_noise(x, latent_elems(me->m.c), m.seed, me->compute));
-    WK(cudaEventRecord(r0, me->compute));  // consumer ready for ctx
     const bool cfgr = cfg_on(m.guidance);
-    WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->payload(cfgr)));
-    WK(cudaEventRecord(w0, me->compute));  // ctx landed
+    const uint64_t bytes = ctx->payload(cfgr);
+    const ChunkPlan cplan = plan_ctx(ctx, bytes);
+    RecvClock& rc = me->rclk[b];
+    const int n = int(m.nchunks);
+    WK(clock_probe(rc, n, os->ready, os->start, os->chunk[n - 1]));
+    ChunkWaitCtx wc{&rc, me->compute, os->chunk};
+    ChunkHook hook;
+    hook.rows_per_chunk = rows_per_chunk(ctx, cplan);
+    hook.nchunks = n;
+    hook.wait = chunk_wait_cb;
+    hook.user = &wc;
     std::vector<float> sig = sigmas_host(S, m.shift);
     const void* cbuf = me->slots.slots[m.slot].buf;
     WK(me->m.prepare(cbuf, sig.data(), S, me->compute, &cd, cfgr ? (const char*)cbuf + ctx->neg_off() : nullptr,
-                     cfgr ? m.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf)));
-    WK(mp_release_slot(ctx, me, m.slot, me->compute));
-    for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute));
-    WK(cudaEventRecord(t1, me->compute));
-    WK(cudaStreamSynchronize(me->compute));
-    if (me->m.prof) me->m.prof->harvest();
-    float ms = 0.f, ex = 0.f;
-    cudaEventElapsedTime(&ms, t0, t1);
-    cudaEventElapsedTime(&ex, r0, w0);
-    MetaRec o = m;
-    o.inst_t = me->id;
-    o.t_end_t = now_s();
-    o.stage_ms_t = ms;
-    o.exposed_t = ex > 0.f ? ex : 0.f;
-    o.hash_src = 0;
-    // edge-0 check: the ctx we received must hash to what E sent
-    if ((ctx->g.handoff_mode & DF_HASH) && me->mp_hash[1] != m.hash_src) {
-      worker_fail(ctx, "mp_t_worker: E->T payload hash mismatch");
-      return;
-    }
-    const int did = pick(ctx, DF_D, m.seq);
-    if (!mp_send(ctx, me, did, x, ctx->lat_bytes, ctx->g.chunk_bytes[1], me->compute, o, 1)) return;
+                     cfgr ? m.guidance : 1.f, i2v_clip(ctx, cbuf), i2v_y(ctx, cbuf), &hook));
+    WK(mp_finish_slot(ctx, me, rc, m.slot, bytes, me->compute));
+    BlockDoneCtx bd{me->hb_ev[b], me->compute};
+    BlockHook bh;
+    bh.lb = lplan.lb;
+    bh.done = block_done_cb;
+    bh.user = &bd;
+    for (int i = 0; i < S; ++i) WK(me->m.step(cd, i, x, nullptr, me->compute, i == S - 1 ? &bh : nullptr));
+    WK(cudaEventRecord(r.t1, me->compute));
+    // r-1 drains while r is queued behind it; finishing (posting) it before claiming a D slot
+    // for r means this worker never holds an unposted D slot while it blocks on backpressure
+    if (pend >= 0 && !mp_t_finish(ctx, me, req[pend], pend)) return;
+    pend = -1;
+    r.out = m;
+    r.out.inst_t = me->id;
+    r.out.t_start_t = ts;
+    r.did = pick(ctx, DF_D, m.seq);
+    if (!mp_send(ctx, me, r.did, x, lplan, me->compute, lplan.n > 1 ? me->hb_ev[b] : nullptr, r.out, 1)) return;
     WK(cudaEventRecord(me->xsent[b], me->comm));
-    me->served++;
+    r.live = true;
+    pend = b;
   }
+  if (pend >= 0) mp_t_finish(ctx, me, req[pend], pend);
+  me->busy.end(now_s());
   cudaStreamSynchronize(me->compute);
   cd.mem.release();
+  for (auto& r : req) {
+    cudaEventDestroy(r.t0);
+    cudaEventDestroy(r.t1);
+  }
+}
+
+// The D worker keeps up to 4 decodes in flight (its host never blocks on one transfer while
+// others could be enqueued) and completes them in order as their device events fire.
+struct MpDReq {
+  MetaRec m{};
+  cudaEvent_t d0 = nullptr, d1 = nullptr, done = nullptr;
+  double t_start = 0;
+};
+
+void mp_d_complete(df_ctx* ctx, Inst* me, MpDReq& q, int k) {
+  RecvClock& rc = me->rclk[k];
+  const MetaRec& m = q.m;
+  auto rs = new ReqState();
+  rs->pre = true;
+  if (m.flags & 1u) {
+    rs->outcopy.resize(ctx->out_bytes / 4);
+    std::memcpy(rs->outcopy.data(), me->stage_host[k], ctx->out_bytes);
+  }
+  df_completion& o = rs->comp;
+  std::memset(&o, 0, sizeof(o));
+  o.id = {m.id_lo, m.id_hi};
+  o.status = DF_OK;
+  o.user_tag = m.user_tag;
+  o.inst[0] = m.inst_e;
+  o.inst[1] = m.inst_t;
+  o.inst[2] = me->id;
+  o.t_submit = m.t_submit;
+  o.t_start[0] = m.t_start_e;
+  o.t_end[0] = m.t_end_e;
+  o.t_start[1] = m.t_start_t;
+  o.t_end[1] = m.t_end_t;
+  o.t_start[2] = q.t_start;
+  o.t_end[2] = o.t_done = now_s();
+  o.stage_ms[0] = m.stage_ms_e;
+  o.stage_ms[1] = m.stage_ms_t;
+  o.stage_ms[2] = ev_ms(q.d0, q.d1);
+  o.exposed_ms[0] = m.exposed_e2t;
+  o.xfer_ms[0] = m.xfer_e2t;
+  o.overlap_ms[0] = m.overlap_e2t;
+  clock_read(rc, o.exposed_ms[1], o.xfer_ms[1], o.overlap_ms[1]);
+  if (!rs->outcopy.empty()) {
+    o.out_view = rs->outcopy.data();
+    o.out_view_bytes = ctx->out_bytes;
+  }
+  if (ctx->g.handoff_mode & DF_HASH) {
+    o.hash_src[0] = m.hash_src_e2t;
+    o.hash_dst[0] = m.hash_dst_e2t;
+    o.hash_src[1] = rc.hash[0];
+    o.hash_dst[1] = rc.hash[1];
+    if (rc.hash[0] != rc.hash[1]) {
+      delete rs;
+      worker_fail(ctx, "mp_d_worker: T->D payload hash mismatch");
+      return;
+    }
+  }
+  me->served++;
+  sched_note(ctx, 2, 0u, o.t_end[2] - o.t_start[2]);
+  {
+    std::lock_guard<std::mutex> lk(ctx->done_mu);
+    while (!ctx->done->push(rs)) std::this_thread::yield();
+  }
+  ctx->done_cv.notify_all();
 }
 
 void mp_d_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
-  cudaEvent_t r0, w0, d0, d1;
-  cudaEventCreate(&r0);
-  cudaEventCreate(&w0);
-  cudaEventCreate(&d0);
-  cudaEventCreate(&d1);
-  MetaRec m;
-  while (mp_recv(ctx, me, m)) {
-    double t_start = now_s();
-    WK(cudaEventRecord(r0, me->compute));
-    WK(mp_wait_chunks(ctx, me, m, me->compute, ctx->lat_bytes));
-    WK(cudaEventRecord(w0, me->compute));
-    WK(cudaEventRecord(d0, me->compute));
-    WK(me->m.decode((const float*)me->slots.slots[m.slot].buf, me->dout, me->compute));
-    WK(cudaEventRecord(d1, me->compute));
-    WK(mp_release_slot(ctx, me, m.slot, me->compute));
-    if (m.flags & 1u)
-      WK(cudaMemcpyAsync(me->stage_host, me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
-    WK(cudaStreamSynchronize(me->compute));
-    auto rs = new ReqState();
-    rs->pre = true;
-    if (m.flags & 1u) {
-      rs->outcopy.resize(ctx->out_bytes / 4);
-      std::memcpy(rs->outcopy.data(), me->stage_host, ctx->out_bytes);
+  constexpr int K = 4;
+  MpDReq q[K];
+  for (auto& e : q) {
+    cudaEventCreate(&e.d0);
+    cudaEventCreate(&e.d1);
+    cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming);
+  }
+  const ChunkPlan lplan = plan_latent(ctx->g.dit, ctx->g.chunk_bytes[1]);
+  std::deque<int> live;  // pending decodes in enqueue order
+  int next = 0;
+  for (;;) {
+    bool did = false;
+    MetaRec m;
+    if (int(live.size()) < K && mp_try_recv(ctx, me, m)) {
+      did = true;
+      const int k = next;
+      next = (next + 1) % K;
+      MpDReq& r = q[k];
+      r.m = m;
+      r.t_start = now_s();
+      me->busy.begin(r.t_start);
+      OpenSet* os = open_set(ctx, me, m.src, int(m.slot));
+      if (!os) {
+        worker_fail(ctx, "mp_d_worker: cannot open the producer's events");
+        return;
+      }
+      RecvClock& rc = me->rclk[k];
+      const int n = int(m.nchunks);
+      WK(clock_probe(rc, n, os->ready, os->start, os->chunk[n - 1]));
+      WK(cudaEventRecord(r.d0, me->compute));
+      const float* lat = (const float*)me->slots.slots[m.slot].buf;
+      for (int c = 0; c < n; ++c) {  // decode each chunk as it lands (a14)
+        WK(clock_chunk(rc, c, me->compute, os->chunk[c]));
+        WK(me->m.decode_block(lat, me->dout, lplan.lb, c, me->compute));
+      }
+      WK(cudaEventRecord(r.d1, me->compute));
+      WK(mp_finish_slot(ctx, me, rc, m.slot, ctx->lat_bytes, me->compute));
+      if (m.flags & 1u)
+        WK(cudaMemcpyAsync(me->stage_host[k], me->dout, ctx->out_bytes, cudaMemcpyDeviceToHost, me->compute));
+      WK(cudaEventRecord(r.done, me->compute));
+      live.push_back(k);
     }
-    df_completion& o = rs->comp;
-    std::memset(&o, 0, sizeof(o));
-    o.id = {m.id_lo, m.id_hi};
-    o.status = DF_OK;
-    o.user_tag = m.user_tag;
-    o.inst[0] = m.inst_e;
-    o.inst[1] = m.inst_t;
-    o.inst[2] = me->id;
-    o.t_submit = m.t_submit;
-    o.t_start[0] = m.t_start_e;
-    o.t_end[0] = m.t_end_e;
-    o.t_end[1] = m.t_end_t;
-    o.t_start[2] = t_start;
-    o.t_end[2] = o.t_done = now_s();
-    o.stage_ms[0] = m.stage_ms_e;
-    o.stage_ms[1] = m.stage_ms_t;
-    cudaEventElapsedTime(&o.stage_ms[2], d0, d1);
-    float ex = 0.f;
-    cudaEventElapsedTime(&ex, r0, w0);
-    o.exposed_ms[0] = m.exposed_t;
-    o.exposed_ms[1] = ex > 0.f ? ex : 0.f;
-    o.xfer_ms[0] = o.xfer_ms[1] = -1.f;  // cross-process copies are timed by neither side's clock
-    if (!rs->outcopy.empty()) {
-      o.out_view = rs->outcopy.data();
-      o.out_view_bytes = ctx->out_bytes;
+    if (!live.empty()) {
+      cudaError_t e = cudaEventQuery(q[live.front()].done);
+      if (e == cudaSuccess) {
+        mp_d_complete(ctx, me, q[live.front()], live.front());
+        live.pop_front();
+        if (live.empty()) me->busy.end(now_s());
+        did = true;
+      } else if (e != cudaErrorNotReady) {
+        worker_fail(ctx, std::string("mp_d_worker: ") + cudaGetErrorString(e));
+        return;
+      }
     }
-    if (ctx->g.handoff_mode & DF_HASH) {
-      o.hash_src[1] = m.hash_src;
-      o.hash_dst[1] = me->mp_hash[1];
-      o.hash_src[0] = o.hash_dst[0] = 1;  // edge 0 was verified by T (mismatch fails the request)
+    if (!did) {
+      if (ctx->stop.load() && live.empty()) break;
+      mp_sleep();
     }
-    me->served++;
-    {
-      std::lock_guard<std::mutex> lk(ctx->done_mu);
-      while (!ctx->done->push(rs)) std::this_thread::yield();
-    }
-    ctx->done_cv.notify_all();
+  }
+  for (auto& e : q) {
+    cudaEventDestroy(e.d0);
+    cudaEventDestroy(e.d1);
+    cudaEventDestroy(e.done);
   }
 }
 
@@ -1228,7 +1679,7 @@ void sched_loop(df_ctx* ctx) {
   df_sched_metrics prev{};
   bool have_prev = false;
   std::vector<uint64_t> busy0(ctx->inst.size());
-  for (size_t i = 0; i < ctx->inst.size(); ++i) busy0[i] = ctx->inst[i]->busy_ns.load();
+  for (size_t i = 0; i < ctx->inst.size(); ++i) busy0[i] = ctx->inst[i]->busy.sample(now_s());
   double t_prev = now_s();
   while (!ctx->sched_stop.load()) {
     for (int k = 0; k < int(c.delta_s * 100) && !ctx->sched_stop.load(); ++k)
@@ -1244,7 +1695,7 @@ void sched_loop(df_ctx* ctx) {
       double busy = 0;
       for (size_t j = 0; j < ids.size(); ++j) {
         Inst& I = *ctx->inst[ids[j]];
-        uint64_t b = I.busy_ns.load();
+        uint64_t b = I.busy.sample(t);
         if (j < g[s]) busy += double(b - busy0[ids[j]]) * 1e-9;
         busy0[ids[j]] = b;
         if (j < g[s] && s != DF_E) m.q[s] += uint32_t(I.inbox.size());
@@ -1520,39 +1971,45 @@ df_status df_init(const df_graph* g, df_ctx** out) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, I.stage == DF_T ? lo : hi);
     cudaStreamCreateWithPriority(&I.comm, cudaStreamNonBlocking, hi);
-    // T receive slots and E send buffers hold up to two ctx (prompt + negative prompt, CFG)
+    cudaStreamCreateWithPriority(&I.aux, cudaStreamNonBlocking, hi);
+    cudaError_t le = cudaSuccess;
+    // T receive slots and E send buffers hold up to two ctx (prompt + negative prompt, CFG);
+    // every receive slot carries a 64-byte trailer (the producer's payload hash, multi-process)
     size_t slot_bytes = I.stage == DF_T ? ctx->payload(true) : (I.stage == DF_D ? ctx->lat_bytes : 0);
+    I.slot_cap = slot_bytes;
     if (slot_bytes) {
       I.slots.slots.resize(g->n_slots);
       for (uint32_t s = 0; s < g->n_slots; ++s) {
-        cudaMalloc(&I.slots.slots[s].buf, slot_bytes);
-        cudaEventCreateWithFlags(&I.slots.slots[s].consumed, cudaEventDisableTiming);
-        cudaEventRecord(I.slots.slots[s].consumed, I.compute);
+        if (le == cudaSuccess) le = cudaMalloc(&I.slots.slots[s].buf, slot_bytes + 64);
+        if (le == cudaSuccess) le = cudaEventCreateWithFlags(&I.slots.slots[s].consumed, cudaEventDisableTiming);
+        if (le == cudaSuccess) le = cudaEventRecord(I.slots.slots[s].consumed, I.compute);
         I.slots.free_list.push_back(int(s));
       }
+      for (auto& rc : I.rclk)
+        if (le == cudaSuccess) le = clock_create(rc);
     }
     if (I.stage == DF_T) {
       for (int b = 0; b < 2; ++b) {
-        cudaMalloc(&I.xbuf[b], ctx->lat_bytes);
-        cudaEventCreateWithFlags(&I.xsent[b], cudaEventDisableTiming);
-        cudaEventRecord(I.xsent[b], I.comm);
+        if (le == cudaSuccess) le = cudaMalloc(&I.xbuf[b], ctx->lat_bytes);
+        if (le == cudaSuccess) le = cudaEventCreateWithFlags(&I.xsent[b], cudaEventDisableTiming);
+        if (le == cudaSuccess) le = cudaEventRecord(I.xsent[b], I.comm);
+        for (int k = 0; k < PL_MAX_CHUNKS && le == cudaSuccess; ++k)
+          le = cudaEventCreateWithFlags(&I.hb_ev[b][k], cudaEventDisableTiming);
       }
     } else if (I.stage == DF_E) {
       for (int b = 0; b < 2; ++b) {
-        cudaMalloc(&I.ebuf[b], ctx->payload(true));
-        cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming);
-        cudaEventRecord(I.esent[b], I.comm);
+        if (le == cudaSuccess) le = cudaMalloc(&I.ebuf[b], ctx->payload(true));
+        if (le == cudaSuccess) le = cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming);
+        if (le == cudaSuccess) le = cudaEventRecord(I.esent[b], I.comm);
       }
-      cudaMalloc(&I.ids_dev, 2 * size_t(c.L_txt) * 4);
+      if (le == cudaSuccess) le = cudaMalloc(&I.ids_dev, 2 * size_t(c.L_txt) * 4);
     } else {
-      cudaMalloc(&I.dout, ctx->out_bytes);
-      cudaHostAlloc(&I.stage_host, ctx->out_bytes, cudaHostAllocPortable);
+      if (le == cudaSuccess) le = cudaMalloc(&I.dout, ctx->out_bytes);
+      for (int k = 0; k < 4 && le == cudaSuccess; ++k)
+        le = cudaHostAlloc(&I.stage_host[k], ctx->out_bytes, cudaHostAllocPortable);
     }
-    cudaError_t le = cudaDeviceSynchronize();
-    if (le == cudaSuccess && mp) {
-      le = cudaHostAlloc(&I.mp_hash, 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable);
-      if (le == cudaSuccess && slot_bytes) le = mp_publish(ctx, I, slot_bytes);
-    }
+    if (le == cudaSuccess) le = cudaDeviceSynchronize();
+    if (le == cudaSuccess && mp && slot_bytes) le = mp_publish(ctx, I, slot_bytes);
     if (le != cudaSuccess) {
       std::string m = std::string("df_init: setup: ") + cudaGetErrorString(le) + " " + df::tls_err;
       df_finalize(ctx);
@@ -1593,8 +2050,6 @@ df_status df_finalize(df_ctx* ctx) {
     for (int sl = 0; sl < PL_MAX_SLOTS; ++sl) {
       if (v.buf[sl]) cudaIpcCloseMemHandle(v.buf[sl]);
       if (v.consumed[sl]) cudaEventDestroy(v.consumed[sl]);
-      for (int c = 0; c < PL_MAX_CHUNKS; ++c)
-        if (v.chunk[sl][c]) cudaEventDestroy(v.chunk[sl][c]);
     }
   }
   for (auto& ip : ctx->inst) {
@@ -1602,12 +2057,38 @@ df_status df_finalize(df_ctx* ctx) {
     if (!I.local) continue;
     cudaSetDevice(I.device);
     cudaDeviceSynchronize();
-    for (int sl = 0; sl < PL_MAX_SLOTS; ++sl) {
+    for (int p = 0; p < PL_MAX_INST; ++p)
+      for (int sl = 0; sl < PL_MAX_SLOTS; ++sl) {
+        OpenSet& os = I.opened[p][sl];
+        if (os.open && os.ipc) {
+          for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
+            cudaEventDestroy(os.ready[c]);
+            cudaEventDestroy(os.chunk[c]);
+          }
+          cudaEventDestroy(os.start);
+        }
+        os = OpenSet{};
+      }
+  }
+  for (auto& ip : ctx->inst) {
+    Inst& I = *ip;
+    if (!I.local) continue;
+    cudaSetDevice(I.device);
+    for (int sl = 0; sl < PL_MAX_SLOTS; ++sl)
       if (I.ipc_consumed[sl]) cudaEventDestroy(I.ipc_consumed[sl]);
-      for (int c = 0; c < PL_MAX_CHUNKS; ++c)
-        if (I.ipc_chunk[sl][c]) cudaEventDestroy(I.ipc_chunk[sl][c]);
-    }
-    if (I.mp_hash) cudaFreeHost(I.mp_hash);
+    for (int p = 0; p < PL_MAX_INST; ++p)
+      for (int sl = 0; sl < PL_MAX_SLOTS; ++sl) {
+        SendSet* ss = I.sendset[p][sl];
+        if (!ss) continue;
+        for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
+          cudaEventDestroy(ss->ready[c]);
+          cudaEventDestroy(ss->chunk[c]);
+        }
+        cudaEventDestroy(ss->start);
+        delete ss;
+        I.sendset[p][sl] = nullptr;
+      }
+    for (auto& rc : I.rclk) clock_destroy(rc);
     for (auto& s : I.slots.slots) {
       if (s.buf) cudaFree(s.buf);
       if (s.consumed) cudaEventDestroy(s.consumed);
@@ -1615,14 +2096,18 @@ df_status df_finalize(df_ctx* ctx) {
     for (int b = 0; b < 2; ++b) {
       if (I.xbuf[b]) cudaFree(I.xbuf[b]);
       if (I.xsent[b]) cudaEventDestroy(I.xsent[b]);
+      for (int k = 0; k < PL_MAX_CHUNKS; ++k)
+        if (I.hb_ev[b][k]) cudaEventDestroy(I.hb_ev[b][k]);
       if (I.ebuf[b]) cudaFree(I.ebuf[b]);
       if (I.esent[b]) cudaEventDestroy(I.esent[b]);
     }
     if (I.ids_dev) cudaFree(I.ids_dev);
     if (I.dout) cudaFree(I.dout);
-    if (I.stage_host) cudaFreeHost(I.stage_host);
+    for (auto* h : I.stage_host)
+      if (h) cudaFreeHost(h);
     if (I.compute) cudaStreamDestroy(I.compute);
     if (I.comm) cudaStreamDestroy(I.comm);
+    if (I.aux) cudaStreamDestroy(I.aux);
     I.m.destroy();
   }
   ReqState* rs;
@@ -1858,8 +2343,15 @@ df_status df_image_cond(df_ctx* ctx, int32_t inst, uint64_t seed, void* clip_dev
 df_status df_handoff(df_ctx* ctx, const df_handoff_desc* d, void* src_stream, df_xfer** out) {
   if (!ctx || !d || !out) return DF_ERR_INVALID;
   if (ctx->failed) return DF_ERR_STATE;
+  ChunkPlan plan;
+  if (d->flags & DF_LATENT_BLOCKS) {
+    if (d->bytes != ctx->lat_bytes) return fail(ctx, "df_handoff: DF_LATENT_BLOCKS needs the latent's size", DF_ERR_INVALID);
+    plan = plan_latent(ctx->g.dit, d->chunk_bytes);
+  } else {
+    plan = plan_bytes(d->bytes, d->chunk_bytes, 16);
+  }
   Xfer* x = nullptr;
-  df_status s = do_handoff(ctx, d, (cudaStream_t)src_stream, &x);
+  df_status s = do_handoff(ctx, d, plan, (cudaStream_t)src_stream, nullptr, &x);
   if (s == DF_OK) *out = x;
   return s;
 }
@@ -1883,9 +2375,8 @@ df_status df_handoff_query(df_ctx* ctx, df_xfer* x, uint32_t* chunks_done, uint6
   if (chunks_done) *chunks_done = n;
   if (hash) {
     hash[0] = hash[1] = 0;
-    if (x->hashed && n == x->nchunks) {
-      cudaSetDevice(x->dst_dev);
-      cudaDeviceSynchronize();
+    if (x->hashed && n == x->nchunks) {  // the source hash precedes the last chunk's event
+      if (x->t_hash) cudaEventSynchronize(x->t_hash);
       hash[0] = x->hash_dev[0];
       hash[1] = x->hash_dev[1];
     }
@@ -1972,17 +2463,8 @@ df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void*
                           int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream) {
   if (!ctx || !Q || !K || !V || !O) return DF_ERR_INVALID;
   g_launches->fetch_add(1);
-  // the first T instance's attention stream-K workspace (taken only for ragged rounds)
-  float* skw = nullptr;
-  unsigned* skf = nullptr;
-  for (auto& ip : ctx->inst)
-    if (ip->stage == DF_T && ip->m.attn_sk_ws) {
-      skw = ip->m.attn_sk_ws;
-      skf = ip->m.attn_sk_flag;
-      break;
-    }
   cudaError_t r = attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, H, Nq, Nk, dh, dh_pad, scale,
-                          (cudaStream_t)stream, 0, skw, skf);
+                          (cudaStream_t)stream, 0);
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_attention: ") + cudaGetErrorString(r));
 }
 

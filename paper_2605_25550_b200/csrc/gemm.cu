@@ -391,8 +391,7 @@ template <int CW, typename OutT, int TK, bool F8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
-                    const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const __grid_constant__ Epi epi,
-                    int epi_skip) {
+                    const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const __grid_constant__ Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS/STS, not generic)
   uint8_t* sA = smem;
@@ -596,7 +595,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       const int row0 = mb * 256 + rank * 128 + ew * 32;
       const int row = row0 + lane;
       const uint32_t trow = tmem_base + (uint32_t(ew * 32) << 16) + acc * 256;
-      if (TK == TK_DIRECT || epi_skip) {
+      if (TK == TK_DIRECT) {
 #pragma unroll 1
         for (int c = c_lo; c < c_hi; c += CW) {
           const int n0 = nb * 256 + c;
@@ -606,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tc_wait_ld();
           if (fix) fixup(v, c, CW);
           if (F8) f8_scale_acc(v, CW);
-          if (!epi_skip) epi_apply<CW, OutT>(epi, row, n0, v);
+          epi_apply<CW, OutT>(epi, row, n0, v);
         }
       } else if (TK == TK_STORE_F32 || TK == TK_GRES) {
 #pragma unroll 1
@@ -881,13 +880,8 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
     ep.sk_ws = nullptr;
     ep.sk_flag = nullptr;
   }
-  static const int skip = [] {  // debug: DF_GEMM_NOEPI=1 drops the epilogue work (timing experiments only)
-    const char* e = getenv("DF_GEMM_NOEPI");
-    return e ? atoi(e) : 0;
-  }();
-  int sk = skip;
-  void* args[] = {(void*)&ta,     (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2], (void*)&M,
-                  (void*)&N,      (void*)&K,  (void*)&ep,    (void*)&sk};
+  void* args[] = {(void*)&ta, (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2],
+                  (void*)&M,  (void*)&N,  (void*)&K,     (void*)&ep};
   return launch_ex((const void*)kern, dim3(grid), dim3(P_THREADS), P_SMEM, st, args);
 }
 

@@ -32,12 +32,8 @@ cudaError_t epi_rows(const float* tmp, const Epi& epi, int out_f32, cudaStream_t
 // Q/K/V head-major [H][Nq|Nk][dh_pad] bf16; O token-major [Nq, H*dh] bf16.
 // heads_per_sample (0 = H): H counts the heads of a stacked batch (B = H / heads_per_sample
 // samples, sample-major [b][h]); O rows are b*Nq + q with heads_per_sample*dh columns.
-// sk_ws / sk_flag (optional): the caller's stream-K workspace (SK_SLOT floats and one flag per
-// co-resident CTA) for the persistent kernel's ragged-round split.
 cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh, int dh_pad,
-                    float scale, cudaStream_t st, int heads_per_sample = 0, float* sk_ws = nullptr,
-                    unsigned* sk_flag = nullptr);
-constexpr size_t ATTN_SK_SLOT_FLOATS = 2 * 2 * 64 * 128 + 2 * 128 + 2 * 2 * 128;
+                    float scale, cudaStream_t st, int heads_per_sample = 0);
 // fp32 validation build: same layout with float and dh_pad == dh.
 cudaError_t attn_simt(const float* Q, const float* K, const float* V, float* O, int H, int Nq, int Nk, int dh,
                       float scale, cudaStream_t st, int heads_per_sample = 0);

@@ -188,8 +188,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
-    else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4) +  // GEMM stream-K
-                al(size_t(num_sms()) * ATTN_SK_SLOT_FLOATS * 4) + al(size_t(num_sms()) * 4);  // attention stream-K
+    else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // GEMM stream-K
   } else if (stage == DF_E) {
     wsb = al(L * dt * 4) + al(L * dt * ab) + al(L * fe * ab) + al(L * 2 * fe * 4);
   }
@@ -214,9 +213,6 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
       sk_ws = (float*)ws.take(size_t(num_sms()) * 128 * 256 * 4);
       sk_flag = (unsigned*)ws.take(size_t(num_sms()) * 4);
       DF_TRY(cudaMemset(sk_flag, 0, size_t(num_sms()) * 4));
-      attn_sk_ws = (float*)ws.take(size_t(num_sms()) * ATTN_SK_SLOT_FLOATS * 4);
-      attn_sk_flag = (unsigned*)ws.take(size_t(num_sms()) * 4);
-      DF_TRY(cudaMemset(attn_sk_flag, 0, size_t(num_sms()) * 4));
     }
     // zero the head-major buffers once: the dh..dhp padding must stay 0 (TMA reads it)
     DF_TRY(cudaMemset(q, 0, 4 * al(hd)));
@@ -374,8 +370,7 @@ cudaError_t Model::attn(const void* Q, const void* K, const void* V, void* O, in
   const int Ht = B * int(c.heads);  // a stacked batch is B x heads sample-major heads
   ProfScope ps(prof, st, cur_kind, 4.0 * Nq * double(Nk) * dh * Ht, 0.0);
   if (!f32()) {
-    DF_L(attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, Ht, Nq, Nk, dh, dhp, scale, st, c.heads,
-                 attn_sk_ws, attn_sk_flag));
+    DF_L(attn_tc((const bf16*)Q, (const bf16*)K, (const bf16*)V, (bf16*)O, Ht, Nq, Nk, dh, dhp, scale, st, c.heads));
   } else {
     DF_L(attn_simt((const float*)Q, (const float*)K, (const float*)V, (float*)O, Ht, Nq, Nk, dh, scale, st, c.heads));
   }

@@ -10,9 +10,15 @@
 //
 // Segment layout (all fixed size, lock-free std::atomic words, no pointers):
 //   Header        magic, world, global request sequence (FAA), per-instance ready flags
-//   InstPlane[i]  for every consumer instance i: slot IPC handles, per-slot consumed
-//                 event + per-chunk events (IPC handles), a free-slot ring (the posted
-//                 destination addresses) and an inbox ring of 128-byte metadata records.
+//   InstPlane[i]  for every consumer instance i: slot IPC handles, a per-slot consumed
+//                 event (consumer-owned), a free-slot ring (the posted destination
+//                 addresses), an inbox ring of fixed-size metadata records, and per slot the
+//                 IPC handles of the events of the transfer currently in that slot.
+// Events are always owned (created and recorded) by the side whose stream records them: a
+// CUDA event can only be recorded on a stream of its own device, while a stream may wait on
+// an event of any device.  So the producer creates its per-(consumer, slot) ready / start /
+// chunk events and publishes their handles into the consumer's slot record when it claims the
+// slot; the consumer records `consumed`.
 #pragma once
 #include <atomic>
 #include <cstddef>
@@ -34,13 +40,15 @@ struct alignas(8) MetaRec {
   uint32_t steps, slot, nchunks, chunk_bytes;
   float shift;
   int32_t inst_e, inst_t;
+  int32_t src;                                    // producer instance of this edge's transfer
   uint32_t flags;
-  double t_submit, t_start_e, t_end_e, t_end_t;  // host CLOCK_MONOTONIC (node-wide)
-  float stage_ms_e, stage_ms_t, exposed_t;
+  double t_submit, t_start_e, t_end_e, t_start_t, t_end_t;  // host CLOCK_MONOTONIC (node-wide)
+  float stage_ms_e, stage_ms_t;
+  float exposed_e2t, xfer_e2t, overlap_e2t;       // edge 0, measured by T on its own clock
   float guidance;                                 // CFG scale (payload holds 2 ctx when on)
-  uint64_t hash_src;                              // payload hash computed by the producer
+  uint64_t hash_src_e2t, hash_dst_e2t;            // edge 0 hashes (T verified them)
 };
-static_assert(sizeof(MetaRec) <= 128, "metadata record must stay fixed-size");
+static_assert(sizeof(MetaRec) <= 192, "metadata record must stay fixed-size");
 
 // Bounded MPMC ring of fixed-size records with per-cell sequence words (Vyukov); the
 // tail/head tickets are claimed by CAS-FAA on shared words.
@@ -98,13 +106,24 @@ struct ShmRing {
   }
 };
 
+// Producer-owned events of one transfer (handles published into the consumer's slot record):
+// ready[c] = chunk c's data existed (comm stream, after waiting the producer's compute, before
+// any injected delay), start = the first copy is issued, chunk[c] = chunk c landed.
+struct XferEvHandles {
+  int32_t producer;                      // instance that published them (consumer caches per producer)
+  uint32_t nchunks;
+  cudaIpcEventHandle_t ready[PL_MAX_CHUNKS];
+  cudaIpcEventHandle_t start;
+  cudaIpcEventHandle_t chunk[PL_MAX_CHUNKS];
+};
+
 struct InstPlane {
   std::atomic<uint32_t> ready;  // consumer published its handles
   uint32_t n_slots, nchunks_max;
-  uint64_t slot_bytes;
+  uint64_t slot_bytes;          // payload capacity; each slot has a 64-byte trailer after it
   cudaIpcMemHandle_t slot_mem[PL_MAX_SLOTS];
   cudaIpcEventHandle_t consumed[PL_MAX_SLOTS];
-  cudaIpcEventHandle_t chunk[PL_MAX_SLOTS][PL_MAX_CHUNKS];
+  XferEvHandles xev[PL_MAX_SLOTS];       // written by the producer that claimed the slot
   ShmRing<uint32_t, 16> free_slots;      // posted destination addresses (slot index)
   ShmRing<MetaRec, PL_RING> inbox;       // control plane into this consumer
 };

@@ -166,8 +166,6 @@ struct Model {
   float* tmp = nullptr;     // fp32 build: raw GEMM out [N, max(3d, 2f)]
   float* sk_ws = nullptr;   // bf16 build: stream-K partial tiles [SMs/2][2][256][128] fp32
   unsigned* sk_flag = nullptr;  // [SMs] epochs
-  float* attn_sk_ws = nullptr;  // bf16 build: attention stream-K partials [SMs][ATTN_SK_SLOT_FLOATS]
-  unsigned* attn_sk_flag = nullptr;  // [SMs] epochs (separate from the GEMM's epoch sequence)
   float* mods = nullptr;    // [layers][6][d]
   float* headmod = nullptr; // [2][d]
   float2* rope = nullptr;

@@ -97,3 +97,72 @@ def test_two_process_pipeline_matches_oracle_and_single_process(mode):
         want = stages.request(P, TINY, seed=s)["out"]
         assert rel_l2(out, want) <= 3e-2
         assert np.array_equal(out, single[s])                 # bit-identical to the 1-process run
+
+
+def _jitter_worker(rank, world, port, shm, seeds, mode, d, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["DF_JITTER_EDGES"] = "2"  # delay the T->D transfers only
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2605_25550_b200 import binding as B, layouts
+    from synth.configs import TINY
+    g = B.make_graph(TINY, layouts.partitioned(world), rank=rank, world=world, shm_name=shm, handoff_mode=mode,
+                     chunk_bytes=(64, 256), jitter=(1.0, d, 3))
+    c = B.Context(g)
+    dist.barrier()
+    if rank == 0:
+        for s in seeds:
+            assert c.submit(TINY.steps, TINY.shift, s, user_tag=s)[0] == B.DF_OK
+    if rank == world - 1:
+        got = []
+        while len(got) < len(seeds):
+            for x in c.poll(8, timeout_ms=60000):
+                got.append((int(x.user_tag), int(x.inst[1]), float(x.t_end[1]), float(x.exposed_ms[1]),
+                            float(x.xfer_ms[1]), float(x.xfer_ms[0]), x.hash_src[0] == x.hash_dst[0] != 0,
+                            x.hash_src[1] == x.hash_dst[1] != 0))
+        q.put(got)
+    dist.barrier()
+    c.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", [4, 4 | 1])  # DF_HASH (async), DF_HASH|DF_SYNC
+def test_two_process_handoff_is_asynchronous(mode):
+    """P:L154 / P:L513 on the one-process-per-GPU path: every T->D transfer is held back by
+    d = 0.2 s on the producer's comm stream.  Asynchronous: a T instance computes its next
+    request without waiting for the delayed send (its two requests finish far less than d
+    apart; the delay shows up only as the decoder's exposed wait).  DF_SYNC: the T
+    compute stream waits for each delivery, so its second request finishes >= d after the
+    first.  Hashes match on both edges; transfers are timed on the consumer's clock."""
+    import torch.multiprocessing as mp
+    d = 0.2
+    seeds = [21, 22, 23, 24]
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    shm = f"/df_gpu_{uuid.uuid4().hex[:10]}"
+    port = _port()
+    procs = [ctxm.Process(target=_jitter_worker, args=(r, 2, port, shm, seeds, mode, d, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sorted(g[0] for g in got) == seeds
+    by_t = {}
+    for tag, t_inst, t_end_t, exposed1, xfer1, xfer0, h0, h1 in got:
+        assert h0 and h1
+        assert exposed1 >= 0.8 * d * 1e3, exposed1          # D stalled on the delayed chunk
+        assert 0 < xfer0 < 0.5 * d * 1e3 and 0 < xfer1 < 0.5 * d * 1e3  # copies timed without the delay
+        by_t.setdefault(t_inst, []).append(t_end_t)
+    assert len(by_t) == 2
+    for t_inst, ends in by_t.items():
+        ends.sort()
+        gap = ends[1] - ends[0]
+        if mode & 1:
+            assert gap >= 0.8 * d, (t_inst, gap)
+        else:
+            assert gap < 0.25 * d, (t_inst, gap)

@@ -1,4 +1,6 @@
 """Stage handoff and E -> T -> D pipeline through the C ABI."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -162,3 +164,65 @@ def test_pipeline_soak_bit_identical_under_reordering():
     b = run(list(reversed(seeds)), (0.3, 0.004, 9))
     for s in seeds:
         assert np.array_equal(a[s], b[s]), s
+
+
+def test_consumers_start_before_the_last_chunk_lands():
+    """Chunk-wise consumption (north_star "the consumer stage starts on the first chunk"; SURVEY
+    §8(a) a13/a14): a delay d injected before chunk 2 of every transfer holds back the later
+    chunks only.  T's prologue is already projecting the first ctx rows, and D already decoding
+    the first latent blocks, while the rest is in flight: on the consumer's own device clock
+    the consumer started chunk 0 at least ~d before the last chunk landed (overlap_ms), and it
+    stalled ~d on the held-back chunk (exposed_ms).  Outputs are byte-identical to the
+    undelayed run and to a run that moves each payload as one chunk (P13: chunking and
+    overlap never change a number)."""
+    cfg = MID
+    d = 0.05
+    seeds = [11, 12]
+
+    def run(chunks, jit, jc=0):
+        with make_ctx(cfg, chunk_bytes=chunks, jitter=jit, jitter_chunk=jc) as c:
+            return _run_requests(c, cfg, seeds, 3, 3.0)
+
+    o_whole, _ = run((0, 0), (0.0, 0.0, 0))
+    o_ref, c_ref = run((4096, 16384), (0.0, 0.0, 0))
+    o_jit, c_jit = run((4096, 16384), (1.0, d, 9), jc=2)
+    for s in seeds:
+        assert np.array_equal(o_ref[s], o_jit[s]) and np.array_equal(o_ref[s], o_whole[s]), s
+    for x in c_jit:
+        for e in range(2):
+            assert x.overlap_ms[e] >= 0.8 * d * 1e3, (e, x.overlap_ms[e])
+            assert x.exposed_ms[e] >= 0.8 * d * 1e3, (e, x.exposed_ms[e])
+            assert x.hash_src[e] == x.hash_dst[e] != 0
+    for x in c_ref:
+        for e in range(2):
+            assert x.exposed_ms[e] < 0.2 * d * 1e3, (e, x.exposed_ms[e])
+            assert x.xfer_ms[e] > 0
+
+
+@pytest.mark.parametrize("chunk", [0, 4096, 8192 * 3, 16384])
+@pytest.mark.parametrize("flags", [0, B.DF_PERMUTE])
+@pytest.mark.parametrize("F", [1, 3])
+def test_latent_block_handoff_bit_exact(chunk, flags, F):
+    """P13 for the T->D chunking (DF_LATENT_BLOCKS, R22): blocks of latent rows of one frame
+    (2-D copies of C strided rows) reassemble the latent exactly, in any order; hashes agree."""
+    cfg = dataclasses.replace(MID, F=F, H=32, W=48, name=f"mid-f{F}")
+    nbytes = cfg.C * cfg.F * cfg.H * cfg.W * 4
+    with make_ctx(cfg) as c:
+        buf = inputs.payload_bytes(nbytes, seed=chunk + 1)
+        src = torch.from_numpy(buf).cuda()
+        dst = torch.zeros_like(src)
+        x = c.handoff(0, 1, src, dst, nbytes, chunk, flags=flags | B.DF_HASH | B.DF_LATENT_BLOCKS, seq=5, edge=1)
+        c.handoff_wait(x)
+        torch.cuda.synchronize()
+        n, h = c.handoff_query(x)
+        c.handoff_release(x)
+        assert np.array_equal(dst.cpu().numpy(), buf)
+        if chunk == 0:
+            want = 1
+        elif F > 1:
+            want = F  # one chunk per latent frame
+        else:
+            hb = max(cfg.ph, (chunk // (cfg.C * cfg.W * 4)) // cfg.ph * cfg.ph)
+            want = -(-cfg.H // hb)
+        assert n == want
+        assert h[0] == h[1] == cap.payload_hash(buf)

@@ -121,7 +121,7 @@ def _run(mut, keep_going=False):
             shutil.copytree(os.path.join(ROOT, d), os.path.join(td, d),
                             ignore=shutil.ignore_patterns("__pycache__", "*.so", "*.o"))
         os.makedirs(os.path.join(td, "tests"))
-        for t in TESTS + ["tests/conftest.py"]:
+        for t in TESTS + ["tests/conftest.py", "tests/oracle_big.py"]:
             shutil.copy(os.path.join(ROOT, t), os.path.join(td, t))
         if old is not None:
             p = os.path.join(td, rel)
