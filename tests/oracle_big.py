@@ -22,9 +22,10 @@ from oracle.philox import stream_words
 _SLICE = 1 << 24  # words per task (a multiple of 4)
 
 
-def _words(args):
-    seed, first, n, tid = args
-    return stream_words(seed, n, tid, 0, first=first)
+def _bits(args):
+    """bf16 bits of words [first, first + n) of tensor tid (the recipe is element-wise)."""
+    seed, first, n, tid, kind, shape, cfg = args
+    return OP.bits_from_words(stream_words(seed, n, tid, 0, first=first), kind, shape, cfg, flat=True)
 
 
 class StreamingParams(OP.Params):
@@ -51,9 +52,9 @@ class StreamingParams(OP.Params):
         n = int(np.prod(shape))
         if n <= 4 * self._slice:
             return super().bits(name)
-        tasks = [(self.seed, f, min(self._slice, n - f), tid) for f in range(0, n, self._slice)]
-        u = np.concatenate(self._pool_get().map(_words, tasks))
-        return OP.bits_from_words(u, kind, shape, self.cfg)
+        # the std of the recipe depends on the tensor's shape (fan-in), not the slice's
+        tasks = [(self.seed, f, min(self._slice, n - f), tid, kind, shape, self.cfg) for f in range(0, n, self._slice)]
+        return np.concatenate(self._pool_get().map(_bits, tasks)).reshape(shape)
 
     def __getitem__(self, name: str) -> np.ndarray:
         if name.startswith("L"):
