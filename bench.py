@@ -196,7 +196,19 @@ def summarize(comps, ecomps=()):
         "xfer": [pos([c.xfer_ms[0] for c in comps]), pos([c.xfer_ms[1] for c in comps])],
         "overlap": [med(c.overlap_ms[0] for c in comps), med(c.overlap_ms[1] for c in comps)],
         "hash_ok": all(c.hash_src[e] == c.hash_dst[e] != 0 for c in list(comps) + list(ecomps) for e in range(2)),
-        "n": len(comps), "t_inst": sorted({int(c.inst[1]) for c in comps})}
+        "n": len(comps), "t_inst": sorted({int(c.inst[1]) for c in comps}),
+        # per-instance stage times for Eq. 6: E host enqueue time (E never waits on the
+        # device), T and D device time of one request
+        "T_s": [med((c.t_end[0] - c.t_start[0]) for c in comps), med(c.stage_ms[1] for c in comps) * 1e-3,
+                med(c.stage_ms[2] for c in comps) * 1e-3]}
+
+
+def eq6_record(g, T, value):
+    """P14 (Eq. 6): the pipeline's throughput bound min_s g_s / T_s from the
+    measured per-instance stage times, and the measured whole-job rate as a fraction of it."""
+    rates = [g[s] / T[s] if T[s] > 0 else float("inf") for s in range(3)]
+    b = min(range(3), key=lambda s: rates[s])
+    return {"g": list(g), "T_s": T, "bound_req_s": rates[b], "bottleneck": "ETD"[b], "measured_over_bound": value / rates[b]}
 
 
 def roofline(kstats, peaks, traffic, config):
@@ -318,6 +330,7 @@ def video_record(args, peaks, local):
             "roofline": roofline(kstats, peaks, None, "video"),
             "clocks": clk.summary(),
             "handoff": handoff_record(cfg, summ),
+            "eq6": eq6_record((1, 1, 1), summ["T_s"], args.video_requests / (ms / 1000.0)),
             "kernel_time_share": shares, "kernel_gflops": gfl}
 
 
@@ -477,6 +490,7 @@ def run_ours(args, cfg):
                      "achieved_tflops": dit_tflops, "frac_of_sustained_peak": dit_tflops / peaks["bf16_sus"],
                      "frac_of_burst_peak": dit_tflops / peaks["bf16"]},
         "handoff": handoff_record(cfg, summary),
+        "eq6": eq6_record((gE, gT, gD), summary["T_s"], value),
         "kernel_time_share": shares,
         "kernel_gflops": tput_kind,
     }
@@ -496,7 +510,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="image", choices=sorted(CONFIGS))
     ap.add_argument("--chunk-ctx", type=int, default=512 * 1024)
-    ap.add_argument("--chunk-lat", type=int, default=256 * 1024)
+    ap.add_argument("--chunk-lat", type=int, default=128 * 1024,
+                    help="T->D chunk: latent rows of one frame, C*W*4 bytes each (image: 16 rows; video: one frame)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exclusive", action="store_true", help="N>1: E and D on GPUs of their own (1:N-2:1)")
     ap.add_argument("--t-per-gpu", type=int, default=1, help="DiT instances per GPU")

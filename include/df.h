@@ -150,10 +150,15 @@ typedef struct {
  * scheduler").  Blocks up to timeout_ms (-1 forever). DF_EMPTY if none. */
 df_status df_poll(df_ctx* ctx, df_completion* out, uint32_t max, uint32_t* n_out, int32_t timeout_ms);
 
-/* Rebalance the E:T:D ratio (Alg. 1 "Apply").  Instances keep their
- * devices; the ratio limits which instances receive new requests.  Retiring
- * instances drain first; no request is lost.  DF_ERR_CAPACITY if a
- * g_s < 1 or more instances than exist are requested. */
+/* Rebalance the E:T:D ratio (Alg. 1 "Apply").  Each instance host keeps its
+ * device.  If a stage has at least g_s instances, the first g_s of them receive new
+ * requests and the rest drain.  If a stage has fewer, instances of stages with
+ * a surplus are re-purposed: taken out of routing, drained (their queued and in-flight
+ * work completes; no request is lost), their old stage freed, the new stage created
+ * (weights regenerated from the weight seed -- the cold start) and put into service; each
+ * move is logged (df_sched_log, action 4, with the drain and cold-start times).  Blocks
+ * until done.  DF_ERR_CAPACITY if a g_s < 1 or sum g exceeds the instance hosts (or G);
+ * DF_ERR_STATE if re-purposing is needed on a multi-process context. */
 df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD);
 
 /* ------------------------------------------------------------------ low-level, stream-ordered */
@@ -283,6 +288,12 @@ typedef struct {
   int32_t stage;                /* for 1/2                                              */
   uint32_t g[3];                /* allocation after the decision                        */
   df_sched_metrics m;
+  /* action 4 (re-purpose, logged by df_set_ratio): instance `inst` moved from from_stage
+   * to `stage`; drain_ms = time to take it out of routing and let it finish its work,
+   * cold_start_ms = time to free its old stage and create the new one (weights regenerated
+   * from the weight seed, buffers, worker) -- P:L357 "cold starts" */
+  int32_t inst, from_stage;
+  float drain_ms, cold_start_ms;
 } df_sched_event;
 /* Pure functions (no GPU, no context): the Eq. 6 planner (exhaustive; cur/budget limit
  * the L1 instance moves from cur, budget < 0 = unlimited; ties -> fewer GPUs, then

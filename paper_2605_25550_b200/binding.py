@@ -74,7 +74,8 @@ class SchedMetricsC(C.Structure):
 
 class SchedEventC(C.Structure):
     _fields_ = [("t", C.c_double), ("action", C.c_int32), ("stage", C.c_int32), ("g", C.c_uint32 * 3),
-                ("m", SchedMetricsC)]
+                ("m", SchedMetricsC), ("inst", C.c_int32), ("from_stage", C.c_int32), ("drain_ms", C.c_float),
+                ("cold_start_ms", C.c_float)]
 
 
 class HandoffDescC(C.Structure):

@@ -37,6 +37,7 @@ struct df_xfer {
   uint32_t nchunks = 0;
   std::vector<cudaEvent_t> chunk_ev;  // source device, source comm stream: chunk c landed
   std::vector<cudaEvent_t> ready_ev;  // source device, source comm stream: chunk c's data existed
+  std::vector<cudaEvent_t> issued_ev; // source device, source comm stream: chunk c's copy issued
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing (source comm stream): first copy issued / last landed
   cudaEvent_t t_hash = nullptr;            // destination hash done (destination aux stream)
   unsigned long long* hash_dev = nullptr;  // [2] src, dst (pinned-mapped host)
@@ -141,8 +142,13 @@ struct Inbox {
     return true;
   }
   bool pop(T& out, std::atomic<bool>& stop) {
+    return pop_until(out, [&] { return stop.load(); });
+  }
+  // blocks until an item arrives (true) or done() holds with the queue empty (false)
+  template <class F>
+  bool pop_until(T& out, F done) {
     std::unique_lock<std::mutex> lk(mu);
-    cv.wait(lk, [&] { return !q.empty() || stop.load(); });
+    cv.wait(lk, [&] { return !q.empty() || done(); });
     if (q.empty()) return false;
     out = q.front();
     q.pop_front();
@@ -183,21 +189,22 @@ struct BusyClock {
 // consumer's device so every difference is one clock:
 //   R[c], A[c]  consumer compute stream, right before / after its wait on chunk c;
 //   P[c]        probe stream, when the producer's "chunk c exists" event fired;
-//   X0, X1      probe stream, when the first copy was issued / the last chunk landed.
+//   I[c], L[c]  probe stream, when chunk c's copy was issued / chunk c landed.
 // exposed = sum_c max(0, A_c - max(R_c, P_c)): the consumer stalled on data in flight (injected
-// delays included), not on upstream compute.  overlap = max(0, X1 - A_0): how long before the
-// last chunk landed the consumer was already working on chunk 0.
+// delays included), not on upstream compute.  xfer = sum_c (L_c - I_c): copy time.
+// overlap = max(0, L_{n-1} - A_0): how long before the last chunk landed the consumer was
+// already working on chunk 0.
 struct RecvClock {
   int n = 0;
   cudaStream_t probe = nullptr;
   cudaEvent_t R[PL_MAX_CHUNKS] = {}, A[PL_MAX_CHUNKS] = {}, P[PL_MAX_CHUNKS] = {};
-  cudaEvent_t X0 = nullptr, X1 = nullptr;
+  cudaEvent_t I[PL_MAX_CHUNKS] = {}, L[PL_MAX_CHUNKS] = {};
   unsigned long long* hash = nullptr;  // mapped pinned [2]: src (producer's, via the slot trailer), dst
 };
 
 // Producer-owned events of the transfers into one (consumer, slot) (multi-process).
 struct SendSet {
-  cudaEvent_t ready[PL_MAX_CHUNKS] = {}, start = nullptr, chunk[PL_MAX_CHUNKS] = {};
+  cudaEvent_t ready[PL_MAX_CHUNKS] = {}, issued[PL_MAX_CHUNKS] = {}, chunk[PL_MAX_CHUNKS] = {};
   XferEvHandles h{};
 };
 // The consumer's handles on a producer's SendSet (opened over IPC, or the producer's own
@@ -205,7 +212,7 @@ struct SendSet {
 struct OpenSet {
   bool open = false;
   bool ipc = false;
-  cudaEvent_t ready[PL_MAX_CHUNKS] = {}, start = nullptr, chunk[PL_MAX_CHUNKS] = {};
+  cudaEvent_t ready[PL_MAX_CHUNKS] = {}, issued[PL_MAX_CHUNKS] = {}, chunk[PL_MAX_CHUNKS] = {};
 };
 
 struct Inst {
@@ -234,6 +241,10 @@ struct Inst {
   float* stage_host[4] = {nullptr, nullptr, nullptr, nullptr};
   BusyClock busy;
   std::atomic<uint64_t> served{0};
+  // re-purposing (df_set_ratio, Alg. 1 "Apply"): producers that picked this instance and have
+  // not handed it the job yet; a retiring instance drains its inbox and these, then stops
+  std::atomic<int> inflight_in{0};
+  std::atomic<bool> retire{false};
   // multi-process
   bool local = true;
   cudaEvent_t ipc_consumed[PL_MAX_SLOTS] = {};
@@ -244,8 +255,9 @@ struct Inst {
 struct df_ctx {
   df_graph g{};
   std::vector<std::unique_ptr<Inst>> inst;
-  std::vector<int> by_stage[3];
-  std::atomic<int> active[3];
+  std::vector<int> by_stage[3];   // routing: instances of each stage (guarded by route_mu)
+  std::atomic<int> active[3];     // the first active[s] of by_stage[s] receive new work
+  std::mutex route_mu;
   std::atomic<bool> stop{false};
   std::atomic<bool> failed{false};
   std::string err;
@@ -492,8 +504,10 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, const ChunkPlan& pla
   CK(ctx, cudaSetDevice(S.device));
   x->chunk_ev.resize(x->nchunks);
   x->ready_ev.resize(x->nchunks);
+  x->issued_ev.resize(x->nchunks);
   for (auto& e : x->chunk_ev) CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : x->ready_ev) CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : x->issued_ev) CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(ctx, cudaEventCreate(&x->t0));
   CK(ctx, cudaEventCreate(&x->t1));
   if (!piece_ready) {  // comm stream runs after the producer's queued work
@@ -530,6 +544,7 @@ df_status do_handoff(df_ctx* ctx, const df_handoff_desc* d, const ChunkPlan& pla
     CK(ctx, cudaEventRecord(x->ready_ev[ci], S.comm));
     if (delay && k == jc) CK(ctx, delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), S.comm));
     if (k == 0) CK(ctx, cudaEventRecord(x->t0, S.comm));
+    CK(ctx, cudaEventRecord(x->issued_ev[ci], S.comm));
     CK(ctx, copy_piece(plan, ci, d->dst, D.device, d->src, S.device, S.comm));
     if (hash && k == plan.n - 1) {  // every piece is final here
       g_launches->fetch_add(1);
@@ -559,6 +574,7 @@ void free_xfer(Xfer* x) {
   if (x->t_hash) cudaEventSynchronize(x->t_hash);  // the pooled hash slot is still being written
   for (auto e : x->chunk_ev) cudaEventDestroy(e);
   for (auto e : x->ready_ev) cudaEventDestroy(e);
+  for (auto e : x->issued_ev) cudaEventDestroy(e);
   if (x->t0) cudaEventDestroy(x->t0);
   if (x->t1) cudaEventDestroy(x->t1);
   if (x->t_hash) cudaEventDestroy(x->t_hash);
@@ -582,41 +598,37 @@ cudaError_t clock_create(RecvClock& rc) {
     DF_TRY(cudaEventCreate(&rc.R[c]));
     DF_TRY(cudaEventCreate(&rc.A[c]));
     DF_TRY(cudaEventCreate(&rc.P[c]));
+    DF_TRY(cudaEventCreate(&rc.I[c]));
+    DF_TRY(cudaEventCreate(&rc.L[c]));
   }
-  DF_TRY(cudaEventCreate(&rc.X0));
-  DF_TRY(cudaEventCreate(&rc.X1));
   rc.hash = hash_pool().get();
   return rc.hash ? cudaSuccess : cudaErrorMemoryAllocation;
 }
 
 void clock_destroy(RecvClock& rc) {
   if (rc.probe) cudaStreamSynchronize(rc.probe);
-  for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
-    if (rc.R[c]) cudaEventDestroy(rc.R[c]);
-    if (rc.A[c]) cudaEventDestroy(rc.A[c]);
-    if (rc.P[c]) cudaEventDestroy(rc.P[c]);
-  }
-  if (rc.X0) cudaEventDestroy(rc.X0);
-  if (rc.X1) cudaEventDestroy(rc.X1);
+  for (cudaEvent_t* set : {rc.R, rc.A, rc.P, rc.I, rc.L})
+    for (int c = 0; c < PL_MAX_CHUNKS; ++c)
+      if (set[c]) cudaEventDestroy(set[c]);
   if (rc.probe) cudaStreamDestroy(rc.probe);
   if (rc.hash) hash_pool().put(rc.hash);
   rc = RecvClock{};
 }
 
-// Probe stream: P_c when the producer's ready[c] fired, X0 at the first copy, X1 when the last
-// chunk landed (waits in the producer's own record order).
-cudaError_t clock_probe(RecvClock& rc, int n, const cudaEvent_t* ready, cudaEvent_t start, cudaEvent_t last) {
+// Probe stream: per chunk, P_c when the producer's ready[c] fired, I_c when its copy was
+// issued, L_c when it landed (waits in the producer's own record order).
+cudaError_t clock_probe(RecvClock& rc, int n, const cudaEvent_t* ready, const cudaEvent_t* issued,
+                        const cudaEvent_t* landed) {
   rc.n = n;
   for (int c = 0; c < n; ++c) {
     DF_TRY(cudaStreamWaitEvent(rc.probe, ready[c], 0));
     DF_TRY(cudaEventRecord(rc.P[c], rc.probe));
-    if (c == 0) {
-      DF_TRY(cudaStreamWaitEvent(rc.probe, start, 0));
-      DF_TRY(cudaEventRecord(rc.X0, rc.probe));
-    }
+    DF_TRY(cudaStreamWaitEvent(rc.probe, issued[c], 0));
+    DF_TRY(cudaEventRecord(rc.I[c], rc.probe));
+    DF_TRY(cudaStreamWaitEvent(rc.probe, landed[c], 0));
+    DF_TRY(cudaEventRecord(rc.L[c], rc.probe));
   }
-  DF_TRY(cudaStreamWaitEvent(rc.probe, last, 0));
-  return cudaEventRecord(rc.X1, rc.probe);
+  return cudaSuccess;
 }
 
 // Consumer stream `st` waits for chunk c (device-side), bracketed by R_c / A_c.
@@ -628,15 +640,16 @@ cudaError_t clock_chunk(RecvClock& rc, int c, cudaStream_t st, cudaEvent_t chunk
 
 // After the consumer's work on this transfer completed on the device.
 void clock_read(RecvClock& rc, float& exposed, float& xfer, float& overlap) {
-  cudaEventSynchronize(rc.X1);
-  double ex = 0;
+  cudaEventSynchronize(rc.L[rc.n - 1]);
+  double ex = 0, xf = 0;
   for (int c = 0; c < rc.n; ++c) {
     const float r = ev_ms(rc.R[0], rc.R[c]), a = ev_ms(rc.R[0], rc.A[c]), p = ev_ms(rc.R[0], rc.P[c]);
     ex += std::max(0.f, a - std::max(r, p));
+    xf += std::max(0.f, ev_ms(rc.I[c], rc.L[c]));
   }
   exposed = float(ex);
-  xfer = ev_ms(rc.X0, rc.X1);
-  overlap = std::max(0.f, ev_ms(rc.A[0], rc.X1));
+  xfer = float(xf);
+  overlap = std::max(0.f, ev_ms(rc.A[0], rc.L[rc.n - 1]));
 }
 
 struct ChunkWaitCtx {
@@ -658,11 +671,20 @@ cudaError_t block_done_cb(void* u, int k) {
 }
 
 // ---------------------------------------------------------------- workers
-int pick(df_ctx* ctx, int stage, uint64_t seq) {
+// Round-robin over the active instances of a stage by request sequence number (deterministic).
+// hold: the caller will hand the chosen instance a job later (single-process workers); the
+// instance cannot finish retiring until that hand-over (release_pick) happened.
+int pick(df_ctx* ctx, int stage, uint64_t seq, bool hold = false) {
+  std::lock_guard<std::mutex> lk(ctx->route_mu);
   int n = ctx->active[stage].load();
   auto& v = ctx->by_stage[stage];
   if (n <= 0 || v.empty()) return -1;
-  return v[seq % uint64_t(std::min<int>(n, int(v.size())))];
+  const int id = v[seq % uint64_t(std::min<int>(n, int(v.size())))];
+  if (hold) ctx->inst[id]->inflight_in++;
+  return id;
+}
+void release_pick(Inst* I) {
+  if (I->inflight_in.fetch_sub(1) == 1) I->inbox.cv.notify_all();
 }
 
 // Stage-time profile for the Eq. 6 planner: EMA of seconds per request per instance, keyed by
@@ -739,9 +761,24 @@ cudaError_t encode_request(df_ctx* ctx, Inst* me, ReqState* rs, int b) {
   return cudaSuccess;
 }
 
+// Whether instance I is in the active prefix of its stage's routing list (E instances pull
+// from the shared request ring, so an encoder beyond g_E must stop pulling by itself).
+bool routed(df_ctx* ctx, const Inst* I) {
+  std::lock_guard<std::mutex> lk(ctx->route_mu);
+  const auto& v = ctx->by_stage[I->stage];
+  const int n = std::min<int>(ctx->active[I->stage].load(), int(v.size()));
+  for (int k = 0; k < n; ++k)
+    if (v[k] == I->id) return true;
+  return false;
+}
+
 void e_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
-  while (!ctx->stop.load()) {
+  while (!ctx->stop.load() && !me->retire.load()) {
+    if (!routed(ctx, me)) {
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+      continue;
+    }
     ReqState* rs = nullptr;
     {
       std::lock_guard<std::mutex> lk(ctx->req_mu);
@@ -758,7 +795,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
     ctx->qd_count[0]++;
     WK(cudaEventCreate(&rs->ev[0]));
     WK(cudaEventCreate(&rs->ev[1]));
-    const int tid = pick(ctx, DF_T, rs->seq);
+    const int tid = pick(ctx, DF_T, rs->seq, true);
     Inst* T = ctx->inst[tid].get();
     rs->inst[1] = tid;
     int b = me->enext;
@@ -800,7 +837,10 @@ void e_worker(df_ctx* ctx, Inst* me) {
     me->served++;
     sched_note(ctx, 0, 0u, (rs->t_end[0] - rs->t_start[0]) - (tw1 - tw));
     T->inbox.push(Job{rs});  // E moves on immediately
+    release_pick(T);
   }
+  me->busy.end(now_s());
+  cudaStreamSynchronize(me->comm);  // its send buffers are read until the last copy landed
 }
 
 // T finishes a request once its compute has drained on the device: stage time and the E->T
@@ -813,10 +853,10 @@ void t_finish(df_ctx* ctx, Inst* me, ReqState* rs, Inst* D) {
   const double dev_s = ev_ms(rs->ev[2], rs->ev[3]) * 1e-3;
   rs->stage_ms[1] = float(dev_s * 1e3);
   clock_read(me->rclk[rs->xbuf], rs->exposed[0], rs->xfer[0], rs->overlap[0]);
-  rs->xfer[0] = ev_ms(rs->x[0]->t0, rs->x[0]->t1);  // exact: both on the producer's comm stream
   me->served++;
   sched_note(ctx, 1, rs->req.steps, dev_s);
   D->inbox.push(Job{rs});
+  release_pick(D);
 }
 
 // One T instance.  The host enqueues request r's whole prologue + S steps + T->D send,
@@ -840,7 +880,8 @@ void t_worker(df_ctx* ctx, Inst* me) {
       if (me->inbox.size() == 0) me->busy.end(now_s());
       continue;
     }
-    if (!pend && !me->inbox.pop(j, ctx->stop)) break;
+    if (!pend && !me->inbox.pop_until(j, [&] { return ctx->stop.load() || (me->retire.load() && me->inflight_in.load() == 0); }))
+      break;
     ReqState* rs = j.rs;
     rs->t_start[1] = now_s();
     me->busy.begin(rs->t_start[1]);
@@ -860,13 +901,14 @@ void t_worker(df_ctx* ctx, Inst* me) {
     // the prologue consumes ctx chunk by chunk as it lands (device-side waits)
     Xfer* x0 = rs->x[0];
     RecvClock& rc = me->rclk[b];
-    WK(clock_probe(rc, int(x0->nchunks), x0->ready_ev.data(), x0->t0, x0->t1));
+    WK(clock_probe(rc, int(x0->nchunks), x0->ready_ev.data(), x0->issued_ev.data(), x0->chunk_ev.data()));
     const bool cfgr = cfg_on(rs->req.guidance);
     const ChunkPlan cplan = plan_ctx(ctx, ctx->payload(cfgr));
     ChunkWaitCtx wc{&rc, me->compute, x0->chunk_ev.data()};
     ChunkHook hook;
     hook.rows_per_chunk = rows_per_chunk(ctx, cplan);
     hook.nchunks = int(x0->nchunks);
+    hook.shift = rs->req.shift;
     hook.wait = chunk_wait_cb;
     hook.user = &wc;
     std::vector<float> sig = sigmas_host(S, rs->req.shift);
@@ -895,7 +937,7 @@ void t_worker(df_ctx* ctx, Inst* me) {
     if (pend) t_finish(ctx, me, pend, pendD);
     pend = nullptr;
     // T -> D: claim a D slot, send the final latent chunk by chunk as its blocks are final
-    const int did = pick(ctx, DF_D, rs->seq);
+    const int did = pick(ctx, DF_D, rs->seq, true);
     Inst* D = ctx->inst[did].get();
     rs->inst[2] = did;
     int s = D->slots.acquire(ctx->stop);
@@ -932,7 +974,7 @@ void d_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
   Job j;
   const ChunkPlan lplan = plan_latent(ctx->g.dit, ctx->g.chunk_bytes[1]);
-  while (me->inbox.pop(j, ctx->stop)) {
+  while (me->inbox.pop_until(j, [&] { return ctx->stop.load() || (me->retire.load() && me->inflight_in.load() == 0); })) {
     ReqState* rs = j.rs;
     rs->t_start[2] = now_s();
     me->busy.begin(rs->t_start[2]);
@@ -942,7 +984,7 @@ void d_worker(df_ctx* ctx, Inst* me) {
     WK(cudaEventCreate(&rs->ev[5]));
     Xfer* x1 = rs->x[1];
     RecvClock& rc = me->rclk[0];
-    WK(clock_probe(rc, int(x1->nchunks), x1->ready_ev.data(), x1->t0, x1->t1));
+    WK(clock_probe(rc, int(x1->nchunks), x1->ready_ev.data(), x1->issued_ev.data(), x1->chunk_ev.data()));
     WK(cudaEventRecord(rs->ev[4], me->compute));
     const float* lat = (const float*)me->slots.slots[rs->slot[1]].buf;
     for (uint32_t k = 0; k < x1->nchunks; ++k) {  // D decodes each chunk as it lands (a14)
@@ -959,7 +1001,6 @@ void d_worker(df_ctx* ctx, Inst* me) {
     if (rs->req.out_host && rs->req.out_bytes >= ctx->out_bytes)
       std::memcpy(rs->req.out_host, me->stage_host[0], ctx->out_bytes);
     clock_read(rc, rs->exposed[1], rs->xfer[1], rs->overlap[1]);
-    rs->xfer[1] = ev_ms(x1->t0, x1->t1);
     rs->stage_ms[2] = ev_ms(rs->ev[4], rs->ev[5]);
     rs->t_end[2] = now_s();
     me->busy.end(rs->t_end[2]);
@@ -1094,12 +1135,12 @@ SendSet* send_set(Inst* me, int ci, int s) {
   bool ok = true;
   for (int c = 0; c < PL_MAX_CHUNKS && ok; ++c) {
     ok = cudaEventCreateWithFlags(&n->ready[c], fl) == cudaSuccess &&
+         cudaEventCreateWithFlags(&n->issued[c], fl) == cudaSuccess &&
          cudaEventCreateWithFlags(&n->chunk[c], fl) == cudaSuccess &&
          cudaIpcGetEventHandle(&n->h.ready[c], n->ready[c]) == cudaSuccess &&
+         cudaIpcGetEventHandle(&n->h.issued[c], n->issued[c]) == cudaSuccess &&
          cudaIpcGetEventHandle(&n->h.chunk[c], n->chunk[c]) == cudaSuccess;
   }
-  ok = ok && cudaEventCreateWithFlags(&n->start, fl) == cudaSuccess &&
-       cudaIpcGetEventHandle(&n->h.start, n->start) == cudaSuccess;
   if (!ok) {
     delete n;
     return nullptr;
@@ -1117,15 +1158,15 @@ OpenSet* open_set(df_ctx* ctx, Inst* me, int p, int s) {
   if (P->local) {  // same process: the producer's own events
     SendSet* ss = P->sendset[me->id][s];
     if (!ss) return nullptr;
-    for (int c = 0; c < PL_MAX_CHUNKS; ++c) os.ready[c] = ss->ready[c], os.chunk[c] = ss->chunk[c];
-    os.start = ss->start;
+    for (int c = 0; c < PL_MAX_CHUNKS; ++c)
+      os.ready[c] = ss->ready[c], os.issued[c] = ss->issued[c], os.chunk[c] = ss->chunk[c];
   } else {
     const XferEvHandles& h = ctx->seg->inst[me->id].xev[s];
     for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
       if (cudaIpcOpenEventHandle(&os.ready[c], h.ready[c]) != cudaSuccess) return nullptr;
+      if (cudaIpcOpenEventHandle(&os.issued[c], h.issued[c]) != cudaSuccess) return nullptr;
       if (cudaIpcOpenEventHandle(&os.chunk[c], h.chunk[c]) != cudaSuccess) return nullptr;
     }
-    if (cudaIpcOpenEventHandle(&os.start, h.start) != cudaSuccess) return nullptr;
     os.ipc = true;
   }
   os.open = true;
@@ -1173,7 +1214,7 @@ bool mp_send(df_ctx* ctx, Inst* me, int ci, const void* src, const ChunkPlan& pl
     if (delay && c == jc &&
         !chk(delay_ns(uint64_t(double(ctx->g.jitter_delay_s) * 1e9), me->comm), "delay"))  // P:L142, R23
       return false;
-    if (c == 0 && !chk(cudaEventRecord(ss->start, me->comm), "start")) return false;
+    if (!chk(cudaEventRecord(ss->issued[c], me->comm), "issued")) return false;
     // IPC-mapped peer memory is addressed from this device: same-device copy kinds
     if (!chk(copy_piece(plan, c, dst, me->device, src, me->device, me->comm), "copy")) return false;
     if (c == plan.n - 1 && (ctx->g.handoff_mode & DF_HASH)) {  // source hash into the slot trailer
@@ -1353,11 +1394,12 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     const ChunkPlan cplan = plan_ctx(ctx, bytes);
     RecvClock& rc = me->rclk[b];
     const int n = int(m.nchunks);
-    WK(clock_probe(rc, n, os->ready, os->start, os->chunk[n - 1]));
+    WK(clock_probe(rc, n, os->ready, os->issued, os->chunk));
     ChunkWaitCtx wc{&rc, me->compute, os->chunk};
     ChunkHook hook;
     hook.rows_per_chunk = rows_per_chunk(ctx, cplan);
     hook.nchunks = n;
+    hook.shift = m.shift;
     hook.wait = chunk_wait_cb;
     hook.user = &wc;
     std::vector<float> sig = sigmas_host(S, m.shift);
@@ -1488,7 +1530,7 @@ void mp_d_worker(df_ctx* ctx, Inst* me) {
       }
       RecvClock& rc = me->rclk[k];
       const int n = int(m.nchunks);
-      WK(clock_probe(rc, n, os->ready, os->start, os->chunk[n - 1]));
+      WK(clock_probe(rc, n, os->ready, os->issued, os->chunk));
       WK(cudaEventRecord(r.d0, me->compute));
       const float* lat = (const float*)me->slots.slots[m.slot].buf;
       for (int c = 0; c < n; ++c) {  // decode each chunk as it lands (a14)
@@ -1528,6 +1570,148 @@ void mp_d_worker(df_ctx* ctx, Inst* me) {
 
 }  // namespace
 
+
+// ---------------------------------------------------------------- instance lifecycle
+// One instance host: streams (created once) plus the model and buffers of its current stage.
+// df_init creates every local instance this way; df_set_ratio re-purposes one (drain ->
+// free -> create for the new stage -> start), "Apply", "cold starts".
+namespace {
+
+cudaError_t inst_create(df_ctx* ctx, Inst& I) {
+  const df_graph* g = &ctx->g;
+  const df_dit_cfg& c = g->dit;
+  DF_TRY(cudaSetDevice(I.device));
+  if (!I.compute) {
+    int lo = 0, hi = 0;
+    DF_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    // T's compute stream at the lowest priority: E's and D's short kernels and every copy
+    // and hash go first when instances share a GPU
+    DF_TRY(cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, I.stage == DF_T ? lo : hi));
+    DF_TRY(cudaStreamCreateWithPriority(&I.comm, cudaStreamNonBlocking, hi));
+    DF_TRY(cudaStreamCreateWithPriority(&I.aux, cudaStreamNonBlocking, hi));
+  }
+  DF_TRY(I.m.create(c, int(g->precision), I.device, I.stage, g->weight_seed, int(g->max_steps)));
+  // T receive slots and E send buffers hold up to two ctx (prompt + negative prompt, CFG);
+  // every receive slot carries a 64-byte trailer (the producer's payload hash, multi-process)
+  size_t slot_bytes = I.stage == DF_T ? ctx->payload(true) : (I.stage == DF_D ? ctx->lat_bytes : 0);
+  I.slot_cap = slot_bytes;
+  if (slot_bytes) {
+    I.slots.slots.resize(g->n_slots);
+    for (uint32_t s = 0; s < g->n_slots; ++s) {
+      DF_TRY(cudaMalloc(&I.slots.slots[s].buf, slot_bytes + 64));
+      DF_TRY(cudaEventCreateWithFlags(&I.slots.slots[s].consumed, cudaEventDisableTiming));
+      DF_TRY(cudaEventRecord(I.slots.slots[s].consumed, I.compute));
+      I.slots.free_list.push_back(int(s));
+    }
+    for (auto& rc : I.rclk) DF_TRY(clock_create(rc));
+  }
+  if (I.stage == DF_T) {
+    for (int b = 0; b < 2; ++b) {
+      DF_TRY(cudaMalloc(&I.xbuf[b], ctx->lat_bytes));
+      DF_TRY(cudaEventCreateWithFlags(&I.xsent[b], cudaEventDisableTiming));
+      DF_TRY(cudaEventRecord(I.xsent[b], I.comm));
+      for (int k = 0; k < PL_MAX_CHUNKS; ++k) DF_TRY(cudaEventCreateWithFlags(&I.hb_ev[b][k], cudaEventDisableTiming));
+    }
+  } else if (I.stage == DF_E) {
+    for (int b = 0; b < 2; ++b) {
+      DF_TRY(cudaMalloc(&I.ebuf[b], ctx->payload(true)));
+      DF_TRY(cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming));
+      DF_TRY(cudaEventRecord(I.esent[b], I.comm));
+    }
+    DF_TRY(cudaMalloc(&I.ids_dev, 2 * size_t(c.L_txt) * 4));
+  } else {
+    DF_TRY(cudaMalloc(&I.dout, ctx->out_bytes));
+    for (int k = 0; k < 4; ++k) DF_TRY(cudaHostAlloc(&I.stage_host[k], ctx->out_bytes, cudaHostAllocPortable));
+  }
+  DF_TRY(cudaDeviceSynchronize());
+  if (ctx->mp && slot_bytes) DF_TRY(mp_publish(ctx, I, slot_bytes));
+  return cudaSuccess;
+}
+
+// Free the model and the stage buffers (not the streams); the instance must be idle.
+void inst_free(Inst& I) {
+  cudaSetDevice(I.device);
+  if (I.compute) cudaStreamSynchronize(I.compute);
+  if (I.comm) cudaStreamSynchronize(I.comm);
+  if (I.aux) cudaStreamSynchronize(I.aux);
+  for (auto& rc : I.rclk) clock_destroy(rc);
+  for (auto& sl : I.slots.slots) {
+    if (sl.buf) cudaFree(sl.buf);
+    if (sl.consumed) cudaEventDestroy(sl.consumed);
+  }
+  {
+    std::lock_guard<std::mutex> lk(I.slots.mu);
+    I.slots.slots.clear();
+    I.slots.free_list.clear();
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (I.xbuf[b]) cudaFree(I.xbuf[b]);
+    if (I.xsent[b]) cudaEventDestroy(I.xsent[b]);
+    for (int k = 0; k < PL_MAX_CHUNKS; ++k) {
+      if (I.hb_ev[b][k]) cudaEventDestroy(I.hb_ev[b][k]);
+      I.hb_ev[b][k] = nullptr;
+    }
+    if (I.ebuf[b]) cudaFree(I.ebuf[b]);
+    if (I.esent[b]) cudaEventDestroy(I.esent[b]);
+    I.xbuf[b] = nullptr, I.xsent[b] = nullptr, I.ebuf[b] = nullptr, I.esent[b] = nullptr;
+  }
+  if (I.ids_dev) cudaFree(I.ids_dev);
+  if (I.dout) cudaFree(I.dout);
+  I.ids_dev = nullptr, I.dout = nullptr;
+  for (auto*& h : I.stage_host) {
+    if (h) cudaFreeHost(h);
+    h = nullptr;
+  }
+  I.xnext = I.enext = 0;
+  I.m.destroy();
+  I.m = Model{};
+}
+
+void inst_start(df_ctx* ctx, Inst* I) {
+  I->retire = false;
+  if (ctx->mp) {
+    if (I->stage == DF_E) I->worker = std::thread(mp_e_worker, ctx, I);
+    else if (I->stage == DF_T) I->worker = std::thread(mp_t_worker, ctx, I);
+    else I->worker = std::thread(mp_d_worker, ctx, I);
+  } else {
+    if (I->stage == DF_E) I->worker = std::thread(e_worker, ctx, I);
+    else if (I->stage == DF_T) I->worker = std::thread(t_worker, ctx, I);
+    else I->worker = std::thread(d_worker, ctx, I);
+  }
+}
+
+// Re-purpose idle-able instance I to `stage`: take it out of routing, let it drain (its inbox
+// and every producer that already picked it), free its old stage, create the new one (model
+// weights regenerated from the weight seed: the cold start) and start serving.  Returns the
+// drain and cold-start times.
+cudaError_t inst_repurpose(df_ctx* ctx, Inst* I, int stage, double& drain_s, double& cold_s) {
+  const double t0 = now_s();
+  {
+    std::lock_guard<std::mutex> lk(ctx->route_mu);
+    auto& v = ctx->by_stage[I->stage];
+    v.erase(std::remove(v.begin(), v.end(), I->id), v.end());
+    ctx->active[I->stage] = std::min<int>(ctx->active[I->stage].load(), int(v.size()));
+  }
+  I->retire = true;
+  I->inbox.cv.notify_all();
+  if (I->worker.joinable()) I->worker.join();
+  inst_free(*I);
+  const double t1 = now_s();
+  I->stage = stage;
+  cudaError_t e = inst_create(ctx, *I);
+  if (e != cudaSuccess) return e;
+  const double t2 = now_s();
+  inst_start(ctx, I);
+  {
+    std::lock_guard<std::mutex> lk(ctx->route_mu);
+    ctx->by_stage[stage].push_back(I->id);
+  }
+  drain_s = t1 - t0;
+  cold_s = t2 - t1;
+  return cudaSuccess;
+}
+
+}  // namespace
 
 // ---------------------------------------------------------------- shared-memory plane
 #include <fcntl.h>
@@ -1728,11 +1912,11 @@ void sched_loop(df_ctx* ctx) {
           else T[s] = std::max(1e-6, it->second);
         }
       }
-      uint32_t capn[3] = {uint32_t(ctx->by_stage[0].size()), uint32_t(ctx->by_stage[1].size()),
-                          uint32_t(ctx->by_stage[2].size())};
-      uint32_t G = c.G ? c.G : capn[0] + capn[1] + capn[2];
+      // any allocation over the instance hosts: df_set_ratio re-purposes instances between
+      // stages when a stage needs more than it has
+      const uint32_t G = c.G ? std::min<uint32_t>(c.G, uint32_t(ctx->inst.size())) : uint32_t(ctx->inst.size());
       uint32_t tgt[3];
-      if (ok && plan_ratio(G, T, g, c.move_budget, capn, tgt) && std::memcmp(tgt, g, sizeof(g)) != 0) {
+      if (ok && plan_ratio(G, T, g, c.move_budget, nullptr, tgt) && std::memcmp(tgt, g, sizeof(g)) != 0) {
         df_set_ratio(ctx, tgt[0], tgt[1], tgt[2]);
         ev.action = 3;
         std::memcpy(ev.g, tgt, sizeof(tgt));
@@ -1747,8 +1931,9 @@ void sched_loop(df_ctx* ctx) {
       if (!cc.G) cc.G = uint32_t(ctx->inst.size());
       react(cc, m, have_prev ? &prev : nullptr, g, dlt);
       uint32_t ng[3] = {g[0], g[1], g[2]};
+      const uint32_t hosts = uint32_t(ctx->inst.size());
       for (int s = 0; s < 3 && ev.action == 0; ++s) {
-        if (dlt[s] > 0 && ng[s] < ctx->by_stage[s].size()) {
+        if (dlt[s] > 0 && ng[0] + ng[1] + ng[2] < hosts) {
           ng[s]++;
           ev.action = 1;
           ev.stage = s;
@@ -1960,75 +2145,15 @@ df_status df_init(const df_graph* g, df_ctx** out) {
   for (auto& ip : ctx->inst) {
     Inst& I = *ip;
     if (!I.local) continue;
-    cudaError_t e = I.m.create(c, int(g->precision), I.device, I.stage, g->weight_seed, int(g->max_steps));
+    cudaError_t e = inst_create(ctx, I);
     if (e != cudaSuccess) {
-      std::string m = std::string("df_init: instance create: ") + cudaGetErrorString(e) + " " + df::tls_err;
-      df_finalize(ctx);
-      return fail(nullptr, m);
-    }
-    cudaSetDevice(I.device);
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, I.stage == DF_T ? lo : hi);
-    cudaStreamCreateWithPriority(&I.comm, cudaStreamNonBlocking, hi);
-    cudaStreamCreateWithPriority(&I.aux, cudaStreamNonBlocking, hi);
-    cudaError_t le = cudaSuccess;
-    // T receive slots and E send buffers hold up to two ctx (prompt + negative prompt, CFG);
-    // every receive slot carries a 64-byte trailer (the producer's payload hash, multi-process)
-    size_t slot_bytes = I.stage == DF_T ? ctx->payload(true) : (I.stage == DF_D ? ctx->lat_bytes : 0);
-    I.slot_cap = slot_bytes;
-    if (slot_bytes) {
-      I.slots.slots.resize(g->n_slots);
-      for (uint32_t s = 0; s < g->n_slots; ++s) {
-        if (le == cudaSuccess) le = cudaMalloc(&I.slots.slots[s].buf, slot_bytes + 64);
-        if (le == cudaSuccess) le = cudaEventCreateWithFlags(&I.slots.slots[s].consumed, cudaEventDisableTiming);
-        if (le == cudaSuccess) le = cudaEventRecord(I.slots.slots[s].consumed, I.compute);
-        I.slots.free_list.push_back(int(s));
-      }
-      for (auto& rc : I.rclk)
-        if (le == cudaSuccess) le = clock_create(rc);
-    }
-    if (I.stage == DF_T) {
-      for (int b = 0; b < 2; ++b) {
-        if (le == cudaSuccess) le = cudaMalloc(&I.xbuf[b], ctx->lat_bytes);
-        if (le == cudaSuccess) le = cudaEventCreateWithFlags(&I.xsent[b], cudaEventDisableTiming);
-        if (le == cudaSuccess) le = cudaEventRecord(I.xsent[b], I.comm);
-        for (int k = 0; k < PL_MAX_CHUNKS && le == cudaSuccess; ++k)
-          le = cudaEventCreateWithFlags(&I.hb_ev[b][k], cudaEventDisableTiming);
-      }
-    } else if (I.stage == DF_E) {
-      for (int b = 0; b < 2; ++b) {
-        if (le == cudaSuccess) le = cudaMalloc(&I.ebuf[b], ctx->payload(true));
-        if (le == cudaSuccess) le = cudaEventCreateWithFlags(&I.esent[b], cudaEventDisableTiming);
-        if (le == cudaSuccess) le = cudaEventRecord(I.esent[b], I.comm);
-      }
-      if (le == cudaSuccess) le = cudaMalloc(&I.ids_dev, 2 * size_t(c.L_txt) * 4);
-    } else {
-      if (le == cudaSuccess) le = cudaMalloc(&I.dout, ctx->out_bytes);
-      for (int k = 0; k < 4 && le == cudaSuccess; ++k)
-        le = cudaHostAlloc(&I.stage_host[k], ctx->out_bytes, cudaHostAllocPortable);
-    }
-    if (le == cudaSuccess) le = cudaDeviceSynchronize();
-    if (le == cudaSuccess && mp && slot_bytes) le = mp_publish(ctx, I, slot_bytes);
-    if (le != cudaSuccess) {
-      std::string m = std::string("df_init: setup: ") + cudaGetErrorString(le) + " " + df::tls_err;
+      std::string m = std::string("df_init: instance setup: ") + cudaGetErrorString(e) + " " + df::tls_err;
       df_finalize(ctx);
       return fail(nullptr, m);
     }
   }
-  for (auto& ip : ctx->inst) {
-    Inst* I = ip.get();
-    if (!I->local) continue;
-    if (mp) {
-      if (I->stage == DF_E) I->worker = std::thread(mp_e_worker, ctx, I);
-      else if (I->stage == DF_T) I->worker = std::thread(mp_t_worker, ctx, I);
-      else I->worker = std::thread(mp_d_worker, ctx, I);
-    } else {
-      if (I->stage == DF_E) I->worker = std::thread(e_worker, ctx, I);
-      else if (I->stage == DF_T) I->worker = std::thread(t_worker, ctx, I);
-      else I->worker = std::thread(d_worker, ctx, I);
-    }
-  }
+  for (auto& ip : ctx->inst)
+    if (ip->local) inst_start(ctx, ip.get());
   *out = ctx;
   return DF_OK;
 }
@@ -2063,9 +2188,9 @@ df_status df_finalize(df_ctx* ctx) {
         if (os.open && os.ipc) {
           for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
             cudaEventDestroy(os.ready[c]);
+            cudaEventDestroy(os.issued[c]);
             cudaEventDestroy(os.chunk[c]);
           }
-          cudaEventDestroy(os.start);
         }
         os = OpenSet{};
       }
@@ -2082,29 +2207,13 @@ df_status df_finalize(df_ctx* ctx) {
         if (!ss) continue;
         for (int c = 0; c < PL_MAX_CHUNKS; ++c) {
           cudaEventDestroy(ss->ready[c]);
+          cudaEventDestroy(ss->issued[c]);
           cudaEventDestroy(ss->chunk[c]);
         }
-        cudaEventDestroy(ss->start);
         delete ss;
         I.sendset[p][sl] = nullptr;
       }
-    for (auto& rc : I.rclk) clock_destroy(rc);
-    for (auto& s : I.slots.slots) {
-      if (s.buf) cudaFree(s.buf);
-      if (s.consumed) cudaEventDestroy(s.consumed);
-    }
-    for (int b = 0; b < 2; ++b) {
-      if (I.xbuf[b]) cudaFree(I.xbuf[b]);
-      if (I.xsent[b]) cudaEventDestroy(I.xsent[b]);
-      for (int k = 0; k < PL_MAX_CHUNKS; ++k)
-        if (I.hb_ev[b][k]) cudaEventDestroy(I.hb_ev[b][k]);
-      if (I.ebuf[b]) cudaFree(I.ebuf[b]);
-      if (I.esent[b]) cudaEventDestroy(I.esent[b]);
-    }
-    if (I.ids_dev) cudaFree(I.ids_dev);
-    if (I.dout) cudaFree(I.dout);
-    for (auto* h : I.stage_host)
-      if (h) cudaFreeHost(h);
+    inst_free(I);
     if (I.compute) cudaStreamDestroy(I.compute);
     if (I.comm) cudaStreamDestroy(I.comm);
     if (I.aux) cudaStreamDestroy(I.aux);
@@ -2191,12 +2300,55 @@ df_status df_poll(df_ctx* ctx, df_completion* out, uint32_t max, uint32_t* n_out
 
 df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD) {
   if (!ctx) return DF_ERR_INVALID;
+  if (ctx->failed) return fail(ctx, ctx->err, DF_ERR_STATE);
   std::lock_guard<std::mutex> lk(ctx->ratio_mu);
-  uint32_t g[3] = {gE, gT, gD};
-  for (int s = 0; s < 3; ++s)
-    if (g[s] < 1 || g[s] > ctx->by_stage[s].size()) return fail(ctx, "df_set_ratio: capacity", DF_ERR_CAPACITY);
-  // New requests go to the first g_s instances of each stage; retirees drain their
-  // inboxes (already-assigned work completes; nothing is dropped).
+  const uint32_t g[3] = {gE, gT, gD};
+  const uint32_t hosts = uint32_t(ctx->inst.size());
+  const uint32_t G = ctx->g.G ? std::min<uint32_t>(ctx->g.G, hosts) : hosts;
+  if (g[0] < 1 || g[1] < 1 || g[2] < 1 || g[0] + g[1] + g[2] > G)  // Eq. 1
+    return fail(ctx, "df_set_ratio: capacity (every g_s >= 1, sum g <= G)", DF_ERR_CAPACITY);
+  int have[3];
+  {
+    std::lock_guard<std::mutex> rl(ctx->route_mu);
+    for (int s = 0; s < 3; ++s) have[s] = int(ctx->by_stage[s].size());
+  }
+  // Stages short of instances take them from stages with a surplus (the last instances of
+  // the donor's routing list, i.e. the ones beyond its active prefix first): drain ->
+  // re-initialise for the new stage -> serve (Alg. 1 "Apply"; cold start P:L357).
+  // Re-purposing needs the instance in this process (single-process contexts).
+  for (int s = 0; s < 3; ++s) {
+    while (have[s] < int(g[s])) {
+      int donor = -1;
+      for (int t = 0; t < 3; ++t)
+        if (t != s && have[t] > int(g[t]) && (donor < 0 || have[t] - int(g[t]) > have[donor] - int(g[donor]))) donor = t;
+      if (donor < 0) return fail(ctx, "df_set_ratio: no instance to re-purpose", DF_ERR_CAPACITY);
+      if (ctx->mp) return fail(ctx, "df_set_ratio: re-purposing needs a single-process context", DF_ERR_STATE);
+      Inst* I;
+      {
+        std::lock_guard<std::mutex> rl(ctx->route_mu);
+        I = ctx->inst[ctx->by_stage[donor].back()].get();
+        ctx->active[donor] = std::min<int>(ctx->active[donor].load(), int(g[donor]));  // stop routing to it first
+      }
+      double drain_s = 0, cold_s = 0;
+      cudaError_t e = inst_repurpose(ctx, I, s, drain_s, cold_s);
+      if (e != cudaSuccess)
+        return fail(ctx, std::string("df_set_ratio: re-purpose: ") + cudaGetErrorString(e) + " " + df::tls_err);
+      have[donor]--, have[s]++;
+      df_sched_event ev{};
+      ev.t = now_s();
+      ev.action = 4;
+      ev.stage = s;
+      ev.inst = I->id;
+      ev.from_stage = donor;
+      ev.drain_ms = float(drain_s * 1e3);
+      ev.cold_start_ms = float(cold_s * 1e3);
+      std::memcpy(ev.g, g, sizeof(ev.g));
+      std::lock_guard<std::mutex> sl(ctx->sched_mu);
+      ctx->sched_log.push_back(ev);
+    }
+  }
+  // New requests go to the first g_s instances of each stage; instances beyond them drain
+  // their inboxes (already-assigned work completes; nothing is dropped).
   for (int s = 0; s < 3; ++s) ctx->active[s] = int(g[s]);
   return DF_OK;
 }

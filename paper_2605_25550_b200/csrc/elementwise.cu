@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(128, 8) rmsnorm_warp_kernel(const float* __res
 
 // Bulk-copy variant: one elected thread moves the CTA's 4 rows of x into shared memory with
 // cp.async.bulk (one mbarrier, no per-thread load instructions in flight), then each warp
-// reduces and normalises its row from shared memory.  DF_RMS_BULK=1 selects it (A/B).
+// reduces and normalises its row from shared memory.  DF_RMS_IMPL=2 selects it (A/B).
 DF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -338,15 +338,127 @@ __global__ void __launch_bounds__(128) rmsnorm_bulk_kernel(const float* __restri
   }
 }
 
+// Persistent streaming variant (the model widths, default): one CTA per SM loops over rows
+// r = blockIdx.x + k * gridDim.x.  A producer thread keeps a ring of STAGES rows in shared
+// memory filled with one cp.async.bulk per row (mbarrier complete_tx), so every SM always has
+// ~STAGES x row bytes of HBM reads in flight; consumer warp w normalises the rows k = w mod NW
+// of its CTA from shared memory (two passes over the row: sum of squares, then scale), writes
+// the bf16/fp32 row with coalesced stores and hands the stage back.  The one-row-per-warp
+// kernel above issues a row's loads, waits, then writes: with the whole grid resident in one
+// wave its read and write phases do not overlap and its launch tail is exposed (3.9 TB/s in
+// the image step).
+constexpr int RMS_NW = 8;  // consumer warps per CTA
+template <int VPT>
+struct RmsStream {
+  static constexpr int ROW = 128 * VPT * 4;                  // bytes of one fp32 row
+  static constexpr int STAGES = (200 * 1024) / ROW < 16 ? (200 * 1024) / ROW : 16;
+  static constexpr int OFF_BAR = STAGES * ROW;
+  static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8 + 128;
+};
+
+template <int VPT, typename OutT>
+__global__ void __launch_bounds__(32 * (RMS_NW + 1), 1)
+    rmsnorm_stream_kernel(const float* __restrict__ x, OutT* __restrict__ out, int M, const float* __restrict__ shift,
+                          const float* __restrict__ scale, const bf16* __restrict__ gain, float eps) {
+  using Cfg = RmsStream<VPT>;
+  constexpr int d = 128 * VPT;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float4* ring = reinterpret_cast<float4*>(sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + Cfg::OFF_BAR);
+  uint64_t* empty = full + Cfg::STAGES;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  const int nk = M > int(blockIdx.x) ? (M - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 0;
+  if (w == RMS_NW) {  // producer
+    if (lane == 0) {
+      for (int k = 0; k < nk; ++k) {
+        const int s = k % Cfg::STAGES;
+        mbar_wait(&empty[s], ((k / Cfg::STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], Cfg::ROW);
+        bulk_g2s(ring + size_t(s) * (d / 4), x + (size_t(blockIdx.x) + size_t(k) * gridDim.x) * d, Cfg::ROW, &full[s]);
+      }
+    }
+    return;
+  }
+  for (int k = w; k < nk; k += RMS_NW) {
+    const int s = k % Cfg::STAGES;
+    mbar_wait(&full[s], (k / Cfg::STAGES) & 1);
+    const float4* xr = ring + size_t(s) * (d / 4);
+    float ss = 0.f;
+#pragma unroll 8
+    for (int i = 0; i < VPT; ++i) {
+      const float4 t = xr[lane + 32 * i];
+      ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / float(d) + eps);
+    OutT* orow = out + (size_t(blockIdx.x) + size_t(k) * gridDim.x) * d;
+#pragma unroll 8
+    for (int i = 0; i < VPT; ++i) {
+      const int c = lane + 32 * i;
+      const float4 t = xr[c];
+      float y[4] = {t.x * inv, t.y * inv, t.z * inv, t.w * inv};
+      if (gain) {
+        const uint2 g = reinterpret_cast<const uint2*>(gain)[c];
+        y[0] *= bf_lo(g.x), y[1] *= bf_hi(g.x), y[2] *= bf_lo(g.y), y[3] *= bf_hi(g.y);
+      } else {
+        const float4 sc = reinterpret_cast<const float4*>(scale)[c];
+        const float4 sh = reinterpret_cast<const float4*>(shift)[c];
+        y[0] = y[0] * (1.f + sc.x) + sh.x;
+        y[1] = y[1] * (1.f + sc.y) + sh.y;
+        y[2] = y[2] * (1.f + sc.z) + sh.z;
+        y[3] = y[3] * (1.f + sc.w) + sh.w;
+      }
+      if constexpr (sizeof(OutT) == 2) {
+        uint2 u;
+        u.x = pack_bf16x2(y[0], y[1]);
+        u.y = pack_bf16x2(y[2], y[3]);
+        reinterpret_cast<uint2*>(orow)[c] = u;
+      } else {
+        reinterpret_cast<float4*>(orow)[c] = make_float4(y[0], y[1], y[2], y[3]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the stage are done
+  }
+}
+
 template <int VPT>
 static cudaError_t launch_rms_warp(const float* x, void* out, int out_f32, int M, const float* shift,
                                    const float* scale, const bf16* gain, float eps, cudaStream_t st) {
   void* args[] = {(void*)&x, (void*)&out, (void*)&M, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
   dim3 grid((M + 3) / 4);
-  static const int bulk = [] {
-    const char* e = getenv("DF_RMS_BULK");
+  static const int impl = [] {  // DF_RMS_IMPL (A/B): 0 streaming (default), 1 warp per row, 2 bulk per CTA
+    const char* e = getenv("DF_RMS_IMPL");
     return e ? atoi(e) : 0;
   }();
+  const int bulk = impl == 2;
+  if (impl == 0 && VPT >= 16) {
+    using Cfg = RmsStream<VPT>;
+    const void* kern =
+        out_f32 ? (const void*)rmsnorm_stream_kernel<VPT, float> : (const void*)rmsnorm_stream_kernel<VPT, bf16>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute((const void*)rmsnorm_stream_kernel<VPT, float>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)rmsnorm_stream_kernel<VPT, bf16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const int g = M < num_sms() ? M : num_sms();
+    return launch_ex(kern, dim3(g), dim3(32 * (RMS_NW + 1)), Cfg::SMEM, st, args);
+  }
   if (bulk) {
     const size_t smem = 16 + size_t(4) * 128 * VPT * 4;
     const void* kern = out_f32 ? (const void*)rmsnorm_bulk_kernel<VPT, float> : (const void*)rmsnorm_bulk_kernel<VPT, bf16>;
@@ -433,6 +545,17 @@ cudaError_t add_into(void* o, const void* oi, size_t n, int f32, cudaStream_t st
 }
 
 // ------------------------------------------------------------------ time conditioning
+__global__ void sigma_kernel(float* sig, int S, float shift) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > S) return;
+  const double si = 1.0 - double(i) / double(S);
+  sig[i] = float(double(shift) * si / (1.0 + (double(shift) - 1.0) * si));
+}
+cudaError_t sigma_schedule(float* sig, int S, float shift, cudaStream_t st) {
+  sigma_kernel<<<(S + 1 + 127) / 128, 128, 0, st>>>(sig, S, shift);
+  return cudaGetLastError();
+}
+
 __global__ void sinusoid_kernel(const float* sig, float* s, int S, int freq_dim) {
   int i = blockIdx.x;
   int half = freq_dim / 2;

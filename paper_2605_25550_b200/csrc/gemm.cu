@@ -320,20 +320,24 @@ enum : int { TK_DIRECT = 0, TK_STORE_F32 = 1, TK_STORE_BF16 = 2, TK_GRES = 3, TK
 // Stream-K (epi.sk_ws set; needs tiles >= pairs): the tiles x KB k-blocks are cut into
 // `pairs` equal contiguous ranges, so every pair gets the same MMA work.  A tile cut
 // between pair p (its first k-blocks, the "head") and pair p + 1 (the rest, the "tail") is
-// finished by p + 1.  Each pair runs its partial units FIRST: the head (raw partial to
-// workspace slot p, published with an epoch flag), then the tail (waits for slot p - 1's
-// flag, adds that partial to its own accumulator, normal epilogue), then its whole tiles.
-// The fix-up therefore overlaps the whole-tile mainloops instead of sitting at the end,
-// and it is one fp32 add of two fixed partials: deterministic.
+// finished by p + 1.  Each pair runs its head FIRST (raw partial to workspace slot p,
+// published with an epoch flag), then one whole tile, then its tail (waits for slot p - 1's
+// flag, adds that partial to its own accumulator, normal epilogue), then its other whole
+// tiles: the fix-up overlaps whole-tile mainloops instead of sitting at the end, and a short
+// partial unit never follows another short one (two in a row left the MMA waiting for the
+// accumulator the previous unit's epilogue was still draining).  One fp32 add of two fixed
+// partials: deterministic.
 struct PairSched {
   int tiles, KB, pairs, cid;
   bool sk;
-  int t;           // data-parallel cursor
-  int n, i;        // stream-K: unit count, cursor
-  int ut[3], u0[3], u1[3];
-  int full0, full1;  // stream-K whole tiles [full0, full1)
+  int t;                 // data-parallel cursor
+  int hd_t, hd_k1;       // stream-K head unit: tile, k-blocks [0, hd_k1) (hd_k1 = 0: none)
+  int tl_t, tl_k0;       // stream-K tail unit: tile, k-blocks [tl_k0, KB) (tl_k0 = 0: none)
+  int full0, full1;      // stream-K whole tiles [full0, full1)
+  int state;             // 0 head, 1 first whole tile, 2 tail, 3 other whole tiles
   DF_DEV PairSched(int tiles_, int KB_, int pairs_, int cid_, bool sk_)
-      : tiles(tiles_), KB(KB_), pairs(pairs_), cid(cid_), sk(sk_), t(cid_), n(0), i(0) {
+      : tiles(tiles_), KB(KB_), pairs(pairs_), cid(cid_), sk(sk_), t(cid_), hd_t(0), hd_k1(0), tl_t(0), tl_k0(0),
+        full0(0), full1(0), state(0) {
     if (!sk) return;
     const long long total = (long long)tiles * KB;
     const long long b = total * cid / pairs, e = total * (cid + 1) / pairs;
@@ -341,14 +345,8 @@ struct PairSched {
     const int tb = int(e / KB), kb = int(e % KB);  // last tile (exclusive when kb == 0), end offset
     full0 = ka ? ta + 1 : ta;
     full1 = tb;
-    if (kb) {  // head: first kb k-blocks of tile tb
-      ut[n] = tb, u0[n] = 0, u1[n] = kb;
-      ++n;
-    }
-    if (ka) {  // tail: k-blocks [ka, KB) of tile ta
-      ut[n] = ta, u0[n] = ka, u1[n] = KB;
-      ++n;
-    }
+    hd_t = tb, hd_k1 = kb;
+    tl_t = ta, tl_k0 = ka;
   }
   // next unit: tile, k-block range [k0, k1)
   DF_DEV bool next(int& tile, int& k0, int& k1) {
@@ -360,16 +358,35 @@ struct PairSched {
       t += pairs;
       return true;
     }
-    if (i < n) {
-      tile = ut[i], k0 = u0[i], k1 = u1[i];
-      ++i;
-      return true;
+    for (;;) {
+      switch (state) {
+        case 0:
+          state = 1;
+          if (hd_k1) {
+            tile = hd_t, k0 = 0, k1 = hd_k1;
+            return true;
+          }
+          break;
+        case 1:
+          state = 2;
+          if (full0 < full1) {
+            tile = full0++, k0 = 0, k1 = KB;
+            return true;
+          }
+          break;
+        case 2:
+          state = 3;
+          if (tl_k0) {
+            tile = tl_t, k0 = tl_k0, k1 = KB;
+            return true;
+          }
+          break;
+        default:
+          if (full0 >= full1) return false;
+          tile = full0++, k0 = 0, k1 = KB;
+          return true;
+      }
     }
-    if (full0 >= full1) return false;
-    tile = full0++;
-    k0 = 0;
-    k1 = KB;
-    return true;
   }
 };
 

@@ -50,6 +50,11 @@ cudaError_t patchify(const float* x, const float* y, int Cy, void* X, int out_f3
                      int ph, int pw, cudaStream_t st);
 // o += oi (bf16 or fp32, n elements)
 cudaError_t add_into(void* o, const void* oi, size_t n, int f32, cudaStream_t st);
+// The sigma schedule (R13) on the device, in fp64 then rounded to fp32 exactly as the host's
+// sigmas_host: s_i = 1 - i/S, sigma_i = shift s_i / (1 + (shift - 1) s_i), i = 0..S.  The
+// pipeline workers use it so that no pageable host->device copy (a host-blocking stream sync)
+// sits on their enqueue path.
+cudaError_t sigma_schedule(float* sig, int S, float shift, cudaStream_t st);
 // sinusoid rows s[i, :] = [cos(1000 sig_i w) | sin(1000 sig_i w)], i < S
 cudaError_t sinusoid(const float* sig_dev, float* s, int S, int freq_dim, cudaStream_t st);
 // mods[l][k][:] = e6[k][:] + M_l[k][:] for k < 6, all layers; head[0..1][:] = head_mod + e

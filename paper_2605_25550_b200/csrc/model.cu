@@ -462,7 +462,11 @@ cudaError_t Model::prepare(const void* ctx_bf16, const float* sig_host, int S, c
   // part runs while the payload is still in flight
   if (!f32()) DF_TRY(cudaMemsetAsync(cd.kc, 0, 2 * al(kvb), st));  // dh padding = 0
   if (i2v() && !f32()) DF_TRY(cudaMemsetAsync(cd.kci, 0, 2 * al(kvbi), st));
-  DF_TRY(cudaMemcpyAsync(cd.sig_dev, sig_host, (S + 1) * 4, cudaMemcpyHostToDevice, st));
+  if (hook && hook->shift > 0.f) {
+    DF_L(sigma_schedule(cd.sig_dev, S, hook->shift, st));  // no pageable copy on a worker's enqueue path
+  } else {
+    DF_TRY(cudaMemcpyAsync(cd.sig_dev, sig_host, (S + 1) * 4, cudaMemcpyHostToDevice, st));
+  }
   // time conditioning for all S steps (R4, R5), fp32 SIMT: the M = S rows are GEMV-like
   DF_L(sinusoid(cd.sig_dev, s, S, fd, st));
   DF_L(gemm_simt(s, 0, fd, ACT_NONE, temb1_wT, fd, t1, d, S, d, fd, temb1_b, ACT_SILU, st));

@@ -16,7 +16,7 @@
 //                 IPC handles of the events of the transfer currently in that slot.
 // Events are always owned (created and recorded) by the side whose stream records them: a
 // CUDA event can only be recorded on a stream of its own device, while a stream may wait on
-// an event of any device.  So the producer creates its per-(consumer, slot) ready / start /
+// an event of any device.  So the producer creates its per-(consumer, slot) ready / issued /
 // chunk events and publishes their handles into the consumer's slot record when it claims the
 // slot; the consumer records `consumed`.
 #pragma once
@@ -108,12 +108,13 @@ struct ShmRing {
 
 // Producer-owned events of one transfer (handles published into the consumer's slot record):
 // ready[c] = chunk c's data existed (comm stream, after waiting the producer's compute, before
-// any injected delay), start = the first copy is issued, chunk[c] = chunk c landed.
+// any injected delay), issued[c] = chunk c's copy is issued (after any delay), chunk[c] =
+// chunk c landed.
 struct XferEvHandles {
   int32_t producer;                      // instance that published them (consumer caches per producer)
   uint32_t nchunks;
   cudaIpcEventHandle_t ready[PL_MAX_CHUNKS];
-  cudaIpcEventHandle_t start;
+  cudaIpcEventHandle_t issued[PL_MAX_CHUNKS];
   cudaIpcEventHandle_t chunk[PL_MAX_CHUNKS];
 };
 

@@ -100,6 +100,7 @@ struct LatentBlocks {
 struct ChunkHook {
   int rows_per_chunk = 0;
   int nchunks = 0;
+  float shift = 0.f;        // > 0: the sigma schedule is generated on the device (sigma_schedule)
   cudaError_t (*wait)(void* user, int c) = nullptr;
   void* user = nullptr;
 };

@@ -155,9 +155,11 @@ def test_two_process_handoff_is_asynchronous(mode):
     by_t = {}
     for tag, t_inst, t_end_t, exposed1, xfer1, xfer0, h0, h1 in got:
         assert h0 and h1
-        assert exposed1 >= 0.8 * d * 1e3, exposed1          # D stalled on the delayed chunk
         assert 0 < xfer0 < 0.5 * d * 1e3 and 0 < xfer1 < 0.5 * d * 1e3  # copies timed without the delay
         by_t.setdefault(t_inst, []).append(t_end_t)
+    # D stalled on delayed data (its decodes are serial, so a stall that overlaps an earlier
+    # request's is counted once, on that request)
+    assert max(g[3] for g in got) >= 0.8 * d * 1e3
     assert len(by_t) == 2
     for t_inst, ends in by_t.items():
         ends.sort()

@@ -180,8 +180,15 @@ def test_consumers_start_before_the_last_chunk_lands():
     seeds = [11, 12]
 
     def run(chunks, jit, jc=0):
+        # one request at a time: the consumers are idle when a transfer starts, so the time they
+        # spend on the early chunks is not hidden behind a previous request's work
+        outs, comps = {}, []
         with make_ctx(cfg, chunk_bytes=chunks, jitter=jit, jitter_chunk=jc) as c:
-            return _run_requests(c, cfg, seeds, 3, 3.0)
+            for s in seeds:
+                o, cc = _run_requests(c, cfg, [s], 3, 3.0)
+                outs.update(o)
+                comps += cc
+        return outs, comps
 
     o_whole, _ = run((0, 0), (0.0, 0.0, 0))
     o_ref, c_ref = run((4096, 16384), (0.0, 0.0, 0))
@@ -226,3 +233,33 @@ def test_latent_block_handoff_bit_exact(chunk, flags, F):
             want = -(-cfg.H // hb)
         assert n == want
         assert h[0] == h[1] == cap.payload_hash(buf)
+
+
+def test_steady_qps_meets_the_eq6_bound():
+    """P14 (Eq. 6): in asynchronous saturating mode the measured steady request
+    rate is at most min_s g_s / T_s over the measured per-instance stage times, and at least
+    0.9x of it.  MID shape, 12-step requests, E:T:D = 1:1:1 on one GPU (E and D are far from
+    the bottleneck; with two DiT instances sharing one GPU each one's device time would
+    include the other's kernels and no longer be its service time).  Steady window:
+    completions 4..N-1 (warm-up and the drain excluded)."""
+    cfg = MID
+    inst = [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)]
+    n = 24
+    with make_ctx(cfg, instances=inst, chunk_bytes=(4096, 16384)) as c:
+        for s in range(n):
+            while c.submit(12, 3.0, 400 + s, user_tag=s)[0] != B.DF_OK:
+                pass
+        comps = []
+        while len(comps) < n:
+            comps += c.poll(16, timeout_ms=60000)
+    comps.sort(key=lambda x: x.t_done)
+    win = comps[4:]
+    rate = (len(win) - 1) / (win[-1].t_done - win[0].t_done)
+    med = lambda v: float(np.median(v))  # noqa: E731
+    T = [med([x.t_end[0] - x.t_start[0] for x in comps]),   # E: host enqueue time (never waits)
+         med([x.stage_ms[1] for x in comps]) * 1e-3,        # T: device time of one request
+         med([x.stage_ms[2] for x in comps]) * 1e-3]        # D: device decode time
+    bound, stage = cap.qps((1, 1, 1), T)
+    assert stage == "T"
+    assert rate <= bound * 1.02, (rate, bound, T)           # 2 %: median-vs-window sampling
+    assert rate >= 0.9 * bound, (rate, bound, T)
