@@ -171,13 +171,28 @@ struct BusyClock {
   std::mutex mu;
   uint64_t acc = 0;
   double since = -1;
+  InstStat* mirror = nullptr;  // multi-process: the same intervals in the shared plane
   void begin(double t) {
     std::lock_guard<std::mutex> lk(mu);
-    if (since < 0) since = t;
+    if (since < 0) {
+      since = t;
+      if (mirror) {
+        uint64_t b;
+        std::memcpy(&b, &t, 8);
+        mirror->busy_since.store(b, std::memory_order_release);
+      }
+    }
   }
   void end(double t) {
     std::lock_guard<std::mutex> lk(mu);
-    if (since >= 0) acc += uint64_t(std::max(0.0, t - since) * 1e9), since = -1;
+    if (since >= 0) {
+      const uint64_t d = uint64_t(std::max(0.0, t - since) * 1e9);
+      acc += d, since = -1;
+      if (mirror) {
+        mirror->busy_ns.fetch_add(d);
+        mirror->busy_since.store(0, std::memory_order_release);
+      }
+    }
   }
   uint64_t sample(double t) {
     std::lock_guard<std::mutex> lk(mu);
@@ -671,12 +686,48 @@ cudaError_t block_done_cb(void* u, int k) {
 }
 
 // ---------------------------------------------------------------- workers
+// Scheduler-visible state lives in the context (one process) or in the shared plane (one
+// process per GPU, so that a controller on any rank sees and steers every rank's instances).
+std::atomic<int>& active_of(df_ctx* ctx, int s) { return ctx->mp ? ctx->seg->active[s] : ctx->active[s]; }
+
+void qd_add(df_ctx* ctx, int s, double sec) {
+  std::atomic<uint64_t>* ns = ctx->mp ? ctx->seg->qd_ns : ctx->qd_ns;
+  std::atomic<uint64_t>* cnt = ctx->mp ? ctx->seg->qd_count : ctx->qd_count;
+  ns[s] += uint64_t(std::max(0.0, sec) * 1e9);
+  cnt[s]++;
+}
+
+struct SpinLock {
+  std::atomic<uint32_t>& l;
+  explicit SpinLock(std::atomic<uint32_t>& x) : l(x) {
+    uint32_t z = 0;
+    while (!l.compare_exchange_weak(z, 1u, std::memory_order_acquire)) {
+      z = 0;
+      std::this_thread::yield();
+    }
+  }
+  ~SpinLock() { l.store(0, std::memory_order_release); }
+};
+
+// Busy nanoseconds of instance i up to now (closed intervals + the open one).
+uint64_t busy_sample(df_ctx* ctx, int i, double t) {
+  if (!ctx->mp) return ctx->inst[i]->busy.sample(t);
+  InstStat& st = ctx->seg->stat[i];
+  uint64_t b = st.busy_ns.load(), sb = st.busy_since.load(std::memory_order_acquire);
+  if (sb) {
+    double since;
+    std::memcpy(&since, &sb, 8);
+    b += uint64_t(std::max(0.0, t - since) * 1e9);
+  }
+  return b;
+}
+
 // Round-robin over the active instances of a stage by request sequence number (deterministic).
 // hold: the caller will hand the chosen instance a job later (single-process workers); the
 // instance cannot finish retiring until that hand-over (release_pick) happened.
 int pick(df_ctx* ctx, int stage, uint64_t seq, bool hold = false) {
   std::lock_guard<std::mutex> lk(ctx->route_mu);
-  int n = ctx->active[stage].load();
+  int n = active_of(ctx, stage).load();
   auto& v = ctx->by_stage[stage];
   if (n <= 0 || v.empty()) return -1;
   const int id = v[seq % uint64_t(std::min<int>(n, int(v.size())))];
@@ -690,10 +741,77 @@ void release_pick(Inst* I) {
 // Stage-time profile for the Eq. 6 planner: EMA of seconds per request per instance, keyed by
 // the workload (steps for T; E and D do not depend on steps, tab:stage_time).
 void sched_note(df_ctx* ctx, int stage, uint32_t key, double sec) {
+  if (ctx->mp) {
+    StageEma& e = ctx->seg->ema[stage];
+    SpinLock lk(e.lock);
+    for (uint32_t k = 0; k < e.n; ++k)
+      if (e.key[k] == key) {
+        e.sec[k] = 0.7 * e.sec[k] + 0.3 * sec;
+        return;
+      }
+    const uint32_t k = e.n < 8 ? e.n++ : 7;
+    e.key[k] = key;
+    e.sec[k] = sec;
+    return;
+  }
   std::lock_guard<std::mutex> lk(ctx->sched_mu);
   auto it = ctx->stage_s[stage].find(key);
   if (it == ctx->stage_s[stage].end()) ctx->stage_s[stage][key] = sec;
   else it->second = 0.7 * it->second + 0.3 * sec;
+}
+
+bool stage_time(df_ctx* ctx, int stage, uint32_t key, double& out) {
+  if (ctx->mp) {
+    StageEma& e = ctx->seg->ema[stage];
+    SpinLock lk(e.lock);
+    for (uint32_t k = 0; k < e.n; ++k)
+      if (e.key[k] == key) {
+        out = e.sec[k];
+        return true;
+      }
+    return false;
+  }
+  std::lock_guard<std::mutex> lk(ctx->sched_mu);
+  auto it = ctx->stage_s[stage].find(key);
+  if (it == ctx->stage_s[stage].end()) return false;
+  out = it->second;
+  return true;
+}
+
+// Workload keys (steps) of the last 64 admitted requests, for Alg. 1's Changed(H).
+void hist_push(df_ctx* ctx, uint32_t key) {
+  if (ctx->mp) {
+    PlaneSeg* g = ctx->seg;
+    SpinLock lk(g->hist_lock);
+    g->hist[(g->hist_head + g->hist_n) % 64] = key;
+    if (g->hist_n < 64) ++g->hist_n;
+    else g->hist_head = (g->hist_head + 1) % 64;
+    return;
+  }
+  std::lock_guard<std::mutex> lk(ctx->sched_mu);
+  ctx->hist.push_back(key);
+  while (ctx->hist.size() > 64) ctx->hist.pop_front();
+}
+std::vector<uint32_t> hist_keys(df_ctx* ctx) {
+  std::vector<uint32_t> k;
+  if (ctx->mp) {
+    PlaneSeg* g = ctx->seg;
+    SpinLock lk(g->hist_lock);
+    for (uint32_t i = 0; i < g->hist_n; ++i) k.push_back(g->hist[(g->hist_head + i) % 64]);
+    return k;
+  }
+  std::lock_guard<std::mutex> lk(ctx->sched_mu);
+  k.assign(ctx->hist.begin(), ctx->hist.end());
+  return k;
+}
+void hist_clear(df_ctx* ctx) {
+  if (ctx->mp) {
+    SpinLock lk(ctx->seg->hist_lock);
+    ctx->seg->hist_n = 0;
+    return;
+  }
+  std::lock_guard<std::mutex> lk(ctx->sched_mu);
+  ctx->hist.clear();
 }
 
 void worker_fail(df_ctx* ctx, const std::string& m) {
@@ -766,7 +884,7 @@ cudaError_t encode_request(df_ctx* ctx, Inst* me, ReqState* rs, int b) {
 bool routed(df_ctx* ctx, const Inst* I) {
   std::lock_guard<std::mutex> lk(ctx->route_mu);
   const auto& v = ctx->by_stage[I->stage];
-  const int n = std::min<int>(ctx->active[I->stage].load(), int(v.size()));
+  const int n = std::min<int>(active_of(ctx, I->stage).load(), int(v.size()));
   for (int k = 0; k < n; ++k)
     if (v[k] == I->id) return true;
   return false;
@@ -791,8 +909,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
     rs->inst[0] = me->id;
     rs->t_start[0] = now_s();
     me->busy.begin(rs->t_start[0]);
-    ctx->qd_ns[0] += uint64_t((rs->t_start[0] - rs->t_submit) * 1e9);
-    ctx->qd_count[0]++;
+    qd_add(ctx, 0, rs->t_start[0] - rs->t_submit);
     WK(cudaEventCreate(&rs->ev[0]));
     WK(cudaEventCreate(&rs->ev[1]));
     const int tid = pick(ctx, DF_T, rs->seq, true);
@@ -885,8 +1002,7 @@ void t_worker(df_ctx* ctx, Inst* me) {
     ReqState* rs = j.rs;
     rs->t_start[1] = now_s();
     me->busy.begin(rs->t_start[1]);
-    ctx->qd_ns[1] += uint64_t(std::max(0.0, rs->t_start[1] - rs->t_end[0]) * 1e9);
-    ctx->qd_count[1]++;
+    qd_add(ctx, 1, rs->t_start[1] - rs->t_end[0]);
     WK(cudaEventCreate(&rs->ev[2]));
     WK(cudaEventCreate(&rs->ev[3]));
     const int S = int(rs->req.steps);
@@ -978,8 +1094,7 @@ void d_worker(df_ctx* ctx, Inst* me) {
     ReqState* rs = j.rs;
     rs->t_start[2] = now_s();
     me->busy.begin(rs->t_start[2]);
-    ctx->qd_ns[2] += uint64_t(std::max(0.0, rs->t_start[2] - rs->t_end[1]) * 1e9);
-    ctx->qd_count[2]++;
+    qd_add(ctx, 2, rs->t_start[2] - rs->t_end[1]);
     WK(cudaEventCreate(&rs->ev[4]));
     WK(cudaEventCreate(&rs->ev[5]));
     Xfer* x1 = rs->x[1];
@@ -1270,16 +1385,26 @@ cudaError_t mp_finish_slot(df_ctx* ctx, Inst* me, RecvClock& rc, uint32_t s, uin
 
 void mp_e_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
+  ReqRec q;
   while (!ctx->stop.load()) {
-    ReqState* rs = nullptr;
-    {
-      std::lock_guard<std::mutex> lk(ctx->req_mu);
-      if (!ctx->requests->pop(rs)) rs = nullptr;
-    }
-    if (!rs) {
+    if (!routed(ctx, me) || !ctx->seg->requests.pop(q)) {  // only encoders in the active prefix pull
       mp_sleep();
       continue;
     }
+    auto rs = new ReqState();
+    rs->seq = q.seq;
+    rs->id = {q.id_lo, q.id_hi};
+    rs->t_submit = q.t_submit;
+    rs->req.seed = q.seed;
+    rs->req.user_tag = q.user_tag;
+    rs->req.steps = q.steps;
+    rs->req.shift = q.shift;
+    rs->req.guidance = q.guidance;
+    rs->req.out_host = (q.flags & 1u) ? reinterpret_cast<void*>(uintptr_t(1)) : nullptr;  // flag only: D delivers
+    const size_t L = ctx->g.dit.L_txt;
+    if (q.flags & 2u) rs->ids.assign(q.tokens[0], q.tokens[0] + L);
+    if (q.flags & 4u) rs->neg_ids.assign(q.tokens[1], q.tokens[1] + L);
+    qd_add(ctx, 0, now_s() - q.t_submit);
     MetaRec m{};
     m.seq = rs->seq;
     m.id_lo = rs->id.lo;
@@ -1303,6 +1428,7 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
     m.t_end_e = now_s();
     m.stage_ms_e = float((m.t_end_e - m.t_start_e) * 1e3);  // host enqueue time (E never waits)
     me->busy.end(m.t_end_e);
+    sched_note(ctx, 0, 0u, m.t_end_e - m.t_start_e);
     const uint64_t bytes = ctx->payload(cfgr);
     if (!mp_send(ctx, me, tid, me->ebuf[b], plan_ctx(ctx, bytes), me->compute, nullptr, m, 0)) {
       free_req(rs);
@@ -1759,7 +1885,10 @@ PlaneSeg* plane_open(const char* name, bool create, uint32_t world, std::string*
     for (int i = 0; i < PL_MAX_INST; ++i) {
       seg->inst[i].free_slots.init();
       seg->inst[i].inbox.init();
+      seg->stat[i].busy_ns = 0;
+      seg->stat[i].busy_since = 0;
     }
+    seg->requests.init();
     seg->magic.store(PLANE_MAGIC, std::memory_order_release);
   } else {
     for (int t = 0; t < 120000 && seg->magic.load(std::memory_order_acquire) != PLANE_MAGIC; ++t)
@@ -1863,7 +1992,7 @@ void sched_loop(df_ctx* ctx) {
   df_sched_metrics prev{};
   bool have_prev = false;
   std::vector<uint64_t> busy0(ctx->inst.size());
-  for (size_t i = 0; i < ctx->inst.size(); ++i) busy0[i] = ctx->inst[i]->busy.sample(now_s());
+  for (size_t i = 0; i < ctx->inst.size(); ++i) busy0[i] = busy_sample(ctx, int(i), now_s());
   double t_prev = now_s();
   while (!ctx->sched_stop.load()) {
     for (int k = 0; k < int(c.delta_s * 100) && !ctx->sched_stop.load(); ++k)
@@ -1873,56 +2002,60 @@ void sched_loop(df_ctx* ctx) {
     t_prev = t;
     df_sched_metrics m{};
     uint32_t g[3];
-    for (int s = 0; s < 3; ++s) g[s] = uint32_t(ctx->active[s].load());
+    for (int s = 0; s < 3; ++s) g[s] = uint32_t(active_of(ctx, s).load());
     for (int s = 0; s < 3; ++s) {
-      const auto& ids = ctx->by_stage[s];
+      std::vector<int> ids;
+      {
+        std::lock_guard<std::mutex> lk(ctx->route_mu);
+        ids = ctx->by_stage[s];
+      }
       double busy = 0;
       for (size_t j = 0; j < ids.size(); ++j) {
-        Inst& I = *ctx->inst[ids[j]];
-        uint64_t b = I.busy.sample(t);
+        const uint64_t b = busy_sample(ctx, ids[j], t);
         if (j < g[s]) busy += double(b - busy0[ids[j]]) * 1e-9;
         busy0[ids[j]] = b;
-        if (j < g[s] && s != DF_E) m.q[s] += uint32_t(I.inbox.size());
+        if (j < g[s] && s != DF_E)
+          m.q[s] += uint32_t(ctx->mp ? ctx->seg->inst[ids[j]].inbox.size_approx() : ctx->inst[ids[j]]->inbox.size());
       }
-      if (s == DF_E) m.q[s] = uint32_t(ctx->requests->size_approx());
+      if (s == DF_E) m.q[s] = uint32_t(ctx->mp ? ctx->seg->requests.size_approx() : ctx->requests->size_approx());
       m.u[s] = float(std::min(1.0, busy / (double(g[s]) * win)));
-      uint64_t n = ctx->qd_count[s].exchange(0);
-      uint64_t tot = ctx->qd_ns[s].exchange(0);
+      std::atomic<uint64_t>* qn = ctx->mp ? ctx->seg->qd_ns : ctx->qd_ns;
+      std::atomic<uint64_t>* qc = ctx->mp ? ctx->seg->qd_count : ctx->qd_count;
+      uint64_t n = qc[s].exchange(0);
+      uint64_t tot = qn[s].exchange(0);
       m.d[s] = n ? float(double(tot) * 1e-9 / double(n)) : 0.f;
     }
     df_sched_event ev{};
     ev.t = t;
     ev.m = m;
     // workload change -> predictive reconfiguration (Alg. 1 lines 6-10)
-    std::vector<uint32_t> keys;
-    {
-      std::lock_guard<std::mutex> lk(ctx->sched_mu);
-      keys.assign(ctx->hist.begin(), ctx->hist.end());
-    }
+    std::vector<uint32_t> keys = hist_keys(ctx);
     bool reconf = false;
     if (changed(keys.data(), uint32_t(keys.size()))) {
       uint32_t key = keys.back();
       double T[3];
       bool ok = true;
-      {
-        std::lock_guard<std::mutex> lk(ctx->sched_mu);
-        for (int s = 0; s < 3; ++s) {
-          auto it = ctx->stage_s[s].find(s == DF_T ? key : 0u);
-          if (it == ctx->stage_s[s].end()) ok = false;
-          else T[s] = std::max(1e-6, it->second);
-        }
+      for (int s = 0; s < 3; ++s) {
+        ok = ok && stage_time(ctx, s, s == DF_T ? key : 0u, T[s]);
+        if (ok) T[s] = std::max(1e-6, T[s]);
       }
       // any allocation over the instance hosts: df_set_ratio re-purposes instances between
-      // stages when a stage needs more than it has
+      // stages when a stage needs more than it has (single process); across processes the
+      // allocation stays within each stage's instances (activation / deactivation only)
       const uint32_t G = c.G ? std::min<uint32_t>(c.G, uint32_t(ctx->inst.size())) : uint32_t(ctx->inst.size());
+      uint32_t capn[3];
+      {
+        std::lock_guard<std::mutex> lk(ctx->route_mu);
+        for (int s = 0; s < 3; ++s) capn[s] = uint32_t(ctx->by_stage[s].size());
+      }
       uint32_t tgt[3];
-      if (ok && plan_ratio(G, T, g, c.move_budget, nullptr, tgt) && std::memcmp(tgt, g, sizeof(g)) != 0) {
+      if (ok && plan_ratio(G, T, g, c.move_budget, ctx->mp ? capn : nullptr, tgt) &&
+          std::memcmp(tgt, g, sizeof(g)) != 0) {
         df_set_ratio(ctx, tgt[0], tgt[1], tgt[2]);
         ev.action = 3;
         std::memcpy(ev.g, tgt, sizeof(tgt));
         reconf = true;
-        std::lock_guard<std::mutex> lk(ctx->sched_mu);
-        ctx->hist.clear();  // the new regime starts a fresh history
+        hist_clear(ctx);  // the new regime starts a fresh history
       }
     }
     if (!reconf) {  // reactive rule (lines 11-17); one action per tick
@@ -1933,7 +2066,12 @@ void sched_loop(df_ctx* ctx) {
       uint32_t ng[3] = {g[0], g[1], g[2]};
       const uint32_t hosts = uint32_t(ctx->inst.size());
       for (int s = 0; s < 3 && ev.action == 0; ++s) {
-        if (dlt[s] > 0 && ng[0] + ng[1] + ng[2] < hosts) {
+        size_t have;
+        {
+          std::lock_guard<std::mutex> lk(ctx->route_mu);
+          have = ctx->by_stage[s].size();
+        }
+        if (dlt[s] > 0 && ng[0] + ng[1] + ng[2] < hosts && (!ctx->mp || ng[s] < have)) {
           ng[s]++;
           ev.action = 1;
           ev.stage = s;
@@ -1981,7 +2119,6 @@ int32_t df_sched_changed(const uint32_t* keys, uint32_t n) { return keys && chan
 
 df_status df_sched_start(df_ctx* ctx, const df_sched_cfg* cfg) {
   if (!ctx || !cfg || !(cfg->delta_s > 0.f) || !(cfg->U_low < cfg->U_high)) return DF_ERR_INVALID;
-  if (ctx->mp) return fail(ctx, "df_sched_start: single-process contexts only", DF_ERR_INVALID);
   if (ctx->sched.joinable()) return fail(ctx, "df_sched_start: already running", DF_ERR_STATE);
   ctx->sched_cfg = *cfg;
   ctx->sched_stop = false;
@@ -2142,6 +2279,14 @@ df_status df_init(const df_graph* g, df_ctx** out) {
     ctx->inst.push_back(std::move(in));
   }
   for (int s = 0; s < 3; ++s) ctx->active[s] = int(ctx->by_stage[s].size());
+  if (mp) {
+    for (int s = 0; s < 3; ++s) {  // every rank proposes the same initial g_s; the first one sets it
+      int32_t z = 0;
+      ctx->seg->active[s].compare_exchange_strong(z, int32_t(ctx->by_stage[s].size()));
+    }
+    for (auto& ip : ctx->inst)
+      if (ip->local) ip->busy.mirror = &ctx->seg->stat[ip->id];
+  }
   for (auto& ip : ctx->inst) {
     Inst& I = *ip;
     if (!I.local) continue;
@@ -2230,12 +2375,9 @@ df_status df_finalize(df_ctx* ctx) {
 
 df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
   if (!ctx || !r) return DF_ERR_INVALID;
-  if (ctx->mp) {
-    bool has_e = false;
-    for (auto& ip : ctx->inst) has_e |= ip->local && ip->stage == DF_E;
-    if (!has_e) return fail(ctx, "df_submit: this rank hosts no encoder instance", DF_ERR_INVALID);
-  }
   if (ctx->failed) return fail(ctx, ctx->err, DF_ERR_STATE);
+  if (ctx->mp && ctx->g.dit.L_txt > uint32_t(PL_MAX_TXT))
+    return fail(ctx, "df_submit: multi-process requests carry at most 512 text tokens", DF_ERR_INVALID);
   if (r->steps == 0 || r->steps > ctx->g.max_steps || !(r->shift > 0.f))
     return fail(ctx, "df_submit: steps in [1, max_steps] and shift > 0", DF_ERR_INVALID);
   if (r->out_host && r->out_bytes < ctx->out_bytes) return fail(ctx, "df_submit: out_bytes too small", DF_ERR_INVALID);
@@ -2244,6 +2386,29 @@ df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
   {
     std::lock_guard<std::mutex> lk(ctx->seen_mu);
     if (!ctx->seen.insert({id.lo, id.hi}).second) return fail(ctx, "df_submit: duplicate id", DF_ERR_DUPLICATE);
+  }
+  if (ctx->mp) {  // the global request ring in the shared plane: any rank submits, every E pulls
+    ReqRec q{};
+    q.id_lo = id.lo, q.id_hi = id.hi;
+    q.seed = r->seed;
+    q.user_tag = r->user_tag;
+    q.steps = r->steps;
+    q.shift = r->shift;
+    q.guidance = r->guidance;
+    q.flags = (r->out_host ? 1u : 0u) | (r->token_ids ? 2u : 0u) | (r->neg_token_ids ? 4u : 0u);
+    const size_t L = ctx->g.dit.L_txt;
+    if (r->token_ids) std::memcpy(q.tokens[0], r->token_ids, L * 4);
+    if (r->neg_token_ids) std::memcpy(q.tokens[1], r->neg_token_ids, L * 4);
+    q.t_submit = now_s();
+    hist_push(ctx, r->steps);
+    q.seq = ctx->seg->seq.fetch_add(1);  // FAA ticket
+    if (!ctx->seg->requests.push(q)) {
+      std::lock_guard<std::mutex> lk(ctx->seen_mu);
+      ctx->seen.erase({id.lo, id.hi});
+      return DF_AGAIN;
+    }
+    if (id_out) *id_out = id;
+    return DF_OK;
   }
   if (ctx->requests->size_approx() >= ctx->requests->capacity()) {
     std::lock_guard<std::mutex> lk(ctx->seen_mu);
@@ -2261,11 +2426,7 @@ df_status df_submit(df_ctx* ctx, const df_request* r, df_req_id* id_out) {
     std::lock_guard<std::mutex> lk(ctx->req_mu);
     rs->seq = ctx->mp ? ctx->seg->seq.fetch_add(1) : ctx->seq.fetch_add(1);  // FAA ticket
   }
-  {
-    std::lock_guard<std::mutex> lk(ctx->sched_mu);
-    ctx->hist.push_back(r->steps);
-    while (ctx->hist.size() > 64) ctx->hist.pop_front();
-  }
+  hist_push(ctx, r->steps);
   if (!ctx->requests->push(rs)) {
     free_req(rs);
     std::lock_guard<std::mutex> lk(ctx->seen_mu);
@@ -2349,7 +2510,7 @@ df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD) {
   }
   // New requests go to the first g_s instances of each stage; instances beyond them drain
   // their inboxes (already-assigned work completes; nothing is dropped).
-  for (int s = 0; s < 3; ++s) ctx->active[s] = int(g[s]);
+  for (int s = 0; s < 3; ++s) active_of(ctx, s) = int(g[s]);
   return DF_OK;
 }
 

@@ -437,12 +437,17 @@ static cudaError_t launch_rms_warp(const float* x, void* out, int out_f32, int M
                                    const float* scale, const bf16* gain, float eps, cudaStream_t st) {
   void* args[] = {(void*)&x, (void*)&out, (void*)&M, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
   dim3 grid((M + 3) / 4);
-  static const int impl = [] {  // DF_RMS_IMPL (A/B): 0 streaming (default), 1 warp per row, 2 bulk per CTA
+  // DF_RMS_IMPL (A/B): 0 auto (default), 1 warp per row, 2 bulk per CTA, 3 streaming.  Auto
+  // streams when every SM has >= 64 rows to stream (video: 161 vs 217 us standalone at
+  // 32760 x 5120); at the image shape (28 rows per SM) the one-wave warp-per-row kernel reads
+  // the residual the previous GEMM epilogue just left in L2 and is as fast in the step
+  // (DESIGN.md §12).
+  static const int impl = [] {
     const char* e = getenv("DF_RMS_IMPL");
     return e ? atoi(e) : 0;
   }();
   const int bulk = impl == 2;
-  if (impl == 0 && VPT >= 16) {
+  if ((impl == 3 || (impl == 0 && M >= 64 * num_sms())) && VPT >= 16) {
     using Cfg = RmsStream<VPT>;
     const void* kern =
         out_f32 ? (const void*)rmsnorm_stream_kernel<VPT, float> : (const void*)rmsnorm_stream_kernel<VPT, bf16>;

@@ -85,6 +85,10 @@ struct ShmRing {
       }
     }
   }
+  uint64_t size_approx() const {
+    const uint64_t t = tail.load(std::memory_order_relaxed), h = head.load(std::memory_order_relaxed);
+    return t > h ? t - h : 0;
+  }
   bool pop(T& out) {
     uint64_t pos = head.load(std::memory_order_relaxed);
     for (;;) {
@@ -129,12 +133,48 @@ struct InstPlane {
   ShmRing<MetaRec, PL_RING> inbox;       // control plane into this consumer
 };
 
+// An admitted request in the global request ring (any rank submits, the encoder instances
+// of every rank pull; "the request scheduler inserts the request into the global
+// request buffer").  Caller token ids travel inside the record.
+constexpr int PL_MAX_TXT = 512;
+struct ReqRec {
+  uint64_t seq, id_lo, id_hi, seed, user_tag;
+  uint32_t steps, flags;  // bit0: deliver the decoded output (to the D rank); bit1: tokens; bit2: negative tokens
+  float shift, guidance;
+  double t_submit;
+  int32_t tokens[2][PL_MAX_TXT];
+};
+
+// Controller-visible state of one instance, written by the rank that hosts it (Alg. 1's u_s).
+struct InstStat {
+  std::atomic<uint64_t> busy_ns;     // closed busy intervals
+  std::atomic<uint64_t> busy_since;  // bit pattern of the open interval's start (double seconds), 0 = idle
+};
+
+// Measured seconds per request per instance for the Eq. 6 planner, per stage and workload key
+// (EMA), shared so that the controller sees the stage times of every rank.
+struct StageEma {
+  std::atomic<uint32_t> lock;
+  uint32_t n;
+  uint32_t key[8];
+  double sec[8];
+};
+
 struct PlaneSeg {
   std::atomic<uint64_t> magic;
   std::atomic<uint64_t> seq;             // global request sequence (FAA)
   std::atomic<uint32_t> attached;
   uint32_t world;
   InstPlane inst[PL_MAX_INST];
+  // hybrid scheduler state shared by all ranks (one controller, any rank)
+  std::atomic<int32_t> active[3];        // g_s: the first active[s] instances of stage s get new work
+  std::atomic<uint64_t> qd_ns[3], qd_count[3];
+  InstStat stat[PL_MAX_INST];
+  StageEma ema[3];
+  std::atomic<uint32_t> hist_lock;
+  uint32_t hist_n, hist_head;
+  uint32_t hist[64];                     // workload keys (steps) of the last admitted requests
+  ShmRing<ReqRec, PL_RING> requests;
 };
 
 // Create (rank 0) or attach to the named segment; returns nullptr on failure.

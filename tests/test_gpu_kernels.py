@@ -121,9 +121,11 @@ def test_attention_special_cases(tiny_ctx):
     assert rel_l2(O.double().cpu().numpy(), want.cpu().numpy()) < 4e-3
 
 
-@pytest.mark.parametrize("d", [200, 3072, 4096, 5120])
-def test_rmsnorm_mod_closed_form(tiny_ctx, d):
-    M = 333  # not a multiple of the 4 rows per CTA
+@pytest.mark.parametrize("d,M", [(200, 333), (3072, 333), (4096, 333), (5120, 333), (3072, 64 * 148 + 7),
+                                 (5120, 64 * 148 + 333)])
+def test_rmsnorm_mod_closed_form(tiny_ctx, d, M):
+    """333 rows: not a multiple of the 4 rows per CTA (one-row-per-warp kernel); >= 64 rows per
+    SM: the persistent streaming kernel, with rows not a multiple of the grid."""
     x = torch.randn(M, d, device="cuda") * 3
     sh = torch.randn(d, device="cuda") * 0.1
     sc = torch.randn(d, device="cuda") * 0.1

@@ -168,3 +168,89 @@ def test_two_process_handoff_is_asynchronous(mode):
             assert gap >= 0.8 * d, (t_inst, gap)
         else:
             assert gap < 0.25 * d, (t_inst, gap)
+
+
+def _sched_worker(rank, world, port, shm, q):
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2605_25550_b200 import binding as B
+    from synth.configs import TINY
+    # rank 0: E0, T1; rank 1: T2, D3, and a second encoder E4 (inactive until scaled out)
+    inst = [(0, B.DF_E, 0), (0, B.DF_T, 0), (0, B.DF_T, 1), (0, B.DF_D, 1), (0, B.DF_E, 1)]
+    g = B.make_graph(TINY, inst, rank=rank, world=world, shm_name=shm, chunk_bytes=(64, 256))
+    c = B.Context(g)
+    dist.barrier()
+    res = {}
+
+    def drain(n):
+        got = []
+        while len(got) < n:
+            got += [(int(x.user_tag), int(x.inst[0]), x.hash_src[0] == x.hash_dst[0] != 0)
+                    for x in c.poll(16, timeout_ms=60000)]
+        return got
+
+    if rank == 0:
+        assert c.set_ratio(1, 2, 1) == B.DF_OK                     # E4 (rank 1) stops pulling
+        # measure only (thresholds no tick can cross): the allocation is steered explicitly below
+        c.sched_start(B.sched_cfg(delta_s=0.05, U_high=1.5, U_low=-0.5, move_budget=0))
+    dist.barrier()
+    # phase A: one encoder; phase B: the controller rank scales E out to rank 1's encoder
+    for phase, seeds in (("A", list(range(100, 140))), ("B", list(range(200, 240)))):
+        if rank == 0:
+            if phase == "B":
+                assert c.set_ratio(2, 2, 1) == B.DF_OK
+            for s in seeds:
+                while c.submit(TINY.steps, TINY.shift, s, user_tag=s)[0] != B.DF_OK:
+                    time.sleep(0.001)
+        if rank == 1:
+            res[phase] = drain(len(seeds))
+        dist.barrier()
+    if rank == 0:
+        time.sleep(0.2)
+        c.sched_stop()
+        log = c.sched_log()
+        res["log"] = [(e.action, tuple(e.g), tuple(e.m.u), tuple(e.m.q)) for e in log]
+    objs = [None, None]
+    dist.all_gather_object(objs, res)
+    if rank == 0:
+        q.put({**objs[0], **objs[1]})
+    dist.barrier()
+    c.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_controller_and_encoder_scale_out():
+    """NEXT-1 across processes (P:L326-357 on the one-process-per-GPU path): the request ring,
+    the allocation g_s and every instance's busy time live in the shared plane.  Rank 0's
+    df_set_ratio activates an encoder hosted by rank 1 (E scale-out): afterwards
+    requests submitted on rank 0 are encoded on both ranks.  The Alg. 1 controller runs on rank
+    0 and measures utilisation and queues of all instances, rank 1's included; no request is
+    lost and every handoff hash matches."""
+    import torch.multiprocessing as mp
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    shm = f"/df_gpu_{uuid.uuid4().hex[:10]}"
+    port = _port()
+    procs = [ctxm.Process(target=_sched_worker, args=(r, 2, port, shm, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    a, b = res["A"], res["B"]
+    assert sorted(x[0] for x in a) == list(range(100, 140)) and sorted(x[0] for x in b) == list(range(200, 240))
+    assert all(x[2] for x in a + b)
+    assert {x[1] for x in a} == {0}                               # one encoder
+    assert {x[1] for x in b} == {0, 4}                            # scaled out to rank 1's encoder
+    log = res["log"]
+    assert len(log) >= 3
+    for action, g, u, qq in log:
+        assert min(g) >= 1 and g[0] <= 2 and g[1] <= 2 and g[2] == 1
+        assert all(0.0 <= x <= 1.0 for x in u)
+    assert any(u[2] > 0 for _, _, u, _ in log)                    # the D on rank 1 is seen as busy
