@@ -44,7 +44,11 @@ typedef enum {
 } df_status;
 
 typedef enum { DF_E = 0, DF_T = 1, DF_D = 2 } df_stage;
-enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1 };               /* df_graph.precision */
+/* df_graph.precision.  DF_FP8 (NEXT-4, R29): bf16 everywhere except the three GEMMs
+ * fed by a normalised activation (QKV, cross-Q, MLP up), which take e4m3 operands -- the
+ * activation quantised per token row by the RMSNorm that produces it, the weight per tensor --
+ * with fp32 accumulation; needs d >= 256 and N >= 256 latent tokens (CTA-pair tiles). */
+enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1, DF_FP8 = 2 };
 enum { DF_ASYNC = 0, DF_SYNC = 1, DF_PERMUTE = 2, DF_HASH = 4, DF_LATENT_BLOCKS = 8 }; /* handoff flags */
 #define DF_ALL_CHUNKS 0xFFFFFFFFu
 #define DF_MAX_INST 32
@@ -79,7 +83,7 @@ typedef struct {
   uint32_t n_slots;             /* receive slots per consumer per edge, >= 2             */
   uint32_t handoff_mode;        /* DF_ASYNC (default) | DF_SYNC (P:L151 comparison)      */
   uint32_t ring_capacity;       /* request ring, power of two                   */
-  uint32_t precision;           /* DF_BF16 | DF_FP32_VALIDATION                          */
+  uint32_t precision;           /* DF_BF16 | DF_FP32_VALIDATION | DF_FP8                 */
   uint32_t max_steps;           /* largest S a request may ask for                       */
   uint64_t weight_seed;
   float jitter_p;               /* each transfer delayed by jitter_delay_s w.p. p */

@@ -862,6 +862,75 @@ __global__ void __launch_bounds__(256) e4m3_quant_kernel(const bf16* __restrict_
   for (size_t i = n8 * 8 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
     q[i] = uint8_t(__nv_cvt_float_to_fp8(__fdiv_rn(bf2f(x[i]), s), __NV_SATFINITE, __NV_E4M3));
 }
+// RMSNorm + modulation (or gain) quantised per row to e4m3 (FP8 step, R29): one warp per row,
+// three passes over the row (the row stays in L1/L2): sum of squares; y and its amax; q.
+template <int VPT>
+__global__ void __launch_bounds__(128) rmsnorm_e4m3_kernel(const float* __restrict__ x, uint8_t* __restrict__ q,
+                                                          float* __restrict__ srow, int M,
+                                                          const float* __restrict__ shift,
+                                                          const float* __restrict__ scale,
+                                                          const bf16* __restrict__ gain, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  constexpr int d = 128 * VPT;
+  const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
+  float ss = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < VPT; ++i) {
+    const float4 t = xr[lane + 32 * i];
+    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+  }
+  ss = warp_sum(ss);
+  const float inv = rsqrtf(ss / float(d) + eps);
+  auto modulate = [&](int c, float* y) {
+    const float4 t = xr[c];
+    y[0] = t.x * inv, y[1] = t.y * inv, y[2] = t.z * inv, y[3] = t.w * inv;
+    if (gain) {
+      const uint2 g = reinterpret_cast<const uint2*>(gain)[c];
+      y[0] *= bf_lo(g.x), y[1] *= bf_hi(g.x), y[2] *= bf_lo(g.y), y[3] *= bf_hi(g.y);
+    } else {
+      const float4 sc = reinterpret_cast<const float4*>(scale)[c];
+      const float4 sh = reinterpret_cast<const float4*>(shift)[c];
+      y[0] = y[0] * (1.f + sc.x) + sh.x;
+      y[1] = y[1] * (1.f + sc.y) + sh.y;
+      y[2] = y[2] * (1.f + sc.z) + sh.z;
+      y[3] = y[3] * (1.f + sc.w) + sh.w;
+    }
+  };
+  float am = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < VPT; ++i) {
+    float y[4];
+    modulate(lane + 32 * i, y);
+    am = fmaxf(am, fmaxf(fmaxf(fabsf(y[0]), fabsf(y[1])), fmaxf(fabsf(y[2]), fabsf(y[3]))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  const float sr = am > 0.f ? __fdiv_rn(am, 448.f) : 1.f;
+  uint32_t* qr = reinterpret_cast<uint32_t*>(q + size_t(row) * d);
+#pragma unroll 8
+  for (int i = 0; i < VPT; ++i) {
+    float y[4];
+    modulate(lane + 32 * i, y);
+    qr[lane + 32 * i] = e4m3x4(y[0], y[1], y[2], y[3], sr);
+  }
+  if (lane == 0) srow[row] = sr;
+}
+
+cudaError_t rmsnorm_e4m3(const float* x, uint8_t* q, float* s, int M, int d, const float* shift, const float* scale,
+                         const bf16* gain, float eps, cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  dim3 grid((M + 3) / 4);
+  switch (d) {
+    case 256: rmsnorm_e4m3_kernel<2><<<grid, 128, 0, st>>>(x, q, s, M, shift, scale, gain, eps); break;
+    case 3072: rmsnorm_e4m3_kernel<24><<<grid, 128, 0, st>>>(x, q, s, M, shift, scale, gain, eps); break;
+    case 5120: rmsnorm_e4m3_kernel<40><<<grid, 128, 0, st>>>(x, q, s, M, shift, scale, gain, eps); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaStream_t st) {
   cudaError_t e0 = cudaMemsetAsync(scale, 0, sizeof(float), st);
   if (e0 != cudaSuccess) return e0;

@@ -56,8 +56,11 @@ struct Epi {
   unsigned sk_epoch;
   int sk_force;  // host: take stream-K whenever the tile count allows it (tests)
   // FP8 (e4m3) operands (NEXT-4): device pointers to the per-tensor dequantisation scales of
-  // A and B; the accumulator is multiplied by *f8_scale[0] * *f8_scale[1] before the epilogue
+  // A and B; the accumulator is multiplied by *f8_scale[0] * *f8_scale[1] before the epilogue.
+  // f8_row (optional): per-row scales of A [M] replace *f8_scale[0] (R29: activations
+  // quantised per token row by the producing RMSNorm)
   const float* f8_scale[2];
+  const float* f8_row;
 };
 
 DF_DEV float bias_at(const Epi& e, int n) { return e.bias ? bf2f(e.bias[n]) : 0.0f; }

@@ -576,7 +576,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < n; ++i) vv[i] += __ldcg(wfix + (col + i) * 128);
       };
-      const float f8a = F8 ? __ldg(epi.f8_scale[0]) * __ldg(epi.f8_scale[1]) : 1.f;  // dequantisation
+      // dequantisation: per-tensor A and B scales, or this thread's row scale of A (R29)
+      const int frow = min(mb * 256 + int(rank) * 128 + ew * 32 + lane, M - 1);
+      const float f8a = F8 ? (epi.f8_row ? __ldg(epi.f8_row + frow) : __ldg(epi.f8_scale[0])) * __ldg(epi.f8_scale[1])
+                           : 1.f;
       auto f8_scale_acc = [&](float* vv, int n) {
 #pragma unroll
         for (int i = 0; i < n; ++i) vv[i] *= f8a;
@@ -713,6 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             tmem_ld32(trow + g + 32 * q, a);
             tc_wait_ld();
             if (fix) fixup(a, g + 32 * q, 32);
+            if (F8) f8_scale_acc(a, 32);
             float w[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -766,6 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
               tmem_ld32(trow + c + q, a);
               tc_wait_ld();
               if (fix) fixup(a, c + q, 32);
+              if (F8) f8_scale_acc(a, 32);
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 const float z = a[i] + s_bias[c + q + i];
@@ -782,6 +787,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             tmem_ld32(trow + c + 64 * hf + 32, w + 32);
             tc_wait_ld();
             if (fix) fixup(w, c + 64 * hf, 64);
+            if (F8) f8_scale_acc(w, 64);
             const float* pb = s_bias + c + 64 * hf;
             const float* pg = s_aux + c + 64 * hf;
 #pragma unroll
@@ -905,6 +911,7 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
 bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
                const uint64_t* strides_bytes, const uint32_t* box);
 
+template <bool F8 = false>
 static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
                                 int out_f32, cudaStream_t st) {
   static const int tma_epi = [] {  // DF_GEMM_TMA_EPI=0: per-thread epilogue stores (A/B)
@@ -918,19 +925,19 @@ static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, in
     if (epi.kind == EPI_STORE && out_f32 && (epi.ldo % 4) == 0) {
       const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 4};
       if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box_f32))
-        return launch_tc2<32, float, TK_STORE_F32>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, float, TK_STORE_F32, F8>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_STORE && !out_f32 && (epi.ldo % 8) == 0) {
       const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 2};
       if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box_bf16))
-        return launch_tc2<32, bf16, TK_STORE_BF16>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, bf16, TK_STORE_BF16, F8>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_GRES && (epi.ldr % 4) == 0) {
       const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldr) * 4};
       if (make_tmap(&to[0], epi.resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box_f32))
-        return launch_tc2<32, float, TK_GRES>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, float, TK_GRES, F8>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_SWIGLU && !out_f32 && (epi.ldo % 8) == 0) {
       const uint64_t dims[2] = {uint64_t(N / 2), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 2};
       if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box_bf16))
-        return launch_tc2<32, bf16, TK_SWIGLU>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, bf16, TK_SWIGLU, F8>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_HEADS && !out_f32 && epi.dh == 128 && epi.dh_pad == 128) {
       const int mper = epi.Mper > 0 ? epi.Mper : M;
       const uint64_t dims[3] = {128, uint64_t(mper), uint64_t(M / mper) * epi.heads};
@@ -939,20 +946,45 @@ static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, in
       bool ok = true;
       for (int s = 0; s < epi.nsec; ++s)
         ok = ok && make_tmap(&to[s], epi.sec_out[s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, dims, str, box);
-      if (ok) return launch_tc2<128, bf16, TK_HEADS>(ta, tb, to, M, N, K, epi, st);
+      if (ok) return launch_tc2<128, bf16, TK_HEADS, F8>(ta, tb, to, M, N, K, epi, st);
     }
   }
-  if (epi.kind == EPI_HEADS) {
-    if (out_f32) return cudaErrorInvalidValue;
-    switch (epi.dh) {
-      case 16: return launch_tc2<16, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
-      case 64: return launch_tc2<64, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
-      case 128: return launch_tc2<128, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
-      default: return cudaErrorInvalidValue;
+  if constexpr (F8) {
+    return cudaErrorInvalidValue;  // the FP8 step uses the TMA-store epilogues only
+  } else {
+    if (epi.kind == EPI_HEADS) {
+      if (out_f32) return cudaErrorInvalidValue;
+      switch (epi.dh) {
+        case 16: return launch_tc2<16, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+        case 64: return launch_tc2<64, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+        case 128: return launch_tc2<128, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+        default: return cudaErrorInvalidValue;
+      }
     }
+    return out_f32 ? launch_tc2<32, float, TK_DIRECT>(ta, tb, to, M, N, K, epi, st)
+                   : launch_tc2<32, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
   }
-  return out_f32 ? launch_tc2<32, float, TK_DIRECT>(ta, tb, to, M, N, K, epi, st)
-                 : launch_tc2<32, bf16, TK_DIRECT>(ta, tb, to, M, N, K, epi, st);
+}
+
+// The FP8 step's GEMMs (R29): e4m3 A [M, K] (per-row scales a_row) and e4m3 W [N, K]
+// (per-tensor scale w_scale), any TMA-store epilogue of the bf16 path (heads, SwiGLU, stores,
+// gated residual) applied to the dequantised fp32 accumulator.  M, N >= 256, K % 16 == 0.
+cudaError_t gemm_e4m3_epi(const uint8_t* qa, const float* a_row, const uint8_t* qw, const float* w_scale, int M, int N,
+                          int K, const Epi& e, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if (K % 16 || M < 256 || N < 256 || !a_row || !w_scale) return cudaErrorInvalidValue;
+  CUtensorMap ta, tb;
+  const uint32_t box_q[2] = {128, 128};
+  const uint64_t da[2] = {uint64_t(K), uint64_t(M)}, db[2] = {uint64_t(K), uint64_t(N)}, sq[1] = {uint64_t(K)};
+  if (!make_tmap(&ta, qa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, da, sq, box_q)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tb, qw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, db, sq, box_q)) return cudaErrorInvalidValue;
+  Epi epi = e;
+  epi.f8_row = a_row;
+  epi.f8_scale[0] = a_row;
+  epi.f8_scale[1] = w_scale;
+  epi.sk_ws = nullptr;  // no stream-K on the FP8 path
+  epi.sk_flag = nullptr;
+  return dispatch_tc2<true>(ta, tb, M, N, K, epi, 0, st);
 }
 
 // e4m3 x e4m3 GEMM (NEXT-4): out[M, N] = sa * sb * (qa[M, K] . qb[N, K]^T), fp32

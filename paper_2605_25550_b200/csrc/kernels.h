@@ -17,6 +17,14 @@ extern int g_disable_pair;  // 1: never use the CTA-pair GEMM (tests)
 // BN in {64, 128, 256}.  Returns cudaError_t of the launch.
 // e4m3 (NEXT-4): per-tensor quantiser (3 launches) and the CTA-pair e4m3 GEMM
 cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaStream_t st);
+// FP8 step (R29): e4m3 A with per-row scales x e4m3 W with a per-tensor scale, through the
+// bf16 path's TMA-store epilogues (heads / SwiGLU / stores / gated residual)
+cudaError_t gemm_e4m3_epi(const uint8_t* qa, const float* a_row, const uint8_t* qw, const float* w_scale, int M, int N,
+                          int K, const Epi& e, cudaStream_t st);
+// RMSNorm (+ modulation or gain) with e4m3 output quantised per row (R29): q[m, :] =
+// e4m3(y[m, :] / s[m]), s[m] = amax|y[m, :]| / 448 (1 for a zero row), y in fp32.
+cudaError_t rmsnorm_e4m3(const float* x, uint8_t* q, float* s, int M, int d, const float* shift, const float* scale,
+                         const bf16* gain, float eps, cudaStream_t st);
 cudaError_t gemm_e4m3(const uint8_t* qa, const uint8_t* qb, const float* sa, const float* sb, int M, int N, int K,
                       void* out, int ldo, int out_f32, cudaStream_t st);
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& epi,

@@ -123,6 +123,8 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
   Pin = (c.C + c.C_y) * c.pt * c.ph * c.pw;
   dh = c.d / c.heads;
   dhp = f32() ? dh : (dh <= 64 ? 64 : 128);
+  if (fp8() && stage == DF_T && (c.d < 256 || N < 256 || dh != 128 || c.d % 16))
+    return cudaErrorInvalidValue;  // the FP8 GEMMs run on CTA-pair tiles with the head-major TMA epilogue
   if (c.d % c.heads || dh > 128 || c.ffn % 16 || c.d % 4 || c.enc_ffn % 16 ||
       c.rope_axes[0] + c.rope_axes[1] + c.rope_axes[2] != uint32_t(dh) ||
       (c.C_y > 0 && (c.L_img == 0 || c.d_img == 0 || c.d_img % 8)))
@@ -187,6 +189,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           (i2v() ? al(N2 * d * ab) : 0) +
           al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
+    if (fp8()) wsb += al(N2 * d) + al(N2 * 4);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
     else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // GEMM stream-K
   } else if (stage == DF_E) {
@@ -204,6 +207,10 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     X = ws.take(Nn * Pin * ab);
     if (i2v()) oi = ws.take(N2 * d * ab);
     vbatch = (float*)ws.take(2 * size_t(c.C) * c.F * c.H * c.W * 4);
+    if (fp8()) {
+      hq = (uint8_t*)ws.take(N2 * d);
+      hs = (float*)ws.take(N2 * 4);
+    }
     mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
     headmod = (float*)ws.take(2 * d * 4);
     rope = (float2*)ws.take(size_t(Fp + Hp + Wp) * dh / 2 * 8 + 64);
@@ -234,7 +241,27 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     etmp = (float*)ws.take(L * 2 * fe * 4);
   }
   DF_TRY(init_weights(0));
+  if (fp8() && stage == DF_T) DF_TRY(quantize_weights(0));
   DF_TRY(cudaDeviceSynchronize());
+  return cudaSuccess;
+}
+
+// FP8 step (R29): per-tensor e4m3 copies of W_qkv, W_cq and W_1 | W_3 (R28's quantiser on the
+// bf16 weights, so the codes are those of the oracle's quantize_per_tensor).
+cudaError_t Model::quantize_weights(cudaStream_t st) {
+  const size_t d = c.d, f = c.ffn;
+  const size_t per = al(3 * d * d) + al(d * d) + al(2 * f * d) + al(3 * 4);
+  DF_TRY(f8mem.reserve(per * c.layers + 4096));
+  for (auto& l : Lw) {
+    l.qkv_q = (uint8_t*)f8mem.take(3 * d * d);
+    l.cq_q = (uint8_t*)f8mem.take(d * d);
+    l.w13_q = (uint8_t*)f8mem.take(2 * f * d);
+    l.f8s = (float*)f8mem.take(3 * 4);
+    if (!l.f8s) return cudaErrorMemoryAllocation;
+    DF_L(quant_e4m3(l.qkv_wT, 3 * d * d, l.qkv_q, l.f8s + 0, st));
+    DF_L(quant_e4m3(l.cq_wT, d * d, l.cq_q, l.f8s + 1, st));
+    DF_L(quant_e4m3(l.w13T, 2 * f * d, l.w13_q, l.f8s + 2, st));
+  }
   return cudaSuccess;
 }
 
@@ -242,6 +269,7 @@ void Model::destroy() {
   cudaSetDevice(device);
   wmem.release();
   ws.release();
+  f8mem.release();
 }
 
 cudaError_t Model::init_weights(cudaStream_t st) {
@@ -404,6 +432,20 @@ Epi Model::heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0
   e.Df2 = c.rope_axes[0] / 2; e.Dh2 = c.rope_axes[1] / 2; e.Dw2 = c.rope_axes[2] / 2;
   e.eps = c.eps;
   return e;
+}
+
+cudaError_t Model::norm_f8(const float* x, int M, const float* shift, const float* scale, const bf16* gain,
+                           cudaStream_t st) {
+  ProfScope ps(prof, st, K_NORM, 0.0, double(M) * c.d * (4.0 + 1.0));
+  DF_L(rmsnorm_e4m3(x, hq, hs, M, int(c.d), shift, scale, gain, c.eps, st));
+  return cudaSuccess;
+}
+
+cudaError_t Model::gemm_f8(const uint8_t* Wq, const float* wscale, int M, int Nn, int K, const Epi& e,
+                           cudaStream_t st) {
+  ProfScope ps(prof, st, cur_kind, 2.0 * M * Nn * K, 0.0);
+  DF_L(gemm_e4m3_epi(hq, hs, Wq, wscale, M, Nn, K, e, st));
+  return cudaSuccess;
 }
 
 cudaError_t Model::norm(const float* x, void* out, int M, int dd, const float* shift, const float* scale,
@@ -576,13 +618,15 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
   const LayerW& w = Lw[l];
   const float* md = mods + size_t(l) * 6 * d;  // sh1, sc1, g1, sh2, sc2, g2
   const size_t per = size_t(B) * c.heads * Lt * dhp * act_bytes();
-  // a4: h = RMSNorm(r)(1 + sc1) + sh1
-  DF_TRY(norm(res, h, M, d, md + 0 * d, md + 1 * d, nullptr, st));
+  // a4: h = RMSNorm(r)(1 + sc1) + sh1  (FP8 step: straight to e4m3 with row scales, R29)
+  if (fp8()) DF_TRY(norm_f8(res, M, md + 0 * d, md + 1 * d, nullptr, st));
+  else DF_TRY(norm(res, h, M, d, md + 0 * d, md + 1 * d, nullptr, st));
   // a5: q,k,v = heads(h Wqkv + b); qk-RMSNorm * g; RoPE3 on q, k
   {
     Epi e = heads_epi(M, 3, w.qkv_b, q, w.g_q, 1, k, w.g_k, 1, v, nullptr, 0, N);
     cur_kind = K_QKV;
-    DF_TRY(gemm(h, d, w.qkv_wT, d, M, 3 * d, d, e, of, st));
+    if (fp8()) DF_TRY(gemm_f8(w.qkv_q, w.f8s + 0, M, 3 * d, d, e, st));
+    else DF_TRY(gemm(h, d, w.qkv_wT, d, M, 3 * d, d, e, of, st));
   }
   // a6: self-attention (per sample)
   cur_kind = K_ATTN_SELF;
@@ -598,11 +642,13 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     DF_TRY(gemm(o, d, w.o_wT, d, M, d, d, e, of, st));
   }
   // a8: cross-attention: hc = RMSNorm(r) g_n3; qc = headRMS(hc Wcq + b) g_cq; r += attn Wco + b
-  DF_TRY(norm(res, h, M, d, nullptr, nullptr, w.g_n3, st));
+  if (fp8()) DF_TRY(norm_f8(res, M, nullptr, nullptr, w.g_n3, st));
+  else DF_TRY(norm(res, h, M, d, nullptr, nullptr, w.g_n3, st));
   {
     Epi e = heads_epi(M, 1, w.cq_b, qc, w.g_cq, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, N);
     cur_kind = K_CQ;
-    DF_TRY(gemm(h, d, w.cq_wT, d, M, d, d, e, of, st));
+    if (fp8()) DF_TRY(gemm_f8(w.cq_q, w.f8s + 1, M, d, d, e, st));
+    else DF_TRY(gemm(h, d, w.cq_wT, d, M, d, d, e, of, st));
   }
   cur_kind = K_ATTN_CROSS;
   DF_TRY(attn(qc, (const char*)cd.kc + l * per, (const char*)cd.vc + l * per, o, N, Lt, st, B));
@@ -620,7 +666,8 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     DF_TRY(gemm(o, d, w.co_wT, d, M, d, d, e, of, st));
   }
   // a9: h2 = RMSNorm(r)(1 + sc2) + sh2
-  DF_TRY(norm(res, h, M, d, md + 3 * d, md + 4 * d, nullptr, st));
+  if (fp8()) DF_TRY(norm_f8(res, M, md + 3 * d, md + 4 * d, nullptr, st));
+  else DF_TRY(norm(res, h, M, d, md + 3 * d, md + 4 * d, nullptr, st));
   // a10: a = SiLU(h2 W1 + b1) * (h2 W3 + b3);  r += g2 * (a W2 + b2)
   {
     Epi e = epi_base(EPI_SWIGLU, M, 2 * f);
@@ -628,7 +675,8 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     cur_kind = K_UP;
     e.out = a;
     e.ldo = f;
-    DF_TRY(gemm(h, d, w.w13T, d, M, 2 * f, d, e, of, st));
+    if (fp8()) DF_TRY(gemm_f8(w.w13_q, w.f8s + 2, M, 2 * f, d, e, st));
+    else DF_TRY(gemm(h, d, w.w13T, d, M, 2 * f, d, e, of, st));
   }
   {
     Epi e = epi_base(EPI_GRES, M, d);

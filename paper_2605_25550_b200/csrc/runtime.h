@@ -42,6 +42,10 @@ struct LayerW {
   bf16 *mod, *qkv_wT, *qkv_b, *g_q, *g_k, *o_wT, *o_b, *g_n3, *cq_wT, *cq_b, *ckv_wT, *ckv_b, *g_cq, *g_ck, *co_wT,
       *co_b, *w13T, *b13, *w2T, *b2;
   bf16 *ckvi_wT = nullptr, *ckvi_b = nullptr, *g_ki = nullptr;  // I2V image-token K | V, K gain
+  // FP8 step (R29): e4m3 copies of the three weights fed by a normalised activation, each with
+  // its per-tensor scale (device fp32): QKV, cross-Q, MLP up (interleaved W1 | W3)
+  uint8_t *qkv_q = nullptr, *cq_q = nullptr, *w13_q = nullptr;
+  float* f8s = nullptr;  // [3]: qkv, cq, w13
 };
 
 // Where a logical tensor lives on the device (for df_weight_bits).
@@ -142,7 +146,7 @@ struct Model {
   // derived
   int N = 0, P = 0, dh = 0, dhp = 0, Fp = 0, Hp = 0, Wp = 0;
   int Pin = 0;              // patch-embedding input width ((C + C_y) pt ph pw)
-  Arena wmem, ws;
+  Arena wmem, ws, f8mem;
   std::vector<TensorLoc> locs;
   // global DiT weights
   bf16 *patch_wT = nullptr, *patch_b = nullptr, *txt1_wT = nullptr, *txt1_b = nullptr, *txt2_wT = nullptr,
@@ -171,6 +175,8 @@ struct Model {
   float* headmod = nullptr; // [2][d]
   float2* rope = nullptr;
   float* vbatch = nullptr;  // [2][C,F,H,W] velocities of a CFG batch
+  uint8_t* hq = nullptr;    // FP8 step: e4m3 normalised activation [2N, d] and its row scales [2N]
+  float* hs = nullptr;
   // encoder workspace
   float* ez = nullptr;      // [L, d_txt]
   void* ea = nullptr;       // [L, d_txt]
@@ -185,6 +191,7 @@ struct Model {
   cudaError_t create(const df_dit_cfg& cfg, int precision, int device, int stage, uint64_t seed, int max_steps);
   void destroy();
   bool f32() const { return precision == DF_FP32_VALIDATION; }
+  bool fp8() const { return precision == DF_FP8; }
   size_t act_bytes() const { return f32() ? 4 : 2; }
 
   cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
@@ -206,6 +213,10 @@ struct Model {
   cudaError_t block(const Cond& c, int i, int l, float* r, cudaStream_t st);
   cudaError_t norm(const float* x, void* out, int M, int dd, const float* shift, const float* scale, const bf16* gain,
                    cudaStream_t st);
+  // FP8 step: the normalised activation straight to e4m3 (hq, hs), then an e4m3 GEMM
+  cudaError_t norm_f8(const float* x, int M, const float* shift, const float* scale, const bf16* gain, cudaStream_t st);
+  cudaError_t gemm_f8(const uint8_t* Wq, const float* wscale, int M, int Nn, int K, const Epi& e, cudaStream_t st);
+  cudaError_t quantize_weights(cudaStream_t st);
   cudaError_t init_weights(cudaStream_t st);
 };
 

@@ -12,3 +12,9 @@ $NCU -k regex:gemm_tc2 -s 7 -o gpurun_out/ncu/cross_o $P > gpurun_out/ncu/cross_
 $NCU -k regex:gemm_tc2 -s 9 -o gpurun_out/ncu/mlp_down $P > gpurun_out/ncu/mlp_down.log 2>&1
 $NCU -k regex:rmsnorm -s 0 -o gpurun_out/ncu/rmsnorm $P > gpurun_out/ncu/rmsnorm.log 2>&1
 $NCU -k regex:attn_pp -s 1 -o gpurun_out/ncu/attn_cross $P > gpurun_out/ncu/attn_cross.log 2>&1
+# summaries here (the reports are tens of MB each; gpurun copies back <= 64 MiB)
+for k in o_proj cross_q cross_o mlp_down rmsnorm attn_cross; do
+  [ -f gpurun_out/ncu/$k.ncu-rep ] && python tools/ncu_summary.py full gpurun_out/ncu/$k.ncu-rep > gpurun_out/ncu/$k.json 2>&1
+  ncu -i gpurun_out/ncu/$k.ncu-rep --page details --csv > gpurun_out/ncu/${k}_details.csv 2>/dev/null
+done
+rm -f gpurun_out/ncu/*.ncu-rep
