@@ -275,32 +275,29 @@ def handoff_record(cfg, summary):
             "dit_instances_used": summary["t_inst"]}
 
 
-def video_record(args, peaks, local):
-    """The north_star's headline shape (BASELINE configs[2], C3): text-to-video 81x480x832 ->
-    32760 tokens, DiT 5120 x40 layers, 50 Euler steps, through the same E -> T -> D pipeline on
-    this GPU: 1 warm-up request (50 denoising steps) then `video_requests` timed requests,
-    inputs device-resident (tokens and noise from the seed), with the DiT step's roofline and
-    the clocks sampled during the timed region."""
+def sub_record(args, peaks, local, cfg, precision, warm, n, what):
+    """A further workload through the same E -> T -> D pipeline on this GPU (E:T:D 1:1:1):
+    `warm` warm-up requests, then `n` timed requests with inputs device-resident (tokens and
+    noise from the seed), the DiT step's roofline and the clocks sampled in the timed region."""
     import torch
     from paper_2605_25550_b200 import binding as B, layouts
-    cfg = CONFIGS["video"]
     inst = layouts.partitioned(1)
-    g = B.make_graph(cfg, inst, precision=B.DF_BF16, weight_seed=0, chunk_bytes=(args.chunk_ctx, args.chunk_lat),
+    g = B.make_graph(cfg, inst, precision=precision, weight_seed=0, chunk_bytes=(args.chunk_ctx, args.chunk_lat),
                      n_slots=2, handoff_mode=B.DF_ASYNC | B.DF_HASH, ring_capacity=64, max_steps=cfg.steps)
     ctx = B.Context(g)
     stream = torch.cuda.current_stream()
 
-    def batch(n, seed0):
-        for k in range(n):
-            while ctx.submit(cfg.steps, cfg.shift, seed0 + k, user_tag=seed0 + k)[0] != B.DF_OK:
+    def batch(k, seed0):
+        for j in range(k):
+            while ctx.submit(cfg.steps, cfg.shift, seed0 + j, user_tag=seed0 + j)[0] != B.DF_OK:
                 time.sleep(0.01)
         comps = []
-        while len(comps) < n:
+        while len(comps) < k:
             comps += ctx.poll(16, timeout_ms=1000)
         return comps
 
     try:
-        batch(1, 5000)
+        batch(warm, 5000)
         torch.cuda.synchronize()
         ctx.profile(4, True)
         l0 = ctx.launch_count()
@@ -308,7 +305,7 @@ def video_record(args, peaks, local):
         with Clocks(local) as clk:
             torch.cuda.synchronize()
             ev0.record(stream)
-            comps = batch(args.video_requests, 6000)
+            comps = batch(n, 6000)
             ev1.record(stream)
             ev1.synchronize()
         ms = ev0.elapsed_time(ev1)
@@ -321,16 +318,15 @@ def video_record(args, peaks, local):
     tflop = cfg.flops_per_request() / 1e12
     tfs = tflop / (summ["t_ms"] / 1000.0)
     shares, gfl = kernel_tables(kstats)
-    return {"workload": workload_name(cfg), "E:T:D": "1:1:1", "requests": args.video_requests, "warmup_requests": 1,
-            "value": args.video_requests / (ms / 1000.0), "unit": UNIT, "ms_per_request": ms / args.video_requests,
-            "gpu_launches": launches,
+    return {"what": what, "workload": workload_name(cfg), "E:T:D": "1:1:1", "requests": n, "warmup_requests": warm,
+            "value": n / (ms / 1000.0), "unit": UNIT, "ms_per_request": ms / n, "gpu_launches": launches,
             "dit_step": {"tflop_per_request": tflop, "tflop_per_step": cfg.flops_per_step() / 1e12,
                          "t_stage_ms_median": summ["t_ms"], "achieved_tflops": tfs,
                          "frac_of_sustained_peak": tfs / peaks["bf16_sus"], "frac_of_burst_peak": tfs / peaks["bf16"]},
-            "roofline": roofline(kstats, peaks, None, "video"),
+            "roofline": roofline(kstats, peaks, None, cfg.name),
             "clocks": clk.summary(),
             "handoff": handoff_record(cfg, summ),
-            "eq6": eq6_record((1, 1, 1), summ["T_s"], args.video_requests / (ms / 1000.0)),
+            "eq6": eq6_record((1, 1, 1), summ["T_s"], n / (ms / 1000.0)),
             "kernel_time_share": shares, "kernel_gflops": gfl}
 
 
@@ -464,9 +460,17 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         s = oracle_sample(cfg)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "oracle", "sample": s["sample"]}
-    video = None
+    video = fp8 = None
     if world == 1 and args.config == "image" and args.video_requests > 0:
-        video = video_record(args, peaks, local)
+        # the north_star's headline shape (BASELINE configs[2], C3): 1 warm-up + K timed 50-step requests
+        video = sub_record(args, peaks, local, CONFIGS["video"], B.DF_BF16, 1, args.video_requests,
+                           "text-to-video (C3) through the same pipeline, bf16")
+    if world == 1 and args.config == "image" and args.fp8_requests > 0:
+        # NEXT-4 (R29): the same image workload with the FP8 step mode (QKV, cross-Q and MLP-up
+        # on e4m3 operands); dtype stays bf16 for the headline above -- this is a separate line
+        fp8 = sub_record(args, peaks, local, cfg, B.DF_FP8, args.warmup, args.fp8_requests,
+                         "text-to-image (C2), FP8 step mode (R29): e4m3 QKV / cross-Q / MLP-up")
+        fp8["dtype"] = "e4m3 x e4m3 -> fp32 (3 GEMM classes), bf16 elsewhere"
     gE, gT, gD = layouts.ratio(inst)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -496,6 +500,8 @@ def run_ours(args, cfg):
     }
     if video is not None:
         line["video"] = video
+    if fp8 is not None:
+        line["fp8"] = fp8
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -519,6 +525,8 @@ def main():
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     ap.add_argument("--video-requests", type=int, default=1,
                     help="N=1 image run: timed C3 (video) requests in the line's `video` sub-record (0: skip)")
+    ap.add_argument("--fp8-requests", type=int, default=5,
+                    help="N=1 image run: timed requests of the FP8 step mode in the line's `fp8` sub-record (0: skip)")
     ap.add_argument("--dit-steps", type=int, default=0,
                     help="Euler steps per request (0: the config's); for the few-step I2V / workload-shift runs")
     args = ap.parse_args()

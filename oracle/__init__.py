@@ -35,4 +35,6 @@ is checked to fail under one-line mutations of the oracle by tools/mutate_oracle
   capacity.payload_hash pinned: splitmix64 published first output, chunk additivity
   fp8 (NEXT-4, R28) pinned: E4M3 closed forms, 256-code round trip, ties-to-even,
                saturation, torch float8_e4m3fn cast, brute-force GEMM
+  dit_fp8 (NEXT-4, R29) pinned: per-row quantiser closed forms (amax-448 row, zero row,
+               power-of-two scaling); wiring = dit.block exactly under identity quantisers
 """

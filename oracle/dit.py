@@ -201,15 +201,20 @@ def _unheads(z: np.ndarray) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- one block
-def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = True, kvi=None) -> np.ndarray:
+def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = True, kvi=None,
+          q8=None) -> np.ndarray:
     """One DiT block (Wan2.1 order, R1): adaLN self-attention, cross-attention,
     adaLN gated MLP.  r [N, d] fp64 -> r' [N, d].  I2V: the cross-attention output is the
-    text term plus the image-token term softmax(qc Ki^T / sqrt(dh)) Vi (Wan I2V, R27)."""
+    text term plus the image-token term softmax(qc Ki^T / sqrt(dh)) Vi (Wan I2V, R27).
+    q8 (FP8 step mode, R29; oracle/dit_fp8.py): the three GEMMs fed by a normalised activation
+    (QKV, cross-Q, MLP up) take q8.act(h) and q8.weight(...) instead of h and the weight."""
     d, H, eps = cfg.d, cfg.heads, cfg.eps
+    act = (lambda x: x) if q8 is None else q8.act
+    wgt = (lambda l_, name: P.layer(l_, name)) if q8 is None else (lambda l_, name: q8.weight(P, l_, name))
     sh1, sc1, g1, sh2, sc2, g2 = (e6 + P.layer(l, "mod"))  # rows 0..5 (R4)
     # --- self-attention (a4-a7)
     h = rms_norm(r, eps) * (1.0 + sc1) + sh1
-    qkv = h @ P.layer(l, "qkv_w") + P.layer(l, "qkv_b")
+    qkv = act(h) @ wgt(l, "qkv_w") + P.layer(l, "qkv_b")
     q, k, v = qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
     q = head_rms_norm(q, H, eps) * P.layer(l, "g_q")
     k = head_rms_norm(k, H, eps) * P.layer(l, "g_k")
@@ -220,15 +225,15 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
     # --- cross-attention (a8): pre-norm with gain, not modulated, ungated (R3)
     if cross:
         hc = rms_norm(r, eps) * P.layer(l, "g_n3")
-        qc = head_rms_norm(hc @ P.layer(l, "cq_w") + P.layer(l, "cq_b"), H, eps) * P.layer(l, "g_cq")
+        qc = head_rms_norm(act(hc) @ wgt(l, "cq_w") + P.layer(l, "cq_b"), H, eps) * P.layer(l, "g_cq")
         kc, vc = kv
         oc = softmax_attention(_heads(qc, H), _heads(kc, H), _heads(vc, H))
         if kvi is not None:
             oc = oc + softmax_attention(_heads(qc, H), _heads(kvi[0], H), _heads(kvi[1], H))
         r = r + (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))
     # --- gated MLP (a9-a10): SwiGLU with biases (R9)
-    h2 = rms_norm(r, eps) * (1.0 + sc2) + sh2
-    a = silu(h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * (h2 @ P.layer(l, "w3") + P.layer(l, "b3"))
+    h2 = act(rms_norm(r, eps) * (1.0 + sc2) + sh2)
+    a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3") + P.layer(l, "b3"))
     r = r + g2 * (a @ P.layer(l, "w2") + P.layer(l, "b2"))
     return r
 
@@ -270,7 +275,7 @@ def head(P, cfg, r: np.ndarray, e: np.ndarray) -> np.ndarray:
     return unpatchify(y, cfg)
 
 
-def velocity(P, cfg, x: np.ndarray, i: int, cond, cross: bool = True, trace=None) -> np.ndarray:
+def velocity(P, cfg, x: np.ndarray, i: int, cond, cross: bool = True, trace=None, q8=None) -> np.ndarray:
     """v(x_i, sigma_i): patch embed -> blocks -> head (a2-a11)."""
     pos = token_positions(cfg)
     xin = np.asarray(x, dtype=np.float64)
@@ -282,7 +287,7 @@ def velocity(P, cfg, x: np.ndarray, i: int, cond, cross: bool = True, trace=None
     kvi = cond.get("kvi")
     for l in range(cfg.layers):
         r = block(P, cfg, l, r, cond["e6"][i], cond["kv"][l], pos, cross=cross,
-                  kvi=kvi[l] if kvi is not None else None)
+                  kvi=kvi[l] if kvi is not None else None, q8=q8)
         if trace is not None:
             trace.append(r.copy())
     return head(P, cfg, r, cond["e"][i])
@@ -297,9 +302,9 @@ def velocity_cfg(P, cfg, x, i, cond, cond_neg, guidance: float) -> np.ndarray:
     return v_u + guidance * (v_c - v_u)
 
 
-def step(P, cfg, x, i, cond, sig):
+def step(P, cfg, x, i, cond, sig, q8=None):
     """One denoising step: returns (x_{i+1}, v_i)."""
-    v = velocity(P, cfg, x, i, cond)
+    v = velocity(P, cfg, x, i, cond, q8=q8)
     return euler_update(np.asarray(x, dtype=np.float64), v, sig[i], sig[i + 1]), v
 
 

@@ -1,0 +1,86 @@
+"""fp64 CPU ORACLE of the FP8 step mode (R29).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): never imported by the product path.
+
+PAPER.md names quantisation only as a serving optimisation of the systems it builds on
+("FP8/INT8 quantisation") and fixes no format.  Reading R29 (on top of R28's E4M3
+format and per-tensor current scaling, oracle/fp8.py):
+  * the three GEMMs of a block whose input is a normalised activation -- QKV (a5), the
+    cross-attention query projection (a8) and the MLP up projection W1 | W3 (a10) -- take
+    e4m3 operands; every other operation is the bf16 model's (oracle/dit.py);
+  * the activation h [N, d] is quantised per token row: h is rounded to fp32 (the kernel's
+    precision, which decides the codes), s_m = the smallest power of two >= fp32(amax_j |h_mj|
+    / 448) (1 for a zero row; a power of two makes h / s_m an exact exponent shift),
+    q_mj = e4m3(h_mj / s_m), and the GEMM sees dec(q_mj) * s_m;
+  * the weight is quantised per tensor (R28) -- the fused W_qkv as one tensor, W_1 and W_3
+    jointly (the GPU stores them interleaved as one tensor) -- and the GEMM sees dec(q) * s;
+  * products are exact and summed in fp64 (the GPU: exact products, fp32 accumulation).
+
+Pinned by tests/test_oracle_fp8.py: quantize_rows' closed forms (a row whose amax is 448
+keeps its e4m3-representable values; a zero row; power-of-two row scaling moves only the
+scale), and the wiring -- block(..., q8=Q8 with identity quantisers) is dit.block exactly,
+so the FP8 mode differs from the pinned bf16 composition only where R29 says.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import fp8
+from . import dit
+
+E4M3_MAX = np.float32(448.0)
+
+
+def pow2_ceil(v):
+    """Smallest power of two >= v (v > 0, fp32): v itself if it is one."""
+    m, e = np.frexp(np.asarray(v, dtype=np.float64))  # v = m 2^e, m in [0.5, 1)
+    return np.where(m == 0.5, v, np.ldexp(1.0, e)).astype(np.float32)
+
+
+def quantize_rows(h):
+    """h [M, K] -> (q bytes [M, K], s fp32 [M]): per-row scaling with power-of-two scales (R29)."""
+    h32 = np.asarray(h, dtype=np.float64).astype(np.float32)
+    amax = np.max(np.abs(h32), axis=-1).astype(np.float32)
+    s = np.where(amax > 0, pow2_ceil((amax / E4M3_MAX).astype(np.float32)), np.float32(1.0)).astype(np.float32)
+    y = (h32.astype(np.float64) / s.astype(np.float64)[:, None])  # exact: s is a power of two
+    return fp8.e4m3_encode(y), s
+
+
+def act(h):
+    """The activation as the e4m3 GEMM sees it: dec(q) * s per row."""
+    q, s = quantize_rows(h)
+    return fp8.e4m3_decode(q) * s.astype(np.float64)[:, None]
+
+
+def weight_q(W):
+    """The weight as the e4m3 GEMM sees it: dec(q) * s per tensor (R28)."""
+    q, s = fp8.quantize_per_tensor(np.asarray(W, dtype=np.float64))
+    return fp8.e4m3_decode(q) * float(s)
+
+
+class Q8:
+    """Quantisers handed to oracle.dit.block (q8=...).  W_1 and W_3 share one scale (they are
+    one interleaved tensor on the GPU); the dequantised weights are cached per layer."""
+
+    def __init__(self, act_fn=act, weight_fn=weight_q):
+        self.act = act_fn
+        self._wq = weight_fn
+        self._cache = {}
+
+    def weight(self, P, l, name):
+        key = (id(P), l, name)
+        if key not in self._cache:
+            if name in ("w1", "w3"):
+                w1, w3 = P.layer(l, "w1"), P.layer(l, "w3")
+                both = self._wq(np.concatenate([w1, w3], axis=1))
+                f = w1.shape[1]
+                self._cache[(id(P), l, "w1")] = both[:, :f]
+                self._cache[(id(P), l, "w3")] = both[:, f:]
+            else:
+                self._cache[key] = self._wq(P.layer(l, name))
+        return self._cache[key]
+
+
+def step(P, cfg, x, i, cond, sig):
+    """One FP8-mode denoising step: (x_{i+1}, v_i)."""
+    return dit.step(P, cfg, x, i, cond, sig, q8=Q8())

@@ -863,9 +863,24 @@ __global__ void __launch_bounds__(256) e4m3_quant_kernel(const bf16* __restrict_
     q[i] = uint8_t(__nv_cvt_float_to_fp8(__fdiv_rn(bf2f(x[i]), s), __NV_SATFINITE, __NV_E4M3));
 }
 // RMSNorm + modulation (or gain) quantised per row to e4m3 (FP8 step, R29): one warp per row,
-// three passes over the row (the row stays in L1/L2): sum of squares; y and its amax; q.
+// three passes over the row (the row stays in L1/L2): sum of squares; y and its amax; q.  The
+// row scale is a power of two (the fp32 amax / 448 rounded up to one), so y / s is an exact
+// exponent shift: one multiply per element instead of an IEEE division.
+DF_DEV float pow2_ceil(float v) {  // smallest power of two >= v (v > 0; 2^-126 for subnormal v)
+  const uint32_t b = __float_as_uint(v);
+  const uint32_t e = b >> 23;
+  if (e == 0) return __uint_as_float(1u << 23);
+  return (b & 0x7FFFFFu) ? __uint_as_float((e + 1) << 23) : v;
+}
+__device__ __forceinline__ uint32_t e4m3x4_mul(float a, float b, float c, float d, float inv) {
+  const uint32_t q0 = __nv_cvt_float_to_fp8(a * inv, __NV_SATFINITE, __NV_E4M3);
+  const uint32_t q1 = __nv_cvt_float_to_fp8(b * inv, __NV_SATFINITE, __NV_E4M3);
+  const uint32_t q2 = __nv_cvt_float_to_fp8(c * inv, __NV_SATFINITE, __NV_E4M3);
+  const uint32_t q3 = __nv_cvt_float_to_fp8(d * inv, __NV_SATFINITE, __NV_E4M3);
+  return q0 | (q1 << 8) | (q2 << 16) | (q3 << 24);
+}
 template <int VPT>
-__global__ void __launch_bounds__(128) rmsnorm_e4m3_kernel(const float* __restrict__ x, uint8_t* __restrict__ q,
+__global__ void __launch_bounds__(128, 8) rmsnorm_e4m3_kernel(const float* __restrict__ x, uint8_t* __restrict__ q,
                                                           float* __restrict__ srow, int M,
                                                           const float* __restrict__ shift,
                                                           const float* __restrict__ scale,
@@ -907,13 +922,14 @@ __global__ void __launch_bounds__(128) rmsnorm_e4m3_kernel(const float* __restri
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
-  const float sr = am > 0.f ? __fdiv_rn(am, 448.f) : 1.f;
+  const float sr = am > 0.f ? pow2_ceil(__fdiv_rn(am, 448.f)) : 1.f;
+  const float rs = __uint_as_float((254u << 23) - __float_as_uint(sr));  // exactly 1 / sr (a power of two)
   uint32_t* qr = reinterpret_cast<uint32_t*>(q + size_t(row) * d);
 #pragma unroll 8
   for (int i = 0; i < VPT; ++i) {
     float y[4];
     modulate(lane + 32 * i, y);
-    qr[lane + 32 * i] = e4m3x4(y[0], y[1], y[2], y[3], sr);
+    qr[lane + 32 * i] = e4m3x4_mul(y[0], y[1], y[2], y[3], rs);
   }
   if (lane == 0) srow[row] = sr;
 }

@@ -79,3 +79,57 @@ def test_gemm_e4m3_rejects_bad_shapes(ctx):
     out = torch.empty((256, 256), device="cuda")
     with pytest.raises(B.DFError):
         ctx.op_gemm_e4m3(q, torch.zeros((256, 200), dtype=torch.uint8, device="cuda"), s, s, out)
+
+
+# ---------------------------------------------------------------- FP8 step mode (R29)
+def _fp8_step(cfg, prec, x, ctx_bits, i):
+    from oracle import dit
+    from gpu_util import bf16_tensor_from_bits, make_ctx
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32)
+    with make_ctx(cfg, precision=prec) as c:
+        cond = c.dit_prepare(1, bf16_tensor_from_bits(ctx_bits), sig)
+        xt = torch.from_numpy(x).cuda()
+        vt = torch.zeros_like(xt)
+        c.dit_step(1, cond, i, xt, vt)
+        torch.cuda.synchronize()
+        c.cond_release(cond)
+        return xt.cpu().numpy(), vt.cpu().numpy()
+
+
+@pytest.mark.parametrize("i", [0, 5])
+def test_fp8_step_matches_the_fp8_oracle(i):
+    """NEXT-4 in the DiT step (R29): QKV, cross-Q and MLP-up on e4m3 operands (activation per
+    row from the RMSNorm kernel, weight per tensor), the rest bf16.  Against the fp64 oracle
+    of the same FP8 mode the step is within the bf16 step tolerance (1e-2): both quantise the
+    same fp32-rounded activations, so codes differ only where the two sides' activations round
+    to different sides of an e4m3 boundary.  Against the bf16 oracle it differs by the
+    quantisation itself (reported, bounded by 0.1)."""
+    from oracle import dit, dit_fp8
+    from oracle import params as OP
+    from synth import inputs
+    from synth.configs import MID
+    from gpu_util import rel_l2
+    from paper_2605_25550_b200 import binding as B
+    cfg = MID
+    x = inputs.latent(cfg, 91)
+    ctx_bits = inputs.ctx_bf16(cfg, 92)
+    gx, gv = _fp8_step(cfg, B.DF_FP8, x, ctx_bits, i)
+    P = OP.Params(cfg, 0)
+    sig = dit.sigmas(cfg.steps, cfg.shift).astype(np.float32).astype(np.float64)
+    cond = dit.prologue(P, cfg, inputs.bf16_bits_to_f64(ctx_bits), sig)
+    ox8, ov8 = dit_fp8.step(P, cfg, x.astype(np.float64), i, cond, sig)
+    ox, ov = dit.step(P, cfg, x.astype(np.float64), i, cond, sig)
+    assert rel_l2(gv, ov8) <= 1e-2, rel_l2(gv, ov8)
+    assert rel_l2(gx, ox8) <= 1e-2
+    q_err = rel_l2(ov8, ov)
+    assert 1e-3 < q_err < 0.1, q_err            # the FP8 mode is not a silent bf16 run
+    assert rel_l2(gv, ov) > 0.5 * q_err
+
+
+def test_fp8_mode_rejects_small_shapes():
+    """The FP8 GEMMs run on CTA-pair tiles (M, N >= 256) with the head-major TMA epilogue."""
+    from synth.configs import TINY
+    from gpu_util import make_ctx
+    from paper_2605_25550_b200 import binding as B
+    with pytest.raises(B.DFError):
+        make_ctx(TINY, precision=B.DF_FP8)

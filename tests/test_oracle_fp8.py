@@ -65,3 +65,44 @@ def test_gemm_bruteforce():
             for k in range(5):
                 acc += fp8.e4m3_decode(qa[i, k]) * fp8.e4m3_decode(qb[j, k])
             assert out[i, j] == pytest.approx(1.5 * acc, rel=1e-12, abs=1e-300)
+
+
+def test_quantize_rows_closed_forms():
+    """R29 per-row scaling: a row whose amax is 448 has s = 1 and keeps its (e4m3-exact)
+    values; a zero row has s = 1 and all-zero codes; scaling a row by 2^k scales only s; a
+    row whose amax / 448 is not a power of two gets the next power of two up (amax 300 ->
+    s = 1, amax 449 -> s = 2)."""
+    from oracle import dit_fp8
+    row = np.array([448.0, -224.0, 1.0, -3.5, 0.0, 0.015625], dtype=np.float64)  # all e4m3 values
+    q, s = dit_fp8.quantize_rows(np.stack([row, np.zeros(6), row * 2.0 ** -7]))
+    assert s[0] == np.float32(1.0) and s[1] == np.float32(1.0) and s[2] == np.float32(2.0 ** -7)
+    assert np.array_equal(fp8.e4m3_decode(q[0]), row)
+    assert np.all(q[1] == 0)
+    assert np.array_equal(q[2], q[0])
+    assert np.array_equal(dit_fp8.act(row[None]), row[None])
+    _, s2 = dit_fp8.quantize_rows(np.array([[300.0, -1.0], [449.0, 2.0], [3.0 * 2.0 ** -20, 0.0]]))
+    assert s2[0] == np.float32(1.0) and s2[1] == np.float32(2.0)
+    assert s2[2] == np.float32(2.0 ** -27)  # 3 * 2^-20 / 448 = 2^-27.2 -> 2^-27
+
+
+def test_fp8_block_wiring_reduces_to_the_bf16_block():
+    """block(..., q8) with identity quantisers is dit.block exactly: the FP8 mode changes the
+    composition only at the three R29 GEMM inputs.  With the real quantisers the block
+    differs from the bf16 one by an amount of the order of e4m3's relative step (2^-4)."""
+    from oracle import dit, dit_fp8
+    from oracle import params as OP
+    from synth import inputs
+    from synth.configs import TINY
+    cfg = TINY
+    P = OP.Params(cfg, 0)
+    r = inputs.residual(cfg, 3).astype(np.float64)
+    rr = np.random.default_rng(1)
+    kv = (rr.standard_normal((cfg.L_txt, cfg.d)), rr.standard_normal((cfg.L_txt, cfg.d)))
+    e6 = rr.standard_normal((6, cfg.d)) * 0.1
+    pos = dit.token_positions(cfg)
+    ref = dit.block(P, cfg, 0, r, e6, kv, pos)
+    ident = dit_fp8.Q8(act_fn=lambda h: h, weight_fn=lambda w: w)
+    assert np.array_equal(dit.block(P, cfg, 0, r, e6, kv, pos, q8=ident), ref)
+    got = dit.block(P, cfg, 0, r, e6, kv, pos, q8=dit_fp8.Q8())
+    rel = np.linalg.norm((got - r) - (ref - r)) / np.linalg.norm(ref - r)
+    assert 1e-3 < rel < 0.2, rel

@@ -66,15 +66,15 @@ MUTATIONS = [
      'sh1, sc1, g1, sh2, sc2, g2 = (e6 + 0 * P.layer(l, "mod"))', "e6 without M_l"),
     ("mod1-sc-not-1+sc", "oracle/dit.py", "h = rms_norm(r, eps) * (1.0 + sc1) + sh1",
      "h = rms_norm(r, eps) * sc1 + sh1", "scale instead of 1 + scale"),
-    ("mod2-swapped-inline", "oracle/dit.py", "h2 = rms_norm(r, eps) * (1.0 + sc2) + sh2",
-     "h2 = rms_norm(r, eps) * (1.0 + sh2) + sc2", "MLP modulation with shift/scale exchanged"),
+    ("mod2-swapped-inline", "oracle/dit.py", "h2 = act(rms_norm(r, eps) * (1.0 + sc2) + sh2)",
+     "h2 = act(rms_norm(r, eps) * (1.0 + sh2) + sc2)", "MLP modulation with shift/scale exchanged"),
     ("swiglu-silu-on-w3", "oracle/dit.py",
-     'a = silu(h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * (h2 @ P.layer(l, "w3") + P.layer(l, "b3"))',
-     'a = (h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * silu(h2 @ P.layer(l, "w3") + P.layer(l, "b3"))',
+     'a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3") + P.layer(l, "b3"))',
+     'a = (h2 @ wgt(l, "w1") + P.layer(l, "b1")) * silu(h2 @ wgt(l, "w3") + P.layer(l, "b3"))',
      "SiLU on the W3 branch"),
     ("swiglu-no-b3", "oracle/dit.py",
-     'a = silu(h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * (h2 @ P.layer(l, "w3") + P.layer(l, "b3"))',
-     'a = silu(h2 @ P.layer(l, "w1") + P.layer(l, "b1")) * (h2 @ P.layer(l, "w3"))', "b3 dropped"),
+     'a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3") + P.layer(l, "b3"))',
+     'a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3"))', "b3 dropped"),
     ("mlp-bias-ungated", "oracle/dit.py", 'r = r + g2 * (a @ P.layer(l, "w2") + P.layer(l, "b2"))',
      'r = r + g2 * (a @ P.layer(l, "w2")) + P.layer(l, "b2")', "b2 outside the gate"),
     ("attn-bias-ungated", "oracle/dit.py", 'r = r + g1 * (_unheads(o) @ P.layer(l, "o_w") + P.layer(l, "o_b"))',
