@@ -206,8 +206,8 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
     """One DiT block (Wan2.1 order, R1): adaLN self-attention, cross-attention,
     adaLN gated MLP.  r [N, d] fp64 -> r' [N, d].  I2V: the cross-attention output is the
     text term plus the image-token term softmax(qc Ki^T / sqrt(dh)) Vi (Wan I2V, R27).
-    q8 (FP8 step mode, R29; oracle/dit_fp8.py): the three GEMMs fed by a normalised activation
-    (QKV, cross-Q, MLP up) take q8.act(h) and q8.weight(...) instead of h and the weight."""
+    q8 (FP8 step mode, R29; oracle/dit_fp8.py): every GEMM of the block takes q8.act(input)
+    and q8.weight(...) instead of its input and weight."""
     d, H, eps = cfg.d, cfg.heads, cfg.eps
     act = (lambda x: x) if q8 is None else q8.act
     wgt = (lambda l_, name: P.layer(l_, name)) if q8 is None else (lambda l_, name: q8.weight(P, l_, name))
@@ -221,7 +221,7 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
     q = rope3(q.reshape(-1, H, cfg.dh), pos, cfg.rope_axes, cfg.rope_theta)
     k = rope3(k.reshape(-1, H, cfg.dh), pos, cfg.rope_axes, cfg.rope_theta)
     o = softmax_attention(q.transpose(1, 0, 2), k.transpose(1, 0, 2), _heads(v, H))
-    r = r + g1 * (_unheads(o) @ P.layer(l, "o_w") + P.layer(l, "o_b"))
+    r = r + g1 * (act(_unheads(o)) @ wgt(l, "o_w") + P.layer(l, "o_b"))
     # --- cross-attention (a8): pre-norm with gain, not modulated, ungated (R3)
     if cross:
         hc = rms_norm(r, eps) * P.layer(l, "g_n3")
@@ -230,11 +230,11 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
         oc = softmax_attention(_heads(qc, H), _heads(kc, H), _heads(vc, H))
         if kvi is not None:
             oc = oc + softmax_attention(_heads(qc, H), _heads(kvi[0], H), _heads(kvi[1], H))
-        r = r + (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))
+        r = r + (act(_unheads(oc)) @ wgt(l, "co_w") + P.layer(l, "co_b"))
     # --- gated MLP (a9-a10): SwiGLU with biases (R9)
     h2 = act(rms_norm(r, eps) * (1.0 + sc2) + sh2)
     a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3") + P.layer(l, "b3"))
-    r = r + g2 * (a @ P.layer(l, "w2") + P.layer(l, "b2"))
+    r = r + g2 * (act(a) @ wgt(l, "w2") + P.layer(l, "b2"))
     return r
 
 

@@ -5,13 +5,13 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): never imported by the product
 PAPER.md names quantisation only as a serving optimisation of the systems it builds on
 ("FP8/INT8 quantisation") and fixes no format.  Reading R29 (on top of R28's E4M3
 format and per-tensor current scaling, oracle/fp8.py):
-  * the three GEMMs of a block whose input is a normalised activation -- QKV (a5), the
-    cross-attention query projection (a8) and the MLP up projection W1 | W3 (a10) -- take
-    e4m3 operands; every other operation is the bf16 model's (oracle/dit.py);
-  * the activation h [N, d] is quantised per token row: h is rounded to fp32 (the kernel's
-    precision, which decides the codes), s_m = the smallest power of two >= fp32(amax_j |h_mj|
-    / 448) (1 for a zero row; a power of two makes h / s_m an exact exponent shift),
-    q_mj = e4m3(h_mj / s_m), and the GEMM sees dec(q_mj) * s_m;
+  * all six GEMMs of a block -- QKV (a5), O (a7), cross-Q and cross-O (a8), MLP up W1 | W3
+    and MLP down (a10) -- take e4m3 operands; every other operation (norms, attention, the
+    prologue, patch embedding, head) is the bf16 model's (oracle/dit.py);
+  * a GEMM's input activation x [N, K] is quantised per token row: x is rounded to fp32 (the
+    kernel's precision, which decides the codes), s_m = the smallest power of two >=
+    fp32(amax_j |x_mj| / 448) (1 for a zero row; a power of two makes x / s_m an exact exponent
+    shift), q_mj = e4m3(x_mj / s_m), and the GEMM sees dec(q_mj) * s_m;
   * the weight is quantised per tensor (R28) -- the fused W_qkv as one tensor, W_1 and W_3
     jointly (the GPU stores them interleaved as one tensor) -- and the GEMM sees dec(q) * s;
   * products are exact and summed in fp64 (the GPU: exact products, fp32 accumulation).

@@ -934,6 +934,48 @@ __global__ void __launch_bounds__(128, 8) rmsnorm_e4m3_kernel(const float* __res
   if (lane == 0) srow[row] = sr;
 }
 
+// A bf16 activation [M, K] quantised per row to e4m3 with power-of-two row scales (R29): the
+// inputs of the O, cross-O and MLP-down projections (attention and SwiGLU outputs).  One warp
+// per row, 8 bf16 per lane per step; pass 1 the row amax, pass 2 the codes (row re-read from L1/L2).
+__global__ void __launch_bounds__(256) quant_rows_e4m3_kernel(const bf16* __restrict__ x, uint8_t* __restrict__ q,
+                                                             float* __restrict__ srow, int M, int K) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * K);
+  const int n8 = K / 8;
+  float am = 0.f;
+  for (int i = lane; i < n8; i += 32) {
+    const uint4 u = __ldg(xr + i);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      am = fmaxf(am, fmaxf(fabsf(__uint_as_float(w[k] << 16)), fabsf(__uint_as_float(w[k] & 0xFFFF0000u))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  const float sr = am > 0.f ? pow2_ceil(__fdiv_rn(am, 448.f)) : 1.f;
+  const float rs = __uint_as_float((254u << 23) - __float_as_uint(sr));
+  uint2* qr = reinterpret_cast<uint2*>(q + size_t(row) * K);
+  for (int i = lane; i < n8; i += 32) {
+    const uint4 u = __ldg(xr + i);
+    uint2 o;
+    o.x = e4m3x4_mul(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xFFFF0000u), rs);
+    o.y = e4m3x4_mul(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u), __uint_as_float(u.w << 16),
+                     __uint_as_float(u.w & 0xFFFF0000u), rs);
+    qr[i] = o;
+  }
+  if (lane == 0) srow[row] = sr;
+}
+
+cudaError_t quant_rows_e4m3(const bf16* x, uint8_t* q, float* s, int M, int K, cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  if (K % 8) return cudaErrorInvalidValue;
+  quant_rows_e4m3_kernel<<<(M + 7) / 8, 256, 0, st>>>(x, q, s, M, K);
+  return cudaGetLastError();
+}
+
 cudaError_t rmsnorm_e4m3(const float* x, uint8_t* q, float* s, int M, int d, const float* shift, const float* scale,
                          const bf16* gain, float eps, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;

@@ -21,6 +21,8 @@ cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaSt
 // bf16 path's TMA-store epilogues (heads / SwiGLU / stores / gated residual)
 cudaError_t gemm_e4m3_epi(const uint8_t* qa, const float* a_row, const uint8_t* qw, const float* w_scale, int M, int N,
                           int K, const Epi& e, cudaStream_t st);
+// bf16 activation [M, K] -> e4m3 per row with power-of-two row scales (R29); K % 8 == 0
+cudaError_t quant_rows_e4m3(const bf16* x, uint8_t* q, float* s, int M, int K, cudaStream_t st);
 // RMSNorm (+ modulation or gain) with e4m3 output quantised per row (R29): q[m, :] =
 // e4m3(y[m, :] / s[m]), s[m] = amax|y[m, :]| / 448 (1 for a zero row), y in fp32.
 cudaError_t rmsnorm_e4m3(const float* x, uint8_t* q, float* s, int M, int d, const float* shift, const float* scale,

@@ -189,7 +189,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           (i2v() ? al(N2 * d * ab) : 0) +
           al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
-    if (fp8()) wsb += al(N2 * d) + al(N2 * 4);
+    if (fp8()) wsb += al(N2 * std::max(d, f)) + al(N2 * 4);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
     else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // GEMM stream-K
   } else if (stage == DF_E) {
@@ -208,7 +208,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     if (i2v()) oi = ws.take(N2 * d * ab);
     vbatch = (float*)ws.take(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (fp8()) {
-      hq = (uint8_t*)ws.take(N2 * d);
+      hq = (uint8_t*)ws.take(N2 * std::max(d, f));
       hs = (float*)ws.take(N2 * 4);
     }
     mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
@@ -246,21 +246,27 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
   return cudaSuccess;
 }
 
-// FP8 step (R29): per-tensor e4m3 copies of W_qkv, W_cq and W_1 | W_3 (R28's quantiser on the
-// bf16 weights, so the codes are those of the oracle's quantize_per_tensor).
+// FP8 step (R29): per-tensor e4m3 copies of every block GEMM's weight (R28's quantiser on the
+// bf16 weights, so the codes are those of the oracle's quantize_per_tensor; W_1 | W_3 jointly).
 cudaError_t Model::quantize_weights(cudaStream_t st) {
   const size_t d = c.d, f = c.ffn;
-  const size_t per = al(3 * d * d) + al(d * d) + al(2 * f * d) + al(3 * 4);
+  const size_t per = al(3 * d * d) + 3 * al(d * d) + 2 * al(2 * f * d) + al(6 * 4);
   DF_TRY(f8mem.reserve(per * c.layers + 4096));
   for (auto& l : Lw) {
     l.qkv_q = (uint8_t*)f8mem.take(3 * d * d);
     l.cq_q = (uint8_t*)f8mem.take(d * d);
     l.w13_q = (uint8_t*)f8mem.take(2 * f * d);
-    l.f8s = (float*)f8mem.take(3 * 4);
+    l.o_q = (uint8_t*)f8mem.take(d * d);
+    l.co_q = (uint8_t*)f8mem.take(d * d);
+    l.w2_q = (uint8_t*)f8mem.take(d * f);
+    l.f8s = (float*)f8mem.take(6 * 4);
     if (!l.f8s) return cudaErrorMemoryAllocation;
     DF_L(quant_e4m3(l.qkv_wT, 3 * d * d, l.qkv_q, l.f8s + 0, st));
     DF_L(quant_e4m3(l.cq_wT, d * d, l.cq_q, l.f8s + 1, st));
     DF_L(quant_e4m3(l.w13T, 2 * f * d, l.w13_q, l.f8s + 2, st));
+    DF_L(quant_e4m3(l.o_wT, d * d, l.o_q, l.f8s + 3, st));
+    DF_L(quant_e4m3(l.co_wT, d * d, l.co_q, l.f8s + 4, st));
+    DF_L(quant_e4m3(l.w2T, d * f, l.w2_q, l.f8s + 5, st));
   }
   return cudaSuccess;
 }
@@ -438,6 +444,12 @@ cudaError_t Model::norm_f8(const float* x, int M, const float* shift, const floa
                            cudaStream_t st) {
   ProfScope ps(prof, st, K_NORM, 0.0, double(M) * c.d * (4.0 + 1.0));
   DF_L(rmsnorm_e4m3(x, hq, hs, M, int(c.d), shift, scale, gain, c.eps, st));
+  return cudaSuccess;
+}
+
+cudaError_t Model::quant_f8(const void* x, int M, int K, cudaStream_t st) {
+  ProfScope ps(prof, st, K_MISC, 0.0, double(M) * K * 3.0);
+  DF_L(quant_rows_e4m3(static_cast<const bf16*>(x), hq, hs, M, K, st));
   return cudaSuccess;
 }
 
@@ -639,7 +651,12 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     e.resid = res;
     e.ldr = d;
     e.gate = md + 2 * d;
-    DF_TRY(gemm(o, d, w.o_wT, d, M, d, d, e, of, st));
+    if (fp8()) {
+      DF_TRY(quant_f8(o, M, d, st));
+      DF_TRY(gemm_f8(w.o_q, w.f8s + 3, M, d, d, e, st));
+    } else {
+      DF_TRY(gemm(o, d, w.o_wT, d, M, d, d, e, of, st));
+    }
   }
   // a8: cross-attention: hc = RMSNorm(r) g_n3; qc = headRMS(hc Wcq + b) g_cq; r += attn Wco + b
   if (fp8()) DF_TRY(norm_f8(res, M, nullptr, nullptr, w.g_n3, st));
@@ -663,7 +680,12 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     cur_kind = K_CO;
     e.resid = res;
     e.ldr = d;
-    DF_TRY(gemm(o, d, w.co_wT, d, M, d, d, e, of, st));
+    if (fp8()) {
+      DF_TRY(quant_f8(o, M, d, st));
+      DF_TRY(gemm_f8(w.co_q, w.f8s + 4, M, d, d, e, st));
+    } else {
+      DF_TRY(gemm(o, d, w.co_wT, d, M, d, d, e, of, st));
+    }
   }
   // a9: h2 = RMSNorm(r)(1 + sc2) + sh2
   if (fp8()) DF_TRY(norm_f8(res, M, md + 3 * d, md + 4 * d, nullptr, st));
@@ -685,7 +707,12 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     e.resid = res;
     e.ldr = d;
     e.gate = md + 5 * d;
-    DF_TRY(gemm(a, f, w.w2T, f, M, d, f, e, of, st));
+    if (fp8()) {
+      DF_TRY(quant_f8(a, M, f, st));
+      DF_TRY(gemm_f8(w.w2_q, w.f8s + 5, M, d, f, e, st));
+    } else {
+      DF_TRY(gemm(a, f, w.w2T, f, M, d, f, e, of, st));
+    }
   }
   return cudaSuccess;
 }

@@ -44,8 +44,8 @@ struct LayerW {
   bf16 *ckvi_wT = nullptr, *ckvi_b = nullptr, *g_ki = nullptr;  // I2V image-token K | V, K gain
   // FP8 step (R29): e4m3 copies of the three weights fed by a normalised activation, each with
   // its per-tensor scale (device fp32): QKV, cross-Q, MLP up (interleaved W1 | W3)
-  uint8_t *qkv_q = nullptr, *cq_q = nullptr, *w13_q = nullptr;
-  float* f8s = nullptr;  // [3]: qkv, cq, w13
+  uint8_t *qkv_q = nullptr, *cq_q = nullptr, *w13_q = nullptr, *o_q = nullptr, *co_q = nullptr, *w2_q = nullptr;
+  float* f8s = nullptr;  // [6]: qkv, cq, w13, o, co, w2
 };
 
 // Where a logical tensor lives on the device (for df_weight_bits).
@@ -175,7 +175,7 @@ struct Model {
   float* headmod = nullptr; // [2][d]
   float2* rope = nullptr;
   float* vbatch = nullptr;  // [2][C,F,H,W] velocities of a CFG batch
-  uint8_t* hq = nullptr;    // FP8 step: e4m3 normalised activation [2N, d] and its row scales [2N]
+  uint8_t* hq = nullptr;    // FP8 step: e4m3 GEMM input [2N, max(d, f)] and its row scales [2N]
   float* hs = nullptr;
   // encoder workspace
   float* ez = nullptr;      // [L, d_txt]
@@ -216,6 +216,7 @@ struct Model {
   // FP8 step: the normalised activation straight to e4m3 (hq, hs), then an e4m3 GEMM
   cudaError_t norm_f8(const float* x, int M, const float* shift, const float* scale, const bf16* gain, cudaStream_t st);
   cudaError_t gemm_f8(const uint8_t* Wq, const float* wscale, int M, int Nn, int K, const Epi& e, cudaStream_t st);
+  cudaError_t quant_f8(const void* x, int M, int K, cudaStream_t st);  // bf16 activation -> hq / hs
   cudaError_t quantize_weights(cudaStream_t st);
   cudaError_t init_weights(cudaStream_t st);
 };

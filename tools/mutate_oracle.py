@@ -75,12 +75,12 @@ MUTATIONS = [
     ("swiglu-no-b3", "oracle/dit.py",
      'a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3") + P.layer(l, "b3"))',
      'a = silu(h2 @ wgt(l, "w1") + P.layer(l, "b1")) * (h2 @ wgt(l, "w3"))', "b3 dropped"),
-    ("mlp-bias-ungated", "oracle/dit.py", 'r = r + g2 * (a @ P.layer(l, "w2") + P.layer(l, "b2"))',
-     'r = r + g2 * (a @ P.layer(l, "w2")) + P.layer(l, "b2")', "b2 outside the gate"),
-    ("attn-bias-ungated", "oracle/dit.py", 'r = r + g1 * (_unheads(o) @ P.layer(l, "o_w") + P.layer(l, "o_b"))',
-     'r = r + g1 * (_unheads(o) @ P.layer(l, "o_w")) + P.layer(l, "o_b")', "o_b outside the gate"),
-    ("cross-gated", "oracle/dit.py", 'r = r + (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))',
-     'r = r + g1 * (_unheads(oc) @ P.layer(l, "co_w") + P.layer(l, "co_b"))', "cross-attention gated by g1"),
+    ("mlp-bias-ungated", "oracle/dit.py", 'r = r + g2 * (act(a) @ wgt(l, "w2") + P.layer(l, "b2"))',
+     'r = r + g2 * (act(a) @ wgt(l, "w2")) + P.layer(l, "b2")', "b2 outside the gate"),
+    ("attn-bias-ungated", "oracle/dit.py", 'r = r + g1 * (act(_unheads(o)) @ wgt(l, "o_w") + P.layer(l, "o_b"))',
+     'r = r + g1 * (act(_unheads(o)) @ wgt(l, "o_w")) + P.layer(l, "o_b")', "o_b outside the gate"),
+    ("cross-gated", "oracle/dit.py", 'r = r + (act(_unheads(oc)) @ wgt(l, "co_w") + P.layer(l, "co_b"))',
+     'r = r + g1 * (act(_unheads(oc)) @ wgt(l, "co_w") + P.layer(l, "co_b"))', "cross-attention gated by g1"),
     ("cross-modulated", "oracle/dit.py", 'hc = rms_norm(r, eps) * P.layer(l, "g_n3")',
      'hc = (rms_norm(r, eps) * (1.0 + sc1) + sh1) * P.layer(l, "g_n3")', "cross pre-norm modulated"),
     ("cross-no-gain", "oracle/dit.py", 'hc = rms_norm(r, eps) * P.layer(l, "g_n3")',
