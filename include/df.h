@@ -44,10 +44,11 @@ typedef enum {
 } df_status;
 
 typedef enum { DF_E = 0, DF_T = 1, DF_D = 2 } df_stage;
-/* df_graph.precision.  DF_FP8 (NEXT-4, R29): bf16 everywhere except the three GEMMs
- * fed by a normalised activation (QKV, cross-Q, MLP up), which take e4m3 operands -- the
- * activation quantised per token row by the RMSNorm that produces it, the weight per tensor --
- * with fp32 accumulation; needs d >= 256 and N >= 256 latent tokens (CTA-pair tiles). */
+/* df_graph.precision.  DF_FP8 (NEXT-4, R29): the six GEMMs of every block (QKV, O,
+ * cross-Q, cross-O, MLP up, MLP down) take e4m3 operands -- activations quantised per token row
+ * with power-of-two scales (by the RMSNorm that produces them, or a row quantiser for the
+ * attention and SwiGLU outputs), weights per tensor -- with fp32 accumulation; everything else
+ * as DF_BF16.  Needs d >= 256, a head size of 128 and N >= 256 latent tokens (CTA-pair tiles). */
 enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1, DF_FP8 = 2 };
 enum { DF_ASYNC = 0, DF_SYNC = 1, DF_PERMUTE = 2, DF_HASH = 4, DF_LATENT_BLOCKS = 8 }; /* handoff flags */
 #define DF_ALL_CHUNKS 0xFFFFFFFFu

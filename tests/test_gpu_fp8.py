@@ -82,6 +82,7 @@ def test_gemm_e4m3_rejects_bad_shapes(ctx):
 
 
 # ---------------------------------------------------------------- FP8 step mode (R29)
+TOL_FP8_STEP = 2.5e-2  # DESIGN.md R29: code flips between two roundings of the same activation
 def _fp8_step(cfg, prec, x, ctx_bits, i):
     from oracle import dit
     from gpu_util import bf16_tensor_from_bits, make_ctx
@@ -98,12 +99,13 @@ def _fp8_step(cfg, prec, x, ctx_bits, i):
 
 @pytest.mark.parametrize("i", [0, 5])
 def test_fp8_step_matches_the_fp8_oracle(i):
-    """NEXT-4 in the DiT step (R29): QKV, cross-Q and MLP-up on e4m3 operands (activation per
-    row from the RMSNorm kernel, weight per tensor), the rest bf16.  Against the fp64 oracle
-    of the same FP8 mode the step is within the bf16 step tolerance (1e-2): both quantise the
-    same fp32-rounded activations, so codes differ only where the two sides' activations round
-    to different sides of an e4m3 boundary.  Against the bf16 oracle it differs by the
-    quantisation itself (reported, bounded by 0.1)."""
+    """NEXT-4 in the DiT step (R29): all six block GEMMs on e4m3 operands (activations per row,
+    weights per tensor), the rest bf16.  Against the fp64 oracle of the same FP8 mode the step
+    is within R29's derived tolerance 2.5e-2: the two sides quantise activations that differ by
+    their own rounding (~3e-3 relative), so ~3 % of the codes land one e4m3 step (~9 %) apart,
+    a ~1.6 % perturbation of each GEMM input.  Against the bf16 oracle it differs by the
+    quantisation itself (reported; larger than the parity error, so the mode is not a silent
+    bf16 run)."""
     from oracle import dit, dit_fp8
     from oracle import params as OP
     from synth import inputs
@@ -119,10 +121,11 @@ def test_fp8_step_matches_the_fp8_oracle(i):
     cond = dit.prologue(P, cfg, inputs.bf16_bits_to_f64(ctx_bits), sig)
     ox8, ov8 = dit_fp8.step(P, cfg, x.astype(np.float64), i, cond, sig)
     ox, ov = dit.step(P, cfg, x.astype(np.float64), i, cond, sig)
-    assert rel_l2(gv, ov8) <= 1e-2, rel_l2(gv, ov8)
-    assert rel_l2(gx, ox8) <= 1e-2
-    q_err = rel_l2(ov8, ov)
-    assert 1e-3 < q_err < 0.1, q_err            # the FP8 mode is not a silent bf16 run
+    err, q_err = rel_l2(gv, ov8), rel_l2(ov8, ov)
+    print(f"fp8 step i={i}: GPU vs FP8 oracle {err:.3e}, FP8 oracle vs bf16 oracle {q_err:.3e}")
+    assert err <= TOL_FP8_STEP, err
+    assert rel_l2(gx, ox8) <= TOL_FP8_STEP
+    assert err < q_err < 0.2, (err, q_err)     # the FP8 mode is not a silent bf16 run
     assert rel_l2(gv, ov) > 0.5 * q_err
 
 

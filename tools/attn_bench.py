@@ -1,6 +1,6 @@
 """Attention microbenchmark through df_op_attention (no model): TFLOP/s of the tcgen05
-flash-attention kernel at the workload shapes.  Variants are selected by env vars
-(DF_ATTN_IMPL, DF_ATTN_POLY) read once per process.
+flash-attention kernel at the workload shapes.  DF_ATTN_IMPL=2 (read once per process)
+selects the attn_tc2 A/B kernel instead of the default persistent attn_pp at dh = 128.
 
     python tools/attn_bench.py --shape video
 """
@@ -58,7 +58,7 @@ def main():
         err = ((got - ref).norm() / ref.norm()).item()
         fl = 4.0 * H * Nq * Nk * dh
         best = min(ms)
-        print({"shape": a.shape, "H": H, "impl": os.environ.get("DF_ATTN_IMPL", "default"), "poly": os.environ.get("DF_ATTN_POLY", "default"),
+        print({"shape": a.shape, "H": H, "impl": os.environ.get("DF_ATTN_IMPL", "default"),
                "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
                "rel_l2_vs_torch": f"{err:.2e}"})
         if a.lib:  # library reference point (not on the product path)
