@@ -319,6 +319,14 @@ df_status df_sched_log(df_ctx* ctx, df_sched_event* out, uint32_t max, uint32_t*
  * whether they arrived in order.  For the CPU multi-process tests. */
 df_status df_ring_selftest(const char* name, int32_t role, uint64_t n, uint64_t* checksum, int32_t* fifo_ok);
 
+/* The chunk plan of a pipeline edge (host logic, no GPU; R22): edge 0 = the E->T
+ * payload of `bytes` bytes in whole ctx rows, edge 1 = the fp32 latent in latent blocks, with
+ * the graph's chunk_bytes[edge].  Writes up to `max` pieces: chunk k covers `height` rows of
+ * `width` bytes starting at byte `off`, rows `pitch` bytes apart (height 1 for byte ranges);
+ * *n = the chunk count.  DF_ERR_INVALID on a null argument or an edge other than 0 / 1. */
+df_status df_chunk_plan(const df_graph* g, uint32_t edge, uint64_t bytes, uint32_t* n, uint64_t* off,
+                        uint64_t* width, uint64_t* height, uint64_t* pitch, uint32_t max);
+
 /* Number of kernel launches this context issued so far (bench "gpu_launches"). */
 uint64_t df_launch_count(const df_ctx* ctx);
 

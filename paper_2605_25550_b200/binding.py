@@ -123,6 +123,9 @@ _SIGS = {
     "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
     "df_launch_count": (C.c_uint64, [C.c_void_p]),
+    "df_chunk_plan": (C.c_int, [C.POINTER(GraphC), C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                C.POINTER(C.c_uint64), C.c_uint32]),
     "df_plan_ratio": (C.c_int, [C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.c_int32,
                                 C.POINTER(C.c_uint32)]),
     "df_sched_react": (C.c_int, [C.POINTER(SchedCfgC), C.POINTER(SchedMetricsC), C.POINTER(SchedMetricsC),
@@ -229,6 +232,17 @@ def sched_react(cfg, now, prev, g):
     if st != DF_OK:
         raise DFError(st, "df_sched_react")
     return tuple(out)
+
+
+def chunk_plan(graph, edge, nbytes, max_pieces=64):
+    """The pipeline edge's chunk plan (host logic): [(off, width, height, pitch)]."""
+    lib = load()
+    n = C.c_uint32()
+    arrs = [(C.c_uint64 * max_pieces)() for _ in range(4)]
+    st = lib.df_chunk_plan(C.byref(graph), int(edge), int(nbytes), C.byref(n), *arrs, max_pieces)
+    if st != DF_OK:
+        raise DFError(st, "df_chunk_plan")
+    return [tuple(int(a[k]) for a in arrs) for k in range(min(n.value, max_pieces))]
 
 
 def sched_changed(keys):

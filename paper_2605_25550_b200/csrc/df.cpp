@@ -2142,6 +2142,23 @@ df_status df_sched_log(df_ctx* ctx, df_sched_event* out, uint32_t max, uint32_t*
   return DF_OK;
 }
 
+df_status df_chunk_plan(const df_graph* g, uint32_t edge, uint64_t bytes, uint32_t* n, uint64_t* off,
+                        uint64_t* width, uint64_t* height, uint64_t* pitch, uint32_t max) {
+  if (!g || !n || edge > 1 || (max && (!off || !width || !height || !pitch))) return DF_ERR_INVALID;
+  ChunkPlan p;
+  if (edge == 0) {
+    uint64_t row = uint64_t(g->dit.d_txt) * 2, a = 16;
+    if (!row || !bytes) return DF_ERR_INVALID;
+    while (a % row) a += 16;
+    p = plan_bytes(bytes, g->chunk_bytes[0], a);
+  } else {
+    p = plan_latent(g->dit, g->chunk_bytes[1]);
+  }
+  *n = uint32_t(p.n);
+  for (uint32_t k = 0; k < std::min<uint32_t>(max, uint32_t(p.n)); ++k) p.piece(int(k), off[k], width[k], height[k], pitch[k]);
+  return DF_OK;
+}
+
 df_status df_ring_selftest(const char* name, int32_t role, uint64_t n, uint64_t* checksum, int32_t* fifo_ok) {
   if (!name || !name[0] || (role != 0 && role != 1)) return DF_ERR_INVALID;
   std::string err;

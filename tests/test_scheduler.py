@@ -72,3 +72,38 @@ def test_change_detector_matches_oracle(B):
         if rnd.random() < 0.5 and n > 8:
             keys = [4] * (n - n // 4) + [1] * (n // 4)
         assert B.sched_changed(keys) == cap.changed(keys), keys
+
+
+def _tile_check(pieces, total):
+    """Every byte of [0, total) is covered by exactly one piece."""
+    import numpy as np
+    cover = np.zeros(total, np.int32)
+    for off, width, height, pitch in pieces:
+        for r in range(height):
+            cover[off + r * pitch: off + r * pitch + width] += 1
+    return bool(np.all(cover == 1))
+
+
+@pytest.mark.parametrize("cfg_name,chunks", [("tiny", (64, 256)), ("mid", (4096, 16384)), ("image", (524288, 131072)),
+                                             ("video", (524288, 131072)), ("image", (0, 0)), ("mid", (1000, 3000))])
+def test_chunk_plans_tile_the_payloads(B, cfg_name, chunks):
+    """R22 host logic (no GPU): the E->T plan cuts the ctx payload into whole rows, the T->D plan
+    cuts the latent into per-frame row blocks (one frame per chunk for video, 16 latent rows at
+    the image shape with 128 KiB), and both tile their payload exactly once."""
+    from synth.configs import CONFIGS
+    cfg = CONFIGS[cfg_name]
+    g = B.make_graph(cfg, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)], chunk_bytes=chunks)
+    ctx_bytes = cfg.L_txt * cfg.d_txt * 2
+    p0 = B.chunk_plan(g, 0, ctx_bytes)
+    assert _tile_check(p0, ctx_bytes)
+    row = cfg.d_txt * 2
+    assert all(w % row == 0 or off + w == ctx_bytes for off, w, h, pt in p0)   # whole rows
+    lat = cfg.C * cfg.F * cfg.H * cfg.W * 4
+    p1 = B.chunk_plan(g, 1, lat)
+    assert _tile_check(p1, lat)
+    if chunks[1] == 0:
+        assert len(p1) == 1
+    elif cfg.F > 1:
+        assert len(p1) == cfg.F and all(h == cfg.C for _, _, h, _ in p1)    # one latent frame each
+    elif cfg_name == "image":
+        assert len(p1) == 8 and p1[0][1] == 16 * cfg.W * 4                  # 16-row blocks
