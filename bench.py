@@ -356,7 +356,8 @@ def run_ours(args, cfg):
     inst = [(local if i[2] == rank else 0, i[1], i[2])
             for i in layouts.partitioned(world, args.exclusive, args.t_per_gpu)]
     shm = f"/df_bench_{os.environ.get('MASTER_PORT', '0')}_{os.getuid()}"
-    g = B.make_graph(cfg, inst, precision=B.DF_BF16, weight_seed=0,
+    prec = B.DF_FP8 if args.precision == "fp8" else B.DF_BF16
+    g = B.make_graph(cfg, inst, precision=prec, weight_seed=0,
                      chunk_bytes=(args.chunk_ctx, args.chunk_lat), n_slots=2,
                      handoff_mode=B.DF_ASYNC | B.DF_HASH, ring_capacity=256, max_steps=cfg.steps,
                      rank=rank, world=world, shm_name=shm if world > 1 else "")
@@ -461,11 +462,11 @@ def run_ours(args, cfg):
         s = oracle_sample(cfg)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "oracle", "sample": s["sample"]}
     video = fp8 = None
-    if world == 1 and args.config == "image" and args.video_requests > 0:
+    if world == 1 and args.config == "image" and args.video_requests > 0 and prec == B.DF_BF16:
         # the north_star's headline shape (BASELINE configs[2], C3): 1 warm-up + K timed 50-step requests
         video = sub_record(args, peaks, local, CONFIGS["video"], B.DF_BF16, 1, args.video_requests,
                            "text-to-video (C3) through the same pipeline, bf16")
-    if world == 1 and args.config == "image" and args.fp8_requests > 0:
+    if world == 1 and args.config == "image" and args.fp8_requests > 0 and prec == B.DF_BF16:
         # NEXT-4 (R29): the same image workload with the FP8 step mode (QKV, cross-Q and MLP-up
         # on e4m3 operands); dtype stays bf16 for the headline above -- this is a separate line
         fp8 = sub_record(args, peaks, local, cfg, B.DF_FP8, args.warmup, args.fp8_requests,
@@ -475,7 +476,7 @@ def run_ours(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / n_total, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic",
+        "dtype": "bf16" if prec == B.DF_BF16 else "e4m3 block GEMMs (R29), bf16 elsewhere", "data": "synthetic",
         "config": {"workload": workload_name(cfg),
                    "layout": ("E+T+D co-resident on GPU 0" if world == 1 else
                               f"stage-partitioned, one process per GPU: E on GPU 0, D on GPU {world - 1}, "
@@ -525,6 +526,8 @@ def main():
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     ap.add_argument("--video-requests", type=int, default=1,
                     help="N=1 image run: timed C3 (video) requests in the line's `video` sub-record (0: skip)")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8"],
+                    help="the headline run's DiT precision (fp8: the R29 step mode; not a bf16 number)")
     ap.add_argument("--fp8-requests", type=int, default=5,
                     help="N=1 image run: timed requests of the FP8 step mode in the line's `fp8` sub-record (0: skip)")
     ap.add_argument("--dit-steps", type=int, default=0,

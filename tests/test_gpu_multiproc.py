@@ -196,25 +196,29 @@ def _sched_worker(rank, world, port, shm, q):
 
     if rank == 0:
         assert c.set_ratio(1, 2, 1) == B.DF_OK                     # E4 (rank 1) stops pulling
-        # measure only (thresholds no tick can cross): the allocation is steered explicitly below
-        c.sched_start(B.sched_cfg(delta_s=0.05, U_high=1.5, U_low=-0.5, move_budget=0))
     dist.barrier()
-    # phase A: one encoder; phase B: the controller rank scales E out to rank 1's encoder
-    for phase, seeds in (("A", list(range(100, 140))), ("B", list(range(200, 240)))):
+    # phase A: one encoder, no controller.  Phase B: the Alg. 1 controller on rank 0 with a
+    # hair-trigger scale-out rule (u > 0, q > 0, d rising) sees the encoder queue of a request
+    # burst and scales E out -- to the encoder hosted by rank 1.  Phase C: back to one encoder
+    # by an explicit df_set_ratio.
+    for phase, seeds in (("A", list(range(100, 140))), ("B", list(range(200, 400))), ("C", list(range(500, 540)))):
         if rank == 0:
             if phase == "B":
-                assert c.set_ratio(2, 2, 1) == B.DF_OK
-            for s in seeds:
+                c.sched_start(B.sched_cfg(delta_s=0.02, U_high=0.0, U_low=-1.0, Q_high=0, move_budget=0))
+            if phase == "C":
+                c.sched_stop()
+                assert c.set_ratio(1, 2, 1) == B.DF_OK
+            for k, s in enumerate(seeds):
                 while c.submit(TINY.steps, TINY.shift, s, user_tag=s)[0] != B.DF_OK:
                     time.sleep(0.001)
+                if phase == "B" and k % 25 == 24:
+                    time.sleep(0.01)  # spread the burst over several controller ticks
         if rank == 1:
             res[phase] = drain(len(seeds))
         dist.barrier()
     if rank == 0:
-        time.sleep(0.2)
-        c.sched_stop()
         log = c.sched_log()
-        res["log"] = [(e.action, tuple(e.g), tuple(e.m.u), tuple(e.m.q)) for e in log]
+        res["log"] = [(e.action, e.stage, tuple(e.g), tuple(e.m.u), tuple(e.m.q)) for e in log]
     objs = [None, None]
     dist.all_gather_object(objs, res)
     if rank == 0:
@@ -226,10 +230,10 @@ def _sched_worker(rank, world, port, shm, q):
 
 def test_two_process_controller_and_encoder_scale_out():
     """NEXT-1 across processes (P:L326-357 on the one-process-per-GPU path): the request ring,
-    the allocation g_s and every instance's busy time live in the shared plane.  Rank 0's
-    df_set_ratio activates an encoder hosted by rank 1 (E scale-out): afterwards
-    requests submitted on rank 0 are encoded on both ranks.  The Alg. 1 controller runs on rank
-    0 and measures utilisation and queues of all instances, rank 1's included; no request is
+    the allocation g_s and every instance's busy time live in the shared plane.  The Alg. 1
+    controller on rank 0 measures all instances (rank 1's D included) and, when the encoder
+    queue builds up, scales E out to the encoder hosted by rank 1, which then pulls
+    requests submitted on rank 0; an explicit df_set_ratio scales it back in.  No request is
     lost and every handoff hash matches."""
     import torch.multiprocessing as mp
     ctxm = mp.get_context("spawn")
@@ -243,14 +247,15 @@ def test_two_process_controller_and_encoder_scale_out():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    a, b = res["A"], res["B"]
-    assert sorted(x[0] for x in a) == list(range(100, 140)) and sorted(x[0] for x in b) == list(range(200, 240))
-    assert all(x[2] for x in a + b)
-    assert {x[1] for x in a} == {0}                               # one encoder
-    assert {x[1] for x in b} == {0, 4}                            # scaled out to rank 1's encoder
+    a, b, cc = res["A"], res["B"], res["C"]
+    assert sorted(x[0] for x in a) == list(range(100, 140)) and sorted(x[0] for x in b) == list(range(200, 400))
+    assert sorted(x[0] for x in cc) == list(range(500, 540))
+    assert all(x[2] for x in a + b + cc)
+    assert {x[1] for x in a} == {0} and {x[1] for x in cc} == {0}   # one encoder
+    assert 4 in {x[1] for x in b}                                  # the controller scaled out to rank 1's encoder
     log = res["log"]
-    assert len(log) >= 3
-    for action, g, u, qq in log:
+    assert any(act == 1 and st == 0 for act, st, _, _, _ in log)   # logged as an E scale-out
+    for action, st, g, u, qq in log:
         assert min(g) >= 1 and g[0] <= 2 and g[1] <= 2 and g[2] == 1
         assert all(0.0 <= x <= 1.0 for x in u)
-    assert any(u[2] > 0 for _, _, u, _ in log)                    # the D on rank 1 is seen as busy
+    assert any(u[2] > 0 for _, _, _, u, _ in log)                 # the D on rank 1 is seen as busy
