@@ -301,6 +301,7 @@ struct df_ctx {
   std::mutex view_mu;
   struct View {
     bool open = false, remote = false;
+    uint32_t gen = 0;         // the consumer's publication this view was opened at
     uint64_t slot_bytes = 0;  // payload capacity; the 64-byte trailer follows
     void* buf[PL_MAX_SLOTS] = {};
     cudaEvent_t consumed[PL_MAX_SLOTS] = {};
@@ -722,10 +723,32 @@ uint64_t busy_sample(df_ctx* ctx, int i, double t) {
   return b;
 }
 
+// Routing: the instances of each stage in order (the first active[s] receive new work).  One
+// process: ctx->by_stage under route_mu.  One process per GPU: the lists live in the shared
+// plane (re-purposing changes them), under a spin lock.
+std::vector<int> route_of(df_ctx* ctx, int s) {
+  if (ctx->mp) {
+    PlaneSeg* g = ctx->seg;
+    SpinLock lk(g->route_lock);
+    return std::vector<int>(g->route[s], g->route[s] + g->route_n[s]);
+  }
+  std::lock_guard<std::mutex> lk(ctx->route_mu);
+  return ctx->by_stage[s];
+}
+
 // Round-robin over the active instances of a stage by request sequence number (deterministic).
-// hold: the caller will hand the chosen instance a job later (single-process workers); the
-// instance cannot finish retiring until that hand-over (release_pick) happened.
+// hold: the caller will hand the chosen instance a job later; the instance cannot finish
+// retiring until that hand-over (release_pick) happened.
 int pick(df_ctx* ctx, int stage, uint64_t seq, bool hold = false) {
+  if (ctx->mp) {
+    PlaneSeg* g = ctx->seg;
+    SpinLock lk(g->route_lock);
+    const int n = std::min<int>(g->active[stage].load(), g->route_n[stage]);
+    if (n <= 0) return -1;
+    const int id = g->route[stage][seq % uint64_t(n)];
+    if (hold) g->inst[id].inflight++;
+    return id;
+  }
   std::lock_guard<std::mutex> lk(ctx->route_mu);
   int n = active_of(ctx, stage).load();
   auto& v = ctx->by_stage[stage];
@@ -734,8 +757,41 @@ int pick(df_ctx* ctx, int stage, uint64_t seq, bool hold = false) {
   if (hold) ctx->inst[id]->inflight_in++;
   return id;
 }
-void release_pick(Inst* I) {
+void release_pick(df_ctx* ctx, Inst* I) {
+  if (ctx->mp) {
+    ctx->seg->inst[I->id].inflight--;
+    return;
+  }
   if (I->inflight_in.fetch_sub(1) == 1) I->inbox.cv.notify_all();
+}
+int inflight_of(df_ctx* ctx, const Inst* I) {
+  return ctx->mp ? ctx->seg->inst[I->id].inflight.load() : I->inflight_in.load();
+}
+
+// Take instance id out of stage s's routing (no new picks after this returns) / add it back.
+void route_remove(df_ctx* ctx, int s, int id) {
+  if (ctx->mp) {
+    PlaneSeg* g = ctx->seg;
+    SpinLock lk(g->route_lock);
+    int n = 0;
+    for (int k = 0; k < g->route_n[s]; ++k)
+      if (g->route[s][k] != id) g->route[s][n++] = g->route[s][k];
+    g->route_n[s] = n;
+    g->active[s] = std::min<int>(g->active[s].load(), n);
+  }
+  std::lock_guard<std::mutex> lk(ctx->route_mu);
+  auto& v = ctx->by_stage[s];
+  v.erase(std::remove(v.begin(), v.end(), id), v.end());
+  ctx->active[s] = std::min<int>(ctx->active[s].load(), int(v.size()));
+}
+void route_add(df_ctx* ctx, int s, int id) {
+  if (ctx->mp) {
+    PlaneSeg* g = ctx->seg;
+    SpinLock lk(g->route_lock);
+    g->route[s][g->route_n[s]++] = id;
+  }
+  std::lock_guard<std::mutex> lk(ctx->route_mu);
+  ctx->by_stage[s].push_back(id);
 }
 
 // Stage-time profile for the Eq. 6 planner: EMA of seconds per request per instance, keyed by
@@ -882,8 +938,7 @@ cudaError_t encode_request(df_ctx* ctx, Inst* me, ReqState* rs, int b) {
 // Whether instance I is in the active prefix of its stage's routing list (E instances pull
 // from the shared request ring, so an encoder beyond g_E must stop pulling by itself).
 bool routed(df_ctx* ctx, const Inst* I) {
-  std::lock_guard<std::mutex> lk(ctx->route_mu);
-  const auto& v = ctx->by_stage[I->stage];
+  const std::vector<int> v = route_of(ctx, I->stage);
   const int n = std::min<int>(active_of(ctx, I->stage).load(), int(v.size()));
   for (int k = 0; k < n; ++k)
     if (v[k] == I->id) return true;
@@ -954,7 +1009,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
     me->served++;
     sched_note(ctx, 0, 0u, (rs->t_end[0] - rs->t_start[0]) - (tw1 - tw));
     T->inbox.push(Job{rs});  // E moves on immediately
-    release_pick(T);
+    release_pick(ctx, T);
   }
   me->busy.end(now_s());
   cudaStreamSynchronize(me->comm);  // its send buffers are read until the last copy landed
@@ -973,7 +1028,7 @@ void t_finish(df_ctx* ctx, Inst* me, ReqState* rs, Inst* D) {
   me->served++;
   sched_note(ctx, 1, rs->req.steps, dev_s);
   D->inbox.push(Job{rs});
-  release_pick(D);
+  release_pick(ctx, D);
 }
 
 // One T instance.  The host enqueues request r's whole prologue + S steps + T->D send,
@@ -1199,12 +1254,23 @@ void mp_sleep() { std::this_thread::sleep_for(std::chrono::microseconds(20)); }
 df_ctx::View* mp_view(df_ctx* ctx, int ci) {
   df_ctx::View& v = ctx->views[ci];
   std::lock_guard<std::mutex> lk(ctx->view_mu);
-  if (v.open) return &v;
   InstPlane& ip = ctx->seg->inst[ci];
   while (ip.ready.load(std::memory_order_acquire) == 0) {
     if (ctx->stop) return nullptr;
     mp_sleep();
   }
+  const uint32_t gen = ip.gen.load(std::memory_order_acquire);
+  if (v.open && v.gen == gen) return &v;
+  if (v.open && v.remote) {  // the consumer was re-created: drop the stale mappings
+    for (uint32_t s = 0; s < uint32_t(PL_MAX_SLOTS); ++s) {
+      if (v.buf[s]) cudaIpcCloseMemHandle(v.buf[s]);
+      if (v.consumed[s]) cudaEventDestroy(v.consumed[s]);
+      v.buf[s] = nullptr, v.consumed[s] = nullptr;
+    }
+  }
+  v.open = false;
+  v.remote = false;
+  v.gen = gen;
   Inst* I = ctx->inst[ci].get();
   v.slot_bytes = ip.slot_bytes;
   for (uint32_t s = 0; s < ip.n_slots; ++s) {
@@ -1224,6 +1290,8 @@ df_ctx::View* mp_view(df_ctx* ctx, int ci) {
 // Publish a local consumer instance's slots and consumed events into the plane.
 cudaError_t mp_publish(df_ctx* ctx, Inst& I, size_t slot_bytes) {
   InstPlane& ip = ctx->seg->inst[I.id];
+  ip.free_slots.init();  // (a re-purposed instance publishes afresh; nothing is in flight to it)
+  ip.inbox.init();
   ip.n_slots = ctx->g.n_slots;
   ip.slot_bytes = slot_bytes;
   ip.nchunks_max = PL_MAX_CHUNKS;
@@ -1236,6 +1304,7 @@ cudaError_t mp_publish(df_ctx* ctx, Inst& I, size_t slot_bytes) {
   DF_TRY(cudaStreamSynchronize(I.compute));
   for (uint32_t s = 0; s < ctx->g.n_slots; ++s)
     while (!ip.free_slots.push(s)) mp_sleep();
+  ip.gen.fetch_add(1);
   ip.ready.store(1, std::memory_order_release);
   return cudaSuccess;
 }
@@ -1360,9 +1429,13 @@ bool mp_post(df_ctx* ctx, int ci, const MetaRec& m) {
 
 bool mp_try_recv(df_ctx* ctx, Inst* me, MetaRec& m) { return ctx->seg->inst[me->id].inbox.pop(m); }
 
+// Blocks for the next record; false on stop, or when this instance is retiring and nothing
+// can still arrive (no producer holds a pick of it).
 bool mp_recv(df_ctx* ctx, Inst* me, MetaRec& m) {
   while (!mp_try_recv(ctx, me, m)) {
     if (ctx->stop) return false;
+    if (me->retire.load() && ctx->seg->inst[me->id].inflight.load() == 0 && !mp_try_recv(ctx, me, m)) return false;
+    if (me->retire.load() && ctx->seg->inst[me->id].inflight.load() == 0) return true;
     mp_sleep();
   }
   return true;
@@ -1386,7 +1459,7 @@ cudaError_t mp_finish_slot(df_ctx* ctx, Inst* me, RecvClock& rc, uint32_t s, uin
 void mp_e_worker(df_ctx* ctx, Inst* me) {
   cudaSetDevice(me->device);
   ReqRec q;
-  while (!ctx->stop.load()) {
+  while (!ctx->stop.load() && !me->retire.load()) {
     if (!routed(ctx, me) || !ctx->seg->requests.pop(q)) {  // only encoders in the active prefix pull
       mp_sleep();
       continue;
@@ -1418,7 +1491,7 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
     m.t_submit = rs->t_submit;
     m.t_start_e = now_s();
     me->busy.begin(m.t_start_e);
-    const int tid = pick(ctx, DF_T, rs->seq);
+    const int tid = pick(ctx, DF_T, rs->seq, true);
     int b = me->enext;
     me->enext ^= 1;
     WK(cudaStreamWaitEvent(me->compute, me->esent[b], 0));
@@ -1435,7 +1508,9 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
       return;
     }
     WK(cudaEventRecord(me->esent[b], me->comm));
-    if (!mp_post(ctx, tid, m)) {  // E moves on immediately
+    const bool posted = mp_post(ctx, tid, m);  // E moves on immediately
+    release_pick(ctx, ctx->inst[tid].get());
+    if (!posted) {
       free_req(rs);
       return;
     }
@@ -1476,7 +1551,9 @@ bool mp_t_finish(df_ctx* ctx, Inst* me, MpTReq& r, int b) {
   sched_note(ctx, 1, o.steps, o.stage_ms_t * 1e-3);
   me->served++;
   r.live = false;
-  return mp_post(ctx, r.did, o);
+  const bool posted = mp_post(ctx, r.did, o);
+  release_pick(ctx, ctx->inst[r.did].get());
+  return posted;
 }
 
 void mp_t_worker(df_ctx* ctx, Inst* me) {
@@ -1547,7 +1624,7 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
     r.out = m;
     r.out.inst_t = me->id;
     r.out.t_start_t = ts;
-    r.did = pick(ctx, DF_D, m.seq);
+    r.did = pick(ctx, DF_D, m.seq, true);
     if (!mp_send(ctx, me, r.did, x, lplan, me->compute, lplan.n > 1 ? me->hb_ev[b] : nullptr, r.out, 1)) return;
     WK(cudaEventRecord(me->xsent[b], me->comm));
     r.live = true;
@@ -1683,7 +1760,9 @@ void mp_d_worker(df_ctx* ctx, Inst* me) {
       }
     }
     if (!did) {
-      if (ctx->stop.load() && live.empty()) break;
+      if (live.empty() && (ctx->stop.load() || (me->retire.load() && ctx->seg->inst[me->id].inflight.load() == 0 &&
+                                                ctx->seg->inst[me->id].inbox.size_approx() == 0)))
+        break;
       mp_sleep();
     }
   }
@@ -1812,15 +1891,18 @@ void inst_start(df_ctx* ctx, Inst* I) {
 // drain and cold-start times.
 cudaError_t inst_repurpose(df_ctx* ctx, Inst* I, int stage, double& drain_s, double& cold_s) {
   const double t0 = now_s();
-  {
-    std::lock_guard<std::mutex> lk(ctx->route_mu);
-    auto& v = ctx->by_stage[I->stage];
-    v.erase(std::remove(v.begin(), v.end(), I->id), v.end());
-    ctx->active[I->stage] = std::min<int>(ctx->active[I->stage].load(), int(v.size()));
-  }
+  route_remove(ctx, I->stage, I->id);
   I->retire = true;
   I->inbox.cv.notify_all();
   if (I->worker.joinable()) I->worker.join();
+  if (ctx->mp) {  // withdraw the posted destination addresses; producers re-open on the next publication
+    InstPlane& ip = ctx->seg->inst[I->id];
+    ip.ready.store(0, std::memory_order_release);
+    cudaSetDevice(I->device);
+    cudaDeviceSynchronize();
+    for (auto& e : I->ipc_consumed)
+      if (e) cudaEventDestroy(e), e = nullptr;
+  }
   inst_free(*I);
   const double t1 = now_s();
   I->stage = stage;
@@ -1828,10 +1910,7 @@ cudaError_t inst_repurpose(df_ctx* ctx, Inst* I, int stage, double& drain_s, dou
   if (e != cudaSuccess) return e;
   const double t2 = now_s();
   inst_start(ctx, I);
-  {
-    std::lock_guard<std::mutex> lk(ctx->route_mu);
-    ctx->by_stage[stage].push_back(I->id);
-  }
+  route_add(ctx, stage, I->id);
   drain_s = t1 - t0;
   cold_s = t2 - t1;
   return cudaSuccess;
@@ -2004,11 +2083,7 @@ void sched_loop(df_ctx* ctx) {
     uint32_t g[3];
     for (int s = 0; s < 3; ++s) g[s] = uint32_t(active_of(ctx, s).load());
     for (int s = 0; s < 3; ++s) {
-      std::vector<int> ids;
-      {
-        std::lock_guard<std::mutex> lk(ctx->route_mu);
-        ids = ctx->by_stage[s];
-      }
+      const std::vector<int> ids = route_of(ctx, s);
       double busy = 0;
       for (size_t j = 0; j < ids.size(); ++j) {
         const uint64_t b = busy_sample(ctx, ids[j], t);
@@ -2043,15 +2118,9 @@ void sched_loop(df_ctx* ctx) {
       // stages when a stage needs more than it has (single process); across processes the
       // allocation stays within each stage's instances (activation / deactivation only)
       const uint32_t G = c.G ? std::min<uint32_t>(c.G, uint32_t(ctx->inst.size())) : uint32_t(ctx->inst.size());
-      uint32_t capn[3];
-      {
-        std::lock_guard<std::mutex> lk(ctx->route_mu);
-        for (int s = 0; s < 3; ++s) capn[s] = uint32_t(ctx->by_stage[s].size());
-      }
       uint32_t tgt[3];
-      if (ok && plan_ratio(G, T, g, c.move_budget, ctx->mp ? capn : nullptr, tgt) &&
-          std::memcmp(tgt, g, sizeof(g)) != 0) {
-        df_set_ratio(ctx, tgt[0], tgt[1], tgt[2]);
+      if (ok && plan_ratio(G, T, g, c.move_budget, nullptr, tgt) && std::memcmp(tgt, g, sizeof(g)) != 0 &&
+          df_set_ratio(ctx, tgt[0], tgt[1], tgt[2]) == DF_OK) {
         ev.action = 3;
         std::memcpy(ev.g, tgt, sizeof(tgt));
         reconf = true;
@@ -2066,12 +2135,7 @@ void sched_loop(df_ctx* ctx) {
       uint32_t ng[3] = {g[0], g[1], g[2]};
       const uint32_t hosts = uint32_t(ctx->inst.size());
       for (int s = 0; s < 3 && ev.action == 0; ++s) {
-        size_t have;
-        {
-          std::lock_guard<std::mutex> lk(ctx->route_mu);
-          have = ctx->by_stage[s].size();
-        }
-        if (dlt[s] > 0 && ng[0] + ng[1] + ng[2] < hosts && (!ctx->mp || ng[s] < have)) {
+        if (dlt[s] > 0 && ng[0] + ng[1] + ng[2] < hosts) {
           ng[s]++;
           ev.action = 1;
           ev.stage = s;
@@ -2081,7 +2145,10 @@ void sched_loop(df_ctx* ctx) {
           ev.stage = s;
         }
       }
-      if (ev.action) df_set_ratio(ctx, ng[0], ng[1], ng[2]);
+      if (ev.action && df_set_ratio(ctx, ng[0], ng[1], ng[2]) != DF_OK) {  // e.g. no local donor (one process per GPU)
+        ev.action = 0;
+        std::memcpy(ng, g, sizeof(g));
+      }
       std::memcpy(ev.g, ng, sizeof(ng));
     }
     prev = m;
@@ -2297,10 +2364,17 @@ df_status df_init(const df_graph* g, df_ctx** out) {
   }
   for (int s = 0; s < 3; ++s) ctx->active[s] = int(ctx->by_stage[s].size());
   if (mp) {
-    for (int s = 0; s < 3; ++s) {  // every rank proposes the same initial g_s; the first one sets it
-      int32_t z = 0;
-      ctx->seg->active[s].compare_exchange_strong(z, int32_t(ctx->by_stage[s].size()));
+    PlaneSeg* pg = ctx->seg;
+    uint32_t z0 = 0;
+    if (pg->route_state.compare_exchange_strong(z0, 1u)) {  // every rank derives the same routing: the first writes it
+      for (int s = 0; s < 3; ++s) {
+        pg->route_n[s] = int32_t(ctx->by_stage[s].size());
+        for (size_t k = 0; k < ctx->by_stage[s].size(); ++k) pg->route[s][k] = ctx->by_stage[s][k];
+        pg->active[s] = int32_t(ctx->by_stage[s].size());
+      }
+      pg->route_state.store(2u, std::memory_order_release);
     }
+    while (pg->route_state.load(std::memory_order_acquire) != 2u) std::this_thread::sleep_for(std::chrono::milliseconds(1));
     for (auto& ip : ctx->inst)
       if (ip->local) ip->busy.mirror = &ctx->seg->stat[ip->id];
   }
@@ -2486,27 +2560,32 @@ df_status df_set_ratio(df_ctx* ctx, uint32_t gE, uint32_t gT, uint32_t gD) {
   if (g[0] < 1 || g[1] < 1 || g[2] < 1 || g[0] + g[1] + g[2] > G)  // Eq. 1
     return fail(ctx, "df_set_ratio: capacity (every g_s >= 1, sum g <= G)", DF_ERR_CAPACITY);
   int have[3];
-  {
-    std::lock_guard<std::mutex> rl(ctx->route_mu);
-    for (int s = 0; s < 3; ++s) have[s] = int(ctx->by_stage[s].size());
-  }
+  for (int s = 0; s < 3; ++s) have[s] = int(route_of(ctx, s).size());
   // Stages short of instances take them from stages with a surplus (the last instances of
   // the donor's routing list, i.e. the ones beyond its active prefix first): drain ->
   // re-initialise for the new stage -> serve (Alg. 1 "Apply"; cold start P:L357).
-  // Re-purposing needs the instance in this process (single-process contexts).
+  // Across processes only an instance hosted by this process can be re-purposed here.
   for (int s = 0; s < 3; ++s) {
     while (have[s] < int(g[s])) {
+      Inst* I = nullptr;
       int donor = -1;
-      for (int t = 0; t < 3; ++t)
-        if (t != s && have[t] > int(g[t]) && (donor < 0 || have[t] - int(g[t]) > have[donor] - int(g[donor]))) donor = t;
-      if (donor < 0) return fail(ctx, "df_set_ratio: no instance to re-purpose", DF_ERR_CAPACITY);
-      if (ctx->mp) return fail(ctx, "df_set_ratio: re-purposing needs a single-process context", DF_ERR_STATE);
-      Inst* I;
-      {
-        std::lock_guard<std::mutex> rl(ctx->route_mu);
-        I = ctx->inst[ctx->by_stage[donor].back()].get();
-        ctx->active[donor] = std::min<int>(ctx->active[donor].load(), int(g[donor]));  // stop routing to it first
+      for (int pass = 0; pass < 3 && !I; ++pass) {  // the donor stage with the largest surplus first
+        int best = -1;
+        for (int t = 0; t < 3; ++t)
+          if (t != s && have[t] > int(g[t]) && (best < 0 || have[t] - int(g[t]) > have[best] - int(g[best]))) {
+            bool has_local = false;
+            for (int id : route_of(ctx, t)) has_local |= ctx->inst[id]->local;
+            if (has_local) best = t;
+          }
+        if (best < 0) break;
+        const std::vector<int> v = route_of(ctx, best);
+        for (int k = int(v.size()) - 1; k >= 0 && !I; --k)
+          if (ctx->inst[v[k]]->local) I = ctx->inst[v[k]].get(), donor = best;
       }
+      if (!I)
+        return fail(ctx, ctx->mp ? "df_set_ratio: no instance of this process can be re-purposed"
+                                 : "df_set_ratio: no instance to re-purpose",
+                    ctx->mp ? DF_ERR_STATE : DF_ERR_CAPACITY);
       double drain_s = 0, cold_s = 0;
       cudaError_t e = inst_repurpose(ctx, I, s, drain_s, cold_s);
       if (e != cudaSuccess)

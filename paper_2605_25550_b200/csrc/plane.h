@@ -124,6 +124,8 @@ struct XferEvHandles {
 
 struct InstPlane {
   std::atomic<uint32_t> ready;  // consumer published its handles
+  std::atomic<uint32_t> gen;    // bumped each time the consumer (re)publishes (producers re-open their views)
+  std::atomic<int32_t> inflight;  // producers (any rank) that picked this instance and have not posted yet
   uint32_t n_slots, nchunks_max;
   uint64_t slot_bytes;          // payload capacity; each slot has a 64-byte trailer after it
   cudaIpcMemHandle_t slot_mem[PL_MAX_SLOTS];
@@ -168,6 +170,10 @@ struct PlaneSeg {
   InstPlane inst[PL_MAX_INST];
   // hybrid scheduler state shared by all ranks (one controller, any rank)
   std::atomic<int32_t> active[3];        // g_s: the first active[s] instances of stage s get new work
+  // routing shared by every rank (re-purposing changes it): instances of each stage in order
+  std::atomic<uint32_t> route_lock, route_state;  // state 0 empty, 1 being written, 2 ready
+  int32_t route_n[3];
+  int32_t route[3][PL_MAX_INST];
   std::atomic<uint64_t> qd_ns[3], qd_count[3];
   InstStat stat[PL_MAX_INST];
   StageEma ema[3];

@@ -259,3 +259,77 @@ def test_two_process_controller_and_encoder_scale_out():
         assert min(g) >= 1 and g[0] <= 2 and g[1] <= 2 and g[2] == 1
         assert all(0.0 <= x <= 1.0 for x in u)
     assert any(u[2] > 0 for _, _, _, u, _ in log)                 # the D on rank 1 is seen as busy
+
+
+def _repurpose_worker(rank, world, port, shm, q):
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2605_25550_b200 import binding as B, layouts
+    from synth.configs import TINY
+    inst = layouts.partitioned(world)  # rank 0: E0, T1; rank 1: T2, D3
+    g = B.make_graph(TINY, inst, rank=rank, world=world, shm_name=shm, chunk_bytes=(64, 256))
+    c = B.Context(g)
+    dist.barrier()
+    res = {}
+    phases = (("A", None, list(range(10, 30))), ("B", (2, 1, 1), list(range(30, 50))),
+              ("C", (1, 2, 1), list(range(50, 70))))
+    for name, ratio, seeds in phases:
+        if rank == 0:
+            if ratio is not None:
+                assert c.set_ratio(*ratio) == B.DF_OK
+            for s in seeds:
+                while c.submit(TINY.steps, TINY.shift, s, user_tag=s)[0] != B.DF_OK:
+                    time.sleep(0.001)
+        if rank == 1:
+            got = []
+            while len(got) < len(seeds):
+                got += [(int(x.user_tag), tuple(int(v) for v in x.inst),
+                         all(x.hash_src[e] == x.hash_dst[e] != 0 for e in range(2)))
+                        for x in c.poll(16, timeout_ms=60000)]
+            res[name] = got
+        dist.barrier()
+    if rank == 0:
+        res["log"] = [(e.action, e.inst, e.from_stage, e.stage, e.cold_start_ms) for e in c.sched_log()]
+    objs = [None, None]
+    dist.all_gather_object(objs, res)
+    if rank == 0:
+        q.put({**objs[0], **objs[1]})
+    dist.barrier()
+    c.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_repurposing():
+    """Re-purposing on the one-process-per-GPU path ("Apply", P:L357 cold start): rank 0's
+    df_set_ratio(2, 1, 1) drains its own DiT instance T1 and re-creates it as a second encoder
+    (the shared routing stops sending it work, producers on every rank finish what they picked);
+    df_set_ratio(1, 2, 1) turns it back into a DiT instance, which re-publishes its receive slots
+    (rank 0's encoder re-opens them; rank 1's decoder keeps receiving from it).  No request is
+    lost, hashes match, and every phase serves from the instances its allocation names."""
+    import torch.multiprocessing as mp
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    shm = f"/df_gpu_{uuid.uuid4().hex[:10]}"
+    port = _port()
+    procs = [ctxm.Process(target=_repurpose_worker, args=(r, 2, port, shm, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for name, lo in (("A", 10), ("B", 30), ("C", 50)):
+        got = res[name]
+        assert sorted(x[0] for x in got) == list(range(lo, lo + 20)) and all(x[2] for x in got)
+    assert {x[1][1] for x in res["A"]} == {1, 2}                   # two DiT instances
+    assert {x[1][1] for x in res["B"]} == {2}                      # T1 is an encoder now
+    assert {x[1][0] for x in res["B"]} <= {0, 1}
+    assert {x[1][1] for x in res["C"]} == {1, 2}                   # and a DiT instance again
+    log = [e for e in res["log"] if e[0] == 4]
+    assert [(e[1], e[2], e[3]) for e in log] == [(1, 1, 0), (1, 0, 1)]
+    assert all(e[4] > 0 for e in log)
