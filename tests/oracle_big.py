@@ -2,10 +2,11 @@
 
 oracle.params.Params caches every tensor it generates; at the C2 / C3 widths and depths
 that is 34 / 135 GB of fp64.  StreamingParams is the same table and the same uniform
-recipe (oracle.params.bits_from_words on oracle.philox.stream_words), with two
-differences that change no value:
-  * the Philox words of a large tensor are generated in slices of whole blocks on a
-    process pool (stream_words(first=...)), then the recipe runs on the concatenation;
+recipe (oracle.params.bits_from_words on oracle.philox.stream_words, then
+oracle.params.bf16_bits_to_f64), with two differences that change no value:
+  * a large tensor is generated in slices of whole Philox blocks on a process pool
+    (stream_words(first=...)), each worker writing its slice's fp64 values straight into a
+    shared-memory buffer (the recipe and the conversion are element-wise);
   * per-layer tensors ("L<l>.*") are not cached: oracle.dit uses each layer weight once per
     block (and once in the prologue for the cross K/V), so memory stays at one layer.
 Calls only oracle/ (never the CUDA path)."""
@@ -13,6 +14,7 @@ from __future__ import annotations
 
 import multiprocessing as mp
 import os
+from multiprocessing import shared_memory
 
 import numpy as np
 
@@ -22,10 +24,18 @@ from oracle.philox import stream_words
 _SLICE = 1 << 24  # words per task (a multiple of 4)
 
 
-def _bits(args):
-    """bf16 bits of words [first, first + n) of tensor tid (the recipe is element-wise)."""
-    seed, first, n, tid, kind, shape, cfg = args
-    return OP.bits_from_words(stream_words(seed, n, tid, 0, first=first), kind, shape, cfg, flat=True)
+def _fill(args):
+    """fp64 values of words [first, first + n) of tensor tid, written into shared memory."""
+    seed, first, n, tid, kind, shape, cfg, shm_name, total = args
+    bits = OP.bits_from_words(stream_words(seed, n, tid, 0, first=first), kind, shape, cfg, flat=True)
+    shm = shared_memory.SharedMemory(name=shm_name)
+    try:
+        out = np.ndarray((total,), dtype=np.float64, buffer=shm.buf)
+        out[first:first + n] = OP.bf16_bits_to_f64(bits)
+        del out
+    finally:
+        shm.close()
+    return n
 
 
 class StreamingParams(OP.Params):
@@ -47,16 +57,31 @@ class StreamingParams(OP.Params):
             self._pool.join()
             self._pool = None
 
-    def bits(self, name: str) -> np.ndarray:
+    def _values(self, name: str) -> np.ndarray:
         tid, kind, shape = self._tab[name]
         n = int(np.prod(shape))
         if n <= 4 * self._slice:
-            return super().bits(name)
-        # the std of the recipe depends on the tensor's shape (fan-in), not the slice's
-        tasks = [(self.seed, f, min(self._slice, n - f), tid, kind, shape, self.cfg) for f in range(0, n, self._slice)]
-        return np.concatenate(self._pool_get().map(_bits, tasks)).reshape(shape)
+            return OP.bf16_bits_to_f64(super().bits(name))
+        shm = shared_memory.SharedMemory(create=True, size=n * 8)
+        try:
+            tasks = [(self.seed, f, min(self._slice, n - f), tid, kind, shape, self.cfg, shm.name, n)
+                     for f in range(0, n, self._slice)]
+            self._pool_get().map(_fill, tasks)
+            return np.ndarray((n,), dtype=np.float64, buffer=shm.buf).copy().reshape(shape)
+        finally:
+            shm.close()
+            shm.unlink()
+
+    def bits(self, name: str) -> np.ndarray:
+        tid, kind, shape = self._tab[name]
+        v = self._values(name)
+        return OP.f32_to_bf16_rne_bits(v.astype(np.float32)).reshape(shape)  # exact: v is bf16-valued
 
     def __getitem__(self, name: str) -> np.ndarray:
         if name.startswith("L"):
-            return OP.bf16_bits_to_f64(self.bits(name))
-        return super().__getitem__(name)
+            return self._values(name)
+        v = self._cache.get(name)
+        if v is None:
+            v = self._values(name)
+            self._cache[name] = v
+        return v
