@@ -26,6 +26,7 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
 #include "ring.h"
 #include "plane.h"
 #include "runtime.h"
@@ -47,6 +48,13 @@ struct df_xfer {
 using Xfer = df_xfer;
 
 namespace {
+
+// NVTX ranges around each stage's host-side work (header-only NVTX3: a no-op unless a tool such
+// as nsys is attached), so a timeline shows the workers next to the streams they feed.
+struct Nvtx {
+  explicit Nvtx(const char* m) { nvtxRangePushA(m); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 double now_s() {
   using namespace std::chrono;
@@ -961,6 +969,7 @@ void e_worker(df_ctx* ctx, Inst* me) {
       std::this_thread::sleep_for(std::chrono::microseconds(50));
       continue;
     }
+    Nvtx nv("E: encode + E->T handoff");
     rs->inst[0] = me->id;
     rs->t_start[0] = now_s();
     me->busy.begin(rs->t_start[0]);
@@ -1055,6 +1064,7 @@ void t_worker(df_ctx* ctx, Inst* me) {
     if (!pend && !me->inbox.pop_until(j, [&] { return ctx->stop.load() || (me->retire.load() && me->inflight_in.load() == 0); }))
       break;
     ReqState* rs = j.rs;
+    Nvtx nv("T: prologue + steps + T->D handoff");
     rs->t_start[1] = now_s();
     me->busy.begin(rs->t_start[1]);
     qd_add(ctx, 1, rs->t_start[1] - rs->t_end[0]);
@@ -1147,6 +1157,7 @@ void d_worker(df_ctx* ctx, Inst* me) {
   const ChunkPlan lplan = plan_latent(ctx->g.dit, ctx->g.chunk_bytes[1]);
   while (me->inbox.pop_until(j, [&] { return ctx->stop.load() || (me->retire.load() && me->inflight_in.load() == 0); })) {
     ReqState* rs = j.rs;
+    Nvtx nv("D: decode");
     rs->t_start[2] = now_s();
     me->busy.begin(rs->t_start[2]);
     qd_add(ctx, 2, rs->t_start[2] - rs->t_end[1]);
@@ -1489,6 +1500,7 @@ void mp_e_worker(df_ctx* ctx, Inst* me) {
     m.inst_e = me->id;
     m.flags = rs->req.out_host ? 1u : 0u;  // bit0: deliver the decoded output
     m.t_submit = rs->t_submit;
+    Nvtx nv("E: encode + E->T handoff (multi-process)");
     m.t_start_e = now_s();
     me->busy.begin(m.t_start_e);
     const int tid = pick(ctx, DF_T, rs->seq, true);
@@ -1575,6 +1587,7 @@ void mp_t_worker(df_ctx* ctx, Inst* me) {
       continue;
     }
     if (pend < 0 && !mp_recv(ctx, me, m)) break;
+    Nvtx nv("T: prologue + steps + T->D handoff (multi-process)");
     const double ts = now_s();
     me->busy.begin(ts);
     const int S = int(m.steps);
@@ -1720,6 +1733,7 @@ void mp_d_worker(df_ctx* ctx, Inst* me) {
     MetaRec m;
     if (int(live.size()) < K && mp_try_recv(ctx, me, m)) {
       did = true;
+      Nvtx nv("D: decode (multi-process)");
       const int k = next;
       next = (next + 1) % K;
       MpDReq& r = q[k];
