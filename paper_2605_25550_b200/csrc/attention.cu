@@ -763,6 +763,346 @@ static cudaError_t launch_attn_pp(const bf16* Q, const bf16* K, const bf16* V, b
   return launch_ex((const void*)kern, grid, dim3(ATTN3_THREADS), SMEM, st, args);
 }
 
+// ------------------------------------------------------------------ attn_sk: short keys (cross-attention)
+// For 257 <= N_kv <= 512 (the text cross-attention of every config, N_kv = L_txt = 512; SURVEY
+// §8(a) a8), where attn_pp's items are only four dependent QK^T -> softmax -> PV links long and
+// the two query tiles of an item reach their epilogues together (ncu: 38.5 % tensor-active on
+// the image shape).  Structure:
+//  * K and V of a head stay resident in shared memory (per CTA of the pair: 4 x 64 keys x dh
+//    of K, 4 x 128 keys x 64 dh of V = 128 KB), loaded once per head segment; a block's
+//    buffer is refilled for the next head as soon as the old head's last QK / PV that reads it
+//    completes, so a head change costs no pipeline drain;
+//  * each CTA pair walks a contiguous, balanced range of (head, 256-query tile) units (one
+//    query tile in flight, Q double-buffered);
+//  * TMEM: S0, S1 (128 columns each: the S ring, depth 2) and O0, O1 (the accumulator of tile
+//    n lives in O[n & 1]), so QK^T of block b + 2 is issued right after PV of block b and
+//    tile n + 1 accumulates while tile n is normalised and stored;
+//  * 16 softmax warps, four threads per query row (each owns 32 key columns of every block;
+//    the row max is exchanged through shared memory), so one block's softmax is a short
+//    chain; PV of key quarter u starts as soon as the four warps owning it published P;
+//  * 4 epilogue warps normalise and store O, off the softmax warps' critical path.
+// Lazy rescale (threshold 2^8) and the polynomial quarter of the exponentials as in attn_pp.
+constexpr int ATTN_SK_THREADS = 22 * 32;
+struct AttnSkCfg {
+  static constexpr int DH = 128;
+  static constexpr int ATOM = 64 * 128;
+  static constexpr int Q_BYTES = 2 * 128 * 128;      // one CTA's 128 query rows (2 dh atoms)
+  static constexpr int K_BYTES = 64 * 128 * 2;       // half K block: 64 keys x 128 dh
+  static constexpr int V_BYTES = 128 * 64 * 2;       // half V block: 128 keys x 64 dh
+  static constexpr int NKB = 4;                      // resident key blocks (N_kv <= 512)
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + NKB * K_BYTES;
+  static constexpr int OFF_Q = OFF_V + NKB * V_BYTES;
+  static constexpr int OFF_BAR = OFF_Q + 2 * Q_BYTES;
+  static constexpr int OFF_RED = OFF_BAR + 512;       // [2 block parity][4 col group][128 rows] row max
+  static constexpr int OFF_LRED = OFF_RED + 4096;     // [2 tile parity][4 col group][128 rows] row sum
+  static constexpr int SMEM = OFF_LRED + 4096 + 1024;
+  static constexpr uint32_t S_COL = 0, O_COL = 256;
+};
+
+template <int EXPM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
+    attn_sk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
+                   float scale_log2, int Hs) {
+  using Cfg = AttnSkCfg;
+  constexpr int DH = Cfg::DH;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint8_t* sQ = smem + Cfg::OFF_Q;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* q_full = bars + 0;        // [2]  leader (both CTAs' bytes)
+  uint64_t* q_empty = bars + 2;       // [2]  both (commit after the tile's last QK)
+  uint64_t* k_full = bars + 4;        // [4]  leader
+  uint64_t* k_empty = bars + 8;       // [4]  both (commit after the head segment's last QK of the block)
+  uint64_t* v_full = bars + 12;       // [4]  leader
+  uint64_t* v_empty = bars + 16;      // [4]  both
+  uint64_t* s_full = bars + 20;       // [2]  both
+  uint64_t* pv_done = bars + 22;      // [2]  both (per PV block, read only by a rescale)
+  uint64_t* o_done = bars + 24;       // [2]  both (tile's last PV)
+  uint64_t* o_free = bars + 26;       // [2]  leader: 4 epilogue warps x 2 CTAs
+  uint64_t* l_full = bars + 28;       // [2]  local: 16 softmax warps
+  uint64_t* p_q = bars + 30;          // [2 S slot][4 quarter] leader: 4 warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 38);
+  float* red = reinterpret_cast<float*>(smem + Cfg::OFF_RED);
+  float* lred = reinterpret_cast<float*>(smem + Cfg::OFF_LRED);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int nkb = (Nk + 127) / 128;   // 3 or 4 (host guarantees)
+  const int ntq = (Nq + 255) / 256;   // query tiles per head
+  const long long U = (long long)ntq * H;
+  const int cid = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int u0 = int(U * cid / npairs), u1 = int(U * (cid + 1) / npairs);
+  const int T = u1 - u0;              // this pair's tiles
+  const int h0 = u0 / ntq;
+  auto head_of = [&](int n) { return (u0 + n) / ntq; };
+  auto seg_last = [&](int n) { return n == T - 1 || head_of(n) != head_of(n + 1); };
+
+  if (warp == 20 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 2);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&pv_done[s], 1);
+      mbar_init(&o_done[s], 1);
+      mbar_init(&o_free[s], 8);
+      mbar_init(&l_full[s], 16);
+    }
+    for (int j = 0; j < Cfg::NKB; ++j) {
+      mbar_init(&k_full[j], 2);
+      mbar_init(&k_empty[j], 1);
+      mbar_init(&v_full[j], 2);
+      mbar_init(&v_empty[j], 1);
+    }
+    for (int i = 0; i < 8; ++i) mbar_init(&p_q[i], 8);
+    fence_mbar_init();
+  }
+  if (warp == 21) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 20) {
+    if (lane == 0) {
+      auto load_q = [&](int n) {
+        const int u = u0 + n, h = u / ntq, qt = u - h * ntq;
+        if (n >= 2) mbar_wait(&q_empty[n & 1], ((n - 2) >> 1) & 1);
+        if (leader) mbar_arrive_expect_tx(&q_full[n & 1], 2 * Cfg::Q_BYTES);
+        else mbar_arrive_cluster(&q_full[n & 1], 0);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_pair(sQ + (n & 1) * Cfg::Q_BYTES + a * 2 * Cfg::ATOM, &tmQ, &q_full[n & 1], a * 64,
+                           qt * 256 + int(rank) * 128, h);
+      };
+      int nq = 0;  // next tile whose Q is to be loaded
+      for (int n = 0; n < T; ++n) {
+        const int h = head_of(n);
+        if (n > 0 && h == head_of(n - 1)) continue;
+        const int s = h - h0;  // head segment of this pair
+        while (nq <= n + 1 && nq < T) load_q(nq++);  // Q of this tile (and the next) first
+        for (int j = 0; j < nkb; ++j) {
+          if (s > 0) mbar_wait(&k_empty[j], (s - 1) & 1);
+          if (leader) mbar_arrive_expect_tx(&k_full[j], 2 * Cfg::K_BYTES);
+          else mbar_arrive_cluster(&k_full[j], 0);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+            tma_load_3d_pair(sK + j * Cfg::K_BYTES + a * Cfg::ATOM, &tmK, &k_full[j], a * 64,
+                             j * 128 + int(rank) * 64, h);
+          if (s > 0) mbar_wait(&v_empty[j], (s - 1) & 1);
+          if (leader) mbar_arrive_expect_tx(&v_full[j], 2 * Cfg::V_BYTES);
+          else mbar_arrive_cluster(&v_full[j], 0);
+          tma_load_3d_pair(sV + j * Cfg::V_BYTES, &tmV, &v_full[j], int(rank) * 64, j * 128, h);
+        }
+        // Q of the tiles up to the next head change
+        int n_end = n + 1;
+        while (n_end < T && head_of(n_end) == h) ++n_end;
+        while (nq < n_end + 1 && nq < T) load_q(nq++);
+      }
+      while (nq < T) load_q(nq++);
+    }
+  } else if (warp == 21) {
+    if (leader) {
+      constexpr uint32_t idesc_qk = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(256, DH, false, true);
+      const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(sV), Cfg::V_BYTES, 1024);
+      const int nb = T * nkb;
+      auto issue_qk = [&](int b) {
+        const int n = b / nkb, j = b - n * nkb;
+        if (j == 0) mbar_wait(&q_full[n & 1], (n >> 1) & 1);
+        mbar_wait(&k_full[j], (head_of(n) - h0) & 1);
+        tc_fence_after();
+        const uint64_t a0 = dq + uint64_t(((n & 1) * Cfg::Q_BYTES) >> 4);
+        const uint64_t b0 = dk + uint64_t((j * Cfg::K_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k)
+            tc_mma_bf16_pair(tmem + Cfg::S_COL + (b & 1) * 128,
+                             a0 + uint64_t(((k >> 2) * 2 * Cfg::ATOM + (k & 3) * 32) >> 4),
+                             b0 + uint64_t(((k >> 2) * Cfg::ATOM + (k & 3) * 32) >> 4), idesc_qk, k > 0);
+          tc_commit_pair(&s_full[b & 1], 0x3);
+          if (j == nkb - 1) tc_commit_pair(&q_empty[n & 1], 0x3);
+          if (seg_last(n)) tc_commit_pair(&k_empty[j], 0x3);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int b) {
+        const int n = b / nkb, j = b - n * nkb;
+        if (j == 0 && n >= 2) mbar_wait(&o_free[n & 1], ((n - 2) >> 1) & 1);  // O[n & 1] read out
+        mbar_wait(&v_full[j], (head_of(n) - h0) & 1);
+        const uint64_t b0 = dv + uint64_t((j * Cfg::V_BYTES) >> 4);
+        const uint32_t d = tmem + Cfg::O_COL + (n & 1) * DH;
+        const uint32_t pa = tmem + Cfg::S_COL + (b & 1) * 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          mbar_wait(&p_q[(b & 1) * 4 + u], (b >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const int k = 2 * u + kk;
+              tc_mma_bf16_ts_pair(d, pa + k * 8, b0 + uint64_t((k * 2048) >> 4), idesc_pv, (j > 0 || k > 0));
+            }
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          tc_commit_pair(&pv_done[b & 1], 0x3);
+          if (j == nkb - 1) tc_commit_pair(&o_done[n & 1], 0x3);
+          if (seg_last(n)) tc_commit_pair(&v_empty[j], 0x3);
+        }
+        __syncwarp();
+      };
+      if (nb > 0) issue_qk(0);
+      if (nb > 1) issue_qk(1);
+      for (int b = 0; b < nb; ++b) {
+        issue_pv(b);
+        if (b + 2 < nb) issue_qk(b + 2);  // S[b & 1] is free once PV(b) has read P(b) (in-order pipe)
+      }
+    }
+  } else if (warp >= 16) {
+    // epilogue: O[n & 1] / l -> bf16 rows of head h
+    const int ew = warp & 3;
+    const int r = ew * 32 + lane;
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    for (int n = 0; n < T; ++n) {
+      mbar_wait(&l_full[n & 1], (n >> 1) & 1);
+      mbar_wait(&o_done[n & 1], (n >> 1) & 1);
+      tc_fence_after();
+      const float* lr = lred + (n & 1) * 512 + r;
+      const float inv = 1.0f / ((lr[0] + lr[128]) + (lr[256] + lr[384]));
+      const int u = u0 + n, h = u / ntq, qt = u - h * ntq;
+      const int q = qt * 256 + int(rank) * 128 + r;
+      const int hb = h / Hs, hl = h - hb * Hs;
+      bf16* orow = O + (size_t(hb) * Nq + q) * Hs * DH + size_t(hl) * DH;
+      const uint32_t to = tmem + lane_off + Cfg::O_COL + (n & 1) * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH; c += 32) {
+        float o[32];
+        tmem_ld32(to + c, o);
+        tc_wait_ld();
+        if (q < Nq) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= inv;
+          store_vec<32>(orow + c, o);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&o_free[n & 1], 0);
+    }
+  } else {
+    // softmax: warp (cg, ew) owns key columns [32 cg, 32 cg + 32) of rows ew*32 .. ew*32+31
+    const int ew = warp & 3, cg = warp >> 2;
+    const int r = ew * 32 + lane;
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    int b = 0;
+    for (int n = 0; n < T; ++n) {
+      float m_used = -INFINITY, l = 0.f;
+      const uint32_t to = tmem + lane_off + Cfg::O_COL + (n & 1) * DH + 32 * cg;
+      for (int j = 0; j < nkb; ++j, ++b) {
+        const uint32_t ts = tmem + lane_off + Cfg::S_COL + (b & 1) * 128;
+        mbar_wait(&s_full[b & 1], (b >> 1) & 1);
+        tc_fence_after();
+        float s[32];
+        tmem_ld32(ts + 32 * cg, s);
+        tc_wait_ld();
+        const int valid = Nk - j * 128 - 32 * cg;
+        if (valid < 32) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i >= valid) s[i] = -INFINITY;
+        }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) m4[v] = fmaxf(m4[v], fmaxf(s[i + 2 * v], s[i + 2 * v + 1]));
+        }
+        float* rb = red + (b & 1) * 512 + r;
+        rb[cg * 128] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+        named_bar_sync(1 + ew, 128);
+        const float mx = fmaxf(fmaxf(rb[0], rb[128]), fmaxf(rb[256], rb[384]));
+        const bool need = mx > m_used + 8.0f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? mx : m_used;
+          if (j > 0) {
+            // PV(b - 1) must have landed in O before it is rescaled
+            mbar_wait(&pv_done[(b - 1) & 1], ((b - 1) >> 1) & 1);
+            tc_fence_after();
+            const float alpha = exp2f(m_used - m_new);
+            l *= alpha;
+            float o[32];
+            tmem_ld32(to, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(to, o);
+          }
+          m_used = m_new;
+        }
+        float2 lsum2 = make_float2(0.f, 0.f);
+        const float2 sc2 = make_float2(scale_log2, scale_log2);
+        const float2 nm2 = make_float2(-m_used, -m_used);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2), i, lsum2);
+        tmem_st16(ts + 16 * cg, pk);  // P: keys 32cg.. as bf16 pairs in columns 16cg..16cg+15
+        l += lsum2.x + lsum2.y;
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&p_q[(b & 1) * 4 + cg], 0);
+      }
+      lred[(n & 1) * 512 + cg * 128 + r] = l;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&l_full[n & 1]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 21) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+static cudaError_t launch_attn_sk(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk,
+                                  float scale, cudaStream_t st, int hs) {
+  using Cfg = AttnSkCfg;
+  static_assert(Cfg::SMEM <= 232448, "attn_sk shared memory");
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
+      !make_tmap_3d(&tv, V, H, Nk, 128, 128))
+    return cudaErrorInvalidValue;
+  auto kern = attn_sk_kernel<2>;
+  static int max_pairs = 0;
+  if (!max_pairs) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    max_pairs = num_sms() / 2;
+  }
+  const long long units = (long long)((Nq + 255) / 256) * H;
+  const int pairs = units < max_pairs ? int(units) : max_pairs;
+  dim3 grid(2 * pairs);
+  float sl2 = scale * 1.4426950408889634f;
+  void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O, (void*)&H, (void*)&Nq, (void*)&Nk, (void*)&sl2, (void*)&hs};
+  return launch_ex((const void*)kern, grid, dim3(ATTN_SK_THREADS), Cfg::SMEM, st, args);
+}
+
 DF_DEV void st_release_u32_attn(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -776,6 +1116,14 @@ template <int DH>
 static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
                                float scale, cudaStream_t st, int hs) {
   if constexpr (DH == 128) {
+    // N_kv in [257, 512] (cross-attention): K/V-resident short-key kernel; DF_ATTN_SK=0 selects
+    // attn_pp for A/B
+    static const bool sk = [] {
+      const char* e = getenv("DF_ATTN_SK");
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (g_attn_impl != 2 && sk && dh == 128 && Nk > 256 && Nk <= 512)
+      return launch_attn_sk(Q, K, V, O, H, Nq, Nk, scale, st, hs);
     if (g_attn_impl != 2) return launch_attn_pp<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
   }
   CUtensorMap tq, tk, tv;

@@ -1,0 +1,110 @@
+"""attn_sk (the K/V-resident short-key attention used for 257 <= N_kv <= 512, i.e. the text
+cross-attention of every config and the I2V image-token attention) against
+fp64 softmax attention (oracle/dit.softmax_attention, P5) on the same bf16 inputs.
+
+The cases cover: one tile per CTA pair and more pairs than tiles; ragged query tiles; N_kv with
+a ragged last key block (3 and 4 key blocks); head-segment changes inside a pair's tile range
+(the resident K/V is refilled per block while the old head drains); the lazy-rescale path
+(later key blocks raising the row maximum by far more than 2^8); run-to-run determinism; and
+the image / video cross-attention shapes on sampled rows."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import dit
+from synth.configs import TINY
+from gpu_util import rel_l2, make_ctx
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    c = make_ctx(TINY)
+    yield c
+    c.close()
+
+
+def _run(ctx, Q, K, V):
+    H, Nq, dh = Q.shape
+    Nk = K.shape[1]
+    O = torch.full((Nq, H * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
+    ctx.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, 1.0 / math.sqrt(dh))
+    torch.cuda.synchronize()
+    return O
+
+
+def _want(Q, K, V, rows=None):
+    H, Nq, dh = Q.shape
+    if rows is not None:
+        Q = Q[:, torch.as_tensor(rows, device=Q.device)]
+    qd = Q.float().cpu().numpy().astype(np.float64)
+    kd, vd = (t.float().cpu().numpy().astype(np.float64) for t in (K, V))
+    return dit.softmax_attention(qd, kd, vd).transpose(1, 0, 2).reshape(qd.shape[1], H * dh)
+
+
+def _inputs(H, Nq, Nk, seed, qs=1.5, ks=1.5):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dh = 128
+    Q = (torch.randn(H, Nq, dh, device="cuda", generator=g) * qs).to(torch.bfloat16)
+    K = (torch.randn(H, Nk, dh, device="cuda", generator=g) * ks).to(torch.bfloat16)
+    V = torch.randn(H, Nk, dh, device="cuda", generator=g).to(torch.bfloat16)
+    return Q, K, V
+
+
+@pytest.mark.parametrize("H,Nq,Nk", [(1, 100, 512), (1, 300, 257), (3, 777, 384), (5, 513, 449), (7, 1000, 511),
+                                     (2, 256, 300)])
+def test_short_key_attention_vs_fp64(ctx, H, Nq, Nk):
+    Q, K, V = _inputs(H, Nq, Nk, seed=H * 1000 + Nk)
+    got = _run(ctx, Q, K, V).float().cpu().numpy()
+    assert np.isfinite(got).all()
+    assert rel_l2(got, _want(Q, K, V)) < 1e-2
+
+
+def test_head_segments_inside_a_pair(ctx):
+    """40 heads x 5 query tiles = 200 tiles on 74 pairs: most pairs' ranges cross a head
+    boundary, so the resident K/V is refilled mid-range; every row of every head checked."""
+    H, Nq, Nk = 40, 1200, 512
+    Q, K, V = _inputs(H, Nq, Nk, seed=7)
+    got = _run(ctx, Q, K, V).float().cpu().numpy()
+    want = _want(Q, K, V)
+    for h in range(H):
+        sl = slice(h * 128, (h + 1) * 128)
+        assert rel_l2(got[:, sl], want[:, sl]) < 1e-2, h
+
+
+def test_lazy_rescale_path(ctx):
+    """Scores grow block by block (key block j scaled by 1 + 2j), so the running maximum of
+    most rows rises by >> 8 (log2 units) after the first block and O is rescaled in TMEM."""
+    H, Nq, Nk = 4, 640, 512
+    Q, K, V = _inputs(H, Nq, Nk, seed=11, qs=2.0, ks=2.0)
+    scale = torch.ones(Nk, device="cuda")
+    for j in range(4):
+        scale[j * 128:(j + 1) * 128] = 1 + 2 * j
+    K = (K.float() * scale[None, :, None]).to(torch.bfloat16)
+    got = _run(ctx, Q, K, V).float().cpu().numpy()
+    assert rel_l2(got, _want(Q, K, V)) < 1e-2
+
+
+def test_deterministic_and_equal_on_repeat(ctx):
+    Q, K, V = _inputs(24, 4096, 512, seed=3)
+    a = _run(ctx, Q, K, V)
+    b = _run(ctx, Q, K, V)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("H,Nq", [(24, 4096), (40, 32760)])
+def test_production_cross_shapes_sampled(ctx, H, Nq):
+    """The image (C2) and video (C3) cross-attention shapes (N_kv = L_txt = 512), sampled rows
+    including the ragged last query tile of the video shape."""
+    Q, K, V = _inputs(H, Nq, 512, seed=Nq)
+    O = _run(ctx, Q, K, V)
+    rows = np.unique(np.concatenate([np.arange(0, Nq, 211), np.arange(Nq - 9, Nq)]))
+    got = O[torch.as_tensor(rows, device=O.device)].float().cpu().numpy()
+    assert np.isfinite(got).all()
+    assert rel_l2(got, _want(Q, K, V, rows)) < 1e-2

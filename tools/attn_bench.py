@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--lib", action="store_true", help="also time torch SDPA (cuDNN / flash backends) on the same inputs")
     ap.add_argument("--H", type=int, default=0, help="override the head count (work-item scaling experiments)")
+    ap.add_argument("--reps", type=int, default=1, help="back-to-back launches per timed sample (amortises launch latency)")
     a = ap.parse_args()
     H, Nq, Nk = SHAPES[a.shape]
     if a.H:
@@ -47,10 +48,11 @@ def main():
         ms = []
         for _ in range(a.iters):
             ev[0].record()
-            c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)
+            for _ in range(a.reps):
+                c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)
             ev[1].record()
             torch.cuda.synchronize()
-            ms.append(ev[0].elapsed_time(ev[1]))
+            ms.append(ev[0].elapsed_time(ev[1]) / a.reps)
         rows = torch.arange(0, Nq, max(1, Nq // 7), device="cuda")[:8]
         qf, kf, vf = Q[:, rows].float(), K.float(), V.float()
         ref = torch.softmax(qf @ kf.transpose(1, 2) * sc, -1) @ vf
@@ -73,10 +75,11 @@ def main():
                         lm = []
                         for _ in range(a.iters):
                             ev[0].record()
-                            f()
+                            for _ in range(a.reps):
+                                f()
                             ev[1].record()
                             torch.cuda.synchronize()
-                            lm.append(ev[0].elapsed_time(ev[1]))
+                            lm.append(ev[0].elapsed_time(ev[1]) / a.reps)
                     print({"shape": a.shape, "lib": str(be), "ms": round(min(lm), 3),
                            "tflops": round(fl / min(lm) / 1e9, 1)}, flush=True)
                 except Exception as ex:  # backend not available for this shape / build
