@@ -16,7 +16,10 @@ Parity status (pins in tests/test_oracle_fp8.py): encode/decode pinned by the fo
 closed-form values, the 256-code round trip, ties-to-even midpoints, saturation and
 torch's float8_e4m3fn cast (a library routine) on in-range values; quantize pinned by the
 scale property (the amax element maps to 448) and the zero tensor; gemm pinned by a
-brute-force loop on a tiny case.
+brute-force loop on a tiny case.  MXFP8 (R30, below): mx_quantize pinned by the block
+exponent's closed form, the worked block 1..32 (ties-to-even at 136), exact round trips of
+representable blocks, OCP saturation, block independence, the zero block and torch's
+float8_e4m3fn cast on the scaled values; gemm_mxf8 by a brute-force loop.
 """
 import numpy as np
 
@@ -80,3 +83,46 @@ def quantize_per_tensor(x):
 def gemm_e4m3(qa, qb, sa, sb):
     """out[M, N] = sa * sb * dec(qa)[M, K] . dec(qb)[N, K]^T in fp64."""
     return float(sa) * float(sb) * (e4m3_decode(qa) @ e4m3_decode(qb).T)
+
+
+# ---------------------------------------------------------------- MXFP8 (R30)
+# OCP Microscaling (MX) Formats Specification v1.0, MXFP8 with E4M3 elements: a block of 32
+# consecutive elements (along K) shares one E8M0 scale X = 2^e (e + 127 stored in a byte,
+# 255 = NaN unused here).  Conversion (spec §6.3): e = floor(log2(max_i |V_i|)) - emax_elem,
+# emax_elem = 8 for E4M3 (448 = 1.75 * 2^8), clamped to the E8M0 range [-127, 127]; each
+# element P_i = e4m3(V_i / X), rounded to nearest even and clamped to +-448 (so a block whose
+# amax mantissa exceeds 1.75 saturates its largest elements -- the spec's behaviour, kept).
+# An all-zero block takes e = -127 (byte 0) and zero codes.  The division by the power of two
+# X is exact in fp64 (and in the kernel's fp32 unless the quotient falls below 2^-126, where
+# every e4m3 code is 0 on both sides).
+MX_BLOCK = 32
+E4M3_EMAX = 8
+
+
+def mx_quantize(x):
+    """x [R, K] (K % 32 == 0, fp32-representable) -> (q uint8 [R, K], sbytes uint8 [R, K/32])."""
+    x = np.asarray(x, dtype=np.float64)
+    R, K = x.shape
+    assert K % MX_BLOCK == 0
+    xb = x.reshape(R, K // MX_BLOCK, MX_BLOCK)
+    amax = np.max(np.abs(xb), axis=-1)
+    with np.errstate(divide="ignore"):
+        e = np.floor(np.log2(np.where(amax > 0, amax, 1.0))) - E4M3_EMAX
+    e = np.where(amax > 0, e, -127.0)
+    e = np.clip(e, -127, 127)
+    q = e4m3_encode(xb / np.exp2(e)[..., None]).reshape(R, K)
+    return q, (e + 127).astype(np.uint8)
+
+
+def mx_dequantize(q, sbytes):
+    """(q [R, K], sbytes [R, K/32]) -> fp64 values dec(q) * 2^(s - 127)."""
+    q = np.asarray(q, dtype=np.uint8)
+    R, K = q.shape
+    sc = np.exp2(np.asarray(sbytes, dtype=np.float64) - 127.0)
+    return (e4m3_decode(q).reshape(R, K // MX_BLOCK, MX_BLOCK) * sc[..., None]).reshape(R, K)
+
+
+def gemm_mxf8(qa, sa, qb, sb):
+    """out[M, N] = mx_dequantize(qa, sa) . mx_dequantize(qb, sb)^T in fp64 (every product of
+    two MXFP8 values is exact in fp64)."""
+    return mx_dequantize(qa, sa) @ mx_dequantize(qb, sb).T

@@ -106,3 +106,107 @@ def test_fp8_block_wiring_reduces_to_the_bf16_block():
     got = dit.block(P, cfg, 0, r, e6, kv, pos, q8=dit_fp8.Q8())
     rel = np.linalg.norm((got - r) - (ref - r)) / np.linalg.norm(ref - r)
     assert 1e-3 < rel < 0.2, rel
+
+
+# ---------------------------------------------------------------- MXFP8 (R30): OCP MX v1.0
+def test_mx_block_exponent_closed_form():
+    """e = floor(log2 amax) - 8 for E4M3 elements, stored as e + 127."""
+    for k in (-20, -3, 0, 1, 7, 30):
+        for mant in (1.0, 1.5, 1.75, 1.99):
+            x = np.zeros((1, 32))
+            x[0, 5] = mant * 2.0 ** k
+            x[0, 6] = -0.25 * 2.0 ** k
+            _, s = fp8.mx_quantize(x)
+            assert s[0, 0] == k - 8 + 127
+
+
+def test_mx_worked_block_1_to_32():
+    """x = 1..32: amax 32 -> e = 5 - 8 = -3, X = 1/8, x/X = 8, 16, ..., 256.  Every multiple of
+    8 up to 128 is exact in e4m3 except the ones needing a 4th mantissa bit; 136 = 1.0625 * 128
+    is the midpoint of 128 and 144 and rounds to even (128); 152, between 144 and 160, to 160."""
+    x = np.arange(1, 33, dtype=np.float64)[None, :]
+    q, s = fp8.mx_quantize(x)
+    assert s[0, 0] == 124
+    got = fp8.mx_dequantize(q, s)[0]
+    assert got[0] == 1.0 and got[15] == 16.0 and got[31] == 32.0
+    assert got[16] == 16.0          # 17 -> 136 -> 128 (tie to even) -> 16
+    assert got[18] == 20.0          # 19 -> 152: midpoint of 144 and 160 -> 160 (even) -> 20
+    assert got[2] == 3.0 and got[6] == 7.0   # 24 = 1.5*16, 56 = 1.75*32: exact
+
+
+def test_mx_representable_blocks_round_trip_exactly():
+    r = np.random.default_rng(1)
+    codes = r.integers(0, 0x7F, size=(4, 64)).astype(np.uint8)  # finite, non-negative e4m3
+    codes[:, ::32] = 0x70                                          # amax 256 = 2^8 in every block
+    vals = fp8.e4m3_decode(codes) * np.where(r.random((4, 64)) < 0.5, -1.0, 1.0)
+    scale = np.exp2(r.integers(-40, 40, size=(4, 2)))[..., None]
+    x = (vals.reshape(4, 2, 32) * scale).reshape(4, 64)
+    q, s = fp8.mx_quantize(x)
+    np.testing.assert_array_equal(fp8.mx_dequantize(q, s), x)
+
+
+def test_mx_saturation_per_ocp():
+    """amax = 1.9 * 2^k: X = 2^(k-8), amax / X = 486.4 > 448 -> the code saturates at 448."""
+    x = np.zeros((1, 32))
+    x[0, 0] = 1.9 * 2.0 ** 3
+    x[0, 1] = -1.9 * 2.0 ** 3
+    x[0, 2] = 1.0
+    q, s = fp8.mx_quantize(x)
+    assert q[0, 0] == 0x7E and q[0, 1] == 0xFE
+    d = fp8.mx_dequantize(q, s)[0]
+    assert d[0] == 1.75 * 2.0 ** 3 and d[2] == 1.0
+
+
+def test_mx_blocks_are_independent_and_zero_block():
+    r = np.random.default_rng(2)
+    x = r.standard_normal((3, 128))
+    q0, s0 = fp8.mx_quantize(x)
+    x2 = x.copy()
+    x2[:, 32:64] *= 1000.0
+    x2[1, 96:128] = 0.0
+    q1, s1 = fp8.mx_quantize(x2)
+    keep = np.r_[0:32, 64:128]
+    np.testing.assert_array_equal(q0[0, keep], q1[0, keep])
+    np.testing.assert_array_equal(q0[:, 0:32], q1[:, 0:32])
+    assert s1[1, 3] == 0 and not q1[1, 96:].any()
+    assert (s1[:, 1] - s0[:, 1] >= 9).all()  # 1000 ~ 2^9.97: the block exponent moved up
+
+
+def test_mx_codes_match_torch_cast_of_scaled_values():
+    torch = pytest.importorskip("torch")
+    r = np.random.default_rng(3)
+    x = (r.standard_normal((8, 256)) * np.exp2(r.integers(-10, 10, size=(8, 1)))).astype(np.float32)
+    q, s = fp8.mx_quantize(x)
+    scaled = x.astype(np.float64).reshape(8, 8, 32) / np.exp2(s.astype(np.float64) - 127)[..., None]
+    assert np.abs(scaled).max() <= 512
+    t = torch.from_numpy(np.clip(scaled, -448, 448).reshape(8, 256)).to(torch.float8_e4m3fn)
+    np.testing.assert_array_equal(q, t.view(torch.uint8).numpy())
+
+
+def test_mx_relative_error_bound():
+    """Unsaturated normal-range elements lose at most half a quantum: |dq - x| <= 2^-4 |x|."""
+    r = np.random.default_rng(4)
+    x = r.standard_normal((16, 256)) * 3.0
+    q, s = fp8.mx_quantize(x)
+    d = fp8.mx_dequantize(q, s)
+    X = np.repeat(np.exp2(s.astype(np.float64) - 127), 32, axis=1)
+    ok = (np.abs(x) / X >= 2.0 ** -6) & (np.abs(x) / X <= 448)
+    assert ok.mean() > 0.9
+    assert (np.abs(d - x)[ok] <= 2.0 ** -4 * np.abs(x)[ok] + 1e-300).all()
+
+
+def test_gemm_mxf8_bruteforce():
+    r = np.random.default_rng(5)
+    a = r.standard_normal((3, 64))
+    b = r.standard_normal((4, 64)) * 10
+    qa, sa = fp8.mx_quantize(a)
+    qb, sb = fp8.mx_quantize(b)
+    want = np.zeros((3, 4))
+    for i in range(3):
+        for j in range(4):
+            acc = 0.0
+            for k in range(64):
+                acc += (fp8.e4m3_decode(qa[i, k:k + 1])[0] * 2.0 ** (int(sa[i, k // 32]) - 127)) * \
+                       (fp8.e4m3_decode(qb[j, k:k + 1])[0] * 2.0 ** (int(sb[j, k // 32]) - 127))
+            want[i, j] = acc
+    np.testing.assert_allclose(fp8.gemm_mxf8(qa, sa, qb, sb), want, rtol=1e-13, atol=1e-12)
