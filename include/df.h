@@ -260,6 +260,25 @@ df_status df_op_quant_e4m3(df_ctx* ctx, const void* x, uint64_t n, void* q, floa
  * (out_f32 = 1) or bf16, row stride N.  Device pointers; stream-ordered. */
 df_status df_op_gemm_e4m3(df_ctx* ctx, const void* qa, const void* qb, const float* sa, const float* sb, int32_t M,
                           int32_t N, int32_t K, void* out, int32_t out_f32, void* stream);
+/* MXFP8 (SURVEY NEXT-4 "MXFP8 block-scaled GEMM"; R30 = OCP Microscaling Formats
+ * v1.0, MXFP8 with E4M3 elements): quantise the bf16 matrix x [M, K] (row-major, device,
+ * 16-byte aligned, K % 128 == 0) in blocks of 32 consecutive elements of a row:
+ * e = floor(log2 max|block|) - 8 clamped to [-127, 127] (-127 for an all-zero block),
+ * q[m, k] = e4m3 bits of RNE_satfinite(x[m, k] * 2^-e) (q: M*K bytes, row-major, 16-byte
+ * aligned), scale byte e + 127 written to sf in the tiled layout the GEMM loads by TMA:
+ * RB = ceil(M / 128) row blocks; the 512-byte atom of (k-group kg = k / 128, row block
+ * rb = m / 128) starts at byte (kg * RB + rb) * 512 and holds row m, k-block kb = k / 32 at
+ * (m % 32) * 16 + ((m % 128) / 32) * 4 + kb % 4.  sf: (K / 128) * RB * 512 bytes (device;
+ * rows [M, 128 RB) get byte 0).  One stream-ordered launch; DF_ERR_INVALID on bad shapes. */
+df_status df_op_mx_quant_e4m3(df_ctx* ctx, const void* x, int32_t M, int32_t K, void* q, void* sf, void* stream);
+/* out[M,N] = sum_k dec(qa[m,k]) 2^(sa(m,k/32) - 127) * dec(qb[n,k]) 2^(sb(n,k/32) - 127): MXFP8
+ * operands as df_op_mx_quant_e4m3 writes them (qa [M,K], qb [N,K] e4m3, sa / sb tiled scale
+ * bytes), fp32 accumulation on the tensor cores (tcgen05 kind::mxf8f6f4.block_scale, scale
+ * factors staged shared memory -> TMEM by tcgen05.cp, CTA pairs, 256 x 256 tiles), out fp32
+ * (out_f32 = 1) or bf16, row stride N.  K % 128 == 0, M and N >= 256.  Device pointers;
+ * stream-ordered. */
+df_status df_op_gemm_mxf8(df_ctx* ctx, const void* qa, const void* sa, const void* qb, const void* sb, int32_t M,
+                          int32_t N, int32_t K, void* out, int32_t out_f32, void* stream);
 /* O[Nq, H*dh] = softmax(Q K^T * scale) V, head-major bf16 Q/K/V [H][N][dh_pad]. */
 df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t H, int32_t Nq,
                           int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream);

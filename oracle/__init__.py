@@ -35,6 +35,10 @@ is checked to fail under one-line mutations of the oracle by tools/mutate_oracle
   capacity.payload_hash pinned: splitmix64 published first output, chunk additivity
   fp8 (NEXT-4, R28) pinned: E4M3 closed forms, 256-code round trip, ties-to-even,
                saturation, torch float8_e4m3fn cast, brute-force GEMM
+  fp8.mx_* (NEXT-4, R30 MXFP8) pinned: block-exponent closed form, worked block 1..32
+               (ties-to-even), exact round trips, OCP saturation, block independence,
+               zero block, torch cast of the scaled values, half-quantum error bound,
+               brute-force GEMM
   dit_fp8 (NEXT-4, R29) pinned: per-row quantiser closed forms (amax-448 row, zero row,
                power-of-two scaling); wiring = dit.block exactly under identity quantisers
 """

@@ -120,6 +120,9 @@ _SIGS = {
     "df_op_quant_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_op_gemm_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "df_op_mx_quant_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "df_op_gemm_mxf8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "df_op_rmsnorm_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
     "df_launch_count": (C.c_uint64, [C.c_void_p]),
@@ -413,6 +416,19 @@ class Context:
         N = qb.shape[0]
         out_f32 = int(str(out.dtype) == "torch.float32")
         self._ck(self.lib.df_op_gemm_e4m3(self.h, _ptr(qa), _ptr(qb), _ptr(sa), _ptr(sb), M, N, K, _ptr(out), out_f32,
+                                          _stream(stream)))
+
+    def op_mx_quant_e4m3(self, x, q, sf, stream=None):
+        """x bf16 [M, K] (K % 128 == 0); q uint8 [M, K]; sf uint8 of (K/128) * ceil(M/128) * 512 bytes."""
+        M, K = x.shape
+        self._ck(self.lib.df_op_mx_quant_e4m3(self.h, _ptr(x), M, K, _ptr(q), _ptr(sf), _stream(stream)))
+
+    def op_gemm_mxf8(self, qa, sa, qb, sb, out, stream=None):
+        """qa uint8 [M,K], qb uint8 [N,K], sa/sb tiled E8M0 scale bytes, out fp32 or bf16 [M,N]."""
+        M, K = qa.shape
+        N = qb.shape[0]
+        out_f32 = int(str(out.dtype) == "torch.float32")
+        self._ck(self.lib.df_op_gemm_mxf8(self.h, _ptr(qa), _ptr(sa), _ptr(qb), _ptr(sb), M, N, K, _ptr(out), out_f32,
                                           _stream(stream)))
 
     def op_attention(self, Q, K, V, O, H, Nq, Nk, dh, dh_pad, scale, stream=None):

@@ -328,6 +328,14 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
 // 3: one MUFU ex2.bf16x2 per pair (input rounded to bf16: coarser, profiling only).
 template <int EXPM>
 DF_DEV uint32_t softmax_exp2(float2 x, int i, float2& lsum2) {
+  if (EXPM == 4) {  // one MUFU ex2.f16x2 per pair (input rounded to f16: |err(x)| <= |x| 2^-11)
+    uint32_t xh, ph;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(xh) : "f"(x.y), "f"(x.x));
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(ph) : "r"(xh));
+    const float2 p = __half22float2(*reinterpret_cast<const __half2*>(&ph));
+    lsum2 = fadd2(lsum2, p);
+    return pack_bf16x2(p.x, p.y);
+  }
   if (EXPM == 3) {
     const uint32_t xb = pack_bf16x2(x.x, x.y);
     uint32_t pb;
@@ -336,7 +344,7 @@ DF_DEV uint32_t softmax_exp2(float2 x, int i, float2& lsum2) {
     return pb;
   }
   float2 p;
-  if ((EXPM == 1 && (i & 7) >= 5) || (EXPM == 2 && (i & 3) == 3)) {
+  if ((EXPM == 1 && (i & 7) >= 5) || (EXPM == 2 && (i & 3) == 3) || (EXPM == 5 && (i & 1))) {
     p = exp2_poly2(x);
   } else {
     p.x = ex2_approx(x.x);
@@ -344,6 +352,14 @@ DF_DEV uint32_t softmax_exp2(float2 x, int i, float2& lsum2) {
   }
   lsum2 = fadd2(lsum2, p);
   return pack_bf16x2(p.x, p.y);
+}
+
+// exponential split of the softmax (A/B, read once): DF_ATTN_EXPM = 2 (default: a quarter of the
+// pairs by polynomial), 1 (3 of 8), 5 (half), 0 (all MUFU), 4 (MUFU ex2.f16x2), 3 (ex2.bf16x2)
+static int attn_expm() {
+  const char* e = getenv("DF_ATTN_EXPM");
+  const int v = e ? atoi(e) : 2;
+  return (v >= 0 && v <= 5) ? v : 2;
 }
 
 // ------------------------------------------------------------------ attn_tc3: 2 threads per query row
@@ -1088,7 +1104,9 @@ static cudaError_t launch_attn_sk(const bf16* Q, const bf16* K, const bf16* V, b
   if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
       !make_tmap_3d(&tv, V, H, Nk, 128, 128))
     return cudaErrorInvalidValue;
-  auto kern = attn_sk_kernel<2>;
+  static const int expm = attn_expm();
+  auto kern = expm == 4 ? attn_sk_kernel<4> : expm == 5 ? attn_sk_kernel<5> : expm == 1 ? attn_sk_kernel<1>
+              : expm == 3 ? attn_sk_kernel<3> : attn_sk_kernel<2>;
   static int max_pairs = 0;
   if (!max_pairs) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1124,7 +1142,17 @@ static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16
     }();
     if (g_attn_impl != 2 && sk && dh == 128 && Nk > 256 && Nk <= 512)
       return launch_attn_sk(Q, K, V, O, H, Nq, Nk, scale, st, hs);
-    if (g_attn_impl != 2) return launch_attn_pp<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+    if (g_attn_impl != 2) {
+      static const int expm = attn_expm();
+      switch (expm) {
+        case 0: return launch_attn_pp<0>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 1: return launch_attn_pp<1>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 3: return launch_attn_pp<3>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 4: return launch_attn_pp<4>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        case 5: return launch_attn_pp<5>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+        default: return launch_attn_pp<2>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
+      }
+    }
   }
   CUtensorMap tq, tk, tv;
   if (!make_tmap_3d(&tq, Q, H, Nq, DH, 128) || !make_tmap_3d(&tk, K, H, Nk, DH, 128) ||

@@ -125,6 +125,28 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major,
          | (uint32_t(M >> 4) << 24);       // m_dim
 }
 
+// Shared-memory matrix descriptor without swizzle (the source of tcgen05.cp: a 32-row x 16-byte
+// scale-factor atom = four 8-row core matrices 128 B apart, SBO = 128).
+DF_DEV uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // version = 1 (sm_100); layout type 0 = no swizzle
+  return d;
+}
+
+// Instruction descriptor, kind::mxf8f6f4.block_scale (MXFP8, R30): E4M3 x E4M3 -> F32 with
+// E8M0 scale factors (scale_format bit 23 = 1); sfa_id / sfb_id select the byte of each
+// 32-bit scale-factor column that this MMA's K = 32 slice uses.
+__host__ __device__ constexpr uint32_t idesc_mxf8(int M, int N, int sfa_id, int sfb_id) {
+  return (uint32_t(sfb_id & 3) << 4)       // b_sf_id
+         | (uint32_t(N >> 3) << 17)        // n_dim
+         | (1u << 23)                      // scale_format = E8M0
+         | (uint32_t(M >> 4) << 24)        // m_dim
+         | (uint32_t(sfa_id & 3) << 29);   // a_sf_id
+}
+
 // Instruction descriptor, kind::f8f6f4: E4M3 x E4M3 -> F32, dense (a/b_format E4M3 = 0).
 __host__ __device__ constexpr uint32_t idesc_e4m3(int M, int N) {
   return (1u << 4)                         // c_format = F32
@@ -265,6 +287,26 @@ DF_DEV void tc_mma_f8_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// CTA-pair block-scaled MXFP8 MMA (kind::mxf8f6f4.block_scale): scale factors of A and B are
+// read from TMEM (columns sfa / sfb, the byte chosen by the descriptor's sf ids)
+DF_DEV void tc_mma_mxf8_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t sfa_tmem,
+                             uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
+// shared memory -> TMEM copy of 32 rows x 128 bits, broadcast to the four lane quarters
+// (each CTA of the pair copies its own shared memory into its own TMEM); in issue order with
+// the MMAs of the issuing thread
+DF_DEV void tc_cp_32x128b_x4_pair(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 // commit prior pair MMAs to the barrier at this offset in every CTA of `mask`
 DF_DEV void tc_commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(

@@ -2917,4 +2917,24 @@ df_status df_op_gemm_e4m3(df_ctx* ctx, const void* qa, const void* qb, const flo
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_gemm_e4m3: ") + cudaGetErrorString(r));
 }
 
+df_status df_op_mx_quant_e4m3(df_ctx* ctx, const void* x, int32_t M, int32_t K, void* q, void* sf, void* stream) {
+  if (!ctx || M < 0 || K < 0 || (M && K && (!x || !q || !sf))) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = mx_quant_e4m3(static_cast<const bf16*>(x), M, K, static_cast<uint8_t*>(q), static_cast<uint8_t*>(sf),
+                                (cudaStream_t)stream);
+  if (r == cudaErrorInvalidValue) return fail(ctx, "df_op_mx_quant_e4m3: K % 128 or alignment", DF_ERR_INVALID);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_mx_quant_e4m3: ") + cudaGetErrorString(r));
+}
+
+df_status df_op_gemm_mxf8(df_ctx* ctx, const void* qa, const void* sa, const void* qb, const void* sb, int32_t M,
+                          int32_t N, int32_t K, void* out, int32_t out_f32, void* stream) {
+  if (!ctx || !qa || !qb || !sa || !sb || !out) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = gemm_mxf8(static_cast<const uint8_t*>(qa), static_cast<const uint8_t*>(sa),
+                            static_cast<const uint8_t*>(qb), static_cast<const uint8_t*>(sb), M, N, K, out, N, out_f32,
+                            (cudaStream_t)stream);
+  if (r == cudaErrorInvalidValue) return fail(ctx, "df_op_gemm_mxf8: unsupported shape", DF_ERR_INVALID);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_gemm_mxf8: ") + cudaGetErrorString(r));
+}
+
 }  // extern "C"

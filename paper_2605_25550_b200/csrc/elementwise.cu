@@ -1004,4 +1004,66 @@ cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaSt
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- MXFP8 quantiser (R30)
+// OCP MX v1.0 with E4M3 elements: per 32-element block of a row, e = floor(log2 amax) - 8
+// (clamped to [-127, 127]; -127 for an all-zero block), q = RNE_satfinite_e4m3(x * 2^-e) --
+// the multiply by a power of two is exact in fp32 unless the quotient is below 2^-126, where
+// the e4m3 code is 0 either way.  One thread per block (four 16-byte loads, two 16-byte
+// stores); the scale byte e + 127 goes to the tiled layout the MXFP8 GEMM loads by TMA:
+// atom (kg = kb / 4, rb = row / 128) at byte (kg * RB + rb) * 512, inside it
+// (row % 32) * 16 + ((row % 128) / 32) * 4 + kb % 4.  Rows [M, RB * 128) get scale byte 0.
+__global__ void __launch_bounds__(256) mx_quant_e4m3_kernel(const bf16* __restrict__ x, int M, int K, int RB,
+                                                            uint8_t* __restrict__ q, uint8_t* __restrict__ sf) {
+  const int KB = K / 32;
+  const long long idx = blockIdx.x * 256ll + threadIdx.x;
+  if (idx >= (long long)RB * 128 * KB) return;
+  const int r = int(idx / KB), kb = int(idx - (long long)r * KB);
+  const size_t sfo = (size_t(kb >> 2) * RB + (r >> 7)) * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4 + (kb & 3);
+  if (r >= M) {
+    sf[sfo] = 0;
+    return;
+  }
+  const uint4* xv = reinterpret_cast<const uint4*>(x + size_t(r) * K + size_t(kb) * 32);
+  uint4 u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u[i] = __ldg(xv + i);
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t w[4] = {u[i].x, u[i].y, u[i].z, u[i].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[8 * i + 2 * k] = __uint_as_float(w[k] << 16);
+      v[8 * i + 2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    }
+  }
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  int e = -127;
+  if (amax > 0.f) {
+    int ex;
+    frexpf(amax, &ex);  // amax = m 2^ex, m in [0.5, 1): floor(log2 amax) = ex - 1
+    e = min(127, max(-127, ex - 1 - 8));
+  }
+  const float inv = scalbnf(1.0f, -e);
+  uint32_t o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = e4m3x4_mul(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3], inv);
+  uint4* qv = reinterpret_cast<uint4*>(q + size_t(r) * K + size_t(kb) * 32);
+  qv[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  qv[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  sf[sfo] = uint8_t(e + 127);
+}
+
+cudaError_t mx_quant_e4m3(const bf16* x, int M, int K, uint8_t* q, uint8_t* sf, cudaStream_t st) {
+  if (M <= 0 || K <= 0) return cudaSuccess;
+  if (K % 128 || !x || !q || !sf || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(q) & 15))
+    return cudaErrorInvalidValue;
+  const int RB = (M + 127) / 128;
+  const long long n = (long long)RB * 128 * (K / 32);
+  mx_quant_e4m3_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(x, M, K, RB, q, sf);
+  return cudaGetLastError();
+}
+
 }  // namespace df

@@ -65,9 +65,10 @@ bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, u
   return r == CUDA_SUCCESS;
 }
 
-// Generic tiled tensor map (128B swizzle; box inner extent must be 128 B).
+// Generic tiled tensor map (128B swizzle unless swz128 is false; box inner extent must be 128 B
+// with the swizzle).
 bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
-               const uint64_t* strides_bytes, const uint32_t* box) {
+               const uint64_t* strides_bytes, const uint32_t* box, bool swz128 = true) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t d[5], st[4];
@@ -80,7 +81,8 @@ bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esi
   }
   (void)esize;
   CUresult r = enc(m, dt, rank, const_cast<void*>(base), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -312,6 +314,11 @@ constexpr int P_THREADS = 128 + 32 * P_EPI_WARPS;
 constexpr int P_OFF_STG = P_OFF_BAR + 1024;                    // 8 epilogue warps x 4 KB staging tile
 constexpr int P_OFF_PRM = P_OFF_STG + P_EPI_WARPS * 4096;      // 8 warps x (128 bias + 128 gate/gain) fp32
 constexpr int P_SMEM = P_OFF_PRM + P_EPI_WARPS * 1024 + 1024;
+// MXFP8 (R30): per stage one 512-byte scale-factor atom of this CTA's 128 A rows and the two
+// atoms of the tile's 256 B rows (every CTA of the pair holds all of them)
+constexpr int P_OFF_SF = P_OFF_PRM + P_EPI_WARPS * 1024;
+constexpr int P_SF_STAGE = 512 + 1024;
+constexpr int P_SMEM_MX = P_OFF_SF + P_STAGES * P_SF_STAGE + 1024;
 
 // Epilogue variants of the pair kernel (compile-time): TK_DIRECT = per-thread stores via
 // epi_apply; the others stage each warp's 32-row slice in a 128B-swizzled 4 KB shared tile
@@ -407,7 +414,13 @@ DF_DEV void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  /
 // 64, and an 8-bit MMA consumes 32 of them (32 bytes) per instruction, so the smem tiles,
 // descriptors and stage bytes are those of the bf16 kernel; only the k-block extent, the
 // MMA kind and the dequantisation scale in the epilogue change.
-template <int CW, typename OutT, int TK, bool F8 = false>
+// MX (with F8): MXFP8 block-scaled operands (R30, kind::mxf8f6f4.block_scale).  The E8M0 scale
+// atoms of each k-block arrive by TMA with the operands (tmO1 = A's, tmO2 = B's scale map) and
+// are copied to TMEM by tcgen05.cp right before the stage's four MMAs (in issue order with
+// them).  TMEM holds the two 256-column accumulators, so the 12 scale columns of a tile sit in
+// the LAST 12 columns of the other accumulator: the epilogue warps that drain those columns
+// read them first and release them (sf_free) before the next tile's first copy.
+template <int CW, typename OutT, int TK, bool F8 = false, bool MX = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
@@ -421,7 +434,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   uint64_t* empty = bars + P_STAGES;
   uint64_t* tfull = bars + 2 * P_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sf_free = tempty + 2;  // MX: [2] leader, the 4 high-column epilogue warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sf_free + 2);
+  static_assert(!MX || (F8 && (TK == TK_STORE_F32 || TK == TK_STORE_BF16)), "MXFP8: store epilogues");
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -434,7 +449,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   const int KB = (K + BKE - 1) / BKE;
   const int cid = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
-  const bool sk = epi.sk_ws != nullptr;
+  const bool sk = !MX && epi.sk_ws != nullptr;
+  const int rb_a = (M + 127) / 128, rb_b = (N + 127) / 128;  // MX: scale-atom row blocks
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -447,6 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);     // multicast commit
       mbar_init(&tempty[s], 2 * 32 * P_EPI_WARPS);  // epilogue threads of both CTAs (leader's copy is used)
+      mbar_init(&sf_free[s], 2 * (P_EPI_WARPS / 2));
     }
     fence_mbar_init();
   }
@@ -469,10 +486,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         tile_coords(t, num_m, num_n, mb, nb);
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (P_STAGE_BYTES + (MX ? P_SF_STAGE : 0)));
           else mbar_arrive_cluster(&full[stage], 0);
           tma_load_2d_pair(sA + stage * P_A_BYTES, &tmA, &full[stage], kb * BKE, mb * 256 + rank * 128);
           tma_load_2d_pair(sB + stage * P_B_BYTES, &tmB, &full[stage], kb * BKE, nb * 256 + rank * 128);
+          if (MX) {  // scale atoms [k-block][row block] of 512 B = 4 rows of the 128-byte-wide maps
+            uint8_t* sf = smem + P_OFF_SF + stage * P_SF_STAGE;
+            tma_load_2d_pair(sf, &tmO1, &full[stage], 0, (kb * rb_a + mb * 2 + int(rank)) * 4);
+            tma_load_2d_pair(sf + 512, &tmO2, &full[stage], 0, (kb * rb_b + nb * 2) * 4);
+          }
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -487,21 +509,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int ntile = 0;  // tiles issued by this pair
       PairSched ps(tiles, KB, nclusters, cid, sk);
       int t, k0, k1;
       while (ps.next(t, k0, k1)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
+        const uint32_t sf_tmem = tmem_base + (acc ^ 1) * 256 + 244;  // MX: [SFA 4 | SFB 8] columns
+        if (MX && ntile > 0) {  // the previous tile's epilogue has read its last 32 columns
+          mbar_wait(&sf_free[acc ^ 1], ((ntile - 1) >> 1) & 1);
+          tc_fence_after();
+        }
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a0 = smem_u32(sA + stage * P_A_BYTES);
             const uint32_t b0 = smem_u32(sB + stage * P_B_BYTES);
+            if constexpr (MX) {
+              const uint32_t sf = smem_u32(smem + P_OFF_SF + stage * P_SF_STAGE);
+              tc_cp_32x128b_x4_pair(sf_tmem, sdesc_noswz(sf, 128, 128));
+              tc_cp_32x128b_x4_pair(sf_tmem + 4, sdesc_noswz(sf + 512, 128, 128));
+              tc_cp_32x128b_x4_pair(sf_tmem + 8, sdesc_noswz(sf + 1024, 128, 128));
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of each 128-byte row
-              if (F8)
+              if (MX)
+                tc_mma_mxf8_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024),
+                                 idesc_mxf8(256, 256, k, k), sf_tmem, sf_tmem + 4, (kb > k0 || k > 0));
+              else if (F8)
                 tc_mma_f8_pair(d_tmem, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                                (kb > k0 || k > 0));
               else
@@ -519,6 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
+        ++ntile;
       }
     }
   } else if (warp >= 4) {
@@ -581,8 +619,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       };
       // dequantisation: per-tensor A and B scales, or this thread's row scale of A (R29)
       const int frow = min(mb * 256 + int(rank) * 128 + ew * 32 + lane, M - 1);
-      const float f8a = F8 ? (epi.f8_row ? __ldg(epi.f8_row + frow) : __ldg(epi.f8_scale[0])) * __ldg(epi.f8_scale[1])
-                           : 1.f;
+      const float f8a = (F8 && !MX)
+                            ? (epi.f8_row ? __ldg(epi.f8_row + frow) : __ldg(epi.f8_scale[0])) * __ldg(epi.f8_scale[1])
+                            : 1.f;
+      // MX: the high-column warps drain their last chunk (the columns the next tile's scale
+      // factors overwrite) first and release it
+      const bool sf_first = MX && eh == 1;
+      auto sf_release = [&]() {
+        if (sf_first) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&sf_free[acc], 0);
+        }
+      };
       auto f8_scale_acc = [&](float* vv, int n) {
 #pragma unroll
         for (int i = 0; i < n; ++i) vv[i] *= f8a;
@@ -632,11 +681,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         }
       } else if (TK == TK_STORE_F32 || TK == TK_GRES) {
 #pragma unroll 1
-        for (int c = c_lo; c < c_hi; c += 32) {
+        for (int ci = 0; ci < 4; ++ci) {
+          const int c = c_lo + 32 * (sf_first ? (ci + 3) & 3 : ci);
           const int n0 = nb * 256 + c;
-          if (n0 >= N) break;
+          if (!MX && n0 >= N) break;
           tmem_ld32(trow + c, v);
           tc_wait_ld();
+          if (ci == 0) sf_release();
+          if (n0 >= N) continue;
           if (fix) fixup(v, c, 32);
           if (F8) f8_scale_acc(v, 32);
 #pragma unroll
@@ -674,13 +726,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         }
       } else if (TK == TK_STORE_BF16) {
 #pragma unroll 1
-        for (int c = c_lo; c < c_hi; c += 64) {
+        for (int ci = 0; ci < 2; ++ci) {
+          const int c = c_lo + 64 * (sf_first ? ci ^ 1 : ci);
           const int n0 = nb * 256 + c;
-          if (n0 >= N) break;
+          if (!MX && n0 >= N) break;
           float w[64];
           tmem_ld32(trow + c, w);
           tmem_ld32(trow + c + 32, w + 32);
           tc_wait_ld();
+          if (ci == 0) sf_release();
+          if (n0 >= N) continue;
           if (fix) fixup(w, c, 64);
           if (F8) f8_scale_acc(w, 64);
           uint8_t* buf = stage_acquire();
@@ -848,13 +903,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   }
 }
 
-template <int CW, typename OutT, int TK, bool F8 = false>
+template <int CW, typename OutT, int TK, bool F8 = false, bool MX = false>
 static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap* to, int M, int N, int K,
                               const Epi& epi, cudaStream_t st) {
-  auto kern = gemm_tc2_kernel<CW, OutT, TK, F8>;
+  auto kern = gemm_tc2_kernel<CW, OutT, TK, F8, MX>;
+  constexpr int smem = MX ? P_SMEM_MX : P_SMEM;
+  static_assert(smem <= 232448, "gemm_tc2 shared memory");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -866,7 +923,7 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms());
     cfg.blockDim = dim3(P_THREADS);
-    cfg.dynamicSmemBytes = P_SMEM;
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -896,7 +953,7 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
   // neutral to negative on K = 3072 and on the two-pass head epilogue -> default on for
   // EPI_GRES with >= 96 k-blocks only; DF_GEMM_SK=1 takes it wherever the waves are ragged
   const bool sk_auto = epi.kind == EPI_GRES && (K + GBK - 1) / GBK >= 96;
-  const bool use_sk = (sk_env || epi.sk_force || sk_auto) && epi.sk_ws && epi.sk_flag && tiles >= pairs &&
+  const bool use_sk = !MX && (sk_env || epi.sk_force || sk_auto) && epi.sk_ws && epi.sk_flag && tiles >= pairs &&
                       tiles % pairs && double(tiles) / (double(waves) * pairs) < 0.92;
   if (use_sk) {
     static std::atomic<unsigned> epoch{0};
@@ -908,11 +965,11 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
   }
   void* args[] = {(void*)&ta, (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2],
                   (void*)&M,  (void*)&N,  (void*)&K,     (void*)&ep};
-  return launch_ex((const void*)kern, dim3(grid), dim3(P_THREADS), P_SMEM, st, args);
+  return launch_ex((const void*)kern, dim3(grid), dim3(P_THREADS), smem, st, args);
 }
 
 bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
-               const uint64_t* strides_bytes, const uint32_t* box);
+               const uint64_t* strides_bytes, const uint32_t* box, bool swz128);
 
 template <bool F8 = false>
 static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
@@ -1169,6 +1226,50 @@ cudaError_t epi_rows(const float* tmp, const Epi& epi, int out_f32, cudaStream_t
   DF_EPI_CASE(128)
 #undef DF_EPI_CASE
   return cudaErrorInvalidValue;
+}
+
+// MXFP8 GEMM (NEXT-4, R30): out[M, N] = sum_k dec(qa)[m, k] 2^(sa[m, k/32] - 127) *
+// dec(qb)[n, k] 2^(sb[n, k/32] - 127), fp32 accumulation on the tensor cores
+// (kind::mxf8f6f4.block_scale, CTA pairs, 256 x 256 tiles), fp32 or bf16 out through the
+// TMA-store epilogue.  qa [M, K], qb [N, K] e4m3 (K contiguous); sa / sb the E8M0 scale bytes
+// in the tiled layout mx_quant_e4m3 writes (df.h).  K % 128 == 0; M, N >= 256.
+cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, const uint8_t* sb, int M, int N, int K,
+                      void* out, int ldo, int out_f32, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if (K % 128 || M < 256 || N < 256 || !qa || !qb || !sa || !sb || !out || ldo < N) return cudaErrorInvalidValue;
+  if ((out_f32 && ldo % 4) || (!out_f32 && ldo % 8)) return cudaErrorInvalidValue;
+  CUtensorMap ta, tb, to[3];
+  std::memset(to, 0, sizeof(to));
+  const uint32_t box_q[2] = {128, 128};
+  const uint64_t da[2] = {uint64_t(K), uint64_t(M)}, db[2] = {uint64_t(K), uint64_t(N)}, sq[1] = {uint64_t(K)};
+  if (!make_tmap(&ta, qa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, da, sq, box_q)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tb, qb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, db, sq, box_q)) return cudaErrorInvalidValue;
+  // scale atoms viewed as rows of 128 bytes: [K / 128][row blocks][4 rows]
+  const uint64_t KG = uint64_t(K / 128), RBa = uint64_t((M + 127) / 128), RBb = uint64_t((N + 127) / 128);
+  const uint64_t dsa[2] = {128, KG * RBa * 4}, dsb[2] = {128, KG * RBb * 4}, s128[1] = {128};
+  const uint32_t box_sa[2] = {128, 4}, box_sb[2] = {128, 8};
+  // unswizzled: the atom must land byte for byte (tcgen05.cp reads it as four 8 x 16-byte core matrices)
+  if (!make_tmap(&to[1], sa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsa, s128, box_sa, false)) return cudaErrorInvalidValue;
+  if (!make_tmap(&to[2], sb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsb, s128, box_sb, false)) return cudaErrorInvalidValue;
+  Epi epi;
+  std::memset(&epi, 0, sizeof(epi));
+  epi.kind = EPI_STORE;
+  epi.M = M;
+  epi.N = N;
+  epi.act = ACT_NONE;
+  epi.out = out;
+  epi.ldo = ldo;
+  const uint64_t dims[2] = {uint64_t(N), uint64_t(M)};
+  if (out_f32) {
+    const uint32_t box[2] = {32, 32};
+    const uint64_t str[1] = {uint64_t(ldo) * 4};
+    if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box)) return cudaErrorInvalidValue;
+    return launch_tc2<32, float, TK_STORE_F32, true, true>(ta, tb, to, M, N, K, epi, st);
+  }
+  const uint32_t box[2] = {64, 32};
+  const uint64_t str[1] = {uint64_t(ldo) * 2};
+  if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box)) return cudaErrorInvalidValue;
+  return launch_tc2<32, bf16, TK_STORE_BF16, true, true>(ta, tb, to, M, N, K, epi, st);
 }
 
 }  // namespace df

@@ -17,6 +17,11 @@ extern int g_disable_pair;  // 1: never use the CTA-pair GEMM (tests)
 // BN in {64, 128, 256}.  Returns cudaError_t of the launch.
 // e4m3 (NEXT-4): per-tensor quantiser (3 launches) and the CTA-pair e4m3 GEMM
 cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaStream_t st);
+// MXFP8 (NEXT-4, R30): OCP MX quantiser (E4M3 elements, 32-element blocks, tiled E8M0 scale
+// bytes) and the block-scaled CTA-pair GEMM (kind::mxf8f6f4.block_scale)
+cudaError_t mx_quant_e4m3(const bf16* x, int M, int K, uint8_t* q, uint8_t* sf, cudaStream_t st);
+cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, const uint8_t* sb, int M, int N, int K,
+                      void* out, int ldo, int out_f32, cudaStream_t st);
 // FP8 step (R29): e4m3 A with per-row scales x e4m3 W with a per-tensor scale, through the
 // bf16 path's TMA-store epilogues (heads / SwiGLU / stores / gated residual)
 cudaError_t gemm_e4m3_epi(const uint8_t* qa, const float* a_row, const uint8_t* qw, const float* w_scale, int M, int N,

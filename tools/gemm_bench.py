@@ -53,6 +53,30 @@ def fp8_shape(c, name, A, W, M, N, K, no_cublas):
     print(row, flush=True)
 
 
+def mx_shape(c, name, A, W, M, N, K, no_cublas):
+    """NEXT-4 MXFP8 (R30): OCP MX e4m3 operands with E8M0 block-32 scales (df_op_mx_quant_e4m3),
+    the block-scaled GEMM (df_op_gemm_mxf8), bf16 out; the per-tensor e4m3 GEMM on the same
+    shape for comparison."""
+    sfn = lambda R: (K // 128) * ((R + 127) // 128) * 512
+    qa = torch.empty(M, K, dtype=torch.uint8, device="cuda")
+    qb = torch.empty(N, K, dtype=torch.uint8, device="cuda")
+    sa = torch.empty(sfn(M), dtype=torch.uint8, device="cuda")
+    sb = torch.empty(sfn(N), dtype=torch.uint8, device="cuda")
+    ms_q = timeit(lambda: c.op_mx_quant_e4m3(A, qa, sa))
+    c.op_mx_quant_e4m3(W, qb, sb)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    ms_mx = timeit(lambda: c.op_gemm_mxf8(qa, sa, qb, sb, out))
+    fl = 2.0 * M * N * K
+    ref = A.float() @ W.float().t()
+    err = ((out.float() - ref).norm() / ref.norm()).item()
+    one = torch.ones(1, device="cuda")
+    out2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    ms_pt = timeit(lambda: c.op_gemm_e4m3(qa, qb, one, one, out2))
+    print({"shape": name, "dtype": "mxf8", "M": M, "N": N, "K": K, "mx_tflops": round(fl / ms_mx / 1e9, 1),
+           "e4m3_per_tensor_tflops": round(fl / ms_pt / 1e9, 1), "rel_err_vs_bf16_product": f"{err:.2e}",
+           "quant_A_gbs": round(A.numel() * (3 + 1 / 32) / ms_q / 1e6, 1)}, flush=True)
+
+
 def main():
     import argparse
     ap = argparse.ArgumentParser()
@@ -60,6 +84,7 @@ def main():
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--tc", type=int, default=1, help="2: allow the stream-K schedule")
     ap.add_argument("--fp8", action="store_true", help="e4m3 GEMM (df_op_gemm_e4m3) vs cuBLASLt torch._scaled_mm")
+    ap.add_argument("--mx", action="store_true", help="MXFP8 block-scaled GEMM (df_op_gemm_mxf8)")
     a = ap.parse_args()
     g = B.make_graph(TINY, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)])
     with B.Context(g) as c:
@@ -68,6 +93,10 @@ def main():
                 continue
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+            if a.mx:
+                mx_shape(c, name, A, W, M, N, K, a.no_cublas)
+                del A, W
+                continue
             if a.fp8:
                 fp8_shape(c, name, A, W, M, N, K, a.no_cublas)
                 del A, W
