@@ -356,7 +356,7 @@ def run_ours(args, cfg):
     inst = [(local if i[2] == rank else 0, i[1], i[2])
             for i in layouts.partitioned(world, args.exclusive, args.t_per_gpu)]
     shm = f"/df_bench_{os.environ.get('MASTER_PORT', '0')}_{os.getuid()}"
-    prec = B.DF_FP8 if args.precision == "fp8" else B.DF_BF16
+    prec = {"fp8": B.DF_FP8, "mxfp8": B.DF_MXFP8}.get(args.precision, B.DF_BF16)
     g = B.make_graph(cfg, inst, precision=prec, weight_seed=0,
                      chunk_bytes=(args.chunk_ctx, args.chunk_lat), n_slots=2,
                      handoff_mode=B.DF_ASYNC | B.DF_HASH, ring_capacity=256, max_steps=cfg.steps,
@@ -461,7 +461,7 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         s = oracle_sample(cfg)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "oracle", "sample": s["sample"]}
-    video = fp8 = None
+    video = fp8 = mxfp8 = None
     if world == 1 and args.config == "image" and args.video_requests > 0 and prec == B.DF_BF16:
         # the north_star's headline shape (BASELINE configs[2], C3): 1 warm-up + K timed 50-step requests
         video = sub_record(args, peaks, local, CONFIGS["video"], B.DF_BF16, 1, args.video_requests,
@@ -470,13 +470,19 @@ def run_ours(args, cfg):
         # NEXT-4 (R29): the same image workload with the FP8 step mode (QKV, cross-Q and MLP-up
         # on e4m3 operands); dtype stays bf16 for the headline above -- this is a separate line
         fp8 = sub_record(args, peaks, local, cfg, B.DF_FP8, args.warmup, args.fp8_requests,
-                         "text-to-image (C2), FP8 step mode (R29): e4m3 QKV / cross-Q / MLP-up")
-        fp8["dtype"] = "e4m3 x e4m3 -> fp32 (3 GEMM classes), bf16 elsewhere"
+                         "text-to-image (C2), FP8 step mode (R29): e4m3 operands on the six block GEMMs")
+        fp8["dtype"] = "e4m3 x e4m3 -> fp32 (six block GEMMs, per-row / per-tensor scales), bf16 elsewhere"
+    if world == 1 and args.config == "image" and args.mxfp8_requests > 0 and prec == B.DF_BF16:
+        # NEXT-4 (R31): the same image workload with MXFP8 block-scaled operands on the six block GEMMs
+        mxfp8 = sub_record(args, peaks, local, cfg, B.DF_MXFP8, args.warmup, args.mxfp8_requests,
+                           "text-to-image (C2), MXFP8 step mode (R31): OCP MX e4m3 block-32 scales, six block GEMMs")
+        mxfp8["dtype"] = "MXFP8 (e4m3 + E8M0 block-32 scales) -> fp32 (six block GEMMs), bf16 elsewhere"
     gE, gT, gD = layouts.ratio(inst)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / n_total, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16" if prec == B.DF_BF16 else "e4m3 block GEMMs (R29), bf16 elsewhere", "data": "synthetic",
+        "dtype": {B.DF_BF16: "bf16", B.DF_FP8: "e4m3 block GEMMs (R29), bf16 elsewhere"}.get(
+            prec, "MXFP8 block GEMMs (R31), bf16 elsewhere"), "data": "synthetic",
         "config": {"workload": workload_name(cfg),
                    "layout": ("E+T+D co-resident on GPU 0" if world == 1 else
                               f"stage-partitioned, one process per GPU: E on GPU 0, D on GPU {world - 1}, "
@@ -503,6 +509,8 @@ def run_ours(args, cfg):
         line["video"] = video
     if fp8 is not None:
         line["fp8"] = fp8
+    if mxfp8 is not None:
+        line["mxfp8"] = mxfp8
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -526,8 +534,10 @@ def main():
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     ap.add_argument("--video-requests", type=int, default=1,
                     help="N=1 image run: timed C3 (video) requests in the line's `video` sub-record (0: skip)")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8"],
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8", "mxfp8"],
                     help="the headline run's DiT precision (fp8: the R29 step mode; not a bf16 number)")
+    ap.add_argument("--mxfp8-requests", type=int, default=5,
+                    help="N=1 image run: timed requests of the MXFP8 step mode in the line's `mxfp8` sub-record (0: skip)")
     ap.add_argument("--fp8-requests", type=int, default=5,
                     help="N=1 image run: timed requests of the FP8 step mode in the line's `fp8` sub-record (0: skip)")
     ap.add_argument("--dit-steps", type=int, default=0,

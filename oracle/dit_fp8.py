@@ -19,7 +19,11 @@ format and per-tensor current scaling, oracle/fp8.py):
 Pinned by tests/test_oracle_fp8.py: quantize_rows' closed forms (a row whose amax is 448
 keeps its e4m3-representable values; a zero row; power-of-two row scaling moves only the
 scale), and the wiring -- block(..., q8=Q8 with identity quantisers) is dit.block exactly,
-so the FP8 mode differs from the pinned bf16 composition only where R29 says.
+so the FP8 mode differs from the pinned bf16 composition only where R29 says.  The MXFP8 mode
+(R31, below) reuses the same wiring with R30's block quantisers; mx_weight is pinned by its
+orientation (scaling one output column by 2^k scales only that column's dequantised weight,
+which neither per-tensor scaling nor blocks along N would do) and mx_act by the MX closed forms
+of oracle/fp8.py.
 """
 from __future__ import annotations
 
@@ -84,3 +88,31 @@ class Q8:
 def step(P, cfg, x, i, cond, sig):
     """One FP8-mode denoising step: (x_{i+1}, v_i)."""
     return dit.step(P, cfg, x, i, cond, sig, q8=Q8())
+
+
+# ---------------------------------------------------------------- MXFP8 step mode (R31)
+# Same six GEMMs as R29, with R30's MXFP8 (OCP MX, E4M3 elements, one E8M0 scale per 32
+# consecutive k) on both operands instead of per-row / per-tensor scaling: the activation is
+# rounded to fp32 (the kernel quantises the fp32 RMSNorm output, or the bf16 attention / SwiGLU
+# output, which is exact in fp32) and block-quantised along K; a weight W [K, N] is
+# block-quantised along K per output column (the GPU quantises W^T [N, K] row by row).
+def mx_act(h):
+    """The activation as the MXFP8 GEMM sees it."""
+    h32 = np.asarray(h, dtype=np.float64).astype(np.float32).astype(np.float64)
+    q, s = fp8.mx_quantize(h32)
+    return fp8.mx_dequantize(q, s)
+
+
+def mx_weight(W):
+    """W [K, N] as the MXFP8 GEMM sees it (blocks along K of each output column)."""
+    q, s = fp8.mx_quantize(np.asarray(W, dtype=np.float64).T)
+    return fp8.mx_dequantize(q, s).T
+
+
+def Q8MX():
+    return Q8(act_fn=mx_act, weight_fn=mx_weight)
+
+
+def step_mx(P, cfg, x, i, cond, sig):
+    """One MXFP8-mode denoising step: (x_{i+1}, v_i)."""
+    return dit.step(P, cfg, x, i, cond, sig, q8=Q8MX())

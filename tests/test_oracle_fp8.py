@@ -210,3 +210,36 @@ def test_gemm_mxf8_bruteforce():
                        (fp8.e4m3_decode(qb[j, k:k + 1])[0] * 2.0 ** (int(sb[j, k // 32]) - 127))
             want[i, j] = acc
     np.testing.assert_allclose(fp8.gemm_mxf8(qa, sa, qb, sb), want, rtol=1e-13, atol=1e-12)
+
+
+def test_mx_weight_blocks_run_along_k_per_output_column():
+    """R31: W [K, N] is block-quantised along K for each output column.  Scaling column j by 2^k
+    must scale exactly that column of the dequantised weight (per-tensor scaling, or blocks
+    along N, would change other columns' codes)."""
+    from oracle import dit_fp8
+    r = np.random.default_rng(7)
+    W = r.standard_normal((64, 8))
+    base = dit_fp8.mx_weight(W)
+    W2 = W.copy()
+    W2[:, 3] *= 2.0 ** 9
+    got = dit_fp8.mx_weight(W2)
+    want = base.copy()
+    want[:, 3] *= 2.0 ** 9
+    np.testing.assert_array_equal(got, want)
+    # blocks are 32 long along K: a spike in rows 0..31 of column 5 leaves rows 32..63 alone
+    W3 = W.copy()
+    W3[0, 5] = 1e4
+    got3 = dit_fp8.mx_weight(W3)
+    np.testing.assert_array_equal(got3[32:, 5], base[32:, 5])
+    assert not np.array_equal(got3[1:32, 5], base[1:32, 5])
+
+
+def test_mx_act_rounds_to_fp32_then_blocks_rows():
+    from oracle import dit_fp8
+    r = np.random.default_rng(8)
+    h = r.standard_normal((3, 64)) * 3
+    h[1] *= 2.0 ** 20  # rows are independent
+    got = dit_fp8.mx_act(h)
+    q, s = fp8.mx_quantize(h.astype(np.float32).astype(np.float64))
+    np.testing.assert_array_equal(got, fp8.mx_dequantize(q, s))
+    np.testing.assert_array_equal(dit_fp8.mx_act(h[[0]]), got[[0]])
