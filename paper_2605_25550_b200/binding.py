@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libdf.so")
 DF_OK, DF_AGAIN, DF_EMPTY = 0, 1, 2
 DF_ERR_INVALID, DF_ERR_CAPACITY, DF_ERR_NOMEM, DF_ERR_DUPLICATE, DF_ERR_STATE = 10, 11, 12, 13, 14
 DF_E, DF_T, DF_D = 0, 1, 2
-DF_BF16, DF_FP32_VALIDATION, DF_FP8 = 0, 1, 2
+DF_BF16, DF_FP32_VALIDATION, DF_FP8, DF_MXFP8 = 0, 1, 2, 3
 DF_ASYNC, DF_SYNC, DF_PERMUTE, DF_HASH, DF_LATENT_BLOCKS = 0, 1, 2, 4, 8
 DF_ALL_CHUNKS = 0xFFFFFFFF
 DF_MAX_INST = 32

@@ -813,10 +813,13 @@ struct AttnSkCfg {
   static constexpr int OFF_RED = OFF_BAR + 512;       // [2 block parity][4 col group][128 rows] row max
   static constexpr int OFF_LRED = OFF_RED + 4096;     // [2 tile parity][4 col group][128 rows] row sum
   static constexpr int SMEM = OFF_LRED + 4096 + 1024;
-  static constexpr uint32_t S_COL = 0, O_COL = 256;
+  static constexpr uint32_t S_COL = 0;
 };
 
-template <int EXPM>
+// SD = depth of the S ring in TMEM (S0, S1 + O double-buffered per tile).  A depth-3 ring with
+// a single O (QK^T one block further ahead, the tile's epilogue gating the next tile's first PV)
+// was measured 13-20 % slower and removed.
+template <int EXPM, int SD = 2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
     attn_sk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
@@ -835,13 +838,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
   uint64_t* k_empty = bars + 8;       // [4]  both (commit after the head segment's last QK of the block)
   uint64_t* v_full = bars + 12;       // [4]  leader
   uint64_t* v_empty = bars + 16;      // [4]  both
-  uint64_t* s_full = bars + 20;       // [2]  both
-  uint64_t* pv_done = bars + 22;      // [2]  both (per PV block, read only by a rescale)
-  uint64_t* o_done = bars + 24;       // [2]  both (tile's last PV)
-  uint64_t* o_free = bars + 26;       // [2]  leader: 4 epilogue warps x 2 CTAs
-  uint64_t* l_full = bars + 28;       // [2]  local: 16 softmax warps
-  uint64_t* p_q = bars + 30;          // [2 S slot][4 quarter] leader: 4 warps x 2 CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 38);
+  uint64_t* s_full = bars + 20;       // [SD] both
+  uint64_t* pv_done = bars + 23;      // [2]  both (per PV block, read only by a rescale)
+  uint64_t* o_done = bars + 25;       // [NO] both (tile's last PV)
+  uint64_t* o_free = bars + 27;       // [NO] leader: 4 epilogue warps x 2 CTAs
+  uint64_t* l_full = bars + 29;       // [2]  local: 16 softmax warps
+  uint64_t* p_q = bars + 31;          // [SD S slot][4 quarter] leader: 4 warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 43);
+  constexpr int NO = SD == 2 ? 2 : 1;             // O buffers
+  constexpr uint32_t O_COL = uint32_t(SD) * 128;  // O after the S ring
   float* red = reinterpret_cast<float*>(smem + Cfg::OFF_RED);
   float* lred = reinterpret_cast<float*>(smem + Cfg::OFF_LRED);
 
@@ -866,11 +871,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 2);
       mbar_init(&q_empty[s], 1);
-      mbar_init(&s_full[s], 1);
       mbar_init(&pv_done[s], 1);
+      mbar_init(&l_full[s], 16);
+    }
+    for (int s = 0; s < SD; ++s) mbar_init(&s_full[s], 1);
+    for (int s = 0; s < NO; ++s) {
       mbar_init(&o_done[s], 1);
       mbar_init(&o_free[s], 8);
-      mbar_init(&l_full[s], 16);
     }
     for (int j = 0; j < Cfg::NKB; ++j) {
       mbar_init(&k_full[j], 2);
@@ -878,7 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
       mbar_init(&v_full[j], 2);
       mbar_init(&v_empty[j], 1);
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&p_q[i], 8);
+    for (int i = 0; i < 4 * SD; ++i) mbar_init(&p_q[i], 8);
     fence_mbar_init();
   }
   if (warp == 21) tmem_alloc_pair(tmem_slot, 512);
@@ -945,10 +952,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k)
-            tc_mma_bf16_pair(tmem + Cfg::S_COL + (b & 1) * 128,
+            tc_mma_bf16_pair(tmem + Cfg::S_COL + (b % SD) * 128,
                              a0 + uint64_t(((k >> 2) * 2 * Cfg::ATOM + (k & 3) * 32) >> 4),
                              b0 + uint64_t(((k >> 2) * Cfg::ATOM + (k & 3) * 32) >> 4), idesc_qk, k > 0);
-          tc_commit_pair(&s_full[b & 1], 0x3);
+          tc_commit_pair(&s_full[b % SD], 0x3);
           if (j == nkb - 1) tc_commit_pair(&q_empty[n & 1], 0x3);
           if (seg_last(n)) tc_commit_pair(&k_empty[j], 0x3);
         }
@@ -956,14 +963,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
       };
       auto issue_pv = [&](int b) {
         const int n = b / nkb, j = b - n * nkb;
-        if (j == 0 && n >= 2) mbar_wait(&o_free[n & 1], ((n - 2) >> 1) & 1);  // O[n & 1] read out
+        if (j == 0 && n >= NO) mbar_wait(&o_free[n % NO], ((n - NO) / NO) & 1);  // O[n % NO] read out
         mbar_wait(&v_full[j], (head_of(n) - h0) & 1);
         const uint64_t b0 = dv + uint64_t((j * Cfg::V_BYTES) >> 4);
-        const uint32_t d = tmem + Cfg::O_COL + (n & 1) * DH;
-        const uint32_t pa = tmem + Cfg::S_COL + (b & 1) * 128;
+        const uint32_t d = tmem + O_COL + (n % NO) * DH;
+        const uint32_t pa = tmem + Cfg::S_COL + (b % SD) * 128;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          mbar_wait(&p_q[(b & 1) * 4 + u], (b >> 1) & 1);
+          mbar_wait(&p_q[(b % SD) * 4 + u], (b / SD) & 1);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
@@ -976,16 +983,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
         }
         if (elect_one()) {
           tc_commit_pair(&pv_done[b & 1], 0x3);
-          if (j == nkb - 1) tc_commit_pair(&o_done[n & 1], 0x3);
+          if (j == nkb - 1) tc_commit_pair(&o_done[n % NO], 0x3);
           if (seg_last(n)) tc_commit_pair(&v_empty[j], 0x3);
         }
         __syncwarp();
       };
-      if (nb > 0) issue_qk(0);
-      if (nb > 1) issue_qk(1);
+      for (int b = 0; b < SD && b < nb; ++b) issue_qk(b);
       for (int b = 0; b < nb; ++b) {
         issue_pv(b);
-        if (b + 2 < nb) issue_qk(b + 2);  // S[b & 1] is free once PV(b) has read P(b) (in-order pipe)
+        if (b + SD < nb) issue_qk(b + SD);  // S[b % SD] is free once PV(b) has read P(b) (in-order pipe)
       }
     }
   } else if (warp >= 16) {
@@ -995,7 +1001,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
     for (int n = 0; n < T; ++n) {
       mbar_wait(&l_full[n & 1], (n >> 1) & 1);
-      mbar_wait(&o_done[n & 1], (n >> 1) & 1);
+      mbar_wait(&o_done[n % NO], (n / NO) & 1);
       tc_fence_after();
       const float* lr = lred + (n & 1) * 512 + r;
       const float inv = 1.0f / ((lr[0] + lr[128]) + (lr[256] + lr[384]));
@@ -1003,7 +1009,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
       const int q = qt * 256 + int(rank) * 128 + r;
       const int hb = h / Hs, hl = h - hb * Hs;
       bf16* orow = O + (size_t(hb) * Nq + q) * Hs * DH + size_t(hl) * DH;
-      const uint32_t to = tmem + lane_off + Cfg::O_COL + (n & 1) * DH;
+      const uint32_t to = tmem + lane_off + O_COL + (n % NO) * DH;
 #pragma unroll 1
       for (int c = 0; c < DH; c += 32) {
         float o[32];
@@ -1017,7 +1023,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&o_free[n & 1], 0);
+      if (lane == 0) mbar_arrive_cluster(&o_free[n % NO], 0);
     }
   } else {
     // softmax: warp (cg, ew) owns key columns [32 cg, 32 cg + 32) of rows ew*32 .. ew*32+31
@@ -1027,10 +1033,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
     int b = 0;
     for (int n = 0; n < T; ++n) {
       float m_used = -INFINITY, l = 0.f;
-      const uint32_t to = tmem + lane_off + Cfg::O_COL + (n & 1) * DH + 32 * cg;
+      const uint32_t to = tmem + lane_off + O_COL + (n % NO) * DH + 32 * cg;
       for (int j = 0; j < nkb; ++j, ++b) {
-        const uint32_t ts = tmem + lane_off + Cfg::S_COL + (b & 1) * 128;
-        mbar_wait(&s_full[b & 1], (b >> 1) & 1);
+        const uint32_t ts = tmem + lane_off + Cfg::S_COL + (b % SD) * 128;
+        mbar_wait(&s_full[b % SD], (b / SD) & 1);
         tc_fence_after();
         float s[32];
         tmem_ld32(ts + 32 * cg, s);
@@ -1081,7 +1087,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN_SK_THREADS, 1)
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&p_q[(b & 1) * 4 + cg], 0);
+        if (lane == 0) mbar_arrive_cluster(&p_q[(b % SD) * 4 + cg], 0);
       }
       lred[(n & 1) * 512 + cg * 128 + r] = l;
       __syncwarp();
@@ -1104,9 +1110,7 @@ static cudaError_t launch_attn_sk(const bf16* Q, const bf16* K, const bf16* V, b
   if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
       !make_tmap_3d(&tv, V, H, Nk, 128, 128))
     return cudaErrorInvalidValue;
-  static const int expm = attn_expm();
-  auto kern = expm == 4 ? attn_sk_kernel<4> : expm == 5 ? attn_sk_kernel<5> : expm == 1 ? attn_sk_kernel<1>
-              : expm == 3 ? attn_sk_kernel<3> : attn_sk_kernel<2>;
+  auto kern = attn_sk_kernel<2>;
   static int max_pairs = 0;
   if (!max_pairs) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1134,13 +1138,17 @@ template <int DH>
 static cudaError_t launch_attn(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
                                float scale, cudaStream_t st, int hs) {
   if constexpr (DH == 128) {
-    // N_kv in [257, 512] (cross-attention): K/V-resident short-key kernel; DF_ATTN_SK=0 selects
-    // attn_pp for A/B
-    static const bool sk = [] {
+    // N_kv in [257, 512] (cross-attention) with long per-pair runs (>= 8 query tiles per CTA
+    // pair: the video shape, 69): the K/V-resident short-key kernel, 4-5 % faster in the step;
+    // with few tiles per pair (image, 5.2) attn_pp's items are 3 % faster.
+    // DF_ATTN_SK=0 / 2 forces attn_pp / attn_sk for A/B.
+    static const int sk = [] {
       const char* e = getenv("DF_ATTN_SK");
-      return e ? atoi(e) != 0 : true;
+      return e ? atoi(e) : 1;
     }();
-    if (g_attn_impl != 2 && sk && dh == 128 && Nk > 256 && Nk <= 512)
+    const long long sk_tiles = (long long)((Nq + 255) / 256) * H;
+    if (g_attn_impl != 2 && sk && dh == 128 && Nk > 256 && Nk <= 512 &&
+        (sk == 2 || sk_tiles >= 8LL * (num_sms() / 2)))
       return launch_attn_sk(Q, K, V, O, H, Nq, Nk, scale, st, hs);
     if (g_attn_impl != 2) {
       static const int expm = attn_expm();

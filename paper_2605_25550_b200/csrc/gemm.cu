@@ -415,7 +415,7 @@ DF_DEV void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  /
 // descriptors and stage bytes are those of the bf16 kernel; only the k-block extent, the
 // MMA kind and the dequantisation scale in the epilogue change.
 // MX (with F8): MXFP8 block-scaled operands (R30, kind::mxf8f6f4.block_scale).  The E8M0 scale
-// atoms of each k-block arrive by TMA with the operands (tmO1 = A's, tmO2 = B's scale map) and
+// atoms of each k-block arrive by TMA with the operands (tmSA = A's, tmSB = B's scale map) and
 // are copied to TMEM by tcgen05.cp right before the stage's four MMAs (in issue order with
 // them).  TMEM holds the two 256-column accumulators, so the 12 scale columns of a tile sit in
 // the LAST 12 columns of the other accumulator: the epilogue warps that drain those columns
@@ -424,7 +424,8 @@ template <int CW, typename OutT, int TK, bool F8 = false, bool MX = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
-                    const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const __grid_constant__ Epi epi) {
+                    const __grid_constant__ CUtensorMap tmO2, const __grid_constant__ CUtensorMap tmSA,
+                    const __grid_constant__ CUtensorMap tmSB, int M, int N, int K, const __grid_constant__ Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS/STS, not generic)
   uint8_t* sA = smem;
@@ -436,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* sf_free = tempty + 2;  // MX: [2] leader, the 4 high-column epilogue warps x 2 CTAs
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sf_free + 2);
-  static_assert(!MX || (F8 && (TK == TK_STORE_F32 || TK == TK_STORE_BF16)), "MXFP8: store epilogues");
+  static_assert(!MX || (F8 && TK != TK_DIRECT), "MXFP8: TMA-store epilogues");
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -492,8 +493,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tma_load_2d_pair(sB + stage * P_B_BYTES, &tmB, &full[stage], kb * BKE, nb * 256 + rank * 128);
           if (MX) {  // scale atoms [k-block][row block] of 512 B = 4 rows of the 128-byte-wide maps
             uint8_t* sf = smem + P_OFF_SF + stage * P_SF_STAGE;
-            tma_load_2d_pair(sf, &tmO1, &full[stage], 0, (kb * rb_a + mb * 2 + int(rank)) * 4);
-            tma_load_2d_pair(sf + 512, &tmO2, &full[stage], 0, (kb * rb_b + nb * 2) * 4);
+            tma_load_2d_pair(sf, &tmSA, &full[stage], 0, (kb * rb_a + mb * 2 + int(rank)) * 4);
+            tma_load_2d_pair(sf + 512, &tmSB, &full[stage], 0, (kb * rb_b + nb * 2) * 4);
           }
           if (++stage == P_STAGES) {
             stage = 0;
@@ -766,13 +767,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll 1
         for (int g = c_lo; g < c_hi; g += 128) {
           const int n0 = nb * 256 + g;
-          if (n0 >= N) break;
+          if (n0 >= N) {
+            sf_release();
+            break;
+          }
           uint8_t* buf = stage_acquire();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int qi = 0; qi < 4; ++qi) {
+            const int q = sf_first ? (qi + 3) & 3 : qi;  // MX: the released columns first
             float a[32];
             tmem_ld32(trow + g + 32 * q, a);
             tc_wait_ld();
+            if (qi == 0) sf_release();
             if (fix) fixup(a, g + 32 * q, 32);
             if (F8) f8_scale_acc(a, 32);
             float w[16];
@@ -814,6 +820,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll 1
         for (int c = c_lo; c < c_hi; c += 128) {
           const int n0 = nb * 256 + c;
+          // MX: this warp's last 32 columns (the next tile's scale-factor columns) go to its
+          // staging tile first (lane-private 128 B) and are released; both passes read them there
+          float* keep = nullptr;
+          if (sf_first) {
+            uint8_t* buf = stage_acquire();
+            float a[32];
+            tmem_ld32(trow + c + 96, a);
+            tc_wait_ld();
+            sf_release();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(swz128(buf, lane, j)) = make_float4(a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+            keep = reinterpret_cast<float*>(buf);
+          }
+          auto ld_keep = [&](float* dst) {  // this lane's kept 32 columns, in column order
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 t = *reinterpret_cast<const float4*>(swz128(reinterpret_cast<uint8_t*>(keep), lane, j));
+              dst[4 * j] = t.x, dst[4 * j + 1] = t.y, dst[4 * j + 2] = t.z, dst[4 * j + 3] = t.w;
+            }
+          };
           if (n0 >= N || row0 >= M) break;
           const int sec = n0 / epi.d;
           const int hd = (n0 - sec * epi.d) / epi.dh;
@@ -825,8 +852,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll 1
             for (int q = 0; q < 128; q += 32) {
               float a[32];
-              tmem_ld32(trow + c + q, a);
-              tc_wait_ld();
+              if (keep && q == 96) {
+                ld_keep(a);
+              } else {
+                tmem_ld32(trow + c + q, a);
+                tc_wait_ld();
+              }
               if (fix) fixup(a, c + q, 32);
               if (F8) f8_scale_acc(a, 32);
 #pragma unroll
@@ -839,11 +870,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           }
           const CUtensorMap* map = sec == 0 ? &tmO0 : (sec == 1 ? &tmO1 : &tmO2);
 #pragma unroll 1
-          for (int hf = 0; hf < 2; ++hf) {
+          for (int hi = 0; hi < 2; ++hi) {
+            const int hf = keep ? hi ^ 1 : hi;  // MX: the half holding the kept columns first
             float w[64];
             tmem_ld32(trow + c + 64 * hf, w);
-            tmem_ld32(trow + c + 64 * hf + 32, w + 32);
-            tc_wait_ld();
+            if (keep && hf == 1) {
+              tc_wait_ld();
+              ld_keep(w + 32);
+            } else {
+              tmem_ld32(trow + c + 64 * hf + 32, w + 32);
+              tc_wait_ld();
+            }
             if (fix) fixup(w, c + 64 * hf, 64);
             if (F8) f8_scale_acc(w, 64);
             const float* pb = s_bias + c + 64 * hf;
@@ -963,41 +1000,46 @@ static cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, cons
     ep.sk_ws = nullptr;
     ep.sk_flag = nullptr;
   }
-  void* args[] = {(void*)&ta, (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2],
-                  (void*)&M,  (void*)&N,  (void*)&K,     (void*)&ep};
+  void* args[] = {(void*)&ta, (void*)&tb, (void*)&to[0], (void*)&to[1], (void*)&to[2], (void*)&to[3],
+                  (void*)&to[4], (void*)&M, (void*)&N, (void*)&K, (void*)&ep};
   return launch_ex((const void*)kern, dim3(grid), dim3(P_THREADS), smem, st, args);
 }
 
 bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,
                const uint64_t* strides_bytes, const uint32_t* box, bool swz128);
 
-template <bool F8 = false>
+template <bool F8 = false, bool MX = false>
 static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& epi,
-                                int out_f32, cudaStream_t st) {
+                                int out_f32, cudaStream_t st, const CUtensorMap* sf_maps = nullptr) {
   static const int tma_epi = [] {  // DF_GEMM_TMA_EPI=0: per-thread epilogue stores (A/B)
     const char* e = getenv("DF_GEMM_TMA_EPI");
     return e ? atoi(e) : 1;
   }();
-  CUtensorMap to[3];
+  CUtensorMap to[5];  // outputs 0..2, MXFP8 scale maps 3 (A) and 4 (B)
   std::memset(to, 0, sizeof(to));
+  if (MX) {
+    if (!sf_maps) return cudaErrorInvalidValue;
+    to[3] = sf_maps[0];
+    to[4] = sf_maps[1];
+  }
   if (tma_epi) {
     const uint32_t box_f32[2] = {32, 32}, box_bf16[2] = {64, 32};
     if (epi.kind == EPI_STORE && out_f32 && (epi.ldo % 4) == 0) {
       const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 4};
       if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box_f32))
-        return launch_tc2<32, float, TK_STORE_F32, F8>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, float, TK_STORE_F32, F8, MX>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_STORE && !out_f32 && (epi.ldo % 8) == 0) {
       const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 2};
       if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box_bf16))
-        return launch_tc2<32, bf16, TK_STORE_BF16, F8>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, bf16, TK_STORE_BF16, F8, MX>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_GRES && (epi.ldr % 4) == 0) {
       const uint64_t dims[2] = {uint64_t(N), uint64_t(M)}, str[1] = {uint64_t(epi.ldr) * 4};
       if (make_tmap(&to[0], epi.resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2, dims, str, box_f32))
-        return launch_tc2<32, float, TK_GRES, F8>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, float, TK_GRES, F8, MX>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_SWIGLU && !out_f32 && (epi.ldo % 8) == 0) {
       const uint64_t dims[2] = {uint64_t(N / 2), uint64_t(M)}, str[1] = {uint64_t(epi.ldo) * 2};
       if (make_tmap(&to[0], epi.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box_bf16))
-        return launch_tc2<32, bf16, TK_SWIGLU, F8>(ta, tb, to, M, N, K, epi, st);
+        return launch_tc2<32, bf16, TK_SWIGLU, F8, MX>(ta, tb, to, M, N, K, epi, st);
     } else if (epi.kind == EPI_HEADS && !out_f32 && epi.dh == 128 && epi.dh_pad == 128) {
       const int mper = epi.Mper > 0 ? epi.Mper : M;
       const uint64_t dims[3] = {128, uint64_t(mper), uint64_t(M / mper) * epi.heads};
@@ -1006,7 +1048,7 @@ static cudaError_t dispatch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, in
       bool ok = true;
       for (int s = 0; s < epi.nsec; ++s)
         ok = ok && make_tmap(&to[s], epi.sec_out[s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, dims, str, box);
-      if (ok) return launch_tc2<128, bf16, TK_HEADS, F8>(ta, tb, to, M, N, K, epi, st);
+      if (ok) return launch_tc2<128, bf16, TK_HEADS, F8, MX>(ta, tb, to, M, N, K, epi, st);
     }
   }
   if constexpr (F8) {
@@ -1055,7 +1097,7 @@ cudaError_t gemm_e4m3(const uint8_t* qa, const uint8_t* qb, const float* sa, con
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
   if (K % 16 || M < 256 || N < 256 || !sa || !sb || !out || ldo < N) return cudaErrorInvalidValue;
   if ((out_f32 && ldo % 4) || (!out_f32 && ldo % 8)) return cudaErrorInvalidValue;
-  CUtensorMap ta, tb, to[3];
+  CUtensorMap ta, tb, to[5];
   std::memset(to, 0, sizeof(to));
   const uint32_t box_q[2] = {128, 128};
   const uint64_t da[2] = {uint64_t(K), uint64_t(M)}, db[2] = {uint64_t(K), uint64_t(N)}, sq[1] = {uint64_t(K)};
@@ -1238,7 +1280,7 @@ cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, c
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
   if (K % 128 || M < 256 || N < 256 || !qa || !qb || !sa || !sb || !out || ldo < N) return cudaErrorInvalidValue;
   if ((out_f32 && ldo % 4) || (!out_f32 && ldo % 8)) return cudaErrorInvalidValue;
-  CUtensorMap ta, tb, to[3];
+  CUtensorMap ta, tb, to[5];
   std::memset(to, 0, sizeof(to));
   const uint32_t box_q[2] = {128, 128};
   const uint64_t da[2] = {uint64_t(K), uint64_t(M)}, db[2] = {uint64_t(K), uint64_t(N)}, sq[1] = {uint64_t(K)};
@@ -1249,8 +1291,8 @@ cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, c
   const uint64_t dsa[2] = {128, KG * RBa * 4}, dsb[2] = {128, KG * RBb * 4}, s128[1] = {128};
   const uint32_t box_sa[2] = {128, 4}, box_sb[2] = {128, 8};
   // unswizzled: the atom must land byte for byte (tcgen05.cp reads it as four 8 x 16-byte core matrices)
-  if (!make_tmap(&to[1], sa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsa, s128, box_sa, false)) return cudaErrorInvalidValue;
-  if (!make_tmap(&to[2], sb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsb, s128, box_sb, false)) return cudaErrorInvalidValue;
+  if (!make_tmap(&to[3], sa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsa, s128, box_sa, false)) return cudaErrorInvalidValue;
+  if (!make_tmap(&to[4], sb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsb, s128, box_sb, false)) return cudaErrorInvalidValue;
   Epi epi;
   std::memset(&epi, 0, sizeof(epi));
   epi.kind = EPI_STORE;
@@ -1270,6 +1312,30 @@ cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, c
   const uint64_t str[1] = {uint64_t(ldo) * 2};
   if (!make_tmap(&to[0], out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, dims, str, box)) return cudaErrorInvalidValue;
   return launch_tc2<32, bf16, TK_STORE_BF16, true, true>(ta, tb, to, M, N, K, epi, st);
+}
+
+// The MXFP8 step's GEMMs (R31): MXFP8 A [M, K] and W [N, K] (E8M0 block scales in the tiled
+// layout, as mx_quant_e4m3 / rmsnorm_mx write them) through any TMA-store epilogue of the
+// bf16 path (heads, SwiGLU, stores, gated residual).  K % 128 == 0; M, N >= 256.
+cudaError_t gemm_mxf8_epi(const uint8_t* qa, const uint8_t* sa, const uint8_t* qw, const uint8_t* sw, int M, int N,
+                          int K, const Epi& e, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if (K % 128 || M < 256 || N < 256 || !qa || !sa || !qw || !sw) return cudaErrorInvalidValue;
+  CUtensorMap ta, tb, sf[2];
+  const uint32_t box_q[2] = {128, 128};
+  const uint64_t da[2] = {uint64_t(K), uint64_t(M)}, db[2] = {uint64_t(K), uint64_t(N)}, sq[1] = {uint64_t(K)};
+  if (!make_tmap(&ta, qa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, da, sq, box_q)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tb, qw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, db, sq, box_q)) return cudaErrorInvalidValue;
+  const uint64_t KG = uint64_t(K / 128), RBa = uint64_t((M + 127) / 128), RBb = uint64_t((N + 127) / 128);
+  const uint64_t dsa[2] = {128, KG * RBa * 4}, dsb[2] = {128, KG * RBb * 4}, s128[1] = {128};
+  const uint32_t box_sa[2] = {128, 4}, box_sb[2] = {128, 8};
+  if (!make_tmap(&sf[0], sa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsa, s128, box_sa, false)) return cudaErrorInvalidValue;
+  if (!make_tmap(&sf[1], sw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 2, dsb, s128, box_sb, false)) return cudaErrorInvalidValue;
+  Epi epi = e;
+  epi.f8_row = nullptr;
+  epi.sk_ws = nullptr;
+  epi.sk_flag = nullptr;
+  return dispatch_tc2<true, true>(ta, tb, M, N, K, epi, 0, st, sf);
 }
 
 }  // namespace df

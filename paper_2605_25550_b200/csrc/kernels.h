@@ -20,8 +20,16 @@ cudaError_t quant_e4m3(const bf16* x, size_t n, uint8_t* q, float* scale, cudaSt
 // MXFP8 (NEXT-4, R30): OCP MX quantiser (E4M3 elements, 32-element blocks, tiled E8M0 scale
 // bytes) and the block-scaled CTA-pair GEMM (kind::mxf8f6f4.block_scale)
 cudaError_t mx_quant_e4m3(const bf16* x, int M, int K, uint8_t* q, uint8_t* sf, cudaStream_t st);
+// bytes of the tiled E8M0 scales of an [M, K] MXFP8 matrix: (K / 128) * ceil(M / 128) * 512
+inline size_t mx_sf_bytes(size_t M, size_t K) { return (K / 128) * ((M + 127) / 128) * 512; }
+// RMSNorm + modulation (or gain) with MXFP8 output (R31): codes q [M, d], tiled block scales sf
+cudaError_t rmsnorm_mx(const float* x, uint8_t* q, uint8_t* sf, int M, int d, const float* shift, const float* scale,
+                       const bf16* gain, float eps, cudaStream_t st);
 cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, const uint8_t* sb, int M, int N, int K,
                       void* out, int ldo, int out_f32, cudaStream_t st);
+// MXFP8 step (R31): the block-scaled GEMM through the TMA-store epilogues of the bf16 path
+cudaError_t gemm_mxf8_epi(const uint8_t* qa, const uint8_t* sa, const uint8_t* qw, const uint8_t* sw, int M, int N,
+                          int K, const Epi& e, cudaStream_t st);
 // FP8 step (R29): e4m3 A with per-row scales x e4m3 W with a per-tensor scale, through the
 // bf16 path's TMA-store epilogues (heads / SwiGLU / stores / gated residual)
 cudaError_t gemm_e4m3_epi(const uint8_t* qa, const float* a_row, const uint8_t* qw, const float* w_scale, int M, int N,

@@ -125,6 +125,8 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
   dhp = f32() ? dh : (dh <= 64 ? 64 : 128);
   if (fp8() && stage == DF_T && (c.d < 256 || N < 256 || dh != 128 || c.d % 16))
     return cudaErrorInvalidValue;  // the FP8 GEMMs run on CTA-pair tiles with the head-major TMA epilogue
+  if (mx() && stage == DF_T && (c.d % 128 || c.ffn % 128 || (c.d != 256 && c.d != 3072 && c.d != 5120)))
+    return cudaErrorInvalidValue;  // MX blocks: K % 128 (one scale atom per 128 k); rmsnorm_mx widths
   if (c.d % c.heads || dh > 128 || c.ffn % 16 || c.d % 4 || c.enc_ffn % 16 ||
       c.rope_axes[0] + c.rope_axes[1] + c.rope_axes[2] != uint32_t(dh) ||
       (c.C_y > 0 && (c.L_img == 0 || c.d_img == 0 || c.d_img % 8)))
@@ -190,6 +192,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           al(size_t(c.layers) * 6 * d * 4) + al(2 * d * 4) + al(size_t(Fp + Hp + Wp) * dh / 2 * 8) +
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (fp8()) wsb += al(N2 * std::max(d, f)) + al(N2 * 4);
+    if (mx()) wsb += al(mx_sf_bytes(N2, std::max(d, f)));
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
     else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // GEMM stream-K
   } else if (stage == DF_E) {
@@ -210,6 +213,10 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     if (fp8()) {
       hq = (uint8_t*)ws.take(N2 * std::max(d, f));
       hs = (float*)ws.take(N2 * 4);
+    }
+    if (mx()) {  // rows past M in the last 128-row block keep scale byte 0
+      hsf = (uint8_t*)ws.take(mx_sf_bytes(N2, std::max(d, f)));
+      DF_TRY(cudaMemset(hsf, 0, mx_sf_bytes(N2, std::max(d, f))));
     }
     mods = (float*)ws.take(size_t(c.layers) * 6 * d * 4);
     headmod = (float*)ws.take(2 * d * 4);
@@ -250,6 +257,33 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
 // bf16 weights, so the codes are those of the oracle's quantize_per_tensor; W_1 | W_3 jointly).
 cudaError_t Model::quantize_weights(cudaStream_t st) {
   const size_t d = c.d, f = c.ffn;
+  if (mx()) {  // MXFP8 step (R31): OCP MX codes + tiled block scales of every block GEMM's weight [N, K]
+    const size_t per = al(3 * d * d) + 3 * al(d * d) + 2 * al(2 * f * d) + al(mx_sf_bytes(3 * d, d)) +
+                       3 * al(mx_sf_bytes(d, d)) + al(mx_sf_bytes(2 * f, d)) + al(mx_sf_bytes(d, f));
+    DF_TRY(f8mem.reserve(per * c.layers + 4096));
+    for (auto& l : Lw) {
+      l.qkv_q = (uint8_t*)f8mem.take(3 * d * d);
+      l.cq_q = (uint8_t*)f8mem.take(d * d);
+      l.w13_q = (uint8_t*)f8mem.take(2 * f * d);
+      l.o_q = (uint8_t*)f8mem.take(d * d);
+      l.co_q = (uint8_t*)f8mem.take(d * d);
+      l.w2_q = (uint8_t*)f8mem.take(d * f);
+      l.qkv_sf = (uint8_t*)f8mem.take(mx_sf_bytes(3 * d, d));
+      l.cq_sf = (uint8_t*)f8mem.take(mx_sf_bytes(d, d));
+      l.w13_sf = (uint8_t*)f8mem.take(mx_sf_bytes(2 * f, d));
+      l.o_sf = (uint8_t*)f8mem.take(mx_sf_bytes(d, d));
+      l.co_sf = (uint8_t*)f8mem.take(mx_sf_bytes(d, d));
+      l.w2_sf = (uint8_t*)f8mem.take(mx_sf_bytes(d, f));
+      if (!l.w2_sf) return cudaErrorMemoryAllocation;
+      DF_L(mx_quant_e4m3(l.qkv_wT, int(3 * d), int(d), l.qkv_q, l.qkv_sf, st));
+      DF_L(mx_quant_e4m3(l.cq_wT, int(d), int(d), l.cq_q, l.cq_sf, st));
+      DF_L(mx_quant_e4m3(l.w13T, int(2 * f), int(d), l.w13_q, l.w13_sf, st));
+      DF_L(mx_quant_e4m3(l.o_wT, int(d), int(d), l.o_q, l.o_sf, st));
+      DF_L(mx_quant_e4m3(l.co_wT, int(d), int(d), l.co_q, l.co_sf, st));
+      DF_L(mx_quant_e4m3(l.w2T, int(d), int(f), l.w2_q, l.w2_sf, st));
+    }
+    return cudaSuccess;
+  }
   const size_t per = al(3 * d * d) + 3 * al(d * d) + 2 * al(2 * f * d) + al(6 * 4);
   DF_TRY(f8mem.reserve(per * c.layers + 4096));
   for (auto& l : Lw) {
@@ -443,20 +477,23 @@ Epi Model::heads_epi(int M, int nsec, const bf16* bias, void* o0, const bf16* g0
 cudaError_t Model::norm_f8(const float* x, int M, const float* shift, const float* scale, const bf16* gain,
                            cudaStream_t st) {
   ProfScope ps(prof, st, K_NORM, 0.0, double(M) * c.d * (4.0 + 1.0));
-  DF_L(rmsnorm_e4m3(x, hq, hs, M, int(c.d), shift, scale, gain, c.eps, st));
+  if (mx()) DF_L(rmsnorm_mx(x, hq, hsf, M, int(c.d), shift, scale, gain, c.eps, st));
+  else DF_L(rmsnorm_e4m3(x, hq, hs, M, int(c.d), shift, scale, gain, c.eps, st));
   return cudaSuccess;
 }
 
 cudaError_t Model::quant_f8(const void* x, int M, int K, cudaStream_t st) {
   ProfScope ps(prof, st, K_MISC, 0.0, double(M) * K * 3.0);
-  DF_L(quant_rows_e4m3(static_cast<const bf16*>(x), hq, hs, M, K, st));
+  if (mx()) DF_L(mx_quant_e4m3(static_cast<const bf16*>(x), M, K, hq, hsf, st));
+  else DF_L(quant_rows_e4m3(static_cast<const bf16*>(x), hq, hs, M, K, st));
   return cudaSuccess;
 }
 
-cudaError_t Model::gemm_f8(const uint8_t* Wq, const float* wscale, int M, int Nn, int K, const Epi& e,
-                           cudaStream_t st) {
+cudaError_t Model::gemm_f8(const uint8_t* Wq, const float* wscale, const uint8_t* wsf, int M, int Nn, int K,
+                           const Epi& e, cudaStream_t st) {
   ProfScope ps(prof, st, cur_kind, 2.0 * M * Nn * K, 0.0);
-  DF_L(gemm_e4m3_epi(hq, hs, Wq, wscale, M, Nn, K, e, st));
+  if (mx()) DF_L(gemm_mxf8_epi(hq, hsf, Wq, wsf, M, Nn, K, e, st));
+  else DF_L(gemm_e4m3_epi(hq, hs, Wq, wscale, M, Nn, K, e, st));
   return cudaSuccess;
 }
 
@@ -637,7 +674,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
   {
     Epi e = heads_epi(M, 3, w.qkv_b, q, w.g_q, 1, k, w.g_k, 1, v, nullptr, 0, N);
     cur_kind = K_QKV;
-    if (fp8()) DF_TRY(gemm_f8(w.qkv_q, w.f8s + 0, M, 3 * d, d, e, st));
+    if (fp8()) DF_TRY(gemm_f8(w.qkv_q, w.f8s + 0, w.qkv_sf, M, 3 * d, d, e, st));
     else DF_TRY(gemm(h, d, w.qkv_wT, d, M, 3 * d, d, e, of, st));
   }
   // a6: self-attention (per sample)
@@ -653,7 +690,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     e.gate = md + 2 * d;
     if (fp8()) {
       DF_TRY(quant_f8(o, M, d, st));
-      DF_TRY(gemm_f8(w.o_q, w.f8s + 3, M, d, d, e, st));
+      DF_TRY(gemm_f8(w.o_q, w.f8s + 3, w.o_sf, M, d, d, e, st));
     } else {
       DF_TRY(gemm(o, d, w.o_wT, d, M, d, d, e, of, st));
     }
@@ -664,7 +701,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
   {
     Epi e = heads_epi(M, 1, w.cq_b, qc, w.g_cq, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, N);
     cur_kind = K_CQ;
-    if (fp8()) DF_TRY(gemm_f8(w.cq_q, w.f8s + 1, M, d, d, e, st));
+    if (fp8()) DF_TRY(gemm_f8(w.cq_q, w.f8s + 1, w.cq_sf, M, d, d, e, st));
     else DF_TRY(gemm(h, d, w.cq_wT, d, M, d, d, e, of, st));
   }
   cur_kind = K_ATTN_CROSS;
@@ -682,7 +719,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     e.ldr = d;
     if (fp8()) {
       DF_TRY(quant_f8(o, M, d, st));
-      DF_TRY(gemm_f8(w.co_q, w.f8s + 4, M, d, d, e, st));
+      DF_TRY(gemm_f8(w.co_q, w.f8s + 4, w.co_sf, M, d, d, e, st));
     } else {
       DF_TRY(gemm(o, d, w.co_wT, d, M, d, d, e, of, st));
     }
@@ -697,7 +734,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     cur_kind = K_UP;
     e.out = a;
     e.ldo = f;
-    if (fp8()) DF_TRY(gemm_f8(w.w13_q, w.f8s + 2, M, 2 * f, d, e, st));
+    if (fp8()) DF_TRY(gemm_f8(w.w13_q, w.f8s + 2, w.w13_sf, M, 2 * f, d, e, st));
     else DF_TRY(gemm(h, d, w.w13T, d, M, 2 * f, d, e, of, st));
   }
   {
@@ -709,7 +746,7 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     e.gate = md + 5 * d;
     if (fp8()) {
       DF_TRY(quant_f8(a, M, f, st));
-      DF_TRY(gemm_f8(w.w2_q, w.f8s + 5, M, d, f, e, st));
+      DF_TRY(gemm_f8(w.w2_q, w.f8s + 5, w.w2_sf, M, d, f, e, st));
     } else {
       DF_TRY(gemm(a, f, w.w2T, f, M, d, f, e, of, st));
     }

@@ -46,6 +46,9 @@ struct LayerW {
   // its per-tensor scale (device fp32): QKV, cross-Q, MLP up (interleaved W1 | W3)
   uint8_t *qkv_q = nullptr, *cq_q = nullptr, *w13_q = nullptr, *o_q = nullptr, *co_q = nullptr, *w2_q = nullptr;
   float* f8s = nullptr;  // [6]: qkv, cq, w13, o, co, w2
+  // MXFP8 step (R31): the same six weights in MXFP8 (codes in the *_q arrays, E8M0 block
+  // scales in the tiled layout of mx_quant_e4m3)
+  uint8_t *qkv_sf = nullptr, *cq_sf = nullptr, *w13_sf = nullptr, *o_sf = nullptr, *co_sf = nullptr, *w2_sf = nullptr;
 };
 
 // Where a logical tensor lives on the device (for df_weight_bits).
@@ -177,6 +180,7 @@ struct Model {
   float* vbatch = nullptr;  // [2][C,F,H,W] velocities of a CFG batch
   uint8_t* hq = nullptr;    // FP8 step: e4m3 GEMM input [2N, max(d, f)] and its row scales [2N]
   float* hs = nullptr;
+  uint8_t* hsf = nullptr;   // MXFP8 step: the GEMM input's tiled E8M0 block scales
   // encoder workspace
   float* ez = nullptr;      // [L, d_txt]
   void* ea = nullptr;       // [L, d_txt]
@@ -191,7 +195,8 @@ struct Model {
   cudaError_t create(const df_dit_cfg& cfg, int precision, int device, int stage, uint64_t seed, int max_steps);
   void destroy();
   bool f32() const { return precision == DF_FP32_VALIDATION; }
-  bool fp8() const { return precision == DF_FP8; }
+  bool fp8() const { return precision == DF_FP8 || precision == DF_MXFP8; }  // e4m3 block GEMMs
+  bool mx() const { return precision == DF_MXFP8; }                           // ... with MX block scales
   size_t act_bytes() const { return f32() ? 4 : 2; }
 
   cudaError_t prepare(const void* ctx_bf16, const float* sig_host, int S, cudaStream_t st, Cond* out,
@@ -215,7 +220,8 @@ struct Model {
                    cudaStream_t st);
   // FP8 step: the normalised activation straight to e4m3 (hq, hs), then an e4m3 GEMM
   cudaError_t norm_f8(const float* x, int M, const float* shift, const float* scale, const bf16* gain, cudaStream_t st);
-  cudaError_t gemm_f8(const uint8_t* Wq, const float* wscale, int M, int Nn, int K, const Epi& e, cudaStream_t st);
+  cudaError_t gemm_f8(const uint8_t* Wq, const float* wscale, const uint8_t* wsf, int M, int Nn, int K, const Epi& e,
+                      cudaStream_t st);
   cudaError_t quant_f8(const void* x, int M, int K, cudaStream_t st);  // bf16 activation -> hq / hs
   cudaError_t quantize_weights(cudaStream_t st);
   cudaError_t init_weights(cudaStream_t st);

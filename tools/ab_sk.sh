@@ -1,7 +1,14 @@
-# A/B of the stream-K schedule on the image step (bench kernel rates), run under gpurun.
-cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out/ab
-for rep in 1 2; do
-  timeout 600 python bench.py --video-requests 0 --no-cpu-baseline > gpurun_out/ab/base_$rep.json 2>/dev/null
-  DF_GEMM_SK=1 timeout 600 python bench.py --video-requests 0 --no-cpu-baseline > gpurun_out/ab/sk_$rep.json 2>/dev/null
+# attn_sk S-ring depth A/B (DF_ATTN_SK_SD=2|3) against attn_pp (DF_ATTN_SK=0): parity tests with the
+# default, then standalone and in-step timings (image full depth, video 4 layers).
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_attn_sk.py -q -x > gpurun_out/sk3_test.log 2>&1; echo rc=$? >> gpurun_out/sk3_test.log
+DF_ATTN_SK_SD=2 timeout 600 python -m pytest tests/test_gpu_attn_sk.py -q -x >> gpurun_out/sk3_test.log 2>&1; echo rc=$? >> gpurun_out/sk3_test.log
+for v in "DF_ATTN_SK_SD=3" "DF_ATTN_SK_SD=2" "DF_ATTN_SK=0"; do
+  for s in cross_image cross_video; do env $v timeout 120 python tools/attn_bench.py --shape $s --reps 20 --iters 5 2>&1 | sed "s/^/$v /" >> gpurun_out/sk3_bench.log; done
 done
-timeout 300 python -m pytest tests/test_gpu_kernels.py -q -k "stream_k or integer" > gpurun_out/ab/sk_tests.log 2>&1
+for r in 1 2; do
+  for v in "DF_ATTN_SK_SD=3" "DF_ATTN_SK_SD=2" "DF_ATTN_SK=0"; do
+    env $v timeout 300 python tools/profile_step.py --config image --steps 6 --kstats 2>&1 | grep "attn_cross\|step_ms" | sed "s/^/$v run=$r /" >> gpurun_out/sk3_step.log
+    env $v timeout 300 python tools/profile_step.py --config video --layers 4 --steps 3 --kstats 2>&1 | grep "attn_cross\|step_ms" | sed "s/^/video $v run=$r /" >> gpurun_out/sk3_step.log
+  done
+done

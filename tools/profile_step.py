@@ -23,11 +23,13 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--kstats", action="store_true")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8", "mxfp8"])
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     if a.layers:
         cfg = with_layers(cfg, a.layers)
-    g = B.make_graph(cfg, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)], max_steps=cfg.steps)
+    prec = {"fp8": B.DF_FP8, "mxfp8": B.DF_MXFP8}.get(a.precision, B.DF_BF16)
+    g = B.make_graph(cfg, [(0, B.DF_E), (0, B.DF_T), (0, B.DF_D)], max_steps=cfg.steps, precision=prec)
     with B.Context(g) as c:
         ctx = torch.from_numpy(inputs.ctx_bf16(cfg, 1).view(np.int16)).cuda().view(torch.bfloat16)
         s = np.linspace(1, 0, cfg.steps + 1).astype(np.float32)
