@@ -48,8 +48,12 @@ typedef enum { DF_E = 0, DF_T = 1, DF_D = 2 } df_stage;
  * cross-Q, cross-O, MLP up, MLP down) take e4m3 operands -- activations quantised per token row
  * with power-of-two scales (by the RMSNorm that produces them, or a row quantiser for the
  * attention and SwiGLU outputs), weights per tensor -- with fp32 accumulation; everything else
- * as DF_BF16.  Needs d >= 256, a head size of 128 and N >= 256 latent tokens (CTA-pair tiles). */
-enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1, DF_FP8 = 2 };
+ * as DF_BF16.  Needs d >= 256, a head size of 128 and N >= 256 latent tokens (CTA-pair tiles).
+ * DF_MXFP8 (NEXT-4, R31): the same six GEMMs on MXFP8 operands (R30: OCP MX, E4M3
+ * elements, one E8M0 scale per 32 consecutive k of a row -- activations quantised by the RMSNorm
+ * or the MX quantiser, weights at init) through the block-scaled tensor-core GEMM; needs d and
+ * the MLP width multiples of 128 and d in {256, 3072, 5120}. */
+enum { DF_BF16 = 0, DF_FP32_VALIDATION = 1, DF_FP8 = 2, DF_MXFP8 = 3 };
 enum { DF_ASYNC = 0, DF_SYNC = 1, DF_PERMUTE = 2, DF_HASH = 4, DF_LATENT_BLOCKS = 8 }; /* handoff flags */
 #define DF_ALL_CHUNKS 0xFFFFFFFFu
 #define DF_MAX_INST 32
@@ -84,7 +88,7 @@ typedef struct {
   uint32_t n_slots;             /* receive slots per consumer per edge, >= 2             */
   uint32_t handoff_mode;        /* DF_ASYNC (default) | DF_SYNC (P:L151 comparison)      */
   uint32_t ring_capacity;       /* request ring, power of two                   */
-  uint32_t precision;           /* DF_BF16 | DF_FP32_VALIDATION | DF_FP8                 */
+  uint32_t precision;           /* DF_BF16 | DF_FP32_VALIDATION | DF_FP8 | DF_MXFP8      */
   uint32_t max_steps;           /* largest S a request may ask for                       */
   uint64_t weight_seed;
   float jitter_p;               /* each transfer delayed by jitter_delay_s w.p. p */
@@ -279,6 +283,15 @@ df_status df_op_mx_quant_e4m3(df_ctx* ctx, const void* x, int32_t M, int32_t K, 
  * stream-ordered. */
 df_status df_op_gemm_mxf8(df_ctx* ctx, const void* qa, const void* sa, const void* qb, const void* sb, int32_t M,
                           int32_t N, int32_t K, void* out, int32_t out_f32, void* stream);
+/* FP8 modes' self-attention (SURVEY NEXT-4 "FP8 ... attention"; R32): q[i] = e4m3 bits of
+ * RNE_satfinite(x[i] * inv) for n bf16 values x (device, 16-byte aligned, n % 8 == 0), inv a
+ * power of two (the kernels use 1 / s with s = the R32 scale of Q or K); q: n bytes (device). */
+df_status df_op_qk_e4m3(df_ctx* ctx, const void* x, uint64_t n, float inv, void* q, void* stream);
+/* O[Nq, H*128] = softmax(dec(Q8) dec(K8)^T * scale) V with e4m3 Q8 [H][Nq][128], K8 [H][Nk][128]
+ * (head-major bytes; QK^T on the tensor cores as kind::f8f6f4, fp32 S) and bf16 V [H][Nk][128];
+ * `scale` carries the two dequantisation scales (s_q s_k / sqrt(dh)).  Device pointers. */
+df_status df_op_attention_qf8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,
+                              int32_t Nq, int32_t Nk, float scale, void* stream);
 /* O[Nq, H*dh] = softmax(Q K^T * scale) V, head-major bf16 Q/K/V [H][N][dh_pad]. */
 df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t H, int32_t Nq,
                           int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream);

@@ -14,7 +14,9 @@ format and per-tensor current scaling, oracle/fp8.py):
     shift), q_mj = e4m3(x_mj / s_m), and the GEMM sees dec(q_mj) * s_m;
   * the weight is quantised per tensor (R28) -- the fused W_qkv as one tensor, W_1 and W_3
     jointly (the GPU stores them interleaved as one tensor) -- and the GEMM sees dec(q) * s;
-  * products are exact and summed in fp64 (the GPU: exact products, fp32 accumulation).
+  * products are exact and summed in fp64 (the GPU: exact products, fp32 accumulation);
+  * R32: the self-attention's QK^T also takes e4m3 Q and K (per-layer power-of-two scales from
+    the qk-norm gains, qk_scale / qk_quant); S, the softmax, P and V stay as in dit.block.
 
 Pinned by tests/test_oracle_fp8.py: quantize_rows' closed forms (a row whose amax is 448
 keeps its e4m3-representable values; a zero row; power-of-two row scaling moves only the
@@ -62,14 +64,36 @@ def weight_q(W):
     return fp8.e4m3_decode(q) * float(s)
 
 
+def qk_scale(g, dh):
+    """R32: the power-of-two e4m3 scale of the self-attention's Q (or K) of a layer.  After the
+    per-head RMSNorm every head vector has norm sqrt(dh), so after the gain g and the RoPE
+    rotation (which keeps each pair's norm) every component is at most sqrt(dh) * max|g|;
+    s = the smallest power of two >= fp32(sqrt(dh) * max|g| / 448) keeps every code unsaturated."""
+    gmax = float(np.max(np.abs(np.asarray(g, dtype=np.float64))))
+    return pow2_ceil(np.float32(np.sqrt(float(dh)) * gmax / 448.0)) if gmax > 0 else np.float32(1.0)
+
+
+def qk_quant(x, s):
+    """Q or K [.., dh] as the e4m3 QK^T sees it: the GPU quantises the bf16 Q / K it stored, so
+    x is rounded to bf16 first; dec(e4m3(bf16(x) / s)) * s (the division is exact)."""
+    from .stages import bf16_round
+    xb, _ = bf16_round(x)
+    return fp8.e4m3_decode(fp8.e4m3_encode(xb / float(s))) * float(s)
+
+
 class Q8:
     """Quantisers handed to oracle.dit.block (q8=...).  W_1 and W_3 share one scale (they are
-    one interleaved tensor on the GPU); the dequantised weights are cached per layer."""
+    one interleaved tensor on the GPU); the dequantised weights are cached per layer.  qk_fn
+    (R32) quantises the self-attention's Q and K with the layer's qk_scale."""
 
-    def __init__(self, act_fn=act, weight_fn=weight_q):
+    def __init__(self, act_fn=act, weight_fn=weight_q, qk_fn=qk_quant):
         self.act = act_fn
         self._wq = weight_fn
+        self._qk = qk_fn
         self._cache = {}
+
+    def qk(self, P, l, x, gname):
+        return self._qk(x, qk_scale(P.layer(l, gname), x.shape[-1]))
 
     def weight(self, P, l, name):
         key = (id(P), l, name)

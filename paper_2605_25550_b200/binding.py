@@ -120,6 +120,9 @@ _SIGS = {
     "df_op_quant_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_op_gemm_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "df_op_qk_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_float, C.c_void_p, C.c_void_p]),
+    "df_op_attention_qf8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_float, C.c_void_p]),
     "df_op_mx_quant_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_op_gemm_mxf8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
@@ -417,6 +420,14 @@ class Context:
         out_f32 = int(str(out.dtype) == "torch.float32")
         self._ck(self.lib.df_op_gemm_e4m3(self.h, _ptr(qa), _ptr(qb), _ptr(sa), _ptr(sb), M, N, K, _ptr(out), out_f32,
                                           _stream(stream)))
+
+    def op_qk_e4m3(self, x, inv, q, stream=None):
+        """x bf16 (any shape, contiguous, numel % 8 == 0); q uint8 of x.numel()."""
+        self._ck(self.lib.df_op_qk_e4m3(self.h, _ptr(x), int(x.numel()), float(inv), _ptr(q), _stream(stream)))
+
+    def op_attention_qf8(self, Q8, K8, V, O, H, Nq, Nk, scale, stream=None):
+        self._ck(self.lib.df_op_attention_qf8(self.h, _ptr(Q8), _ptr(K8), _ptr(V), _ptr(O), H, Nq, Nk, float(scale),
+                                              _stream(stream)))
 
     def op_mx_quant_e4m3(self, x, q, sf, stream=None):
         """x bf16 [M, K] (K % 128 == 0); q uint8 [M, K]; sf uint8 of (K/128) * ceil(M/128) * 512 bytes."""

@@ -25,6 +25,7 @@
 namespace df {
 
 bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint32_t box_rows);
+bool make_tmap_3d_u8(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
 // ------------------------------------------------------------------ attn_tc2: 2 Q tiles / CTA
 // Two 128-query tiles of one head share every K/V block (halving L2->SMEM traffic per
@@ -399,11 +400,15 @@ DF_DEV float lds_f32(uint32_t a) {
 // issues for both; ring barriers live on the leader (count 2: its expect_tx + the peer's
 // arrive), MMA completions are multicast to both CTAs. Softmax is per CTA over its own 128
 // rows, exactly as in attn_tc2 (P written into TMEM, consumed as the A operand of PV).
-struct AttnPairCfg {
+// QF8 (FP8 modes, R32): Q and K in e4m3 -- a 128-dh row is one 128-byte SW128 row, so a Q tile
+// is one atom column (16 KB) and a half K block 8 KB; QK^T runs as four kind::f8f6f4 MMAs
+// (K = 32 bytes each) instead of eight kind::f16 ones.  S, P and V stay as in the bf16 kernel.
+template <bool QF8>
+struct AttnPairCfgT {
   static constexpr int DH = 128;
   static constexpr int ATOM = 64 * 128;              // SW128 atom of 64 rows (8 KB)
-  static constexpr int Q_BYTES = 2 * 128 * 128;      // one 128-row Q tile (2 dh atoms of 16 KB)
-  static constexpr int K_BYTES = 64 * 128 * 2;       // half K block: 64 keys x 128 dh
+  static constexpr int Q_BYTES = QF8 ? 128 * 128 : 2 * 128 * 128;  // one 128-row Q tile
+  static constexpr int K_BYTES = QF8 ? 64 * 128 : 64 * 128 * 2;    // half K block: 64 keys x 128 dh
   static constexpr int V_BYTES = 128 * 64 * 2;       // half V block: 128 keys x 64 dh
   static constexpr int KST = 4;
   static constexpr int VST = 4;
@@ -414,6 +419,7 @@ struct AttnPairCfg {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t O_COL = 256;
 };
+using AttnPairCfg = AttnPairCfgT<false>;
 
 // ------------------------------------------------------------------ attn_pair3: CTA pair + 2 threads per row
 // attn_pair's tensor-core schedule (M = 256 over a CTA pair: per SM the QK^T shared-memory
@@ -429,12 +435,12 @@ struct AttnPairCfg {
 // previous O (the first PV of an item waits for o_free, the epilogue's release of O_t).
 // Short-key launches (cross-attention, 4 key blocks per item) are dominated by exactly
 // these per-item costs.  All barrier phases run on counters that continue across items.
-template <int EXPM>
+template <int EXPM, bool QF8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
                    int dh_real, float scale_log2, int Hs) {
-  using Cfg = AttnPairCfg;
+  using Cfg = AttnPairCfgT<QF8>;
   constexpr int DH = Cfg::DH;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS/STS, not generic)
@@ -507,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
 #pragma unroll
         for (int t = 0; t < 2; ++t)
 #pragma unroll
-          for (int a = 0; a < 2; ++a)
+          for (int a = 0; a < (QF8 ? 1 : 2); ++a)
             tma_load_3d_pair(sQ + t * Cfg::Q_BYTES + a * 2 * Cfg::ATOM, &tmQ, q_full, a * 64,
                              qp + t * 256 + int(rank) * 128, h);
         const int k_end = jk + nkb, v_end = jv + nkb;
@@ -519,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
             else mbar_arrive_cluster(&k_full[st], 0);
             const int kb = jk - (k_end - nkb);
 #pragma unroll
-            for (int a = 0; a < 2; ++a)
+            for (int a = 0; a < (QF8 ? 1 : 2); ++a)
               tma_load_3d_pair(sK + st * Cfg::K_BYTES + a * Cfg::ATOM, &tmK, &k_full[st], a * 64,
                                kb * 128 + int(rank) * 64, h);
             ++jk;
@@ -537,7 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     }
   } else if (warp == 17) {
     if (leader) {  // whole warp runs the schedule; one elected lane issues each MMA batch
-      constexpr uint32_t idesc_qk = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idesc_qk = QF8 ? idesc_e4m3(256, 128) : idesc_bf16(256, 128, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16(256, DH, false, true);
       const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
@@ -546,10 +552,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
         const uint64_t a0 = dq + uint64_t((t * Cfg::Q_BYTES) >> 4);
         const uint64_t b0 = dk + uint64_t(((jg % Cfg::KST) * Cfg::K_BYTES) >> 4);
         if (elect_one()) {
+          if constexpr (QF8) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // 4 x 32 bytes of each 128-byte e4m3 row
+              tc_mma_f8_pair(tmem + t * 128, a0 + uint64_t((k * 32) >> 4), b0 + uint64_t((k * 32) >> 4), idesc_qk,
+                             k > 0);
+          } else {
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k)
             tc_mma_bf16_pair(tmem + t * 128, a0 + uint64_t(((k >> 2) * 2 * Cfg::ATOM + (k & 3) * 32) >> 4),
                              b0 + uint64_t(((k >> 2) * Cfg::ATOM + (k & 3) * 32) >> 4), idesc_qk, k > 0);
+          }
           tc_commit_pair(&s_full[t], 0x3);
         }
         __syncwarp();
@@ -738,17 +751,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
   }
 }
 
-template <int EXPM>
-static cudaError_t launch_attn_pp(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
+template <int EXPM, bool QF8 = false>
+static cudaError_t launch_attn_pp(const void* Q, const void* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
                                   float scale, cudaStream_t st, int hs) {
-  using Cfg = AttnPairCfg;
+  using Cfg = AttnPairCfgT<QF8>;
   constexpr int SMEM = Cfg::OFF_BAR + 512 + 4096 + 1024;
   static_assert(SMEM <= 232448, "attn_pp shared memory");
   CUtensorMap tq, tk, tv;
-  if (!make_tmap_3d(&tq, Q, H, Nq, 128, 128) || !make_tmap_3d(&tk, K, H, Nk, 128, 64) ||
-      !make_tmap_3d(&tv, V, H, Nk, 128, 128))
-    return cudaErrorInvalidValue;
-  auto kern = attn_pp_kernel<EXPM>;
+  const bool ok = QF8 ? (make_tmap_3d_u8(&tq, Q, H, Nq, 128, 128) && make_tmap_3d_u8(&tk, K, H, Nk, 128, 64))
+                      : (make_tmap_3d(&tq, Q, H, Nq, 128, 128) && make_tmap_3d(&tk, K, H, Nk, 128, 64));
+  if (!ok || !make_tmap_3d(&tv, V, H, Nk, 128, 128)) return cudaErrorInvalidValue;
+  auto kern = attn_pp_kernel<EXPM, QF8>;
   static int max_pairs = 0;
   if (!max_pairs) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -1185,6 +1198,16 @@ cudaError_t attn_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, int H,
   if (dh_pad == 64) return launch_attn<64>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
   if (dh_pad == 128) return launch_attn<128>(Q, K, V, O, H, Nq, Nk, dh, scale, st, hs);
   return cudaErrorInvalidValue;
+}
+
+// FP8 modes (R32): self-attention with e4m3 Q and K ([H][N][128] bytes, head-major like the
+// bf16 path) and bf16 V; `scale` already carries the two dequantisation scales.  dh = 128.
+cudaError_t attn_tc_qf8(const uint8_t* Q8, const uint8_t* K8, const bf16* V, bf16* O, int H, int Nq, int Nk,
+                        float scale, cudaStream_t st, int heads_per_sample) {
+  const int hs = heads_per_sample > 0 ? heads_per_sample : H;
+  if (Nq <= 0) return cudaSuccess;
+  if (Nk <= 0 || H % hs) return cudaErrorInvalidValue;
+  return launch_attn_pp<2, true>(Q8, K8, V, O, H, Nq, Nk, 128, scale, st, hs);
 }
 
 // ------------------------------------------------------------------ fp32 SIMT attention

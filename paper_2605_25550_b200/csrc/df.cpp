@@ -2917,6 +2917,25 @@ df_status df_op_gemm_e4m3(df_ctx* ctx, const void* qa, const void* qb, const flo
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_gemm_e4m3: ") + cudaGetErrorString(r));
 }
 
+df_status df_op_qk_e4m3(df_ctx* ctx, const void* x, uint64_t n, float inv, void* q, void* stream) {
+  if (!ctx || (n && (!x || !q))) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = qk_e4m3(static_cast<const bf16*>(x), size_t(n), inv, static_cast<uint8_t*>(q), (cudaStream_t)stream);
+  if (r == cudaErrorInvalidValue) return fail(ctx, "df_op_qk_e4m3: n % 8 or alignment", DF_ERR_INVALID);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_qk_e4m3: ") + cudaGetErrorString(r));
+}
+
+df_status df_op_attention_qf8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,
+                              int32_t Nq, int32_t Nk, float scale, void* stream) {
+  if (!ctx || !Q8 || !K8 || !V || !O) return DF_ERR_INVALID;
+  g_launches->fetch_add(1);
+  cudaError_t r = attn_tc_qf8(static_cast<const uint8_t*>(Q8), static_cast<const uint8_t*>(K8),
+                              static_cast<const bf16*>(V), static_cast<bf16*>(O), H, Nq, Nk, scale, (cudaStream_t)stream,
+                              0);
+  if (r == cudaErrorInvalidValue) return fail(ctx, "df_op_attention_qf8: unsupported shape", DF_ERR_INVALID);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_attention_qf8: ") + cudaGetErrorString(r));
+}
+
 df_status df_op_mx_quant_e4m3(df_ctx* ctx, const void* x, int32_t M, int32_t K, void* q, void* sf, void* stream) {
   if (!ctx || M < 0 || K < 0 || (M && K && (!x || !q || !sf))) return DF_ERR_INVALID;
   g_launches->fetch_add(1);

@@ -1080,6 +1080,8 @@ __global__ void __launch_bounds__(128, 8) rmsnorm_mx_kernel(const float* __restr
                                                         const bf16* __restrict__ gain, float eps) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  pdl_wait();
+  pdl_launch_dependents();
   if (row >= M) return;
   constexpr int d = 128 * VPT;
   const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
@@ -1127,131 +1129,51 @@ __global__ void __launch_bounds__(128, 8) rmsnorm_mx_kernel(const float* __restr
   }
 }
 
-// Streaming variant (the model widths): rmsnorm_stream_kernel's persistent ring of rows in
-// shared memory (one cp.async.bulk per row, one HBM read of the residual), consumer warps
-// compute the MX codes of a row from shared memory (two passes over the staged row).
-template <int VPT>
-__global__ void __launch_bounds__(32 * (RMS_NW + 1), 1)
-    rmsnorm_mx_stream_kernel(const float* __restrict__ x, uint8_t* __restrict__ q, uint8_t* __restrict__ sf, int M,
-                             int RB, const float* __restrict__ shift, const float* __restrict__ scale,
-                             const bf16* __restrict__ gain, float eps) {
-  using Cfg = RmsStream<VPT>;
-  constexpr int d = 128 * VPT;
-  extern __shared__ __align__(128) uint8_t sm[];
-  float4* ring = reinterpret_cast<float4*>(sm);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + Cfg::OFF_BAR);
-  uint64_t* empty = full + Cfg::STAGES;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_wait();
-  pdl_launch_dependents();
-  const int nk = M > int(blockIdx.x) ? (M - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 0;
-  if (w == RMS_NW) {  // producer
-    if (lane == 0) {
-      for (int k = 0; k < nk; ++k) {
-        const int s = k % Cfg::STAGES;
-        mbar_wait(&empty[s], ((k / Cfg::STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[s], Cfg::ROW);
-        bulk_g2s(ring + size_t(s) * (d / 4), x + (size_t(blockIdx.x) + size_t(k) * gridDim.x) * d, Cfg::ROW, &full[s]);
-      }
-    }
-    return;
-  }
-  for (int k = w; k < nk; k += RMS_NW) {
-    const int s = k % Cfg::STAGES;
-    const int row = int(blockIdx.x) + k * int(gridDim.x);
-    mbar_wait(&full[s], (k / Cfg::STAGES) & 1);
-    const float4* xr = ring + size_t(s) * (d / 4);
-    float ss = 0.f;
-#pragma unroll 8
-    for (int i = 0; i < VPT; ++i) {
-      const float4 t = xr[lane + 32 * i];
-      ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
-    }
-    ss = warp_sum(ss);
-    const float inv = rsqrtf(ss / float(d) + eps);
-    uint32_t* qr = reinterpret_cast<uint32_t*>(q + size_t(row) * d);
-    const size_t sf_row = size_t(row >> 7) * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
-#pragma unroll 4
-    for (int i = 0; i < VPT; ++i) {
-      const int c = lane + 32 * i;
-      const float4 t = xr[c];
-      float y[4] = {t.x * inv, t.y * inv, t.z * inv, t.w * inv};
-      if (gain) {
-        const uint2 g = reinterpret_cast<const uint2*>(gain)[c];
-        y[0] *= bf_lo(g.x), y[1] *= bf_hi(g.x), y[2] *= bf_lo(g.y), y[3] *= bf_hi(g.y);
-      } else {
-        const float4 sc = reinterpret_cast<const float4*>(scale)[c];
-        const float4 sh = reinterpret_cast<const float4*>(shift)[c];
-        y[0] = y[0] * (1.f + sc.x) + sh.x;
-        y[1] = y[1] * (1.f + sc.y) + sh.y;
-        y[2] = y[2] * (1.f + sc.z) + sh.z;
-        y[3] = y[3] * (1.f + sc.w) + sh.w;
-      }
-      float am = fmaxf(fmaxf(fabsf(y[0]), fabsf(y[1])), fmaxf(fabsf(y[2]), fabsf(y[3])));
-      am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 1));
-      am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 2));
-      am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 4));
-      int e = -127;
-      if (am > 0.f) {
-        int ex;
-        frexpf(am, &ex);
-        e = min(127, max(-127, ex - 1 - 8));
-      }
-      qr[c] = e4m3x4_mul(y[0], y[1], y[2], y[3], scalbnf(1.0f, -e));
-      if ((lane & 7) == 0) {
-        const int kb = c >> 3;
-        sf[(size_t(kb >> 2) * RB) * 512 + sf_row + (kb & 3)] = uint8_t(e + 127);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-template <int VPT>
-static cudaError_t launch_rms_mx_stream(const float* x, uint8_t* q, uint8_t* sf, int M, int RB, const float* shift,
-                                        const float* scale, const bf16* gain, float eps, cudaStream_t st) {
-  using Cfg = RmsStream<VPT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)rmsnorm_mx_stream_kernel<VPT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  void* args[] = {(void*)&x, (void*)&q, (void*)&sf, (void*)&M, (void*)&RB, (void*)&shift, (void*)&scale,
-                  (void*)&gain, (void*)&eps};
-  const int g = M < num_sms() ? M : num_sms();
-  return launch_ex((const void*)rmsnorm_mx_stream_kernel<VPT>, dim3(g), dim3(32 * (RMS_NW + 1)), Cfg::SMEM, st, args);
-}
-
 cudaError_t rmsnorm_mx(const float* x, uint8_t* q, uint8_t* sf, int M, int d, const float* shift, const float* scale,
                        const bf16* gain, float eps, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
   if (d % 128) return cudaErrorInvalidValue;
   const int RB = (M + 127) / 128;
-  static const int impl = [] {  // DF_RMS_MX=1: the one-warp-per-row kernel (A/B)
-    const char* e = getenv("DF_RMS_MX");
-    return e ? atoi(e) : 0;
-  }();
-  if (impl == 0 && d == 3072) return launch_rms_mx_stream<24>(x, q, sf, M, RB, shift, scale, gain, eps, st);
-  if (impl == 0 && d == 5120) return launch_rms_mx_stream<40>(x, q, sf, M, RB, shift, scale, gain, eps, st);
+  // one warp per row: a persistent TMA-streaming variant (one HBM read of the row, as the bf16
+  // norm's at video sizes) measured 2x slower here at both the image and the video shape
+  // (51.8 vs 24.7 us, 594 vs 284 us in the MXFP8 step) and was removed
+  void* args[] = {(void*)&x, (void*)&q, (void*)&sf, (void*)&M, (void*)&RB, (void*)&shift, (void*)&scale,
+                  (void*)&gain, (void*)&eps};
   const dim3 grid((M + 3) / 4);
   switch (d / 128) {
-    case 2: rmsnorm_mx_kernel<2><<<grid, 128, 0, st>>>(x, q, sf, M, RB, shift, scale, gain, eps); break;
-    case 24: rmsnorm_mx_kernel<24><<<grid, 128, 0, st>>>(x, q, sf, M, RB, shift, scale, gain, eps); break;
-    case 40: rmsnorm_mx_kernel<40><<<grid, 128, 0, st>>>(x, q, sf, M, RB, shift, scale, gain, eps); break;
+    case 2: return launch_ex((const void*)rmsnorm_mx_kernel<2>, grid, dim3(128), 0, st, args);
+    case 24: return launch_ex((const void*)rmsnorm_mx_kernel<24>, grid, dim3(128), 0, st, args);
+    case 40: return launch_ex((const void*)rmsnorm_mx_kernel<40>, grid, dim3(128), 0, st, args);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
+}
+
+// FP8 modes (R32): head-major bf16 Q or K -> e4m3 codes q = RNE_satfinite(x * inv) with inv a
+// power of two (exact), 8 elements per thread (one 16-byte load, one 8-byte store).
+__global__ void __launch_bounds__(256) qk_e4m3_kernel(const bf16* __restrict__ x, size_t n8, float inv,
+                                                      uint8_t* __restrict__ q) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(x) + i);
+    uint2 o;
+    o.x = e4m3x4_mul(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xFFFF0000u), inv);
+    o.y = e4m3x4_mul(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u), __uint_as_float(u.w << 16),
+                     __uint_as_float(u.w & 0xFFFF0000u), inv);
+    reinterpret_cast<uint2*>(q)[i] = o;
+  }
+}
+
+cudaError_t qk_e4m3(const bf16* x, size_t n, float inv, uint8_t* q, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  if (n % 8 || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(q) & 7))
+    return cudaErrorInvalidValue;
+  size_t n8 = n / 8;
+  const unsigned grid = unsigned(std::min<size_t>((n8 + 255) / 256, size_t(num_sms()) * 8));
+  void* args[] = {(void*)&x, (void*)&n8, (void*)&inv, (void*)&q};
+  return launch_ex((const void*)qk_e4m3_kernel, dim3(grid), dim3(256), 0, st, args);
 }
 
 }  // namespace df

@@ -27,6 +27,11 @@ cudaError_t rmsnorm_mx(const float* x, uint8_t* q, uint8_t* sf, int M, int d, co
                        const bf16* gain, float eps, cudaStream_t st);
 cudaError_t gemm_mxf8(const uint8_t* qa, const uint8_t* sa, const uint8_t* qb, const uint8_t* sb, int M, int N, int K,
                       void* out, int ldo, int out_f32, cudaStream_t st);
+// FP8 modes (R32): self-attention with e4m3 Q, K (scale folded into `scale`) and bf16 V, and the
+// quantiser of the head-major bf16 Q / K: q = e4m3(x * inv), inv a power of two
+cudaError_t attn_tc_qf8(const uint8_t* Q8, const uint8_t* K8, const bf16* V, bf16* O, int H, int Nq, int Nk,
+                        float scale, cudaStream_t st, int heads_per_sample);
+cudaError_t qk_e4m3(const bf16* x, size_t n, float inv, uint8_t* q, cudaStream_t st);
 // MXFP8 step (R31): the block-scaled GEMM through the TMA-store epilogues of the bf16 path
 cudaError_t gemm_mxf8_epi(const uint8_t* qa, const uint8_t* sa, const uint8_t* qw, const uint8_t* sw, int M, int N,
                           int K, const Epi& e, cudaStream_t st);

@@ -3,6 +3,7 @@
 // Each launch is counted for bench.py's "gpu_launches".
 #include <atomic>
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include "runtime.h"
 
@@ -193,6 +194,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (fp8()) wsb += al(N2 * std::max(d, f)) + al(N2 * 4);
     if (mx()) wsb += al(mx_sf_bytes(N2, std::max(d, f)));
+    if (fp8()) wsb += 2 * al(hd / 2);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
     else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // GEMM stream-K
   } else if (stage == DF_E) {
@@ -213,6 +215,10 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     if (fp8()) {
       hq = (uint8_t*)ws.take(N2 * std::max(d, f));
       hs = (float*)ws.take(N2 * 4);
+    }
+    if (fp8()) {
+      q8 = (uint8_t*)ws.take(hd / 2);
+      k8 = (uint8_t*)ws.take(hd / 2);
     }
     if (mx()) {  // rows past M in the last 128-row block keep scale byte 0
       hsf = (uint8_t*)ws.take(mx_sf_bytes(N2, std::max(d, f)));
@@ -257,6 +263,28 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
 // bf16 weights, so the codes are those of the oracle's quantize_per_tensor; W_1 | W_3 jointly).
 cudaError_t Model::quantize_weights(cudaStream_t st) {
   const size_t d = c.d, f = c.ffn;
+  {  // R32: the self-attention's e4m3 Q / K scales from the qk-norm gains (host copies, once)
+    std::vector<uint16_t> g(d);
+    auto qscale = [&](const bf16* gain) -> float {
+      if (cudaMemcpy(g.data(), gain, d * 2, cudaMemcpyDeviceToHost) != cudaSuccess) return 0.f;
+      float gmax = 0.f;
+      for (size_t i = 0; i < d; ++i) {
+        uint32_t b = uint32_t(g[i]) << 16;
+        float v;
+        std::memcpy(&v, &b, 4);
+        gmax = std::max(gmax, std::fabs(v));
+      }
+      const float bound = float(std::sqrt(double(dh)) * double(gmax) / 448.0);
+      int e;
+      const float m = std::frexp(bound, &e);  // bound = m 2^e, m in [0.5, 1)
+      return bound > 0.f ? (m == 0.5f ? bound : std::ldexp(1.0f, e)) : 1.f;
+    };
+    for (auto& l : Lw) {
+      l.sq = qscale(l.g_q);
+      l.sk = qscale(l.g_k);
+      if (l.sq <= 0.f || l.sk <= 0.f) return cudaErrorUnknown;
+    }
+  }
   if (mx()) {  // MXFP8 step (R31): OCP MX codes + tiled block scales of every block GEMM's weight [N, K]
     const size_t per = al(3 * d * d) + 3 * al(d * d) + 2 * al(2 * f * d) + al(mx_sf_bytes(3 * d, d)) +
                        3 * al(mx_sf_bytes(d, d)) + al(mx_sf_bytes(2 * f, d)) + al(mx_sf_bytes(d, f));
@@ -442,6 +470,21 @@ cudaError_t Model::attn(const void* Q, const void* K, const void* V, void* O, in
   } else {
     DF_L(attn_simt((const float*)Q, (const float*)K, (const float*)V, (float*)O, Ht, Nq, Nk, dh, scale, st, c.heads));
   }
+  return cudaSuccess;
+}
+
+cudaError_t Model::attn_qf8(int l, int Nq, int B, cudaStream_t st) {
+  const LayerW& w = Lw[l];
+  const int Ht = B * int(c.heads);
+  const size_t n = size_t(Ht) * Nq * 128;
+  {
+    ProfScope ps(prof, st, K_MISC, 0.0, double(n) * 6.0);
+    DF_L(qk_e4m3((const bf16*)q, n, 1.0f / w.sq, q8, st));
+    DF_L(qk_e4m3((const bf16*)k, n, 1.0f / w.sk, k8, st));
+  }
+  ProfScope ps(prof, st, cur_kind, 4.0 * Nq * double(Nq) * dh * Ht, 0.0);
+  const float scale = w.sq * w.sk / std::sqrt(float(dh));
+  DF_L(attn_tc_qf8(q8, k8, (const bf16*)v, (bf16*)o, Ht, Nq, Nq, scale, st, c.heads));
   return cudaSuccess;
 }
 
@@ -677,9 +720,10 @@ cudaError_t Model::block(const Cond& cd, int i, int l, float* res, cudaStream_t 
     if (fp8()) DF_TRY(gemm_f8(w.qkv_q, w.f8s + 0, w.qkv_sf, M, 3 * d, d, e, st));
     else DF_TRY(gemm(h, d, w.qkv_wT, d, M, 3 * d, d, e, of, st));
   }
-  // a6: self-attention (per sample)
+  // a6: self-attention (per sample); FP8 modes: QK^T on e4m3 Q and K (R32)
   cur_kind = K_ATTN_SELF;
-  DF_TRY(attn(q, k, v, o, N, N, st, B));
+  if (fp8()) DF_TRY(attn_qf8(l, N, B, st));
+  else DF_TRY(attn(q, k, v, o, N, N, st, B));
   // a7: r += g1 * (o Wo + bo)
   {
     Epi e = epi_base(EPI_GRES, M, d);

@@ -49,6 +49,9 @@ struct LayerW {
   // MXFP8 step (R31): the same six weights in MXFP8 (codes in the *_q arrays, E8M0 block
   // scales in the tiled layout of mx_quant_e4m3)
   uint8_t *qkv_sf = nullptr, *cq_sf = nullptr, *w13_sf = nullptr, *o_sf = nullptr, *co_sf = nullptr, *w2_sf = nullptr;
+  // FP8 modes' self-attention (R32): power-of-two e4m3 scales of Q and K bounding every
+  // component (sqrt(dh) * max|gain| / 448, rounded up to a power of two)
+  float sq = 1.f, sk = 1.f;
 };
 
 // Where a logical tensor lives on the device (for df_weight_bits).
@@ -181,6 +184,8 @@ struct Model {
   uint8_t* hq = nullptr;    // FP8 step: e4m3 GEMM input [2N, max(d, f)] and its row scales [2N]
   float* hs = nullptr;
   uint8_t* hsf = nullptr;   // MXFP8 step: the GEMM input's tiled E8M0 block scales
+  uint8_t* q8 = nullptr;    // FP8 modes: e4m3 Q and K of the self-attention (R32) [B*heads][N][128]
+  uint8_t* k8 = nullptr;
   // encoder workspace
   float* ez = nullptr;      // [L, d_txt]
   void* ea = nullptr;       // [L, d_txt]
@@ -220,6 +225,7 @@ struct Model {
                    cudaStream_t st);
   // FP8 step: the normalised activation straight to e4m3 (hq, hs), then an e4m3 GEMM
   cudaError_t norm_f8(const float* x, int M, const float* shift, const float* scale, const bf16* gain, cudaStream_t st);
+  cudaError_t attn_qf8(int l, int Nq, int B, cudaStream_t st);
   cudaError_t gemm_f8(const uint8_t* Wq, const float* wscale, const uint8_t* wsf, int M, int Nn, int K, const Epi& e,
                       cudaStream_t st);
   cudaError_t quant_f8(const void* x, int M, int K, cudaStream_t st);  // bf16 activation -> hq / hs

@@ -165,3 +165,49 @@ def test_fp8_pipeline_end_to_end():
         assert np.array_equal(a[s], b[s])
         assert np.all(np.isfinite(a[s]))
         assert 1e-4 < rel_l2(a[s], ref[s]) < 0.1, rel_l2(a[s], ref[s])
+
+
+# ---------------------------------------------------------------- FP8 self-attention (R32)
+@pytest.mark.parametrize("H,Nq,Nk", [(2, 300, 260), (3, 1000, 1000), (24, 4096, 4096)])
+def test_attention_qf8_vs_fp64(ctx, H, Nq, Nk):
+    """QK^T on e4m3 Q and K (R32): the GPU quantiser's codes equal the oracle's (qk_quant on
+    the same bf16 values), and the attention equals fp64 softmax attention on the dequantised
+    Q, K and the bf16 V within the bf16 attention's tolerance (sampled rows at the image shape)."""
+    import math
+    from oracle import dit, dit_fp8
+    from gpu_util import rel_l2
+    dh = 128
+    g = torch.Generator(device="cuda").manual_seed(H + Nq)
+    gq = torch.rand(dh, device="cuda", generator=g) + 0.5
+    gk = torch.rand(dh, device="cuda", generator=g) + 0.5
+
+    def normed(n, gain):
+        t = torch.randn(H, n, dh, device="cuda", generator=g)
+        return (t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + 1e-6) * gain).to(torch.bfloat16)
+    Q, K = normed(Nq, gq), normed(Nk, gk)
+    V = torch.randn(H, Nk, dh, device="cuda", generator=g).to(torch.bfloat16)
+    sq = float(dit_fp8.qk_scale(gq.cpu().numpy(), dh))
+    sk = float(dit_fp8.qk_scale(gk.cpu().numpy(), dh))
+    Q8 = torch.empty((H, Nq, dh), dtype=torch.uint8, device="cuda")
+    K8 = torch.empty((H, Nk, dh), dtype=torch.uint8, device="cuda")
+    ctx.op_qk_e4m3(Q, 1.0 / sq, Q8)
+    ctx.op_qk_e4m3(K, 1.0 / sk, K8)
+    O = torch.full((Nq, H * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
+    ctx.op_attention_qf8(Q8, K8, V, O, H, Nq, Nk, sq * sk / math.sqrt(dh))
+    torch.cuda.synchronize()
+    qd = Q.float().cpu().numpy().astype(np.float64)
+    kd = K.float().cpu().numpy().astype(np.float64)
+    assert np.array_equal(Q8.cpu().numpy(), fp8.e4m3_encode(qd / sq))
+    assert np.array_equal(K8.cpu().numpy(), fp8.e4m3_encode(kd / sk))
+    rows = np.arange(Nq) if Nq <= 1000 else np.unique(np.r_[np.arange(0, Nq, 97), np.arange(Nq - 5, Nq)])
+    qq = dit_fp8.qk_quant(qd[:, rows], sq)
+    kk = dit_fp8.qk_quant(kd, sk)
+    want = dit.softmax_attention(qq, kk, V.float().cpu().numpy().astype(np.float64))
+    want = want.transpose(1, 0, 2).reshape(len(rows), H * dh)
+    got = O.float().cpu().numpy()[rows]
+    assert np.isfinite(got).all()
+    assert rel_l2(got, want) < 1e-2
+    # and it differs from the bf16 attention by the Q / K quantisation only (a few 1e-3 .. 1e-2)
+    full = dit.softmax_attention(qd[:, rows], kd, V.float().cpu().numpy().astype(np.float64))
+    print("qf8 attention: vs its oracle %.3g, vs bf16-input attention %.3g"
+          % (rel_l2(got, want), rel_l2(got, full.transpose(1, 0, 2).reshape(len(rows), H * dh))))

@@ -101,7 +101,7 @@ def test_fp8_block_wiring_reduces_to_the_bf16_block():
     e6 = rr.standard_normal((6, cfg.d)) * 0.1
     pos = dit.token_positions(cfg)
     ref = dit.block(P, cfg, 0, r, e6, kv, pos)
-    ident = dit_fp8.Q8(act_fn=lambda h: h, weight_fn=lambda w: w)
+    ident = dit_fp8.Q8(act_fn=lambda h: h, weight_fn=lambda w: w, qk_fn=lambda x, s: x)
     assert np.array_equal(dit.block(P, cfg, 0, r, e6, kv, pos, q8=ident), ref)
     got = dit.block(P, cfg, 0, r, e6, kv, pos, q8=dit_fp8.Q8())
     rel = np.linalg.norm((got - r) - (ref - r)) / np.linalg.norm(ref - r)
@@ -243,3 +243,27 @@ def test_mx_act_rounds_to_fp32_then_blocks_rows():
     q, s = fp8.mx_quantize(h.astype(np.float32).astype(np.float64))
     np.testing.assert_array_equal(got, fp8.mx_dequantize(q, s))
     np.testing.assert_array_equal(dit_fp8.mx_act(h[[0]]), got[[0]])
+
+
+def test_qk_scale_bounds_every_component_and_is_a_power_of_two():
+    """R32: after the per-head RMSNorm, the gain and RoPE, every component of Q is at most
+    sqrt(dh) max|g|; the worst case (all of a head's energy in one component, at the largest
+    gain) lands exactly at or below 448 after dividing by qk_scale -- never saturated."""
+    from oracle import dit, dit_fp8
+    dh = 128
+    r = np.random.default_rng(3)
+    g = r.uniform(0.5, 1.5, size=dh)
+    s = float(dit_fp8.qk_scale(g, dh))
+    assert s > 0 and np.log2(s) == np.round(np.log2(s))
+    x = np.zeros((1, dh))
+    x[0, int(np.argmax(g))] = 1.0
+    worst = dit.rms_norm(x, 1e-6) * g               # sqrt(dh) * max|g| in one component
+    assert worst.max() / s <= 448.0
+    assert worst.max() / s > 448.0 / 2              # the scale is the tightest power of two
+    q = dit_fp8.qk_quant(worst, s)
+    assert abs(q.max() - worst.max()) <= 2.0 ** -4 * worst.max()
+    # a typical head vector keeps e4m3's relative precision (no subnormal codes)
+    v = dit.rms_norm(r.standard_normal((64, dh)), 1e-6) * g
+    qv = dit_fp8.qk_quant(v, s)
+    big = np.abs(v) > 0.05
+    assert (np.abs(qv - v)[big] <= 2.0 ** -4 * np.abs(v)[big] + 2.0 ** -8 * np.abs(v)[big]).all()
