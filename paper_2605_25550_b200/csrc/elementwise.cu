@@ -887,6 +887,8 @@ __global__ void __launch_bounds__(128, 8) rmsnorm_e4m3_kernel(const float* __res
                                                           const bf16* __restrict__ gain, float eps) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  pdl_wait();
+  pdl_launch_dependents();
   if (row >= M) return;
   constexpr int d = 128 * VPT;
   const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
@@ -941,6 +943,8 @@ __global__ void __launch_bounds__(256) quant_rows_e4m3_kernel(const bf16* __rest
                                                              float* __restrict__ srow, int M, int K) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  pdl_wait();
+  pdl_launch_dependents();
   if (row >= M) return;
   const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * K);
   const int n8 = K / 8;
@@ -972,7 +976,11 @@ __global__ void __launch_bounds__(256) quant_rows_e4m3_kernel(const bf16* __rest
 cudaError_t quant_rows_e4m3(const bf16* x, uint8_t* q, float* s, int M, int K, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
   if (K % 8) return cudaErrorInvalidValue;
-  quant_rows_e4m3_kernel<<<(M + 7) / 8, 256, 0, st>>>(x, q, s, M, K);
+  {
+    void* args[] = {(void*)&x, (void*)&q, (void*)&s, (void*)&M, (void*)&K};
+    cudaError_t e = launch_ex((const void*)quant_rows_e4m3_kernel, dim3((M + 7) / 8), dim3(256), 0, st, args);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
@@ -980,10 +988,11 @@ cudaError_t rmsnorm_e4m3(const float* x, uint8_t* q, float* s, int M, int d, con
                          const bf16* gain, float eps, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
   dim3 grid((M + 3) / 4);
+  void* args[] = {(void*)&x, (void*)&q, (void*)&s, (void*)&M, (void*)&shift, (void*)&scale, (void*)&gain, (void*)&eps};
   switch (d) {
-    case 256: rmsnorm_e4m3_kernel<2><<<grid, 128, 0, st>>>(x, q, s, M, shift, scale, gain, eps); break;
-    case 3072: rmsnorm_e4m3_kernel<24><<<grid, 128, 0, st>>>(x, q, s, M, shift, scale, gain, eps); break;
-    case 5120: rmsnorm_e4m3_kernel<40><<<grid, 128, 0, st>>>(x, q, s, M, shift, scale, gain, eps); break;
+    case 256: return launch_ex((const void*)rmsnorm_e4m3_kernel<2>, grid, dim3(128), 0, st, args);
+    case 3072: return launch_ex((const void*)rmsnorm_e4m3_kernel<24>, grid, dim3(128), 0, st, args);
+    case 5120: return launch_ex((const void*)rmsnorm_e4m3_kernel<40>, grid, dim3(128), 0, st, args);
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
