@@ -292,6 +292,13 @@ df_status df_op_qk_e4m3(df_ctx* ctx, const void* x, uint64_t n, float inv, void*
  * `scale` carries the two dequantisation scales (s_q s_k / sqrt(dh)).  Device pointers. */
 df_status df_op_attention_qf8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,
                               int32_t Nq, int32_t Nk, float scale, void* stream);
+/* DESIGN.md R33: as df_op_attention_qf8 with PV on e4m3 too: V (bf16 [H][Nk][128], device) is
+ * quantised per tensor -- s_v = the smallest power of two >= amax|V| / 448, written to *vscale
+ * (one device float) -- and transposed into v8t (e4m3 V^T [H][128][ldv], ldv = Nk rounded up
+ * to 64; H * 128 * ldv bytes of device scratch), P is rounded to e4m3 in TMEM and O is scaled
+ * by s_v.  Four stream-ordered launches. */
+df_status df_op_attention_f8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,
+                             int32_t Nq, int32_t Nk, float scale, void* v8t, float* vscale, void* stream);
 /* O[Nq, H*dh] = softmax(Q K^T * scale) V, head-major bf16 Q/K/V [H][N][dh_pad]. */
 df_status df_op_attention(df_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t H, int32_t Nq,
                           int32_t Nk, int32_t dh, int32_t dh_pad, float scale, void* stream);

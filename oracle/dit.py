@@ -222,6 +222,8 @@ def block(P, cfg, l: int, r: np.ndarray, e6: np.ndarray, kv, pos, cross: bool = 
     k = rope3(k.reshape(-1, H, cfg.dh), pos, cfg.rope_axes, cfg.rope_theta)
     if q8 is not None and hasattr(q8, "qk"):  # FP8 modes (R32): e4m3 Q, K for QK^T
         q, k = q8.qk(P, l, q, "g_q"), q8.qk(P, l, k, "g_k")
+    if q8 is not None and hasattr(q8, "vq"):  # FP8 modes (R33): e4m3 V for PV
+        v = q8.vq(v)
     o = softmax_attention(q.transpose(1, 0, 2), k.transpose(1, 0, 2), _heads(v, H))
     r = r + g1 * (act(_unheads(o)) @ wgt(l, "o_w") + P.layer(l, "o_b"))
     # --- cross-attention (a8): pre-norm with gain, not modulated, ungated (R3)

@@ -16,7 +16,8 @@ format and per-tensor current scaling, oracle/fp8.py):
     jointly (the GPU stores them interleaved as one tensor) -- and the GEMM sees dec(q) * s;
   * products are exact and summed in fp64 (the GPU: exact products, fp32 accumulation);
   * R32: the self-attention's QK^T also takes e4m3 Q and K (per-layer power-of-two scales from
-    the qk-norm gains, qk_scale / qk_quant); S, the softmax, P and V stay as in dit.block.
+    the qk-norm gains, qk_scale / qk_quant); R33: its PV takes e4m3 V (per-tensor power-of-two
+    scale, v_quant) -- and, on the GPU only, e4m3 P (not mirrored, see v_quant).
 
 Pinned by tests/test_oracle_fp8.py: quantize_rows' closed forms (a row whose amax is 448
 keeps its e4m3-representable values; a zero row; power-of-two row scaling moves only the
@@ -81,15 +82,28 @@ def qk_quant(x, s):
     return fp8.e4m3_decode(fp8.e4m3_encode(xb / float(s))) * float(s)
 
 
+def v_quant(v):
+    """R33: V (all heads of a sample) as the e4m3 PV sees it: the GPU quantises its bf16 V per
+    tensor with s = the smallest power of two >= fp32(amax|V| / 448); dec(e4m3(bf16(v) / s)) * s.
+    (P's e4m3 rounding inside the kernel depends on its running row maximum and is not
+    mirrored: the tolerance covers it, R33.)"""
+    from .stages import bf16_round
+    vb, _ = bf16_round(v)
+    amax = np.float32(np.max(np.abs(vb))) if vb.size else np.float32(0)
+    s = pow2_ceil(np.float32(amax / E4M3_MAX)) if amax > 0 else np.float32(1.0)
+    return fp8.e4m3_decode(fp8.e4m3_encode(vb / float(s))) * float(s)
+
+
 class Q8:
     """Quantisers handed to oracle.dit.block (q8=...).  W_1 and W_3 share one scale (they are
     one interleaved tensor on the GPU); the dequantised weights are cached per layer.  qk_fn
     (R32) quantises the self-attention's Q and K with the layer's qk_scale."""
 
-    def __init__(self, act_fn=act, weight_fn=weight_q, qk_fn=qk_quant):
+    def __init__(self, act_fn=act, weight_fn=weight_q, qk_fn=qk_quant, v_fn=v_quant):
         self.act = act_fn
         self._wq = weight_fn
         self._qk = qk_fn
+        self.vq = v_fn
         self._cache = {}
 
     def qk(self, P, l, x, gname):

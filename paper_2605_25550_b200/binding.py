@@ -123,6 +123,8 @@ _SIGS = {
     "df_op_qk_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_float, C.c_void_p, C.c_void_p]),
     "df_op_attention_qf8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                       C.c_int32, C.c_int32, C.c_float, C.c_void_p]),
+    "df_op_attention_f8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                     C.c_int32, C.c_int32, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_op_mx_quant_e4m3": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "df_op_gemm_mxf8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
@@ -428,6 +430,10 @@ class Context:
     def op_attention_qf8(self, Q8, K8, V, O, H, Nq, Nk, scale, stream=None):
         self._ck(self.lib.df_op_attention_qf8(self.h, _ptr(Q8), _ptr(K8), _ptr(V), _ptr(O), H, Nq, Nk, float(scale),
                                               _stream(stream)))
+
+    def op_attention_f8(self, Q8, K8, V, O, H, Nq, Nk, scale, v8t, vscale, stream=None):
+        self._ck(self.lib.df_op_attention_f8(self.h, _ptr(Q8), _ptr(K8), _ptr(V), _ptr(O), H, Nq, Nk, float(scale),
+                                             _ptr(v8t), _ptr(vscale), _stream(stream)))
 
     def op_mx_quant_e4m3(self, x, q, sf, stream=None):
         """x bf16 [M, K] (K % 128 == 0); q uint8 [M, K]; sf uint8 of (K/128) * ceil(M/128) * 512 bytes."""

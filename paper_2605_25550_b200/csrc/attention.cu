@@ -17,6 +17,7 @@
 // faster, and removed.)
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cudaTypedefs.h>
 #include <cmath>
 #include <cstdlib>
@@ -26,6 +27,8 @@ namespace df {
 
 bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint32_t box_rows);
 bool make_tmap_3d_u8(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint32_t box_rows);
+bool make_tmap_3d_u8s(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint64_t ld,
+                      uint32_t box_rows);
 
 // ------------------------------------------------------------------ attn_tc2: 2 Q tiles / CTA
 // Two 128-query tiles of one head share every K/V block (halving L2->SMEM traffic per
@@ -327,6 +330,26 @@ static cudaError_t launch_attn2(const CUtensorMap& tq, const CUtensorMap& tk, co
 // p = 2^x for a pair of logits, packed to bf16x2 for P; adds the pair to the row sum.
 // EXPM 0: MUFU ex2 (fp32); 1: 3 of 8 pairs by polynomial on the FMA pipe; 2: 1 of 4 pairs;
 // 3: one MUFU ex2.bf16x2 per pair (input rounded to bf16: coarser, profiling only).
+// p = 2^x for a pair (fp32), added to the row sum: the MUFU / polynomial split of softmax_exp2
+template <int EXPM>
+DF_DEV float2 softmax_exp2f(float2 x, int i, float2& lsum2) {
+  float2 p;
+  if ((EXPM == 1 && (i & 7) >= 5) || (EXPM == 2 && (i & 3) == 3) || (EXPM == 5 && (i & 1))) {
+    p = exp2_poly2(x);
+  } else {
+    p.x = ex2_approx(x.x);
+    p.y = ex2_approx(x.y);
+  }
+  lsum2 = fadd2(lsum2, p);
+  return p;
+}
+// four fp32 -> e4m3 bytes (RNE, satfinite), a.x in the lowest byte
+DF_DEV uint32_t pack_e4m3x4(float2 a, float2 b) {
+  const uint32_t lo = __nv_cvt_float2_to_fp8x2(a, __NV_SATFINITE, __NV_E4M3);
+  const uint32_t hi = __nv_cvt_float2_to_fp8x2(b, __NV_SATFINITE, __NV_E4M3);
+  return lo | (hi << 16);
+}
+
 template <int EXPM>
 DF_DEV uint32_t softmax_exp2(float2 x, int i, float2& lsum2) {
   if (EXPM == 4) {  // one MUFU ex2.f16x2 per pair (input rounded to f16: |err(x)| <= |x| 2^-11)
@@ -400,16 +423,19 @@ DF_DEV float lds_f32(uint32_t a) {
 // issues for both; ring barriers live on the leader (count 2: its expect_tx + the peer's
 // arrive), MMA completions are multicast to both CTAs. Softmax is per CTA over its own 128
 // rows, exactly as in attn_tc2 (P written into TMEM, consumed as the A operand of PV).
-// QF8 (FP8 modes, R32): Q and K in e4m3 -- a 128-dh row is one 128-byte SW128 row, so a Q tile
-// is one atom column (16 KB) and a half K block 8 KB; QK^T runs as four kind::f8f6f4 MMAs
-// (K = 32 bytes each) instead of eight kind::f16 ones.  S, P and V stay as in the bf16 kernel.
-template <bool QF8>
+// QF8 (FP8 modes): 1 (R32) -- Q and K in e4m3: a 128-dh row is one 128-byte SW128 row, so a Q
+// tile is one atom column (16 KB) and a half K block 8 KB; QK^T runs as four kind::f8f6f4 MMAs
+// (K = 32 bytes each) instead of eight kind::f16 ones.  2 (R33) -- also PV on e4m3: P written
+// as e4m3 into TMEM (four keys per 32-bit column, the A operand of a kind::f8f6f4 TS MMA per
+// 32-key quarter) and V^T e4m3 [H][dh][keys] (K-major like K: a half V block is 64 dh rows x
+// 128 keys = 8 KB); the per-tensor V scale is applied in the O normalisation.
+template <int QF8>
 struct AttnPairCfgT {
   static constexpr int DH = 128;
   static constexpr int ATOM = 64 * 128;              // SW128 atom of 64 rows (8 KB)
   static constexpr int Q_BYTES = QF8 ? 128 * 128 : 2 * 128 * 128;  // one 128-row Q tile
   static constexpr int K_BYTES = QF8 ? 64 * 128 : 64 * 128 * 2;    // half K block: 64 keys x 128 dh
-  static constexpr int V_BYTES = 128 * 64 * 2;       // half V block: 128 keys x 64 dh
+  static constexpr int V_BYTES = QF8 == 2 ? 64 * 128 : 128 * 64 * 2;  // half V block
   static constexpr int KST = 4;
   static constexpr int VST = 4;
   static constexpr int OFF_Q = 0;
@@ -419,7 +445,7 @@ struct AttnPairCfgT {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t O_COL = 256;
 };
-using AttnPairCfg = AttnPairCfgT<false>;
+using AttnPairCfg = AttnPairCfgT<0>;
 
 // ------------------------------------------------------------------ attn_pair3: CTA pair + 2 threads per row
 // attn_pair's tensor-core schedule (M = 256 over a CTA pair: per SM the QK^T shared-memory
@@ -435,11 +461,11 @@ using AttnPairCfg = AttnPairCfgT<false>;
 // previous O (the first PV of an item waits for o_free, the epilogue's release of O_t).
 // Short-key launches (cross-attention, 4 key blocks per item) are dominated by exactly
 // these per-item costs.  All barrier phases run on counters that continue across items.
-template <int EXPM, bool QF8 = false>
+template <int EXPM, int QF8 = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ O, int H, int Nq, int Nk,
-                   int dh_real, float scale_log2, int Hs) {
+                   int dh_real, float scale_log2, int Hs, const float* __restrict__ vscale) {
   using Cfg = AttnPairCfgT<QF8>;
   constexpr int DH = Cfg::DH;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -535,7 +561,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
             if (leader) mbar_arrive_expect_tx(&v_full[st], 2 * Cfg::V_BYTES);
             else mbar_arrive_cluster(&v_full[st], 0);
             const int vb = jv - (v_end - nkb);
-            tma_load_3d_pair(sV + st * Cfg::V_BYTES, &tmV, &v_full[st], int(rank) * 64, vb * 128, h);
+            if (QF8 == 2) tma_load_3d_pair(sV + st * Cfg::V_BYTES, &tmV, &v_full[st], vb * 128, int(rank) * 64, h);
+            else tma_load_3d_pair(sV + st * Cfg::V_BYTES, &tmV, &v_full[st], int(rank) * 64, vb * 128, h);
             ++jv;
           }
         }
@@ -544,10 +571,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
   } else if (warp == 17) {
     if (leader) {  // whole warp runs the schedule; one elected lane issues each MMA batch
       constexpr uint32_t idesc_qk = QF8 ? idesc_e4m3(256, 128) : idesc_bf16(256, 128, false, false);
-      constexpr uint32_t idesc_pv = idesc_bf16(256, DH, false, true);
+      constexpr uint32_t idesc_pv = QF8 == 2 ? idesc_e4m3(256, DH) : idesc_bf16(256, DH, false, true);
       const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
-      const uint64_t dv = sdesc_sw128(smem_u32(sV), Cfg::V_BYTES, 1024);
+      const uint64_t dv = QF8 == 2 ? sdesc_sw128(smem_u32(sV), 16, 1024) : sdesc_sw128(smem_u32(sV), Cfg::V_BYTES, 1024);
       auto issue_qk = [&](int t, int jg) {
         const uint64_t a0 = dq + uint64_t((t * Cfg::Q_BYTES) >> 4);
         const uint64_t b0 = dk + uint64_t(((jg % Cfg::KST) * Cfg::K_BYTES) >> 4);
@@ -570,11 +597,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       auto issue_pv = [&](int t, int jg, int u, bool first) {
         const uint64_t b0 = dv + uint64_t(((jg % Cfg::VST) * Cfg::V_BYTES) >> 4);
         if (elect_one()) {
+          if constexpr (QF8 == 2) {  // keys 32u .. 32u + 31: P columns 8u .., V^T bytes 32u ..
+            tc_mma_f8_ts_pair(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + u * 8, b0 + uint64_t((u * 32) >> 4),
+                              idesc_pv, !first);
+          } else {
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
             const int k = 2 * u + kk;
             tc_mma_bf16_ts_pair(tmem + Cfg::O_COL + t * DH, tmem + t * 128 + k * 8, b0 + uint64_t((k * 2048) >> 4),
                                 idesc_pv, !(first && kk == 0));
+          }
           }
         }
         __syncwarp();
@@ -699,6 +731,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
         const float2 sc2 = make_float2(scale_log2, scale_log2);
         const float2 nm2 = make_float2(-m_used, -m_used);
         uint32_t pk[16];
+        if constexpr (QF8 == 2) {  // P as e4m3 (p <= 2^8 by the lazy rescale): 4 keys per column
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 a = softmax_exp2f<EXPM>(ffma2(make_float2(s[4 * i], s[4 * i + 1]), sc2, nm2), 2 * i, lsum2);
+            const float2 b = softmax_exp2f<EXPM>(ffma2(make_float2(s[4 * i + 2], s[4 * i + 3]), sc2, nm2), 2 * i + 1, lsum2);
+            pk[i] = pack_e4m3x4(a, b);
+          }
+          tmem_st8(ts + 16 * hc, pk);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 a = softmax_exp2f<EXPM>(ffma2(make_float2(s[32 + 4 * i], s[32 + 4 * i + 1]), sc2, nm2), 2 * i, lsum2);
+            const float2 b = softmax_exp2f<EXPM>(ffma2(make_float2(s[32 + 4 * i + 2], s[32 + 4 * i + 3]), sc2, nm2), 2 * i + 1, lsum2);
+            pk[i] = pack_e4m3x4(a, b);
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2), i, lsum2);
@@ -706,11 +753,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = softmax_exp2<EXPM>(ffma2(make_float2(s[32 + 2 * i], s[32 + 2 * i + 1]), sc2, nm2), i, lsum2);
+        }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&p_q[t * 4 + 2 * hc], 0);
-        tmem_st16(ts + 32 * hc + 16, pk);
+        if constexpr (QF8 == 2) tmem_st8(ts + 16 * hc + 8, pk);
+        else tmem_st16(ts + 32 * hc + 16, pk);
         l += lsum2.x + lsum2.y;
         tc_wait_st();
         tc_fence_before();
@@ -721,7 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
       tc_fence_after();
       sts_f32(lred_own, l);
       named_bar_sync(1 + t, 256);
-      const float inv = 1.0f / (l + lds_f32(lred_oth));
+      const float inv = (QF8 == 2 ? __ldg(vscale) : 1.0f) / (l + lds_f32(lred_oth));
       const int it = cid + n * npairs;
       const int h = it / nqp, qp = (it - h * nqp) * 512;
       const int q = qp + t * 256 + int(rank) * 128 + r;
@@ -751,16 +800,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATTN3_THREADS, 1)
   }
 }
 
-template <int EXPM, bool QF8 = false>
-static cudaError_t launch_attn_pp(const void* Q, const void* K, const bf16* V, bf16* O, int H, int Nq, int Nk, int dh,
-                                  float scale, cudaStream_t st, int hs) {
+template <int EXPM, int QF8 = 0>
+static cudaError_t launch_attn_pp(const void* Q, const void* K, const void* V, bf16* O, int H, int Nq, int Nk, int dh,
+                                  float scale, cudaStream_t st, int hs, const float* vscale = nullptr, int ldv = 0) {
   using Cfg = AttnPairCfgT<QF8>;
   constexpr int SMEM = Cfg::OFF_BAR + 512 + 4096 + 1024;
   static_assert(SMEM <= 232448, "attn_pp shared memory");
   CUtensorMap tq, tk, tv;
   const bool ok = QF8 ? (make_tmap_3d_u8(&tq, Q, H, Nq, 128, 128) && make_tmap_3d_u8(&tk, K, H, Nk, 128, 64))
                       : (make_tmap_3d(&tq, Q, H, Nq, 128, 128) && make_tmap_3d(&tk, K, H, Nk, 128, 64));
-  if (!ok || !make_tmap_3d(&tv, V, H, Nk, 128, 128)) return cudaErrorInvalidValue;
+  // QF8 == 2: V^T e4m3 [H][128 dh][ldv] bytes (keys contiguous, row stride ldv >= Nk, % 16 == 0)
+  const bool okv = QF8 == 2 ? make_tmap_3d_u8s(&tv, V, H, 128, Nk, ldv, 64) : make_tmap_3d(&tv, V, H, Nk, 128, 128);
+  if (!ok || !okv) return cudaErrorInvalidValue;
   auto kern = attn_pp_kernel<EXPM, QF8>;
   static int max_pairs = 0;
   if (!max_pairs) {
@@ -788,7 +839,7 @@ static cudaError_t launch_attn_pp(const void* Q, const void* K, const bf16* V, b
   dim3 grid(2 * (items < max_pairs ? items : max_pairs));
   float sl2 = scale * 1.4426950408889634f;
   void* args[] = {(void*)&tq, (void*)&tk, (void*)&tv, (void*)&O,   (void*)&H,
-                  (void*)&Nq, (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs};
+                  (void*)&Nq, (void*)&Nk, (void*)&dh, (void*)&sl2, (void*)&hs, (void*)&vscale};
   return launch_ex((const void*)kern, grid, dim3(ATTN3_THREADS), SMEM, st, args);
 }
 
@@ -1207,7 +1258,17 @@ cudaError_t attn_tc_qf8(const uint8_t* Q8, const uint8_t* K8, const bf16* V, bf1
   const int hs = heads_per_sample > 0 ? heads_per_sample : H;
   if (Nq <= 0) return cudaSuccess;
   if (Nk <= 0 || H % hs) return cudaErrorInvalidValue;
-  return launch_attn_pp<2, true>(Q8, K8, V, O, H, Nq, Nk, 128, scale, st, hs);
+  return launch_attn_pp<2, 1>(Q8, K8, V, O, H, Nq, Nk, 128, scale, st, hs);
+}
+
+// R33: QK^T and PV on e4m3 -- Q8, K8 as above, V8T = e4m3 V^T [H][128][ldv] (keys contiguous)
+// with the per-tensor dequantisation scale *vscale (device).
+cudaError_t attn_tc_f8(const uint8_t* Q8, const uint8_t* K8, const uint8_t* V8T, int ldv, const float* vscale, bf16* O,
+                       int H, int Nq, int Nk, float scale, cudaStream_t st, int heads_per_sample) {
+  const int hs = heads_per_sample > 0 ? heads_per_sample : H;
+  if (Nq <= 0) return cudaSuccess;
+  if (Nk <= 0 || H % hs || ldv < Nk || ldv % 16 || !vscale) return cudaErrorInvalidValue;
+  return launch_attn_pp<2, 2>(Q8, K8, V8T, O, H, Nq, Nk, 128, scale, st, hs, vscale, ldv);
 }
 
 // ------------------------------------------------------------------ fp32 SIMT attention

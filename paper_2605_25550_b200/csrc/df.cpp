@@ -2936,6 +2936,20 @@ df_status df_op_attention_qf8(df_ctx* ctx, const void* Q8, const void* K8, const
   return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_attention_qf8: ") + cudaGetErrorString(r));
 }
 
+df_status df_op_attention_f8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,
+                             int32_t Nq, int32_t Nk, float scale, void* v8t, float* vscale, void* stream) {
+  if (!ctx || !Q8 || !K8 || !V || !O || !v8t || !vscale) return DF_ERR_INVALID;
+  g_launches->fetch_add(4);
+  const int ldv = (Nk + 63) / 64 * 64;
+  cudaError_t r = v_e4m3t(static_cast<const bf16*>(V), H, Nk, ldv, vscale, static_cast<uint8_t*>(v8t),
+                          (cudaStream_t)stream);
+  if (r == cudaSuccess)
+    r = attn_tc_f8(static_cast<const uint8_t*>(Q8), static_cast<const uint8_t*>(K8), static_cast<const uint8_t*>(v8t),
+                   ldv, vscale, static_cast<bf16*>(O), H, Nq, Nk, scale, (cudaStream_t)stream, 0);
+  if (r == cudaErrorInvalidValue) return fail(ctx, "df_op_attention_f8: unsupported shape", DF_ERR_INVALID);
+  return r == cudaSuccess ? DF_OK : fail(ctx, std::string("df_op_attention_f8: ") + cudaGetErrorString(r));
+}
+
 df_status df_op_mx_quant_e4m3(df_ctx* ctx, const void* x, int32_t M, int32_t K, void* q, void* sf, void* stream) {
   if (!ctx || M < 0 || K < 0 || (M && K && (!x || !q || !sf))) return DF_ERR_INVALID;
   g_launches->fetch_add(1);

@@ -1185,4 +1185,68 @@ cudaError_t qk_e4m3(const bf16* x, size_t n, float inv, uint8_t* q, cudaStream_t
   return launch_ex((const void*)qk_e4m3_kernel, dim3(grid), dim3(256), 0, st, args);
 }
 
+// R33: V [H][N][128] bf16 -> V^T e4m3 [H][128][ldv] (keys contiguous: the K-major B operand of
+// the e4m3 PV MMA) with one per-tensor power-of-two scale s = pow2ceil(fp32(amax|V| / 448)).
+__global__ void v_scale_kernel(float* s) {
+  const float a = __uint_as_float(*reinterpret_cast<const unsigned*>(s));
+  *s = a > 0.f ? pow2_ceil(__fdiv_rn(a, 448.f)) : 1.f;
+}
+// one block per (64 keys, head): 64 x 128 bf16 -> e4m3 through a shared [128][64 + 16] tile
+__global__ void __launch_bounds__(256) v_e4m3t_kernel(const bf16* __restrict__ V, int N, int ldv,
+                                                      const float* __restrict__ sp, uint8_t* __restrict__ VT) {
+  __shared__ uint8_t tile[128][80];
+  const int h = blockIdx.y, k0 = blockIdx.x * 64;
+  const float inv = __uint_as_float((254u << 23) - __float_as_uint(__ldg(sp)));  // exactly 1 / s
+  const int t = threadIdx.x;
+  {  // load: thread t -> key k0 + t / 4, dh [32 (t % 4), +32)
+    const int k = k0 + (t >> 2), c0 = (t & 3) * 32;
+    uint32_t w[16];
+    if (k < N) {
+      const uint4* src = reinterpret_cast<const uint4*>(V + (size_t(h) * N + k) * 128 + c0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 u = __ldg(src + i);
+        w[4 * i] = u.x, w[4 * i + 1] = u.y, w[4 * i + 2] = u.z, w[4 * i + 3] = u.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = 0;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t q2 = __nv_cvt_float2_to_fp8x2(
+          make_float2(__uint_as_float(w[i] << 16) * inv, __uint_as_float(w[i] & 0xFFFF0000u) * inv), __NV_SATFINITE,
+          __NV_E4M3);
+      tile[c0 + 2 * i][t >> 2] = uint8_t(q2 & 0xFF);
+      tile[c0 + 2 * i + 1][t >> 2] = uint8_t(q2 >> 8);
+    }
+  }
+  __syncthreads();
+  {  // store: thread t -> dh row t / 2, keys [32 (t % 2), +32)
+    const int r = t >> 1, kk = (t & 1) * 32;
+    if (k0 + kk < N) {
+      const uint4* src = reinterpret_cast<const uint4*>(&tile[r][kk]);
+      uint4* dst = reinterpret_cast<uint4*>(VT + (size_t(h) * 128 + r) * ldv + k0 + kk);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    }
+  }
+}
+
+cudaError_t v_e4m3t(const bf16* V, int H, int N, int ldv, float* vscale, uint8_t* VT, cudaStream_t st) {
+  if (H <= 0 || N <= 0) return cudaSuccess;
+  if (ldv < ((N + 63) / 64) * 64 || ldv % 16 || (reinterpret_cast<uintptr_t>(V) & 15) ||
+      (reinterpret_cast<uintptr_t>(VT) & 15))
+    return cudaErrorInvalidValue;
+  const size_t n = size_t(H) * N * 128;
+  cudaError_t e = cudaMemsetAsync(vscale, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  const int per = 256 * 8 * 4;
+  const unsigned grid = unsigned(std::max<size_t>(1, std::min<size_t>((n + per - 1) / per, size_t(num_sms()) * 8)));
+  e4m3_amax_kernel<<<grid, 256, 0, st>>>(V, n, reinterpret_cast<unsigned*>(vscale));
+  v_scale_kernel<<<1, 1, 0, st>>>(vscale);
+  v_e4m3t_kernel<<<dim3((N + 63) / 64, H), 256, 0, st>>>(V, N, ldv, vscale, VT);
+  return cudaGetLastError();
+}
+
 }  // namespace df

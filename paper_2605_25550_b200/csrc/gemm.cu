@@ -80,6 +80,22 @@ bool make_tmap_3d_u8(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows
   return r == CUDA_SUCCESS;
 }
 
+// As make_tmap_3d_u8 with an explicit row stride ld (bytes, % 16 == 0): the FP8 attention's
+// V^T [z][rows][ld] (R33), keys beyond `cols` zero-filled by TMA.
+bool make_tmap_3d_u8s(CUtensorMap* m, const void* base, uint64_t z, uint64_t rows, uint64_t cols, uint64_t ld,
+                      uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cols, rows, z};
+  cuuint64_t strides[2] = {ld, ld * rows};
+  cuuint32_t box[3] = {128, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Generic tiled tensor map (128B swizzle unless swz128 is false; box inner extent must be 128 B
 // with the swizzle).
 bool make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rank, const uint64_t* dims,

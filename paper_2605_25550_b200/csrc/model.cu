@@ -194,7 +194,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
           al(2 * size_t(c.C) * c.F * c.H * c.W * 4);
     if (fp8()) wsb += al(N2 * std::max(d, f)) + al(N2 * 4);
     if (mx()) wsb += al(mx_sf_bytes(N2, std::max(d, f)));
-    if (fp8()) wsb += 2 * al(hd / 2);
+    if (fp8()) wsb += 2 * al(hd / 2) + al(size_t(2) * c.heads * 128 * ((Nn + 63) / 64 * 64)) + al(64);
     if (f32()) wsb += al(N2 * std::max(3 * d, 2 * f) * 4);
     else wsb += al(size_t(num_sms()) * 128 * 256 * 4) + al(size_t(num_sms()) * 4);  // GEMM stream-K
   } else if (stage == DF_E) {
@@ -219,6 +219,9 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
     if (fp8()) {
       q8 = (uint8_t*)ws.take(hd / 2);
       k8 = (uint8_t*)ws.take(hd / 2);
+      ldv8 = int((Nn + 63) / 64 * 64);
+      v8t = (uint8_t*)ws.take(size_t(2) * c.heads * 128 * ldv8);
+      v8s = (float*)ws.take(64);
     }
     if (mx()) {  // rows past M in the last 128-row block keep scale byte 0
       hsf = (uint8_t*)ws.take(mx_sf_bytes(N2, std::max(d, f)));
@@ -482,9 +485,19 @@ cudaError_t Model::attn_qf8(int l, int Nq, int B, cudaStream_t st) {
     DF_L(qk_e4m3((const bf16*)q, n, 1.0f / w.sq, q8, st));
     DF_L(qk_e4m3((const bf16*)k, n, 1.0f / w.sk, k8, st));
   }
+  // DF_ATTN_F8 (A/B): 2 (default) QK^T and PV on e4m3 (R33), 1 QK^T only (R32)
+  static const int lvl = [] {
+    const char* e = getenv("DF_ATTN_F8");
+    return e ? atoi(e) : 2;
+  }();
+  if (lvl == 2) {
+    ProfScope pv(prof, st, K_MISC, 0.0, double(n) * 3.0);
+    DF_L(v_e4m3t((const bf16*)v, Ht, Nq, ldv8, v8s, v8t, st));
+  }
   ProfScope ps(prof, st, cur_kind, 4.0 * Nq * double(Nq) * dh * Ht, 0.0);
   const float scale = w.sq * w.sk / std::sqrt(float(dh));
-  DF_L(attn_tc_qf8(q8, k8, (const bf16*)v, (bf16*)o, Ht, Nq, Nq, scale, st, c.heads));
+  if (lvl == 2) DF_L(attn_tc_f8(q8, k8, v8t, ldv8, v8s, (bf16*)o, Ht, Nq, Nq, scale, st, c.heads));
+  else DF_L(attn_tc_qf8(q8, k8, (const bf16*)v, (bf16*)o, Ht, Nq, Nq, scale, st, c.heads));
   return cudaSuccess;
 }
 

@@ -186,6 +186,9 @@ struct Model {
   uint8_t* hsf = nullptr;   // MXFP8 step: the GEMM input's tiled E8M0 block scales
   uint8_t* q8 = nullptr;    // FP8 modes: e4m3 Q and K of the self-attention (R32) [B*heads][N][128]
   uint8_t* k8 = nullptr;
+  uint8_t* v8t = nullptr;   // FP8 modes: e4m3 V^T [B*heads][128][ldv8] (R33) and its scale (device)
+  float* v8s = nullptr;
+  int ldv8 = 0;
   // encoder workspace
   float* ez = nullptr;      // [L, d_txt]
   void* ea = nullptr;       // [L, d_txt]

@@ -101,7 +101,7 @@ def test_fp8_block_wiring_reduces_to_the_bf16_block():
     e6 = rr.standard_normal((6, cfg.d)) * 0.1
     pos = dit.token_positions(cfg)
     ref = dit.block(P, cfg, 0, r, e6, kv, pos)
-    ident = dit_fp8.Q8(act_fn=lambda h: h, weight_fn=lambda w: w, qk_fn=lambda x, s: x)
+    ident = dit_fp8.Q8(act_fn=lambda h: h, weight_fn=lambda w: w, qk_fn=lambda x, s: x, v_fn=lambda v: v)
     assert np.array_equal(dit.block(P, cfg, 0, r, e6, kv, pos, q8=ident), ref)
     got = dit.block(P, cfg, 0, r, e6, kv, pos, q8=dit_fp8.Q8())
     rel = np.linalg.norm((got - r) - (ref - r)) / np.linalg.norm(ref - r)
@@ -267,3 +267,18 @@ def test_qk_scale_bounds_every_component_and_is_a_power_of_two():
     qv = dit_fp8.qk_quant(v, s)
     big = np.abs(v) > 0.05
     assert (np.abs(qv - v)[big] <= 2.0 ** -4 * np.abs(v)[big] + 2.0 ** -8 * np.abs(v)[big]).all()
+
+
+def test_v_quant_per_tensor_power_of_two():
+    """R33: one power-of-two scale for the whole V: values that are e4m3 codes times the scale
+    the amax implies (amax 56 = 448 / 8 -> s = 1/8) come back exactly; otherwise every element
+    within e4m3's normal range keeps half-a-quantum relative precision."""
+    from oracle import dit_fp8
+    r = np.random.default_rng(5)
+    v = r.standard_normal((64, 256))
+    q = dit_fp8.v_quant(v)
+    codes = fp8.e4m3_encode(np.array([1.0, -2.5, 448.0, 0.125]))
+    vals = fp8.e4m3_decode(codes)[None, :] * 2.0 ** -3
+    np.testing.assert_array_equal(dit_fp8.v_quant(vals), vals)   # amax 56 = 448 / 8: s = 1/8
+    big = np.abs(v) > 0.5
+    assert (np.abs(q - v)[big] <= 2.0 ** -4 * np.abs(v)[big] + 2.0 ** -8).all()
