@@ -282,3 +282,7 @@ def test_v_quant_per_tensor_power_of_two():
     np.testing.assert_array_equal(dit_fp8.v_quant(vals), vals)   # amax 56 = 448 / 8: s = 1/8
     big = np.abs(v) > 0.5
     assert (np.abs(q - v)[big] <= 2.0 ** -4 * np.abs(v)[big] + 2.0 ** -8).all()
+    # the scale is a power of two: amax 100 -> s = 2^-2 (not 100 / 448), 100 / s = 400 is the
+    # midpoint of 384 and 416 and rounds to even (384): the amax comes back as 96, not 100
+    w = np.array([[100.0, 1.0, -3.0]])
+    assert dit_fp8.v_quant(w)[0, 0] == 96.0

@@ -20,10 +20,36 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_math.py", "tests/test_oracle_stages.py",
-         "tests/test_oracle_rng.py"]
+         "tests/test_oracle_rng.py", "tests/test_oracle_fp8.py"]
 
 # (id, file, old, new, what it models)
 MUTATIONS = [
+    # ---- FP8 / MXFP8 (R28-R33), added with the MXFP8 and FP8-attention oracles
+    ("mx-emax-7", "oracle/fp8.py", "- E4M3_EMAX\n", "- E4M3_EMAX + 1\n", "MX scale exponent with emax 7"),
+    ("mx-ceil", "oracle/fp8.py", "e = np.floor(np.log2(np.where(amax > 0, amax, 1.0))) - E4M3_EMAX",
+     "e = np.ceil(np.log2(np.where(amax > 0, amax, 1.0))) - E4M3_EMAX", "ceil instead of OCP's floor"),
+    ("mx-zero-block-e0", "oracle/fp8.py", "e = np.where(amax > 0, e, -127.0)", "e = np.where(amax > 0, e, 0.0)",
+     "zero block with scale byte 127"),
+    ("mx-bias-126", "oracle/fp8.py", "sc = np.exp2(np.asarray(sbytes, dtype=np.float64) - 127.0)",
+     "sc = np.exp2(np.asarray(sbytes, dtype=np.float64) - 126.0)", "E8M0 bias off by one"),
+    ("mx-weight-blocks-along-n", "oracle/dit_fp8.py",
+     "q, s = fp8.mx_quantize(np.asarray(W, dtype=np.float64).T)\n    return fp8.mx_dequantize(q, s).T",
+     "q, s = fp8.mx_quantize(np.asarray(W, dtype=np.float64))\n    return fp8.mx_dequantize(q, s)",
+     "MX weight blocks along N instead of K"),
+    ("qk-scale-no-sqrt-dh", "oracle/dit_fp8.py", "np.sqrt(float(dh)) * gmax / 448.0", "gmax / 448.0",
+     "Q/K scale without the sqrt(dh) bound"),
+    ("qk-scale-not-pow2", "oracle/dit_fp8.py",
+     "return pow2_ceil(np.float32(np.sqrt(float(dh)) * gmax / 448.0)) if gmax > 0 else np.float32(1.0)",
+     "return np.float32(np.sqrt(float(dh)) * gmax / 448.0) if gmax > 0 else np.float32(1.0)",
+     "Q/K scale not rounded to a power of two"),
+    ("v-scale-not-pow2", "oracle/dit_fp8.py",
+     "s = pow2_ceil(np.float32(amax / E4M3_MAX)) if amax > 0 else np.float32(1.0)\n    return fp8.e4m3_decode",
+     "s = np.float32(amax / E4M3_MAX) if amax > 0 else np.float32(1.0)\n    return fp8.e4m3_decode",
+     "V scale not rounded to a power of two"),
+    ("rowq-not-pow2", "oracle/dit_fp8.py",
+     "s = np.where(amax > 0, pow2_ceil((amax / E4M3_MAX).astype(np.float32)), np.float32(1.0)).astype(np.float32)",
+     "s = np.where(amax > 0, (amax / E4M3_MAX).astype(np.float32), np.float32(1.0)).astype(np.float32)",
+     "per-row FP8 scale not rounded to a power of two"),
     ("temb-silu-dropped", "oracle/dit.py",
      'e = silu(s @ P["temb1_w"] + P["temb1_b"]) @ P["temb2_w"] + P["temb2_b"]',
      'e = (s @ P["temb1_w"] + P["temb1_b"]) @ P["temb2_w"] + P["temb2_b"]', "time MLP without its SiLU"),
