@@ -41,4 +41,9 @@ is checked to fail under one-line mutations of the oracle by tools/mutate_oracle
                brute-force GEMM
   dit_fp8 (NEXT-4, R29) pinned: per-row quantiser closed forms (amax-448 row, zero row,
                power-of-two scaling); wiring = dit.block exactly under identity quantisers
+  dit_fp8.mx_act / mx_weight (R31) pinned: blocks along K per output column, row independence
+  dit_fp8.qk_scale / qk_quant (R32) pinned: the worst-case component bound (lands in
+               (224, 448]), power of two, e4m3 relative precision of typical components
+  dit_fp8.v_quant (R33) pinned: exact round trip of scaled codes, power-of-two scale
+               (amax 100 -> 96 by ties-to-even), half-quantum relative error
 """
