@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--lib", action="store_true", help="also time torch SDPA (cuDNN / flash backends) on the same inputs")
     ap.add_argument("--H", type=int, default=0, help="override the head count (work-item scaling experiments)")
     ap.add_argument("--reps", type=int, default=1, help="back-to-back launches per timed sample (amortises launch latency)")
+    ap.add_argument("--f8", type=int, default=0, help="1: e4m3 Q/K (R32); 2: e4m3 Q/K/V and P (R33) -- FP8 modes")
     a = ap.parse_args()
     H, Nq, Nk = SHAPES[a.shape]
     if a.H:
@@ -42,14 +43,27 @@ def main():
         V = torch.randn(H, Nk, dh, device="cuda").to(torch.bfloat16)
         O = torch.empty(Nq, H * dh, device="cuda", dtype=torch.bfloat16)
         sc = 1.0 / math.sqrt(dh)
-        c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)
+        run = lambda: c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)  # noqa: E731
+        if a.f8:  # unit gains: s = pow2ceil(sqrt(128) / 448) = 2^-5 for Q and K
+            s8 = 2.0 ** -5
+            Q8 = torch.empty((H, Nq, dh), dtype=torch.uint8, device="cuda")
+            K8 = torch.empty((H, Nk, dh), dtype=torch.uint8, device="cuda")
+            c.op_qk_e4m3(Q, 1.0 / s8, Q8)
+            c.op_qk_e4m3(K, 1.0 / s8, K8)
+            if a.f8 == 1:
+                run = lambda: c.op_attention_qf8(Q8, K8, V, O, H, Nq, Nk, sc * s8 * s8)  # noqa: E731
+            else:
+                v8t = torch.zeros((H, 128, (Nk + 63) // 64 * 64), dtype=torch.uint8, device="cuda")
+                vs = torch.zeros(1, device="cuda")
+                run = lambda: c.op_attention_f8(Q8, K8, V, O, H, Nq, Nk, sc * s8 * s8, v8t, vs)  # noqa: E731
+        run()
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ms = []
         for _ in range(a.iters):
             ev[0].record()
             for _ in range(a.reps):
-                c.op_attention(Q, K, V, O, H, Nq, Nk, dh, dh, sc)
+                run()
             ev[1].record()
             torch.cuda.synchronize()
             ms.append(ev[0].elapsed_time(ev[1]) / a.reps)
@@ -60,7 +74,7 @@ def main():
         err = ((got - ref).norm() / ref.norm()).item()
         fl = 4.0 * H * Nq * Nk * dh
         best = min(ms)
-        print({"shape": a.shape, "H": H, "impl": os.environ.get("DF_ATTN_IMPL", "default"),
+        print({"shape": a.shape, "H": H, "impl": os.environ.get("DF_ATTN_IMPL", "default"), "f8": a.f8,
                "ms": round(best, 3), "tflops": round(fl / best / 1e9, 1),
                "rel_l2_vs_torch": f"{err:.2e}"})
         if a.lib:  # library reference point (not on the product path)
