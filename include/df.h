@@ -293,8 +293,9 @@ df_status df_op_qk_e4m3(df_ctx* ctx, const void* x, uint64_t n, float inv, void*
 df_status df_op_attention_qf8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,
                               int32_t Nq, int32_t Nk, float scale, void* stream);
 /* DESIGN.md R33: as df_op_attention_qf8 with PV on e4m3 too: V (bf16 [H][Nk][128], device) is
- * quantised per tensor -- s_v = the smallest power of two >= amax|V| / 448, written to *vscale
- * (one device float) -- and transposed into v8t (e4m3 V^T [H][128][ldv], ldv = Nk rounded up
+ * quantised per tensor -- s_v = the smallest power of two >= amax|V| / 448, written to vscale[0]
+ * (two device floats, zero-initialised before the first call: vscale[1] is an amax accumulator
+ * the call leaves zero again) -- and transposed into v8t (e4m3 V^T [H][128][ldv], ldv = Nk rounded up
  * to 64; H * 128 * ldv bytes of device scratch), P is rounded to e4m3 in TMEM and O is scaled
  * by s_v.  Four stream-ordered launches. */
 df_status df_op_attention_f8(df_ctx* ctx, const void* Q8, const void* K8, const void* V, void* O, int32_t H,

@@ -794,6 +794,8 @@ cudaError_t delay_ns(uint64_t ns, cudaStream_t st) {
 // Three stream-ordered launches: amax (one atomicMax per warp on the float bits -- valid for
 // non-negative floats), the scale (one thread, in place), the quantisation (8 per thread).
 __global__ void __launch_bounds__(256) e4m3_amax_kernel(const bf16* __restrict__ x, size_t n, unsigned* amax) {
+  pdl_wait();
+  pdl_launch_dependents();
   float m = 0.f;
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   const size_t n8 = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / 8;
@@ -1187,15 +1189,21 @@ cudaError_t qk_e4m3(const bf16* x, size_t n, float inv, uint8_t* q, cudaStream_t
 
 // R33: V [H][N][128] bf16 -> V^T e4m3 [H][128][ldv] (keys contiguous: the K-major B operand of
 // the e4m3 PV MMA) with one per-tensor power-of-two scale s = pow2ceil(fp32(amax|V| / 448)).
+// s[0] = the scale from the amax accumulated in s[1]; s[1] is re-zeroed for the next call
 __global__ void v_scale_kernel(float* s) {
-  const float a = __uint_as_float(*reinterpret_cast<const unsigned*>(s));
-  *s = a > 0.f ? pow2_ceil(__fdiv_rn(a, 448.f)) : 1.f;
+  pdl_wait();
+  pdl_launch_dependents();
+  const float a = __uint_as_float(reinterpret_cast<const unsigned*>(s)[1]);
+  s[0] = a > 0.f ? pow2_ceil(__fdiv_rn(a, 448.f)) : 1.f;
+  reinterpret_cast<unsigned*>(s)[1] = 0u;
 }
 // one block per (64 keys, head): 64 x 128 bf16 -> e4m3 through a shared [128][64 + 16] tile
 __global__ void __launch_bounds__(256) v_e4m3t_kernel(const bf16* __restrict__ V, int N, int ldv,
                                                       const float* __restrict__ sp, uint8_t* __restrict__ VT) {
   __shared__ uint8_t tile[128][80];
   const int h = blockIdx.y, k0 = blockIdx.x * 64;
+  pdl_wait();
+  pdl_launch_dependents();
   const float inv = __uint_as_float((254u << 23) - __float_as_uint(__ldg(sp)));  // exactly 1 / s
   const int t = threadIdx.x;
   {  // load: thread t -> key k0 + t / 4, dh [32 (t % 4), +32)
@@ -1238,15 +1246,20 @@ cudaError_t v_e4m3t(const bf16* V, int H, int N, int ldv, float* vscale, uint8_t
   if (ldv < ((N + 63) / 64) * 64 || ldv % 16 || (reinterpret_cast<uintptr_t>(V) & 15) ||
       (reinterpret_cast<uintptr_t>(VT) & 15))
     return cudaErrorInvalidValue;
-  const size_t n = size_t(H) * N * 128;
-  cudaError_t e = cudaMemsetAsync(vscale, 0, 4, st);
-  if (e != cudaSuccess) return e;
+  size_t n = size_t(H) * N * 128;
   const int per = 256 * 8 * 4;
   const unsigned grid = unsigned(std::max<size_t>(1, std::min<size_t>((n + per - 1) / per, size_t(num_sms()) * 8)));
-  e4m3_amax_kernel<<<grid, 256, 0, st>>>(V, n, reinterpret_cast<unsigned*>(vscale));
-  v_scale_kernel<<<1, 1, 0, st>>>(vscale);
-  v_e4m3t_kernel<<<dim3((N + 63) / 64, H), 256, 0, st>>>(V, N, ldv, vscale, VT);
-  return cudaGetLastError();
+  // three PDL launches; vscale[1] (the amax accumulator) is zero on entry and left zero
+  unsigned* acc = reinterpret_cast<unsigned*>(vscale) + 1;
+  void* a1[] = {(void*)&V, (void*)&n, (void*)&acc};
+  cudaError_t e = launch_ex((const void*)e4m3_amax_kernel, dim3(grid), dim3(256), 0, st, a1);
+  if (e != cudaSuccess) return e;
+  void* a2[] = {(void*)&vscale};
+  e = launch_ex((const void*)v_scale_kernel, dim3(1), dim3(1), 0, st, a2);
+  if (e != cudaSuccess) return e;
+  const float* sp = vscale;
+  void* a3[] = {(void*)&V, (void*)&N, (void*)&ldv, (void*)&sp, (void*)&VT};
+  return launch_ex((const void*)v_e4m3t_kernel, dim3((N + 63) / 64, H), dim3(256), 0, st, a3);
 }
 
 }  // namespace df

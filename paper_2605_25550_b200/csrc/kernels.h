@@ -36,7 +36,7 @@ cudaError_t qk_e4m3(const bf16* x, size_t n, float inv, uint8_t* q, cudaStream_t
 cudaError_t attn_tc_f8(const uint8_t* Q8, const uint8_t* K8, const uint8_t* V8T, int ldv, const float* vscale, bf16* O,
                        int H, int Nq, int Nk, float scale, cudaStream_t st, int heads_per_sample);
 // head-major bf16 V [H][N][128] -> e4m3 V^T [H][128][ldv] with s = pow2ceil(amax|V| / 448) written
-// to *vscale (three stream-ordered launches: amax, scale, transpose-quantise)
+// to vscale[0]; vscale[1] is the amax accumulator (zero on entry, left zero); three PDL launches
 cudaError_t v_e4m3t(const bf16* V, int H, int N, int ldv, float* vscale, uint8_t* VT, cudaStream_t st);
 // MXFP8 step (R31): the block-scaled GEMM through the TMA-store epilogues of the bf16 path
 cudaError_t gemm_mxf8_epi(const uint8_t* qa, const uint8_t* sa, const uint8_t* qw, const uint8_t* sw, int M, int N,

@@ -222,6 +222,7 @@ cudaError_t Model::create(const df_dit_cfg& cfg, int prec, int dev, int stg, uin
       ldv8 = int((Nn + 63) / 64 * 64);
       v8t = (uint8_t*)ws.take(size_t(2) * c.heads * 128 * ldv8);
       v8s = (float*)ws.take(64);
+      DF_TRY(cudaMemset(v8s, 0, 64));  // [1]: v_e4m3t's amax accumulator, zero between calls
     }
     if (mx()) {  // rows past M in the last 128-row block keep scale byte 0
       hsf = (uint8_t*)ws.take(mx_sf_bytes(N2, std::max(d, f)));

@@ -242,7 +242,7 @@ def test_attention_f8_vs_fp64(ctx, H, Nq, Nk):
     ctx.op_qk_e4m3(K, 1.0 / sk, K8)
     ldv = (Nk + 63) // 64 * 64
     v8t = torch.zeros((H, 128, ldv), dtype=torch.uint8, device="cuda")
-    vs = torch.zeros(1, device="cuda")
+    vs = torch.zeros(2, device="cuda")
     O = torch.full((Nq, H * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
     ctx.op_attention_f8(Q8, K8, V, O, H, Nq, Nk, sq * sk / math.sqrt(dh), v8t, vs)
     torch.cuda.synchronize()
@@ -250,7 +250,8 @@ def test_attention_f8_vs_fp64(ctx, H, Nq, Nk):
     kd = K.float().cpu().numpy().astype(np.float64)
     vd = V.float().cpu().numpy().astype(np.float64)
     vq = dit_fp8.v_quant(vd)
-    s_v = float(vs.item())
+    s_v = float(vs[0].item())
+    assert float(vs[1].item()) == 0.0  # the amax accumulator is left zero
     assert s_v == float(dit_fp8.pow2_ceil(np.float32(np.float32(np.abs(vd).max()) / np.float32(448.0))))
     assert np.array_equal(v8t[:, :, :Nk].cpu().numpy(), fp8.e4m3_encode(vd / s_v).transpose(0, 2, 1))
     rows = np.arange(Nq) if Nq <= 1000 else np.unique(np.r_[np.arange(0, Nq, 97), np.arange(Nq - 5, Nq)])

@@ -54,7 +54,7 @@ def main():
                 run = lambda: c.op_attention_qf8(Q8, K8, V, O, H, Nq, Nk, sc * s8 * s8)  # noqa: E731
             else:
                 v8t = torch.zeros((H, 128, (Nk + 63) // 64 * 64), dtype=torch.uint8, device="cuda")
-                vs = torch.zeros(1, device="cuda")
+                vs = torch.zeros(2, device="cuda")
                 run = lambda: c.op_attention_f8(Q8, K8, V, O, H, Nq, Nk, sc * s8 * s8, v8t, vs)  # noqa: E731
         run()
         torch.cuda.synchronize()
